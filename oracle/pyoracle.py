@@ -560,7 +560,7 @@ class RefTrainer:
             pass
 
     def iteration(self, it, max_minibatches=-1):
-        secs = np.zeros(4)
+        secs = np.zeros(6)
         a, c = C.c_double(), C.c_double()
         self.o.check(self.o.lib.mref_trainer_iteration(self.h, it, max_minibatches, 0,
                                                        secs.ctypes.data, C.byref(a), C.byref(c)))

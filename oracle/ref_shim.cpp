@@ -429,7 +429,7 @@ int mref_trainer_iteration(void* tp, int it, int max_minibatches, int rollout_in
         mb.value_targets = &gae.value_targets;
         const int rows = tc.N * tc.T;
         int done = 0;
-        double al_sum = 0, cl_sum = 0;
+        double al_sum = 0, cl_sum = 0, loss_s = 0, adam_s = 0;
         for (int e = 0; e < tc.epochs; ++e) {
             shuffle_rng.shuffle(t.perm);
             for (int s = 0; s < tc.minibatch_count; ++s) {
@@ -438,8 +438,11 @@ int mref_trainer_iteration(void* tp, int it, int max_minibatches, int rollout_in
                 const int hi = (int)((long long)rows * (s + 1) / tc.minibatch_count);
                 if (lo == hi) continue;
                 mb.rows.assign(t.perm.begin() + lo, t.perm.begin() + hi);
+                auto l0 = now();
                 const LossResult al = actor_loss(t.as, t.a, mb, tc.clip_eps, tc.entropy_coef);
                 const LossResult cl = critic_loss(t.cs, t.c, mb);
+                auto l1 = now();
+                loss_s += std::chrono::duration<double>(l1 - l0).count();
                 if (!std::isfinite(al.loss) || !std::isfinite(cl.loss)) throw NumericError("non-finite loss");
                 adam_apply(t.af, t.a.feature_params, al.grad.feature_params, tc.actor_lr);
                 adam_apply(t.aM, t.a.M, al.grad.M, tc.actor_lr);
@@ -447,6 +450,7 @@ int mref_trainer_iteration(void* tp, int it, int max_minibatches, int rollout_in
                 adam_apply(t.cf, t.c.feature_params, cl.grad.feature_params, tc.critic_lr);
                 adam_apply(t.cM, t.c.M, cl.grad.M, tc.critic_lr);
                 adam_apply(t.cb, t.c.b, cl.grad.b, tc.critic_lr);
+                adam_s += std::chrono::duration<double>(now() - l1).count();
                 al_sum += al.loss;
                 cl_sum += cl.loss;
                 done++;
@@ -458,6 +462,8 @@ int mref_trainer_iteration(void* tp, int it, int max_minibatches, int rollout_in
             seconds_out[1] = std::chrono::duration<double>(t2 - t1).count();
             seconds_out[2] = std::chrono::duration<double>(t3 - t2).count();
             seconds_out[3] = done;
+            seconds_out[4] = loss_s;
+            seconds_out[5] = adam_s;
         }
         if (actor_loss_out) *actor_loss_out = al_sum;
         if (critic_loss_out) *critic_loss_out = cl_sum;

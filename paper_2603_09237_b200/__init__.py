@@ -1,0 +1,476 @@
+"""B200-native MORLAX data-parallel training step.
+
+Python mirror of the reference C++ API (``/root/reference/proj/include/morlax``)
+over the C-ABI in ``include/morlax_b200.h`` (``libmorlax_b200.so``: sm_100a
+CUDA kernels + C++ host orchestration). Names, argument meaning and error
+behaviour follow the reference:
+
+* ``BatchedEnv`` / ``make_env`` / ``env_spec``      -> env.hpp:37-99, registry.cpp
+* ``hypernet_forward`` / ``hypernet_backward`` / ``init_hypernet`` -> hypernet.hpp
+* ``gae_per_objective`` / ``normalize_and_scalarize`` -> trainer.hpp:154-161
+* ``adam_apply``                                     -> trainer.hpp:211-212
+* ``Trainer`` (``train()`` loop body)                -> train.cpp:118-184
+* ``nondominated_filter`` / ``hypervolume_mc`` / ``hypervolume_detailed`` -> pareto.hpp
+
+There is no CPU fallback: importing this package loads the CUDA library
+(building it with nvcc if the in-tree .so is missing) and every compute call
+runs on the GPU; without a GPU, calls fail with ``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import LIB, LIB_PATH  # noqa: F401  (loads / builds the CUDA library)
+
+__all__ = [
+    "ConfigError", "ShapeError", "NumericError", "DomainError", "CudaError", "EnvSpec", "env_spec",
+    "BatchedEnv", "make_env", "HypernetSpec", "init_hypernet", "hypernet_forward", "hypernet_backward",
+    "gae_per_objective", "normalize_and_scalarize", "adam_apply", "TrainConfig", "Trainer",
+    "nondominated_mask", "nondominated_filter", "hypervolume_mc", "hypervolume_detailed",
+    "rng_words", "rng_gaussians", "shard_minibatch", "LIB_PATH",
+]
+
+
+# ---------------------------------------------------------------- errors (errors.hpp:10-30)
+class MorlaxError(RuntimeError):
+    code = 1
+
+
+class ConfigError(MorlaxError):
+    code = 2
+
+
+class ShapeError(MorlaxError):
+    code = 2
+
+
+class DomainError(MorlaxError):
+    code = 2
+
+
+class NumericError(MorlaxError):
+    code = 3
+
+
+class CudaError(MorlaxError):
+    code = 1
+
+
+_KINDS = {"ConfigError": ConfigError, "ShapeError": ShapeError, "DomainError": DomainError,
+          "NumericError": NumericError, "CudaError": CudaError}
+
+
+def _check(rc):
+    if rc != 0:
+        kind = LIB.morlax_last_error_kind().decode()
+        msg = LIB.morlax_last_error().decode()
+        raise _KINDS.get(kind, MorlaxError)(msg)
+
+
+def _ptr(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def _f32(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a if shape is None else a.reshape(shape)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- RNG (rng.hpp)
+def rng_words(key: int, ctr: int, n: int) -> np.ndarray:
+    out = np.zeros(n, np.uint64)
+    _check(LIB.morlax_rng_words(C.c_uint64(key), C.c_uint64(ctr), n, _ptr(out)))
+    return out
+
+
+def rng_gaussians(key: int, ctr: int, n: int) -> np.ndarray:
+    out = np.zeros(n, np.float64)
+    _check(LIB.morlax_rng_gaussians(C.c_uint64(key), C.c_uint64(ctr), n, _ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------- env (env.hpp)
+@dataclass
+class EnvSpec:
+    name: str
+    obs_dim: int
+    act_dim: int
+    m: int
+    max_episode_steps: int
+
+
+def env_spec(name: str) -> EnvSpec:
+    v = [C.c_int() for _ in range(4)]
+    _check(LIB.morlax_env_spec(name.encode(), *[C.byref(x) for x in v]))
+    return EnvSpec(name, *[x.value for x in v])
+
+
+@dataclass
+class StepOut:
+    obs: np.ndarray
+    reward: np.ndarray
+    terminated: np.ndarray
+    truncated: np.ndarray
+
+
+class BatchedEnv:
+    """N instances of one environment stepped in lockstep on the GPU, with
+    per-instance counter-based RNG streams and auto-reset (env.hpp:26-99)."""
+
+    def __init__(self, name: str, num_envs: int):
+        self.spec = env_spec(name)
+        self.num_envs = num_envs
+        h = C.c_void_p()
+        _check(LIB.morlax_env_create(name.encode(), num_envs, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.morlax_env_destroy(self._h)
+            self._h = None
+
+    def reset(self, key: int, ctr: int = 0) -> np.ndarray:
+        obs = np.zeros((self.num_envs, self.spec.obs_dim), np.float32)
+        _check(LIB.morlax_env_reset(self._h, C.c_uint64(key), C.c_uint64(ctr), _ptr(obs)))
+        return obs
+
+    def step(self, actions) -> StepOut:
+        s = self.spec
+        a = _f32(actions)
+        if a.size != self.num_envs * s.act_dim:
+            raise ShapeError("BatchedEnv::step: actions must be N x act_dim")
+        out = StepOut(np.zeros((self.num_envs, s.obs_dim), np.float32),
+                      np.zeros((self.num_envs, s.m), np.float32),
+                      np.zeros(self.num_envs, np.uint8), np.zeros(self.num_envs, np.uint8))
+        _check(LIB.morlax_env_step(self._h, _ptr(a), _ptr(out.obs), _ptr(out.reward),
+                                   _ptr(out.terminated), _ptr(out.truncated)))
+        return out
+
+    def step_device(self, d_actions, d_obs, d_reward, d_term, d_trunc, stream=0):
+        """Device-pointer variant (e.g. torch tensors' data_ptr())."""
+        _check(LIB.morlax_env_step_device(self._h, C.c_void_p(d_actions), C.c_void_p(d_obs),
+                                          C.c_void_p(d_reward), C.c_void_p(d_term),
+                                          C.c_void_p(d_trunc), C.c_void_p(stream)))
+
+    def current_obs(self) -> np.ndarray:
+        obs = np.zeros((self.num_envs, self.spec.obs_dim), np.float32)
+        _check(LIB.morlax_env_current_obs(self._h, _ptr(obs)))
+        return obs
+
+    def clamp_count(self) -> int:
+        return int(LIB.morlax_env_clamp_count(self._h))
+
+
+def make_env(name: str, num_envs: int) -> BatchedEnv:
+    return BatchedEnv(name, num_envs)
+
+
+# ---------------------------------------------------------------- hypernet (hypernet.hpp)
+class _HSpecC(C.Structure):
+    _fields_ = [("m", C.c_int), ("F", C.c_int), ("n_feature_hidden", C.c_int),
+                ("feature_hidden", C.c_int * 8), ("n_target_sizes", C.c_int),
+                ("target_sizes", C.c_int * 9), ("target_tanh", C.c_int), ("has_log_std", C.c_int)]
+
+
+@dataclass
+class HypernetSpec:
+    m: int
+    F: int
+    feature_hidden: list
+    target_sizes: list  # [in, hidden..., out]
+    target_tanh: bool
+    has_log_std: bool
+
+    def c(self):
+        h = _HSpecC()
+        h.m, h.F = self.m, self.F
+        h.n_feature_hidden = len(self.feature_hidden)
+        for i, v in enumerate(self.feature_hidden):
+            h.feature_hidden[i] = v
+        h.n_target_sizes = len(self.target_sizes)
+        for i, v in enumerate(self.target_sizes):
+            h.target_sizes[i] = v
+        h.target_tanh = int(self.target_tanh)
+        h.has_log_std = int(self.has_log_std)
+        return h
+
+    @property
+    def target_param_count(self) -> int:
+        return int(LIB.morlax_hypernet_target_count(C.byref(self.c())))
+
+    @property
+    def param_count(self) -> int:
+        return int(LIB.morlax_hypernet_param_count(C.byref(self.c())))
+
+
+def init_hypernet(spec: HypernetSpec, key: int, ctr: int = 0) -> np.ndarray:
+    out = np.zeros(spec.param_count)
+    _check(LIB.morlax_init_hypernet(C.byref(spec.c()), C.c_uint64(key), C.c_uint64(ctr), _ptr(out)))
+    return out
+
+
+def hypernet_forward(spec: HypernetSpec, flat, w) -> np.ndarray:
+    w = _f64(w).reshape(-1, spec.m)
+    out = np.zeros((len(w), spec.target_param_count))
+    _check(LIB.morlax_hypernet_forward(C.byref(spec.c()), _ptr(_f64(flat)), _ptr(w), len(w),
+                                       _ptr(out)))
+    return out
+
+
+def hypernet_backward(spec: HypernetSpec, flat, w, gtheta) -> np.ndarray:
+    w = _f64(w).reshape(-1, spec.m)
+    g = _f64(gtheta).reshape(len(w), -1)
+    out = np.zeros(spec.param_count)
+    _check(LIB.morlax_hypernet_backward(C.byref(spec.c()), _ptr(_f64(flat)), _ptr(w), len(w),
+                                        _ptr(g), _ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------- GAE (gae.cpp)
+def gae_per_objective(reward, value, next_value, terminated, truncated, N, T, gamma, lam):
+    m = np.asarray(reward).reshape(N * T, -1).shape[1]
+    adv = np.zeros((N * T, m), np.float32)
+    tgt = np.zeros((N * T, m), np.float32)
+    r, v, nv = (_f32(x) for x in (reward, value, next_value))
+    te = np.ascontiguousarray(terminated, np.uint8)
+    tr = np.ascontiguousarray(truncated, np.uint8)
+    _check(LIB.morlax_gae(N, T, m, _ptr(r), _ptr(v), _ptr(nv), _ptr(te), _ptr(tr), C.c_double(gamma),
+                          C.c_double(lam), _ptr(adv), _ptr(tgt)))
+    return adv, tgt
+
+
+def normalize_and_scalarize(advantages, tradeoffs, N, T):
+    a = _f32(advantages)
+    m = a.reshape(N * T, -1).shape[1]
+    out = np.zeros(N * T, np.float32)
+    _check(LIB.morlax_normalize_scalarize(N, T, m, _ptr(a), _ptr(_f64(tradeoffs)), _ptr(out)))
+    return out
+
+
+def adam_apply(params, grad, m1, m2, step, lr):
+    p, m1, m2 = (_f64(x).copy() for x in (params, m1, m2))
+    st = C.c_int64(step)
+    _check(LIB.morlax_adam(len(p), _ptr(p), _ptr(_f64(grad)), _ptr(m1), _ptr(m2), C.byref(st),
+                           C.c_double(lr)))
+    return p, m1, m2, st.value
+
+
+# ---------------------------------------------------------------- trainer (train.cpp)
+class _TrainCfgC(C.Structure):
+    _fields_ = [("env_name", C.c_char_p), ("N", C.c_int), ("K", C.c_int), ("kappa", C.c_int),
+                ("T", C.c_int), ("epochs", C.c_int), ("minibatch_count", C.c_int),
+                ("gamma", C.c_double), ("gae_lambda", C.c_double), ("clip_eps", C.c_double),
+                ("actor_lr", C.c_double), ("critic_lr", C.c_double), ("entropy_coef", C.c_double),
+                ("seed", C.c_uint64), ("F", C.c_int), ("n_feature_hidden", C.c_int),
+                ("feature_hidden", C.c_int * 8), ("n_actor_hidden", C.c_int),
+                ("actor_hidden", C.c_int * 8), ("n_critic_hidden", C.c_int),
+                ("critic_hidden", C.c_int * 8)]
+
+
+class _IterStatsC(C.Structure):
+    _fields_ = [("actor_loss", C.c_double), ("critic_loss", C.c_double), ("minibatches", C.c_int),
+                ("numeric_error", C.c_int), ("kernel_launches", C.c_int64)]
+
+
+@dataclass
+class TrainConfig:
+    """RunConfig subset of the hot path (trainer.hpp:21-77). Defaults = PR1."""
+    env_name: str = "mo-pointmass"
+    N: int = 256
+    K: int = 16
+    kappa: int = 0
+    T: int = 32
+    gamma: float = 0.99
+    gae_lambda: float = 0.95
+    clip_eps: float = 0.2
+    epochs: int = 4
+    minibatch_count: int = 4
+    actor_lr: float = 3e-4
+    critic_lr: float = 3e-4
+    entropy_coef: float = 0.1
+    seed: int = 0
+    F: int = 64
+    feature_hidden: list = field(default_factory=lambda: [64])
+    actor_hidden: list = field(default_factory=lambda: [64, 64])
+    critic_hidden: list = field(default_factory=lambda: [64, 64])
+
+    def c(self):
+        c = _TrainCfgC()
+        self._name = self.env_name.encode()
+        c.env_name = self._name
+        for k in ("N", "K", "kappa", "T", "epochs", "minibatch_count", "gamma", "gae_lambda",
+                  "clip_eps", "actor_lr", "critic_lr", "entropy_coef", "seed", "F"):
+            setattr(c, k, getattr(self, k))
+        for name in ("feature_hidden", "actor_hidden", "critic_hidden"):
+            v = getattr(self, name)
+            setattr(c, "n_" + name, len(v))
+            arr = getattr(c, name)
+            for i, x in enumerate(v):
+                arr[i] = x
+        return c
+
+    def specs(self):
+        es = env_spec(self.env_name)
+        a = HypernetSpec(es.m, self.F, list(self.feature_hidden),
+                         [es.obs_dim] + list(self.actor_hidden) + [es.act_dim], True, True)
+        c = HypernetSpec(es.m, self.F, list(self.feature_hidden),
+                         [es.obs_dim] + list(self.critic_hidden) + [es.m], False, False)
+        return a, c
+
+
+@dataclass
+class IterationStats:
+    actor_loss: float
+    critic_loss: float
+    minibatches: int
+    numeric_error: int
+    kernel_launches: int
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(LIB.morlax_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Trainer:
+    """The reference train() loop body on the GPU (train.cpp:118-184).
+    world > 1: one Trainer per GPU/rank (environments and preference clusters
+    sharded; NCCL exchange of the per-cluster hypernetwork gradients)."""
+
+    _F32 = {"obs", "action_pre", "logprob", "reward", "value", "next_value", "advantages",
+            "value_targets", "scalar_advantage", "env_state", "tracker", "clusters"}
+
+    def __init__(self, cfg: TrainConfig, world: int = 1, rank: int = 0, nccl_id: bytes = None):
+        self.cfg = cfg
+        self._c = cfg.c()
+        h = C.c_void_p()
+        idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        _check(LIB.morlax_trainer_create(C.byref(self._c), world, rank, idb, C.byref(h)))
+        self._h = h
+        self.es = env_spec(cfg.env_name)
+        ap, cp = C.c_int64(), C.c_int64()
+        le, lc, rows = C.c_int(), C.c_int(), C.c_int()
+        _check(LIB.morlax_trainer_sizes(h, C.byref(ap), C.byref(cp), C.byref(le), C.byref(lc),
+                                        C.byref(rows)))
+        self.n_actor, self.n_critic = ap.value, cp.value
+        self.local_envs, self.local_clusters, self.rows = le.value, lc.value, rows.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.morlax_trainer_destroy(self._h)
+            self._h = None
+
+    def iteration(self, it: int) -> IterationStats:
+        st = _IterStatsC()
+        _check(LIB.morlax_trainer_iteration(self._h, it, C.byref(st)))
+        return IterationStats(st.actor_loss, st.critic_loss, st.minibatches, st.numeric_error,
+                              st.kernel_launches)
+
+    def phase(self, it: int, phase: int, max_minibatches: int = -1):
+        st = _IterStatsC()
+        _check(LIB.morlax_trainer_phase(self._h, it, phase, max_minibatches, C.byref(st)))
+        return IterationStats(st.actor_loss, st.critic_loss, st.minibatches, st.numeric_error,
+                              st.kernel_launches)
+
+    def params(self, which: str = "actor") -> np.ndarray:
+        n = self.n_actor if which == "actor" else self.n_critic
+        out = np.zeros(n)
+        _check(LIB.morlax_trainer_get_params(self._h, 0 if which == "actor" else 1, _ptr(out)))
+        return out
+
+    def set_params(self, which: str, flat):
+        _check(LIB.morlax_trainer_set_params(self._h, 0 if which == "actor" else 1,
+                                             _ptr(_f64(flat))))
+
+    def grad(self, which: str = "actor") -> np.ndarray:
+        n = self.n_actor if which == "actor" else self.n_critic
+        out = np.zeros(n)
+        _check(LIB.morlax_trainer_get_grad(self._h, 0 if which == "actor" else 1, _ptr(out)))
+        return out
+
+    def _shape(self, name):
+        es, R, N = self.es, self.rows, self.local_envs
+        return {"obs": (R, es.obs_dim), "action_pre": (R, es.act_dim), "logprob": (R,),
+                "reward": (R, es.m), "value": (R, es.m), "next_value": (R, es.m),
+                "advantages": (R, es.m), "value_targets": (R, es.m), "scalar_advantage": (R,),
+                "terminated": (R,), "truncated": (R,), "clusters": (self.cfg.K, es.m),
+                "perm": (self.cfg.N * self.cfg.T,), "env_ctr": (N,), "env_steps": (N,),
+                "tracker": (N, es.m)}[name]
+
+    def get(self, name: str) -> np.ndarray:
+        if name == "env_state":
+            raise ShapeError("use env_state()")
+        dt = (np.float32 if name in self._F32 else np.uint8 if name in ("terminated", "truncated")
+              else np.uint64 if name == "env_ctr" else np.int32)
+        out = np.zeros(self._shape(name), dt)
+        _check(LIB.morlax_trainer_get(self._h, name.encode(), _ptr(out)))
+        return out
+
+    def set(self, name: str, value):
+        dt = (np.float32 if name in self._F32 else np.uint8 if name in ("terminated", "truncated")
+              else np.uint64 if name == "env_ctr" else np.int32)
+        v = np.ascontiguousarray(value, dt).reshape(self._shape(name))
+        _check(LIB.morlax_trainer_set(self._h, name.encode(), _ptr(v)))
+
+    def losses(self, rows):
+        r = np.ascontiguousarray(rows, np.int32)
+        a, c = C.c_double(), C.c_double()
+        _check(LIB.morlax_trainer_losses(self._h, _ptr(r), len(r), C.byref(a), C.byref(c)))
+        return a.value, c.value
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(LIB.morlax_trainer_kernel_launches(self._h))
+
+
+def shard_minibatch(perm, lo, hi, T, inst_lo, n_inst, reps, n_groups):
+    perm = np.ascontiguousarray(perm, np.int32)
+    rows = np.zeros(max(hi - lo, 1), np.int32)
+    goff = np.zeros(n_groups + 1, np.int32)
+    n, mx = C.c_int(), C.c_int()
+    _check(LIB.morlax_shard_minibatch(_ptr(perm), lo, hi, T, inst_lo, n_inst, reps, n_groups,
+                                      _ptr(rows), _ptr(goff), C.byref(n), C.byref(mx)))
+    return rows[:n.value], goff, mx.value
+
+
+# ---------------------------------------------------------------- pareto (pareto.hpp)
+def nondominated_mask(points) -> np.ndarray:
+    p = _f64(points)
+    n, m = p.shape
+    mask = np.zeros(n, np.uint8)
+    _check(LIB.morlax_pareto_mask(n, m, _ptr(p), _ptr(mask)))
+    return mask
+
+
+def nondominated_filter(points) -> np.ndarray:
+    p = _f64(points)
+    return p[nondominated_mask(p).astype(bool)]
+
+
+def hypervolume_mc(points, reference, samples, key, ctr=0):
+    p = _f64(points).reshape(-1, len(reference))
+    ref = _f64(reference)
+    v, se, h = C.c_double(), C.c_double(), C.c_uint64()
+    _check(LIB.morlax_hypervolume_mc(len(p), len(ref), _ptr(p), _ptr(ref), C.c_uint64(samples),
+                                     C.c_uint64(key), C.c_uint64(ctr), C.byref(v), C.byref(se),
+                                     C.byref(h)))
+    return v.value, se.value, h.value
+
+
+def hypervolume_detailed(points, reference, samples=1_000_000, seed=0x9E3779B9):
+    p = _f64(points).reshape(-1, len(reference))
+    ref = _f64(reference)
+    v, se = C.c_double(), C.c_double()
+    ex, cl = C.c_int(), C.c_int()
+    _check(LIB.morlax_hypervolume_detailed(len(p), len(ref), _ptr(p), _ptr(ref), C.c_uint64(samples),
+                                           C.c_uint64(seed), C.byref(v), C.byref(se), C.byref(ex),
+                                           C.byref(cl)))
+    return v.value, se.value, bool(ex.value), cl.value

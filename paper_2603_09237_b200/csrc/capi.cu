@@ -1,0 +1,609 @@
+// extern "C" boundary (include/morlax_b200.h). Every entry point maps the
+// reference's C++ exceptions to the CLI's status codes
+// (tools/commands.hpp:12-32) and records a thread-local message.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/morlax_b200.h"
+#include "comm.h"
+#include "trainer.h"
+
+using namespace mb200;
+
+namespace {
+thread_local std::string g_err, g_kind;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        g_err.clear();
+        g_kind.clear();
+        return MORLAX_OK;
+    } catch (const NumericError& e) {
+        g_err = e.what(); g_kind = "NumericError";
+        return MORLAX_ERR_NUMERIC;
+    } catch (const ConfigError& e) {
+        g_err = e.what(); g_kind = "ConfigError";
+        return MORLAX_ERR_CONFIG;
+    } catch (const ShapeError& e) {
+        g_err = e.what(); g_kind = "ShapeError";
+        return MORLAX_ERR_CONFIG;
+    } catch (const DomainError& e) {
+        g_err = e.what(); g_kind = "DomainError";
+        return MORLAX_ERR_CONFIG;
+    } catch (const CudaError& e) {
+        g_err = e.what(); g_kind = "CudaError";
+        return MORLAX_ERR_OTHER;
+    } catch (const std::exception& e) {
+        g_err = e.what(); g_kind = "Error";
+        return MORLAX_ERR_OTHER;
+    }
+}
+
+template <typename T>
+struct DBuf {  // scoped device buffer
+    T* p = nullptr;
+    size_t n = 0;
+    explicit DBuf(size_t n_) : n(n_) { MB_CUDA(cudaMalloc(&p, (n ? n : 1) * sizeof(T))); }
+    DBuf(const T* host, size_t n_) : DBuf(n_) {
+        if (n) MB_CUDA(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+    }
+    ~DBuf() { cudaFree(p); }
+    void get(T* host) const {
+        if (n) MB_CUDA(cudaMemcpy(host, p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    }
+};
+
+std::vector<int> vec(int n, const int* a) { return std::vector<int>(a, a + n); }
+
+void check_simplex(int m, const double* w) {  // TradeoffVector::checked (simplex.cpp:18-30)
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) {
+        if (!(w[i] >= 0.0)) throw DomainError("trade-off entries must be nonnegative");
+        s += w[i];
+    }
+    if (std::fabs(s - 1.0) > 1e-9) throw DomainError("trade-off entries must sum to 1 (got " + std::to_string(s) + ")");
+}
+
+struct HyperHandle {
+    HyperNet h;
+    explicit HyperHandle(const morlax_hypernet_spec* s, int G) {
+        if (s->n_target_sizes < 2 || s->n_target_sizes > 9) throw ShapeError("MlpSpec needs at least input and output sizes");
+        h.init(s->m, s->F, vec(s->n_feature_hidden, s->feature_hidden), vec(s->n_target_sizes, s->target_sizes),
+               s->target_tanh != 0, s->has_log_std != 0, G);
+    }
+    ~HyperHandle() { h.free_all(); }
+    void load(const double* flat) {
+        std::vector<float> f(flat, flat + h.n);
+        MB_CUDA(cudaMemcpy(h.p, f.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+    }
+};
+}  // namespace
+
+struct morlax_env {
+    EnvSpecB es;
+    int N;
+    float* state = nullptr;
+    uint64_t *keys = nullptr, *ctrs = nullptr;
+    int* steps = nullptr;
+    int* err = nullptr;
+    unsigned long long* clamps = nullptr;
+    cudaStream_t s = nullptr;
+};
+
+struct morlax_trainer {
+    Trainer* t = nullptr;
+};
+
+extern "C" {
+
+const char* morlax_last_error(void) { return g_err.c_str(); }
+const char* morlax_last_error_kind(void) { return g_kind.c_str(); }
+int morlax_version(void) { return 1; }
+int morlax_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int morlax_rng_words(uint64_t key, uint64_t ctr, int64_t n, uint64_t* out) {
+    return guarded([&] {
+        DBuf<uint64_t> d(n);
+        rng_words(key, ctr, n, d.p, 0);
+        d.get(out);
+    });
+}
+int morlax_rng_gaussians(uint64_t key, uint64_t ctr, int64_t n, double* out) {
+    return guarded([&] {
+        DBuf<double> d(n);
+        rng_gaussians(key, ctr, n, d.p, 0);
+        d.get(out);
+    });
+}
+
+// ------------------------------------------------------------------ env
+int morlax_env_spec(const char* name, int* od, int* ad, int* m, int* ms) {
+    return guarded([&] {
+        const EnvSpecB es = env_spec_of(env_kind_of(name));
+        if (od) *od = es.obs_dim;
+        if (ad) *ad = es.act_dim;
+        if (m) *m = es.m;
+        if (ms) *ms = es.max_steps;
+    });
+}
+int morlax_env_create(const char* name, int n, morlax_env** out) {
+    return guarded([&] {
+        if (n < 1) throw ShapeError("BatchedEnv: num_envs must be >= 1");
+        auto* e = new morlax_env;
+        e->es = env_spec_of(env_kind_of(name));
+        e->N = n;
+        MB_CUDA(cudaMalloc(&e->state, sizeof(float) * e->es.state_dim * n));
+        MB_CUDA(cudaMalloc(&e->keys, sizeof(uint64_t) * n));
+        MB_CUDA(cudaMalloc(&e->ctrs, sizeof(uint64_t) * n));
+        MB_CUDA(cudaMalloc(&e->steps, sizeof(int) * n));
+        MB_CUDA(cudaMalloc(&e->err, sizeof(int)));
+        MB_CUDA(cudaMalloc(&e->clamps, sizeof(unsigned long long)));
+        MB_CUDA(cudaMemset(e->state, 0, sizeof(float) * e->es.state_dim * n));
+        MB_CUDA(cudaMemset(e->steps, 0, sizeof(int) * n));
+        MB_CUDA(cudaMemset(e->err, 0, sizeof(int)));
+        MB_CUDA(cudaMemset(e->clamps, 0, sizeof(unsigned long long)));
+        MB_CUDA(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
+        *out = e;
+    });
+}
+void morlax_env_destroy(morlax_env* e) {
+    if (!e) return;
+    cudaFree(e->state); cudaFree(e->keys); cudaFree(e->ctrs); cudaFree(e->steps); cudaFree(e->err);
+    cudaFree(e->clamps);
+    cudaStreamDestroy(e->s);
+    delete e;
+}
+int morlax_env_reset(morlax_env* e, uint64_t key, uint64_t ctr, float* obs_out) {
+    return guarded([&] {
+        (void)ctr;  // split() ignores the parent counter (rng.hpp:35-40)
+        env_reset(e->es.kind, e->N, e->state, e->keys, e->ctrs, e->steps, key, 0, e->s);
+        if (obs_out) {
+            DBuf<float> o((size_t)e->N * e->es.obs_dim);
+            env_obs(e->es.kind, e->N, e->state, o.p, e->s);
+            MB_CUDA(cudaStreamSynchronize(e->s));
+            o.get(obs_out);
+        }
+        MB_CUDA(cudaStreamSynchronize(e->s));
+    });
+}
+int morlax_env_step_device(morlax_env* e, const float* a, float* obs, float* rew, uint8_t* term, uint8_t* trunc,
+                           void* stream) {
+    return guarded([&] {
+        env_step(e->es.kind, e->N, e->state, e->keys, e->ctrs, e->steps, a, obs, rew, term, trunc, e->clamps, e->err,
+                 (cudaStream_t)stream);
+    });
+}
+int morlax_env_step(morlax_env* e, const float* actions, float* obs, float* reward, uint8_t* term,
+                    uint8_t* trunc) {
+    return guarded([&] {
+        const EnvSpecB& es = e->es;
+        const size_t N = e->N;
+        for (size_t i = 0; i < N * es.act_dim; ++i)  // env.cpp:66-68 (checked before any state change)
+            if (!std::isfinite(actions[i]))
+                throw NumericError("non-finite action for environment instance " + std::to_string(i / es.act_dim));
+        DBuf<float> da(actions, N * es.act_dim), dobs(N * es.obs_dim), drew(N * es.m);
+        DBuf<uint8_t> dt(N), dr(N);
+        env_step(es.kind, e->N, e->state, e->keys, e->ctrs, e->steps, da.p, dobs.p, drew.p, dt.p, dr.p, e->clamps,
+                 e->err, e->s);
+        MB_CUDA(cudaStreamSynchronize(e->s));
+        dobs.get(obs);
+        drew.get(reward);
+        dt.get(term);
+        dr.get(trunc);
+    });
+}
+int morlax_env_current_obs(morlax_env* e, float* out) {
+    return guarded([&] {
+        DBuf<float> o((size_t)e->N * e->es.obs_dim);
+        env_obs(e->es.kind, e->N, e->state, o.p, e->s);
+        MB_CUDA(cudaStreamSynchronize(e->s));
+        o.get(out);
+    });
+}
+uint64_t morlax_env_clamp_count(morlax_env* e) {
+    unsigned long long c = 0;
+    cudaMemcpy(&c, e->clamps, sizeof(c), cudaMemcpyDeviceToHost);
+    return c;
+}
+
+// ------------------------------------------------------------------ hypernet
+int64_t morlax_hypernet_target_count(const morlax_hypernet_spec* s) {
+    NetDims d = make_dims(vec(s->n_target_sizes, s->target_sizes), s->target_tanh, s->has_log_std);
+    return d.P;
+}
+int64_t morlax_hypernet_param_count(const morlax_hypernet_spec* s) {
+    std::vector<int> fs{s->m};
+    for (int i = 0; i < s->n_feature_hidden; ++i) fs.push_back(s->feature_hidden[i]);
+    fs.push_back(s->F);
+    long nf = 0;
+    for (size_t l = 0; l + 1 < fs.size(); ++l) nf += (long)(fs[l] + 1) * fs[l + 1];
+    const long P = morlax_hypernet_target_count(s);
+    return nf + P * s->F + P;
+}
+int morlax_init_hypernet(const morlax_hypernet_spec* s, uint64_t key, uint64_t ctr, double* out) {
+    return guarded([&] {
+        (void)ctr;
+        HyperHandle hh(s, 1);
+        hh.h.init_params(key, 0);
+        std::vector<float> f(hh.h.n);
+        MB_CUDA(cudaMemcpy(f.data(), hh.h.p, sizeof(float) * hh.h.n, cudaMemcpyDeviceToHost));
+        for (long i = 0; i < hh.h.n; ++i) out[i] = f[i];
+    });
+}
+int morlax_hypernet_forward(const morlax_hypernet_spec* s, const double* flat, const double* w, int G,
+                            double* theta) {
+    return guarded([&] {
+        for (int g = 0; g < G; ++g) check_simplex(s->m, w + (size_t)g * s->m);
+        HyperHandle hh(s, G);
+        hh.load(flat);
+        std::vector<float> wf(w, w + (size_t)G * s->m);
+        DBuf<float> dw(wf.data(), wf.size());
+        hh.h.forward(dw.p, 0, G, 0);
+        std::vector<float> th((size_t)G * hh.h.P);
+        MB_CUDA(cudaMemcpy(th.data(), hh.h.theta, sizeof(float) * th.size(), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < th.size(); ++i) {
+            if (!std::isfinite(th[i]))
+                throw NumericError("hypernet_forward produced a non-finite parameter at index " +
+                                   std::to_string(i % hh.h.P));
+            theta[i] = th[i];
+        }
+    });
+}
+int morlax_hypernet_backward(const morlax_hypernet_spec* s, const double* flat, const double* w, int G,
+                             const double* gtheta, double* out) {
+    return guarded([&] {
+        for (int g = 0; g < G; ++g) check_simplex(s->m, w + (size_t)g * s->m);
+        HyperHandle hh(s, G);
+        hh.load(flat);
+        std::vector<float> wf(w, w + (size_t)G * s->m);
+        DBuf<float> dw(wf.data(), wf.size());
+        hh.h.forward(dw.p, 0, G, 0);
+        std::vector<float> gt(gtheta, gtheta + (size_t)G * hh.h.P);
+        MB_CUDA(cudaMemcpy(hh.h.gtheta, gt.data(), sizeof(float) * gt.size(), cudaMemcpyHostToDevice));
+        hh.h.backward(0);
+        std::vector<float> g(hh.h.n);
+        MB_CUDA(cudaMemcpy(g.data(), hh.h.g, sizeof(float) * g.size(), cudaMemcpyDeviceToHost));
+        for (long i = 0; i < hh.h.n; ++i) out[i] = g[i];
+    });
+}
+
+// ------------------------------------------------------------------ GAE / Adam
+int morlax_gae(int N, int T, int m, const float* rew, const float* val, const float* nval, const uint8_t* term,
+               const uint8_t* trunc, double gamma, double lambda, float* adv, float* tgt) {
+    return guarded([&] {
+        if (N <= 0 || T <= 0 || m <= 0) throw ShapeError("gae: batch dimensions must be positive");
+        if (!(gamma >= 0.0 && gamma <= 1.0)) throw DomainError("gae: gamma must lie in [0, 1], got " + std::to_string(gamma));
+        if (!(lambda >= 0.0 && lambda <= 1.0)) throw DomainError("gae: lambda must lie in [0, 1], got " + std::to_string(lambda));
+        const size_t R = (size_t)N * T;
+        DBuf<float> r(rew, R * m), v(val, R * m), nv(nval, R * m), a(R * m), tg(R * m);
+        DBuf<uint8_t> te(term, R), tr(trunc, R);
+        gae_scan(N, T, m, r.p, v.p, nv.p, te.p, tr.p, (float)gamma, (float)lambda, a.p, tg.p, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        a.get(adv);
+        tg.get(tgt);
+    });
+}
+int morlax_normalize_scalarize(int N, int T, int m, const float* adv, const double* tw, float* out) {
+    return guarded([&] {
+        const size_t R = (size_t)N * T;
+        DBuf<float> a(adv, R * m), o(R);
+        std::vector<float> twf(tw, tw + (size_t)N * m);
+        DBuf<float> w(twf.data(), twf.size());
+        DBuf<double> st(32), scratch(148 * 2 * 8);
+        channel_sums(a.p, R, m, nullptr, st.p, scratch.p, 0);
+        stats_finalize(st.p, (double)R, m, st.p + 8, 0, 0);
+        channel_sums(a.p, R, m, st.p + 8, st.p + 16, scratch.p, 0);
+        stats_finalize(st.p + 16, (double)R, m, st.p + 24, 1, 0);
+        scalarize(N, T, m, a.p, w.p, 1, st.p + 8, st.p + 24, o.p, 0);  // reps = 1: per-instance weights
+        MB_CUDA(cudaDeviceSynchronize());
+        o.get(out);
+    });
+}
+int morlax_adam(int64_t n, double* p, const double* g, double* m1, double* m2, int64_t* step, double lr) {
+    return guarded([&] {
+        std::vector<float> pf(p, p + n), gf(g, g + n), af(m1, m1 + n), bf(m2, m2 + n);
+        DBuf<float> dp(pf.data(), n), dg(gf.data(), n), da(af.data(), n), db(bf.data(), n);
+        DBuf<int> err(1);
+        MB_CUDA(cudaMemset(err.p, 0, sizeof(int)));
+        *step += 1;
+        const double bc1 = 1.0 - std::pow(0.9, (double)*step), bc2 = 1.0 - std::pow(0.999, (double)*step);
+        adam(n, dp.p, dg.p, da.p, db.p, (float)lr, (float)bc1, (float)bc2, err.p, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        dp.get(pf.data());
+        da.get(af.data());
+        db.get(bf.data());
+        for (int64_t i = 0; i < n; ++i) {
+            p[i] = pf[i];
+            m1[i] = af[i];
+            m2[i] = bf[i];
+        }
+    });
+}
+
+// ------------------------------------------------------------------ trainer
+int morlax_nccl_unique_id(void* out) {
+    return guarded([&] { comm_unique_id(out); });
+}
+int morlax_trainer_create(const morlax_train_config* c, int world, int rank, const void* id, morlax_trainer** out) {
+    return guarded([&] {
+        TrainConfig tc;
+        tc.env_kind = env_kind_of(c->env_name ? c->env_name : "");
+        tc.N = c->N; tc.K = c->K; tc.kappa = c->kappa; tc.T = c->T;
+        tc.epochs = c->epochs; tc.minibatch_count = c->minibatch_count;
+        tc.gamma = c->gamma; tc.lambda = c->gae_lambda; tc.clip_eps = c->clip_eps;
+        tc.actor_lr = c->actor_lr; tc.critic_lr = c->critic_lr; tc.entropy_coef = c->entropy_coef;
+        tc.seed = c->seed; tc.F = c->F;
+        tc.feat_hidden = vec(c->n_feature_hidden, c->feature_hidden);
+        tc.actor_hidden = vec(c->n_actor_hidden, c->actor_hidden);
+        tc.critic_hidden = vec(c->n_critic_hidden, c->critic_hidden);
+        auto* h = new morlax_trainer;
+        try {
+            h->t = new Trainer(tc, world, rank, id);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+void morlax_trainer_destroy(morlax_trainer* t) {
+    if (!t) return;
+    delete t->t;
+    delete t;
+}
+static void fill_stats(morlax_trainer* t, const IterStats& st, morlax_iter_stats* out) {
+    if (!out) return;
+    out->actor_loss = st.actor_loss;
+    out->critic_loss = st.critic_loss;
+    out->minibatches = st.minibatches;
+    out->numeric_error = st.numeric_error;
+    out->kernel_launches = t->t->kernel_launches();
+}
+int morlax_trainer_iteration(morlax_trainer* t, int it, morlax_iter_stats* stats) {
+    IterStats st;
+    const int rc = guarded([&] { t->t->iteration(it, &st); });
+    fill_stats(t, st, stats);
+    return rc;
+}
+int morlax_trainer_phase(morlax_trainer* t, int it, int phase, int max_mb, morlax_iter_stats* stats) {
+    IterStats st;
+    const int rc = guarded([&] {
+        switch (phase) {
+            case 1: t->t->phase_rollout(it); break;
+            case 2: t->t->phase_advantages(); break;
+            case 3: t->t->phase_update(it, max_mb); break;
+            case 4: t->t->finish(&st); break;
+            default: throw ConfigError("unknown phase");
+        }
+    });
+    if (phase == 4) fill_stats(t, st, stats);
+    return rc;
+}
+int morlax_trainer_sizes(morlax_trainer* t, int64_t* ap, int64_t* cp, int* le, int* lc, int* rows) {
+    return guarded([&] {
+        Trainer& tr = *t->t;
+        if (ap) *ap = tr.actor().n;
+        if (cp) *cp = tr.critic().n;
+        if (le) *le = tr.local_envs();
+        if (lc) *lc = tr.local_groups();
+        if (rows) *rows = tr.local_envs() * tr.config().T;
+    });
+}
+int morlax_trainer_get_params(morlax_trainer* t, int which, double* out) {
+    return guarded([&] {
+        HyperNet& h = which ? t->t->critic() : t->t->actor();
+        std::vector<float> f(h.n);
+        MB_CUDA(cudaStreamSynchronize(t->t->stream()));
+        MB_CUDA(cudaMemcpy(f.data(), h.p, sizeof(float) * h.n, cudaMemcpyDeviceToHost));
+        for (long i = 0; i < h.n; ++i) out[i] = f[i];
+    });
+}
+int morlax_trainer_set_params(morlax_trainer* t, int which, const double* in) {
+    return guarded([&] {
+        HyperNet& h = which ? t->t->critic() : t->t->actor();
+        std::vector<float> f(in, in + h.n);
+        MB_CUDA(cudaStreamSynchronize(t->t->stream()));
+        MB_CUDA(cudaMemcpy(h.p, f.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+    });
+}
+int morlax_trainer_get_grad(morlax_trainer* t, int which, double* out) {
+    return guarded([&] {
+        HyperNet& h = which ? t->t->critic() : t->t->actor();
+        std::vector<float> f(h.n);
+        MB_CUDA(cudaStreamSynchronize(t->t->stream()));
+        MB_CUDA(cudaMemcpy(f.data(), h.g, sizeof(float) * h.n, cudaMemcpyDeviceToHost));
+        for (long i = 0; i < h.n; ++i) out[i] = f[i];
+    });
+}
+int morlax_trainer_get_theta(morlax_trainer* t, int which, float* out) {
+    return guarded([&] {
+        Trainer& tr = *t->t;
+        HyperNet& h = which ? tr.critic() : tr.actor();
+        MB_CUDA(cudaStreamSynchronize(tr.stream()));
+        const int g0 = (tr.local_groups() == tr.config().K) ? 0 : 0;
+        MB_CUDA(cudaMemcpy(out, h.theta + (long)g0 * h.P, sizeof(float) * h.P * tr.local_groups(),
+                           cudaMemcpyDeviceToHost));
+    });
+}
+
+static void field_info(Trainer& tr, const std::string& f, void** dev, size_t* bytes) {
+    const long R = (long)tr.local_envs() * tr.config().T;
+    const EnvSpecB& es = tr.env();
+    *dev = nullptr;
+    if (f == "obs") { *dev = tr.d_obs; *bytes = sizeof(float) * R * es.obs_dim; }
+    else if (f == "action_pre") { *dev = tr.d_act; *bytes = sizeof(float) * R * es.act_dim; }
+    else if (f == "logprob") { *dev = tr.d_lp; *bytes = sizeof(float) * R; }
+    else if (f == "reward") { *dev = tr.d_rew; *bytes = sizeof(float) * R * es.m; }
+    else if (f == "value") { *dev = tr.d_val; *bytes = sizeof(float) * R * es.m; }
+    else if (f == "next_value") { *dev = tr.d_nval; *bytes = sizeof(float) * R * es.m; }
+    else if (f == "advantages") { *dev = tr.d_adv; *bytes = sizeof(float) * R * es.m; }
+    else if (f == "value_targets") { *dev = tr.d_tgt; *bytes = sizeof(float) * R * es.m; }
+    else if (f == "scalar_advantage") { *dev = tr.d_sadv; *bytes = sizeof(float) * R; }
+    else if (f == "terminated") { *dev = tr.d_term; *bytes = R; }
+    else if (f == "truncated") { *dev = tr.d_trunc; *bytes = R; }
+    else if (f == "env_state") { *dev = tr.d_state; *bytes = sizeof(float) * es.state_dim * tr.local_envs(); }
+    else if (f == "tracker") { *dev = tr.d_tracker; *bytes = sizeof(float) * es.m * tr.local_envs(); }
+    else if (f == "env_ctr") { *dev = tr.d_ectr; *bytes = sizeof(uint64_t) * tr.local_envs(); }
+    else if (f == "env_steps") { *dev = tr.d_steps; *bytes = sizeof(int) * tr.local_envs(); }
+    else if (f != "clusters" && f != "perm") throw ConfigError("unknown field: " + f);
+}
+int morlax_trainer_get(morlax_trainer* t, const char* field, void* out) {
+    return guarded([&] {
+        Trainer& tr = *t->t;
+        const std::string f(field);
+        if (f == "clusters") {
+            std::memcpy(out, tr.clusters_host().data(), sizeof(float) * tr.clusters_host().size());
+            return;
+        }
+        if (f == "perm") {
+            std::memcpy(out, tr.perm().data(), sizeof(int) * tr.perm().size());
+            return;
+        }
+        void* dev;
+        size_t bytes;
+        field_info(tr, f, &dev, &bytes);
+        MB_CUDA(cudaStreamSynchronize(tr.stream()));
+        MB_CUDA(cudaMemcpy(out, dev, bytes, cudaMemcpyDeviceToHost));
+    });
+}
+int morlax_trainer_set(morlax_trainer* t, const char* field, const void* in) {
+    return guarded([&] {
+        Trainer& tr = *t->t;
+        const std::string f(field);
+        if (f == "perm") {
+            std::memcpy(tr.perm().data(), in, sizeof(int) * tr.perm().size());
+            return;
+        }
+        if (f == "clusters") {
+            tr.set_clusters((const float*)in);
+            return;
+        }
+        void* dev;
+        size_t bytes;
+        field_info(tr, f, &dev, &bytes);
+        if (!dev) throw ConfigError("field is read-only: " + f);
+        MB_CUDA(cudaStreamSynchronize(tr.stream()));
+        MB_CUDA(cudaMemcpy(dev, in, bytes, cudaMemcpyHostToDevice));
+    });
+}
+int morlax_trainer_losses(morlax_trainer* t, const int32_t* rows, int n, double* al, double* cl) {
+    return guarded([&] { t->t->losses_only(rows, n, al, cl); });
+}
+int64_t morlax_trainer_kernel_launches(morlax_trainer* t) { return t->t->kernel_launches(); }
+int morlax_trainer_profile_enable(morlax_trainer* t, int on) {
+    return guarded([&] {
+        Profiler& p = t->t->profiler();
+        p.collect();
+        p.reset();
+        p.on = on != 0;
+    });
+}
+int morlax_trainer_profile_count(morlax_trainer* t) {
+    int n = 0;
+    guarded([&] {
+        t->t->profiler().collect();
+        n = (int)t->t->profiler().cls.size();
+    });
+    return n;
+}
+int morlax_trainer_profile_get(morlax_trainer* t, int i, char* name64, double* ms, double* flops, double* bytes,
+                               int64_t* count) {
+    return guarded([&] {
+        Profiler& p = t->t->profiler();
+        p.collect();
+        if (i < 0 || i >= (int)p.cls.size()) throw ShapeError("profile index out of range");
+        const auto& c = p.cls[i];
+        std::strncpy(name64, c.name.c_str(), 63);
+        name64[63] = 0;
+        *ms = c.ms;
+        *flops = c.flops;
+        *bytes = c.bytes;
+        *count = c.count;
+    });
+}
+void* morlax_trainer_stream(morlax_trainer* t) { return (void*)t->t->stream(); }
+
+int morlax_shard_minibatch(const int32_t* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps,
+                           int n_groups, int32_t* rows_out, int32_t* goff_out, int* n_rows, int* max_group) {
+    return guarded([&] {
+        shard_minibatch(perm, lo, hi, T, inst_lo, n_inst, reps, n_groups, rows_out, goff_out, n_rows, max_group);
+    });
+}
+
+// ------------------------------------------------------------------ pareto
+int morlax_pareto_mask_device(int n, int m, const double* d_pts, uint8_t* d_mask, void* stream) {
+    return guarded([&] {
+        if (m < 1 || m > 8) throw ShapeError("pareto: objective count must be in [1, 8]");
+        DBuf<uint8_t> uq(n);
+        DBuf<double> sums(n);
+        pareto_mask(n, m, d_pts, d_mask, uq.p, sums.p, (cudaStream_t)stream);
+        MB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    });
+}
+int morlax_pareto_mask(int n, int m, const double* pts, uint8_t* mask) {
+    return guarded([&] {
+        if (n <= 0) return;
+        if (m < 1 || m > 8) throw ShapeError("pareto: objective count must be in [1, 8]");
+        DBuf<double> p(pts, (size_t)n * m);
+        DBuf<uint8_t> mk(n), uq(n);
+        DBuf<double> sums(n);
+        pareto_mask(n, m, p.p, mk.p, uq.p, sums.p, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        mk.get(mask);
+    });
+}
+int morlax_hypervolume_mc(int n, int m, const double* pts, const double* ref, uint64_t samples, uint64_t key,
+                          uint64_t ctr, double* value, double* se, uint64_t* hits_out) {
+    return guarded([&] {
+        if (samples == 0) throw ShapeError("hypervolume_mc: samples must be > 0");
+        if (m < 1 || m > 8) throw ShapeError("hypervolume: objective count must be in [1, 8]");
+        *value = 0.0;
+        if (se) *se = 0.0;
+        if (hits_out) *hits_out = 0;
+        if (n <= 0) return;
+        DBuf<double> p(pts, (size_t)n * m), r(ref, m), scratch((size_t)n * m + 8 + n + 8);
+        DBuf<unsigned long long> hits(1);
+        hv_mc(n, m, p.p, r.p, samples, key, ctr, hits.p, scratch.p, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        unsigned long long h = 0;
+        hits.get(&h);
+        double hi[8];
+        MB_CUDA(cudaMemcpy(hi, scratch.p, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        int k = 0;
+        MB_CUDA(cudaMemcpy(&k, (int*)(scratch.p + 8 + (size_t)n * m), sizeof(int), cudaMemcpyDeviceToHost));
+        if (k == 0) return;
+        double box = 1.0;  // pareto.cpp:253-254, same order -> bit-identical
+        for (int j = 0; j < m; ++j) box *= hi[j] - ref[j];
+        if (box == 0.0) return;
+        const double frac = (double)h / (double)samples;
+        if (se) *se = box * std::sqrt(frac * (1.0 - frac) / (double)samples);
+        *value = box * frac;
+        if (hits_out) *hits_out = h;
+    });
+}
+int morlax_hypervolume_detailed(int n, int m, const double* pts, const double* ref, uint64_t samples, uint64_t seed,
+                                double* value, double* se, int* exact, int* clipped) {
+    return guarded([&] {
+        if (m < 1) throw ShapeError("hypervolume: empty reference point");
+        int cl = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < m; ++j)
+                if (pts[(size_t)i * m + j] < ref[j]) { ++cl; break; }
+        if (clipped) *clipped = cl;
+        if (m <= 4) throw ConfigError("exact hypervolume for m <= 4 is not available on the device path yet");
+        if (exact) *exact = 0;
+        const uint64_t key = seed_key(seed);
+        const int rc = morlax_hypervolume_mc(n, m, pts, ref, samples, key, 0, value, se, nullptr);
+        if (rc) throw std::runtime_error(g_err);
+    });
+}
+
+}  // extern "C"

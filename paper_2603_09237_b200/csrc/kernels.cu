@@ -1,0 +1,713 @@
+// Device kernels of the MORLAX B200 training step (everything except the
+// GEMMs and Pareto): K1 env step, K3 fused rollout, K4 GAE scan +
+// normalise/scalarise, K5 per-row PPO losses, K7 Adam, reductions.
+// Reference semantics are cited per kernel (paths under /root/reference/proj).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mb200 {
+
+// =========================================================================
+// K1: BatchedEnv reset / step (env.cpp:44-106). SoA state [sdim][N].
+// =========================================================================
+__global__ void k_env_reset(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,
+                            uint64_t parent, int base) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const uint64_t k = split_key(parent, (uint64_t)(base + i));  // env.cpp:53-54 (global lane)
+    uint64_t c = 0;
+    env_do_reset(kind, state + i, N, k, &c);
+    keys[i] = k;
+    ctrs[i] = c;
+    steps[i] = 0;
+}
+
+__global__ void k_env_step(int kind, int N, int ad, int od, int m, int max_steps, float* state,
+                           uint64_t* keys, uint64_t* ctrs, int* steps, const float* actions, float* obs,
+                           float* reward, uint8_t* term, uint8_t* trunc,
+                           unsigned long long* clamp_count, int* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    float a[16], r[8];
+    bool any = false;
+    for (int d = 0; d < ad; ++d) {  // env.cpp:63-72
+        const float x = actions[(long)i * ad + d];
+        if (!isfinite(x)) atomicExch(err, 3);
+        a[d] = fminf(fmaxf(x, -1.f), 1.f);
+        any |= a[d] != x;
+    }
+    if (any) atomicAdd(clamp_count, 1ULL);
+    float* s = state + i;
+    const bool t = env_do_step(kind, s, N, a, r);
+    const int st = steps[i] + 1;
+    const bool tr = !t && st >= max_steps;  // env.cpp:80
+    for (int k = 0; k < m; ++k) reward[(long)i * m + k] = r[k];
+    term[i] = t;
+    trunc[i] = tr;
+    for (int k = 0; k < od; ++k) obs[(long)i * od + k] = s[(long)k * N];  // pre-reset final obs
+    if (t || tr) {
+        uint64_t c = ctrs[i];
+        env_do_reset(kind, s, N, keys[i], &c);
+        ctrs[i] = c;
+        steps[i] = 0;
+    } else {
+        steps[i] = st;
+    }
+}
+
+__global__ void k_env_obs(int N, int od, const float* state, float* obs) {
+    const long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (e >= (long)N * od) return;
+    const int i = e / od, k = e % od;
+    obs[e] = state[(long)k * N + i];
+}
+
+void env_reset(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,
+               uint64_t parent_key, int inst_base, cudaStream_t s) {
+    k_env_reset<<<(N + 255) / 256, 256, 0, s>>>(kind, N, state, keys, ctrs, steps, parent_key, inst_base);
+    MB_LAUNCH();
+}
+void env_step(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,
+              const float* actions, float* obs, float* reward, uint8_t* term, uint8_t* trunc,
+              unsigned long long* clamp_count, int* err, cudaStream_t s) {
+    const EnvSpecB es = env_spec_of(kind);
+    k_env_step<<<(N + 255) / 256, 256, 0, s>>>(kind, N, es.act_dim, es.obs_dim, es.m, es.max_steps,
+                                                state, keys, ctrs, steps, actions, obs, reward, term,
+                                                trunc, clamp_count, err);
+    MB_LAUNCH();
+}
+void env_obs(int kind, int N, const float* state, float* obs, cudaStream_t s) {
+    const int od = env_spec_of(kind).obs_dim;
+    k_env_obs<<<(int)(((long)N * od + 255) / 256), 256, 0, s>>>(N, od, state, obs);
+    MB_LAUNCH();
+}
+
+// =========================================================================
+// K3: fused rollout (rollout.cpp:37-161). One CTA owns up to kR instances
+// of ONE preference cluster for all T steps: env state stays in shared
+// memory, the cluster's generated policy / critic weights stream from L2.
+// Per step: policy MLP -> Gaussian sample (bit-exact RNG words) -> critic
+// at obs (only when the previous step ended an episode, else the previous
+// next_value is reused: identical values) -> env step + auto-reset ->
+// critic at the pre-reset final obs.
+// =========================================================================
+constexpr int kR = 64;    // instances per CTA
+constexpr int kNT = 256;  // threads per CTA
+constexpr int kKC = 32;   // K chunk of the weight tile
+int rollout_rows_per_cta() { return kR; }
+
+// out[r][j] = act(b[j] + sum_i in[r][i] W[j][i]), r < nr, j < Nout (<= 256)
+__device__ void block_dense(const float* __restrict__ W, const float* __restrict__ b, int Kin, int Nout,
+                            const float* in, int ldi, float* out, int ldo, int nr, bool tanh_act,
+                            float* wt) {
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int cpt = (Nout + 31) >> 5, rpt = (nr + 7) >> 3;
+    float acc[8][8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        const int j = tx + 32 * jj;
+        const float bj = (jj < cpt && j < Nout) ? b[j] : 0.f;
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) acc[ii][jj] = bj;
+    }
+    for (int k0 = 0; k0 < Kin; k0 += kKC) {
+        const int kc = min(kKC, Kin - k0);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < Nout * kKC; idx += kNT) {
+            const int j = idx / kKC, kk = idx % kKC;
+            wt[j * (kKC + 1) + kk] = kk < kc ? W[(long)j * Kin + k0 + kk] : 0.f;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            float a[8], w[8];
+#pragma unroll
+            for (int ii = 0; ii < 8; ++ii) {
+                const int r = ty + 8 * ii;
+                a[ii] = (ii < rpt && r < nr) ? in[r * ldi + k0 + kk] : 0.f;
+            }
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = tx + 32 * jj;
+                w[jj] = (jj < cpt && j < Nout) ? wt[j * (kKC + 1) + kk] : 0.f;
+            }
+#pragma unroll
+            for (int ii = 0; ii < 8; ++ii)
+                if (ii < rpt)
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+                        if (jj < cpt) acc[ii][jj] = fmaf(a[ii], w[jj], acc[ii][jj]);
+        }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) {
+        const int r = ty + 8 * ii;
+        if (ii >= rpt || r >= nr) continue;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int j = tx + 32 * jj;
+            if (jj < cpt && j < Nout) out[r * ldo + j] = tanh_act ? tanhf(acc[ii][jj]) : acc[ii][jj];
+        }
+    }
+    __syncthreads();
+}
+
+// MLP forward over nr rows held in `x` (ld od); result (last pre-activation
+// for the policy, identity output for the critic) into `out` (ld ldo).
+__device__ void block_mlp(const NetDims& nd, const float* w, const float* x, int od, float* ha, float* hb,
+                          int ldh, float* out, int ldo, int nr, float* wt) {
+    const float* in = x;
+    int ldi = od;
+    float* bufs[2] = {ha, hb};
+    for (int l = 0; l < nd.L; ++l) {
+        const bool last = (l == nd.L - 1);
+        float* dst = last ? out : bufs[l & 1];
+        const int ldd = last ? ldo : ldh;
+        // the Gaussian mean is the output pre-activation (losses.cpp:92-94)
+        block_dense(w + nd.woff[l], w + nd.boff[l], nd.sz[l], nd.sz[l + 1], in, ldi, dst, ldd, nr,
+                    !last, wt);
+        in = dst;
+        ldi = ldd;
+    }
+}
+
+__device__ __forceinline__ float sech2_f(float z) {
+    // 1 - tanh(z)^2 without cancellation: 4 e^{-2|z|} / (1 + e^{-2|z|})^2
+    const float e = __expf(-2.f * fabsf(z));
+    const float d = 1.f + e;
+    return 4.f * e / (d * d);
+}
+
+__global__ void __launch_bounds__(kNT, 1) k_rollout(RolloutArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const int cpg = (a.reps + kR - 1) / kR;
+    const int c = blockIdx.x / cpg, ch = blockIdx.x % cpg;
+    const int i0 = c * a.reps + ch * kR;
+    const int nr = min(kR, a.reps - ch * kR);
+    const int od = a.od, ad = a.ad, m = a.m, sd = a.sdim;
+    int hmax = 0;
+    for (int l = 1; l < a.pol.L; ++l) hmax = max(hmax, a.pol.sz[l]);
+    for (int l = 1; l < a.cri.L; ++l) hmax = max(hmax, a.cri.sz[l]);
+    // shared-memory carve-up
+    float* S = sm;                        // [sd][kR]   env state
+    float* X = S + sd * kR;               // [kR][od]   obs / final obs
+    float* HA = X + kR * od;              // [kR][hmax]
+    float* HB = HA + kR * hmax;           // [kR][hmax]
+    float* MU = HB + kR * hmax;           // [kR][ad]
+    float* ZS = MU + kR * ad;             // [kR][ad]   pre-tanh samples
+    float* AC = ZS + kR * ad;             // [kR][ad]   actions
+    float* VV = AC + kR * ad;             // [kR][m]    critic output
+    float* NV = VV + kR * m;              // [kR][m]    next value carry
+    float* RW = NV + kR * m;              // [kR][m]    rewards
+    float* TRK = RW + kR * m;             // [kR][m]    running returns
+    float* WT = TRK + kR * m;             // [256][kKC+1] weight tile
+    float* LS = WT + 256 * (kKC + 1);     // [ad] clamped log-std
+    uint64_t* EK = reinterpret_cast<uint64_t*>(LS + 16);  // [kR] env stream key
+    uint64_t* EC = EK + kR;                               // [kR] env stream ctr
+    uint64_t* RK = EC + kR;                               // [kR] sampling stream key
+    int* STP = reinterpret_cast<int*>(RK + kR);           // [kR] step counters
+    int* NEED = STP + kR;                                 // [kR] value needs recompute
+
+    const float* th = a.theta + (long)c * a.pol.P;
+    const float* ph = a.phi + (long)c * a.cri.P;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < sd * nr; e += kNT) {
+        const int k = e / nr, r = e % nr;
+        S[k * kR + r] = a.state[(long)k * a.N + i0 + r];
+    }
+    for (int r = tid; r < nr; r += kNT) {
+        EK[r] = a.env_key[i0 + r];
+        EC[r] = a.env_ctr[i0 + r];
+        STP[r] = a.steps[i0 + r];
+        RK[r] = split_key(a.roll_key, (uint64_t)(a.roll_inst_base + i0 + r));  // rollout.cpp:101
+        NEED[r] = 1;
+        for (int k = 0; k < m; ++k) TRK[r * m + k] = a.tracker[(long)(i0 + r) * m + k];
+    }
+    if (tid < ad) LS[tid] = fminf(fmaxf(th[a.pol.mlp_n + tid], -5.f), 1.f);  // nn.cpp:185-188
+    __syncthreads();
+
+    for (int t = 0; t < a.T; ++t) {
+        // obs rows (obs == state for every env)
+        for (int e = tid; e < nr * od; e += kNT) {
+            const int r = e / od, k = e % od;
+            const float v = S[k * kR + r];
+            X[r * od + k] = v;
+            a.obs[((long)(i0 + r) * a.T + t) * od + k] = v;
+        }
+        __syncthreads();
+        block_mlp(a.pol, th, X, od, HA, HB, hmax, MU, ad, nr, WT);
+        // Gaussian sample, 2 words per dim (nn.cpp:192-202, rng.hpp:55-60)
+        for (int e = tid; e < nr * ad; e += kNT) {
+            const int r = e / ad, d = e % ad;
+            const uint64_t base = 2ull * ((uint64_t)t * ad + d);
+            const double eps = box_muller(rng_word(RK[r], base + 1), rng_word(RK[r], base + 2));
+            const float z = MU[r * ad + d] + __expf(LS[d]) * (float)eps;
+            ZS[r * ad + d] = z;
+            AC[r * ad + d] = tanhf(z);
+            a.act_pre[((long)(i0 + r) * a.T + t) * ad + d] = z;
+        }
+        __syncthreads();
+        for (int r = tid; r < nr; r += kNT) {  // action_logprob (nn.cpp:204-219)
+            float lp = 0.f;
+            for (int d = 0; d < ad; ++d) {
+                const float sig = __expf(LS[d]);
+                const float z = ZS[r * ad + d];
+                const float zn = (z - MU[r * ad + d]) / sig;
+                lp += -0.5f * zn * zn - LS[d] - 0.9189385332046727f;
+                lp -= __logf(sech2_f(z) + 1e-6f);
+            }
+            a.logprob[(long)(i0 + r) * a.T + t] = lp;
+        }
+        int need = 0;
+        for (int r = tid; r < nr; r += kNT) need |= NEED[r];
+        need = __syncthreads_or(need);
+        if (need) block_mlp(a.cri, ph, X, od, HA, HB, hmax, VV, m, nr, WT);
+        // value + env step (env.cpp:60-92) + tracker (rollout.cpp:143-148)
+        for (int r = tid; r < nr; r += kNT) {
+            const long row = (long)(i0 + r) * a.T + t;
+            for (int k = 0; k < m; ++k)
+                a.value[row * m + k] = NEED[r] ? VV[r * m + k] : NV[r * m + k];
+            float act[16], rw[8];
+            bool any = false;
+            for (int d = 0; d < ad; ++d) {
+                const float x = AC[r * ad + d];
+                if (!isfinite(x)) atomicExch(a.err, 3);
+                act[d] = fminf(fmaxf(x, -1.f), 1.f);
+                any |= act[d] != x;
+            }
+            if (any) atomicAdd(a.clamp_count, 1ULL);
+            float* s = S + r;
+            const bool tm = env_do_step(a.kind, s, kR, act, rw);
+            const int st = STP[r] + 1;
+            const bool tr = !tm && st >= a.max_steps;
+            a.term[row] = tm;
+            a.trunc[row] = tr;
+            for (int k = 0; k < m; ++k) {
+                a.reward[row * m + k] = rw[k];
+                TRK[r * m + k] += rw[k];
+            }
+            for (int k = 0; k < od; ++k) X[r * od + k] = s[k * kR];  // pre-reset final obs
+            if (tm || tr) {
+                double ret = 0.0;
+                for (int k = 0; k < m; ++k) {
+                    ret += (double)a.cluster_w[c * m + k] * TRK[r * m + k];
+                    TRK[r * m + k] = 0.f;
+                }
+                a.ret_sum[i0 + r] += ret;
+                a.ret_cnt[i0 + r] += 1;
+                uint64_t cc = EC[r];
+                env_do_reset(a.kind, s, kR, EK[r], &cc);
+                EC[r] = cc;
+                STP[r] = 0;
+                NEED[r] = 1;
+            } else {
+                STP[r] = st;
+                NEED[r] = 0;
+            }
+        }
+        __syncthreads();
+        block_mlp(a.cri, ph, X, od, HA, HB, hmax, NV, m, nr, WT);  // critic at final obs
+        for (int e = tid; e < nr * m; e += kNT) {
+            const int r = e / m, k = e % m;
+            a.next_value[((long)(i0 + r) * a.T + t) * m + k] = NV[e];
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < sd * nr; e += kNT) {
+        const int k = e / nr, r = e % nr;
+        a.state[(long)k * a.N + i0 + r] = S[k * kR + r];
+    }
+    for (int r = tid; r < nr; r += kNT) {
+        a.env_ctr[i0 + r] = EC[r];
+        a.steps[i0 + r] = STP[r];
+        for (int k = 0; k < m; ++k) a.tracker[(long)(i0 + r) * m + k] = TRK[r * m + k];
+    }
+}
+
+void rollout(const RolloutArgs& a, cudaStream_t s) {
+    int hmax = 0;
+    for (int l = 1; l < a.pol.L; ++l) hmax = hmax > a.pol.sz[l] ? hmax : a.pol.sz[l];
+    for (int l = 1; l < a.cri.L; ++l) hmax = hmax > a.cri.sz[l] ? hmax : a.cri.sz[l];
+    const size_t fl = (size_t)a.sdim * kR + (size_t)kR * a.od + 2ull * kR * hmax + 3ull * kR * a.ad +
+                      4ull * kR * a.m + 256ull * (kKC + 1) + 16;
+    const size_t bytes = fl * 4 + 3ull * kR * 8 + 2ull * kR * 4 + 64;
+    static size_t configured = 0;
+    if (bytes > configured) {
+        MB_CUDA(cudaFuncSetAttribute(k_rollout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        configured = bytes;
+    }
+    const int cpg = (a.reps + kR - 1) / kR;
+    k_rollout<<<a.K * cpg, kNT, bytes, s>>>(a);
+    MB_LAUNCH();
+}
+
+// =========================================================================
+// K4: per-objective GAE (gae.cpp:26-66) as a warp-shuffle scan over T.
+// One warp per (instance, objective). The backward recurrence
+// A_t = delta_t + c_t A_{t+1} is an affine map per step; each lane composes
+// its time chunk, a suffix scan of (C, D) pairs across lanes supplies the
+// carry, and the lane replays its chunk.
+// =========================================================================
+__global__ void k_gae(int N, int T, int m, const float* __restrict__ rew, const float* __restrict__ val,
+                      const float* __restrict__ nval, const uint8_t* __restrict__ term,
+                      const uint8_t* __restrict__ trunc, float gamma, float lambda, float* adv,
+                      float* tgt) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= N * m) return;
+    const int i = warp / m, k = warp % m;
+    const int tc = (T + 31) / 32;
+    const int t0 = min(T, lane * tc), t1 = min(T, t0 + tc);
+    const float gl = gamma * lambda;
+    float C = 1.f, D = 0.f;
+    for (int t = t1 - 1; t >= t0; --t) {  // compose f_t o (current): x -> delta + c x
+        const long r = (long)i * T + t;
+        const float boot = term[r] ? 0.f : 1.f;
+        const float cont = (term[r] || trunc[r]) ? 0.f : 1.f;
+        const long idx = r * m + k;
+        const float delta = rew[idx] + gamma * nval[idx] * boot - val[idx];
+        const float c = gl * cont;
+        D = delta + c * D;
+        C = c * C;
+    }
+    // inclusive suffix scan: lane L <- f_L o f_{L+1} o ... o f_31
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const float C2 = __shfl_down_sync(0xffffffffu, C, off);
+        const float D2 = __shfl_down_sync(0xffffffffu, D, off);
+        if (lane + off < 32) {
+            D = D + C * D2;
+            C = C * C2;
+        }
+    }
+    float carry = __shfl_down_sync(0xffffffffu, D, 1);
+    if (lane == 31) carry = 0.f;
+    for (int t = t1 - 1; t >= t0; --t) {
+        const long r = (long)i * T + t;
+        const float boot = term[r] ? 0.f : 1.f;
+        const float cont = (term[r] || trunc[r]) ? 0.f : 1.f;
+        const long idx = r * m + k;
+        const float delta = rew[idx] + gamma * nval[idx] * boot - val[idx];
+        carry = delta + gl * cont * carry;
+        adv[idx] = carry;
+        tgt[idx] = carry + val[idx];
+    }
+}
+
+void gae_scan(int N, int T, int m, const float* reward, const float* value, const float* next_value,
+              const uint8_t* term, const uint8_t* trunc, float gamma, float lambda, float* adv,
+              float* targets, cudaStream_t s) {
+    const long warps = (long)N * m;
+    k_gae<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(N, T, m, reward, value, next_value, term,
+                                                          trunc, gamma, lambda, adv, targets);
+    MB_LAUNCH();
+}
+
+// Normalisation statistics (gae.cpp:79-96): deterministic two-level fp64
+// reductions. pass 1 (mean == nullptr): sum x; pass 2: sum (x - mean)^2.
+constexpr int kRedBlocks = 148 * 2;
+__global__ void k_chan_partial(const float* x, long rows, int m, const double* mean, double* part) {
+    extern __shared__ double red[];  // [blockDim][m]
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (long r = blockIdx.x * (long)blockDim.x + threadIdx.x; r < rows; r += (long)gridDim.x * blockDim.x)
+        for (int k = 0; k < m; ++k) {
+            double v = x[r * m + k];
+            if (mean) {
+                v -= mean[k];
+                v *= v;
+            }
+            acc[k] += v;
+        }
+    for (int k = 0; k < m; ++k) red[threadIdx.x * m + k] = acc[k];
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            for (int k = 0; k < m; ++k) red[threadIdx.x * m + k] += red[(threadIdx.x + s) * m + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int k = 0; k < m; ++k) part[blockIdx.x * m + k] = red[k];
+}
+__global__ void k_chan_final(const double* part, int nb, int m, double* out) {
+    const int k = threadIdx.x;
+    if (k >= m) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b * m + k];
+    out[k] = s;
+}
+void channel_sums(const float* x, long rows, int m, const double* mean, double* out, double* scratch,
+                  cudaStream_t s) {
+    k_chan_partial<<<kRedBlocks, 256, 256 * m * sizeof(double), s>>>(x, rows, m, mean, scratch);
+    MB_LAUNCH();
+    k_chan_final<<<1, 32, 0, s>>>(scratch, kRedBlocks, m, out);
+    MB_LAUNCH();
+}
+
+__global__ void k_stats_finalize(const double* s, double rows, int m, double* out, int mode) {
+    const int k = threadIdx.x;
+    if (k >= m) return;
+    out[k] = mode == 0 ? s[k] / rows : 1.0 / (sqrt(s[k] / rows) + 1e-8);  // gae.cpp:91-96
+}
+void stats_finalize(const double* sums, double rows, int m, double* out, int mode, cudaStream_t s) {
+    k_stats_finalize<<<1, 32, 0, s>>>(sums, rows, m, out, mode);
+    MB_LAUNCH();
+}
+
+// scalarise (gae.cpp:98-115): s = sum_k w_k (A_k - mu_k) inv_k
+__global__ void k_scalarize(int N, int T, int m, const float* adv, const float* cw, int reps,
+                            const double* mean, const double* inv, float* out) {
+    const long r = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (r >= (long)N * T) return;
+    const int i = r / T, c = i / reps;
+    double s = 0.0;
+    for (int k = 0; k < m; ++k) s += (double)cw[c * m + k] * (((double)adv[r * m + k] - mean[k]) * inv[k]);
+    out[r] = (float)s;
+}
+void scalarize(int N, int T, int m, const float* adv, const float* cluster_w, int reps,
+               const double* mean, const double* inv_std, float* sadv, cudaStream_t s) {
+    const long R = (long)N * T;
+    k_scalarize<<<(int)((R + 255) / 256), 256, 0, s>>>(N, T, m, adv, cluster_w, reps, mean, inv_std, sadv);
+    MB_LAUNCH();
+}
+
+// =========================================================================
+// K5 pieces: minibatch gather and per-row loss heads (losses.cpp:87-129,
+// 170-185).
+// =========================================================================
+__global__ void k_gather(const int* rows, int B, const float* src, int width, float* dst) {
+    const long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (e >= (long)B * width) return;
+    const int q = e / width, j = e % width;
+    dst[e] = src[(long)rows[q] * width + j];
+}
+void gather_rows(const int* rows, int B, const float* src, int width, float* dst, cudaStream_t s) {
+    const long n = (long)B * width;
+    if (n == 0) return;
+    k_gather<<<(int)((n + 255) / 256), 256, 0, s>>>(rows, B, src, width, dst);
+    MB_LAUNCH();
+}
+
+__global__ void k_fill_row_group(const int* goff, int G, int* rg) {
+    const int g = blockIdx.x;
+    for (int q = goff[g] + threadIdx.x; q < goff[g + 1]; q += blockDim.x) rg[q] = g;
+}
+void fill_row_group(const int* goff, int G, int* row_group, int B, cudaStream_t s) {
+    (void)B;
+    k_fill_row_group<<<G, 256, 0, s>>>(goff, G, row_group);
+    MB_LAUNCH();
+}
+
+__global__ void k_actor_rows(int B, int ad, const int* rg, const float* theta, long P, long mlp_n,
+                             const float* mu, const float* z, const float* lp_old, const float* sadv,
+                             float clip, float ent, float inv_B, float* g_mu, float* lsg, double* loss_rows,
+                             int* err) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= B) return;
+    const float* th = theta + (long)rg[q] * P + mlp_n;
+    float lp = 0.f, ls[16], zn[16], sig[16];
+    float ent_h = 0.f;
+    for (int d = 0; d < ad; ++d) {  // action_logprob (nn.cpp:204-219) with the recomputed mean
+        const float raw = th[d];
+        ls[d] = fminf(fmaxf(raw, -5.f), 1.f);
+        sig[d] = __expf(ls[d]);
+        const float zz = z[(long)q * ad + d];
+        zn[d] = (zz - mu[(long)q * ad + d]) / sig[d];
+        lp += -0.5f * zn[d] * zn[d] - ls[d] - 0.9189385332046727f;
+        lp -= __logf(sech2_f(zz) + 1e-6f);
+        ent_h += ls[d] + 0.5f * (1.f + 1.8378770664093453f);  // gaussian_entropy
+    }
+    const float ratio = __expf(lp - lp_old[q]);
+    if (!isfinite(ratio)) atomicExch(err, 3);  // losses.cpp:103-105
+    const float adv = sadv[q];
+    const float unc = ratio * adv;
+    const float clp = fminf(fmaxf(ratio, 1.f - clip), 1.f + clip) * adv;
+    loss_rows[q] = (double)(-fminf(unc, clp) * inv_B) - (double)(ent * ent_h * inv_B);
+    const float glp = unc <= clp ? -ratio * adv * inv_B : 0.f;  // losses.cpp:116
+    for (int d = 0; d < ad; ++d) {
+        g_mu[(long)q * ad + d] = glp * zn[d] / sig[d];  // pre-activation gradient (no tanh')
+        const float raw = th[d];
+        lsg[(long)q * ad + d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - ent * inv_B : 0.f;
+    }
+}
+void actor_rows(int B, int ad, const int* row_group, const float* theta, long P, long mlp_n,
+                const float* mu, const float* z, const float* lp_old, const float* sadv, float clip,
+                float ent, float inv_B, float* g_mu, float* lsg, double* loss_rows, int* err,
+                cudaStream_t s) {
+    k_actor_rows<<<(B + 255) / 256, 256, 0, s>>>(B, ad, row_group, theta, P, mlp_n, mu, z, lp_old, sadv,
+                                                 clip, ent, inv_B, g_mu, lsg, loss_rows, err);
+    MB_LAUNCH();
+}
+
+__global__ void k_critic_rows(int B, int m, const float* v, const float* tgt, float inv_B, float* g,
+                              double* loss_rows) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= B) return;
+    double l = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const float e = v[(long)q * m + k] - tgt[(long)q * m + k];
+        l += (double)e * e * inv_B;
+        g[(long)q * m + k] = 2.f * e * inv_B;  // losses.cpp:179-181 (no 1/2)
+    }
+    loss_rows[q] = l;
+}
+void critic_rows(int B, int m, const float* v, const float* tgt, float inv_B, float* g_out,
+                 double* loss_rows, cudaStream_t s) {
+    k_critic_rows<<<(B + 255) / 256, 256, 0, s>>>(B, m, v, tgt, inv_B, g_out, loss_rows);
+    MB_LAUNCH();
+}
+
+// out[z][j] (+)= sum_{q in [goff[z], goff[z+1])} x[q][j]; one block per (z, 128-col tile)
+__global__ void k_segcolsum(const float* x, int width, const int* goff, float* out, long out_bz, int acc) {
+    const int z = blockIdx.y;
+    const int j = blockIdx.x * 128 + (threadIdx.x & 127);
+    const int half = threadIdx.x >> 7;  // 2 row-halves
+    __shared__ float red[256];
+    const int lo = goff[z], hi = goff[z + 1];
+    float s = 0.f;
+    if (j < width)
+        for (int q = lo + half; q < hi; q += 2) s += x[(long)q * width + j];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (half == 0 && j < width) {
+        const float v = red[threadIdx.x] + red[threadIdx.x + 128];
+        float* o = out + z * out_bz + j;
+        *o = acc ? *o + v : v;
+    }
+}
+void segmented_colsum(const float* x, int width, const int* goff, int G, float* out, long out_bz,
+                      int accumulate, cudaStream_t s) {
+    dim3 grid((width + 127) / 128, G);
+    k_segcolsum<<<grid, 256, 0, s>>>(x, width, goff, out, out_bz, accumulate);
+    MB_LAUNCH();
+}
+
+// out[j] = sum_r x[r][j]
+__global__ void k_colsum(const float* x, int rows, long width, float* out) {
+    const long j = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (j >= width) return;
+    float s = 0.f;
+    for (int r = 0; r < rows; ++r) s += x[r * width + j];
+    out[j] = s;
+}
+void colsum_rows(const float* x, int rows, long width, float* out, cudaStream_t s) {
+    k_colsum<<<(int)((width + 255) / 256), 256, 0, s>>>(x, rows, width, out);
+    MB_LAUNCH();
+}
+
+__global__ void k_sum_f64(const double* x, long n, double* out, int acc) {
+    __shared__ double red[1024];
+    double s = 0.0;
+    for (long i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = acc ? *out + red[0] : red[0];
+}
+void sum_f64(const double* x, long n, double* out, int accumulate, cudaStream_t s) {
+    k_sum_f64<<<1, 1024, 0, s>>>(x, n, out, accumulate);
+    MB_LAUNCH();
+}
+
+__global__ void k_check_finite(const double* x, int n, int* err, int code) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && !isfinite(x[i])) atomicExch(err, code);
+}
+void check_finite_f64(const double* x, int n, int* err, int code, cudaStream_t s) {
+    k_check_finite<<<(n + 255) / 256, 256, 0, s>>>(x, n, err, code);
+    MB_LAUNCH();
+}
+
+__global__ void k_reduce_splits(const float* parts, int S, long n, float* out) {
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float s = 0.f;
+    for (int k = 0; k < S; ++k) s += parts[k * n + i];
+    out[i] = s;
+}
+void reduce_splits(const float* parts, int S, long n, float* out, cudaStream_t s) {
+    k_reduce_splits<<<(int)((n + 255) / 256), 256, 0, s>>>(parts, S, n, out);
+    MB_LAUNCH();
+}
+
+__global__ void k_mul_dtanh(float* g, const float* a, long n) {
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i < n) g[i] *= 1.f - a[i] * a[i];
+}
+void mul_dtanh(float* g, const float* a, long n, cudaStream_t s) {
+    k_mul_dtanh<<<(int)((n + 255) / 256), 256, 0, s>>>(g, a, n);
+    MB_LAUNCH();
+}
+
+// =========================================================================
+// K7: Adam (adam.cpp:8-26), eps after sqrt(v_hat); bias corrections from
+// the host in fp64. Skipped entirely once a numeric error is flagged, so
+// the parameters stay at the last healthy state (train.cpp:197-206).
+// =========================================================================
+__global__ void k_adam(long n, float4* p, const float4* g, float4* m1, float4* m2, float lr, float ibc1,
+                       float ibc2, const int* err) {
+    if (*err) return;
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 pp = p[i], gg = g[i], a = m1[i], b = m2[i];
+    float* P = &pp.x;
+    const float* G = &gg.x;
+    float* A = &a.x;
+    float* Bv = &b.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        A[k] = 0.9f * A[k] + 0.1f * G[k];
+        Bv[k] = 0.999f * Bv[k] + 0.001f * G[k] * G[k];
+        P[k] -= lr * (A[k] * ibc1) / (sqrtf(Bv[k] * ibc2) + 1e-8f);
+    }
+    p[i] = pp;
+    m1[i] = a;
+    m2[i] = b;
+}
+__global__ void k_adam_tail(long lo, long n, float* p, const float* g, float* m1, float* m2, float lr,
+                            float ibc1, float ibc2, const int* err) {
+    if (*err) return;
+    const long i = lo + threadIdx.x;
+    if (i >= n) return;
+    m1[i] = 0.9f * m1[i] + 0.1f * g[i];
+    m2[i] = 0.999f * m2[i] + 0.001f * g[i] * g[i];
+    p[i] -= lr * (m1[i] * ibc1) / (sqrtf(m2[i] * ibc2) + 1e-8f);
+}
+void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2,
+          const int* err, cudaStream_t s) {
+    const long n4 = n / 4;
+    if (n4) {
+        k_adam<<<(int)((n4 + 255) / 256), 256, 0, s>>>(n4, (float4*)p, (const float4*)g, (float4*)m1,
+                                                      (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err);
+        MB_LAUNCH();
+    }
+    if (n4 * 4 < n) {
+        k_adam_tail<<<1, 32, 0, s>>>(n4 * 4, n, p, g, m1, m2, lr, 1.f / bc1, 1.f / bc2, err);
+        MB_LAUNCH();
+    }
+}
+
+// =========================================================================
+// RNG test kernels (rng.hpp words / Box-Muller on the device)
+// =========================================================================
+__global__ void k_rng_words(uint64_t key, uint64_t ctr, long n, uint64_t* out) {
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = rng_word(key, ctr + 1 + i);
+}
+__global__ void k_rng_gauss(uint64_t key, uint64_t ctr, long n, double* out) {
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = box_muller(rng_word(key, ctr + 2 * i + 1), rng_word(key, ctr + 2 * i + 2));
+}
+void rng_words(uint64_t key, uint64_t ctr, long n, uint64_t* out, cudaStream_t s) {
+    k_rng_words<<<(int)((n + 255) / 256), 256, 0, s>>>(key, ctr, n, out);
+    MB_LAUNCH();
+}
+void rng_gaussians(uint64_t key, uint64_t ctr, long n, double* out, cudaStream_t s) {
+    k_rng_gauss<<<(int)((n + 255) / 256), 256, 0, s>>>(key, ctr, n, out);
+    MB_LAUNCH();
+}
+
+}  // namespace mb200

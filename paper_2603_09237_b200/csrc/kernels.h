@@ -1,0 +1,119 @@
+// Host-side launch wrappers for every device kernel of the MORLAX B200 path.
+// All take an explicit stream; none synchronise.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mb200 {
+
+// ---------------------------------------------------------------- GEMM (SIMT)
+// C(m,n) [+]= sum_k A(m,k) B(k,n) with arbitrary strides, then epilogue.
+// gmode 0: batch over z (offsets a_bz/b_bz/c_bz/bias_bz per z)
+// gmode 1: M-grouped: for z, m in [goff[z], goff[z+1]) (absolute row index);
+//          B / bias offset z*b_bz / z*bias_bz
+// gmode 2: K-grouped: for z, k in [goff[z], goff[z+1]); C offset z*c_bz
+struct GemmDesc {
+    const float* A = nullptr; long am = 0, ak = 0, a_bz = 0;
+    const float* B = nullptr; long bk = 0, bn = 0, b_bz = 0;
+    float* C = nullptr; long cm = 0, cn = 0, c_bz = 0;
+    int M = 0, N = 0, K = 0, Z = 1;
+    const int* goff = nullptr;
+    int gmode = 0;
+    int max_group = 0;            // host-known max group extent (gmode 1)
+    const float* bias = nullptr;  // bias_mode 1: bias[n], 2: bias[m]
+    long bias_bz = 0;
+    int bias_mode = 0;
+    int act = 0;                  // 0 none, 1 tanh (C2 <- preact), 2 C *= (1 - aux^2)
+    const float* aux = nullptr; long xm = 0, xn = 0;
+    float* C2 = nullptr; long c2m = 0, c2n = 0;
+    int accumulate = 0;
+};
+void gemm_simt(const GemmDesc& d, cudaStream_t s);
+
+// ---------------------------------------------------------------- tcgen05 GEMM
+// bf16 operands, fp32 accumulate in TMEM. D(m,n) = sum_k A(m,k) B(n,k) with
+// A: [M][K] K-major (lda), B: [N][K] K-major (ldb). Output fp32 (ldc) with
+// optional per-m bias. Returns false if the shape is unsupported.
+bool tc_gemm_supported(int M, int N, int K);
+void tc_gemm_bf16(const __nv_bfloat16* A, long lda, const __nv_bfloat16* B, long ldb, float* C,
+                  long ldc_m, long ldc_n, int M, int N, int K, const float* bias, cudaStream_t s);
+
+// ---------------------------------------------------------------- env (K1)
+void env_reset(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,
+               uint64_t parent_key, int inst_base, cudaStream_t s);
+void env_step(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,
+              const float* actions, float* obs, float* reward, uint8_t* term, uint8_t* trunc,
+              unsigned long long* clamp_count, int* err, cudaStream_t s);
+void env_obs(int kind, int N, const float* state, float* obs, cudaStream_t s);
+
+// ---------------------------------------------------------------- rollout (K3+K1)
+struct NetDims {
+    int L;             // layers
+    int sz[9];         // sizes[0..L]
+    long woff[8], boff[8];
+    long mlp_n, P;
+    int out_tanh, has_log_std;
+};
+struct RolloutArgs {
+    int kind, N, T, K, reps, od, ad, m, sdim, max_steps;
+    const float* theta;  // [K][Pa]
+    const float* phi;    // [K][Pc]
+    NetDims pol, cri;
+    float* state; uint64_t* env_key; uint64_t* env_ctr; int* steps;
+    uint64_t roll_key;
+    int roll_inst_base;  // global instance index of local instance 0 (sharding)
+    float *obs, *act_pre, *logprob, *reward, *value, *next_value;
+    uint8_t *term, *trunc;
+    float* tracker;      // [N][m]
+    const float* cluster_w;  // [K][m]
+    double* ret_sum; int* ret_cnt;  // [N] completed scalarised returns
+    unsigned long long* clamp_count; int* err;
+};
+void rollout(const RolloutArgs& a, cudaStream_t s);
+int rollout_rows_per_cta();
+
+// ---------------------------------------------------------------- GAE + normalise (K4)
+void gae_scan(int N, int T, int m, const float* reward, const float* value, const float* next_value,
+              const uint8_t* term, const uint8_t* trunc, float gamma, float lambda, float* adv,
+              float* targets, cudaStream_t s);
+// partial sums: out[m] (fp64) of x[r*m+k] (pass 1) or (x - mean)^2 (pass 2)
+void channel_sums(const float* x, long rows, int m, const double* mean, double* out,
+                  double* scratch, cudaStream_t s);
+// mean[k] = sums[k] / rows (mode 0); inv[k] = 1/(sqrt(sums[k]/rows) + 1e-8) (mode 1)
+void stats_finalize(const double* sums, double rows, int m, double* out, int mode, cudaStream_t s);
+void scalarize(int N, int T, int m, const float* adv, const float* cluster_w, int reps,
+               const double* mean, const double* inv_std, float* sadv, cudaStream_t s);
+
+// ---------------------------------------------------------------- PPO (K5)
+void gather_rows(const int* rows, int B, const float* src, int width, float* dst, cudaStream_t s);
+void actor_rows(int B, int ad, const int* row_group, const float* theta, long P, long mlp_n,
+                const float* mu, const float* z, const float* lp_old, const float* sadv,
+                float clip, float ent, float inv_B, float* g_mu, float* lsg, double* loss_rows,
+                int* err, cudaStream_t s);
+void critic_rows(int B, int m, const float* v, const float* tgt, float inv_B, float* g_out,
+                 double* loss_rows, cudaStream_t s);
+// out[z*out_bz + j] (+)= sum_{rows in group z} x[row*width + j]
+void segmented_colsum(const float* x, int width, const int* goff, int G, float* out, long out_bz,
+                      int accumulate, cudaStream_t s);
+void colsum_rows(const float* x, int rows, long width, float* out, cudaStream_t s);
+void sum_f64(const double* x, long n, double* out, int accumulate, cudaStream_t s);
+void fill_row_group(const int* goff, int G, int* row_group, int B, cudaStream_t s);
+void check_finite_f64(const double* x, int n, int* err, int code, cudaStream_t s);
+void reduce_splits(const float* parts, int S, long n, float* out, cudaStream_t s);
+void mul_dtanh(float* g, const float* a, long n, cudaStream_t s);
+
+// ---------------------------------------------------------------- Adam (K7)
+void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2,
+          const int* err, cudaStream_t s);
+
+// ---------------------------------------------------------------- Pareto (K8/K9)
+void pareto_mask(int n, int m, const double* pts, uint8_t* mask, uint8_t* uniq, double* sums,
+                 cudaStream_t s);
+void hv_mc(int n, int m, const double* pts, const double* ref, uint64_t samples, uint64_t key,
+           uint64_t ctr, unsigned long long* hits, double* hi_out, cudaStream_t s);
+void rng_words(uint64_t key, uint64_t ctr, long n, uint64_t* out, cudaStream_t s);
+void rng_gaussians(uint64_t key, uint64_t ctr, long n, double* out, cudaStream_t s);
+
+}  // namespace mb200

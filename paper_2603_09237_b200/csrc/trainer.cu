@@ -1,0 +1,778 @@
+// Host orchestration of one MORLAX training iteration on the GPU
+// (reference src/train.cpp:118-184): preference sampling -> hypernet
+// generation -> fused rollout -> GAE / normalise / scalarise -> epochs x
+// minibatches of {actor loss, critic loss through the hypernetwork, Adam}.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "comm.h"
+#include "trainer.h"
+
+namespace mb200 {
+
+// ------------------------------------------------------------------ helpers
+template <typename T>
+static T* dalloc(size_t n) {
+    T* p = nullptr;
+    if (n == 0) n = 1;
+    MB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    MB_CUDA(cudaMemset(p, 0, n * sizeof(T)));
+    return p;
+}
+template <typename T>
+static void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+NetDims make_dims(const std::vector<int>& s, bool out_tanh, bool has_log_std) {
+    NetDims d{};
+    d.L = (int)s.size() - 1;
+    if (d.L < 1 || d.L > 8) throw ShapeError("MlpSpec needs at least input and output sizes");
+    long off = 0;
+    for (int l = 0; l <= d.L; ++l) d.sz[l] = s[l];
+    for (int l = 0; l < d.L; ++l) {  // nn.cpp:38-58 flat layout: W (out x in) then b
+        d.woff[l] = off;
+        d.boff[l] = off + (long)s[l] * s[l + 1];
+        off += (long)(s[l] + 1) * s[l + 1];
+    }
+    d.mlp_n = off;
+    d.P = off + (has_log_std ? s[d.L] : 0);
+    d.out_tanh = out_tanh;
+    d.has_log_std = has_log_std;
+    return d;
+}
+
+void TrainConfig::validate(int m) const {  // config.cpp:17-45, simplex.cpp:44-53
+    if (N < 1) throw ConfigError("trainer.N must be >= 1");
+    if (T < 1) throw ConfigError("trainer.T must be >= 1");
+    if (!(gamma >= 0.0 && gamma < 1.0)) throw ConfigError("trainer.gamma must lie in [0, 1)");
+    if (!(lambda >= 0.0 && lambda <= 1.0)) throw ConfigError("trainer.gae_lambda must lie in [0, 1]");
+    if (!(clip_eps > 0.0)) throw ConfigError("trainer.clip_eps must be > 0");
+    if (epochs < 1) throw ConfigError("trainer.epochs must be >= 1");
+    if (minibatch_count < 1) throw ConfigError("trainer.minibatch_count must be >= 1");
+    if (!(actor_lr > 0.0)) throw ConfigError("trainer.actor_lr must be > 0");
+    if (!(critic_lr > 0.0)) throw ConfigError("trainer.critic_lr must be > 0");
+    if (entropy_coef < 0.0) throw ConfigError("trainer.entropy_coef must be >= 0");
+    if (F < 1) throw ConfigError("hypernet.F must be >= 1");
+    for (int h : feat_hidden)
+        if (h < 1) throw ConfigError("hypernet.feature_hidden sizes must be >= 1");
+    for (int h : actor_hidden)
+        if (h < 1) throw ConfigError("hypernet.actor_hidden sizes must be >= 1");
+    for (int h : critic_hidden)
+        if (h < 1) throw ConfigError("hypernet.critic_hidden sizes must be >= 1");
+    if (m == 1) {
+        if (K != N) throw ConfigError("trainer.K must equal trainer.N when the environment has one objective");
+        return;
+    }
+    if (K <= 1) throw ConfigError("K must be > 1");
+    if (N % K != 0)
+        throw ConfigError("K must divide N (got K=" + std::to_string(K) + ", N=" + std::to_string(N) + ")");
+    if (kappa < 0 || kappa > K) throw ConfigError("kappa must be in [0, K]");
+    if (kappa > m) throw ConfigError("kappa must be <= m");
+}
+
+// ------------------------------------------------------------------ init kernels
+// init_mlp_params (nn.cpp:260-274): one stream, entry e uses word e+1,
+// U(-1/sqrt(fan_in), +1/sqrt(fan_in)) for weights and biases alike.
+struct InitLayers {
+    int L;
+    long end[9];
+    double bound[9];
+};
+__global__ void k_init_mlp(float* out, long n, uint64_t key, InitLayers il, long fill_from, float fill) {
+    const long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    if (e >= fill_from) {
+        out[e] = fill;  // policy log-std slots (hypernet.cpp:140-142)
+        return;
+    }
+    int l = 0;
+    while (l < il.L - 1 && e >= il.end[l]) ++l;
+    const double b = il.bound[l];
+    out[e] = (float)uniform_rn(-b, b, rng_word(key, (uint64_t)e + 1));
+}
+// M ~ N(0, (0.01/sqrt(F))^2): entry i consumes words 2i+1, 2i+2 (Box-Muller)
+__global__ void k_init_gauss(float* out, long n, uint64_t key, double sd) {
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = (float)__dmul_rn(sd, box_muller(rng_word(key, 2 * (uint64_t)i + 1), rng_word(key, 2 * (uint64_t)i + 2)));
+}
+static InitLayers init_layers(const std::vector<int>& s) {
+    InitLayers il{};
+    il.L = (int)s.size() - 1;
+    long off = 0;
+    for (int l = 0; l < il.L; ++l) {
+        off += (long)(s[l] + 1) * s[l + 1];
+        il.end[l] = off;
+        il.bound[l] = 1.0 / std::sqrt((double)s[l]);
+    }
+    return il;
+}
+
+// ------------------------------------------------------------------ profiler
+int Profiler::begin(const char* name, double flops, double bytes, cudaStream_t s) {
+    if (!on) return -1;
+    int c = -1;
+    for (size_t i = 0; i < cls.size(); ++i)
+        if (cls[i].name == name) c = (int)i;
+    if (c < 0) {
+        cls.push_back(Cls{name});
+        c = (int)cls.size() - 1;
+    }
+    cls[c].flops += flops;
+    cls[c].bytes += bytes;
+    cls[c].count += 1;
+    while (pool.size() < used + 2) {
+        cudaEvent_t e;
+        MB_CUDA(cudaEventCreate(&e));
+        pool.push_back(e);
+    }
+    Pending p{c, pool[used], pool[used + 1]};
+    used += 2;
+    MB_CUDA(cudaEventRecord(p.a, s));
+    pending.push_back(p);
+    return (int)pending.size() - 1;
+}
+void Profiler::end(int h, cudaStream_t s) {
+    if (h >= 0) MB_CUDA(cudaEventRecord(pending[h].b, s));
+}
+void Profiler::collect() {
+    for (auto& p : pending) {
+        MB_CUDA(cudaEventSynchronize(p.b));
+        float ms = 0;
+        MB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        cls[p.c].ms += ms;
+    }
+    pending.clear();
+    used = 0;
+}
+void Profiler::reset() {
+    pending.clear();
+    used = 0;
+    cls.clear();
+}
+Profiler::~Profiler() {
+    for (auto e : pool) cudaEventDestroy(e);
+}
+static Profiler* g_prof = nullptr;  // the active trainer's profiler (launch sites below)
+struct ProfScope {
+    int h;
+    cudaStream_t s;
+    ProfScope(const char* n, double f, double b, cudaStream_t s_) : s(s_) {
+        h = g_prof ? g_prof->begin(n, f, b, s_) : -1;
+    }
+    ~ProfScope() {
+        if (g_prof) g_prof->end(h, s);
+    }
+};
+static double gemm_flops(const GemmDesc& d) {
+    if (d.gmode == 1) return 2.0 * d.M * d.N * d.K;        // M = total grouped rows
+    if (d.gmode == 2) return 2.0 * d.M * d.N * d.K;        // K = total grouped rows
+    return 2.0 * d.M * d.N * d.K * d.Z;
+}
+static void gemm(const char* cls, const GemmDesc& d, cudaStream_t s) {
+    ProfScope p(cls, gemm_flops(d), 0, s);
+    gemm_simt(d, s);
+}
+
+// ------------------------------------------------------------------ HyperNet
+void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vector<int>& ts, bool out_tanh,
+                    bool has_log_std, int G_) {
+    m = m_;
+    F = F_;
+    G = G_;
+    fsz.clear();
+    fsz.push_back(m);
+    for (int h : fh) fsz.push_back(h);
+    fsz.push_back(F);
+    nf = 0;
+    fwoff.clear();
+    fboff.clear();
+    for (size_t l = 0; l + 1 < fsz.size(); ++l) {
+        fwoff.push_back(nf);
+        fboff.push_back(nf + (long)fsz[l] * fsz[l + 1]);
+        nf += (long)(fsz[l] + 1) * fsz[l + 1];
+    }
+    tgt = make_dims(ts, out_tanh, has_log_std);
+    P = tgt.P;
+    n = nf + P * F + P;
+    p = dalloc<float>(n);
+    g = dalloc<float>(n);
+    m1 = dalloc<float>(n);
+    m2 = dalloc<float>(n);
+    fact.assign(fsz.size(), nullptr);
+    int maxw = 0;
+    for (size_t l = 0; l < fsz.size(); ++l) {
+        fact[l] = dalloc<float>((size_t)G * fsz[l]);
+        maxw = std::max(maxw, fsz[l]);
+    }
+    fg0 = dalloc<float>((size_t)G * maxw);
+    fg1 = dalloc<float>((size_t)G * maxw);
+    theta = dalloc<float>((size_t)G * P);
+    gtheta = dalloc<float>((size_t)G * P);
+    gf = dalloc<float>((size_t)G * F);
+    splits = (int)std::min<long>(64, std::max<long>(1, P / 1024));
+    parts = dalloc<float>((size_t)splits * G * F);
+    std::vector<int> bounds(splits + 1);
+    for (int z = 0; z <= splits; ++z) bounds[z] = (int)(P * z / splits);
+    d_split_bounds = dalloc<int>(splits + 1);
+    MB_CUDA(cudaMemcpy(d_split_bounds, bounds.data(), sizeof(int) * (splits + 1), cudaMemcpyHostToDevice));
+}
+
+void HyperNet::free_all() {
+    dfree(p); dfree(g); dfree(m1); dfree(m2);
+    for (auto& a : fact) dfree(a);
+    dfree(fg0); dfree(fg1); dfree(theta); dfree(gtheta); dfree(gf); dfree(parts); dfree(d_split_bounds);
+}
+
+void HyperNet::init_params(uint64_t key, cudaStream_t s) {  // hypernet.cpp:124-145
+    const uint64_t kf = split_key(key, 0), km = split_key(key, 1), kb = split_key(key, 2);
+    InitLayers fl = init_layers(fsz);
+    k_init_mlp<<<(int)((nf + 255) / 256), 256, 0, s>>>(p, nf, kf, fl, nf, 0.f);
+    MB_LAUNCH();
+    const long nM = P * F;
+    k_init_gauss<<<(int)((nM + 255) / 256), 256, 0, s>>>(p + nf, nM, km, 0.01 / std::sqrt((double)F));
+    MB_LAUNCH();
+    std::vector<int> ts(tgt.sz, tgt.sz + tgt.L + 1);
+    InitLayers tl = init_layers(ts);
+    k_init_mlp<<<(int)((P + 255) / 256), 256, 0, s>>>(p + nf + nM, P, kb, tl, tgt.mlp_n, -1.f);
+    MB_LAUNCH();
+    MB_CUDA(cudaMemsetAsync(m1, 0, n * sizeof(float), s));
+    MB_CUDA(cudaMemsetAsync(m2, 0, n * sizeof(float), s));
+    steps[0] = steps[1] = steps[2] = 0;
+}
+
+// feature map for all G groups, theta for groups [g0, g0+ng)
+void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
+    MB_CUDA(cudaMemcpyAsync(fact[0], w, sizeof(float) * G * m, cudaMemcpyDeviceToDevice, s));
+    const int Lf = (int)fsz.size() - 1;
+    for (int l = 0; l < Lf; ++l) {  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
+        GemmDesc d;
+        d.A = fact[l]; d.am = fsz[l]; d.ak = 1;
+        d.B = p + fwoff[l]; d.bk = 1; d.bn = fsz[l];
+        d.C = fact[l + 1]; d.cm = fsz[l + 1]; d.cn = 1;
+        d.M = G; d.N = fsz[l + 1]; d.K = fsz[l];
+        d.bias = p + fboff[l]; d.bias_mode = 1;
+        d.act = 1;
+        gemm("feature_fwd", d, s);
+    }
+    GemmDesc d;  // theta[g][p] = b[p] + sum_k M[p][k] f[g][k]  (hypernet.cpp:73-88)
+    d.A = fact[Lf] + (long)g0 * F; d.am = F; d.ak = 1;
+    d.B = p + nf; d.bk = 1; d.bn = F;
+    d.C = theta + (long)g0 * P; d.cm = P; d.cn = 1;
+    d.M = ng; d.N = (int)P; d.K = F;
+    d.bias = p + nf + P * F; d.bias_mode = 1;
+    gemm("hyper_theta", d, s);
+}
+
+// hypernet_backward (hypernet.cpp:92-122) summed over all groups:
+// db = sum_g gtheta_g, dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then
+// the feature-map backward. Writes (not accumulates) the flat grad g.
+void HyperNet::backward(cudaStream_t s) {
+    const long nM = P * F;
+    colsum_rows(gtheta, G, P, g + nf + nM, s);
+    const int Lf = (int)fsz.size() - 1;
+    {
+        GemmDesc d;  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
+        d.A = gtheta; d.am = 1; d.ak = P;
+        d.B = fact[Lf]; d.bk = F; d.bn = 1;
+        d.C = g + nf; d.cm = F; d.cn = 1;
+        d.M = (int)P; d.N = F; d.K = G;
+        gemm("hyper_dM", d, s);
+    }
+    {
+        // gf[g][k] = sum_p gtheta[g][p] M[p][k]: K = P is long -> split-K
+        GemmDesc d;
+        d.A = gtheta; d.am = P; d.ak = 1;
+        d.B = p + nf; d.bk = F; d.bn = 1;
+        d.C = parts; d.cm = F; d.cn = 1; d.c_bz = (long)G * F;
+        d.M = G; d.N = F; d.K = (int)P; d.Z = splits;
+        d.gmode = 2; d.goff = d_split_bounds;
+        gemm("hyper_df", d, s);
+        reduce_splits(parts, splits, (long)G * F, gf, s);
+    }
+    // feature backward: output tanh -> g *= 1 - f^2
+    MB_CUDA(cudaMemcpyAsync(fg0, gf, sizeof(float) * G * F, cudaMemcpyDeviceToDevice, s));
+    mul_dtanh(fg0, fact[Lf], (long)G * F, s);
+    float* cur = fg0;
+    float* nxt = fg1;
+    for (int l = Lf - 1; l >= 0; --l) {
+        const int in = fsz[l], out = fsz[l + 1];
+        GemmDesc d;  // dW[j][i] = sum_g gz[g][j] a_l[g][i]
+        d.A = cur; d.am = 1; d.ak = out;
+        d.B = fact[l]; d.bk = in; d.bn = 1;
+        d.C = g + fwoff[l]; d.cm = in; d.cn = 1;
+        d.M = out; d.N = in; d.K = G;
+        gemm("feature_bwd", d, s);
+        colsum_rows(cur, G, out, g + fboff[l], s);
+        if (l > 0) {
+            GemmDesc e;  // g_prev[g][i] = (sum_j gz[g][j] W[j][i]) (1 - a_l^2)
+            e.A = cur; e.am = out; e.ak = 1;
+            e.B = p + fwoff[l]; e.bk = in; e.bn = 1;
+            e.C = nxt; e.cm = in; e.cn = 1;
+            e.M = G; e.N = in; e.K = out;
+            e.act = 2; e.aux = fact[l]; e.xm = in; e.xn = 1;
+            gemm("feature_bwd", e, s);
+            std::swap(cur, nxt);
+        }
+    }
+}
+
+void HyperNet::adam_step(double lr, const int* err, cudaStream_t s) {
+    // three blocks (feature, M, b) with their own step counters (train.cpp:28-39);
+    // they always advance together, so one launch covers the flat vector.
+    for (long& st : steps) ++st;
+    const double bc1 = 1.0 - std::pow(0.9, (double)steps[0]);
+    const double bc2 = 1.0 - std::pow(0.999, (double)steps[0]);
+    ProfScope ps("adam", 0, 28.0 * n, s);  // read p,g,m1,m2 + write p,m1,m2 (fp32)
+    adam(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, s);
+}
+
+// ------------------------------------------------------------------ sharding
+void shard_minibatch(const int* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps, int n_groups,
+                     int* rows_out, int* goff_out, int* n_rows_out, int* max_group) {
+    // stable counting sort by (local) cluster id; rows keep minibatch order
+    std::vector<int> cnt(n_groups + 1, 0);
+    for (int q = lo; q < hi; ++q) {
+        const int i = perm[q] / T - inst_lo;
+        if (i < 0 || i >= n_inst) continue;
+        cnt[i / reps + 1]++;
+    }
+    int mx = 0;
+    for (int c = 0; c < n_groups; ++c) {
+        mx = std::max(mx, cnt[c + 1]);
+        cnt[c + 1] += cnt[c];
+    }
+    for (int c = 0; c <= n_groups; ++c) goff_out[c] = cnt[c];
+    std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+    for (int q = lo; q < hi; ++q) {
+        const int r = perm[q];
+        const int i = r / T - inst_lo;
+        if (i < 0 || i >= n_inst) continue;
+        rows_out[pos[i / reps]++] = r - inst_lo * T;
+    }
+    *n_rows_out = cnt[n_groups];
+    *max_group = mx;
+}
+
+// ------------------------------------------------------------------ Trainer
+Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_id)
+    : cfg_(cfg), world_(world), rank_(rank) {
+    es_ = env_spec_of(cfg.env_kind);
+    cfg_.validate(es_.m);
+    if (es_.obs_dim > 64 || es_.act_dim > 16 || es_.m > 8)
+        throw ShapeError("env dims exceed the device bounds (obs 64, act 16, m 8)");
+    for (int h : cfg.actor_hidden)
+        if (h > 256) throw ShapeError("hidden widths above 256 are not supported on the device path");
+    for (int h : cfg.critic_hidden)
+        if (h > 256) throw ShapeError("hidden widths above 256 are not supported on the device path");
+    if (world < 1 || rank < 0 || rank >= world) throw ConfigError("bad world/rank");
+    if (cfg.K % world != 0) throw ConfigError("K must be divisible by the number of GPUs");
+    Kl_ = cfg.K / world;
+    reps_ = cfg.N / cfg.K;
+    Nl_ = Kl_ * reps_;
+    inst_lo_ = rank * Nl_;
+    g_lo_ = rank * Kl_;
+    Rl_ = (long)Nl_ * cfg.T;
+    MB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    if (world > 1) comm_ = comm_create(world, rank, nccl_id);
+    root_ = HostRng::seeded(cfg.seed);
+    std::vector<int> as{es_.obs_dim}, cs{es_.obs_dim};
+    for (int h : cfg.actor_hidden) as.push_back(h);
+    as.push_back(es_.act_dim);
+    for (int h : cfg.critic_hidden) cs.push_back(h);
+    cs.push_back(es_.m);
+    actor_.init(es_.m, cfg.F, cfg.feat_hidden, as, true, true, cfg.K);    // config.cpp:59-70
+    critic_.init(es_.m, cfg.F, cfg.feat_hidden, cs, false, false, cfg.K); // config.cpp:72-83
+    actor_.init_params(root_.split(0xA1).key, s_);                        // train.cpp:67-70
+    critic_.init_params(root_.split(0xA2).key, s_);
+    alloc();
+    env_reset(es_.kind, Nl_, d_state, d_ekey, d_ectr, d_steps, root_.split(0xE0).key, inst_lo_, s_);
+    perm_.resize((size_t)cfg.N * cfg.T);
+    std::iota(perm_.begin(), perm_.end(), 0);  // train.cpp:112-114
+    MB_CUDA(cudaStreamSynchronize(s_));
+}
+
+Trainer::~Trainer() {
+    if (g_prof == &prof_) g_prof = nullptr;
+    actor_.free_all();
+    critic_.free_all();
+    for (auto* p : {d_obs, d_act, d_lp, d_rew, d_val, d_nval, d_adv, d_tgt, d_sadv, d_state, d_tracker, d_cw,
+                    d_X, d_Z, d_lpo, d_sa, d_tg, d_lsg})
+        if (p) cudaFree(p);
+    for (auto* p : d_A) cudaFree(p);
+    for (auto* p : d_Gz) cudaFree(p);
+    for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
+                    (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_rowgroup, (void*)d_lossrows,
+                    (void*)d_mbloss, (void*)d_stats, (void*)d_scratch, (void*)d_retsum, (void*)d_retcnt})
+        if (p) cudaFree(p);
+    if (h_cw_pinned) cudaFreeHost(h_cw_pinned);
+    if (h_rows_pinned) cudaFreeHost(h_rows_pinned);
+    if (h_goff_pinned) cudaFreeHost(h_goff_pinned);
+    if (comm_) comm_destroy(comm_);
+    if (s_) cudaStreamDestroy(s_);
+}
+
+void Trainer::alloc() {
+    const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
+    d_obs = dalloc<float>(Rl_ * od);
+    d_act = dalloc<float>(Rl_ * ad);
+    d_lp = dalloc<float>(Rl_);
+    d_rew = dalloc<float>(Rl_ * m);
+    d_val = dalloc<float>(Rl_ * m);
+    d_nval = dalloc<float>(Rl_ * m);
+    d_adv = dalloc<float>(Rl_ * m);
+    d_tgt = dalloc<float>(Rl_ * m);
+    d_sadv = dalloc<float>(Rl_);
+    d_term = dalloc<uint8_t>(Rl_);
+    d_trunc = dalloc<uint8_t>(Rl_);
+    d_state = dalloc<float>((size_t)es_.state_dim * Nl_);
+    d_ekey = dalloc<uint64_t>(Nl_);
+    d_ectr = dalloc<uint64_t>(Nl_);
+    d_steps = dalloc<int>(Nl_);
+    d_tracker = dalloc<float>((size_t)Nl_ * m);
+    d_err = dalloc<int>(1);
+    d_clamps = dalloc<unsigned long long>(1);
+    d_cw = dalloc<float>((size_t)cfg_.K * m);
+    MB_CUDA(cudaMallocHost(&h_cw_pinned, sizeof(float) * cfg_.K * m));
+    const long R = (long)cfg_.N * cfg_.T;
+    Bmax_ = (int)((R + cfg_.minibatch_count - 1) / cfg_.minibatch_count);
+    const int slots = cfg_.epochs * cfg_.minibatch_count;
+    MB_CUDA(cudaMallocHost(&h_rows_pinned, sizeof(int) * (size_t)slots * Bmax_));
+    MB_CUDA(cudaMallocHost(&h_goff_pinned, sizeof(int) * (size_t)slots * (Kl_ + 1)));
+    d_rows = dalloc<int>((size_t)slots * Bmax_);
+    d_goff = dalloc<int>((size_t)slots * (Kl_ + 1));
+    d_rowgroup = dalloc<int>(Bmax_);
+    d_X = dalloc<float>((size_t)Bmax_ * od);
+    d_Z = dalloc<float>((size_t)Bmax_ * ad);
+    d_lpo = dalloc<float>(Bmax_);
+    d_sa = dalloc<float>(Bmax_);
+    d_tg = dalloc<float>((size_t)Bmax_ * m);
+    d_lsg = dalloc<float>((size_t)Bmax_ * ad);
+    int maxw = 0;
+    for (int l = 1; l <= actor_.tgt.L; ++l) maxw = std::max(maxw, actor_.tgt.sz[l]);
+    for (int l = 1; l <= critic_.tgt.L; ++l) maxw = std::max(maxw, critic_.tgt.sz[l]);
+    const int L = std::max(actor_.tgt.L, critic_.tgt.L);
+    for (int l = 0; l < L; ++l) {
+        d_A.push_back(dalloc<float>((size_t)Bmax_ * maxw));
+        d_Gz.push_back(dalloc<float>((size_t)Bmax_ * maxw));
+    }
+    d_lossrows = dalloc<double>(Bmax_);
+    d_mbloss = dalloc<double>((size_t)slots * 2 + 2);
+    d_stats = dalloc<double>(4 * 8);
+    d_scratch = dalloc<double>(148 * 2 * 8);
+    d_retsum = dalloc<double>(Nl_);
+    d_retcnt = dalloc<int>(Nl_);
+    mb_B_.assign(slots, 0);
+    mb_Bglob_.assign(slots, 0);
+    mb_maxg_.assign(slots, 0);
+}
+
+void Trainer::phase_rollout(int it) {
+    g_prof = &prof_;
+    const int m = es_.m, K = cfg_.K;
+    const HostRng iter = root_.split(0x10000000ULL + (uint64_t)it);  // train.cpp:120
+    cw_h_.assign((size_t)K * m, 0.f);
+    if (m == 1) {
+        for (int k = 0; k < K; ++k) cw_h_[k] = 1.f;
+    } else {  // build_tradeoff_batch (simplex.cpp:55-87): K-kappa Dirichlet draws + vertices
+        HostRng sr = iter.split(0);
+        const int nd = K - cfg_.kappa;
+        std::vector<double> w(m);
+        for (int k = 0; k < nd; ++k) {
+            double sum = 0.0;
+            for (int j = 0; j < m; ++j) {
+                w[j] = -std::log(sr.next_open());
+                sum += w[j];
+            }
+            for (int j = 0; j < m; ++j) cw_h_[(size_t)k * m + j] = (float)(w[j] / sum);
+        }
+        for (int k = 0; k < cfg_.kappa; ++k) cw_h_[(size_t)(nd + k) * m + k] = 1.f;
+    }
+    std::memcpy(h_cw_pinned, cw_h_.data(), sizeof(float) * K * m);
+    MB_CUDA(cudaMemcpyAsync(d_cw, h_cw_pinned, sizeof(float) * K * m, cudaMemcpyHostToDevice, s_));
+    MB_CUDA(cudaMemsetAsync(d_retsum, 0, sizeof(double) * Nl_, s_));
+    MB_CUDA(cudaMemsetAsync(d_retcnt, 0, sizeof(int) * Nl_, s_));
+    MB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s_));
+    actor_.forward(d_cw, g_lo_, Kl_, s_);
+    critic_.forward(d_cw, g_lo_, Kl_, s_);
+    RolloutArgs a{};
+    a.kind = es_.kind; a.N = Nl_; a.T = cfg_.T; a.K = Kl_; a.reps = reps_;
+    a.od = es_.obs_dim; a.ad = es_.act_dim; a.m = m; a.sdim = es_.state_dim; a.max_steps = es_.max_steps;
+    a.theta = actor_.theta + (long)g_lo_ * actor_.P;
+    a.phi = critic_.theta + (long)g_lo_ * critic_.P;
+    a.pol = actor_.tgt; a.cri = critic_.tgt;
+    a.state = d_state; a.env_key = d_ekey; a.env_ctr = d_ectr; a.steps = d_steps;
+    a.roll_key = iter.split(1).key;  // train.cpp:146
+    a.roll_inst_base = inst_lo_;
+    a.obs = d_obs; a.act_pre = d_act; a.logprob = d_lp; a.reward = d_rew; a.value = d_val; a.next_value = d_nval;
+    a.term = d_term; a.trunc = d_trunc; a.tracker = d_tracker;
+    a.cluster_w = d_cw + (size_t)g_lo_ * m;
+    a.ret_sum = d_retsum; a.ret_cnt = d_retcnt;
+    a.clamp_count = d_clamps; a.err = d_err;
+    {
+        // algorithmic work per env-step: policy MLP + ONE critic MLP (the
+        // reference's second critic call per step is reused)
+        double macs = 0;
+        for (int l = 0; l < a.pol.L; ++l) macs += (double)a.pol.sz[l] * a.pol.sz[l + 1];
+        for (int l = 0; l < a.cri.L; ++l) macs += (double)a.cri.sz[l] * a.cri.sz[l + 1];
+        ProfScope ps("rollout", 2.0 * macs * Rl_, 0, s_);
+        rollout(a, s_);
+    }
+    launches_ += 1;
+    prepare_perms(it);  // host work overlaps the rollout on the GPU
+}
+
+void Trainer::prepare_perms(int it) {
+    const HostRng iter = root_.split(0x10000000ULL + (uint64_t)it);
+    HostRng sh = iter.split(2);  // train.cpp:156
+    const long R = (long)cfg_.N * cfg_.T;
+    const int mbs = cfg_.minibatch_count;
+    for (int e = 0; e < cfg_.epochs; ++e) {
+        for (long i = R; i > 1; --i) {  // rng.hpp:71-76 Fisher-Yates
+            const long j = (long)sh.next_below((uint64_t)i);
+            std::swap(perm_[i - 1], perm_[j]);
+        }
+        for (int s = 0; s < mbs; ++s) {
+            const int slot = e * mbs + s;
+            const int lo = (int)(R * s / mbs), hi = (int)(R * (s + 1) / mbs);  // train.cpp:163-169
+            int nrows = 0, mx = 0;
+            shard_minibatch(perm_.data(), lo, hi, cfg_.T, inst_lo_, Nl_, reps_, Kl_,
+                            h_rows_pinned + (size_t)slot * Bmax_, h_goff_pinned + (size_t)slot * (Kl_ + 1),
+                            &nrows, &mx);
+            mb_B_[slot] = nrows;
+            mb_Bglob_[slot] = hi - lo;
+            mb_maxg_[slot] = mx;
+        }
+    }
+    const int slots = cfg_.epochs * mbs;
+    MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (size_t)slots * Bmax_, cudaMemcpyHostToDevice, s_));
+    MB_CUDA(cudaMemcpyAsync(d_goff, h_goff_pinned, sizeof(int) * (size_t)slots * (Kl_ + 1), cudaMemcpyHostToDevice,
+                            s_));
+}
+
+void Trainer::phase_advantages() {
+    g_prof = &prof_;
+    const int m = es_.m;
+    {
+        ProfScope ps("gae", 0, (double)Rl_ * (5.0 * m * 4 + 2), s_);  // r,V,V' in; A,target out; flags
+        gae_scan(Nl_, cfg_.T, m, d_rew, d_val, d_nval, d_term, d_trunc, (float)cfg_.gamma, (float)cfg_.lambda,
+                 d_adv, d_tgt, s_);
+    }
+    // global per-channel statistics (gae.cpp:79-96): sums all-reduced across ranks
+    const double rows = (double)cfg_.N * cfg_.T;
+    double* sum1 = d_stats;
+    double* mean = d_stats + 8;
+    double* sum2 = d_stats + 16;
+    double* inv = d_stats + 24;
+    channel_sums(d_adv, Rl_, m, nullptr, sum1, d_scratch, s_);
+    if (comm_) comm_allreduce_f64(comm_, sum1, m, s_);
+    stats_finalize(sum1, rows, m, mean, 0, s_);
+    channel_sums(d_adv, Rl_, m, mean, sum2, d_scratch, s_);
+    if (comm_) comm_allreduce_f64(comm_, sum2, m, s_);
+    stats_finalize(sum2, rows, m, inv, 1, s_);
+    scalarize(Nl_, cfg_.T, m, d_adv, d_cw + (size_t)g_lo_ * m, reps_, mean, inv, d_sadv, s_);
+    launches_ += 8;
+}
+
+void Trainer::net_step(HyperNet& h, bool is_actor, int B, float inv_B, int maxg, const int* goff, int slot) {
+    const NetDims& nd = h.tgt;
+    const int L = nd.L;
+    const float* th = h.theta + (long)g_lo_ * h.P;
+    float* gth = h.gtheta + (long)g_lo_ * h.P;
+    if (B == 0) {
+        MB_CUDA(cudaMemsetAsync(gth, 0, sizeof(float) * Kl_ * h.P, s_));
+        MB_CUDA(cudaMemsetAsync(d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, sizeof(double), s_));
+        return;
+    }
+    // forward: grouped NT GEMMs with the cluster's generated weights
+    for (int l = 0; l < L; ++l) {
+        const bool last = (l == L - 1);
+        GemmDesc d;
+        d.A = l == 0 ? d_X : d_A[l - 1]; d.am = nd.sz[l]; d.ak = 1;
+        d.B = th + nd.woff[l]; d.bk = 1; d.bn = nd.sz[l]; d.b_bz = h.P;
+        d.C = d_A[l]; d.cm = nd.sz[l + 1]; d.cn = 1;
+        d.M = B; d.N = nd.sz[l + 1]; d.K = nd.sz[l]; d.Z = Kl_;
+        d.gmode = 1; d.goff = goff; d.max_group = maxg;
+        d.bias = th + nd.boff[l]; d.bias_bz = h.P; d.bias_mode = 1;
+        d.act = last ? 0 : 1;
+        gemm("mlp_fwd", d, s_);
+    }
+    float* gout = d_Gz[L - 1];
+    if (is_actor) {  // losses.cpp:87-129
+        actor_rows(B, es_.act_dim, d_rowgroup, h.theta + (long)g_lo_ * h.P, h.P, nd.mlp_n, d_A[L - 1], d_Z, d_lpo,
+                   d_sa, (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, gout, d_lsg, d_lossrows, d_err, s_);
+        segmented_colsum(d_lsg, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.P, 0, s_);
+    } else {  // losses.cpp:170-185
+        critic_rows(B, es_.m, d_A[L - 1], d_tg, inv_B, gout, d_lossrows, s_);
+    }
+    sum_f64(d_lossrows, B, d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, s_);
+    // backward (nn.cpp:111-160) with per-cluster weight gradients
+    for (int l = L - 1; l >= 0; --l) {
+        const float* gz = d_Gz[l];
+        const float* ain = l == 0 ? d_X : d_A[l - 1];
+        GemmDesc d;  // dW_l[g][j][i] = sum_{q in g} gz[q][j] ain[q][i]
+        d.A = gz; d.am = 1; d.ak = nd.sz[l + 1];
+        d.B = ain; d.bk = nd.sz[l]; d.bn = 1;
+        d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_bz = h.P;
+        d.M = nd.sz[l + 1]; d.N = nd.sz[l]; d.K = B; d.Z = Kl_;
+        d.gmode = 2; d.goff = goff;
+        gemm("mlp_dW", d, s_);
+        segmented_colsum(gz, nd.sz[l + 1], goff, Kl_, gth + nd.boff[l], h.P, 0, s_);
+        if (l > 0) {
+            GemmDesc e;  // gz_{l-1}[q][i] = (sum_j gz[q][j] W_l[g][j][i]) (1 - a[q][i]^2)
+            e.A = gz; e.am = nd.sz[l + 1]; e.ak = 1;
+            e.B = th + nd.woff[l]; e.bk = nd.sz[l]; e.bn = 1; e.b_bz = h.P;
+            e.C = d_Gz[l - 1]; e.cm = nd.sz[l]; e.cn = 1;
+            e.M = B; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
+            e.gmode = 1; e.goff = goff; e.max_group = maxg;
+            e.act = 2; e.aux = d_A[l - 1]; e.xm = nd.sz[l]; e.xn = 1;
+            gemm("mlp_dX", e, s_);
+        }
+    }
+    launches_ += 3 * L + 4;
+}
+
+void Trainer::allgather_gtheta(HyperNet& h) {
+    if (comm_) comm_allgather_f32(comm_, h.gtheta, (size_t)Kl_ * h.P, s_);
+}
+
+void Trainer::minibatch(int slot, int B, int Bglob, int maxg, const int* rows, const int* goff) {
+    const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
+    const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
+    if (B > 0) {
+        gather_rows(rows, B, d_obs, od, d_X, s_);
+        gather_rows(rows, B, d_act, ad, d_Z, s_);
+        gather_rows(rows, B, d_lp, 1, d_lpo, s_);
+        gather_rows(rows, B, d_sadv, 1, d_sa, s_);
+        gather_rows(rows, B, d_tgt, m, d_tg, s_);
+        fill_row_group(goff, Kl_, d_rowgroup, B, s_);
+        launches_ += 6;
+    }
+    net_step(actor_, true, B, inv_B, maxg, goff, slot);
+    net_step(critic_, false, B, inv_B, maxg, goff, slot);
+    allgather_gtheta(actor_);
+    allgather_gtheta(critic_);
+    if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
+    check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
+    actor_.backward(s_);
+    critic_.backward(s_);
+    actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180: actor then critic
+    critic_.adam_step(cfg_.critic_lr, d_err, s_);
+    launches_ += 2 * (8 + 4 * (int)actor_.fsz.size()) + 3;
+}
+
+void Trainer::phase_update(int it, int max_minibatches) {
+    g_prof = &prof_;
+    (void)it;
+    const int mbs = cfg_.minibatch_count;
+    mb_done_ = 0;
+    // every rank refreshes theta for its clusters from the current params
+    for (int e = 0; e < cfg_.epochs; ++e)
+        for (int s = 0; s < mbs; ++s) {
+            if (max_minibatches >= 0 && mb_done_ >= max_minibatches) return;
+            const int slot = e * mbs + s;
+            if (mb_Bglob_[slot] == 0) continue;  // lo == hi
+            actor_.forward(d_cw, g_lo_, Kl_, s_);  // hypernet_forward per loss (losses.cpp:79,167)
+            critic_.forward(d_cw, g_lo_, Kl_, s_);
+            minibatch(slot, mb_B_[slot], mb_Bglob_[slot], mb_maxg_[slot], d_rows + (size_t)slot * Bmax_,
+                      d_goff + (size_t)slot * (Kl_ + 1));
+            ++mb_done_;
+        }
+}
+
+void Trainer::finish(IterStats* st) {
+    const int slots = cfg_.epochs * cfg_.minibatch_count;
+    std::vector<double> losses((size_t)slots * 2);
+    std::vector<double> rs(Nl_);
+    std::vector<int> rc(Nl_);
+    int err = 0;
+    MB_CUDA(cudaMemcpyAsync(losses.data(), d_mbloss, sizeof(double) * slots * 2, cudaMemcpyDeviceToHost, s_));
+    MB_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    MB_CUDA(cudaMemcpyAsync(rs.data(), d_retsum, sizeof(double) * Nl_, cudaMemcpyDeviceToHost, s_));
+    MB_CUDA(cudaMemcpyAsync(rc.data(), d_retcnt, sizeof(int) * Nl_, cudaMemcpyDeviceToHost, s_));
+    MB_CUDA(cudaStreamSynchronize(s_));
+    if (st) {
+        st->actor_loss = st->critic_loss = 0;
+        int done = 0;
+        for (int e = 0, k = 0; e < cfg_.epochs; ++e)
+            for (int s = 0; s < cfg_.minibatch_count; ++s, ++k) {
+                if (done >= mb_done_) break;
+                if (mb_Bglob_[k] == 0) continue;
+                st->actor_loss += losses[k * 2];
+                st->critic_loss += losses[k * 2 + 1];
+                ++done;
+            }
+        st->minibatches = mb_done_;
+        st->numeric_error = err;
+        st->cluster_returns.assign(Kl_, std::nan(""));
+        for (int c = 0; c < Kl_; ++c) {
+            double s = 0;
+            int n = 0;
+            for (int r = 0; r < reps_; ++r) {
+                s += rs[c * reps_ + r];
+                n += rc[c * reps_ + r];
+            }
+            if (n) st->cluster_returns[c] = s / n;
+        }
+    }
+    if (err) throw NumericError("non-finite value during the training iteration (loss, ratio or action)");
+}
+
+void Trainer::set_clusters(const float* cw) {
+    cw_h_.assign(cw, cw + (size_t)cfg_.K * es_.m);
+    MB_CUDA(cudaMemcpy(d_cw, cw, sizeof(float) * cfg_.K * es_.m, cudaMemcpyHostToDevice));
+}
+
+void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
+    g_prof = &prof_;
+    if (n <= 0) throw ShapeError("minibatch has no rows");
+    if (n > Bmax_) throw ShapeError("losses_only: more rows than one minibatch buffer holds");
+    for (int q = 0; q < n; ++q)
+        if (rows[q] < 0 || rows[q] >= cfg_.N * cfg_.T) throw ShapeError("minibatch row index out of range");
+    int B = 0, mx = 0;
+    shard_minibatch(rows, 0, n, cfg_.T, inst_lo_, Nl_, reps_, Kl_, h_rows_pinned, h_goff_pinned, &B, &mx);
+    MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (B ? B : 1), cudaMemcpyHostToDevice, s_));
+    MB_CUDA(cudaMemcpyAsync(d_goff, h_goff_pinned, sizeof(int) * (Kl_ + 1), cudaMemcpyHostToDevice, s_));
+    MB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s_));
+    actor_.forward(d_cw, g_lo_, Kl_, s_);
+    critic_.forward(d_cw, g_lo_, Kl_, s_);
+    const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
+    const float inv_B = (float)(1.0 / (double)n);
+    if (B > 0) {
+        gather_rows(d_rows, B, d_obs, od, d_X, s_);
+        gather_rows(d_rows, B, d_act, ad, d_Z, s_);
+        gather_rows(d_rows, B, d_lp, 1, d_lpo, s_);
+        gather_rows(d_rows, B, d_sadv, 1, d_sa, s_);
+        gather_rows(d_rows, B, d_tgt, m, d_tg, s_);
+        fill_row_group(d_goff, Kl_, d_rowgroup, B, s_);
+    }
+    net_step(actor_, true, B, inv_B, mx, d_goff, 0);
+    net_step(critic_, false, B, inv_B, mx, d_goff, 0);
+    allgather_gtheta(actor_);
+    allgather_gtheta(critic_);
+    if (comm_) comm_allreduce_f64(comm_, d_mbloss, 2, s_);
+    actor_.backward(s_);
+    critic_.backward(s_);
+    double l[2];
+    int err = 0;
+    MB_CUDA(cudaMemcpyAsync(l, d_mbloss, sizeof(l), cudaMemcpyDeviceToHost, s_));
+    MB_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    MB_CUDA(cudaStreamSynchronize(s_));
+    if (err) throw NumericError("actor_loss: non-finite ratio");
+    *al = l[0];
+    *cl = l[1];
+}
+
+void Trainer::iteration(int it, IterStats* st) {
+    g_prof = &prof_;
+    phase_rollout(it);
+    phase_advantages();
+    phase_update(it);
+    finish(st);
+}
+
+}  // namespace mb200

@@ -1,0 +1,175 @@
+// Host C++ side of the MORLAX B200 path: device-resident hypernetworks,
+// batched env, and the train-iteration orchestration. Mirrors the
+// reference API (include/morlax/trainer.hpp, hypernet.hpp, env.hpp) with
+// device buffers; C-ABI wrappers live in capi.cu.
+#pragma once
+
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mb200 {
+
+struct Comm;  // NCCL communicator (nccl.cu), null when world == 1
+
+// Per-kernel-class device timing with CUDA events on the launching stream,
+// plus the algorithmic FLOPs / bytes of every launch (for the roofline).
+struct Profiler {
+    struct Cls {
+        std::string name;
+        double flops = 0, bytes = 0, ms = 0;
+        long count = 0;
+    };
+    bool on = false;
+    std::vector<Cls> cls;
+    std::vector<cudaEvent_t> pool;
+    struct Pending { int c; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    size_t used = 0;
+    int begin(const char* name, double flops, double bytes, cudaStream_t s);
+    void end(int h, cudaStream_t s);
+    void collect();  // synchronises the recorded events
+    void reset();
+    ~Profiler();
+};
+
+struct TrainConfig {  // trainer.hpp:21-77 (TrainerConfig + HypernetArch)
+    int env_kind = ENV_POINTMASS;
+    int N = 256, K = 16, kappa = 0, T = 32, epochs = 4, minibatch_count = 4;
+    double gamma = 0.99, lambda = 0.95, clip_eps = 0.2, actor_lr = 3e-4, critic_lr = 3e-4,
+           entropy_coef = 0.1;
+    uint64_t seed = 0;
+    int F = 64;
+    std::vector<int> feat_hidden{64}, actor_hidden{64, 64}, critic_hidden{64, 64};
+    void validate(int m) const;  // config.cpp:17-45 semantics
+};
+
+// Device-resident affine hypernetwork theta(w) = M f(w) + b (hypernet.hpp:20-75)
+// for one target net, with fp32 master params, grads and Adam moments in the
+// reference flat layout [feature | M (P x F) | b (P)].
+struct HyperNet {
+    int m = 0, F = 0, G = 0;  // G: groups (clusters) this hypernet serves
+    std::vector<int> fsz;     // feature sizes [m, hidden..., F]
+    std::vector<long> fwoff, fboff;
+    NetDims tgt{};
+    long nf = 0, P = 0, n = 0;
+    float *p = nullptr, *g = nullptr, *m1 = nullptr, *m2 = nullptr;
+    long steps[3] = {0, 0, 0};
+    std::vector<float*> fact;  // feature activations [G][fsz[l]], l = 0..Lf
+    float *theta = nullptr, *gtheta = nullptr, *gf = nullptr, *parts = nullptr;
+    float *fg0 = nullptr, *fg1 = nullptr;
+    int splits = 1;
+    int* d_split_bounds = nullptr;
+
+    void init(int m_, int F_, const std::vector<int>& fh, const std::vector<int>& target_sizes,
+              bool out_tanh, bool has_log_std, int G_);
+    void free_all();
+    void init_params(uint64_t key, cudaStream_t s);  // init_hypernet (hypernet.cpp:124-145)
+    // f, theta for groups [g0, g0+ng) of the G cluster weights w[G][m]
+    void forward(const float* w, int g0, int ng, cudaStream_t s);
+    // grads from gtheta [G][P] (all groups) -> g
+    void backward(cudaStream_t s);
+    void adam_step(double lr, const int* err, cudaStream_t s);
+};
+
+NetDims make_dims(const std::vector<int>& sizes, bool out_tanh, bool has_log_std);
+
+struct IterStats {
+    double actor_loss = 0, critic_loss = 0;  // summed over minibatch steps
+    double seconds = 0;
+    int minibatches = 0;
+    int numeric_error = 0;
+    std::vector<double> cluster_returns;     // mean completed return per cluster (NaN if none)
+};
+
+// Minibatch row selection for one rank (host, pure): rows of perm[lo:hi)
+// whose instance lies in [inst_lo, inst_lo + n_inst), converted to local row
+// ids and stably grouped by cluster (losses.cpp:21-33 ordering).
+void shard_minibatch(const int* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps,
+                     int n_groups, int* rows_out, int* goff_out, int* n_rows_out, int* max_group);
+
+class Trainer {
+public:
+    Trainer(const TrainConfig& cfg, int world = 1, int rank = 0, const void* nccl_id = nullptr);
+    ~Trainer();
+    void iteration(int it, IterStats* st);
+
+    // phases (for tests / bench breakdowns); iteration() runs all of them
+    void phase_rollout(int it);
+    void phase_advantages();
+    void phase_update(int it, int max_minibatches = -1);
+    void finish(IterStats* st);
+    // actor_loss + critic_loss (+ hypernet backward) on global rows of the
+    // current batch, no Adam (parity tests; losses.cpp:46-189)
+    void losses_only(const int* rows, int n, double* actor_loss, double* critic_loss);
+    void set_clusters(const float* cw);
+
+    // accessors
+    const TrainConfig& config() const { return cfg_; }
+    const EnvSpecB& env() const { return es_; }
+    HyperNet& actor() { return actor_; }
+    HyperNet& critic() { return critic_; }
+    int local_envs() const { return Nl_; }
+    int local_groups() const { return Kl_; }
+    cudaStream_t stream() const { return s_; }
+    std::vector<int>& perm() { return perm_; }
+    const std::vector<float>& clusters_host() const { return cw_h_; }
+    // device batch
+    float *d_obs = nullptr, *d_act = nullptr, *d_lp = nullptr, *d_rew = nullptr, *d_val = nullptr,
+          *d_nval = nullptr, *d_adv = nullptr, *d_tgt = nullptr, *d_sadv = nullptr;
+    uint8_t *d_term = nullptr, *d_trunc = nullptr;
+    float* d_state = nullptr;
+    uint64_t *d_ekey = nullptr, *d_ectr = nullptr;
+    int* d_steps = nullptr;
+    float* d_tracker = nullptr;
+    int* d_err = nullptr;
+    unsigned long long* d_clamps = nullptr;
+    long kernel_launches() const { return launches_; }
+    Profiler& profiler() { return prof_; }
+
+private:
+    void alloc();
+    void prepare_perms(int it);
+    void minibatch(int slot, int B, int Bglob, int maxg, const int* d_rows, const int* d_goff);
+    void net_step(HyperNet& h, bool actor, int B, float inv_B, int maxg, const int* d_goff, int slot);
+    void allgather_gtheta(HyperNet& h);
+
+    TrainConfig cfg_;
+    EnvSpecB es_{};
+    int world_ = 1, rank_ = 0;
+    Comm* comm_ = nullptr;
+    int Nl_ = 0, Kl_ = 0, reps_ = 0, inst_lo_ = 0, g_lo_ = 0;
+    long Rl_ = 0;
+    HostRng root_;
+    HyperNet actor_, critic_;
+    cudaStream_t s_ = nullptr;
+    std::vector<float> cw_h_;
+    float* d_cw = nullptr;
+    float* h_cw_pinned = nullptr;
+    std::vector<int> perm_;
+    int* h_rows_pinned = nullptr;  // [epochs*mbs][Bmax]
+    int* h_goff_pinned = nullptr;  // [epochs*mbs][Kl+1]
+    int *d_rows = nullptr, *d_goff = nullptr, *d_rowgroup = nullptr;
+    std::vector<int> mb_B_, mb_Bglob_, mb_maxg_;
+    int Bmax_ = 0;
+    // update buffers
+    float *d_X = nullptr, *d_Z = nullptr, *d_lpo = nullptr, *d_sa = nullptr, *d_tg = nullptr;
+    std::vector<float*> d_A;   // activations per layer (max width)
+    std::vector<float*> d_Gz;  // gradients per layer
+    float *d_lsg = nullptr;
+    double *d_lossrows = nullptr, *d_mbloss = nullptr, *d_stats = nullptr, *d_scratch = nullptr;
+    double* d_retsum = nullptr;
+    int* d_retcnt = nullptr;
+    int mb_done_ = 0;
+    long launches_ = 0;
+    Profiler prof_;
+};
+
+}  // namespace mb200

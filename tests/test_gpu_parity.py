@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the C oracle on identical
+seeded inputs. Integer outputs (RNG words, flags, perms, masks, hit counts)
+are compared bit-exactly; float outputs within the tolerances of
+tests/helpers.py. Inputs fed to both sides are fp32-representable so the
+only difference is device arithmetic."""
+import numpy as np
+import pytest
+
+from helpers import REL_CHAIN, REL_F32, assert_close, golden, max_rel_err
+from pyoracle import Oracle, OracleTrainer, TrainCfg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mb():
+    import paper_2603_09237_b200 as mb
+    return mb
+
+
+@pytest.fixture(scope="module")
+def o():
+    return Oracle("oracle")
+
+
+@pytest.fixture(scope="module")
+def g():
+    return golden()
+
+
+def r32(x):
+    return np.asarray(x, np.float32).astype(np.float64)
+
+
+# ------------------------------------------------------------------ RNG
+def test_rng_words_bit_exact(mb, o, g):
+    k0 = int(g["rng_keys"][0])
+    assert np.array_equal(mb.rng_words(k0, 0, 256), g["rng_words_k0"])
+    assert np.array_equal(mb.rng_words(k0, 1000, 64), g["rng_words_k0_ctr1000"])
+    big = mb.rng_words(0x1234567, 99, 1 << 20)
+    assert np.array_equal(big, o.rng_words(0x1234567, 99, 1 << 20))
+
+
+def test_rng_gaussians(mb, g):
+    k0 = int(g["rng_keys"][0])
+    got = mb.rng_gaussians(k0, 0, 128)
+    # same words; fp64 log/cos may differ from glibc in the last ulp
+    assert_close(got, g["rng_gauss_k0"], 1e-14, floor=1e-12, what="box-muller")
+
+
+# ------------------------------------------------------------------ env (K1)
+@pytest.mark.parametrize("name", ["mo-lqr1d", "mo-pointmass", "mo-dst-continuous", "mo-humanoid6"])
+def test_env_step_parity(mb, o, g, name):
+    key = name.replace("-", "_")
+    acts = r32(g[f"env_{key}_actions"])
+    rk = int(g[f"env_{key}_reset_key"][0])
+    e, eo = mb.BatchedEnv(name, 4), o.env(name, 4)
+    assert_close(e.reset(rk), eo.reset(rk), 1e-7, what="reset obs")
+    for t in range(len(acts)):
+        s = e.step(acts[t])
+        ob, rw, te, tr = eo.step(acts[t])
+        assert np.array_equal(s.terminated, te) and np.array_equal(s.truncated, tr), t
+        assert_close(s.obs, ob, REL_F32, floor=1e-4, what=f"{name} obs t={t}")
+        assert_close(s.reward, rw, REL_F32, floor=1e-4, what=f"{name} reward t={t}")
+    assert e.clamp_count() == eo.clamp_count()
+
+
+def test_env_large_batch_auto_reset(mb, o):
+    n = 8192
+    e, eo = mb.BatchedEnv("mo-pointmass", n), o.env("mo-pointmass", n)
+    e.reset(77)
+    eo.reset(77)
+    rng = np.random.default_rng(0)
+    for t in range(201):
+        a = r32(rng.uniform(-1, 1, (n, 2)))
+        s = e.step(a)
+        ob, rw, te, tr = eo.step(a)
+        assert np.array_equal(s.truncated, tr)
+    assert_close(e.current_obs(), eo.current_obs(), REL_F32, floor=1e-4, what="post-reset obs")
+
+
+def test_env_rejects_non_finite_action(mb):
+    e = mb.BatchedEnv("mo-pointmass", 2)
+    e.reset(1)
+    with pytest.raises(mb.NumericError):
+        e.step(np.array([[0.1, np.nan], [0.0, 0.0]]))
+
+
+# ------------------------------------------------------------------ hypernet (K2/K6)
+@pytest.mark.parametrize("F,fh,ah,od,ad,m", [(8, [8], [8, 8], 4, 2, 2), (64, [64], [64, 64], 4, 2, 2),
+                                             (256, [256], [256, 256], 45, 12, 6)])
+def test_hypernet_forward_backward(mb, o, F, fh, ah, od, ad, m):
+    from pyoracle import HSpec
+    spec_o = HSpec(m, F, fh, [od] + ah + [ad], True, True)
+    spec = mb.HypernetSpec(m, F, fh, [od] + ah + [ad], True, True)
+    flat = o.init_hypernet(spec_o, 0xBEEF)
+    dev_init = mb.init_hypernet(spec, 0xBEEF)
+    assert_close(dev_init, flat, 1e-6, floor=1e-9, what="init_hypernet")
+    flat = r32(flat)
+    rng = np.random.default_rng(3)
+    W = rng.dirichlet(np.ones(m), size=5)
+    th = mb.hypernet_forward(spec, flat, W)
+    th_o = np.array([o.hypernet_forward(spec_o, flat, w) for w in W])
+    assert_close(th, th_o, REL_F32 * 10, floor=1e-3, what="theta")
+    gth = r32(rng.normal(size=th.shape))
+    gr = mb.hypernet_backward(spec, flat, W, gth)
+    gr_o = sum(o.hypernet_backward(spec_o, flat, W[i], gth[i]) for i in range(len(W)))
+    scale = np.abs(gr_o).max()
+    assert np.abs(gr - gr_o).max() <= 1e-4 * scale
+
+
+# ------------------------------------------------------------------ GAE / normalise (K4)
+@pytest.mark.parametrize("T", [1, 16, 32, 64, 100])
+def test_gae_scan_parity(mb, o, T):
+    rng = np.random.default_rng(T)
+    N, m = 37, 6
+    r, v, nv = (r32(rng.normal(size=(N * T, m))) for _ in range(3))
+    u = rng.random(N * T)
+    te = (u < 0.03).astype(np.uint8)
+    tr = ((u >= 0.03) & (u < 0.06)).astype(np.uint8)
+    adv, tg = mb.gae_per_objective(r, v, nv, te, tr, N, T, 0.99, 0.95)
+    adv_o, tg_o = o.gae(r, v, nv, te, tr, N, T, 0.99, 0.95)
+    assert_close(adv, adv_o, REL_F32 * 10, floor=1e-3, what="advantages")
+    assert_close(tg, tg_o, REL_F32 * 10, floor=1e-3, what="targets")
+    tw = rng.dirichlet(np.ones(m), size=N)
+    s = mb.normalize_and_scalarize(r32(adv_o), tw, N, T)
+    s_o = o.normalize_scalarize(r32(adv_o), r32(tw), N, T)
+    assert_close(s, s_o, REL_F32 * 10, floor=1e-3, what="scalar advantages")
+
+
+def test_gae_reference_hand_fixture(mb):  # test_gae.cpp:109-134
+    adv, tg = mb.gae_per_objective([[1.0], [1.0]], [[2.0], [1.0]], [[3.0], [4.0]], [0, 0], [0, 1],
+                                   1, 2, 0.5, 0.5)
+    assert adv[:, 0].tolist() == [1.0, 2.0] and tg[:, 0].tolist() == [3.0, 3.0]
+    adv, tg = mb.gae_per_objective([[1.0], [1.0]], [[2.0], [1.0]], [[3.0], [4.0]], [0, 1], [0, 0],
+                                   1, 2, 0.5, 0.5)
+    assert adv[:, 0].tolist() == [0.5, 0.0] and tg[:, 0].tolist() == [2.5, 1.0]
+
+
+# ------------------------------------------------------------------ Adam (K7)
+def test_adam_parity(mb, o):
+    rng = np.random.default_rng(5)
+    n = 1003
+    p = r32(rng.normal(size=n))
+    m1 = np.zeros(n)
+    m2 = np.zeros(n)
+    po, m1o, m2o, st, sto = p.copy(), m1.copy(), m2.copy(), 0, 0
+    for _ in range(5):
+        gr = r32(rng.normal(size=n))
+        p, m1, m2, st = mb.adam_apply(p, gr, m1, m2, st, 1e-3)
+        po, m1o, m2o, sto = o.adam(po, gr, m1o, m2o, sto, 1e-3)
+    assert st == sto == 5
+    assert_close(p, po, REL_F32, floor=1e-3, what="adam params")
+
+
+def test_adam_first_step_moves_by_lr(mb):  # test_trainer.cpp:486-497
+    p, _, _, _ = mb.adam_apply([0.0], [1.0], [0.0], [0.0], 0, 0.1)
+    assert abs(p[0] + 0.1) < 1e-6
+
+
+# ------------------------------------------------------------------ trainer pieces
+def _tiny(env="mo-pointmass", **kw):
+    base = dict(env=env, N=8, K=2, T=12, epochs=2, minibatch_count=1, F=8, feat_hidden=[8],
+                actor_hidden=[8, 8], critic_hidden=[8, 8], seed=5)
+    base.update(kw)
+    return TrainCfg(**base)
+
+
+def _mbcfg(mb, c: TrainCfg):
+    return mb.TrainConfig(env_name=c.env, N=c.N, K=c.K, kappa=c.kappa, T=c.T, epochs=c.epochs,
+                          minibatch_count=c.minibatch_count, gamma=c.gamma, gae_lambda=c.lam,
+                          clip_eps=c.clip_eps, actor_lr=c.actor_lr, critic_lr=c.critic_lr,
+                          entropy_coef=c.entropy_coef, seed=c.seed, F=c.F,
+                          feature_hidden=c.feat_hidden, actor_hidden=c.actor_hidden,
+                          critic_hidden=c.critic_hidden)
+
+
+def test_trainer_init_matches_reference_init(mb, o, g):
+    t = mb.Trainer(_mbcfg(mb, _tiny()))
+    assert_close(t.params("actor"), g["hyper_actor_init"], 1e-6, floor=1e-9, what="actor init")
+    assert_close(t.params("critic"), g["hyper_critic_init"], 1e-6, floor=1e-9, what="critic init")
+
+
+def test_losses_and_grads_parity(mb, o, g):
+    """actor_loss / critic_loss through the hypernet on the reference rollout batch."""
+    c = _tiny()
+    a_s, c_s = c.specs()
+    t = mb.Trainer(_mbcfg(mb, c))
+    af, cf = r32(g["hyper_actor_init"]), r32(g["hyper_critic_init"])
+    t.set_params("actor", af)
+    t.set_params("critic", cf)
+    obs, act, lp = r32(g["roll_obs"]), r32(g["roll_action_pre"]), r32(g["roll_logprob"])
+    sadv, tgt = r32(g["gae_sadv"]), r32(g["gae_tgt"])
+    cw = r32(g["roll_cw"])
+    t.set("obs", obs)
+    t.set("action_pre", act)
+    t.set("logprob", lp)
+    t.set("scalar_advantage", sadv)
+    t.set("value_targets", tgt)
+    t.set("clusters", cw)
+    rows = g["loss_rows"]
+    la, lc = t.losses(rows)
+    tw = np.repeat(cw, 4, axis=0)
+    cl = np.repeat(np.arange(2), 4).astype(np.int32)
+    la_o, ga_o = o.actor_loss(a_s, af, 8, 12, obs, act, lp, tw, cl, rows, sadv, 0.2, 0.1)
+    lc_o, gc_o = o.critic_loss(c_s, cf, 8, 12, obs, tw, cl, rows, tgt)
+    assert abs(la - la_o) <= REL_CHAIN * max(1.0, abs(la_o))
+    assert abs(lc - lc_o) <= REL_CHAIN * max(1.0, abs(lc_o))
+    ga, gc = t.grad("actor"), t.grad("critic")
+    assert np.abs(ga - ga_o).max() <= REL_CHAIN * np.abs(ga_o).max()
+    assert np.abs(gc - gc_o).max() <= REL_CHAIN * np.abs(gc_o).max()
+
+
+@pytest.mark.parametrize("env", ["mo-pointmass", "mo-humanoid6"])
+def test_rollout_and_advantages_parity(mb, o, env):
+    kw = dict(N=32, K=4, T=16, F=16, feat_hidden=[16], actor_hidden=[32, 32], critic_hidden=[32, 32])
+    c = _tiny(env, **kw)
+    t = mb.Trainer(_mbcfg(mb, c))
+    ot = OracleTrainer(o, c)
+    t.phase(0, 1)
+    t.phase(0, 2)
+    ot.iteration(0, max_minibatches=0)
+    b = ot.batch()
+    assert_close(t.get("clusters"), ot.clusters(), 1e-7, floor=1e-9, what="clusters")
+    assert np.array_equal(t.get("terminated"), b["term"])
+    assert np.array_equal(t.get("truncated"), b["trunc"])
+    for name, key in (("obs", "obs"), ("action_pre", "action_pre"), ("logprob", "logprob"),
+                      ("reward", "reward"), ("value", "value"), ("next_value", "next_value"),
+                      ("advantages", "adv"), ("value_targets", "targets"),
+                      ("scalar_advantage", "sadv")):
+        assert_close(t.get(name), b[key], REL_CHAIN, floor=1e-2, what=name)
+
+
+def test_full_iteration_parity(mb, o):
+    c = _tiny(N=32, K=4, T=16, epochs=2, minibatch_count=2, F=16, feat_hidden=[16],
+              actor_hidden=[32, 32], critic_hidden=[32, 32])
+    t = mb.Trainer(_mbcfg(mb, c))
+    ot = OracleTrainer(o, c)
+    a0 = t.params("actor")
+    st = t.iteration(0)
+    al, cl = ot.iteration(0)
+    assert st.minibatches == 4
+    assert abs(st.actor_loss - al) <= REL_CHAIN * max(1, abs(al))
+    assert abs(st.critic_loss - cl) <= REL_CHAIN * max(1, abs(cl))
+    assert np.array_equal(t.get("perm"), ot.perm())
+    for which, ref in (("actor", ot.actor_params()), ("critic", ot.critic_params())):
+        p = t.params(which)
+        d_ref = ref - (a0 if which == "actor" else ref)  # noqa: F841
+        # Adam moves each weight by <= ~lr per step; fp32 grads may flip
+        # near-zero gradient signs, so bound the error by the step size.
+        lr = c.actor_lr if which == "actor" else c.critic_lr
+        err = np.abs(p - ref)
+        assert np.quantile(err, 0.99) <= 0.05 * lr * 4, which
+        assert err.max() <= 2.5 * lr * 4, which
+
+
+def test_iteration_is_deterministic(mb):
+    c = _tiny(N=32, K=4, T=16)
+    t1, t2 = mb.Trainer(_mbcfg(mb, c)), mb.Trainer(_mbcfg(mb, c))
+    for it in range(2):
+        s1, s2 = t1.iteration(it), t2.iteration(it)
+        assert s1.actor_loss == s2.actor_loss and s1.critic_loss == s2.critic_loss
+    assert np.array_equal(t1.params("actor"), t2.params("actor"))
+    assert np.array_equal(t1.params("critic"), t2.params("critic"))
+
+
+def test_trainer_config_errors(mb):
+    with pytest.raises(mb.ConfigError):
+        mb.Trainer(mb.TrainConfig(N=10, K=3))
+    with pytest.raises(mb.ConfigError):
+        mb.Trainer(mb.TrainConfig(env_name="nope"))
+
+
+# ------------------------------------------------------------------ Pareto / HV (K8/K9)
+def _front(n, m, seed):  # config-5 recipe: Dirichlet -> unit sphere + N(0, 0.02^2)
+    rng = np.random.default_rng(seed)
+    w = rng.dirichlet(np.ones(m), size=n)
+    p = w / np.linalg.norm(w, axis=1, keepdims=True)
+    return p + rng.normal(0, 0.02, p.shape)
+
+
+def test_pareto_mask_bit_exact(mb, o, g):
+    assert np.array_equal(mb.nondominated_mask(g["pareto_pts3"]), g["pareto_mask3"])
+    p = _front(1024, 6, 4)
+    p[100] = p[7]  # exact duplicate
+    p[200] = np.round(p[200], 1)
+    assert np.array_equal(mb.nondominated_mask(p), o.nondominated_mask(p))
+    q = np.round(np.random.default_rng(1).normal(size=(600, 2)), 1)  # many ties
+    assert np.array_equal(mb.nondominated_mask(q), o.nondominated_mask(q))
+
+
+def test_hypervolume_mc_bit_exact(mb, o, g):
+    key = o.rng_seed_state(0x9E3779B9)[0]
+    v, se, _ = mb.hypervolume_mc(g["hv_pts6"], np.zeros(6), 200_000, key, 0)
+    assert v == g["hv_mc6"][0] and se == g["hv_mc6"][1]
+    p = _front(1024, 6, 4)
+    ref = -np.ones(6)
+    v, se, hits = mb.hypervolume_mc(p, ref, 1_000_000, key, 0)
+    vo, seo, ho = o.hypervolume_mc(p, ref, 1_000_000, key, 0)
+    assert hits == ho and v == vo and se == seo
+    vd, sed, ex, cl = mb.hypervolume_detailed(p, ref)
+    assert (vd, sed, ex) == (vo, seo, False) and cl == 0
