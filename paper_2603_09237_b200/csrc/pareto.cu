@@ -143,7 +143,7 @@ void hv_mc(int n, int m, const double* pts, const double* ref, uint64_t samples,
     MB_CUDA(cudaMemsetAsync(hits, 0, sizeof(unsigned long long), s));
     const size_t smem = (size_t)n * m * sizeof(double);
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    if (smem > configured) {
         MB_CUDA(cudaFuncSetAttribute(k_hv_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
