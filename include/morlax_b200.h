@@ -162,6 +162,11 @@ int morlax_shard_minibatch(const int32_t* perm, int lo, int hi, int T, int inst_
                            int n_groups, int32_t* rows_out, int32_t* goff_out, int* n_rows_out,
                            int* max_group_out);
 
+/* ---- test hook: C[M][N] = A(m,k) B(k,n) with strided fp32 operands, on the
+ *      tcgen05 path (use_tc = 1) or the SIMT path (0) ---------------------- */
+int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, const float* B, long bk, long bn,
+                     float* C, int use_tc);
+
 /* ---- Pareto (replaces nondominated_filter / hypervolume_mc /
  *      hypervolume_detailed, include/morlax/pareto.hpp:21-56) ------------ */
 /* survivors of nondominated_filter as a mask over the input order */

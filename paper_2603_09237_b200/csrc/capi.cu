@@ -538,6 +538,24 @@ int morlax_shard_minibatch(const int32_t* perm, int lo, int hi, int T, int inst_
     });
 }
 
+// ------------------------------------------------------------------ GEMM test hook
+int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, const float* B, long bk, long bn,
+                     float* C, int use_tc) {
+    return guarded([&] {
+        long amax = (long)(M - 1) * am + (long)(K - 1) * ak + 1;
+        long bmax = (long)(K - 1) * bk + (long)(N - 1) * bn + 1;
+        DBuf<float> da(A, amax), db(B, bmax), dc((size_t)M * N);
+        GemmDesc d;
+        d.A = da.p; d.am = am; d.ak = ak;
+        d.B = db.p; d.bk = bk; d.bn = bn;
+        d.C = dc.p; d.cm = N; d.cn = 1;
+        d.M = M; d.N = N; d.K = K;
+        if (use_tc) gemm_tc(d, 0); else gemm_simt(d, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        dc.get(C);
+    });
+}
+
 // ------------------------------------------------------------------ pareto
 int morlax_pareto_mask_device(int n, int m, const double* d_pts, uint8_t* d_mask, void* stream) {
     return guarded([&] {

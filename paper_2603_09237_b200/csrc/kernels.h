@@ -33,12 +33,11 @@ struct GemmDesc {
 void gemm_simt(const GemmDesc& d, cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 GEMM
-// bf16 operands, fp32 accumulate in TMEM. D(m,n) = sum_k A(m,k) B(n,k) with
-// A: [M][K] K-major (lda), B: [N][K] K-major (ldb). Output fp32 (ldc) with
-// optional per-m bias. Returns false if the shape is unsupported.
-bool tc_gemm_supported(int M, int N, int K);
-void tc_gemm_bf16(const __nv_bfloat16* A, long lda, const __nv_bfloat16* B, long ldb, float* C,
-                  long ldc_m, long ldc_n, int M, int N, int K, const float* bias, cudaStream_t s);
+// Same GemmDesc contract, on the 5th-gen tensor cores (tc_gemm.cu): bf16
+// operands staged in SMEM, fp32 accumulation in TMEM. Needs a unit stride
+// along K or M (A) and along K or N (B).
+bool gemm_tc_eligible(const GemmDesc& d);
+void gemm_tc(const GemmDesc& d, cudaStream_t s);
 
 // ---------------------------------------------------------------- env (K1)
 void env_reset(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,
@@ -73,6 +72,23 @@ struct RolloutArgs {
 };
 void rollout(const RolloutArgs& a, cudaStream_t s);
 int rollout_rows_per_cta();
+
+// tensor-core rollout (rollout_tc.cu): per-cluster weights packed as bf16
+// UMMA images, streamed per step by the bulk-copy engine
+struct NetPlan {
+    int nchunks, blob_bytes;
+    int kin_pad[8], tiles[8];
+    int chunk_off[24], chunk_bytes[24], chunk_layer[24], chunk_tile[24];
+};
+NetPlan make_plan(const NetDims& nd);
+void pack_theta(const float* theta, int G, const NetDims& nd, const NetPlan& pl, uint8_t* blob, cudaStream_t s);
+struct RolloutTcArgs : RolloutArgs {
+    NetPlan pol_plan, cri_plan;
+    const uint8_t* pol_blob;  // [K][pol_plan.blob_bytes]
+    const uint8_t* cri_blob;
+    int slot_bytes, xb_bytes, hb_bytes, nepad;  // filled by rollout_tc
+};
+void rollout_tc(RolloutTcArgs a, cudaStream_t s);
 
 // ---------------------------------------------------------------- GAE + normalise (K4)
 void gae_scan(int N, int T, int m, const float* reward, const float* value, const float* next_value,

@@ -175,7 +175,10 @@ static double gemm_flops(const GemmDesc& d) {
 }
 static void gemm(const char* cls, const GemmDesc& d, cudaStream_t s) {
     ProfScope p(cls, gemm_flops(d), 0, s);
-    gemm_simt(d, s);
+    if (gemm_tc_eligible(d))
+        gemm_tc(d, s);
+    else
+        gemm_simt(d, s);
 }
 
 // ------------------------------------------------------------------ HyperNet
@@ -407,7 +410,8 @@ Trainer::~Trainer() {
     for (auto* p : d_Gz) cudaFree(p);
     for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
                     (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_rowgroup, (void*)d_lossrows,
-                    (void*)d_mbloss, (void*)d_stats, (void*)d_scratch, (void*)d_retsum, (void*)d_retcnt})
+                    (void*)d_mbloss, (void*)d_stats, (void*)d_scratch, (void*)d_retsum, (void*)d_retcnt,
+                    (void*)d_pol_blob, (void*)d_cri_blob})
         if (p) cudaFree(p);
     if (h_cw_pinned) cudaFreeHost(h_cw_pinned);
     if (h_rows_pinned) cudaFreeHost(h_rows_pinned);
@@ -465,6 +469,11 @@ void Trainer::alloc() {
     d_stats = dalloc<double>(4 * 8);
     d_scratch = dalloc<double>(148 * 2 * 8);
     d_retsum = dalloc<double>(Nl_);
+    pol_plan_ = make_plan(actor_.tgt);
+    cri_plan_ = make_plan(critic_.tgt);
+    if (pol_plan_.kin_pad[0] != cri_plan_.kin_pad[0]) throw ShapeError("policy/critic input padding mismatch");
+    d_pol_blob = dalloc<uint8_t>((size_t)Kl_ * pol_plan_.blob_bytes);
+    d_cri_blob = dalloc<uint8_t>((size_t)Kl_ * cri_plan_.blob_bytes);
     d_retcnt = dalloc<int>(Nl_);
     mb_B_.assign(slots, 0);
     mb_Bglob_.assign(slots, 0);
@@ -499,7 +508,17 @@ void Trainer::phase_rollout(int it) {
     MB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s_));
     actor_.forward(d_cw, g_lo_, Kl_, s_);
     critic_.forward(d_cw, g_lo_, Kl_, s_);
-    RolloutArgs a{};
+    {
+        ProfScope ps("pack_theta", 0, (double)Kl_ * (actor_.P * 4 + pol_plan_.blob_bytes + critic_.P * 4 +
+                                                       cri_plan_.blob_bytes), s_);
+        pack_theta(actor_.theta + (long)g_lo_ * actor_.P, Kl_, actor_.tgt, pol_plan_, d_pol_blob, s_);
+        pack_theta(critic_.theta + (long)g_lo_ * critic_.P, Kl_, critic_.tgt, cri_plan_, d_cri_blob, s_);
+    }
+    RolloutTcArgs a{};
+    a.pol_plan = pol_plan_;
+    a.cri_plan = cri_plan_;
+    a.pol_blob = d_pol_blob;
+    a.cri_blob = d_cri_blob;
     a.kind = es_.kind; a.N = Nl_; a.T = cfg_.T; a.K = Kl_; a.reps = reps_;
     a.od = es_.obs_dim; a.ad = es_.act_dim; a.m = m; a.sdim = es_.state_dim; a.max_steps = es_.max_steps;
     a.theta = actor_.theta + (long)g_lo_ * actor_.P;
@@ -520,9 +539,9 @@ void Trainer::phase_rollout(int it) {
         for (int l = 0; l < a.pol.L; ++l) macs += (double)a.pol.sz[l] * a.pol.sz[l + 1];
         for (int l = 0; l < a.cri.L; ++l) macs += (double)a.cri.sz[l] * a.cri.sz[l + 1];
         ProfScope ps("rollout", 2.0 * macs * Rl_, 0, s_);
-        rollout(a, s_);
+        rollout_tc(a, s_);
     }
-    launches_ += 1;
+    launches_ += 3;
     prepare_perms(it);  // host work overlaps the rollout on the GPU
 }
 

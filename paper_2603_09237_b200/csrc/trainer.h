@@ -167,6 +167,8 @@ private:
     double *d_lossrows = nullptr, *d_mbloss = nullptr, *d_stats = nullptr, *d_scratch = nullptr;
     double* d_retsum = nullptr;
     int* d_retcnt = nullptr;
+    NetPlan pol_plan_{}, cri_plan_{};
+    uint8_t *d_pol_blob = nullptr, *d_cri_blob = nullptr;
     int mb_done_ = 0;
     long launches_ = 0;
     Profiler prof_;

@@ -12,9 +12,22 @@ REF_SRC = "/root/reference/proj"
 
 # fp32 single-kernel results (env step, GAE, scalarise, Adam, hypernet fwd)
 REL_F32 = 1e-5
-# fp32 results that pass through long reductions / recurrences or through the
-# trained MLP stack (losses, gradients, rollouts, updated weights)
-REL_CHAIN = 2e-3
+# GEMM-fed results: the policy / critic / hypernet contractions run on the
+# tcgen05 tensor cores with bf16 operands and fp32 accumulation (north star:
+# "bf16 in, fp32 accumulate"). Stated bf16 tolerance, NORMWISE:
+#   max|gpu - ref| <= REL_BF16 * max|ref|   (theta, losses, gradients)
+REL_BF16 = 5e-3
+# trajectories fed back through the bf16 policy (rollout obs / actions /
+# values over T steps) and post-Adam weights
+REL_CHAIN = 2e-2
+
+
+def assert_normwise(a, b, rel, what=""):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    scale = max(float(np.abs(b).max()), 1e-30)
+    e = float(np.abs(a - b).max()) / scale
+    assert e <= rel, f"{what}: normwise rel err {e:.3g} > {rel:.3g}"
 
 
 def golden():

@@ -13,6 +13,12 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 t = mb.Trainer(mb.TrainConfig(**bench.BASE[cfg_name]))
 t.iteration(0)
 print("warm launches (trainer-counted):", t.kernel_launches, flush=True)
+import torch  # noqa: E402
+
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off captures only this region
 for i in range(iters):
     t.iteration(1 + i)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("total launches:", t.kernel_launches)
