@@ -79,6 +79,7 @@ struct HyperHandle {
     void load(const double* flat) {
         std::vector<float> f(flat, flat + h.n);
         MB_CUDA(cudaMemcpy(h.p, f.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+        h.refresh_images(0);
     }
 };
 }  // namespace
@@ -412,6 +413,8 @@ int morlax_trainer_set_params(morlax_trainer* t, int which, const double* in) {
         std::vector<float> f(in, in + h.n);
         MB_CUDA(cudaStreamSynchronize(t->t->stream()));
         MB_CUDA(cudaMemcpy(h.p, f.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+        h.refresh_images(t->t->stream());
+        MB_CUDA(cudaStreamSynchronize(t->t->stream()));
     });
 }
 int morlax_trainer_get_grad(morlax_trainer* t, int which, double* out) {
@@ -545,12 +548,31 @@ int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, cons
         long amax = (long)(M - 1) * am + (long)(K - 1) * ak + 1;
         long bmax = (long)(K - 1) * bk + (long)(N - 1) * bn + 1;
         DBuf<float> da(A, amax), db(B, bmax), dc((size_t)M * N);
-        GemmDesc d;
-        d.A = da.p; d.am = am; d.ak = ak;
-        d.B = db.p; d.bk = bk; d.bn = bn;
-        d.C = dc.p; d.cm = N; d.cn = 1;
-        d.M = M; d.N = N; d.K = K;
-        if (use_tc) gemm_tc(d, 0); else gemm_simt(d, 0);
+        if (use_tc) {
+            // operands -> tiled bf16 images in the orientation their strides
+            // describe (unit stride along K: view 0; along M/N: view 1)
+            const int a_view = ak == 1 ? 0 : 1, b_view = bk == 1 ? 0 : 1;
+            const int aR = a_view ? K : M, aC = a_view ? M : K, bR = b_view ? K : N, bC = b_view ? N : K;
+            DBuf<uint8_t> ia(img_bytes(aR, aC)), ib(img_bytes(bR, bC));
+            MB_CUDA(cudaMemset(ia.p, 0, img_bytes(aR, aC)));
+            MB_CUDA(cudaMemset(ib.p, 0, img_bytes(bR, bC)));
+            Img IA{ia.p, aR, aC, 0}, IB{ib.p, bR, bC, 0};
+            to_img(da.p, a_view ? am * 0 + (ak == 1 ? 1 : ak) : am, 0, aR, aC, IA, 1, 0);
+            to_img(db.p, b_view ? bn * 0 + bk : bn, 0, bR, bC, IB, 1, 0);
+            IGemm d;
+            d.A = IA; d.a_view = a_view;
+            d.B = IB; d.b_view = b_view;
+            d.M = M; d.N = N; d.K = K;
+            d.C = dc.p; d.cm = N; d.cn = 1;
+            img_gemm(d, 0);
+        } else {
+            GemmDesc d;
+            d.A = da.p; d.am = am; d.ak = ak;
+            d.B = db.p; d.bk = bk; d.bn = bn;
+            d.C = dc.p; d.cm = N; d.cn = 1;
+            d.M = M; d.N = N; d.K = K;
+            gemm_simt(d, 0);
+        }
         MB_CUDA(cudaDeviceSynchronize());
         dc.get(C);
     });

@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "umma.cuh"
 
 namespace mb200 {
 
@@ -642,6 +643,93 @@ void mul_dtanh(float* g, const float* a, long n, cudaStream_t s) {
     MB_LAUNCH();
 }
 
+// image-output variants (tcgen05 update path): padded rows (rows[q] < 0)
+// get zero loss and zero gradient
+__global__ void k_actor_rows_img(int Bp, int ad, const int* rows, const int* rg, const float* theta, long P,
+                                 long mlp_n, const float* mu, int ldmu, const float* z, const float* lp_old,
+                                 const float* sadv, float clip, float ent, float inv_B, Img gimg, float* lsg,
+                                 double* loss_rows, int* err) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Bp) return;
+    float g[16];
+    for (int d = 0; d < 16; ++d) g[d] = 0.f;
+    if (rows[q] < 0) {
+        loss_rows[q] = 0.0;
+        for (int d = 0; d < ad; ++d) lsg[(long)q * ad + d] = 0.f;
+    } else {
+        const float* th = theta + (long)rg[q] * P + mlp_n;
+        float lp = 0.f, ls[16], zn[16], sig[16], ent_h = 0.f;
+        for (int d = 0; d < ad; ++d) {  // action_logprob (nn.cpp:204-219)
+            ls[d] = fminf(fmaxf(th[d], -5.f), 1.f);
+            sig[d] = __expf(ls[d]);
+            const float zz = z[(long)q * ad + d];
+            zn[d] = (zz - mu[(long)q * ldmu + d]) / sig[d];
+            lp += -0.5f * zn[d] * zn[d] - ls[d] - 0.9189385332046727f;
+            lp -= __logf(sech2_f(zz) + 1e-6f);
+            ent_h += ls[d] + 0.5f * (1.f + 1.8378770664093453f);
+        }
+        const float ratio = __expf(lp - lp_old[q]);
+        if (!isfinite(ratio)) atomicExch(err, 3);
+        const float adv = sadv[q];
+        const float unc = ratio * adv;
+        const float clp = fminf(fmaxf(ratio, 1.f - clip), 1.f + clip) * adv;
+        loss_rows[q] = (double)(-fminf(unc, clp) * inv_B) - (double)(ent * ent_h * inv_B);
+        const float glp = unc <= clp ? -ratio * adv * inv_B : 0.f;  // losses.cpp:116
+        for (int d = 0; d < ad; ++d) {
+            g[d] = glp * zn[d] / sig[d];
+            const float raw = th[d];
+            lsg[(long)q * ad + d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - ent * inv_B : 0.f;
+        }
+    }
+    const int CT = img_ct(gimg.C);
+    for (int h = 0; h < (ad + 7) / 8; ++h) {
+        uint4 w;
+        w.x = umma::pack_bf16(g[8 * h + 0], g[8 * h + 1]);
+        w.y = umma::pack_bf16(g[8 * h + 2], g[8 * h + 3]);
+        w.z = umma::pack_bf16(g[8 * h + 4], g[8 * h + 5]);
+        w.w = umma::pack_bf16(g[8 * h + 6], g[8 * h + 7]);
+        *reinterpret_cast<uint4*>(gimg.p + img_off(q, 8 * h, CT)) = w;
+    }
+}
+void actor_rows_img(int Bp, int ad, const int* rows, const int* row_group, const float* theta, long P, long mlp_n,
+                    const float* mu, int ldmu, const float* z, const float* lp_old, const float* sadv, float clip,
+                    float ent, float inv_B, const Img& g_out, float* lsg, double* loss_rows, int* err,
+                    cudaStream_t s) {
+    k_actor_rows_img<<<(Bp + 255) / 256, 256, 0, s>>>(Bp, ad, rows, row_group, theta, P, mlp_n, mu, ldmu, z, lp_old,
+                                                      sadv, clip, ent, inv_B, g_out, lsg, loss_rows, err);
+    MB_LAUNCH();
+}
+
+__global__ void k_critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, const float* tgt,
+                                  float inv_B, Img gimg, double* loss_rows) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Bp) return;
+    float g[16];
+    for (int k = 0; k < 16; ++k) g[k] = 0.f;
+    double l = 0.0;
+    if (rows[q] >= 0)
+        for (int k = 0; k < m; ++k) {
+            const float e = v[(long)q * ldv + k] - tgt[(long)q * m + k];
+            l += (double)e * e * inv_B;
+            g[k] = 2.f * e * inv_B;  // losses.cpp:179-181 (no 1/2)
+        }
+    loss_rows[q] = l;
+    const int CT = img_ct(gimg.C);
+    for (int h = 0; h < (m + 7) / 8; ++h) {
+        uint4 w;
+        w.x = umma::pack_bf16(g[8 * h + 0], g[8 * h + 1]);
+        w.y = umma::pack_bf16(g[8 * h + 2], g[8 * h + 3]);
+        w.z = umma::pack_bf16(g[8 * h + 4], g[8 * h + 5]);
+        w.w = umma::pack_bf16(g[8 * h + 6], g[8 * h + 7]);
+        *reinterpret_cast<uint4*>(gimg.p + img_off(q, 8 * h, CT)) = w;
+    }
+}
+void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, const float* tgt, float inv_B,
+                     const Img& g_out, double* loss_rows, cudaStream_t s) {
+    k_critic_rows_img<<<(Bp + 255) / 256, 256, 0, s>>>(Bp, m, rows, v, ldv, tgt, inv_B, g_out, loss_rows);
+    MB_LAUNCH();
+}
+
 // =========================================================================
 // K7: Adam (adam.cpp:8-26), eps after sqrt(v_hat); bias corrections from
 // the host in fp64. Skipped entirely once a numeric error is flagged, so
@@ -688,6 +776,34 @@ void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, floa
         k_adam_tail<<<1, 32, 0, s>>>(n4 * 4, n, p, g, m1, m2, lr, 1.f / bc1, 1.f / bc2, err);
         MB_LAUNCH();
     }
+}
+
+// Adam that also refreshes the bf16 image of the hypernet M block
+// (flat indices [m_lo, m_lo + P*F) -> image (p, f)), used as the operand of
+// the next theta-generation and df GEMMs.
+__global__ void k_adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float ibc1, float ibc2,
+                           const int* err, long m_lo, long m_hi, int F, Img mimg) {
+    if (*err) return;
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float gi = g[i];
+    const float a = 0.9f * m1[i] + 0.1f * gi;
+    const float b = 0.999f * m2[i] + 0.001f * gi * gi;
+    const float pv = p[i] - lr * (a * ibc1) / (sqrtf(b * ibc2) + 1e-8f);
+    m1[i] = a;
+    m2[i] = b;
+    p[i] = pv;
+    if (i >= m_lo && i < m_hi) {
+        const long e = i - m_lo;
+        *reinterpret_cast<__nv_bfloat16*>(mimg.p + img_off(e / F, e % F, img_ct(F))) = __float2bfloat16_rn(pv);
+    }
+}
+void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2, const int* err,
+              long m_lo, int F, const Img& mimg, cudaStream_t s) {
+    const long m_hi = m_lo + (long)mimg.R * F;
+    k_adam_img<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, p, g, m1, m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi,
+                                                          F, mimg);
+    MB_LAUNCH();
 }
 
 // =========================================================================

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "img.cuh"
+
 namespace mb200 {
 
 // ---------------------------------------------------------------- GEMM (SIMT)
@@ -32,12 +34,41 @@ struct GemmDesc {
 };
 void gemm_simt(const GemmDesc& d, cudaStream_t s);
 
-// ---------------------------------------------------------------- tcgen05 GEMM
-// Same GemmDesc contract, on the 5th-gen tensor cores (tc_gemm.cu): bf16
-// operands staged in SMEM, fp32 accumulation in TMEM. Needs a unit stride
-// along K or M (A) and along K or N (B).
-bool gemm_tc_eligible(const GemmDesc& d);
-void gemm_tc(const GemmDesc& d, cudaStream_t s);
+// ---------------------------------------------------------------- tcgen05 GEMM v2
+// D(m,n) = sum_k A(m,k) B(n,k) over tiled bf16 images (img.cuh), operands
+// streamed by the bulk-copy engine (img_gemm.cu). view 0: (row, col) =
+// (m|n, k) K-major; view 1: (row, col) = (k, m|n) MN-major.
+struct IGemm {
+    Img A; int a_view = 0;
+    Img B; int b_view = 0;
+    int M = 0, N = 0, K = 0, Z = 1;
+    const int* goff = nullptr;  // 128-aligned group offsets (gmode 1: rows, 2: K)
+    int gmode = 0, max_group = 0;
+    const float* bias = nullptr; long bias_gs = 0; int bias_mode = 0;  // 1: bias[n], 2: bias[m]
+    int act = 0;                 // 0 none, 1 tanh (C2 <- pre-activation), 2 x *= 1 - aux(m,n)^2
+    Img aux;                     // rows view (row = m, col = n), aux.gs ignored for gmode 1
+    float* C = nullptr; long cm = 0, cn = 0, c_gs = 0;
+    float* C2 = nullptr; long c2m = 0, c2n = 0, c2_gs = 0;
+    int accumulate = 0;
+    Img O; int o_mode = 0;       // 0 none, 1 image (row = m, col = n)
+};
+void img_gemm(const IGemm& d, cudaStream_t s);
+// dst(r, c) <- src[z*src_gs + r*ld + c] for z < G (dst.gs per z)
+void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
+void gather_img(const int* rows, int Bp, const float* src, int width, const Img& dst, cudaStream_t s);
+void gather_pad(const int* rows, int Bp, const float* src, int width, float* dst, cudaStream_t s);
+void img_segcolsum(const Img& x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg, long c0,
+                   cudaStream_t s);
+void segcolsum_f32(const float* x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg,
+                   long c0, cudaStream_t s);
+// per-row loss heads writing the output-layer gradient into an image
+void actor_rows_img(int Bp, int ad, const int* rows, const int* row_group, const float* theta, long P, long mlp_n,
+                    const float* mu, int ldmu, const float* z, const float* lp_old, const float* sadv, float clip,
+                    float ent, float inv_B, const Img& g_out, float* lsg, double* loss_rows, int* err, cudaStream_t s);
+void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, const float* tgt, float inv_B,
+                     const Img& g_out, double* loss_rows, cudaStream_t s);
+void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2, const int* err,
+              long m_lo, int F, const Img& mimg, cudaStream_t s);
 
 // ---------------------------------------------------------------- env (K1)
 void env_reset(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,

@@ -173,12 +173,9 @@ static double gemm_flops(const GemmDesc& d) {
     if (d.gmode == 2) return 2.0 * d.M * d.N * d.K;        // K = total grouped rows
     return 2.0 * d.M * d.N * d.K * d.Z;
 }
-static void gemm(const char* cls, const GemmDesc& d, cudaStream_t s) {
+static void gemm(const char* cls, const GemmDesc& d, cudaStream_t s) {  // tiny feature-map GEMMs
     ProfScope p(cls, gemm_flops(d), 0, s);
-    if (gemm_tc_eligible(d))
-        gemm_tc(d, s);
-    else
-        gemm_simt(d, s);
+    gemm_simt(d, s);
 }
 
 // ------------------------------------------------------------------ HyperNet
@@ -223,12 +220,45 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     for (int z = 0; z <= splits; ++z) bounds[z] = (int)(P * z / splits);
     d_split_bounds = dalloc<int>(splits + 1);
     MB_CUDA(cudaMemcpy(d_split_bounds, bounds.data(), sizeof(int) * (splits + 1), cudaMemcpyHostToDevice));
+    // images (zero-filled: padding stays zero forever)
+    auto mk = [](int R, int C, long gs, int groups) {
+        Img im;
+        im.R = R;
+        im.C = C;
+        im.gs = gs;
+        im.p = dalloc<uint8_t>((size_t)(groups > 1 ? gs * groups : img_bytes(R, C)));
+        return im;
+    };
+    mimg = mk((int)P, F, 0, 1);
+    fimg = mk(G, F, 0, 1);
+    gimg = mk(G, (int)P, 0, 1);
+    wimg_off.clear();
+    long ws = 0;
+    for (int l = 0; l < tgt.L; ++l) {
+        wimg_off.push_back(ws);
+        ws += img_bytes(tgt.sz[l + 1], tgt.sz[l]);
+    }
+    wimg.R = wimg.C = 0;
+    wimg.gs = ws;
+    wimg.p = dalloc<uint8_t>((size_t)ws * G);
+    // 128-aligned K splits of P for the df GEMM (split-K over tcgen05 CTAs)
+    const int kchunks = (int)((P + 127) / 128);
+    splits = std::max(1, std::min(kchunks, 148));
+    std::vector<int> kb(splits + 1);
+    for (int z = 0; z <= splits; ++z) kb[z] = (int)std::min<long>(P, 128L * ((long)kchunks * z / splits));
+    kb[splits] = (int)(((P + 127) / 128) * 128);
+    cudaFree(d_split_bounds);
+    d_split_bounds = dalloc<int>(splits + 1);
+    MB_CUDA(cudaMemcpy(d_split_bounds, kb.data(), sizeof(int) * (splits + 1), cudaMemcpyHostToDevice));
+    cudaFree(parts);
+    parts = dalloc<float>((size_t)splits * G * F);
 }
 
 void HyperNet::free_all() {
     dfree(p); dfree(g); dfree(m1); dfree(m2);
     for (auto& a : fact) dfree(a);
     dfree(fg0); dfree(fg1); dfree(theta); dfree(gtheta); dfree(gf); dfree(parts); dfree(d_split_bounds);
+    dfree(mimg.p); dfree(fimg.p); dfree(gimg.p); dfree(wimg.p);
 }
 
 void HyperNet::init_params(uint64_t key, cudaStream_t s) {  // hypernet.cpp:124-145
@@ -246,10 +276,21 @@ void HyperNet::init_params(uint64_t key, cudaStream_t s) {  // hypernet.cpp:124-
     MB_CUDA(cudaMemsetAsync(m1, 0, n * sizeof(float), s));
     MB_CUDA(cudaMemsetAsync(m2, 0, n * sizeof(float), s));
     steps[0] = steps[1] = steps[2] = 0;
+    to_img(p + nf, F, 0, (int)P, F, mimg, 1, s);
 }
 
-// feature map for all G groups, theta for groups [g0, g0+ng)
+static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
+    const double f = 2.0 * d.M * d.N * d.K * (d.gmode == 0 ? d.Z : 1);
+    ProfScope p(cls, f, 0, s);
+    img_gemm(d, s);
+}
+
+// feature map f(w) for all G groups (SIMT: K = m is tiny), then on the tensor
+// cores theta[g][p] = b[p] + sum_k M[p][k] f[g][k] (hypernet.cpp:73-88) for
+// all groups; [g0, g0+ng) are this rank's clusters.
 void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
+    (void)g0;
+    (void)ng;
     MB_CUDA(cudaMemcpyAsync(fact[0], w, sizeof(float) * G * m, cudaMemcpyDeviceToDevice, s));
     const int Lf = (int)fsz.size() - 1;
     for (int l = 0; l < Lf; ++l) {  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
@@ -260,15 +301,29 @@ void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
         d.M = G; d.N = fsz[l + 1]; d.K = fsz[l];
         d.bias = p + fboff[l]; d.bias_mode = 1;
         d.act = 1;
-        gemm("feature_fwd", d, s);
+        ProfScope ps("feature_fwd", 2.0 * G * fsz[l + 1] * fsz[l], 0, s);
+        gemm_simt(d, s);
     }
-    GemmDesc d;  // theta[g][p] = b[p] + sum_k M[p][k] f[g][k]  (hypernet.cpp:73-88)
-    d.A = fact[Lf] + (long)g0 * F; d.am = F; d.ak = 1;
-    d.B = p + nf; d.bk = 1; d.bn = F;
-    d.C = theta + (long)g0 * P; d.cm = P; d.cn = 1;
-    d.M = ng; d.N = (int)P; d.K = F;
-    d.bias = p + nf + P * F; d.bias_mode = 1;
-    gemm("hyper_theta", d, s);
+    to_img(fact[Lf], F, 0, G, F, fimg, 1, s);
+    IGemm d;
+    d.A = mimg; d.a_view = 0;          // (m = p, k = f)
+    d.B = fimg; d.b_view = 0;          // (n = g, k = f)
+    d.M = (int)P; d.N = G; d.K = F;
+    d.bias = p + nf + P * F; d.bias_mode = 2;
+    d.C = theta; d.cm = 1; d.cn = P;   // theta[g][p]
+    igemm("hyper_theta", d, s);
+}
+
+void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, mimg, 1, s); }
+
+void HyperNet::pack_weights(int g0, int ng, cudaStream_t s) {
+    for (int l = 0; l < tgt.L; ++l) {
+        Img dst = wimg;
+        dst.p = wimg.p + wimg_off[l];
+        dst.R = tgt.sz[l + 1];
+        dst.C = tgt.sz[l];
+        to_img(theta + (long)g0 * P + tgt.woff[l], tgt.sz[l], P, tgt.sz[l + 1], tgt.sz[l], dst, ng, s);
+    }
 }
 
 // hypernet_backward (hypernet.cpp:92-122) summed over all groups:
@@ -278,23 +333,23 @@ void HyperNet::backward(cudaStream_t s) {
     const long nM = P * F;
     colsum_rows(gtheta, G, P, g + nf + nM, s);
     const int Lf = (int)fsz.size() - 1;
+    to_img(gtheta, P, 0, G, (int)P, gimg, 1, s);
     {
-        GemmDesc d;  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
-        d.A = gtheta; d.am = 1; d.ak = P;
-        d.B = fact[Lf]; d.bk = F; d.bn = 1;
-        d.C = g + nf; d.cm = F; d.cn = 1;
+        IGemm d;  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
+        d.A = gimg; d.a_view = 1;  // (m = p, k = g)
+        d.B = fimg; d.b_view = 1;  // (n = f, k = g)
         d.M = (int)P; d.N = F; d.K = G;
-        gemm("hyper_dM", d, s);
+        d.C = g + nf; d.cm = F; d.cn = 1;
+        igemm("hyper_dM", d, s);
     }
     {
-        // gf[g][k] = sum_p gtheta[g][p] M[p][k]: K = P is long -> split-K
-        GemmDesc d;
-        d.A = gtheta; d.am = P; d.ak = 1;
-        d.B = p + nf; d.bk = F; d.bn = 1;
-        d.C = parts; d.cm = F; d.cn = 1; d.c_bz = (long)G * F;
+        IGemm d;  // gf[g][k] = sum_p gtheta[g][p] M[p][k], split-K over 128-aligned P ranges
+        d.A = gimg; d.a_view = 0;  // (m = g, k = p)
+        d.B = mimg; d.b_view = 1;  // (n = f, k = p)
         d.M = G; d.N = F; d.K = (int)P; d.Z = splits;
         d.gmode = 2; d.goff = d_split_bounds;
-        gemm("hyper_df", d, s);
+        d.C = parts; d.cm = F; d.cn = 1; d.c_gs = (long)G * F;
+        igemm("hyper_df", d, s);
         reduce_splits(parts, splits, (long)G * F, gf, s);
     }
     // feature backward: output tanh -> g *= 1 - f^2
@@ -330,8 +385,8 @@ void HyperNet::adam_step(double lr, const int* err, cudaStream_t s) {
     for (long& st : steps) ++st;
     const double bc1 = 1.0 - std::pow(0.9, (double)steps[0]);
     const double bc2 = 1.0 - std::pow(0.999, (double)steps[0]);
-    ProfScope ps("adam", 0, 28.0 * n, s);  // read p,g,m1,m2 + write p,m1,m2 (fp32)
-    adam(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, s);
+    ProfScope ps("adam", 0, 28.0 * n + 2.0 * P * F, s);  // p,g,m1,m2 in; p,m1,m2 out (fp32); M image (bf16)
+    adam_img(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, nf, F, mimg, s);
 }
 
 // ------------------------------------------------------------------ sharding
@@ -359,6 +414,25 @@ void shard_minibatch(const int* perm, int lo, int hi, int T, int inst_lo, int n_
     }
     *n_rows_out = cnt[n_groups];
     *max_group = mx;
+}
+
+// pad every cluster's row range to a multiple of 128 (row id -1 = padding);
+// rewrites goff in place, returns the max padded group size
+int pad_groups(const int* rows, int* goff, int G, int* rows_out, int* n_out) {
+    int q = 0, mx = 0;
+    std::vector<int> og(goff, goff + G + 1);
+    for (int z = 0; z < G; ++z) {
+        const int cnt = og[z + 1] - og[z];
+        const int pc = (cnt + 127) / 128 * 128;
+        goff[z] = q;
+        for (int i = 0; i < cnt; ++i) rows_out[q + i] = rows[og[z] + i];
+        for (int i = cnt; i < pc; ++i) rows_out[q + i] = -1;
+        q += pc;
+        mx = std::max(mx, pc);
+    }
+    goff[G] = q;
+    *n_out = q;
+    return mx;
 }
 
 // ------------------------------------------------------------------ Trainer
@@ -404,10 +478,10 @@ Trainer::~Trainer() {
     actor_.free_all();
     critic_.free_all();
     for (auto* p : {d_obs, d_act, d_lp, d_rew, d_val, d_nval, d_adv, d_tgt, d_sadv, d_state, d_tracker, d_cw,
-                    d_X, d_Z, d_lpo, d_sa, d_tg, d_lsg})
+                    d_Z, d_lpo, d_sa, d_tg, d_lsg})
         if (p) cudaFree(p);
-    for (auto* p : d_A) cudaFree(p);
-    for (auto* p : d_Gz) cudaFree(p);
+    for (auto* p : img_allocs_) cudaFree(p);
+    for (auto& u : ub_) cudaFree(u.Zf);
     for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
                     (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_rowgroup, (void*)d_lossrows,
                     (void*)d_mbloss, (void*)d_stats, (void*)d_scratch, (void*)d_retsum, (void*)d_retcnt,
@@ -450,21 +524,36 @@ void Trainer::alloc() {
     d_rows = dalloc<int>((size_t)slots * Bmax_);
     d_goff = dalloc<int>((size_t)slots * (Kl_ + 1));
     d_rowgroup = dalloc<int>(Bmax_);
-    d_X = dalloc<float>((size_t)Bmax_ * od);
     d_Z = dalloc<float>((size_t)Bmax_ * ad);
     d_lpo = dalloc<float>(Bmax_);
     d_sa = dalloc<float>(Bmax_);
     d_tg = dalloc<float>((size_t)Bmax_ * m);
     d_lsg = dalloc<float>((size_t)Bmax_ * ad);
-    int maxw = 0;
-    for (int l = 1; l <= actor_.tgt.L; ++l) maxw = std::max(maxw, actor_.tgt.sz[l]);
-    for (int l = 1; l <= critic_.tgt.L; ++l) maxw = std::max(maxw, critic_.tgt.sz[l]);
-    const int L = std::max(actor_.tgt.L, critic_.tgt.L);
-    for (int l = 0; l < L; ++l) {
-        d_A.push_back(dalloc<float>((size_t)Bmax_ * maxw));
-        d_Gz.push_back(dalloc<float>((size_t)Bmax_ * maxw));
+    // tcgen05 update path: group-padded (128-aligned) minibatch rows
+    Bpmax_ = ((Bmax_ + 127) / 128 + Kl_) * 128;
+    MB_CUDA(cudaFreeHost(h_rows_pinned));
+    MB_CUDA(cudaMallocHost(&h_rows_pinned, sizeof(int) * (size_t)slots * Bpmax_));
+    cudaFree(d_rows);
+    d_rows = dalloc<int>((size_t)slots * Bpmax_);
+    cudaFree(d_rowgroup);
+    d_rowgroup = dalloc<int>(Bpmax_);
+    for (float** f : {&d_Z, &d_lpo, &d_sa, &d_tg, &d_lsg}) cudaFree(*f);
+    d_Z = dalloc<float>((size_t)Bpmax_ * ad);
+    d_lpo = dalloc<float>(Bpmax_);
+    d_sa = dalloc<float>(Bpmax_);
+    d_tg = dalloc<float>((size_t)Bpmax_ * m);
+    d_lsg = dalloc<float>((size_t)Bpmax_ * ad);
+    Xi_ = new_img(Bpmax_, od);
+    for (int w = 0; w < 2; ++w) {
+        const NetDims& nd = w == 0 ? actor_.tgt : critic_.tgt;
+        for (int l = 0; l < nd.L; ++l) {
+            if (l < nd.L - 1) ub_[w].A.push_back(new_img(Bpmax_, nd.sz[l + 1]));
+            ub_[w].G.push_back(new_img(Bpmax_, nd.sz[l + 1]));
+        }
+        ub_[w].Zf = dalloc<float>((size_t)Bpmax_ * 16);
     }
-    d_lossrows = dalloc<double>(Bmax_);
+    d_lossrows = dalloc<double>(Bpmax_);
+    rows_tmp_.assign((size_t)Bmax_ + 1, 0);
     d_mbloss = dalloc<double>((size_t)slots * 2 + 2);
     d_stats = dalloc<double>(4 * 8);
     d_scratch = dalloc<double>(148 * 2 * 8);
@@ -478,6 +567,15 @@ void Trainer::alloc() {
     mb_B_.assign(slots, 0);
     mb_Bglob_.assign(slots, 0);
     mb_maxg_.assign(slots, 0);
+}
+
+Img Trainer::new_img(int R, int C) {
+    Img im;
+    im.R = R;
+    im.C = C;
+    im.p = dalloc<uint8_t>((size_t)img_bytes(R, C));
+    img_allocs_.push_back(im.p);
+    return im;
 }
 
 void Trainer::phase_rollout(int it) {
@@ -559,16 +657,16 @@ void Trainer::prepare_perms(int it) {
             const int slot = e * mbs + s;
             const int lo = (int)(R * s / mbs), hi = (int)(R * (s + 1) / mbs);  // train.cpp:163-169
             int nrows = 0, mx = 0;
-            shard_minibatch(perm_.data(), lo, hi, cfg_.T, inst_lo_, Nl_, reps_, Kl_,
-                            h_rows_pinned + (size_t)slot * Bmax_, h_goff_pinned + (size_t)slot * (Kl_ + 1),
-                            &nrows, &mx);
-            mb_B_[slot] = nrows;
+            int* goff = h_goff_pinned + (size_t)slot * (Kl_ + 1);
+            shard_minibatch(perm_.data(), lo, hi, cfg_.T, inst_lo_, Nl_, reps_, Kl_, rows_tmp_.data(), goff, &nrows,
+                            &mx);
             mb_Bglob_[slot] = hi - lo;
-            mb_maxg_[slot] = mx;
+            mb_maxg_[slot] = pad_groups(rows_tmp_.data(), goff, Kl_, h_rows_pinned + (size_t)slot * Bpmax_,
+                                        &mb_B_[slot]);
         }
     }
     const int slots = cfg_.epochs * mbs;
-    MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (size_t)slots * Bmax_, cudaMemcpyHostToDevice, s_));
+    MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (size_t)slots * Bpmax_, cudaMemcpyHostToDevice, s_));
     MB_CUDA(cudaMemcpyAsync(d_goff, h_goff_pinned, sizeof(int) * (size_t)slots * (Kl_ + 1), cudaMemcpyHostToDevice,
                             s_));
 }
@@ -597,82 +695,99 @@ void Trainer::phase_advantages() {
     launches_ += 8;
 }
 
-void Trainer::net_step(HyperNet& h, bool is_actor, int B, float inv_B, int maxg, const int* goff, int slot) {
+// One net's loss + backward through its generated weights on one minibatch
+// (losses.cpp:46-189), every contraction on the tensor cores over bf16
+// images: forward Z_l = A_{l-1} W_l^T (grouped rows), per-row loss head,
+// dW_l = G_l^T A_{l-1} (K = the cluster's rows), dX = (G_l W_l) * tanh'.
+// Leaves gtheta [local clusters][P] (fp32, reference flat layout) complete.
+void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg, const int* rows, const int* goff,
+                       int slot) {
     const NetDims& nd = h.tgt;
     const int L = nd.L;
-    const float* th = h.theta + (long)g_lo_ * h.P;
+    UpdBufs& u = ub_[is_actor ? 0 : 1];
     float* gth = h.gtheta + (long)g_lo_ * h.P;
-    if (B == 0) {
+    if (Bp == 0) {
         MB_CUDA(cudaMemsetAsync(gth, 0, sizeof(float) * Kl_ * h.P, s_));
         MB_CUDA(cudaMemsetAsync(d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, sizeof(double), s_));
         return;
     }
-    // forward: grouped NT GEMMs with the cluster's generated weights
-    for (int l = 0; l < L; ++l) {
+    const float* th = h.theta + (long)g_lo_ * h.P;
+    {
+        ProfScope ps("pack_weights", 0, 6.0 * Kl_ * nd.mlp_n, s_);
+        h.pack_weights(g_lo_, Kl_, s_);
+    }
+    auto wl = [&](int l) {
+        Img w = h.wimg;
+        w.p = h.wimg.p + h.wimg_off[l];
+        w.R = nd.sz[l + 1];
+        w.C = nd.sz[l];
+        return w;
+    };
+    for (int l = 0; l < L; ++l) {  // forward
         const bool last = (l == L - 1);
-        GemmDesc d;
-        d.A = l == 0 ? d_X : d_A[l - 1]; d.am = nd.sz[l]; d.ak = 1;
-        d.B = th + nd.woff[l]; d.bk = 1; d.bn = nd.sz[l]; d.b_bz = h.P;
-        d.C = d_A[l]; d.cm = nd.sz[l + 1]; d.cn = 1;
-        d.M = B; d.N = nd.sz[l + 1]; d.K = nd.sz[l]; d.Z = Kl_;
+        IGemm d;
+        d.A = l == 0 ? Xi_ : u.A[l - 1]; d.a_view = 0;  // (m = row, k = in)
+        d.B = wl(l); d.b_view = 0;                     // (n = out, k = in)
+        d.M = Bp; d.N = nd.sz[l + 1]; d.K = nd.sz[l]; d.Z = Kl_;
         d.gmode = 1; d.goff = goff; d.max_group = maxg;
-        d.bias = th + nd.boff[l]; d.bias_bz = h.P; d.bias_mode = 1;
-        d.act = last ? 0 : 1;
-        gemm("mlp_fwd", d, s_);
+        d.bias = th + nd.boff[l]; d.bias_gs = h.P; d.bias_mode = 1;
+        if (last) {
+            d.C = u.Zf; d.cm = 16; d.cn = 1;  // Gaussian mean / values (pre-activation)
+        } else {
+            d.act = 1; d.O = u.A[l]; d.o_mode = 1;
+        }
+        igemm("mlp_fwd", d, s_);
     }
-    float* gout = d_Gz[L - 1];
     if (is_actor) {  // losses.cpp:87-129
-        actor_rows(B, es_.act_dim, d_rowgroup, h.theta + (long)g_lo_ * h.P, h.P, nd.mlp_n, d_A[L - 1], d_Z, d_lpo,
-                   d_sa, (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, gout, d_lsg, d_lossrows, d_err, s_);
-        segmented_colsum(d_lsg, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.P, 0, s_);
+        actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, th, h.P, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
+                       (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], d_lsg, d_lossrows, d_err, s_);
+        segcolsum_f32(d_lsg, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.P, Img{}, 0, s_);
     } else {  // losses.cpp:170-185
-        critic_rows(B, es_.m, d_A[L - 1], d_tg, inv_B, gout, d_lossrows, s_);
+        critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], d_lossrows, s_);
     }
-    sum_f64(d_lossrows, B, d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, s_);
-    // backward (nn.cpp:111-160) with per-cluster weight gradients
-    for (int l = L - 1; l >= 0; --l) {
-        const float* gz = d_Gz[l];
-        const float* ain = l == 0 ? d_X : d_A[l - 1];
-        GemmDesc d;  // dW_l[g][j][i] = sum_{q in g} gz[q][j] ain[q][i]
-        d.A = gz; d.am = 1; d.ak = nd.sz[l + 1];
-        d.B = ain; d.bk = nd.sz[l]; d.bn = 1;
-        d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_bz = h.P;
-        d.M = nd.sz[l + 1]; d.N = nd.sz[l]; d.K = B; d.Z = Kl_;
+    sum_f64(d_lossrows, Bp, d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, s_);
+    for (int l = L - 1; l >= 0; --l) {  // backward (nn.cpp:111-160)
+        const Img& ain = l == 0 ? Xi_ : u.A[l - 1];
+        IGemm d;  // dW_l[z][j][i] = sum_{q in z} G_l[q][j] A_{l-1}[q][i]
+        d.A = u.G[l]; d.a_view = 1;  // (m = j, k = q)
+        d.B = ain; d.b_view = 1;     // (n = i, k = q)
+        d.M = nd.sz[l + 1]; d.N = nd.sz[l]; d.K = Bp; d.Z = Kl_;
         d.gmode = 2; d.goff = goff;
-        gemm("mlp_dW", d, s_);
-        segmented_colsum(gz, nd.sz[l + 1], goff, Kl_, gth + nd.boff[l], h.P, 0, s_);
+        d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = h.P;
+        igemm("mlp_dW", d, s_);
+        img_segcolsum(u.G[l], nd.sz[l + 1], goff, Kl_, gth + nd.boff[l], h.P, Img{}, 0, s_);
         if (l > 0) {
-            GemmDesc e;  // gz_{l-1}[q][i] = (sum_j gz[q][j] W_l[g][j][i]) (1 - a[q][i]^2)
-            e.A = gz; e.am = nd.sz[l + 1]; e.ak = 1;
-            e.B = th + nd.woff[l]; e.bk = nd.sz[l]; e.bn = 1; e.b_bz = h.P;
-            e.C = d_Gz[l - 1]; e.cm = nd.sz[l]; e.cn = 1;
-            e.M = B; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
+            IGemm e;  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
+            e.A = u.G[l]; e.a_view = 0;  // (m = q, k = j)
+            e.B = wl(l); e.b_view = 1;   // (n = i, k = j)
+            e.M = Bp; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
             e.gmode = 1; e.goff = goff; e.max_group = maxg;
-            e.act = 2; e.aux = d_A[l - 1]; e.xm = nd.sz[l]; e.xn = 1;
-            gemm("mlp_dX", e, s_);
+            e.act = 2; e.aux = u.A[l - 1];
+            e.O = u.G[l - 1]; e.o_mode = 1;
+            igemm("mlp_dX", e, s_);
         }
     }
-    launches_ += 3 * L + 4;
+    launches_ += 4 * L + 5;
 }
 
 void Trainer::allgather_gtheta(HyperNet& h) {
     if (comm_) comm_allgather_f32(comm_, h.gtheta, (size_t)Kl_ * h.P, s_);
 }
 
-void Trainer::minibatch(int slot, int B, int Bglob, int maxg, const int* rows, const int* goff) {
+void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, const int* goff) {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
-    if (B > 0) {
-        gather_rows(rows, B, d_obs, od, d_X, s_);
-        gather_rows(rows, B, d_act, ad, d_Z, s_);
-        gather_rows(rows, B, d_lp, 1, d_lpo, s_);
-        gather_rows(rows, B, d_sadv, 1, d_sa, s_);
-        gather_rows(rows, B, d_tgt, m, d_tg, s_);
-        fill_row_group(goff, Kl_, d_rowgroup, B, s_);
+    if (Bp > 0) {
+        gather_img(rows, Bp, d_obs, od, Xi_, s_);
+        gather_pad(rows, Bp, d_act, ad, d_Z, s_);
+        gather_pad(rows, Bp, d_lp, 1, d_lpo, s_);
+        gather_pad(rows, Bp, d_sadv, 1, d_sa, s_);
+        gather_pad(rows, Bp, d_tgt, m, d_tg, s_);
+        fill_row_group(goff, Kl_, d_rowgroup, Bp, s_);
         launches_ += 6;
     }
-    net_step(actor_, true, B, inv_B, maxg, goff, slot);
-    net_step(critic_, false, B, inv_B, maxg, goff, slot);
+    net_step(actor_, true, Bp, inv_B, maxg, rows, goff, slot);
+    net_step(critic_, false, Bp, inv_B, maxg, rows, goff, slot);
     allgather_gtheta(actor_);
     allgather_gtheta(critic_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
@@ -681,7 +796,7 @@ void Trainer::minibatch(int slot, int B, int Bglob, int maxg, const int* rows, c
     critic_.backward(s_);
     actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180: actor then critic
     critic_.adam_step(cfg_.critic_lr, d_err, s_);
-    launches_ += 2 * (8 + 4 * (int)actor_.fsz.size()) + 3;
+    launches_ += 2 * (10 + 4 * (int)actor_.fsz.size()) + 3;
 }
 
 void Trainer::phase_update(int it, int max_minibatches) {
@@ -697,7 +812,7 @@ void Trainer::phase_update(int it, int max_minibatches) {
             if (mb_Bglob_[slot] == 0) continue;  // lo == hi
             actor_.forward(d_cw, g_lo_, Kl_, s_);  // hypernet_forward per loss (losses.cpp:79,167)
             critic_.forward(d_cw, g_lo_, Kl_, s_);
-            minibatch(slot, mb_B_[slot], mb_Bglob_[slot], mb_maxg_[slot], d_rows + (size_t)slot * Bmax_,
+            minibatch(slot, mb_B_[slot], mb_Bglob_[slot], mb_maxg_[slot], d_rows + (size_t)slot * Bpmax_,
                       d_goff + (size_t)slot * (Kl_ + 1));
             ++mb_done_;
         }
@@ -752,25 +867,26 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
     if (n > Bmax_) throw ShapeError("losses_only: more rows than one minibatch buffer holds");
     for (int q = 0; q < n; ++q)
         if (rows[q] < 0 || rows[q] >= cfg_.N * cfg_.T) throw ShapeError("minibatch row index out of range");
-    int B = 0, mx = 0;
-    shard_minibatch(rows, 0, n, cfg_.T, inst_lo_, Nl_, reps_, Kl_, h_rows_pinned, h_goff_pinned, &B, &mx);
-    MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (B ? B : 1), cudaMemcpyHostToDevice, s_));
+    int B = 0, mx = 0, Bp = 0;
+    shard_minibatch(rows, 0, n, cfg_.T, inst_lo_, Nl_, reps_, Kl_, rows_tmp_.data(), h_goff_pinned, &B, &mx);
+    mx = pad_groups(rows_tmp_.data(), h_goff_pinned, Kl_, h_rows_pinned, &Bp);
+    MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (Bp ? Bp : 1), cudaMemcpyHostToDevice, s_));
     MB_CUDA(cudaMemcpyAsync(d_goff, h_goff_pinned, sizeof(int) * (Kl_ + 1), cudaMemcpyHostToDevice, s_));
     MB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s_));
     actor_.forward(d_cw, g_lo_, Kl_, s_);
     critic_.forward(d_cw, g_lo_, Kl_, s_);
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)n);
-    if (B > 0) {
-        gather_rows(d_rows, B, d_obs, od, d_X, s_);
-        gather_rows(d_rows, B, d_act, ad, d_Z, s_);
-        gather_rows(d_rows, B, d_lp, 1, d_lpo, s_);
-        gather_rows(d_rows, B, d_sadv, 1, d_sa, s_);
-        gather_rows(d_rows, B, d_tgt, m, d_tg, s_);
-        fill_row_group(d_goff, Kl_, d_rowgroup, B, s_);
+    if (Bp > 0) {
+        gather_img(d_rows, Bp, d_obs, od, Xi_, s_);
+        gather_pad(d_rows, Bp, d_act, ad, d_Z, s_);
+        gather_pad(d_rows, Bp, d_lp, 1, d_lpo, s_);
+        gather_pad(d_rows, Bp, d_sadv, 1, d_sa, s_);
+        gather_pad(d_rows, Bp, d_tgt, m, d_tg, s_);
+        fill_row_group(d_goff, Kl_, d_rowgroup, Bp, s_);
     }
-    net_step(actor_, true, B, inv_B, mx, d_goff, 0);
-    net_step(critic_, false, B, inv_B, mx, d_goff, 0);
+    net_step(actor_, true, Bp, inv_B, mx, d_rows, d_goff, 0);
+    net_step(critic_, false, Bp, inv_B, mx, d_rows, d_goff, 0);
     allgather_gtheta(actor_);
     allgather_gtheta(critic_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss, 2, s_);

@@ -67,6 +67,14 @@ struct HyperNet {
     float *fg0 = nullptr, *fg1 = nullptr;
     int splits = 1;
     int* d_split_bounds = nullptr;
+    // bf16 tiled images (img.cuh) feeding the tcgen05 GEMMs
+    Img mimg;                    // M [P][F]      (refreshed by Adam)
+    Img fimg;                    // f(w) [G][F]
+    Img gimg;                    // gtheta [G][P]
+    Img wimg;                    // generated weights, per group (wimg.gs): layer l at wimg_off[l]
+    std::vector<long> wimg_off;
+    void pack_weights(int g0, int ng, cudaStream_t s);  // theta -> wimg for groups [g0, g0+ng)
+    void refresh_images(cudaStream_t s);                 // p (M block) -> mimg after external loads
 
     void init(int m_, int F_, const std::vector<int>& fh, const std::vector<int>& target_sizes,
               bool out_tanh, bool has_log_std, int G_);
@@ -94,6 +102,7 @@ struct IterStats {
 // ids and stably grouped by cluster (losses.cpp:21-33 ordering).
 void shard_minibatch(const int* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps,
                      int n_groups, int* rows_out, int* goff_out, int* n_rows_out, int* max_group);
+int pad_groups(const int* rows, int* goff, int G, int* rows_out, int* n_out);
 
 class Trainer {
 public:
@@ -138,7 +147,8 @@ private:
     void alloc();
     void prepare_perms(int it);
     void minibatch(int slot, int B, int Bglob, int maxg, const int* d_rows, const int* d_goff);
-    void net_step(HyperNet& h, bool actor, int B, float inv_B, int maxg, const int* d_goff, int slot);
+    void net_step(HyperNet& h, bool actor, int Bp, float inv_B, int maxg, const int* rows, const int* d_goff,
+                  int slot);
     void allgather_gtheta(HyperNet& h);
 
     TrainConfig cfg_;
@@ -158,11 +168,18 @@ private:
     int* h_goff_pinned = nullptr;  // [epochs*mbs][Kl+1]
     int *d_rows = nullptr, *d_goff = nullptr, *d_rowgroup = nullptr;
     std::vector<int> mb_B_, mb_Bglob_, mb_maxg_;
-    int Bmax_ = 0;
+    int Bmax_ = 0, Bpmax_ = 0;  // real / group-padded (128-aligned) rows per minibatch
+    struct UpdBufs {            // per-net tcgen05 update buffers
+        std::vector<Img> A;     // [Bp][h_l] hidden activations (post-tanh)
+        std::vector<Img> G;     // [Bp][out_l] gradient at the pre-activation of layer l
+        float* Zf = nullptr;    // [Bp][16] output layer (policy mean / values), fp32
+    } ub_[2];
+    Img Xi_;                    // [Bp][obs] gathered observations (bf16 image)
+    std::vector<uint8_t*> img_allocs_;
+    std::vector<int> rows_tmp_;
+    Img new_img(int R, int C);
     // update buffers
-    float *d_X = nullptr, *d_Z = nullptr, *d_lpo = nullptr, *d_sa = nullptr, *d_tg = nullptr;
-    std::vector<float*> d_A;   // activations per layer (max width)
-    std::vector<float*> d_Gz;  // gradients per layer
+    float *d_Z = nullptr, *d_lpo = nullptr, *d_sa = nullptr, *d_tg = nullptr;
     float *d_lsg = nullptr;
     double *d_lossrows = nullptr, *d_mbloss = nullptr, *d_stats = nullptr, *d_scratch = nullptr;
     double* d_retsum = nullptr;
