@@ -1,17 +1,19 @@
-// tcgen05 GEMM v2: D(m, n) = sum_k A(m, k) B(n, k) over tiled bf16 images
-// (img.cuh), every operand chunk brought in by the TMA bulk-copy engine.
+// tcgen05 GEMM v3: D(m, n) = sum_k A(m, k) B(n, k) over tiled bf16 images
+// (img.cuh). Persistent, warp-specialised, double-buffered accumulators:
 //
-//   * CTA tile 128 x BN (BN <= 256), K in chunks of 128, S-stage smem ring;
-//   * thread 0 = producer: cp.async.bulk of the A chunk and the B chunk(s)
-//     of K-chunk kc into stage kc % S, completion on full[s] (expect_tx);
-//   * thread 32 = MMA issuer: waits full[s], issues 8 x (K = 16)
-//     tcgen05.mma per B chunk, tcgen05.commit -> empty[s] frees the stage,
-//     a final commit -> done;
-//   * all 8 warps: epilogue from TMEM (32 lanes x 16 columns per tcgen05.ld)
-//     with bias / tanh / tanh-derivative (aux image) / accumulate, writing
-//     fp32 (strided) and/or a bf16 image (for the next GEMM).
-// Grouped modes: gmode 1 = rows grouped (A rows and output rows start at
-// goff[z], 128-aligned; B / bias per group), gmode 2 = K grouped (K range
+//   * grid = min(#tiles, #SMs); each CTA walks output tiles (128 x BN)
+//     round-robin (tile order: N fastest, then M, then group z);
+//   * warp 0 / lane 0 = producer: cp.async.bulk of the A chunk and B
+//     chunk(s) of every 128-wide K chunk into an S-stage smem ring
+//     (full[s] expect_tx, empty[s] released by tcgen05.commit);
+//   * warp 1 / lane 0 = MMA issuer: 8 x (K = 16) tcgen05.mma per B chunk
+//     into TMEM accumulator buffer (tile & 1); tcgen05.commit -> tfull;
+//   * warps 4..7 = epilogue (TMEM lanes 32*(w-4)..): tcgen05.ld 16 columns at
+//     a time, fused bias / tanh / tanh' / fp32 + bf16-image stores, then
+//     arrive tempty so the MMA warp can reuse the buffer -- the epilogue of
+//     tile i overlaps the loads and MMAs of tile i+1.
+// Grouped modes: gmode 1 = rows grouped (A/output rows start at goff[z],
+// 128-aligned; B / bias per group), gmode 2 = K grouped (K range
 // [goff[z], goff[z+1]), 128-aligned; output per group).
 #include "common.cuh"
 #include "img.cuh"
@@ -23,14 +25,17 @@ namespace mb200 {
 namespace {
 constexpr int NT = 256;
 constexpr int CHUNK = 32768;
+constexpr int EPI_WARP0 = 4;
 
 template <int BN>
 struct Cfg {
-    static constexpr int NB = BN > 128 ? 2 : 1;          // B chunks per stage
-    static constexpr int STAGES = BN > 128 ? 2 : 3;
+    static constexpr int NB = BN > 128 ? 2 : 1;      // B chunks per stage
     static constexpr int STAGE = CHUNK * (1 + NB);
-    static constexpr int SMEM = STAGES * STAGE + 256;
-    static constexpr int NMMA = BN > 128 ? 128 : BN;      // N per MMA instruction
+    static constexpr int STAGES = BN > 128 ? 2 : 3;
+    static constexpr int NMMA = BN > 128 ? 128 : BN;  // N per MMA instruction
+    static constexpr int ACC = BN < 32 ? 32 : BN;     // TMEM columns per accumulator buffer
+    static constexpr int TCOLS = 2 * ACC;             // double buffered (<= 512)
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 4 * BN;
 };
 
 __device__ __forceinline__ long chunk_index(int view, int mt, int kc, int CT) {
@@ -38,52 +43,56 @@ __device__ __forceinline__ long chunk_index(int view, int mt, int kc, int CT) {
     return view == 0 ? (long)mt * CT + kc : (long)kc * CT + mt;
 }
 
-template <int BN>
-__global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d) {
+struct TileInfo {
+    int z, m0, n0, m_hi, k_lo, nk;
+    bool valid;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const IGemm& d, int t, int ntn, int ntm) {
+    TileInfo ti;
+    const int x = t % ntn, y = (t / ntn) % ntm;
+    ti.z = t / (ntn * ntm);
+    int m_lo = 0, m_hi = d.M, k_lo = 0, k_hi = d.K;
+    if (d.gmode == 1) {
+        m_lo = d.goff[ti.z];
+        m_hi = d.goff[ti.z + 1];
+    } else if (d.gmode == 2) {
+        k_lo = d.goff[ti.z];
+        k_hi = d.goff[ti.z + 1];
+    }
+    ti.m0 = m_lo + y * 128;
+    ti.n0 = x * (d.N_tile);
+    ti.m_hi = m_hi;
+    ti.k_lo = k_lo;
+    ti.nk = (k_hi - k_lo + 127) >> 7;
+    ti.valid = ti.m0 < m_hi;
+    return ti;
+}
+
+// EPI: 0 = fp32 out (bias optional), 1 = tanh -> image (+ optional fp32 pre-act),
+//      2 = tanh' (aux image) -> image
+template <int BN, int EPI>
+__global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn, int ntm) {
     using C = Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
     uint64_t* empty = full + C::STAGES;
-    uint64_t* done = empty + C::STAGES;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = empty + C::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* sbias = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 1024);  // [BN]
 
-    const int z = blockIdx.z;
-    int m_lo = 0, m_hi = d.M, k_lo = 0, k_hi = d.K;
-    const uint8_t* Ab = d.A.p;
-    const uint8_t* Bb = d.B.p;
-    const float* bias = d.bias;
-    long cz = 0, oz = 0;
-    if (d.gmode == 0) {
-        Ab += z * d.A.gs;
-        Bb += z * d.B.gs;
-        if (bias) bias += z * d.bias_gs;
-        cz = z;
-    } else if (d.gmode == 1) {
-        m_lo = d.goff[z];
-        m_hi = d.goff[z + 1];
-        Bb += z * d.B.gs;
-        if (bias) bias += z * d.bias_gs;
-    } else {
-        k_lo = d.goff[z];
-        k_hi = d.goff[z + 1];
-        cz = z;
-    }
-    oz = z;
-    const int m0 = m_lo + blockIdx.y * 128;
-    const int n0 = blockIdx.x * BN;
-    if (m0 >= m_hi || n0 >= d.N) return;
-    const int nk = (k_hi - k_lo + 127) >> 7;
-    const int kc0 = k_lo >> 7;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t kCols = BN < 32 ? 32 : BN;
-
-    if (warp == 0) umma::tmem_alloc(tslot, kCols);
+    if (warp == 0) umma::tmem_alloc(tslot, C::TCOLS);
     if (threadIdx.x == 32) {
         for (int s = 0; s < C::STAGES; ++s) {
             umma::mbar_init(&full[s], 1);
             umma::mbar_init(&empty[s], 1);
         }
-        umma::mbar_init(done, 1);
+        for (int b = 0; b < 2; ++b) {
+            umma::mbar_init(&tfull[b], 1);
+            umma::mbar_init(&tempty[b], 128);
+        }
         umma::fence_barrier_init();
     }
     umma::fence_before_sync();
@@ -91,146 +100,202 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d) {
     umma::fence_after_sync();
     const uint32_t tbase = *tslot;
     const int CTa = img_ct(d.A.C), CTb = img_ct(d.B.C);
-    const int mt = m0 >> 7;
-    const int nt0 = n0 >> 7;
 
-    if (threadIdx.x == 0) {  // ---------------- producer
-        // B bytes per chunk: a row-view operand narrower than 128 only needs
-        // the first BN/8 row blocks of its chunk
-        const uint32_t bbytes = (d.b_view == 0 && BN < 128) ? (uint32_t)BN * 256 : (uint32_t)CHUNK;
-        for (int kc = 0; kc < nk; ++kc) {
-            const int s = kc % C::STAGES;
-            if (kc >= C::STAGES) umma::mbar_wait(&empty[s], ((kc / C::STAGES) - 1) & 1);
-            uint8_t* st = smem + s * C::STAGE;
-            umma::mbar_arrive_expect_tx(&full[s], CHUNK + C::NB * bbytes);
-            umma::bulk_g2s(st, Ab + chunk_index(d.a_view, mt, kc0 + kc, CTa) * CHUNK, CHUNK, &full[s]);
-            for (int j = 0; j < C::NB; ++j)
-                umma::bulk_g2s(st + CHUNK * (1 + j), Bb + chunk_index(d.b_view, nt0 + j, kc0 + kc, CTb) * CHUNK,
-                               bbytes, &full[s]);
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- producer
+            const uint32_t bbytes = (d.b_view == 0 && BN < 128) ? (uint32_t)BN * 256 : (uint32_t)CHUNK;
+            long g = 0;  // global chunk counter
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const TileInfo ti = tile_info(d, t, ntn, ntm);
+                if (!ti.valid) continue;
+                const uint8_t* Ab = d.A.p + (d.gmode == 0 ? ti.z * d.A.gs : 0);
+                const uint8_t* Bb = d.B.p + (d.gmode != 2 ? ti.z * d.B.gs : 0);
+                const int mt = ti.m0 >> 7, nt0 = ti.n0 >> 7, kc0 = ti.k_lo >> 7;
+                for (int kc = 0; kc < ti.nk; ++kc, ++g) {
+                    const int s = (int)(g % C::STAGES);
+                    umma::mbar_wait(&empty[s], (uint32_t)(((g / C::STAGES) & 1) ^ 1));
+                    uint8_t* st = smem + s * C::STAGE;
+                    umma::mbar_arrive_expect_tx(&full[s], CHUNK + C::NB * bbytes);
+                    umma::bulk_g2s(st, Ab + chunk_index(d.a_view, mt, kc0 + kc, CTa) * CHUNK, CHUNK, &full[s]);
+#pragma unroll
+                    for (int j = 0; j < C::NB; ++j)
+                        umma::bulk_g2s(st + CHUNK * (1 + j),
+                                       Bb + chunk_index(d.b_view, nt0 + j, kc0 + kc, CTb) * CHUNK, bbytes, &full[s]);
+                }
+            }
         }
-    } else if (threadIdx.x == 32) {  // ---------------- MMA issuer
-        const uint32_t idesc = umma::idesc_bf16(128, C::NMMA, d.a_view == 1, d.b_view == 1);
-        const uint32_t a_lbo = d.a_view ? 2048 : 128, a_sbo = d.a_view ? 128 : 2048, a_step = d.a_view ? 4096 : 256;
-        const uint32_t b_lbo = d.b_view ? 2048 : 128, b_sbo = d.b_view ? 128 : 2048, b_step = d.b_view ? 4096 : 256;
-        for (int kc = 0; kc < nk; ++kc) {
-            const int s = kc % C::STAGES;
-            umma::mbar_wait(&full[s], (kc / C::STAGES) & 1);
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            const uint32_t idesc = umma::idesc_bf16(128, C::NMMA, d.a_view == 1, d.b_view == 1);
+            const uint32_t a_lbo = d.a_view ? 2048 : 128, a_sbo = d.a_view ? 128 : 2048;
+            const uint32_t a_step = d.a_view ? 4096 : 256;
+            const uint32_t b_lbo = d.b_view ? 2048 : 128, b_sbo = d.b_view ? 128 : 2048;
+            const uint32_t b_step = d.b_view ? 4096 : 256;
+            long g = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const TileInfo ti = tile_info(d, t, ntn, ntm);
+                if (!ti.valid) continue;
+                const int acc = it & 1;
+                umma::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
+                umma::fence_after_sync();
+                const uint32_t dcol = tbase + (uint32_t)(acc * C::ACC);
+                for (int kc = 0; kc < ti.nk; ++kc, ++g) {
+                    const int s = (int)(g % C::STAGES);
+                    umma::mbar_wait(&full[s], (uint32_t)((g / C::STAGES) & 1));
+                    umma::fence_after_sync();
+                    const uint32_t a0 = umma::smem_u32(smem + s * C::STAGE);
+#pragma unroll
+                    for (int j = 0; j < C::NB; ++j) {
+                        const uint32_t b0 = a0 + CHUNK * (1 + j);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)
+                            umma::mma_bf16(dcol + j * 128, umma::smem_desc(a0 + kk * a_step, a_lbo, a_sbo),
+                                           umma::smem_desc(b0 + kk * b_step, b_lbo, b_sbo), idesc,
+                                           (kc | kk) ? 1u : 0u);
+                    }
+                    umma::commit(&empty[s]);
+                }
+                umma::commit(&tfull[acc]);
+                ++it;
+            }
+        }
+        __syncwarp();
+    } else if (warp >= EPI_WARP0) {  // ---------------- epilogue
+        const int lg = warp - EPI_WARP0;
+        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..127
+        int it = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const TileInfo ti = tile_info(d, t, ntn, ntm);
+            if (!ti.valid) continue;
+            const int acc = it & 1;
+            const float* bias = d.bias ? d.bias + (d.gmode != 2 ? ti.z * d.bias_gs : 0) : nullptr;
+            // stage the tile's per-n bias in smem (previous tile's readers are done:
+            // they arrived on tempty before this loop iteration's named barrier)
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (d.bias_mode == 1)
+                for (int j = et; j < BN; j += 128) sbias[j] = (ti.n0 + j < d.N) ? bias[ti.n0 + j] : 0.f;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));  // committed even when nk == 0
             umma::fence_after_sync();
-            const uint32_t a0 = umma::smem_u32(smem + s * C::STAGE);
+            const int m = ti.m0 + lg * 32 + lane;
+            const bool mrow = m < ti.m_hi;
+            const float bm = (d.bias_mode == 2 && mrow) ? bias[m] : 0.f;
+            const long cz = d.gmode == 1 ? 0 : ti.z;
+            float* crow = d.C ? d.C + cz * d.c_gs + (long)m * d.cm : nullptr;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                float v[16];
+                if (ti.nk > 0) {
+                    umma::tmem_ld16(tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * C::ACC + c0), v);
+                } else {
 #pragma unroll
-            for (int j = 0; j < C::NB; ++j) {
-                const uint32_t b0 = a0 + CHUNK * (1 + j);
+                    for (int i = 0; i < 16; ++i) v[i] = 0.f;
+                }
+                const int nb = ti.n0 + c0;
+                if (!mrow || nb >= d.N) continue;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    umma::mma_bf16(tbase + j * 128, umma::smem_desc(a0 + kk * a_step, a_lbo, a_sbo),
-                                   umma::smem_desc(b0 + kk * b_step, b_lbo, b_sbo), idesc, (kc | kk) ? 1u : 0u);
-            }
-            umma::commit(&empty[s]);
-        }
-        umma::commit(done);
-    }
-    __syncwarp();
-    // ---------------- epilogue (all warps)
-    if (nk > 0) umma::mbar_wait(done, 0);
-    umma::fence_after_sync();
-    const int lg = warp & 3, half = warp >> 2;
-    const int m = m0 + lg * 32 + lane;
-    constexpr int HALF = BN >= 32 ? BN / 2 : BN;
-    const bool active = BN >= 32 || half == 0;
-    const int CTo = img_ct(d.O.C), CTx = img_ct(d.aux.C);
-    if (active) {
-        for (int c0 = half * HALF; c0 < half * HALF + HALF; c0 += 16) {
-            float v[16];
-            if (nk > 0) {
-                umma::tmem_ld16(tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)c0, v);
-            } else {
+                for (int i = 0; i < 16; ++i) v[i] += (d.bias_mode == 1 ? sbias[c0 + i] : bm);
+                if (EPI == 0) {
+                    if (d.accumulate)
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = 0.f;
-            }
-            if (m >= m_hi) continue;
-            const int nb = n0 + c0;
-            // aux (tanh-derivative) values for these 16 columns
-            float ax[16];
-            if (d.act == 2) {
+                        for (int i = 0; i < 16; ++i)
+                            if (nb + i < d.N) v[i] += crow[(long)(nb + i) * d.cn];
+                    if (d.cn == 1 && nb + 16 <= d.N && ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0)) {
+                        float4* q = reinterpret_cast<float4*>(crow + nb);
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint8_t* ap = d.aux.p + oz * d.aux.gs + img_off(m, nb + 8 * h, CTx);
-                    const uint4 q = *reinterpret_cast<const uint4*>(ap);
-                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+                        for (int h = 0; h < 4; ++h) q[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+                    } else {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f = __bfloat1622float2(b2[e]);
-                        ax[8 * h + 2 * e] = f.x;
-                        ax[8 * h + 2 * e + 1] = f.y;
+                        for (int i = 0; i < 16; ++i)
+                            if (nb + i < d.N) crow[(long)(nb + i) * d.cn] = v[i];
+                    }
+                } else {
+                    if (EPI == 1) {
+                        if (d.C2)
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (nb + i < d.N) d.C2[(long)m * d.c2m + (long)(nb + i) * d.c2n] = v[i];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = tanhf(v[i]);
+                    } else {
+                        const int CTx = img_ct(d.aux.C);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint4 q = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb + 8 * h, CTx));
+                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float2 f = __bfloat1622float2(b2[e]);
+                                v[8 * h + 2 * e] *= 1.f - f.x * f.x;
+                                v[8 * h + 2 * e + 1] *= 1.f - f.y * f.y;
+                            }
+                        }
+                    }
+                    const int CTo = img_ct(d.O.C);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (nb + 8 * h >= d.N) continue;
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            if (nb + 8 * h + e >= d.N) v[8 * h + e] = 0.f;  // keep padding zero
+                        uint4 q;
+                        q.x = umma::pack_bf16(v[8 * h + 0], v[8 * h + 1]);
+                        q.y = umma::pack_bf16(v[8 * h + 2], v[8 * h + 3]);
+                        q.z = umma::pack_bf16(v[8 * h + 4], v[8 * h + 5]);
+                        q.w = umma::pack_bf16(v[8 * h + 6], v[8 * h + 7]);
+                        *reinterpret_cast<uint4*>(d.O.p + img_off(m, nb + 8 * h, CTo)) = q;
                     }
                 }
             }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int n = nb + i;
-                float x = v[i];
-                if (d.bias_mode == 1) x += n < d.N ? bias[n] : 0.f;
-                else if (d.bias_mode == 2) x += bias[m];
-                if (d.C && d.accumulate && n < d.N) x += d.C[cz * d.c_gs + (long)m * d.cm + (long)n * d.cn];
-                if (d.act == 1) {
-                    if (d.C2 && n < d.N) d.C2[cz * d.c2_gs + (long)m * d.c2m + (long)n * d.c2n] = x;
-                    x = tanhf(x);
-                } else if (d.act == 2) {
-                    x *= 1.f - ax[i] * ax[i];
-                }
-                v[i] = x;
-                if (d.C && n < d.N) d.C[cz * d.c_gs + (long)m * d.cm + (long)n * d.cn] = x;
-            }
-            if (d.o_mode == 1) {  // image (row = m, col = n): two 16-B stores
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (nb + 8 * h >= d.N) continue;
-                    uint4 q;
-                    q.x = umma::pack_bf16(v[8 * h + 0], v[8 * h + 1]);
-                    q.y = umma::pack_bf16(v[8 * h + 2], v[8 * h + 3]);
-                    q.z = umma::pack_bf16(v[8 * h + 4], v[8 * h + 5]);
-                    q.w = umma::pack_bf16(v[8 * h + 6], v[8 * h + 7]);
-                    if (nb + 8 * h + 8 > d.N) {  // partial: keep padding columns zero
-                        float t[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) t[e] = (nb + 8 * h + e < d.N) ? v[8 * h + e] : 0.f;
-                        q.x = umma::pack_bf16(t[0], t[1]);
-                        q.y = umma::pack_bf16(t[2], t[3]);
-                        q.z = umma::pack_bf16(t[4], t[5]);
-                        q.w = umma::pack_bf16(t[6], t[7]);
-                    }
-                    *reinterpret_cast<uint4*>(d.O.p + oz * d.O.gs + img_off(m, nb + 8 * h, CTo)) = q;
-                }
-            }
+            umma::fence_before_sync();
+            umma::mbar_arrive(&tempty[acc]);
+            ++it;
         }
     }
-    umma::fence_before_sync();
     __syncthreads();
-    if (warp == 0) umma::tmem_free(tbase, kCols);
+    if (warp == 0) umma::tmem_free(tbase, C::TCOLS);
 }
 
-template <int BN>
-void launch(const IGemm& d, cudaStream_t s) {
+template <int BN, int EPI>
+void launch(IGemm d, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_img_gemm<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+        MB_CUDA(cudaFuncSetAttribute(k_img_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Cfg<BN>::SMEM));
         configured = true;
     }
+    d.N_tile = BN;
     const int mext = d.gmode == 1 ? d.max_group : d.M;
-    dim3 grid((d.N + BN - 1) / BN, (mext + 127) / 128, d.Z);
-    k_img_gemm<BN><<<grid, NT, Cfg<BN>::SMEM, s>>>(d);
+    const int ntn = (d.N + BN - 1) / BN, ntm = (mext + 127) / 128;
+    const int ntiles = ntn * ntm * d.Z;
+    const int grid = ntiles < 148 ? ntiles : 148;
+    k_img_gemm<BN, EPI><<<grid, NT, Cfg<BN>::SMEM, s>>>(d, ntiles, ntn, ntm);
     MB_LAUNCH();
+}
+
+template <int EPI>
+void dispatch_bn(const IGemm& d, cudaStream_t s) {
+    if (d.N <= 16) launch<16, EPI>(d, s);
+    else if (d.N <= 32) launch<32, EPI>(d, s);
+    else if (d.N <= 64) launch<64, EPI>(d, s);
+    else if (d.N <= 128) launch<128, EPI>(d, s);
+    else launch<256, EPI>(d, s);
 }
 }  // namespace
 
 void img_gemm(const IGemm& d, cudaStream_t s) {
     if (d.M <= 0 || d.N <= 0 || d.Z <= 0) return;
     if (d.gmode == 1 && d.max_group <= 0) return;
-    if (d.N <= 16) launch<16>(d, s);
-    else if (d.N <= 32) launch<32>(d, s);
-    else if (d.N <= 64) launch<64>(d, s);
-    else if (d.N <= 128) launch<128>(d, s);
-    else launch<256>(d, s);
+    if (d.act == 0) {
+        if (d.o_mode != 0) throw ShapeError("img_gemm: image output needs an activation epilogue");
+        dispatch_bn<0>(d, s);
+    } else if (d.act == 1) {
+        dispatch_bn<1>(d, s);
+    } else {
+        dispatch_bn<2>(d, s);
+    }
 }
 
 // ---- image packing / unpacking helpers ------------------------------------

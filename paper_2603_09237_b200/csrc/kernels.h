@@ -51,6 +51,7 @@ struct IGemm {
     float* C2 = nullptr; long c2m = 0, c2n = 0, c2_gs = 0;
     int accumulate = 0;
     Img O; int o_mode = 0;       // 0 none, 1 image (row = m, col = n)
+    int N_tile = 0;              // set by the launcher
 };
 void img_gemm(const IGemm& d, cudaStream_t s);
 // dst(r, c) <- src[z*src_gs + r*ld + c] for z < G (dst.gs per z)
