@@ -35,7 +35,7 @@ struct Cfg {
     static constexpr int NMMA = BN > 128 ? 128 : BN;  // N per MMA instruction
     static constexpr int ACC = BN < 32 ? 32 : BN;     // TMEM columns per accumulator buffer
     static constexpr int TCOLS = 2 * ACC;             // double buffered (<= 512)
-    static constexpr int SMEM = STAGES * STAGE + 1024 + 4 * BN;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 4 * BN + 16 * BN;
 };
 
 __device__ __forceinline__ long chunk_index(int view, int mt, int kc, int CT) {
@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
     uint64_t* tempty = tfull + 2;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
     float* sbias = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 1024);  // [BN]
+    float* sred = sbias + BN;                                                        // [4][BN] column partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) umma::tmem_alloc(tslot, C::TCOLS);
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
                     for (int i = 0; i < 16; ++i) v[i] = 0.f;
                 }
                 const int nb = ti.n0 + c0;
-                if (!mrow || nb >= d.N) continue;
+                if ((EPI != 2 || !d.psum) && (!mrow || nb >= d.N)) continue;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] += (d.bias_mode == 1 ? sbias[c0 + i] : bm);
                 if (EPI == 0) {
@@ -221,9 +222,11 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
                         for (int i = 0; i < 16; ++i) v[i] = tanhf(v[i]);
                     } else {
                         const int CTx = img_ct(d.aux.C);
+                        const bool ok = mrow && nb < d.N;
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            const uint4 q = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb + 8 * h, CTx));
+                            uint4 q = make_uint4(0, 0, 0, 0);
+                            if (ok) q = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb + 8 * h, CTx));
                             const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
@@ -232,6 +235,26 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
                                 v[8 * h + 2 * e + 1] *= 1.f - f.y * f.y;
                             }
                         }
+                        if (d.psum) {  // warp reduce-scatter of 16 columns over 32 rows: 16 shuffles
+                            float a[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) a[i] = (ok && nb + i < d.N) ? v[i] : 0.f;
+                            int col = 0;
+#pragma unroll
+                            for (int w = 8; w >= 1; w >>= 1) {  // keep w columns, 2x rows each step
+                                const int sel = (lane & (2 * w)) ? w : 0;
+                                col += sel;
+#pragma unroll
+                                for (int i = 0; i < w; ++i) {
+                                    const float mine = sel ? a[w + i] : a[i];
+                                    const float other = sel ? a[i] : a[w + i];
+                                    a[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * w);
+                                }
+                            }
+                            a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+                            if ((lane & 1) == 0) sred[lg * BN + c0 + col] = a[0];
+                        }
+                        if (!ok) continue;
                     }
                     const int CTo = img_ct(d.O.C);
 #pragma unroll
@@ -251,6 +274,13 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             }
             umma::fence_before_sync();
             umma::mbar_arrive(&tempty[acc]);
+            if (EPI == 2 && d.psum) {  // psum[m-tile][n] = sum over the tile's 128 rows
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                for (int j = et; j < BN; j += 128)
+                    if (ti.n0 + j < d.N)
+                        d.psum[(long)(ti.m0 >> 7) * d.psum_ld + ti.n0 + j] =
+                            sred[j] + sred[BN + j] + sred[2 * BN + j] + sred[3 * BN + j];
+            }
             ++it;
         }
     }
@@ -296,6 +326,20 @@ void img_gemm(const IGemm& d, cudaStream_t s) {
     } else {
         dispatch_bn<2>(d, s);
     }
+}
+
+__global__ void k_tile_segsum(const float* psum, long ld, int width, const int* goff, float* out, long out_gs) {
+    const int z = blockIdx.x;
+    const int j = threadIdx.x;
+    if (j >= width) return;
+    float acc = 0.f;
+    for (int t = goff[z] >> 7; t < (goff[z + 1] >> 7); ++t) acc += psum[(long)t * ld + j];
+    out[(long)z * out_gs + j] = acc;
+}
+void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, float* out, long out_gs,
+                 cudaStream_t s) {
+    k_tile_segsum<<<G, ((width + 31) / 32) * 32, 0, s>>>(psum, ld, width, goff, out, out_gs);
+    MB_LAUNCH();
 }
 
 // ---- image packing / unpacking helpers ------------------------------------

@@ -643,19 +643,35 @@ void mul_dtanh(float* g, const float* a, long n, cudaStream_t s) {
     MB_LAUNCH();
 }
 
-// image-output variants (tcgen05 update path): padded rows (rows[q] < 0)
-// get zero loss and zero gradient
-__global__ void k_actor_rows_img(int Bp, int ad, const int* rows, const int* rg, const float* theta, long P,
-                                 long mlp_n, const float* mu, int ldmu, const float* z, const float* lp_old,
-                                 const float* sadv, float clip, float ent, float inv_B, Img gimg, float* lsg,
-                                 double* loss_rows, int* err) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= Bp) return;
-    float g[16];
-    for (int d = 0; d < 16; ++d) g[d] = 0.f;
+// image-output variants (tcgen05 update path): one block = one 128-row tile;
+// padded rows (rows[q] < 0) get zero loss and zero gradient. Per-tile column
+// sums of the output gradient (bias grads) and of the log-std terms go to
+// psum / psls [tile][16] (deterministic, summed per cluster by tile_segsum).
+__device__ __forceinline__ void tile_colsum(const float* g, int width, float* red, float* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int d = 0; d < width; ++d) {
+        float x = g[d];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) red[warp * 16 + d] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < width) out[threadIdx.x] = red[threadIdx.x] + red[16 + threadIdx.x] + red[32 + threadIdx.x] +
+                                                red[48 + threadIdx.x];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(128) k_actor_rows_img(int ad, const int* rows, const int* rg, const float* theta,
+                                                        long P, long mlp_n, const float* mu, int ldmu,
+                                                        const float* z, const float* lp_old, const float* sadv,
+                                                        float clip, float ent, float inv_B, Img gimg, float* psum,
+                                                        float* psls, double* loss_rows, int* err) {
+    __shared__ float red[64];
+    const int q = blockIdx.x * 128 + threadIdx.x;
+    float g[16], gl[16];
+    for (int d = 0; d < 16; ++d) g[d] = gl[d] = 0.f;
     if (rows[q] < 0) {
         loss_rows[q] = 0.0;
-        for (int d = 0; d < ad; ++d) lsg[(long)q * ad + d] = 0.f;
     } else {
         const float* th = theta + (long)rg[q] * P + mlp_n;
         float lp = 0.f, ls[16], zn[16], sig[16], ent_h = 0.f;
@@ -677,8 +693,8 @@ __global__ void k_actor_rows_img(int Bp, int ad, const int* rows, const int* rg,
         const float glp = unc <= clp ? -ratio * adv * inv_B : 0.f;  // losses.cpp:116
         for (int d = 0; d < ad; ++d) {
             g[d] = glp * zn[d] / sig[d];
-            const float raw = th[d];
-            lsg[(long)q * ad + d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - ent * inv_B : 0.f;
+            const float raw = th[d];  // clamp mask (losses.cpp:124-128)
+            gl[d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - ent * inv_B : 0.f;
         }
     }
     const int CT = img_ct(gimg.C);
@@ -690,20 +706,23 @@ __global__ void k_actor_rows_img(int Bp, int ad, const int* rows, const int* rg,
         w.w = umma::pack_bf16(g[8 * h + 6], g[8 * h + 7]);
         *reinterpret_cast<uint4*>(gimg.p + img_off(q, 8 * h, CT)) = w;
     }
+    tile_colsum(g, ad, red, psum + blockIdx.x * 16);
+    tile_colsum(gl, ad, red, psls + blockIdx.x * 16);
 }
 void actor_rows_img(int Bp, int ad, const int* rows, const int* row_group, const float* theta, long P, long mlp_n,
                     const float* mu, int ldmu, const float* z, const float* lp_old, const float* sadv, float clip,
-                    float ent, float inv_B, const Img& g_out, float* lsg, double* loss_rows, int* err,
+                    float ent, float inv_B, const Img& g_out, float* psum, float* psls, double* loss_rows, int* err,
                     cudaStream_t s) {
-    k_actor_rows_img<<<(Bp + 255) / 256, 256, 0, s>>>(Bp, ad, rows, row_group, theta, P, mlp_n, mu, ldmu, z, lp_old,
-                                                      sadv, clip, ent, inv_B, g_out, lsg, loss_rows, err);
+    k_actor_rows_img<<<Bp / 128, 128, 0, s>>>(ad, rows, row_group, theta, P, mlp_n, mu, ldmu, z, lp_old, sadv, clip,
+                                              ent, inv_B, g_out, psum, psls, loss_rows, err);
     MB_LAUNCH();
 }
 
-__global__ void k_critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, const float* tgt,
-                                  float inv_B, Img gimg, double* loss_rows) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= Bp) return;
+__global__ void __launch_bounds__(128) k_critic_rows_img(int m, const int* rows, const float* v, int ldv,
+                                                         const float* tgt, float inv_B, Img gimg, float* psum,
+                                                         double* loss_rows) {
+    __shared__ float red[64];
+    const int q = blockIdx.x * 128 + threadIdx.x;
     float g[16];
     for (int k = 0; k < 16; ++k) g[k] = 0.f;
     double l = 0.0;
@@ -723,10 +742,11 @@ __global__ void k_critic_rows_img(int Bp, int m, const int* rows, const float* v
         w.w = umma::pack_bf16(g[8 * h + 6], g[8 * h + 7]);
         *reinterpret_cast<uint4*>(gimg.p + img_off(q, 8 * h, CT)) = w;
     }
+    tile_colsum(g, m, red, psum + blockIdx.x * 16);
 }
 void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, const float* tgt, float inv_B,
-                     const Img& g_out, double* loss_rows, cudaStream_t s) {
-    k_critic_rows_img<<<(Bp + 255) / 256, 256, 0, s>>>(Bp, m, rows, v, ldv, tgt, inv_B, g_out, loss_rows);
+                     const Img& g_out, float* psum, double* loss_rows, cudaStream_t s) {
+    k_critic_rows_img<<<Bp / 128, 128, 0, s>>>(m, rows, v, ldv, tgt, inv_B, g_out, psum, loss_rows);
     MB_LAUNCH();
 }
 
@@ -780,30 +800,50 @@ void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, floa
 
 // Adam that also refreshes the bf16 image of the hypernet M block
 // (flat indices [m_lo, m_lo + P*F) -> image (p, f)), used as the operand of
-// the next theta-generation and df GEMMs.
-__global__ void k_adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float ibc1, float ibc2,
-                           const int* err, long m_lo, long m_hi, int F, Img mimg) {
+// the next theta-generation and df GEMMs. 4 parameters per thread; m_lo and
+// F are multiples of 4 so a quad never straddles an 8-column image group.
+__global__ void k_adam_img(long n4, float4* p, const float4* g, float4* m1, float4* m2, float lr, float ibc1,
+                           float ibc2, const int* err, long m_lo, long m_hi, int F, Img mimg) {
     if (*err) return;
     const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const float gi = g[i];
-    const float a = 0.9f * m1[i] + 0.1f * gi;
-    const float b = 0.999f * m2[i] + 0.001f * gi * gi;
-    const float pv = p[i] - lr * (a * ibc1) / (sqrtf(b * ibc2) + 1e-8f);
+    if (i >= n4) return;
+    float4 pp = p[i], gg = g[i], a = m1[i], b = m2[i];
+    float* P = &pp.x;
+    const float* G = &gg.x;
+    float* A = &a.x;
+    float* Bv = &b.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        A[k] = 0.9f * A[k] + 0.1f * G[k];
+        Bv[k] = 0.999f * Bv[k] + 0.001f * G[k] * G[k];
+        P[k] -= lr * (A[k] * ibc1) / (sqrtf(Bv[k] * ibc2) + 1e-8f);
+    }
+    p[i] = pp;
     m1[i] = a;
     m2[i] = b;
-    p[i] = pv;
-    if (i >= m_lo && i < m_hi) {
-        const long e = i - m_lo;
-        *reinterpret_cast<__nv_bfloat16*>(mimg.p + img_off(e / F, e % F, img_ct(F))) = __float2bfloat16_rn(pv);
+    const long e = 4 * i;
+    if (e >= m_lo && e < m_hi) {
+        const long r = (e - m_lo) / F, c = (e - m_lo) - r * F;
+        uint2 q;
+        q.x = umma::pack_bf16(P[0], P[1]);
+        q.y = umma::pack_bf16(P[2], P[3]);
+        *reinterpret_cast<uint2*>(mimg.p + img_off(r, c, img_ct(F))) = q;
     }
 }
 void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2, const int* err,
               long m_lo, int F, const Img& mimg, cudaStream_t s) {
     const long m_hi = m_lo + (long)mimg.R * F;
-    k_adam_img<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, p, g, m1, m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi,
-                                                          F, mimg);
+    if (m_lo % 4 || F % 8) throw ShapeError("adam_img: M block must be 4-aligned with F % 8 == 0");
+    const long n4 = n / 4;
+    if (n4)
+        k_adam_img<<<(unsigned)((n4 + 255) / 256), 256, 0, s>>>(n4, (float4*)p, (const float4*)g, (float4*)m1,
+                                                               (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi,
+                                                               F, mimg);
     MB_LAUNCH();
+    if (n4 * 4 < n) {  // tail (never inside the M block: it ends at b, after M)
+        k_adam_tail<<<1, 32, 0, s>>>(n4 * 4, n, p, g, m1, m2, lr, 1.f / bc1, 1.f / bc2, err);
+        MB_LAUNCH();
+    }
 }
 
 // =========================================================================

@@ -52,7 +52,12 @@ struct IGemm {
     int accumulate = 0;
     Img O; int o_mode = 0;       // 0 none, 1 image (row = m, col = n)
     int N_tile = 0;              // set by the launcher
+    float* psum = nullptr;       // act 2: per-128-row-tile column sums [Bp/128][psum_ld]
+    long psum_ld = 0;
 };
+// out[z*out_gs + j] = sum over row tiles t of group z (goff/128) of psum[t*ld + j]
+void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, float* out, long out_gs,
+                 cudaStream_t s);
 void img_gemm(const IGemm& d, cudaStream_t s);
 // dst(r, c) <- src[z*src_gs + r*ld + c] for z < G (dst.gs per z)
 void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
@@ -63,11 +68,14 @@ void img_segcolsum(const Img& x, int width, const int* goff, int G, float* out, 
 void segcolsum_f32(const float* x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg,
                    long c0, cudaStream_t s);
 // per-row loss heads writing the output-layer gradient into an image
+// psum / psls: per-128-row-tile column sums [Bp/128][16] of the output
+// gradient (bias grads) and of the log-std gradient terms
 void actor_rows_img(int Bp, int ad, const int* rows, const int* row_group, const float* theta, long P, long mlp_n,
                     const float* mu, int ldmu, const float* z, const float* lp_old, const float* sadv, float clip,
-                    float ent, float inv_B, const Img& g_out, float* lsg, double* loss_rows, int* err, cudaStream_t s);
+                    float ent, float inv_B, const Img& g_out, float* psum, float* psls, double* loss_rows, int* err,
+                    cudaStream_t s);
 void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, const float* tgt, float inv_B,
-                     const Img& g_out, double* loss_rows, cudaStream_t s);
+                     const Img& g_out, float* psum, double* loss_rows, cudaStream_t s);
 void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2, const int* err,
               long m_lo, int F, const Img& mimg, cudaStream_t s);
 

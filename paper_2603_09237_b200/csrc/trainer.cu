@@ -455,6 +455,10 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     g_lo_ = rank * Kl_;
     Rl_ = (long)Nl_ * cfg.T;
     MB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    MB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_c_done_})
+        MB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    MB_CUDA(cudaEventRecord(ev_c_done_, s2_));
     if (world > 1) comm_ = comm_create(world, rank, nccl_id);
     root_ = HostRng::seeded(cfg.seed);
     std::vector<int> as{es_.obs_dim}, cs{es_.obs_dim};
@@ -481,6 +485,14 @@ Trainer::~Trainer() {
                     d_Z, d_lpo, d_sa, d_tg, d_lsg})
         if (p) cudaFree(p);
     for (auto* p : img_allocs_) cudaFree(p);
+    for (auto& u : ub_) {
+        cudaFree(u.psum);
+        cudaFree(u.psls);
+        cudaFree(u.lossrows);
+    }
+    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_c_done_})
+        if (e) cudaEventDestroy(e);
+    if (s2_) cudaStreamDestroy(s2_);
     for (auto& u : ub_) cudaFree(u.Zf);
     for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
                     (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_rowgroup, (void*)d_lossrows,
@@ -553,6 +565,16 @@ void Trainer::alloc() {
         ub_[w].Zf = dalloc<float>((size_t)Bpmax_ * 16);
     }
     d_lossrows = dalloc<double>(Bpmax_);
+    {
+        int wmax = 16;
+        for (int l = 1; l <= actor_.tgt.L; ++l) wmax = std::max(wmax, actor_.tgt.sz[l]);
+        for (int l = 1; l <= critic_.tgt.L; ++l) wmax = std::max(wmax, critic_.tgt.sz[l]);
+        for (auto& u : ub_) {
+            u.psum = dalloc<float>((size_t)(Bpmax_ / 128) * wmax);
+            u.psls = dalloc<float>((size_t)(Bpmax_ / 128) * 16);
+            u.lossrows = dalloc<double>(Bpmax_);
+        }
+    }
     rows_tmp_.assign((size_t)Bmax_ + 1, 0);
     d_mbloss = dalloc<double>((size_t)slots * 2 + 2);
     d_stats = dalloc<double>(4 * 8);
@@ -701,11 +723,13 @@ void Trainer::phase_advantages() {
 // dW_l = G_l^T A_{l-1} (K = the cluster's rows), dX = (G_l W_l) * tanh'.
 // Leaves gtheta [local clusters][P] (fp32, reference flat layout) complete.
 void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg, const int* rows, const int* goff,
-                       int slot) {
+                       int slot, cudaStream_t s_) {
     const NetDims& nd = h.tgt;
     const int L = nd.L;
     UpdBufs& u = ub_[is_actor ? 0 : 1];
     float* gth = h.gtheta + (long)g_lo_ * h.P;
+    float *d_psum = u.psum, *d_psls = u.psls;
+    double* d_lossrows = u.lossrows;
     if (Bp == 0) {
         MB_CUDA(cudaMemsetAsync(gth, 0, sizeof(float) * Kl_ * h.P, s_));
         MB_CUDA(cudaMemsetAsync(d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, sizeof(double), s_));
@@ -740,11 +764,13 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
     }
     if (is_actor) {  // losses.cpp:87-129
         actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, th, h.P, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
-                       (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], d_lsg, d_lossrows, d_err, s_);
-        segcolsum_f32(d_lsg, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.P, Img{}, 0, s_);
+                       (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], d_psum, d_psls, d_lossrows,
+                       d_err, s_);
+        tile_segsum(d_psls, 16, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.P, s_);  // log-std grads
     } else {  // losses.cpp:170-185
-        critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], d_lossrows, s_);
+        critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], d_psum, d_lossrows, s_);
     }
+    tile_segsum(d_psum, 16, nd.sz[L], goff, Kl_, gth + nd.boff[L - 1], h.P, s_);  // output-layer bias grads
     sum_f64(d_lossrows, Bp, d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, s_);
     for (int l = L - 1; l >= 0; --l) {  // backward (nn.cpp:111-160)
         const Img& ain = l == 0 ? Xi_ : u.A[l - 1];
@@ -755,7 +781,6 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         d.gmode = 2; d.goff = goff;
         d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = h.P;
         igemm("mlp_dW", d, s_);
-        img_segcolsum(u.G[l], nd.sz[l + 1], goff, Kl_, gth + nd.boff[l], h.P, Img{}, 0, s_);
         if (l > 0) {
             IGemm e;  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
             e.A = u.G[l]; e.a_view = 0;  // (m = q, k = j)
@@ -764,7 +789,9 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
             e.gmode = 1; e.goff = goff; e.max_group = maxg;
             e.act = 2; e.aux = u.A[l - 1];
             e.O = u.G[l - 1]; e.o_mode = 1;
+            e.psum = d_psum; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
             igemm("mlp_dX", e, s_);
+            tile_segsum(d_psum, nd.sz[l], nd.sz[l], goff, Kl_, gth + nd.boff[l - 1], h.P, s_);
         }
     }
     launches_ += 4 * L + 5;
@@ -774,9 +801,15 @@ void Trainer::allgather_gtheta(HyperNet& h) {
     if (comm_) comm_allgather_f32(comm_, h.gtheta, (size_t)Kl_ * h.P, s_);
 }
 
+// One PPO minibatch (train.cpp:163-180). The actor chain runs on s_, the
+// critic chain on s2_: the two losses / backward passes / Adam steps are
+// independent, so their many small kernels overlap. Joins: both losses are
+// checked for finiteness before either Adam (train.cpp:174-178), and the
+// next minibatch's gather waits for the critic to release the shared inputs.
 void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, const int* goff) {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
     if (Bp > 0) {
         gather_img(rows, Bp, d_obs, od, Xi_, s_);
         gather_pad(rows, Bp, d_act, ad, d_Z, s_);
@@ -786,16 +819,25 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         fill_row_group(goff, Kl_, d_rowgroup, Bp, s_);
         launches_ += 6;
     }
-    net_step(actor_, true, Bp, inv_B, maxg, rows, goff, slot);
-    net_step(critic_, false, Bp, inv_B, maxg, rows, goff, slot);
+    MB_CUDA(cudaEventRecord(ev_gather_, s_));
+    MB_CUDA(cudaStreamWaitEvent(s2_, ev_gather_, 0));
+    critic_.forward(d_cw, g_lo_, Kl_, s2_);  // hypernet_forward per loss (losses.cpp:79,167)
+    net_step(critic_, false, Bp, inv_B, maxg, rows, goff, slot, s2_);
+    MB_CUDA(cudaEventRecord(ev_c_net_, s2_));
+    actor_.forward(d_cw, g_lo_, Kl_, s_);
+    net_step(actor_, true, Bp, inv_B, maxg, rows, goff, slot, s_);
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_c_net_, 0));
     allgather_gtheta(actor_);
     allgather_gtheta(critic_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
+    MB_CUDA(cudaEventRecord(ev_chk_, s_));
+    MB_CUDA(cudaStreamWaitEvent(s2_, ev_chk_, 0));
+    critic_.backward(s2_);
+    critic_.adam_step(cfg_.critic_lr, d_err, s2_);
+    MB_CUDA(cudaEventRecord(ev_c_done_, s2_));
     actor_.backward(s_);
-    critic_.backward(s_);
-    actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180: actor then critic
-    critic_.adam_step(cfg_.critic_lr, d_err, s_);
+    actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
     launches_ += 2 * (10 + 4 * (int)actor_.fsz.size()) + 3;
 }
 
@@ -810,8 +852,6 @@ void Trainer::phase_update(int it, int max_minibatches) {
             if (max_minibatches >= 0 && mb_done_ >= max_minibatches) return;
             const int slot = e * mbs + s;
             if (mb_Bglob_[slot] == 0) continue;  // lo == hi
-            actor_.forward(d_cw, g_lo_, Kl_, s_);  // hypernet_forward per loss (losses.cpp:79,167)
-            critic_.forward(d_cw, g_lo_, Kl_, s_);
             minibatch(slot, mb_B_[slot], mb_Bglob_[slot], mb_maxg_[slot], d_rows + (size_t)slot * Bpmax_,
                       d_goff + (size_t)slot * (Kl_ + 1));
             ++mb_done_;
@@ -819,6 +859,7 @@ void Trainer::phase_update(int it, int max_minibatches) {
 }
 
 void Trainer::finish(IterStats* st) {
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
     const int slots = cfg_.epochs * cfg_.minibatch_count;
     std::vector<double> losses((size_t)slots * 2);
     std::vector<double> rs(Nl_);
@@ -885,8 +926,8 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
         gather_pad(d_rows, Bp, d_tgt, m, d_tg, s_);
         fill_row_group(d_goff, Kl_, d_rowgroup, Bp, s_);
     }
-    net_step(actor_, true, Bp, inv_B, mx, d_rows, d_goff, 0);
-    net_step(critic_, false, Bp, inv_B, mx, d_rows, d_goff, 0);
+    net_step(actor_, true, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
+    net_step(critic_, false, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
     allgather_gtheta(actor_);
     allgather_gtheta(critic_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss, 2, s_);

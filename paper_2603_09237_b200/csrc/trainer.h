@@ -148,7 +148,7 @@ private:
     void prepare_perms(int it);
     void minibatch(int slot, int B, int Bglob, int maxg, const int* d_rows, const int* d_goff);
     void net_step(HyperNet& h, bool actor, int Bp, float inv_B, int maxg, const int* rows, const int* d_goff,
-                  int slot);
+                  int slot, cudaStream_t st);
     void allgather_gtheta(HyperNet& h);
 
     TrainConfig cfg_;
@@ -173,7 +173,11 @@ private:
         std::vector<Img> A;     // [Bp][h_l] hidden activations (post-tanh)
         std::vector<Img> G;     // [Bp][out_l] gradient at the pre-activation of layer l
         float* Zf = nullptr;    // [Bp][16] output layer (policy mean / values), fp32
+        float *psum = nullptr, *psls = nullptr;  // per-128-row-tile column sums (bias / log-std grads)
+        double* lossrows = nullptr;
     } ub_[2];
+    cudaStream_t s2_ = nullptr;  // critic chain of the update
+    cudaEvent_t ev_gather_ = nullptr, ev_c_net_ = nullptr, ev_chk_ = nullptr, ev_c_done_ = nullptr;
     Img Xi_;                    // [Bp][obs] gathered observations (bf16 image)
     std::vector<uint8_t*> img_allocs_;
     std::vector<int> rows_tmp_;
