@@ -302,7 +302,7 @@ def main():
         print(json.dumps({
             "metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": iter_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (SIMT fp32 GEMMs; bf16 tcgen05 planned)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 (tcgen05 GEMMs, fp32 accumulate; fp32 env/elementwise, fp64 RNG transforms)",
             "data": "synthetic (seeded env rollouts; random-init hypernetworks)",
             "config": {"workload": WORKLOAD[args.config], "envs": cfg.N, "clusters": cfg.K, "T": cfg.T,
                        "env": cfg.env_name, "ppo": f"{cfg.epochs}x{cfg.minibatch_count}",
