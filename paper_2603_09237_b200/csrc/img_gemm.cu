@@ -8,7 +8,7 @@
 //     (full[s] expect_tx, empty[s] released by tcgen05.commit);
 //   * warp 1 / lane 0 = MMA issuer: 8 x (K = 16) tcgen05.mma per B chunk
 //     into TMEM accumulator buffer (tile & 1); tcgen05.commit -> tfull;
-//   * warps 4..7 = epilogue (TMEM lanes 32*(w-4)..): tcgen05.ld 16 columns at
+//   * warps 4..11 = epilogue (TMEM lanes 32*(w%4).., column half (w-4)/4): tcgen05.ld 16 columns at
 //     a time, fused bias / tanh / tanh' / fp32 + bf16-image stores, then
 //     arrive tempty so the MMA warp can reuse the buffer -- the epilogue of
 //     tile i overlaps the loads and MMAs of tile i+1.
@@ -23,7 +23,7 @@
 namespace mb200 {
 
 namespace {
-constexpr int NT = 256;
+constexpr int NT = 384;  // warps 0-3: producer / MMA / spare, 4-11: epilogue
 constexpr int CHUNK = 32768;
 constexpr int EPI_WARP0 = 4;
 
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
         }
         for (int b = 0; b < 2; ++b) {
             umma::mbar_init(&tfull[b], 1);
-            umma::mbar_init(&tempty[b], 128);
+            umma::mbar_init(&tempty[b], 256);
         }
         umma::fence_barrier_init();
     }
@@ -163,21 +163,23 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             }
         }
         __syncwarp();
-    } else if (warp >= EPI_WARP0) {  // ---------------- epilogue
-        const int lg = warp - EPI_WARP0;
-        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..127
+    } else if (warp >= EPI_WARP0) {  // ---------------- epilogue (8 warps)
+        const int ew = warp - EPI_WARP0;           // 0..7
+        const int lg = ew & 3, half = ew >> 2;     // TMEM lane quadrant, column half
+        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..255
+        constexpr int HALF = BN >= 32 ? BN / 2 : BN;
+        const bool active = BN >= 32 || half == 0;
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const TileInfo ti = tile_info(d, t, ntn, ntm);
             if (!ti.valid) continue;
             const int acc = it & 1;
             const float* bias = d.bias ? d.bias + (d.gmode != 2 ? ti.z * d.bias_gs : 0) : nullptr;
-            // stage the tile's per-n bias in smem (previous tile's readers are done:
-            // they arrived on tempty before this loop iteration's named barrier)
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            // per-n bias -> smem (the previous tile's readers passed this barrier already)
+            asm volatile("bar.sync 1, 256;" ::: "memory");
             if (d.bias_mode == 1)
-                for (int j = et; j < BN; j += 128) sbias[j] = (ti.n0 + j < d.N) ? bias[ti.n0 + j] : 0.f;
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+                for (int j = et; j < BN; j += 256) sbias[j] = (ti.n0 + j < d.N) ? bias[ti.n0 + j] : 0.f;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
             umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));  // committed even when nk == 0
             umma::fence_after_sync();
             const int m = ti.m0 + lg * 32 + lane;
@@ -185,49 +187,61 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             const float bm = (d.bias_mode == 2 && mrow) ? bias[m] : 0.f;
             const long cz = d.gmode == 1 ? 0 : ti.z;
             float* crow = d.C ? d.C + cz * d.c_gs + (long)m * d.cm : nullptr;
+            const int CTo = img_ct(d.O.C), CTx = img_ct(d.aux.C);
+            if (active) {
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-                float v[16];
-                if (ti.nk > 0) {
-                    umma::tmem_ld16(tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * C::ACC + c0), v);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] = 0.f;
-                }
-                const int nb = ti.n0 + c0;
-                if ((EPI != 2 || !d.psum) && (!mrow || nb >= d.N)) continue;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] += (d.bias_mode == 1 ? sbias[c0 + i] : bm);
-                if (EPI == 0) {
-                    if (d.accumulate)
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (nb + i < d.N) v[i] += crow[(long)(nb + i) * d.cn];
-                    if (d.cn == 1 && nb + 16 <= d.N && ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0)) {
-                        float4* q = reinterpret_cast<float4*>(crow + nb);
-#pragma unroll
-                        for (int h = 0; h < 4; ++h) q[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+                for (int c0 = half * HALF; c0 < half * HALF + HALF; c0 += 16) {
+                    const int nb = ti.n0 + c0;
+                    const bool full = mrow && nb + 16 <= d.N;
+                    const bool any = mrow && nb < d.N;
+                    uint4 ax[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+                    if (EPI == 2 && any) {  // issue the tanh' operand loads before the TMEM load
+                        ax[0] = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb, CTx));
+                        if (nb + 8 < d.N) ax[1] = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb + 8, CTx));
+                    }
+                    float v[16];
+                    if (ti.nk > 0) {
+                        umma::tmem_ld16(tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * C::ACC + c0), v);
                     } else {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (nb + i < d.N) crow[(long)(nb + i) * d.cn] = v[i];
+                        for (int i = 0; i < 16; ++i) v[i] = 0.f;
                     }
-                } else {
+                    if (d.bias_mode == 1) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] += sbias[c0 + i];
+                    } else if (d.bias_mode == 2) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] += bm;
+                    }
+                    if (EPI == 0) {
+                        if (!any) continue;
+                        if (d.accumulate)
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (nb + i < d.N) v[i] += crow[(long)(nb + i) * d.cn];
+                        if (full && d.cn == 1 && ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0)) {
+                            float4* q = reinterpret_cast<float4*>(crow + nb);
+#pragma unroll
+                            for (int h = 0; h < 4; ++h)
+                                q[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (nb + i < d.N) crow[(long)(nb + i) * d.cn] = v[i];
+                        }
+                        continue;
+                    }
                     if (EPI == 1) {
-                        if (d.C2)
+                        if (d.C2 && any)
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
                                 if (nb + i < d.N) d.C2[(long)m * d.c2m + (long)(nb + i) * d.c2n] = v[i];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) v[i] = tanhf(v[i]);
+                        for (int i = 0; i < 16; ++i) v[i] = umma::tanh_approx(v[i]);
                     } else {
-                        const int CTx = img_ct(d.aux.C);
-                        const bool ok = mrow && nb < d.N;
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            uint4 q = make_uint4(0, 0, 0, 0);
-                            if (ok) q = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb + 8 * h, CTx));
-                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&ax[h]);
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 const float2 f = __bfloat1622float2(b2[e]);
@@ -236,9 +250,9 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
                             }
                         }
                         if (d.psum) {  // warp reduce-scatter of 16 columns over 32 rows: 16 shuffles
-                            float a[16];
+                            float a2[16];
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) a[i] = (ok && nb + i < d.N) ? v[i] : 0.f;
+                            for (int i = 0; i < 16; ++i) a2[i] = (full || (any && nb + i < d.N)) ? v[i] : 0.f;
                             int col = 0;
 #pragma unroll
                             for (int w = 8; w >= 1; w >>= 1) {  // keep w columns, 2x rows each step
@@ -246,23 +260,23 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
                                 col += sel;
 #pragma unroll
                                 for (int i = 0; i < w; ++i) {
-                                    const float mine = sel ? a[w + i] : a[i];
-                                    const float other = sel ? a[i] : a[w + i];
-                                    a[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * w);
+                                    const float mine = sel ? a2[w + i] : a2[i];
+                                    const float other = sel ? a2[i] : a2[w + i];
+                                    a2[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * w);
                                 }
                             }
-                            a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
-                            if ((lane & 1) == 0) sred[lg * BN + c0 + col] = a[0];
+                            a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 1);
+                            if ((lane & 1) == 0) sred[lg * BN + c0 + col] = a2[0];
                         }
-                        if (!ok) continue;
                     }
-                    const int CTo = img_ct(d.O.C);
+                    if (!any) continue;
+                    if (!full)
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (nb + i >= d.N) v[i] = 0.f;  // keep padding zero
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        if (nb + 8 * h >= d.N) continue;
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (nb + 8 * h + e >= d.N) v[8 * h + e] = 0.f;  // keep padding zero
+                        if (!full && nb + 8 * h >= d.N) continue;
                         uint4 q;
                         q.x = umma::pack_bf16(v[8 * h + 0], v[8 * h + 1]);
                         q.y = umma::pack_bf16(v[8 * h + 2], v[8 * h + 3]);
@@ -275,8 +289,8 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             umma::fence_before_sync();
             umma::mbar_arrive(&tempty[acc]);
             if (EPI == 2 && d.psum) {  // psum[m-tile][n] = sum over the tile's 128 rows
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                for (int j = et; j < BN; j += 128)
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                for (int j = et; j < BN; j += 256)
                     if (ti.n0 + j < d.N)
                         d.psum[(long)(ti.m0 >> 7) * d.psum_ld + ti.n0 + j] =
                             sred[j] + sred[BN + j] + sred[2 * BN + j] + sred[3 * BN + j];
