@@ -167,6 +167,9 @@ int morlax_shard_minibatch(const int32_t* perm, int lo, int hi, int T, int inst_
 int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, const float* B, long bk, long bn,
                      float* C, int use_tc);
 
+/* microbenchmark hook for the tcgen05 GEMM (tools/gemm_bench.py): ms per launch */
+int morlax_gemm_bench(int M, int N, int K, int a_view, int b_view, int act, int iters, double* ms);
+
 /* ---- Pareto (replaces nondominated_filter / hypervolume_mc /
  *      hypervolume_detailed, include/morlax/pareto.hpp:21-56) ------------ */
 /* survivors of nondominated_filter as a mask over the input order */

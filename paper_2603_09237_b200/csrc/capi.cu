@@ -249,7 +249,8 @@ int morlax_hypernet_forward(const morlax_hypernet_spec* s, const double* flat, c
         DBuf<float> dw(wf.data(), wf.size());
         hh.h.forward(dw.p, 0, G, 0);
         std::vector<float> th((size_t)G * hh.h.P);
-        MB_CUDA(cudaMemcpy(th.data(), hh.h.theta, sizeof(float) * th.size(), cudaMemcpyDeviceToHost));
+        MB_CUDA(cudaMemcpy2D(th.data(), sizeof(float) * hh.h.P, hh.h.theta, sizeof(float) * hh.h.ld,
+                             sizeof(float) * hh.h.P, G, cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < th.size(); ++i) {
             if (!std::isfinite(th[i]))
                 throw NumericError("hypernet_forward produced a non-finite parameter at index " +
@@ -268,7 +269,8 @@ int morlax_hypernet_backward(const morlax_hypernet_spec* s, const double* flat, 
         DBuf<float> dw(wf.data(), wf.size());
         hh.h.forward(dw.p, 0, G, 0);
         std::vector<float> gt(gtheta, gtheta + (size_t)G * hh.h.P);
-        MB_CUDA(cudaMemcpy(hh.h.gtheta, gt.data(), sizeof(float) * gt.size(), cudaMemcpyHostToDevice));
+        MB_CUDA(cudaMemcpy2D(hh.h.gtheta, sizeof(float) * hh.h.ld, gt.data(), sizeof(float) * hh.h.P,
+                             sizeof(float) * hh.h.P, G, cudaMemcpyHostToDevice));
         hh.h.backward(0);
         std::vector<float> g(hh.h.n);
         MB_CUDA(cudaMemcpy(g.data(), hh.h.g, sizeof(float) * g.size(), cudaMemcpyDeviceToHost));
@@ -432,8 +434,8 @@ int morlax_trainer_get_theta(morlax_trainer* t, int which, float* out) {
         HyperNet& h = which ? tr.critic() : tr.actor();
         MB_CUDA(cudaStreamSynchronize(tr.stream()));
         const int g0 = (tr.local_groups() == tr.config().K) ? 0 : 0;
-        MB_CUDA(cudaMemcpy(out, h.theta + (long)g0 * h.P, sizeof(float) * h.P * tr.local_groups(),
-                           cudaMemcpyDeviceToHost));
+        MB_CUDA(cudaMemcpy2D(out, sizeof(float) * h.P, h.theta + (long)g0 * h.ld, sizeof(float) * h.ld,
+                             sizeof(float) * h.P, tr.local_groups(), cudaMemcpyDeviceToHost));
     });
 }
 
@@ -482,7 +484,7 @@ int morlax_trainer_set(morlax_trainer* t, const char* field, const void* in) {
         Trainer& tr = *t->t;
         const std::string f(field);
         if (f == "perm") {
-            std::memcpy(tr.perm().data(), in, sizeof(int) * tr.perm().size());
+            tr.set_perm(static_cast<const int*>(in));
             return;
         }
         if (f == "clusters") {
@@ -575,6 +577,38 @@ int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, cons
         }
         MB_CUDA(cudaDeviceSynchronize());
         dc.get(C);
+    });
+}
+
+// microbenchmark hook: D = A(view a) B(view b)^T over random bf16 images,
+// epilogue `act` (0 fp32 out, 1 tanh -> image, 2 tanh' -> image); returns ms/launch
+int morlax_gemm_bench(int M, int N, int K, int a_view, int b_view, int act, int iters, double* ms) {
+    return guarded([&] {
+        const int aR = a_view ? K : M, aC = a_view ? M : K, bR = b_view ? K : N, bC = b_view ? N : K;
+        DBuf<uint8_t> ia(img_bytes(aR, aC)), ib(img_bytes(bR, bC)), io(img_bytes(M, N)), ix(img_bytes(M, N));
+        DBuf<float> c((size_t)M * N);
+        MB_CUDA(cudaMemset(ia.p, 0x3c, img_bytes(aR, aC)));
+        MB_CUDA(cudaMemset(ib.p, 0x3c, img_bytes(bR, bC)));
+        MB_CUDA(cudaMemset(ix.p, 0x3c, img_bytes(M, N)));
+        IGemm d;
+        d.A = Img{ia.p, aR, aC, 0}; d.a_view = a_view;
+        d.B = Img{ib.p, bR, bC, 0}; d.b_view = b_view;
+        d.M = M; d.N = N; d.K = K;
+        if (act == 0) { d.C = c.p; d.cm = N; d.cn = 1; }
+        else { d.act = act; d.O = Img{io.p, M, N, 0}; d.o_mode = 1; d.aux = Img{ix.p, M, N, 0}; }
+        img_gemm(d, 0);
+        cudaEvent_t e0, e1;
+        MB_CUDA(cudaEventCreate(&e0));
+        MB_CUDA(cudaEventCreate(&e1));
+        MB_CUDA(cudaEventRecord(e0, 0));
+        for (int i = 0; i < iters; ++i) img_gemm(d, 0);
+        MB_CUDA(cudaEventRecord(e1, 0));
+        MB_CUDA(cudaEventSynchronize(e1));
+        float t = 0;
+        MB_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        *ms = t / iters;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
     });
 }
 

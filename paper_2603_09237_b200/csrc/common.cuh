@@ -3,6 +3,8 @@
 // of the reference) and the environment dynamics (fp32 state).
 #pragma once
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,7 +29,14 @@ struct CudaError : std::runtime_error { using std::runtime_error::runtime_error;
             throw ::mb200::CudaError(std::string("CUDA error ") + cudaGetErrorString(_e) + \
                                      " at " __FILE__ ":" + std::to_string(__LINE__)); \
     } while (0)
-#define MB_LAUNCH() MB_CUDA(cudaGetLastError())
+// every kernel launch of the library goes through MB_LAUNCH: the counter is
+// the bench's gpu_launches figure (kernels.cu defines it)
+extern std::atomic<long> g_kernel_launches;
+#define MB_LAUNCH()                                                        \
+    do {                                                                   \
+        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);         \
+        MB_CUDA(cudaGetLastError());                                       \
+    } while (0)
 
 // ---- RNG: include/morlax/rng.hpp:18-93 -----------------------------------
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;

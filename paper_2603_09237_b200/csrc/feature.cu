@@ -1,0 +1,156 @@
+// Hypernetwork feature map f(w) (hypernet.cpp:10-17, 92-122): a tanh MLP
+// (tanh on the output too) over the K cluster weight vectors. The work is
+// tiny (K = 128 rows, widths of a few hundred) and sits on the critical path
+// of every minibatch, so the limit is L2 latency, not bandwidth or flops:
+// every contraction is one launch of k_dense16, a 16 x 16 output tile per
+// CTA (>= 128 CTAs per layer) that stages its whole K extent (in 128-wide
+// slices) of both operands in shared memory with one round of loads, then
+// one FMA chain per thread. fp32 throughout.
+//   forward : per layer Y = tanh(X W^T + b); the last layer also writes the
+//             bf16 image of f for the theta GEMM;
+//   backward: gz_L = (sum of the split-K partials of M^T gtheta) * tanh';
+//             per layer gz_{l-1} = (gz_l W_l) * tanh'(a_l);
+//             dW_l = gz_l^T a_l with db_l as an extra all-ones column.
+#include "common.cuh"
+#include "img.cuh"
+#include "kernels.h"
+
+namespace mb200 {
+
+namespace {
+constexpr int KC = 128;  // K slice staged per round
+
+struct Dense16 {
+    const float* A;  // A(r, k) = A[r * ar + k * ak]
+    long ar, ak;
+    const float* B;  // B(c, k) = B[c * bc + k * bk]; c == N -> 1 when ones_col
+    long bc, bk;
+    int R, N, K;
+    const float* bias;  // [N] or null
+    int act;            // 0 none, 1 tanh, 2 * (1 - aux^2)
+    const float* aux;   // aux(r, c) = aux[r * xr + c]
+    long xr;
+    float* C;           // C(r, c) = C[r * cr + c * cc]
+    long cr, cc;
+    int ones_col;       // column N of the output = sum_k A(r, k) -> Cb[r]
+    float* Cb;
+    Img img;            // optional bf16 image copy of the output (row r, col c)
+};
+
+__global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
+    __shared__ float As[16][KC + 1];
+    __shared__ float Bs[16][KC + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int r0 = blockIdx.y * 16, c0 = blockIdx.x * 16;
+    const int ncols = d.N + (d.ones_col ? 1 : 0);
+    float acc0 = 0.f, acc1 = 0.f;
+    for (int k0 = 0; k0 < d.K; k0 += KC) {
+        const int kn = min(KC, d.K - k0);
+        // 16 rows x kn of each operand: thread t loads k = t % KC.., row = t / KC..
+        for (int e = threadIdx.x; e < 16 * KC; e += 256) {
+            const int rr = e / KC, kk = e % KC;
+            const int r = r0 + rr, c = c0 + rr, k = k0 + kk;
+            float a = 0.f, b = 0.f;
+            if (kk < kn) {
+                if (r < d.R) a = d.A[r * d.ar + k * d.ak];
+                if (c < d.N) b = d.B[c * d.bc + k * d.bk];
+                else if (c == d.N && d.ones_col) b = 1.f;
+            }
+            As[rr][kk] = a;
+            Bs[rr][kk] = b;
+        }
+        __syncthreads();
+        int kk = 0;
+        for (; kk + 2 <= kn; kk += 2) {
+            acc0 = fmaf(As[ty][kk], Bs[tx][kk], acc0);
+            acc1 = fmaf(As[ty][kk + 1], Bs[tx][kk + 1], acc1);
+        }
+        if (kk < kn) acc0 = fmaf(As[ty][kk], Bs[tx][kk], acc0);
+        __syncthreads();
+    }
+    const int r = r0 + ty, c = c0 + tx;
+    if (r >= d.R || c >= ncols) return;
+    float v = acc0 + acc1;
+    if (c == d.N) {  // ones column: row sums of A (bias gradients)
+        d.Cb[r] = v;
+        return;
+    }
+    if (d.bias) v += d.bias[c];
+    if (d.act == 1) {
+        v = tanhf(v);
+    } else if (d.act == 2) {
+        const float a = d.aux[r * d.xr + c];
+        v *= 1.f - a * a;
+    }
+    d.C[r * d.cr + c * d.cc] = v;
+    if (d.img.p)
+        *reinterpret_cast<__nv_bfloat16*>(d.img.p + img_off(r, c, img_ct(d.img.C))) = __float2bfloat16_rn(v);
+}
+
+void dense16(const Dense16& d, cudaStream_t s) {
+    const int ncols = d.N + (d.ones_col ? 1 : 0);
+    dim3 grid((ncols + 15) / 16, (d.R + 15) / 16);
+    k_dense16<<<grid, 256, 0, s>>>(d);
+    MB_LAUNCH();
+}
+
+// gz[g][j] = (sum_k parts[k][g][j]) * (1 - f[g][j]^2)
+__global__ void k_split_dtanh(const float* __restrict__ parts, int splits, long n, const float* __restrict__ f,
+                              float* gz) {
+    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int k = 0;
+    for (; k + 8 <= splits; k += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += parts[(long)(k + u) * n + i];
+    for (; k < splits; ++k) a[0] += parts[(long)k * n + i];
+    const float x = f[i];
+    gz[i] = (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]))) * (1.f - x * x);
+}
+}  // namespace
+
+void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, cudaStream_t s) {
+    for (int l = 0; l < fd.L; ++l) {
+        Dense16 d{};
+        d.A = l == 0 ? w : fd.act[l];  // act[0] is not materialised: w is the input
+        d.ar = fd.sz[l]; d.ak = 1;
+        d.B = p + fd.woff[l]; d.bc = fd.sz[l]; d.bk = 1;  // W [out][in]
+        d.R = G; d.N = fd.sz[l + 1]; d.K = fd.sz[l];
+        d.bias = p + fd.boff[l];
+        d.act = 1;
+        d.C = fd.act[l + 1]; d.cr = fd.sz[l + 1]; d.cc = 1;
+        if (l == fd.L - 1) d.img = fimg;
+        dense16(d, s);
+    }
+}
+
+void feature_backward(const FeatDims& fd, const float* p, const float* w, const float* parts, int splits, int G,
+                      float* gout, cudaStream_t s) {
+    const int L = fd.L;
+    const long n = (long)G * fd.sz[L];
+    k_split_dtanh<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(parts, splits, n, fd.act[L], fd.gz[L - 1]);
+    MB_LAUNCH();
+    for (int l = L - 1; l >= 0; --l) {
+        const int in = fd.sz[l], out = fd.sz[l + 1];
+        const float* a_in = l == 0 ? w : fd.act[l];
+        Dense16 d{};  // dW[j][i] = sum_g gz[g][j] a[g][i]; db[j] = sum_g gz[g][j]
+        d.A = fd.gz[l]; d.ar = 1; d.ak = out;
+        d.B = a_in; d.bc = 1; d.bk = in;
+        d.R = out; d.N = in; d.K = G;
+        d.C = gout + fd.woff[l]; d.cr = in; d.cc = 1;
+        d.ones_col = 1; d.Cb = gout + fd.boff[l];
+        dense16(d, s);
+        if (l > 0) {
+            Dense16 e{};  // gz_{l-1}[g][i] = (sum_j gz_l[g][j] W[j][i]) (1 - a_l[g][i]^2)
+            e.A = fd.gz[l]; e.ar = out; e.ak = 1;
+            e.B = p + fd.woff[l]; e.bc = 1; e.bk = in;
+            e.R = G; e.N = in; e.K = out;
+            e.act = 2; e.aux = fd.act[l]; e.xr = in;
+            e.C = fd.gz[l - 1]; e.cr = in; e.cc = 1;
+            dense16(e, s);
+        }
+    }
+}
+
+}  // namespace mb200

@@ -35,7 +35,7 @@ struct Cfg {
     static constexpr int NMMA = BN > 128 ? 128 : BN;  // N per MMA instruction
     static constexpr int ACC = BN < 32 ? 32 : BN;     // TMEM columns per accumulator buffer
     static constexpr int TCOLS = 2 * ACC;             // double buffered (<= 512)
-    static constexpr int SMEM = STAGES * STAGE + 1024 + 4 * BN + 16 * BN;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 4 * BN + 16 * BN + 8 * 512 * 4;
 };
 
 __device__ __forceinline__ long chunk_index(int view, int mt, int kc, int CT) {
@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
     float* sbias = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 1024);  // [BN]
     float* sred = sbias + BN;                                                        // [4][BN] column partials
+    float* sstg = sred + 4 * BN;  // [8 warps][32 x 16] fp32 store staging
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) umma::tmem_alloc(tslot, C::TCOLS);
@@ -180,24 +181,159 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             if (d.bias_mode == 1)
                 for (int j = et; j < BN; j += 256) sbias[j] = (ti.n0 + j < d.N) ? bias[ti.n0 + j] : 0.f;
             asm volatile("bar.sync 1, 256;" ::: "memory");
-            umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));  // committed even when nk == 0
-            umma::fence_after_sync();
             const int m = ti.m0 + lg * 32 + lane;
             const bool mrow = m < ti.m_hi;
             const float bm = (d.bias_mode == 2 && mrow) ? bias[m] : 0.f;
             const long cz = d.gmode == 1 ? 0 : ti.z;
             float* crow = d.C ? d.C + cz * d.c_gs + (long)m * d.cm : nullptr;
             const int CTo = img_ct(d.O.C), CTx = img_ct(d.aux.C);
-            if (active) {
-#pragma unroll 1
-                for (int c0 = half * HALF; c0 < half * HALF + HALF; c0 += 16) {
+            // full tile (every grouped tile: groups are 128-row padded): no
+            // per-chunk guards, addresses = per-thread base + compile-time offset
+            const bool fast = ti.m0 + 128 <= ti.m_hi && ti.n0 + BN <= d.N && !d.accumulate &&
+                              (EPI != 0 || (d.cn == 1 && (d.cm & 3) == 0 && (d.c_gs & 3) == 0 &&
+                                            (reinterpret_cast<uintptr_t>(d.C) & 15) == 0)) &&
+                              (EPI != 1 || !d.C2);
+            if (active && fast) {
+                constexpr int NCH = HALF / 16, PF = NCH < 4 ? NCH : 4;
+                // image byte offset of (row m, column n0 + half * HALF); + chunk offset below
+                const long rowo_x = ((long)(m >> 7) * CTx) * 32768 + ((m & 127) >> 3) * 2048 + (m & 7) * 16;
+                const long rowo_o = ((long)(m >> 7) * CTo) * 32768 + ((m & 127) >> 3) * 2048 + (m & 7) * 16;
+                const int cb = ti.n0 + half * HALF;  // multiple of 16; chunks below never cross 128
+                const long colo = (long)(cb >> 7) * 32768 + ((cb & 127) >> 3) * 128;
+                const uint8_t* xb = d.aux.p + rowo_x + colo;
+                uint8_t* ob = d.O.p + rowo_o + colo;
+                // EPI 0: first row of this warp's 32-row slab, first column of the half
+                float* cwarp = d.C ? d.C + cz * d.c_gs + (long)(ti.m0 + lg * 32) * d.cm + cb : nullptr;
+                float* stg = sstg + ew * 512;
+                // chunk ci = columns cb + 16 ci .. +15, inside one 128-column chunk
+                // for every BN ((cb & 127) + 16 ci <= 112): 2 core-matrix columns
+                auto coff = [](int ci) -> long { return (long)ci * 256; };
+                uint4 ring[PF][2];
+                if (EPI == 2) {
+#pragma unroll
+                    for (int q = 0; q < PF; ++q) {
+                        ring[q][0] = *reinterpret_cast<const uint4*>(xb + coff(q));
+                        ring[q][1] = *reinterpret_cast<const uint4*>(xb + coff(q) + 128);
+                    }
+                }
+                umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+                umma::fence_after_sync();
+#pragma unroll
+                for (int ci = 0; ci < NCH; ++ci) {
+                    const int c0 = half * HALF + ci * 16;
+                    float v[16];
+                    if (ti.nk > 0) {
+                        umma::tmem_ld16(tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * C::ACC + c0), v);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+                    }
+                    if (d.bias_mode == 1) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] += sbias[c0 + i];
+                    } else if (d.bias_mode == 2) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] += bm;
+                    }
+                    if (EPI == 0) {
+                        // transpose the warp's 32 rows x 16 columns through shared memory
+                        // (XOR-swizzled float4 slots, conflict-free both ways) so every
+                        // store instruction writes 8 rows x 64 contiguous bytes
+#pragma unroll
+                        for (int h = 0; h < 4; ++h)
+                            *reinterpret_cast<float4*>(stg + lane * 16 + ((h ^ ((lane >> 1) & 3)) << 2)) =
+                                make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+                        __syncwarp();
+#pragma unroll
+                        for (int s8 = 0; s8 < 4; ++s8) {
+                            const int r = s8 * 8 + (lane >> 2), h = lane & 3;
+                            const float4 x = *reinterpret_cast<const float4*>(stg + r * 16 + ((h ^ ((r >> 1) & 3)) << 2));
+                            *reinterpret_cast<float4*>(cwarp + (long)r * d.cm + ci * 16 + h * 4) = x;
+                        }
+                        __syncwarp();
+                        continue;
+                    }
+                    if (EPI == 1) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = umma::tanh_approx(v[i]);
+                    } else {
+                        uint4 ax[2] = {ring[ci % PF][0], ring[ci % PF][1]};
+                        if (ci + PF < NCH) {
+                            ring[ci % PF][0] = *reinterpret_cast<const uint4*>(xb + coff(ci + PF));
+                            ring[ci % PF][1] = *reinterpret_cast<const uint4*>(xb + coff(ci + PF) + 128);
+                        }
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&ax[h]);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float2 f = __bfloat1622float2(b2[e]);
+                                v[8 * h + 2 * e] *= 1.f - f.x * f.x;
+                                v[8 * h + 2 * e + 1] *= 1.f - f.y * f.y;
+                            }
+                        }
+                        if (d.psum) {  // warp reduce-scatter of 16 columns over 32 rows
+                            float a2[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) a2[i] = v[i];
+                            int col = 0;
+#pragma unroll
+                            for (int w = 8; w >= 1; w >>= 1) {
+                                const bool up = (lane & (2 * w)) != 0;
+                                col += up ? w : 0;
+#pragma unroll
+                                for (int i = 0; i < w; ++i) {
+                                    const float mine = up ? a2[w + i] : a2[i];
+                                    const float other = up ? a2[i] : a2[w + i];
+                                    a2[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * w);
+                                }
+                            }
+                            a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 1);
+                            if ((lane & 1) == 0) sred[lg * BN + c0 + col] = a2[0];
+                        }
+                    }
+                    uint4 q0, q1;
+                    q0.x = umma::pack_bf16(v[0], v[1]);
+                    q0.y = umma::pack_bf16(v[2], v[3]);
+                    q0.z = umma::pack_bf16(v[4], v[5]);
+                    q0.w = umma::pack_bf16(v[6], v[7]);
+                    q1.x = umma::pack_bf16(v[8], v[9]);
+                    q1.y = umma::pack_bf16(v[10], v[11]);
+                    q1.z = umma::pack_bf16(v[12], v[13]);
+                    q1.w = umma::pack_bf16(v[14], v[15]);
+                    *reinterpret_cast<uint4*>(ob + coff(ci)) = q0;
+                    *reinterpret_cast<uint4*>(ob + coff(ci) + 128) = q1;
+                }
+            } else if (active) {
+                // tanh' operand: 4-deep register prefetch ring (loads issued up to
+                // four 16-column chunks ahead, the first four before the tfull wait)
+                constexpr int NCH = HALF / 16, PF = NCH < 4 ? NCH : 4;
+                uint4 ring[PF][2];
+                auto aux_load = [&](int ci, uint4* dst) {
+                    const int nb2 = ti.n0 + half * HALF + ci * 16;
+                    dst[0] = dst[1] = make_uint4(0, 0, 0, 0);
+                    if (EPI == 2 && mrow && nb2 < d.N) {
+                        dst[0] = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb2, CTx));
+                        if (nb2 + 8 < d.N) dst[1] = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb2 + 8, CTx));
+                    }
+                };
+                if (EPI == 2) {
+#pragma unroll
+                    for (int q = 0; q < PF; ++q) aux_load(q, ring[q]);
+                }
+                umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));  // committed even when nk == 0
+                umma::fence_after_sync();
+#pragma unroll
+                for (int ci = 0; ci < NCH; ++ci) {
+                    const int c0 = half * HALF + ci * 16;
                     const int nb = ti.n0 + c0;
                     const bool full = mrow && nb + 16 <= d.N;
                     const bool any = mrow && nb < d.N;
                     uint4 ax[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-                    if (EPI == 2 && any) {  // issue the tanh' operand loads before the TMEM load
-                        ax[0] = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb, CTx));
-                        if (nb + 8 < d.N) ax[1] = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb + 8, CTx));
+                    if (EPI == 2) {
+                        ax[0] = ring[ci % PF][0];
+                        ax[1] = ring[ci % PF][1];
+                        if (ci + PF < NCH) aux_load(ci + PF, ring[ci % PF]);
                     }
                     float v[16];
                     if (ti.nk > 0) {

@@ -10,6 +10,8 @@
 
 namespace mb200 {
 
+std::atomic<long> g_kernel_launches{0};
+
 // =========================================================================
 // K1: BatchedEnv reset / step (env.cpp:44-106). SoA state [sdim][N].
 // =========================================================================
@@ -85,262 +87,11 @@ void env_obs(int kind, int N, const float* state, float* obs, cudaStream_t s) {
     MB_LAUNCH();
 }
 
-// =========================================================================
-// K3: fused rollout (rollout.cpp:37-161). One CTA owns up to kR instances
-// of ONE preference cluster for all T steps: env state stays in shared
-// memory, the cluster's generated policy / critic weights stream from L2.
-// Per step: policy MLP -> Gaussian sample (bit-exact RNG words) -> critic
-// at obs (only when the previous step ended an episode, else the previous
-// next_value is reused: identical values) -> env step + auto-reset ->
-// critic at the pre-reset final obs.
-// =========================================================================
-constexpr int kR = 64;    // instances per CTA
-constexpr int kNT = 256;  // threads per CTA
-constexpr int kKC = 32;   // K chunk of the weight tile
-int rollout_rows_per_cta() { return kR; }
-
-// out[r][j] = act(b[j] + sum_i in[r][i] W[j][i]), r < nr, j < Nout (<= 256)
-__device__ void block_dense(const float* __restrict__ W, const float* __restrict__ b, int Kin, int Nout,
-                            const float* in, int ldi, float* out, int ldo, int nr, bool tanh_act,
-                            float* wt) {
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int cpt = (Nout + 31) >> 5, rpt = (nr + 7) >> 3;
-    float acc[8][8];
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-        const int j = tx + 32 * jj;
-        const float bj = (jj < cpt && j < Nout) ? b[j] : 0.f;
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) acc[ii][jj] = bj;
-    }
-    for (int k0 = 0; k0 < Kin; k0 += kKC) {
-        const int kc = min(kKC, Kin - k0);
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < Nout * kKC; idx += kNT) {
-            const int j = idx / kKC, kk = idx % kKC;
-            wt[j * (kKC + 1) + kk] = kk < kc ? W[(long)j * Kin + k0 + kk] : 0.f;
-        }
-        __syncthreads();
-        for (int kk = 0; kk < kc; ++kk) {
-            float a[8], w[8];
-#pragma unroll
-            for (int ii = 0; ii < 8; ++ii) {
-                const int r = ty + 8 * ii;
-                a[ii] = (ii < rpt && r < nr) ? in[r * ldi + k0 + kk] : 0.f;
-            }
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                const int j = tx + 32 * jj;
-                w[jj] = (jj < cpt && j < Nout) ? wt[j * (kKC + 1) + kk] : 0.f;
-            }
-#pragma unroll
-            for (int ii = 0; ii < 8; ++ii)
-                if (ii < rpt)
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj)
-                        if (jj < cpt) acc[ii][jj] = fmaf(a[ii], w[jj], acc[ii][jj]);
-        }
-    }
-#pragma unroll
-    for (int ii = 0; ii < 8; ++ii) {
-        const int r = ty + 8 * ii;
-        if (ii >= rpt || r >= nr) continue;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-            const int j = tx + 32 * jj;
-            if (jj < cpt && j < Nout) out[r * ldo + j] = tanh_act ? tanhf(acc[ii][jj]) : acc[ii][jj];
-        }
-    }
-    __syncthreads();
-}
-
-// MLP forward over nr rows held in `x` (ld od); result (last pre-activation
-// for the policy, identity output for the critic) into `out` (ld ldo).
-__device__ void block_mlp(const NetDims& nd, const float* w, const float* x, int od, float* ha, float* hb,
-                          int ldh, float* out, int ldo, int nr, float* wt) {
-    const float* in = x;
-    int ldi = od;
-    float* bufs[2] = {ha, hb};
-    for (int l = 0; l < nd.L; ++l) {
-        const bool last = (l == nd.L - 1);
-        float* dst = last ? out : bufs[l & 1];
-        const int ldd = last ? ldo : ldh;
-        // the Gaussian mean is the output pre-activation (losses.cpp:92-94)
-        block_dense(w + nd.woff[l], w + nd.boff[l], nd.sz[l], nd.sz[l + 1], in, ldi, dst, ldd, nr,
-                    !last, wt);
-        in = dst;
-        ldi = ldd;
-    }
-}
-
 __device__ __forceinline__ float sech2_f(float z) {
     // 1 - tanh(z)^2 without cancellation: 4 e^{-2|z|} / (1 + e^{-2|z|})^2
     const float e = __expf(-2.f * fabsf(z));
     const float d = 1.f + e;
     return 4.f * e / (d * d);
-}
-
-__global__ void __launch_bounds__(kNT, 1) k_rollout(RolloutArgs a) {
-    extern __shared__ __align__(16) float sm[];
-    const int cpg = (a.reps + kR - 1) / kR;
-    const int c = blockIdx.x / cpg, ch = blockIdx.x % cpg;
-    const int i0 = c * a.reps + ch * kR;
-    const int nr = min(kR, a.reps - ch * kR);
-    const int od = a.od, ad = a.ad, m = a.m, sd = a.sdim;
-    int hmax = 0;
-    for (int l = 1; l < a.pol.L; ++l) hmax = max(hmax, a.pol.sz[l]);
-    for (int l = 1; l < a.cri.L; ++l) hmax = max(hmax, a.cri.sz[l]);
-    // shared-memory carve-up
-    float* S = sm;                        // [sd][kR]   env state
-    float* X = S + sd * kR;               // [kR][od]   obs / final obs
-    float* HA = X + kR * od;              // [kR][hmax]
-    float* HB = HA + kR * hmax;           // [kR][hmax]
-    float* MU = HB + kR * hmax;           // [kR][ad]
-    float* ZS = MU + kR * ad;             // [kR][ad]   pre-tanh samples
-    float* AC = ZS + kR * ad;             // [kR][ad]   actions
-    float* VV = AC + kR * ad;             // [kR][m]    critic output
-    float* NV = VV + kR * m;              // [kR][m]    next value carry
-    float* RW = NV + kR * m;              // [kR][m]    rewards
-    float* TRK = RW + kR * m;             // [kR][m]    running returns
-    float* WT = TRK + kR * m;             // [256][kKC+1] weight tile
-    float* LS = WT + 256 * (kKC + 1);     // [ad] clamped log-std
-    uint64_t* EK = reinterpret_cast<uint64_t*>(LS + 16);  // [kR] env stream key
-    uint64_t* EC = EK + kR;                               // [kR] env stream ctr
-    uint64_t* RK = EC + kR;                               // [kR] sampling stream key
-    int* STP = reinterpret_cast<int*>(RK + kR);           // [kR] step counters
-    int* NEED = STP + kR;                                 // [kR] value needs recompute
-
-    const float* th = a.theta + (long)c * a.pol.P;
-    const float* ph = a.phi + (long)c * a.cri.P;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < sd * nr; e += kNT) {
-        const int k = e / nr, r = e % nr;
-        S[k * kR + r] = a.state[(long)k * a.N + i0 + r];
-    }
-    for (int r = tid; r < nr; r += kNT) {
-        EK[r] = a.env_key[i0 + r];
-        EC[r] = a.env_ctr[i0 + r];
-        STP[r] = a.steps[i0 + r];
-        RK[r] = split_key(a.roll_key, (uint64_t)(a.roll_inst_base + i0 + r));  // rollout.cpp:101
-        NEED[r] = 1;
-        for (int k = 0; k < m; ++k) TRK[r * m + k] = a.tracker[(long)(i0 + r) * m + k];
-    }
-    if (tid < ad) LS[tid] = fminf(fmaxf(th[a.pol.mlp_n + tid], -5.f), 1.f);  // nn.cpp:185-188
-    __syncthreads();
-
-    for (int t = 0; t < a.T; ++t) {
-        // obs rows (obs == state for every env)
-        for (int e = tid; e < nr * od; e += kNT) {
-            const int r = e / od, k = e % od;
-            const float v = S[k * kR + r];
-            X[r * od + k] = v;
-            a.obs[((long)(i0 + r) * a.T + t) * od + k] = v;
-        }
-        __syncthreads();
-        block_mlp(a.pol, th, X, od, HA, HB, hmax, MU, ad, nr, WT);
-        // Gaussian sample, 2 words per dim (nn.cpp:192-202, rng.hpp:55-60)
-        for (int e = tid; e < nr * ad; e += kNT) {
-            const int r = e / ad, d = e % ad;
-            const uint64_t base = 2ull * ((uint64_t)t * ad + d);
-            const double eps = box_muller(rng_word(RK[r], base + 1), rng_word(RK[r], base + 2));
-            const float z = MU[r * ad + d] + __expf(LS[d]) * (float)eps;
-            ZS[r * ad + d] = z;
-            AC[r * ad + d] = tanhf(z);
-            a.act_pre[((long)(i0 + r) * a.T + t) * ad + d] = z;
-        }
-        __syncthreads();
-        for (int r = tid; r < nr; r += kNT) {  // action_logprob (nn.cpp:204-219)
-            float lp = 0.f;
-            for (int d = 0; d < ad; ++d) {
-                const float sig = __expf(LS[d]);
-                const float z = ZS[r * ad + d];
-                const float zn = (z - MU[r * ad + d]) / sig;
-                lp += -0.5f * zn * zn - LS[d] - 0.9189385332046727f;
-                lp -= __logf(sech2_f(z) + 1e-6f);
-            }
-            a.logprob[(long)(i0 + r) * a.T + t] = lp;
-        }
-        int need = 0;
-        for (int r = tid; r < nr; r += kNT) need |= NEED[r];
-        need = __syncthreads_or(need);
-        if (need) block_mlp(a.cri, ph, X, od, HA, HB, hmax, VV, m, nr, WT);
-        // value + env step (env.cpp:60-92) + tracker (rollout.cpp:143-148)
-        for (int r = tid; r < nr; r += kNT) {
-            const long row = (long)(i0 + r) * a.T + t;
-            for (int k = 0; k < m; ++k)
-                a.value[row * m + k] = NEED[r] ? VV[r * m + k] : NV[r * m + k];
-            float act[16], rw[8];
-            bool any = false;
-            for (int d = 0; d < ad; ++d) {
-                const float x = AC[r * ad + d];
-                if (!isfinite(x)) atomicExch(a.err, 3);
-                act[d] = fminf(fmaxf(x, -1.f), 1.f);
-                any |= act[d] != x;
-            }
-            if (any) atomicAdd(a.clamp_count, 1ULL);
-            float* s = S + r;
-            const bool tm = env_do_step(a.kind, s, kR, act, rw);
-            const int st = STP[r] + 1;
-            const bool tr = !tm && st >= a.max_steps;
-            a.term[row] = tm;
-            a.trunc[row] = tr;
-            for (int k = 0; k < m; ++k) {
-                a.reward[row * m + k] = rw[k];
-                TRK[r * m + k] += rw[k];
-            }
-            for (int k = 0; k < od; ++k) X[r * od + k] = s[k * kR];  // pre-reset final obs
-            if (tm || tr) {
-                double ret = 0.0;
-                for (int k = 0; k < m; ++k) {
-                    ret += (double)a.cluster_w[c * m + k] * TRK[r * m + k];
-                    TRK[r * m + k] = 0.f;
-                }
-                a.ret_sum[i0 + r] += ret;
-                a.ret_cnt[i0 + r] += 1;
-                uint64_t cc = EC[r];
-                env_do_reset(a.kind, s, kR, EK[r], &cc);
-                EC[r] = cc;
-                STP[r] = 0;
-                NEED[r] = 1;
-            } else {
-                STP[r] = st;
-                NEED[r] = 0;
-            }
-        }
-        __syncthreads();
-        block_mlp(a.cri, ph, X, od, HA, HB, hmax, NV, m, nr, WT);  // critic at final obs
-        for (int e = tid; e < nr * m; e += kNT) {
-            const int r = e / m, k = e % m;
-            a.next_value[((long)(i0 + r) * a.T + t) * m + k] = NV[e];
-        }
-        __syncthreads();
-    }
-    for (int e = tid; e < sd * nr; e += kNT) {
-        const int k = e / nr, r = e % nr;
-        a.state[(long)k * a.N + i0 + r] = S[k * kR + r];
-    }
-    for (int r = tid; r < nr; r += kNT) {
-        a.env_ctr[i0 + r] = EC[r];
-        a.steps[i0 + r] = STP[r];
-        for (int k = 0; k < m; ++k) a.tracker[(long)(i0 + r) * m + k] = TRK[r * m + k];
-    }
-}
-
-void rollout(const RolloutArgs& a, cudaStream_t s) {
-    int hmax = 0;
-    for (int l = 1; l < a.pol.L; ++l) hmax = hmax > a.pol.sz[l] ? hmax : a.pol.sz[l];
-    for (int l = 1; l < a.cri.L; ++l) hmax = hmax > a.cri.sz[l] ? hmax : a.cri.sz[l];
-    const size_t fl = (size_t)a.sdim * kR + (size_t)kR * a.od + 2ull * kR * hmax + 3ull * kR * a.ad +
-                      4ull * kR * a.m + 256ull * (kKC + 1) + 16;
-    const size_t bytes = fl * 4 + 3ull * kR * 8 + 2ull * kR * 4 + 64;
-    static size_t configured = 0;
-    if (bytes > configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_rollout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        configured = bytes;
-    }
-    const int cpg = (a.reps + kR - 1) / kR;
-    k_rollout<<<a.K * cpg, kNT, bytes, s>>>(a);
-    MB_LAUNCH();
 }
 
 // =========================================================================
@@ -584,22 +335,34 @@ void segmented_colsum(const float* x, int width, const int* goff, int G, float* 
 }
 
 // out[j] = sum_r x[r][j]
-__global__ void k_colsum(const float* x, int rows, long width, float* out) {
+__global__ void k_colsum(const float* __restrict__ x, int rows, long width, long ld, float* out) {
     const long j = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (j >= width) return;
-    float s = 0.f;
-    for (int r = 0; r < rows; ++r) s += x[r * width + j];
-    out[j] = s;
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 8 independent chains: loads stay in flight
+    int r = 0;
+    for (; r + 8 <= rows; r += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += x[(long)(r + u) * ld + j];
+    for (; r < rows; ++r) a[0] += x[(long)r * ld + j];
+    out[j] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
-void colsum_rows(const float* x, int rows, long width, float* out, cudaStream_t s) {
-    k_colsum<<<(int)((width + 255) / 256), 256, 0, s>>>(x, rows, width, out);
+void colsum_rows(const float* x, int rows, long width, long ld, float* out, cudaStream_t s) {
+    k_colsum<<<(int)((width + 255) / 256), 256, 0, s>>>(x, rows, width, ld, out);
     MB_LAUNCH();
 }
 
-__global__ void k_sum_f64(const double* x, long n, double* out, int acc) {
+__global__ void k_sum_f64(const double* __restrict__ x, long n, double* out, int acc) {
     __shared__ double red[1024];
-    double s = 0.0;
-    for (long i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    long i = threadIdx.x;
+    for (; i + 3 * (long)blockDim.x < n; i += 4 * (long)blockDim.x) {
+        s0 += x[i];
+        s1 += x[i + blockDim.x];
+        s2 += x[i + 2 * (long)blockDim.x];
+        s3 += x[i + 3 * (long)blockDim.x];
+    }
+    for (; i < n; i += blockDim.x) s0 += x[i];
+    double s = (s0 + s1) + (s2 + s3);
     red[threadIdx.x] = s;
     __syncthreads();
     for (int k = blockDim.x / 2; k > 0; k >>= 1) {
@@ -622,12 +385,16 @@ void check_finite_f64(const double* x, int n, int* err, int code, cudaStream_t s
     MB_LAUNCH();
 }
 
-__global__ void k_reduce_splits(const float* parts, int S, long n, float* out) {
+__global__ void k_reduce_splits(const float* __restrict__ parts, int S, long n, float* out) {
     const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float s = 0.f;
-    for (int k = 0; k < S; ++k) s += parts[k * n + i];
-    out[i] = s;
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int k = 0;
+    for (; k + 8 <= S; k += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += parts[(long)(k + u) * n + i];
+    for (; k < S; ++k) a[0] += parts[(long)k * n + i];
+    out[i] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
 void reduce_splits(const float* parts, int S, long n, float* out, cudaStream_t s) {
     k_reduce_splits<<<(int)((n + 255) / 256), 256, 0, s>>>(parts, S, n, out);
@@ -646,7 +413,8 @@ void mul_dtanh(float* g, const float* a, long n, cudaStream_t s) {
 // image-output variants (tcgen05 update path): one block = one 128-row tile;
 // padded rows (rows[q] < 0) get zero loss and zero gradient. Per-tile column
 // sums of the output gradient (bias grads) and of the log-std terms go to
-// psum / psls [tile][16] (deterministic, summed per cluster by tile_segsum).
+// psum / psls [tile][16] (deterministic, summed per cluster by tile_segsum);
+// loss_rows[tile] = the tile's loss sum (fp64).
 __device__ __forceinline__ void tile_colsum(const float* g, int width, float* red, float* out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int d = 0; d < width; ++d) {
@@ -661,6 +429,16 @@ __device__ __forceinline__ void tile_colsum(const float* g, int width, float* re
     __syncthreads();
 }
 
+// fp64 sum of one value per thread of a 128-thread block -> *out (thread 0)
+__device__ __forceinline__ void tile_sum_f64(double x, double* out) {
+    __shared__ double wsum[4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) *out = (wsum[0] + wsum[1]) + (wsum[2] + wsum[3]);
+}
+
 __global__ void __launch_bounds__(128) k_actor_rows_img(int ad, const int* rows, const int* rg, const float* theta,
                                                         long P, long mlp_n, const float* mu, int ldmu,
                                                         const float* z, const float* lp_old, const float* sadv,
@@ -670,9 +448,8 @@ __global__ void __launch_bounds__(128) k_actor_rows_img(int ad, const int* rows,
     const int q = blockIdx.x * 128 + threadIdx.x;
     float g[16], gl[16];
     for (int d = 0; d < 16; ++d) g[d] = gl[d] = 0.f;
-    if (rows[q] < 0) {
-        loss_rows[q] = 0.0;
-    } else {
+    double lrow = 0.0;
+    if (rows[q] >= 0) {
         const float* th = theta + (long)rg[q] * P + mlp_n;
         float lp = 0.f, ls[16], zn[16], sig[16], ent_h = 0.f;
         for (int d = 0; d < ad; ++d) {  // action_logprob (nn.cpp:204-219)
@@ -689,7 +466,7 @@ __global__ void __launch_bounds__(128) k_actor_rows_img(int ad, const int* rows,
         const float adv = sadv[q];
         const float unc = ratio * adv;
         const float clp = fminf(fmaxf(ratio, 1.f - clip), 1.f + clip) * adv;
-        loss_rows[q] = (double)(-fminf(unc, clp) * inv_B) - (double)(ent * ent_h * inv_B);
+        lrow = (double)(-fminf(unc, clp) * inv_B) - (double)(ent * ent_h * inv_B);
         const float glp = unc <= clp ? -ratio * adv * inv_B : 0.f;  // losses.cpp:116
         for (int d = 0; d < ad; ++d) {
             g[d] = glp * zn[d] / sig[d];
@@ -697,6 +474,7 @@ __global__ void __launch_bounds__(128) k_actor_rows_img(int ad, const int* rows,
             gl[d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - ent * inv_B : 0.f;
         }
     }
+    tile_sum_f64(lrow, loss_rows + blockIdx.x);  // per-tile loss partial
     const int CT = img_ct(gimg.C);
     for (int h = 0; h < (ad + 7) / 8; ++h) {
         uint4 w;
@@ -732,7 +510,7 @@ __global__ void __launch_bounds__(128) k_critic_rows_img(int m, const int* rows,
             l += (double)e * e * inv_B;
             g[k] = 2.f * e * inv_B;  // losses.cpp:179-181 (no 1/2)
         }
-    loss_rows[q] = l;
+    tile_sum_f64(l, loss_rows + blockIdx.x);  // per-tile loss partial
     const int CT = img_ct(gimg.C);
     for (int h = 0; h < (m + 7) / 8; ++h) {
         uint4 w;

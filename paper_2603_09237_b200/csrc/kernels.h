@@ -97,8 +97,9 @@ struct NetDims {
 };
 struct RolloutArgs {
     int kind, N, T, K, reps, od, ad, m, sdim, max_steps;
-    const float* theta;  // [K][Pa]
-    const float* phi;    // [K][Pc]
+    const float* theta;  // [K][theta_ld] (first Pa used)
+    const float* phi;    // [K][phi_ld]
+    long theta_ld, phi_ld;
     NetDims pol, cri;
     float* state; uint64_t* env_key; uint64_t* env_ctr; int* steps;
     uint64_t roll_key;
@@ -110,8 +111,6 @@ struct RolloutArgs {
     double* ret_sum; int* ret_cnt;  // [N] completed scalarised returns
     unsigned long long* clamp_count; int* err;
 };
-void rollout(const RolloutArgs& a, cudaStream_t s);
-int rollout_rows_per_cta();
 
 // tensor-core rollout (rollout_tc.cu): per-cluster weights packed as bf16
 // UMMA images, streamed per step by the bulk-copy engine
@@ -121,7 +120,7 @@ struct NetPlan {
     int chunk_off[24], chunk_bytes[24], chunk_layer[24], chunk_tile[24];
 };
 NetPlan make_plan(const NetDims& nd);
-void pack_theta(const float* theta, int G, const NetDims& nd, const NetPlan& pl, uint8_t* blob, cudaStream_t s);
+void pack_theta(const float* theta, long ld, int G, const NetDims& nd, const NetPlan& pl, uint8_t* blob, cudaStream_t s);
 struct RolloutTcArgs : RolloutArgs {
     NetPlan pol_plan, cri_plan;
     const uint8_t* pol_blob;  // [K][pol_plan.blob_bytes]
@@ -153,11 +152,26 @@ void critic_rows(int B, int m, const float* v, const float* tgt, float inv_B, fl
 // out[z*out_bz + j] (+)= sum_{rows in group z} x[row*width + j]
 void segmented_colsum(const float* x, int width, const int* goff, int G, float* out, long out_bz,
                       int accumulate, cudaStream_t s);
-void colsum_rows(const float* x, int rows, long width, float* out, cudaStream_t s);
+void colsum_rows(const float* x, int rows, long width, long ld, float* out, cudaStream_t s);
 void sum_f64(const double* x, long n, double* out, int accumulate, cudaStream_t s);
 void fill_row_group(const int* goff, int G, int* row_group, int B, cudaStream_t s);
 void check_finite_f64(const double* x, int n, int* err, int code, cudaStream_t s);
 void reduce_splits(const float* parts, int S, long n, float* out, cudaStream_t s);
+
+// hypernetwork feature map (feature.cu): fused tanh MLP over the cluster rows
+constexpr int kMaxFeatLayers = 8;
+struct FeatDims {
+    int L = 0;
+    int sz[kMaxFeatLayers + 1] = {};
+    long woff[kMaxFeatLayers] = {}, boff[kMaxFeatLayers] = {};
+    float* act[kMaxFeatLayers + 1] = {};   // activations [G][sz[l]] (act[0] = w)
+    float* gz[kMaxFeatLayers] = {};        // pre-activation gradients [G][sz[l+1]]
+};
+// act[1..L], fimg (bf16 image of f) for all G rows of the cluster weights w [G][m]
+void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, cudaStream_t s);
+// df = sum of the split-K partials [splits][G][F]; writes dW/db of every layer into gout (flat layout)
+void feature_backward(const FeatDims& fd, const float* p, const float* w, const float* parts, int splits, int G,
+                      float* gout, cudaStream_t s);
 void mul_dtanh(float* g, const float* a, long n, cudaStream_t s);
 
 // ---------------------------------------------------------------- Adam (K7)

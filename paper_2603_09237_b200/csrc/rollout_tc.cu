@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(RolloutTcArgs a) {
     x.nepad = a.nepad;
     x.issued = x.consumed = 0;
 
-    const float* th = a.theta + (long)c * a.pol.P;
-    const float* ph = a.phi + (long)c * a.cri.P;
+    const float* th = a.theta + (long)c * a.theta_ld;
+    const float* ph = a.phi + (long)c * a.phi_ld;
     // zero the operand buffers once: padded K rows / env columns stay zero
     for (int e = tid; e < (a.xb_bytes + 2 * a.hb_bytes) / 16; e += RNT)
         reinterpret_cast<uint4*>(x.xb)[e] = make_uint4(0, 0, 0, 0);
@@ -430,9 +430,9 @@ NetPlan make_plan(const NetDims& nd) {
     return pl;
 }
 
-void pack_theta(const float* theta, int G, const NetDims& nd, const NetPlan& pl, uint8_t* blob, cudaStream_t s) {
+void pack_theta(const float* theta, long ld, int G, const NetDims& nd, const NetPlan& pl, uint8_t* blob, cudaStream_t s) {
     dim3 grid((unsigned)((pl.blob_bytes / 16 + 255) / 256), G);
-    k_pack_theta<<<grid, 256, 0, s>>>(theta, nd.P, nd, pl, blob);
+    k_pack_theta<<<grid, 256, 0, s>>>(theta, ld, nd, pl, blob);
     MB_LAUNCH();
 }
 

@@ -198,6 +198,7 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     }
     tgt = make_dims(ts, out_tanh, has_log_std);
     P = tgt.P;
+    ld = (P + 7) / 8 * 8;
     n = nf + P * F + P;
     p = dalloc<float>(n);
     g = dalloc<float>(n);
@@ -209,10 +210,23 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
         fact[l] = dalloc<float>((size_t)G * fsz[l]);
         maxw = std::max(maxw, fsz[l]);
     }
-    fg0 = dalloc<float>((size_t)G * maxw);
-    fg1 = dalloc<float>((size_t)G * maxw);
-    theta = dalloc<float>((size_t)G * P);
-    gtheta = dalloc<float>((size_t)G * P);
+    const int Lf = (int)fsz.size() - 1;
+    if (Lf < 1 || Lf > kMaxFeatLayers) throw ConfigError("feature map must have 1.." + std::to_string(kMaxFeatLayers) + " layers");
+    fgz.assign(Lf, nullptr);
+    fd = FeatDims{};
+    fd.L = Lf;
+    for (int l = 0; l <= Lf; ++l) {
+        fd.sz[l] = fsz[l];
+        fd.act[l] = fact[l];
+    }
+    for (int l = 0; l < Lf; ++l) {
+        fgz[l] = dalloc<float>((size_t)G * fsz[l + 1]);
+        fd.gz[l] = fgz[l];
+        fd.woff[l] = fwoff[l];
+        fd.boff[l] = fboff[l];
+    }
+    theta = dalloc<float>((size_t)G * ld);
+    gtheta = dalloc<float>((size_t)G * ld);
     gf = dalloc<float>((size_t)G * F);
     splits = (int)std::min<long>(64, std::max<long>(1, P / 1024));
     parts = dalloc<float>((size_t)splits * G * F);
@@ -257,7 +271,8 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
 void HyperNet::free_all() {
     dfree(p); dfree(g); dfree(m1); dfree(m2);
     for (auto& a : fact) dfree(a);
-    dfree(fg0); dfree(fg1); dfree(theta); dfree(gtheta); dfree(gf); dfree(parts); dfree(d_split_bounds);
+    for (auto& a : fgz) dfree(a);
+    dfree(theta); dfree(gtheta); dfree(gf); dfree(parts); dfree(d_split_bounds);
     dfree(mimg.p); dfree(fimg.p); dfree(gimg.p); dfree(wimg.p);
 }
 
@@ -291,26 +306,19 @@ static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
 void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
     (void)g0;
     (void)ng;
-    MB_CUDA(cudaMemcpyAsync(fact[0], w, sizeof(float) * G * m, cudaMemcpyDeviceToDevice, s));
-    const int Lf = (int)fsz.size() - 1;
-    for (int l = 0; l < Lf; ++l) {  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
-        GemmDesc d;
-        d.A = fact[l]; d.am = fsz[l]; d.ak = 1;
-        d.B = p + fwoff[l]; d.bk = 1; d.bn = fsz[l];
-        d.C = fact[l + 1]; d.cm = fsz[l + 1]; d.cn = 1;
-        d.M = G; d.N = fsz[l + 1]; d.K = fsz[l];
-        d.bias = p + fboff[l]; d.bias_mode = 1;
-        d.act = 1;
-        ProfScope ps("feature_fwd", 2.0 * G * fsz[l + 1] * fsz[l], 0, s);
-        gemm_simt(d, s);
+    {
+        double fl = 0;
+        for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 2.0 * G * fsz[l] * fsz[l + 1];
+        ProfScope ps("feature_fwd", fl, 0, s);
+        w_last = w;
+        feature_forward(fd, p, w, G, fimg, s);  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
     }
-    to_img(fact[Lf], F, 0, G, F, fimg, 1, s);
     IGemm d;
     d.A = mimg; d.a_view = 0;          // (m = p, k = f)
     d.B = fimg; d.b_view = 0;          // (n = g, k = f)
     d.M = (int)P; d.N = G; d.K = F;
     d.bias = p + nf + P * F; d.bias_mode = 2;
-    d.C = theta; d.cm = 1; d.cn = P;   // theta[g][p]
+    d.C = theta; d.cm = 1; d.cn = ld;  // theta[g][p]
     igemm("hyper_theta", d, s);
 }
 
@@ -322,7 +330,7 @@ void HyperNet::pack_weights(int g0, int ng, cudaStream_t s) {
         dst.p = wimg.p + wimg_off[l];
         dst.R = tgt.sz[l + 1];
         dst.C = tgt.sz[l];
-        to_img(theta + (long)g0 * P + tgt.woff[l], tgt.sz[l], P, tgt.sz[l + 1], tgt.sz[l], dst, ng, s);
+        to_img(theta + (long)g0 * ld + tgt.woff[l], tgt.sz[l], ld, tgt.sz[l + 1], tgt.sz[l], dst, ng, s);
     }
 }
 
@@ -331,9 +339,8 @@ void HyperNet::pack_weights(int g0, int ng, cudaStream_t s) {
 // the feature-map backward. Writes (not accumulates) the flat grad g.
 void HyperNet::backward(cudaStream_t s) {
     const long nM = P * F;
-    colsum_rows(gtheta, G, P, g + nf + nM, s);
-    const int Lf = (int)fsz.size() - 1;
-    to_img(gtheta, P, 0, G, (int)P, gimg, 1, s);
+    colsum_rows(gtheta, G, P, ld, g + nf + nM, s);
+    to_img(gtheta, ld, 0, G, (int)P, gimg, 1, s);
     {
         IGemm d;  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
         d.A = gimg; d.a_view = 1;  // (m = p, k = g)
@@ -350,32 +357,12 @@ void HyperNet::backward(cudaStream_t s) {
         d.gmode = 2; d.goff = d_split_bounds;
         d.C = parts; d.cm = F; d.cn = 1; d.c_gs = (long)G * F;
         igemm("hyper_df", d, s);
-        reduce_splits(parts, splits, (long)G * F, gf, s);
     }
-    // feature backward: output tanh -> g *= 1 - f^2
-    MB_CUDA(cudaMemcpyAsync(fg0, gf, sizeof(float) * G * F, cudaMemcpyDeviceToDevice, s));
-    mul_dtanh(fg0, fact[Lf], (long)G * F, s);
-    float* cur = fg0;
-    float* nxt = fg1;
-    for (int l = Lf - 1; l >= 0; --l) {
-        const int in = fsz[l], out = fsz[l + 1];
-        GemmDesc d;  // dW[j][i] = sum_g gz[g][j] a_l[g][i]
-        d.A = cur; d.am = 1; d.ak = out;
-        d.B = fact[l]; d.bk = in; d.bn = 1;
-        d.C = g + fwoff[l]; d.cm = in; d.cn = 1;
-        d.M = out; d.N = in; d.K = G;
-        gemm("feature_bwd", d, s);
-        colsum_rows(cur, G, out, g + fboff[l], s);
-        if (l > 0) {
-            GemmDesc e;  // g_prev[g][i] = (sum_j gz[g][j] W[j][i]) (1 - a_l^2)
-            e.A = cur; e.am = out; e.ak = 1;
-            e.B = p + fwoff[l]; e.bk = in; e.bn = 1;
-            e.C = nxt; e.cm = in; e.cn = 1;
-            e.M = G; e.N = in; e.K = out;
-            e.act = 2; e.aux = fact[l]; e.xm = in; e.xn = 1;
-            gemm("feature_bwd", e, s);
-            std::swap(cur, nxt);
-        }
+    {  // df reduction + feature-map backward (all layers' dW, db)
+        double fl = 0;
+        for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 4.0 * G * fsz[l] * fsz[l + 1];
+        ProfScope ps("feature_bwd", fl, 0, s);
+        feature_backward(fd, p, w_last, parts, splits, G, g, s);
     }
 }
 
@@ -478,6 +465,12 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
 }
 
 Trainer::~Trainer() {
+    join_worker();
+    for (auto& p : plan_) {
+        if (p.rows) cudaFreeHost(p.rows);
+        if (p.goff) cudaFreeHost(p.goff);
+        if (p.uploaded) cudaEventDestroy(p.uploaded);
+    }
     if (g_prof == &prof_) g_prof = nullptr;
     actor_.free_all();
     critic_.free_all();
@@ -576,6 +569,15 @@ void Trainer::alloc() {
         }
     }
     rows_tmp_.assign((size_t)Bmax_ + 1, 0);
+    for (auto& p : plan_) {
+        MB_CUDA(cudaMallocHost(&p.rows, sizeof(int) * (size_t)slots * Bpmax_));
+        MB_CUDA(cudaMallocHost(&p.goff, sizeof(int) * (size_t)slots * (Kl_ + 1)));
+        p.B.assign(slots, 0);
+        p.Bglob.assign(slots, 0);
+        p.maxg.assign(slots, 0);
+        p.tmp.assign((size_t)Bmax_ + 1, 0);
+        MB_CUDA(cudaEventCreateWithFlags(&p.uploaded, cudaEventDisableTiming));
+    }
     d_mbloss = dalloc<double>((size_t)slots * 2 + 2);
     d_stats = dalloc<double>(4 * 8);
     d_scratch = dalloc<double>(148 * 2 * 8);
@@ -631,8 +633,8 @@ void Trainer::phase_rollout(int it) {
     {
         ProfScope ps("pack_theta", 0, (double)Kl_ * (actor_.P * 4 + pol_plan_.blob_bytes + critic_.P * 4 +
                                                        cri_plan_.blob_bytes), s_);
-        pack_theta(actor_.theta + (long)g_lo_ * actor_.P, Kl_, actor_.tgt, pol_plan_, d_pol_blob, s_);
-        pack_theta(critic_.theta + (long)g_lo_ * critic_.P, Kl_, critic_.tgt, cri_plan_, d_cri_blob, s_);
+        pack_theta(actor_.theta + (long)g_lo_ * actor_.ld, actor_.ld, Kl_, actor_.tgt, pol_plan_, d_pol_blob, s_);
+        pack_theta(critic_.theta + (long)g_lo_ * critic_.ld, critic_.ld, Kl_, critic_.tgt, cri_plan_, d_cri_blob, s_);
     }
     RolloutTcArgs a{};
     a.pol_plan = pol_plan_;
@@ -641,8 +643,10 @@ void Trainer::phase_rollout(int it) {
     a.cri_blob = d_cri_blob;
     a.kind = es_.kind; a.N = Nl_; a.T = cfg_.T; a.K = Kl_; a.reps = reps_;
     a.od = es_.obs_dim; a.ad = es_.act_dim; a.m = m; a.sdim = es_.state_dim; a.max_steps = es_.max_steps;
-    a.theta = actor_.theta + (long)g_lo_ * actor_.P;
-    a.phi = critic_.theta + (long)g_lo_ * critic_.P;
+    a.theta = actor_.theta + (long)g_lo_ * actor_.ld;
+    a.theta_ld = actor_.ld;
+    a.phi = critic_.theta + (long)g_lo_ * critic_.ld;
+    a.phi_ld = critic_.ld;
     a.pol = actor_.tgt; a.cri = critic_.tgt;
     a.state = d_state; a.env_key = d_ekey; a.env_ctr = d_ectr; a.steps = d_steps;
     a.roll_key = iter.split(1).key;  // train.cpp:146
@@ -661,36 +665,81 @@ void Trainer::phase_rollout(int it) {
         ProfScope ps("rollout", 2.0 * macs * Rl_, 0, s_);
         rollout_tc(a, s_);
     }
-    launches_ += 3;
     prepare_perms(it);  // host work overlaps the rollout on the GPU
 }
 
-void Trainer::prepare_perms(int it) {
+void Trainer::build_plan(PermPlan& p, int it, const std::vector<int>& perm_before, long version) {
+    if (p.uploaded) MB_CUDA(cudaEventSynchronize(p.uploaded));  // pinned buffers free again
+    p.it = -1;
+    p.perm = perm_before;
     const HostRng iter = root_.split(0x10000000ULL + (uint64_t)it);
     HostRng sh = iter.split(2);  // train.cpp:156
     const long R = (long)cfg_.N * cfg_.T;
     const int mbs = cfg_.minibatch_count;
+    int* perm = p.perm.data();
     for (int e = 0; e < cfg_.epochs; ++e) {
         for (long i = R; i > 1; --i) {  // rng.hpp:71-76 Fisher-Yates
             const long j = (long)sh.next_below((uint64_t)i);
-            std::swap(perm_[i - 1], perm_[j]);
+            std::swap(perm[i - 1], perm[j]);
         }
         for (int s = 0; s < mbs; ++s) {
             const int slot = e * mbs + s;
             const int lo = (int)(R * s / mbs), hi = (int)(R * (s + 1) / mbs);  // train.cpp:163-169
             int nrows = 0, mx = 0;
-            int* goff = h_goff_pinned + (size_t)slot * (Kl_ + 1);
-            shard_minibatch(perm_.data(), lo, hi, cfg_.T, inst_lo_, Nl_, reps_, Kl_, rows_tmp_.data(), goff, &nrows,
-                            &mx);
-            mb_Bglob_[slot] = hi - lo;
-            mb_maxg_[slot] = pad_groups(rows_tmp_.data(), goff, Kl_, h_rows_pinned + (size_t)slot * Bpmax_,
-                                        &mb_B_[slot]);
+            int* goff = p.goff + (size_t)slot * (Kl_ + 1);
+            shard_minibatch(perm, lo, hi, cfg_.T, inst_lo_, Nl_, reps_, Kl_, p.tmp.data(), goff, &nrows, &mx);
+            p.Bglob[slot] = hi - lo;
+            p.maxg[slot] = pad_groups(p.tmp.data(), goff, Kl_, p.rows + (size_t)slot * Bpmax_, &p.B[slot]);
         }
     }
-    const int slots = cfg_.epochs * mbs;
-    MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (size_t)slots * Bpmax_, cudaMemcpyHostToDevice, s_));
-    MB_CUDA(cudaMemcpyAsync(d_goff, h_goff_pinned, sizeof(int) * (size_t)slots * (Kl_ + 1), cudaMemcpyHostToDevice,
-                            s_));
+    p.version = version;
+    p.it = it;
+}
+
+void Trainer::join_worker() {
+    if (worker_.joinable()) worker_.join();
+}
+
+void Trainer::set_perm(const int* in) {
+    join_worker();
+    std::memcpy(perm_.data(), in, sizeof(int) * perm_.size());
+    ++perm_version_;
+}
+
+void Trainer::prepare_perms(int it) {
+    join_worker();
+    int use = -1;
+    for (int b = 0; b < 2; ++b)
+        if (plan_[b].it == it && plan_[b].version == perm_version_) use = b;
+    if (use < 0) {  // no look-ahead plan (first iteration, perm set externally, iteration skipped)
+        use = worker_plan_ >= 0 ? worker_plan_ : 0;
+        build_plan(plan_[use], it, perm_, perm_version_);
+    }
+    PermPlan& p = plan_[use];
+    perm_.swap(p.perm);
+    p.perm.clear();
+    p.it = -1;  // consumed
+    ++perm_version_;
+    mb_B_ = p.B;
+    mb_Bglob_ = p.Bglob;
+    mb_maxg_ = p.maxg;
+    const int slots = cfg_.epochs * cfg_.minibatch_count;
+    MB_CUDA(cudaMemcpyAsync(d_rows, p.rows, sizeof(int) * (size_t)slots * Bpmax_, cudaMemcpyHostToDevice, s_));
+    MB_CUDA(cudaMemcpyAsync(d_goff, p.goff, sizeof(int) * (size_t)slots * (Kl_ + 1), cudaMemcpyHostToDevice, s_));
+    MB_CUDA(cudaEventRecord(p.uploaded, s_));
+    // look ahead: the next iteration's plan on the other buffer, from the
+    // permutation this iteration leaves behind
+    const int nxt = use ^ 1;
+    worker_plan_ = nxt;
+    const long ver = perm_version_;
+    std::vector<int> base = perm_;
+    worker_ = std::thread([this, nxt, it, ver, base = std::move(base)]() {
+        try {
+            build_plan(plan_[nxt], it + 1, base, ver);
+        } catch (...) {
+            plan_[nxt].it = -1;  // rebuilt (and the error raised) synchronously when needed
+        }
+    });
 }
 
 void Trainer::phase_advantages() {
@@ -714,7 +763,6 @@ void Trainer::phase_advantages() {
     if (comm_) comm_allreduce_f64(comm_, sum2, m, s_);
     stats_finalize(sum2, rows, m, inv, 1, s_);
     scalarize(Nl_, cfg_.T, m, d_adv, d_cw + (size_t)g_lo_ * m, reps_, mean, inv, d_sadv, s_);
-    launches_ += 8;
 }
 
 // One net's loss + backward through its generated weights on one minibatch
@@ -727,15 +775,15 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
     const NetDims& nd = h.tgt;
     const int L = nd.L;
     UpdBufs& u = ub_[is_actor ? 0 : 1];
-    float* gth = h.gtheta + (long)g_lo_ * h.P;
+    float* gth = h.gtheta + (long)g_lo_ * h.ld;
     float *d_psum = u.psum, *d_psls = u.psls;
     double* d_lossrows = u.lossrows;
     if (Bp == 0) {
-        MB_CUDA(cudaMemsetAsync(gth, 0, sizeof(float) * Kl_ * h.P, s_));
+        MB_CUDA(cudaMemsetAsync(gth, 0, sizeof(float) * Kl_ * h.ld, s_));
         MB_CUDA(cudaMemsetAsync(d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, sizeof(double), s_));
         return;
     }
-    const float* th = h.theta + (long)g_lo_ * h.P;
+    const float* th = h.theta + (long)g_lo_ * h.ld;
     {
         ProfScope ps("pack_weights", 0, 6.0 * Kl_ * nd.mlp_n, s_);
         h.pack_weights(g_lo_, Kl_, s_);
@@ -754,7 +802,7 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         d.B = wl(l); d.b_view = 0;                     // (n = out, k = in)
         d.M = Bp; d.N = nd.sz[l + 1]; d.K = nd.sz[l]; d.Z = Kl_;
         d.gmode = 1; d.goff = goff; d.max_group = maxg;
-        d.bias = th + nd.boff[l]; d.bias_gs = h.P; d.bias_mode = 1;
+        d.bias = th + nd.boff[l]; d.bias_gs = h.ld; d.bias_mode = 1;
         if (last) {
             d.C = u.Zf; d.cm = 16; d.cn = 1;  // Gaussian mean / values (pre-activation)
         } else {
@@ -763,15 +811,15 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         igemm("mlp_fwd", d, s_);
     }
     if (is_actor) {  // losses.cpp:87-129
-        actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, th, h.P, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
+        actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, th, h.ld, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
                        (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], d_psum, d_psls, d_lossrows,
                        d_err, s_);
-        tile_segsum(d_psls, 16, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.P, s_);  // log-std grads
+        tile_segsum(d_psls, 16, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.ld, s_);  // log-std grads
     } else {  // losses.cpp:170-185
         critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], d_psum, d_lossrows, s_);
     }
-    tile_segsum(d_psum, 16, nd.sz[L], goff, Kl_, gth + nd.boff[L - 1], h.P, s_);  // output-layer bias grads
-    sum_f64(d_lossrows, Bp, d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, s_);
+    tile_segsum(d_psum, 16, nd.sz[L], goff, Kl_, gth + nd.boff[L - 1], h.ld, s_);  // output-layer bias grads
+    sum_f64(d_lossrows, Bp / 128, d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, s_);  // tile partials
     for (int l = L - 1; l >= 0; --l) {  // backward (nn.cpp:111-160)
         const Img& ain = l == 0 ? Xi_ : u.A[l - 1];
         IGemm d;  // dW_l[z][j][i] = sum_{q in z} G_l[q][j] A_{l-1}[q][i]
@@ -779,7 +827,7 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         d.B = ain; d.b_view = 1;     // (n = i, k = q)
         d.M = nd.sz[l + 1]; d.N = nd.sz[l]; d.K = Bp; d.Z = Kl_;
         d.gmode = 2; d.goff = goff;
-        d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = h.P;
+        d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = h.ld;
         igemm("mlp_dW", d, s_);
         if (l > 0) {
             IGemm e;  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
@@ -791,14 +839,13 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
             e.O = u.G[l - 1]; e.o_mode = 1;
             e.psum = d_psum; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
             igemm("mlp_dX", e, s_);
-            tile_segsum(d_psum, nd.sz[l], nd.sz[l], goff, Kl_, gth + nd.boff[l - 1], h.P, s_);
+            tile_segsum(d_psum, nd.sz[l], nd.sz[l], goff, Kl_, gth + nd.boff[l - 1], h.ld, s_);
         }
     }
-    launches_ += 4 * L + 5;
 }
 
 void Trainer::allgather_gtheta(HyperNet& h) {
-    if (comm_) comm_allgather_f32(comm_, h.gtheta, (size_t)Kl_ * h.P, s_);
+    if (comm_) comm_allgather_f32(comm_, h.gtheta, (size_t)Kl_ * h.ld, s_);
 }
 
 // One PPO minibatch (train.cpp:163-180). The actor chain runs on s_, the
@@ -817,7 +864,6 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         gather_pad(rows, Bp, d_sadv, 1, d_sa, s_);
         gather_pad(rows, Bp, d_tgt, m, d_tg, s_);
         fill_row_group(goff, Kl_, d_rowgroup, Bp, s_);
-        launches_ += 6;
     }
     MB_CUDA(cudaEventRecord(ev_gather_, s_));
     MB_CUDA(cudaStreamWaitEvent(s2_, ev_gather_, 0));
@@ -838,7 +884,6 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     MB_CUDA(cudaEventRecord(ev_c_done_, s2_));
     actor_.backward(s_);
     actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
-    launches_ += 2 * (10 + 4 * (int)actor_.fsz.size()) + 3;
 }
 
 void Trainer::phase_update(int it, int max_minibatches) {

@@ -60,11 +60,14 @@ struct HyperNet {
     std::vector<long> fwoff, fboff;
     NetDims tgt{};
     long nf = 0, P = 0, n = 0;
+    long ld = 0;  // row stride of theta / gtheta (P rounded up to 8: aligned vector stores)
     float *p = nullptr, *g = nullptr, *m1 = nullptr, *m2 = nullptr;
     long steps[3] = {0, 0, 0};
     std::vector<float*> fact;  // feature activations [G][fsz[l]], l = 0..Lf
     float *theta = nullptr, *gtheta = nullptr, *gf = nullptr, *parts = nullptr;
-    float *fg0 = nullptr, *fg1 = nullptr;
+    std::vector<float*> fgz;   // feature pre-activation gradients [G][fsz[l+1]]
+    FeatDims fd{};             // device view of the feature MLP (feature.cu)
+    const float* w_last = nullptr;  // cluster weights of the last forward (feature-map input)
     int splits = 1;
     int* d_split_bounds = nullptr;
     // bf16 tiled images (img.cuh) feeding the tcgen05 GEMMs
@@ -128,7 +131,8 @@ public:
     int local_envs() const { return Nl_; }
     int local_groups() const { return Kl_; }
     cudaStream_t stream() const { return s_; }
-    std::vector<int>& perm() { return perm_; }
+    const std::vector<int>& perm() const { return perm_; }
+    void set_perm(const int* p);  // invalidates the look-ahead plan
     const std::vector<float>& clusters_host() const { return cw_h_; }
     // device batch
     float *d_obs = nullptr, *d_act = nullptr, *d_lp = nullptr, *d_rew = nullptr, *d_val = nullptr,
@@ -140,12 +144,30 @@ public:
     float* d_tracker = nullptr;
     int* d_err = nullptr;
     unsigned long long* d_clamps = nullptr;
-    long kernel_launches() const { return launches_; }
+    long kernel_launches() const { return g_kernel_launches.load(); }  // process-wide
     Profiler& profiler() { return prof_; }
 
 private:
     void alloc();
     void prepare_perms(int it);
+    // Minibatch plan of one iteration (train.cpp:156-169): the shuffled
+    // persistent permutation and every minibatch's sharded, group-padded row
+    // map. Pure host work keyed by the iteration's RNG lane, so the plan for
+    // it+1 is built on a worker thread while the GPU runs iteration it.
+    struct PermPlan {
+        int it = -1;
+        long version = -1;       // perm_version_ it was built from
+        std::vector<int> perm;   // permutation after this iteration's shuffles
+        int* rows = nullptr;     // pinned [slots][Bpmax]
+        int* goff = nullptr;     // pinned [slots][Kl+1]
+        std::vector<int> B, Bglob, maxg, tmp;
+        cudaEvent_t uploaded = nullptr;  // last upload from these pinned buffers
+    } plan_[2];
+    void build_plan(PermPlan& p, int it, const std::vector<int>& perm_before, long version);
+    void join_worker();
+    std::thread worker_;
+    int worker_plan_ = -1;
+    long perm_version_ = 0;
     void minibatch(int slot, int B, int Bglob, int maxg, const int* d_rows, const int* d_goff);
     void net_step(HyperNet& h, bool actor, int Bp, float inv_B, int maxg, const int* rows, const int* d_goff,
                   int slot, cudaStream_t st);
@@ -191,7 +213,6 @@ private:
     NetPlan pol_plan_{}, cri_plan_{};
     uint8_t *d_pol_blob = nullptr, *d_cri_blob = nullptr;
     int mb_done_ = 0;
-    long launches_ = 0;
     Profiler prof_;
 };
 
