@@ -136,6 +136,8 @@ int morlax_trainer_sizes(morlax_trainer* t, int64_t* actor_params, int64_t* crit
 /* which: 0 actor, 1 critic. fp64 reference flat layout */
 int morlax_trainer_get_params(morlax_trainer* t, int which, double* out);
 int morlax_trainer_set_params(morlax_trainer* t, int which, const double* in);
+/* flat hypernet gradient of the last backward pass (morlax_trainer_losses
+ * or the last minibatch of an iteration) */
 int morlax_trainer_get_grad(morlax_trainer* t, int which, double* out);
 int morlax_trainer_get_theta(morlax_trainer* t, int which, float* out /* local K x P */);
 /* field: obs action_pre logprob reward value next_value advantages

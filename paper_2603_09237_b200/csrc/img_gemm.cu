@@ -203,8 +203,25 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
                 const uint8_t* xb = d.aux.p + rowo_x + colo;
                 uint8_t* ob = d.O.p + rowo_o + colo;
                 // EPI 0: first row of this warp's 32-row slab, first column of the half
-                float* cwarp = d.C ? d.C + cz * d.c_gs + (long)(ti.m0 + lg * 32) * d.cm + cb : nullptr;
+                const long wofs = cz * d.c_gs + (long)(ti.m0 + lg * 32) * d.cm + cb;
                 float* stg = sstg + ew * 512;
+                // transpose the warp's 32 rows x 16 columns through shared memory
+                // (XOR-swizzled float4 slots, conflict-free both ways) so every
+                // store instruction writes 8 rows x 64 contiguous bytes
+                auto stage_store = [&](float* dst, const float* x) {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+                        *reinterpret_cast<float4*>(stg + lane * 16 + ((h ^ ((lane >> 1) & 3)) << 2)) =
+                            make_float4(x[4 * h], x[4 * h + 1], x[4 * h + 2], x[4 * h + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int s8 = 0; s8 < 4; ++s8) {
+                        const int r = s8 * 8 + (lane >> 2), h = lane & 3;
+                        const float4 y = *reinterpret_cast<const float4*>(stg + r * 16 + ((h ^ ((r >> 1) & 3)) << 2));
+                        *reinterpret_cast<float4*>(dst + (long)r * d.cm + h * 4) = y;
+                    }
+                    __syncwarp();
+                };
                 // chunk ci = columns cb + 16 ci .. +15, inside one 128-column chunk
                 // for every BN ((cb & 127) + 16 ci <= 112): 2 core-matrix columns
                 auto coff = [](int ci) -> long { return (long)ci * 256; };
@@ -236,21 +253,7 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
                         for (int i = 0; i < 16; ++i) v[i] += bm;
                     }
                     if (EPI == 0) {
-                        // transpose the warp's 32 rows x 16 columns through shared memory
-                        // (XOR-swizzled float4 slots, conflict-free both ways) so every
-                        // store instruction writes 8 rows x 64 contiguous bytes
-#pragma unroll
-                        for (int h = 0; h < 4; ++h)
-                            *reinterpret_cast<float4*>(stg + lane * 16 + ((h ^ ((lane >> 1) & 3)) << 2)) =
-                                make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
-                        __syncwarp();
-#pragma unroll
-                        for (int s8 = 0; s8 < 4; ++s8) {
-                            const int r = s8 * 8 + (lane >> 2), h = lane & 3;
-                            const float4 x = *reinterpret_cast<const float4*>(stg + r * 16 + ((h ^ ((r >> 1) & 3)) << 2));
-                            *reinterpret_cast<float4*>(cwarp + (long)r * d.cm + ci * 16 + h * 4) = x;
-                        }
-                        __syncwarp();
+                        stage_store(d.C + wofs + ci * 16, v);
                         continue;
                     }
                     if (EPI == 1) {
@@ -517,6 +520,41 @@ void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst
     if (units == 0) return;
     dim3 grid((unsigned)std::min<long>((units + 255) / 256, 4096), G);
     k_to_img<<<grid, 256, 0, s>>>(src, ld, src_gs, R, C, dst);
+    MB_LAUNCH();
+}
+
+// generated weights theta[g0 + z][woff_l + j * in_l + i] -> layer images of
+// group z (row j, col i), every layer of every group in one launch; one thread
+// per 8-column unit (coalesced fp32 reads, one 16-byte image store)
+__global__ void k_pack_weights(const float* __restrict__ theta, long ld, int g0, int ng, PackDims pd, uint8_t* wimg,
+                               long gs) {
+    const long per = pd.ustart[pd.L];
+    for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < per * ng; u += (long)gridDim.x * blockDim.x) {
+        const int z = (int)(u / per);
+        const long r = u - (long)z * per;
+        int l = 0;
+        while (r >= pd.ustart[l + 1]) ++l;
+        const int in = pd.in[l], cpr = (in + 7) >> 3;
+        const int e = (int)(r - pd.ustart[l]);
+        const int j = e / cpr, c = (e - j * cpr) * 8;
+        const float* src = theta + (long)(g0 + z) * ld + pd.woff[l] + (long)j * in + c;
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = c + q < in ? src[q] : 0.f;
+        uint4 w;
+        w.x = umma::pack_bf16(v[0], v[1]);
+        w.y = umma::pack_bf16(v[2], v[3]);
+        w.z = umma::pack_bf16(v[4], v[5]);
+        w.w = umma::pack_bf16(v[6], v[7]);
+        *reinterpret_cast<uint4*>(wimg + (long)z * gs + pd.ioff[l] + img_off(j, c, img_ct(in))) = w;
+    }
+}
+void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
+                  cudaStream_t s) {
+    const long n = pd.ustart[pd.L] * ng;
+    if (n == 0) return;
+    k_pack_weights<<<(unsigned)std::min<long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(theta, ld, g0, ng, pd, wimg,
+                                                                                     gs);
     MB_LAUNCH();
 }
 

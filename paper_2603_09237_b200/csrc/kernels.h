@@ -61,6 +61,15 @@ void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, 
 void img_gemm(const IGemm& d, cudaStream_t s);
 // dst(r, c) <- src[z*src_gs + r*ld + c] for z < G (dst.gs per z)
 void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
+// all layers' generated weights of groups [g0, g0+ng) -> per-group layer images
+struct PackDims {
+    int L = 0;
+    int in[8] = {}, out[8] = {};
+    long woff[8] = {}, ioff[8] = {};
+    long ustart[9] = {};  // 8-column units per group before layer l
+};
+void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
+                  cudaStream_t s);
 void gather_img(const int* rows, int Bp, const float* src, int width, const Img& dst, cudaStream_t s);
 void gather_pad(const int* rows, int Bp, const float* src, int width, float* dst, cudaStream_t s);
 void img_segcolsum(const Img& x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg, long c0,

@@ -304,8 +304,6 @@ static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
 // cores theta[g][p] = b[p] + sum_k M[p][k] f[g][k] (hypernet.cpp:73-88) for
 // all groups; [g0, g0+ng) are this rank's clusters.
 void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
-    (void)g0;
-    (void)ng;
     {
         double fl = 0;
         for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 2.0 * G * fsz[l] * fsz[l + 1];
@@ -313,27 +311,31 @@ void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
         w_last = w;
         feature_forward(fd, p, w, G, fimg, s);  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
     }
-    IGemm d;
-    d.A = mimg; d.a_view = 0;          // (m = p, k = f)
-    d.B = fimg; d.b_view = 0;          // (n = g, k = f)
-    d.M = (int)P; d.N = G; d.K = F;
-    d.bias = p + nf + P * F; d.bias_mode = 2;
-    d.C = theta; d.cm = 1; d.cn = ld;  // theta[g][p]
+    IGemm d;  // theta[g][p] = b[p] + sum_k f[g][k] M[p][k]: rows = clusters, contiguous theta rows
+    d.A = fimg; d.a_view = 0;          // (m = g, k = f)
+    d.B = mimg; d.b_view = 0;          // (n = p, k = f)
+    d.M = G; d.N = (int)P; d.K = F;
+    d.bias = p + nf + P * F; d.bias_mode = 1;
+    d.C = theta; d.cm = ld; d.cn = 1;
     igemm("hyper_theta", d, s);
+    PackDims pd;  // generated weights of this rank's clusters -> per-layer bf16 images
+    pd.L = tgt.L;
+    for (int l = 0; l < tgt.L; ++l) {
+        pd.in[l] = tgt.sz[l];
+        pd.out[l] = tgt.sz[l + 1];
+        pd.woff[l] = tgt.woff[l];
+        pd.ioff[l] = wimg_off[l];
+        pd.ustart[l + 1] = pd.ustart[l] + (long)tgt.sz[l + 1] * ((tgt.sz[l] + 7) / 8);
+    }
+    ProfScope ps("pack_weights", 0, 6.0 * ng * tgt.mlp_n, s);
+    pack_weights(theta, ld, g0, ng, pd, wimg.p, wimg.gs, s);
 }
 
 void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, mimg, 1, s); }
 
-void HyperNet::pack_weights(int g0, int ng, cudaStream_t s) {
-    for (int l = 0; l < tgt.L; ++l) {
-        Img dst = wimg;
-        dst.p = wimg.p + wimg_off[l];
-        dst.R = tgt.sz[l + 1];
-        dst.C = tgt.sz[l];
-        to_img(theta + (long)g0 * ld + tgt.woff[l], tgt.sz[l], ld, tgt.sz[l + 1], tgt.sz[l], dst, ng, s);
-    }
-}
-
+// hypernet_backward (hypernet.cpp:92-122) summed over all groups:
+// db = sum_g gtheta_g, dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then
+// the feature-map backward. Writes (not accumulates) the flat grad g.
 // hypernet_backward (hypernet.cpp:92-122) summed over all groups:
 // db = sum_g gtheta_g, dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then
 // the feature-map backward. Writes (not accumulates) the flat grad g.
@@ -784,10 +786,7 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         return;
     }
     const float* th = h.theta + (long)g_lo_ * h.ld;
-    {
-        ProfScope ps("pack_weights", 0, 6.0 * Kl_ * nd.mlp_n, s_);
-        h.pack_weights(g_lo_, Kl_, s_);
-    }
+    // the generated weight images (h.wimg) were written by h.forward's theta GEMM
     auto wl = [&](int l) {
         Img w = h.wimg;
         w.p = h.wimg.p + h.wimg_off[l];

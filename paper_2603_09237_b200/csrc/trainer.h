@@ -76,7 +76,6 @@ struct HyperNet {
     Img gimg;                    // gtheta [G][P]
     Img wimg;                    // generated weights, per group (wimg.gs): layer l at wimg_off[l]
     std::vector<long> wimg_off;
-    void pack_weights(int g0, int ng, cudaStream_t s);  // theta -> wimg for groups [g0, g0+ng)
     void refresh_images(cudaStream_t s);                 // p (M block) -> mimg after external loads
 
     void init(int m_, int F_, const std::vector<int>& fh, const std::vector<int>& target_sizes,
