@@ -558,6 +558,57 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
     MB_LAUNCH();
 }
 
+// gtheta [G][ld] (fp32) -> bf16 image (row g, col p) for the dM / df GEMMs and
+// db[p] = sum_g gtheta[g][p] (hypernet.cpp:92-122) in one read. A block covers
+// 64 8-column units x 4 row slices; the slices' sums combine in a fixed order.
+__global__ void __launch_bounds__(256) k_gtheta_prep(const float* __restrict__ gt, long ld, int G, int P, Img gimg,
+                                                     float* db) {
+    __shared__ float part[4][64][9];
+    const int ul = threadIdx.x & 63, sl = threadIdx.x >> 6;
+    const long u = blockIdx.x * 64L + ul;
+    const int p0 = (int)(u * 8);
+    const int CT = img_ct(gimg.C);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (p0 < P) {
+        const bool full = p0 + 8 <= P;
+        const int rs = (G + 3) / 4, r0 = sl * rs, r1 = min(G, r0 + rs);
+#pragma unroll 4
+        for (int g = r0; g < r1; ++g) {
+            const float* src = gt + (long)g * ld + p0;
+            float v[8];
+            if (full) {
+                const float4 a = *reinterpret_cast<const float4*>(src);
+                const float4 b = *reinterpret_cast<const float4*>(src + 4);
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = p0 + e < P ? src[e] : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += v[e];
+            uint4 w;
+            w.x = umma::pack_bf16(v[0], v[1]);
+            w.y = umma::pack_bf16(v[2], v[3]);
+            w.z = umma::pack_bf16(v[4], v[5]);
+            w.w = umma::pack_bf16(v[6], v[7]);
+            *reinterpret_cast<uint4*>(gimg.p + img_off(g, p0, CT)) = w;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) part[sl][ul][e] = acc[e];
+    __syncthreads();
+    if (sl == 0 && p0 < P)
+        for (int e = 0; e < 8 && p0 + e < P; ++e)
+            db[p0 + e] = (part[0][ul][e] + part[1][ul][e]) + (part[2][ul][e] + part[3][ul][e]);
+}
+void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s) {
+    if (ld % 4) throw ShapeError("gtheta_prep: row stride must be a multiple of 4");
+    const long units = (P + 7) / 8;
+    k_gtheta_prep<<<(unsigned)((units + 63) / 64), 256, 0, s>>>(gt, ld, G, P, gimg, db);
+    MB_LAUNCH();
+}
+
 // gather minibatch rows (row map, -1 = padding) of src[.][width] into an image
 __global__ void k_gather_img(const int* rows, int Bp, const float* __restrict__ src, int width, Img dst) {
     const int CT = img_ct(width);
@@ -581,6 +632,45 @@ void gather_img(const int* rows, int Bp, const float* src, int width, const Img&
     const long units = (long)Bp * ((width + 7) / 8);
     if (units == 0) return;
     k_gather_img<<<(unsigned)std::min<long>((units + 255) / 256, 8192), 256, 0, s>>>(rows, Bp, src, width, dst);
+    MB_LAUNCH();
+}
+
+// the whole minibatch in one launch (losses.cpp:21-33 row selection): thread
+// per padded row q (row map rows[q], -1 = padding -> zeros): observation row ->
+// bf16 image, actions / old log-prob / scalar advantage / value targets -> fp32
+// rows, and the row's cluster (goff search) -> rg
+__global__ void k_gather_minibatch(MbGather a) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= a.Bp) return;
+    const int r = a.rows[q];
+    const bool ok = r >= 0;
+    int lo = 0, hi = a.G;  // goff[lo] <= q < goff[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.goff[mid] <= q) lo = mid;
+        else hi = mid;
+    }
+    a.rg[q] = lo;
+    const int CT = img_ct(a.od);
+    for (int c = 0; c < a.od; c += 8) {
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = (ok && c + e < a.od) ? a.obs[(long)r * a.od + c + e] : 0.f;
+        uint4 w;
+        w.x = umma::pack_bf16(v[0], v[1]);
+        w.y = umma::pack_bf16(v[2], v[3]);
+        w.z = umma::pack_bf16(v[4], v[5]);
+        w.w = umma::pack_bf16(v[6], v[7]);
+        *reinterpret_cast<uint4*>(a.Xi.p + img_off(q, c, CT)) = w;
+    }
+    for (int e = 0; e < a.ad; ++e) a.act_o[(long)q * a.ad + e] = ok ? a.act[(long)r * a.ad + e] : 0.f;
+    for (int e = 0; e < a.m; ++e) a.tgt_o[(long)q * a.m + e] = ok ? a.tgt[(long)r * a.m + e] : 0.f;
+    a.lp_o[q] = ok ? a.lp[r] : 0.f;
+    a.sadv_o[q] = ok ? a.sadv[r] : 0.f;
+}
+void gather_minibatch(const MbGather& a, cudaStream_t s) {
+    if (a.Bp <= 0) return;
+    k_gather_minibatch<<<(a.Bp + 127) / 128, 128, 0, s>>>(a);
     MB_LAUNCH();
 }
 

@@ -70,6 +70,17 @@ struct PackDims {
 };
 void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
                   cudaStream_t s);
+// gtheta [G][ld] -> bf16 image + column sums db[P] (one pass)
+void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s);
+struct MbGather {
+    int Bp = 0, G = 0, od = 0, ad = 0, m = 0;
+    const int *rows = nullptr, *goff = nullptr;
+    const float *obs = nullptr, *act = nullptr, *lp = nullptr, *sadv = nullptr, *tgt = nullptr;
+    Img Xi;
+    float *act_o = nullptr, *lp_o = nullptr, *sadv_o = nullptr, *tgt_o = nullptr;
+    int* rg = nullptr;
+};
+void gather_minibatch(const MbGather& a, cudaStream_t s);
 void gather_img(const int* rows, int Bp, const float* src, int width, const Img& dst, cudaStream_t s);
 void gather_pad(const int* rows, int Bp, const float* src, int width, float* dst, cudaStream_t s);
 void img_segcolsum(const Img& x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg, long c0,

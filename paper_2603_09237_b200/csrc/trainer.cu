@@ -341,8 +341,7 @@ void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, 
 // the feature-map backward. Writes (not accumulates) the flat grad g.
 void HyperNet::backward(cudaStream_t s) {
     const long nM = P * F;
-    colsum_rows(gtheta, G, P, ld, g + nf + nM, s);
-    to_img(gtheta, ld, 0, G, (int)P, gimg, 1, s);
+    gtheta_prep(gtheta, ld, G, (int)P, gimg, g + nf + nM, s);  // gimg + db in one pass
     {
         IGemm d;  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
         d.A = gimg; d.a_view = 1;  // (m = p, k = g)
@@ -857,12 +856,12 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
     if (Bp > 0) {
-        gather_img(rows, Bp, d_obs, od, Xi_, s_);
-        gather_pad(rows, Bp, d_act, ad, d_Z, s_);
-        gather_pad(rows, Bp, d_lp, 1, d_lpo, s_);
-        gather_pad(rows, Bp, d_sadv, 1, d_sa, s_);
-        gather_pad(rows, Bp, d_tgt, m, d_tg, s_);
-        fill_row_group(goff, Kl_, d_rowgroup, Bp, s_);
+        MbGather ga;
+        ga.Bp = Bp; ga.G = Kl_; ga.od = od; ga.ad = ad; ga.m = m;
+        ga.rows = rows; ga.goff = goff;
+        ga.obs = d_obs; ga.act = d_act; ga.lp = d_lp; ga.sadv = d_sadv; ga.tgt = d_tgt;
+        ga.Xi = Xi_; ga.act_o = d_Z; ga.lp_o = d_lpo; ga.sadv_o = d_sa; ga.tgt_o = d_tg; ga.rg = d_rowgroup;
+        gather_minibatch(ga, s_);
     }
     MB_CUDA(cudaEventRecord(ev_gather_, s_));
     MB_CUDA(cudaStreamWaitEvent(s2_, ev_gather_, 0));
@@ -963,12 +962,12 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)n);
     if (Bp > 0) {
-        gather_img(d_rows, Bp, d_obs, od, Xi_, s_);
-        gather_pad(d_rows, Bp, d_act, ad, d_Z, s_);
-        gather_pad(d_rows, Bp, d_lp, 1, d_lpo, s_);
-        gather_pad(d_rows, Bp, d_sadv, 1, d_sa, s_);
-        gather_pad(d_rows, Bp, d_tgt, m, d_tg, s_);
-        fill_row_group(d_goff, Kl_, d_rowgroup, Bp, s_);
+        MbGather ga;
+        ga.Bp = Bp; ga.G = Kl_; ga.od = od; ga.ad = ad; ga.m = m;
+        ga.rows = d_rows; ga.goff = d_goff;
+        ga.obs = d_obs; ga.act = d_act; ga.lp = d_lp; ga.sadv = d_sadv; ga.tgt = d_tgt;
+        ga.Xi = Xi_; ga.act_o = d_Z; ga.lp_o = d_lpo; ga.sadv_o = d_sa; ga.tgt_o = d_tg; ga.rg = d_rowgroup;
+        gather_minibatch(ga, s_);
     }
     net_step(actor_, true, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
     net_step(critic_, false, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
