@@ -11,8 +11,8 @@ for r in rows:
     name = d["Kernel Name"].split("(")[0]
     v = float(d["Metric Value"].replace(",", ""))
     unit = d.get("Metric Unit", "")
-    if unit == "nsecond": v /= 1000
-    elif unit == "msecond": v *= 1000
+    if unit in ("nsecond", "ns"): v /= 1000
+    elif unit in ("msecond", "ms"): v *= 1000
     agg[name][0] += 1; agg[name][1] += v
 tot = sum(a[1] for a in agg.values())
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
