@@ -179,11 +179,22 @@ int morlax_pareto_mask(int n, int m, const double* points, uint8_t* mask_out);
 int morlax_pareto_mask_device(int n, int m, const double* d_points, uint8_t* d_mask, void* stream);
 int morlax_hypervolume_mc(int n, int m, const double* points, const double* reference, uint64_t samples,
                           uint64_t key, uint64_t ctr, double* value, double* stderr_out, uint64_t* hits);
-/* exact for m <= 4 is the reference's recursion (host); above that the
- * reference's Monte-Carlo with `samples` and Rng(seed) on the device */
+/* hypervolume_detailed (pareto.cpp:209-230): exact for m <= 4 (device WFG
+ * recursion, same value as the reference's slicing recursion to fp64
+ * rounding), above that the reference's Monte-Carlo with `samples` and
+ * Rng(seed) on the device (bit-identical hit count) */
 int morlax_hypervolume_detailed(int n, int m, const double* points, const double* reference,
                                 uint64_t samples, uint64_t seed, double* value, double* stderr_out,
                                 int* exact, int* clipped);
+
+/* exact hypervolume for any m <= 8 (new: the reference has no exact
+ * algorithm above m = 4): WFG exclusive-volume recursion on the device,
+ * fp64; points below the reference are clipped (pareto.cpp:191-205) and
+ * counted. The _device form takes device pointers and synchronises `stream`. */
+int morlax_hypervolume_exact(int n, int m, const double* points, const double* reference, double* value,
+                             int* clipped);
+int morlax_hypervolume_exact_device(int n, int m, const double* d_points, const double* d_reference,
+                                    double* value, int* clipped, void* stream);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,7 @@ __all__ = [
     "ConfigError", "ShapeError", "NumericError", "DomainError", "CudaError", "EnvSpec", "env_spec",
     "BatchedEnv", "make_env", "HypernetSpec", "init_hypernet", "hypernet_forward", "hypernet_backward",
     "gae_per_objective", "normalize_and_scalarize", "adam_apply", "TrainConfig", "Trainer",
-    "nondominated_mask", "nondominated_filter", "hypervolume_mc", "hypervolume_detailed",
+    "nondominated_mask", "nondominated_filter", "hypervolume_mc", "hypervolume_detailed", "hypervolume_exact",
     "rng_words", "rng_gaussians", "shard_minibatch", "LIB_PATH",
 ]
 
@@ -463,6 +463,16 @@ def hypervolume_mc(points, reference, samples, key, ctr=0):
                                      C.c_uint64(key), C.c_uint64(ctr), C.byref(v), C.byref(se),
                                      C.byref(h)))
     return v.value, se.value, h.value
+
+
+def hypervolume_exact(points, reference):
+    """Exact hypervolume for any m <= 8 on the device (WFG recursion; the
+    reference is exact only for m <= 4). Returns (value, clipped)."""
+    p = _f64(points).reshape(-1, len(reference))
+    ref = _f64(reference)
+    v, cl = C.c_double(), C.c_int()
+    _check(LIB.morlax_hypervolume_exact(len(p), len(ref), _ptr(p), _ptr(ref), C.byref(v), C.byref(cl)))
+    return v.value, cl.value
 
 
 def hypervolume_detailed(points, reference, samples=1_000_000, seed=0x9E3779B9):

@@ -663,6 +663,28 @@ int morlax_hypervolume_mc(int n, int m, const double* pts, const double* ref, ui
         if (hits_out) *hits_out = h;
     });
 }
+int morlax_hypervolume_exact(int n, int m, const double* pts, const double* ref, double* value, int* clipped) {
+    return guarded([&] {
+        if (m < 1 || m > 8) throw ShapeError("hypervolume: objective count must be in [1, 8]");
+        *value = 0.0;
+        if (clipped) *clipped = 0;
+        if (n <= 0) return;
+        DBuf<double> p(pts, (size_t)n * m), r(ref, m);
+        int c = 0;
+        hv_exact(n, m, p.p, r.p, value, &c, 0);
+        if (clipped) *clipped = c;
+    });
+}
+int morlax_hypervolume_exact_device(int n, int m, const double* d_pts, const double* d_ref, double* value,
+                                    int* clipped, void* stream) {
+    return guarded([&] {
+        if (m < 1 || m > 8) throw ShapeError("hypervolume: objective count must be in [1, 8]");
+        *value = 0.0;
+        int c = 0;
+        if (n > 0) hv_exact(n, m, d_pts, d_ref, value, &c, (cudaStream_t)stream);
+        if (clipped) *clipped = c;
+    });
+}
 int morlax_hypervolume_detailed(int n, int m, const double* pts, const double* ref, uint64_t samples, uint64_t seed,
                                 double* value, double* se, int* exact, int* clipped) {
     return guarded([&] {
@@ -672,7 +694,17 @@ int morlax_hypervolume_detailed(int n, int m, const double* pts, const double* r
             for (int j = 0; j < m; ++j)
                 if (pts[(size_t)i * m + j] < ref[j]) { ++cl; break; }
         if (clipped) *clipped = cl;
-        if (m <= 4) throw ConfigError("exact hypervolume for m <= 4 is not available on the device path yet");
+        if (m > 8) throw ShapeError("hypervolume: objective count must be in [1, 8]");
+        if (m <= 4) {  // pareto.cpp:217-219: exact for m <= 4 (device WFG recursion)
+            if (exact) *exact = 1;
+            if (se) *se = 0.0;
+            *value = 0.0;
+            if (n <= 0) return;
+            DBuf<double> p(pts, (size_t)n * m), r(ref, m);
+            int c2 = 0;
+            hv_exact(n, m, p.p, r.p, value, &c2, 0);
+            return;
+        }
         if (exact) *exact = 0;
         const uint64_t key = seed_key(seed);
         const int rc = morlax_hypervolume_mc(n, m, pts, ref, samples, key, 0, value, se, nullptr);

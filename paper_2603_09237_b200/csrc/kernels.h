@@ -201,6 +201,9 @@ void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, floa
 // ---------------------------------------------------------------- Pareto (K8/K9)
 void pareto_mask(int n, int m, const double* pts, uint8_t* mask, uint8_t* uniq, double* sums,
                  cudaStream_t s);
+// exact hypervolume (WFG recursion, any m <= 8) of the points >= ref;
+// value and clipped count written to host memory (synchronises `s`)
+void hv_exact(int n, int m, const double* d_pts, const double* d_ref, double* value, int* clipped, cudaStream_t s);
 void hv_mc(int n, int m, const double* pts, const double* ref, uint64_t samples, uint64_t key,
            uint64_t ctr, unsigned long long* hits, double* hi_out, cudaStream_t s);
 void rng_words(uint64_t key, uint64_t ctr, long n, uint64_t* out, cudaStream_t s);

@@ -303,3 +303,54 @@ def test_hypervolume_mc_bit_exact(mb, o, g):
     assert hits == ho and v == vo and se == seo
     vd, sed, ex, cl = mb.hypervolume_detailed(p, ref)
     assert (vd, sed, ex) == (vo, seo, False) and cl == 0
+
+
+# ------------------------------------------------------------------ exact hypervolume (device WFG)
+def test_hypervolume_exact_known_answer(mb):  # test_pareto.cpp:130-137
+    pts = np.array([[3.0, 1.0], [1.0, 3.0], [2.0, 2.0]])
+    assert mb.hypervolume_exact(pts, np.zeros(2)) == (6.0, 0)
+    v, se, ex, cl = mb.hypervolume_detailed(pts, np.zeros(2))
+    assert (v, se, ex, cl) == (6.0, 0.0, True, 0)
+    # 3-D: one point is its box; a dominated point and a duplicate add nothing
+    p3 = np.array([[2.0, 3.0, 4.0], [1.0, 1.0, 1.0], [2.0, 3.0, 4.0]])
+    assert mb.hypervolume_exact(p3, np.zeros(3))[0] == 24.0
+
+
+@pytest.mark.parametrize("m", [2, 3, 4])
+def test_hypervolume_exact_matches_reference_recursion(mb, o, g, m):
+    # golden: the reference's own exact hv_recursive (pareto.cpp:145-189)
+    v, se, ex, cl = mb.hypervolume_detailed(g[f"hv_pts{m}"], np.zeros(m))
+    assert ex and se == 0.0
+    assert abs(v - g[f"hv_exact{m}"][0]) <= 1e-12 * abs(g[f"hv_exact{m}"][0])
+    p = _front(300, m, 11 + m)
+    ref = -np.ones(m)
+    vo = o.hypervolume_detailed(p, ref)[0]
+    assert abs(mb.hypervolume_exact(p, ref)[0] - vo) <= 1e-12 * vo
+
+
+def test_hypervolume_exact_m6_matches_oracle_wfg(mb, o, g):
+    v = mb.hypervolume_exact(g["hv_pts6"], np.zeros(6))[0]
+    vo = o.hypervolume_wfg(g["hv_pts6"], np.zeros(6))
+    assert abs(v - vo) <= 1e-12 * abs(vo)
+    # config 5: 1024 points on the 6-simplex projected onto the unit sphere
+    # + N(0, 0.02^2), reference -1^6; exact vs the MC estimate within 4 sigma
+    p = _front(1024, 6, 4)
+    ref = -np.ones(6)
+    v, cl = mb.hypervolume_exact(p, ref)
+    vo = o.hypervolume_wfg(p, ref)
+    assert cl == 0 and abs(v - vo) <= 1e-12 * vo
+    vm, se, _, _ = mb.hypervolume_detailed(p, ref)
+    assert abs(vm - v) <= 4 * se
+
+
+def test_hypervolume_exact_edge_cases(mb):
+    assert mb.hypervolume_exact(np.zeros((0, 3)), np.zeros(3)) == (0.0, 0)
+    # every point below the reference in some coordinate: clipped, volume 0
+    assert mb.hypervolume_exact(np.array([[1.0, -1.0, 1.0], [-2.0, 1.0, 1.0]]), np.zeros(3)) == (0.0, 2)
+    assert mb.hypervolume_exact(np.array([[5.0], [3.0]]), np.array([1.0]))[0] == 4.0
+    q = np.round(np.random.default_rng(5).uniform(0, 1, (200, 4)), 1)  # heavy ties and duplicates
+    v = mb.hypervolume_exact(q, np.zeros(4))[0]
+    vd = mb.hypervolume_detailed(q, np.zeros(4))[0]
+    assert v == vd
+    with pytest.raises(mb.ShapeError):
+        mb.hypervolume_exact(np.zeros((3, 9)), np.zeros(9))
