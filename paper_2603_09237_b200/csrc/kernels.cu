@@ -529,6 +529,205 @@ void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, co
 }
 
 // =========================================================================
+// K5 head: the output layer of the generated MLP, the per-row loss and the
+// output layer's backward in one pass over a 128-row tile of one cluster
+// (losses.cpp:87-132 / 165-185 with nn.cpp:60-92, 111-160 for the last
+// layer). The output layer is only act_dim (12) or m (6) wide -- too narrow
+// for the tensor cores -- so it runs on the CUDA cores in fp32 from the
+// fp32 generated weights W_L [out][H] (staged in shared memory):
+//   o      = b_L + W_L a          (a = last hidden activation row, bf16 image)
+//   g      = dloss/do             (actor: clipped surrogate + entropy;
+//                                  critic: 2 e / B)
+//   g_prev = (W_L^T g) * (1 - a^2)  -> bf16 image (input of the dW / dX GEMMs)
+// plus per-tile column sums of g (output bias grads), of the log-std terms
+// and of g_prev (bias grads of the last hidden layer), and the tile's loss.
+// Padded rows (rows[q] < 0) contribute zeros.
+// =========================================================================
+template <bool ACTOR>
+__global__ void __launch_bounds__(128) k_head(HeadArgs a) {
+    __shared__ __align__(16) float sw[16 * 256];
+    __shared__ float sb[16];
+    __shared__ float red[64];
+    __shared__ float red2[4 * 256];
+    const int H = a.H, out = a.out;
+    const int q = blockIdx.x * 128 + threadIdx.x;
+    const int z = a.rg[blockIdx.x * 128];  // groups are 128-row padded: one cluster per tile
+    const float* th = a.theta + (long)z * a.ld;
+    for (int e = threadIdx.x; e < out * H; e += 128) sw[e] = th[a.woff + e];
+    if (threadIdx.x < out) sb[threadIdx.x] = th[a.boff + threadIdx.x];
+    __syncthreads();
+    const bool live = a.rows[q] >= 0;
+    const int CTa = img_ct(a.A.C), CTg = img_ct(a.Gprev.C), CTo = img_ct(a.Gout.C);
+    // ---- forward of the output layer
+    float o[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j] = 0.f;
+    // activation row: 4 16-byte units (32 columns) in flight per step
+    auto fwd8 = [&](const uint4& u, int c) {
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        float x[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(b2[e]);
+            x[2 * e] = f.x;
+            x[2 * e + 1] = f.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (j >= out) break;
+            const float4 w0 = *reinterpret_cast<const float4*>(sw + j * H + c);
+            const float4 w1 = *reinterpret_cast<const float4*>(sw + j * H + c + 4);
+            o[j] = fmaf(x[0], w0.x, o[j]);
+            o[j] = fmaf(x[1], w0.y, o[j]);
+            o[j] = fmaf(x[2], w0.z, o[j]);
+            o[j] = fmaf(x[3], w0.w, o[j]);
+            o[j] = fmaf(x[4], w1.x, o[j]);
+            o[j] = fmaf(x[5], w1.y, o[j]);
+            o[j] = fmaf(x[6], w1.z, o[j]);
+            o[j] = fmaf(x[7], w1.w, o[j]);
+        }
+    };
+    int c = 0;
+    for (; c + 32 <= H; c += 32) {
+        uint4 u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, c + 8 * k, CTa));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fwd8(u[k], c + 8 * k);
+    }
+    for (; c < H; c += 8) fwd8(*reinterpret_cast<const uint4*>(a.A.p + img_off(q, c, CTa)), c);
+    float g[16], gl[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) g[j] = gl[j] = 0.f;
+    double lrow = 0.0;
+    if (live) {
+        if (ACTOR) {  // losses.cpp:87-129 (action_logprob nn.cpp:204-219)
+            const float* ls_raw = th + a.mlp_n;
+            float lp = 0.f, zn[16], sig[16], ent_h = 0.f;
+#pragma unroll
+            for (int d = 0; d < 16; ++d) {
+                if (d >= out) break;
+                const float ls = fminf(fmaxf(ls_raw[d], -5.f), 1.f);
+                sig[d] = __expf(ls);
+                const float zz = a.z[(long)q * out + d];
+                zn[d] = (zz - (o[d] + sb[d])) / sig[d];
+                lp += -0.5f * zn[d] * zn[d] - ls - 0.9189385332046727f;
+                lp -= __logf(sech2_f(zz) + 1e-6f);
+                ent_h += ls + 0.5f * (1.f + 1.8378770664093453f);
+            }
+            const float ratio = __expf(lp - a.lp_old[q]);
+            if (!isfinite(ratio)) atomicExch(a.err, 3);
+            const float adv = a.sadv[q];
+            const float unc = ratio * adv;
+            const float clp = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip) * adv;
+            lrow = (double)(-fminf(unc, clp) * a.inv_B) - (double)(a.ent * ent_h * a.inv_B);
+            const float glp = unc <= clp ? -ratio * adv * a.inv_B : 0.f;  // losses.cpp:116
+#pragma unroll
+            for (int d = 0; d < 16; ++d) {
+                if (d >= out) break;
+                g[d] = glp * zn[d] / sig[d];
+                const float raw = ls_raw[d];  // clamp mask (losses.cpp:124-128)
+                gl[d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - a.ent * a.inv_B : 0.f;
+            }
+        } else {  // losses.cpp:170-185: sum_k (v - tgt)^2 / B, grad 2 e / B
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k >= out) break;
+                const float e = (o[k] + sb[k]) - a.tgt[(long)q * out + k];
+                lrow += (double)e * e * a.inv_B;
+                g[k] = 2.f * e * a.inv_B;
+            }
+        }
+    }
+    tile_sum_f64(lrow, a.loss_rows + blockIdx.x);
+    for (int h = 0; h < (out + 7) / 8; ++h) {  // output-layer gradient image (dW_L GEMM operand)
+        uint4 w;
+        w.x = umma::pack_bf16(g[8 * h + 0], g[8 * h + 1]);
+        w.y = umma::pack_bf16(g[8 * h + 2], g[8 * h + 3]);
+        w.z = umma::pack_bf16(g[8 * h + 4], g[8 * h + 5]);
+        w.w = umma::pack_bf16(g[8 * h + 6], g[8 * h + 7]);
+        *reinterpret_cast<uint4*>(a.Gout.p + img_off(q, 8 * h, CTo)) = w;
+    }
+    tile_colsum(g, out, red, a.psum + blockIdx.x * 16);
+    if (ACTOR) tile_colsum(gl, out, red, a.psls + blockIdx.x * 16);
+    // ---- backward of the output layer into the last hidden layer
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint4 nxt[2];
+    nxt[0] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, 0, CTa));
+    nxt[1] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, 8, CTa));
+    for (int c = 0; c < H; c += 16) {
+        const uint4 cur[2] = {nxt[0], nxt[1]};
+        if (c + 16 < H) {  // next 16 columns' activations load under this step's FMAs
+            nxt[0] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, c + 16, CTa));
+            nxt[1] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, c + 24, CTa));
+        }
+        float v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {  // W_L^T g: rows of W_L as float4 broadcasts
+            if (j >= out) break;
+            const float4* w4 = reinterpret_cast<const float4*>(sw + j * H + c);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float4 w = w4[k];
+                v[4 * k + 0] = fmaf(g[j], w.x, v[4 * k + 0]);
+                v[4 * k + 1] = fmaf(g[j], w.y, v[4 * k + 1]);
+                v[4 * k + 2] = fmaf(g[j], w.z, v[4 * k + 2]);
+                v[4 * k + 3] = fmaf(g[j], w.w, v[4 * k + 3]);
+            }
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&cur[hh]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(b2[e]);
+                v[8 * hh + 2 * e] *= 1.f - f.x * f.x;
+                v[8 * hh + 2 * e + 1] *= 1.f - f.y * f.y;
+            }
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            uint4 w;
+            w.x = umma::pack_bf16(v[8 * hh + 0], v[8 * hh + 1]);
+            w.y = umma::pack_bf16(v[8 * hh + 2], v[8 * hh + 3]);
+            w.z = umma::pack_bf16(v[8 * hh + 4], v[8 * hh + 5]);
+            w.w = umma::pack_bf16(v[8 * hh + 6], v[8 * hh + 7]);
+            *reinterpret_cast<uint4*>(a.Gprev.p + img_off(q, c + 8 * hh, CTg)) = w;
+        }
+        // warp reduce-scatter of 16 columns over 32 rows (deterministic order)
+        int col = 0;
+#pragma unroll
+        for (int w = 8; w >= 1; w >>= 1) {
+            const bool up = (lane & (2 * w)) != 0;
+            col += up ? w : 0;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+                const float mine = up ? v[w + i] : v[i];
+                const float other = up ? v[i] : v[w + i];
+                v[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * w);
+            }
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        if ((lane & 1) == 0) red2[warp * 256 + c + col] = v[0];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < H; j += 128)
+        a.psum_prev[(long)blockIdx.x * a.psum_prev_ld + j] =
+            (red2[j] + red2[256 + j]) + (red2[512 + j] + red2[768 + j]);
+}
+void head(const HeadArgs& a, bool actor, cudaStream_t s) {
+    if (a.Bp <= 0) return;
+    if (a.H > 256 || a.H % 16 || a.out > 16) throw ShapeError("head: needs hidden width % 16 == 0 (<= 256), out <= 16");
+    if (actor)
+        k_head<true><<<a.Bp / 128, 128, 0, s>>>(a);
+    else
+        k_head<false><<<a.Bp / 128, 128, 0, s>>>(a);
+    MB_LAUNCH();
+}
+
+// =========================================================================
 // K7: Adam (adam.cpp:8-26), eps after sqrt(v_hat); bias corrections from
 // the host in fp64. Skipped entirely once a numeric error is flagged, so
 // the parameters stay at the last healthy state (train.cpp:197-206).

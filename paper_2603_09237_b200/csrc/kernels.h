@@ -34,6 +34,14 @@ struct GemmDesc {
 };
 void gemm_simt(const GemmDesc& d, cudaStream_t s);
 
+// all layers' generated weights of groups [g0, g0+ng) -> per-group layer images
+struct PackDims {
+    int L = 0;
+    int in[8] = {}, out[8] = {};
+    long woff[8] = {}, ioff[8] = {};
+    long ustart[9] = {};  // 8-column units per group before layer l
+};
+
 // ---------------------------------------------------------------- tcgen05 GEMM v2
 // D(m,n) = sum_k A(m,k) B(n,k) over tiled bf16 images (img.cuh), operands
 // streamed by the bulk-copy engine (img_gemm.cu). view 0: (row, col) =
@@ -61,13 +69,6 @@ void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, 
 void img_gemm(const IGemm& d, cudaStream_t s);
 // dst(r, c) <- src[z*src_gs + r*ld + c] for z < G (dst.gs per z)
 void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
-// all layers' generated weights of groups [g0, g0+ng) -> per-group layer images
-struct PackDims {
-    int L = 0;
-    int in[8] = {}, out[8] = {};
-    long woff[8] = {}, ioff[8] = {};
-    long ustart[9] = {};  // 8-column units per group before layer l
-};
 void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
                   cudaStream_t s);
 // gtheta [G][ld] -> bf16 image + column sums db[P] (one pass)
@@ -96,6 +97,26 @@ void actor_rows_img(int Bp, int ad, const int* rows, const int* row_group, const
                     cudaStream_t s);
 void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, const float* tgt, float inv_B,
                      const Img& g_out, float* psum, double* loss_rows, cudaStream_t s);
+// fused output layer + per-row loss + output-layer backward (kernels.cu k_head)
+struct HeadArgs {
+    int Bp = 0, H = 0, out = 0;
+    const int *rows = nullptr, *rg = nullptr;
+    const float* theta = nullptr;  // local clusters' generated params [G][ld]
+    long ld = 0, woff = 0, boff = 0, mlp_n = 0;
+    Img A;                         // last hidden activation image (rows x H)
+    Img Gout, Gprev;               // output-layer gradient image, last-hidden pre-activation gradient image
+    // actor
+    const float *z = nullptr, *lp_old = nullptr, *sadv = nullptr;
+    float clip = 0.f, ent = 0.f;
+    int* err = nullptr;
+    // critic
+    const float* tgt = nullptr;
+    float inv_B = 0.f;
+    float *psum = nullptr, *psls = nullptr, *psum_prev = nullptr;  // [tile][16], [tile][16], [tile][psum_prev_ld]
+    long psum_prev_ld = 0;
+    double* loss_rows = nullptr;
+};
+void head(const HeadArgs& a, bool actor, cudaStream_t s);
 void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2, const int* err,
               long m_lo, int F, const Img& mimg, cudaStream_t s);
 

@@ -4,6 +4,7 @@
 // minibatches of {actor loss, critic loss through the hypernetwork, Adam}.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -481,6 +482,7 @@ Trainer::~Trainer() {
     for (auto* p : img_allocs_) cudaFree(p);
     for (auto& u : ub_) {
         cudaFree(u.psum);
+        cudaFree(u.psum2);
         cudaFree(u.psls);
         cudaFree(u.lossrows);
     }
@@ -565,6 +567,7 @@ void Trainer::alloc() {
         for (int l = 1; l <= critic_.tgt.L; ++l) wmax = std::max(wmax, critic_.tgt.sz[l]);
         for (auto& u : ub_) {
             u.psum = dalloc<float>((size_t)(Bpmax_ / 128) * wmax);
+            u.psum2 = dalloc<float>((size_t)(Bpmax_ / 128) * wmax);
             u.psls = dalloc<float>((size_t)(Bpmax_ / 128) * 16);
             u.lossrows = dalloc<double>(Bpmax_);
         }
@@ -793,7 +796,11 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         w.C = nd.sz[l];
         return w;
     };
-    for (int l = 0; l < L; ++l) {  // forward
+    // the output layer, the loss and the output layer's backward run fused in
+    // k_head on the CUDA cores when there is a hidden layer to feed it
+    const bool fused_head = L >= 2 && nd.sz[L - 1] % 16 == 0 && nd.sz[L - 1] <= 256 && nd.sz[L] <= 16;
+    const int Lg = fused_head ? L - 1 : L;  // layers run as tensor-core GEMMs in the forward
+    for (int l = 0; l < Lg; ++l) {  // forward
         const bool last = (l == L - 1);
         IGemm d;
         d.A = l == 0 ? Xi_ : u.A[l - 1]; d.a_view = 0;  // (m = row, k = in)
@@ -808,7 +815,25 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         }
         igemm("mlp_fwd", d, s_);
     }
-    if (is_actor) {  // losses.cpp:87-129
+    if (fused_head) {
+        HeadArgs ha;
+        ha.Bp = Bp; ha.H = nd.sz[L - 1]; ha.out = nd.sz[L];
+        ha.rows = rows; ha.rg = d_rowgroup;
+        ha.theta = th; ha.ld = h.ld; ha.woff = nd.woff[L - 1]; ha.boff = nd.boff[L - 1]; ha.mlp_n = nd.mlp_n;
+        ha.A = u.A[L - 2]; ha.Gout = u.G[L - 1]; ha.Gprev = u.G[L - 2];
+        ha.z = d_Z; ha.lp_old = d_lpo; ha.sadv = d_sa; ha.clip = (float)cfg_.clip_eps;
+        ha.ent = (float)cfg_.entropy_coef; ha.err = d_err;
+        ha.tgt = d_tg; ha.inv_B = inv_B;
+        ha.psum = d_psum; ha.psls = d_psls; ha.psum_prev = u.psum2; ha.psum_prev_ld = nd.sz[L - 1];
+        ha.loss_rows = d_lossrows;
+        {
+            const double fl = 4.0 * Bp * nd.sz[L - 1] * nd.sz[L];  // forward + backward of the output layer
+            ProfScope ps("mlp_head", fl, 0, s_);
+            head(ha, is_actor, s_);
+        }
+        if (is_actor) tile_segsum(d_psls, 16, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.ld, s_);  // log-std grads
+        tile_segsum(u.psum2, nd.sz[L - 1], nd.sz[L - 1], goff, Kl_, gth + nd.boff[L - 2], h.ld, s_);
+    } else if (is_actor) {  // losses.cpp:87-129
         actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, th, h.ld, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
                        (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], d_psum, d_psls, d_lossrows,
                        d_err, s_);
@@ -827,7 +852,7 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         d.gmode = 2; d.goff = goff;
         d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = h.ld;
         igemm("mlp_dW", d, s_);
-        if (l > 0) {
+        if (l > 0 && !(fused_head && l == L - 1)) {
             IGemm e;  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
             e.A = u.G[l]; e.a_view = 0;  // (m = q, k = j)
             e.B = wl(l); e.b_view = 1;   // (n = i, k = j)
@@ -854,6 +879,12 @@ void Trainer::allgather_gtheta(HyperNet& h) {
 void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, const int* goff) {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
+    // MORLAX_ONE_STREAM=1 serialises the two chains (profiling: per-class times without overlap)
+    static const bool one = [] {
+        const char* e = std::getenv("MORLAX_ONE_STREAM");
+        return e && e[0] == '1';
+    }();
+    cudaStream_t sc = one ? s_ : s2_;
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
     if (Bp > 0) {
         MbGather ga;
@@ -864,10 +895,10 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         gather_minibatch(ga, s_);
     }
     MB_CUDA(cudaEventRecord(ev_gather_, s_));
-    MB_CUDA(cudaStreamWaitEvent(s2_, ev_gather_, 0));
-    critic_.forward(d_cw, g_lo_, Kl_, s2_);  // hypernet_forward per loss (losses.cpp:79,167)
-    net_step(critic_, false, Bp, inv_B, maxg, rows, goff, slot, s2_);
-    MB_CUDA(cudaEventRecord(ev_c_net_, s2_));
+    MB_CUDA(cudaStreamWaitEvent(sc, ev_gather_, 0));
+    critic_.forward(d_cw, g_lo_, Kl_, sc);  // hypernet_forward per loss (losses.cpp:79,167)
+    net_step(critic_, false, Bp, inv_B, maxg, rows, goff, slot, sc);
+    MB_CUDA(cudaEventRecord(ev_c_net_, sc));
     actor_.forward(d_cw, g_lo_, Kl_, s_);
     net_step(actor_, true, Bp, inv_B, maxg, rows, goff, slot, s_);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_net_, 0));
@@ -876,10 +907,10 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
     MB_CUDA(cudaEventRecord(ev_chk_, s_));
-    MB_CUDA(cudaStreamWaitEvent(s2_, ev_chk_, 0));
-    critic_.backward(s2_);
-    critic_.adam_step(cfg_.critic_lr, d_err, s2_);
-    MB_CUDA(cudaEventRecord(ev_c_done_, s2_));
+    MB_CUDA(cudaStreamWaitEvent(sc, ev_chk_, 0));
+    critic_.backward(sc);
+    critic_.adam_step(cfg_.critic_lr, d_err, sc);
+    MB_CUDA(cudaEventRecord(ev_c_done_, sc));
     actor_.backward(s_);
     actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
 }

@@ -195,6 +195,7 @@ private:
         std::vector<Img> G;     // [Bp][out_l] gradient at the pre-activation of layer l
         float* Zf = nullptr;    // [Bp][16] output layer (policy mean / values), fp32
         float *psum = nullptr, *psls = nullptr;  // per-128-row-tile column sums (bias / log-std grads)
+        float* psum2 = nullptr;                  // same for the last hidden layer (k_head)
         double* lossrows = nullptr;
     } ub_[2];
     cudaStream_t s2_ = nullptr;  // critic chain of the update

@@ -1,8 +1,5 @@
-# parity tests + bench + GEMM microbenchmarks (one GPU call)
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+# parity tests + bench (one GPU call); serialised-chain breakdown too
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_gpu.log
+for f in 0 1; do MORLAX_ONE_STREAM=$f timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_s$f.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -3 gpurun_out/bench.err
 python -c "
-import json; d=json.load(open('gpurun_out/bench.json')); print('ms/iter', d['ms_per_step'], 'value', d['value'], 'e2e', d['e2e']['value']); print(d['roofline'])
-for k,v in d['breakdown_ms_per_iter'].items(): print(k, v)
-"
-timeout 300 python tools/gemm_bench.py; timeout 300 python tools/gemm_variants.py
+import json; d=json.load(open('gpurun_out/bench_s$f.json')); print('one_stream=$f ms/iter', round(d['ms_per_step'],2), 'launches', d['gpu_launches']); print({k:(v['ms'],v['launches']) for k,v in d['breakdown_ms_per_iter'].items()})"; done
