@@ -164,6 +164,100 @@ def run_reference(args):
     }))
 
 
+# ---------------------------------------------------------------- other BASELINE configs (rank 0, N = 1)
+def _events_ms(stream, fn, iters):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(iters):
+        fn(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def leg_pr1(mb, cpu):
+    """Config 1 (PR1): mo-pointmass, 256 envs x T 32, 16 preferences, full
+    training iteration; the reference's full iteration beside it."""
+    import torch
+    cfg = mb.TrainConfig(**BASE["pr1"])
+    t = mb.Trainer(cfg)
+    stream = torch.cuda.ExternalStream(mb.LIB.morlax_trainer_stream(t._h))
+    for i in range(3):
+        t.iteration(i)
+    ms = _events_ms(stream, lambda i: t.iteration(3 + i), 10)
+    out = {"workload": WORKLOAD["pr1"], "metric": "env-steps/s", "value": cfg.N * cfg.T / (ms / 1e3),
+           "ms_per_step": ms}
+    if cpu:
+        v, sample, _ = reference_sample(BASE["pr1"], os.cpu_count() or 1)
+        out["cpu_reference"] = {"value": v, "unit": "env-steps/s", "cores": os.cpu_count(), "sample": sample}
+    return out
+
+
+def leg_c2(mb, tflops_peak):
+    """Config 2: hypernetwork + per-preference policy forward microbench: 64
+    preferences ~ Dirichlet(1,1,1), 2048 N(0,1) observations each (131072
+    rows, obs 48, act 12); hypernet 3 -> 256 -> F 256, policy 48-256-256-12,
+    bf16 operands / fp32 accumulation; reference init (seeded) in place of
+    Xavier."""
+    import torch
+    G, R = 64, 2048
+    spec = mb.HypernetSpec(3, 256, [256], [48, 256, 256, 12], True, True)
+    pf = mb.PolicyForward(spec, G, R)
+    pf.set_params(mb.init_hypernet(spec, mb.rng_words(1, 0, 1)[0]))
+    rng = np.random.default_rng(1)
+    w = torch.tensor(rng.dirichlet(np.ones(3), size=G), dtype=torch.float32, device="cuda")
+    obs = torch.tensor(rng.normal(size=(G * R, 48)), dtype=torch.float32, device="cuda")
+    pre = torch.empty((G * R, 12), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    fwd = lambda i: pf.forward_device(w.data_ptr(), obs.data_ptr(), pre.data_ptr(), stream.cuda_stream)
+    for i in range(3):
+        fwd(i)
+    ms = _events_ms(stream, fwd, 20)
+    tf = pf.flops / (ms / 1e3) / 1e12
+    return {"workload": "config2-hypernet+policy-forward-64pref-x2048obs", "metric": "forward_us",
+            "value": ms * 1e3, "unit": "us", "rows_per_s": G * R / (ms / 1e3), "gflop": pf.flops / 1e9,
+            "tflops": tf, "roofline": {"bound": "tensor", "achieved": tf, "peak": tflops_peak,
+                                       "unit": "TFLOP/s", "frac": tf / tflops_peak}}
+
+
+def leg_c4(mb):
+    """Config 4: GAE + PPO update on 262144 synthetic transitions (4096 envs x
+    T 64): rewards / values ~ N(0,1) (6 objectives), next_value = the next
+    step's value (one extra draw at T-1), terminated ~ Bernoulli(0.01),
+    64 preference groups ~ Dirichlet(1^6), obs ~ N(0,1), actions ~ N(0,1),
+    old log-probs ~ N(-36, 1); 4 epochs x 8 minibatches, entropy 0.01,
+    hypernet 6 -> 256 -> F 256 with mo-humanoid6 dims (obs 45, act 12)."""
+    import torch
+    base = dict(BASE["c3"], N=4096, K=64, seed=3)
+    cfg = mb.TrainConfig(**base)
+    t = mb.Trainer(cfg)
+    es, R, N, T = t.es, t.rows, cfg.N, cfg.T
+    rng = np.random.default_rng(3)
+    v = rng.normal(size=(N, T + 1, es.m))
+    t.set("obs", rng.normal(size=(R, es.obs_dim)))
+    t.set("action_pre", rng.normal(size=(R, es.act_dim)))
+    t.set("logprob", rng.normal(-36.0, 1.0, size=R))
+    t.set("reward", rng.normal(size=(R, es.m)))
+    t.set("value", v[:, :T].reshape(R, es.m))
+    t.set("next_value", v[:, 1:].reshape(R, es.m))
+    t.set("terminated", rng.random(R) < 0.01)
+    t.set("truncated", np.zeros(R, np.uint8))
+    t.set("clusters", rng.dirichlet(np.ones(es.m), size=cfg.K))
+    stream = torch.cuda.ExternalStream(mb.LIB.morlax_trainer_stream(t._h))
+
+    def step(i):
+        for ph in (5, 2, 3, 4):
+            t.phase(i, ph)
+
+    for i in range(3):
+        step(i)
+    ms = _events_ms(stream, lambda i: step(3 + i), 5)
+    return {"workload": "config4-gae+ppo-update-4096env-T64-64pref", "metric": "transitions/s",
+            "value": R / (ms / 1e3), "ms_per_step": ms}
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -173,6 +267,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(BASE))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-legs", action="store_true", help="skip the config 1 / 2 / 4 legs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -295,6 +390,10 @@ def main():
         except Exception as ex:  # reported, never silently replaced
             cpu = {"value": None, "unit": "env-steps/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+    legs = None
+    if rank == 0 and world == 1 and not args.no_legs:
+        legs = {"config1_pr1": leg_pr1(mb, not args.no_cpu_baseline), "config2": leg_c2(mb, peaks()[1]),
+                "config4": leg_c4(mb)}
     es = mb.env_spec(cfg.env_name)
     slots = cfg.epochs * cfg.minibatch_count
     bmax = -(-cfg.N * cfg.T // cfg.minibatch_count)
@@ -312,7 +411,7 @@ def main():
             "e2e": {"value": e2e, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-            "breakdown_ms_per_iter": breakdown, "pareto": pareto,
+            "breakdown_ms_per_iter": breakdown, "pareto": pareto, "other_configs": legs,
         }))
     if world > 1:
         dist.destroy_process_group()

@@ -80,6 +80,23 @@ int morlax_hypernet_forward(const morlax_hypernet_spec* spec, const double* flat
 int morlax_hypernet_backward(const morlax_hypernet_spec* spec, const double* flat, const double* w, int G,
                              const double* gtheta /* G*P */, double* grad_out);
 
+/* ---- Per-preference-group policy forward (replaces policy_forward,
+ *      src/nn.cpp:162-190, over hypernet_forward's generated weights,
+ *      src/hypernet.cpp:69-90, for G preferences x R observations each) --- */
+typedef struct morlax_policy morlax_policy;
+int morlax_policy_create(const morlax_hypernet_spec* spec, int groups, int rows_per_group, morlax_policy** out);
+void morlax_policy_destroy(morlax_policy* p);
+/* flat = [feature | M | b] (reference flatten_hypernet order) */
+int morlax_policy_set_params(morlax_policy* p, const double* flat);
+/* w [G][m] on the simplex (ShapeError/DomainError as hypernet_forward),
+ * obs [G*R][obs_dim] grouped by preference -> pre [G*R][out]: the Gaussian
+ * mean before the tanh squash (GaussianAction::pre); host buffers */
+int morlax_policy_forward(morlax_policy* p, const double* w, const float* obs, float* pre_out);
+/* same on device buffers (w as fp32), async on `stream` */
+int morlax_policy_forward_device(morlax_policy* p, const float* d_w, const float* d_obs, float* d_pre, void* stream);
+/* algorithmic FLOPs of one forward (feature MLP + theta GEMM + per-row MLP) */
+double morlax_policy_flops(morlax_policy* p);
+
 /* ---- Advantage estimation (replaces gae_per_objective /
  *      normalize_and_scalarize, include/morlax/trainer.hpp:154-161) ------ */
 int morlax_gae(int N, int T, int m, const float* reward, const float* value, const float* next_value,
@@ -129,7 +146,9 @@ void morlax_trainer_destroy(morlax_trainer* t);
  * preferences and minibatch indices, D2H of the stats, inside the call) */
 int morlax_trainer_iteration(morlax_trainer* t, int it, morlax_iter_stats* stats);
 /* phases: 1 sampling + rollout, 2 GAE + normalise, 3 update (first
- * max_minibatches, -1 = all), 4 finish (sync, stats, NumericError) */
+ * max_minibatches, -1 = all), 4 finish (sync, stats, NumericError),
+ * 5 minibatch plans only (instead of 1 when the batch and the clusters were
+ * set through morlax_trainer_set: the GAE + PPO update of config 4) */
 int morlax_trainer_phase(morlax_trainer* t, int it, int phase, int max_minibatches, morlax_iter_stats* stats);
 int morlax_trainer_sizes(morlax_trainer* t, int64_t* actor_params, int64_t* critic_params, int* local_envs,
                          int* local_clusters, int* rows_per_iteration);

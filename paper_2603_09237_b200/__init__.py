@@ -27,7 +27,7 @@ from ._lib import LIB, LIB_PATH  # noqa: F401  (loads / builds the CUDA library)
 
 __all__ = [
     "ConfigError", "ShapeError", "NumericError", "DomainError", "CudaError", "EnvSpec", "env_spec",
-    "BatchedEnv", "make_env", "HypernetSpec", "init_hypernet", "hypernet_forward", "hypernet_backward",
+    "BatchedEnv", "make_env", "HypernetSpec", "PolicyForward", "init_hypernet", "hypernet_forward", "hypernet_backward",
     "gae_per_objective", "normalize_and_scalarize", "adam_apply", "TrainConfig", "Trainer",
     "nondominated_mask", "nondominated_filter", "hypervolume_mc", "hypervolume_detailed", "hypervolume_exact",
     "rng_words", "rng_gaussians", "shard_minibatch", "LIB_PATH",
@@ -222,6 +222,47 @@ def hypernet_forward(spec: HypernetSpec, flat, w) -> np.ndarray:
     _check(LIB.morlax_hypernet_forward(C.byref(spec.c()), _ptr(_f64(flat)), _ptr(w), len(w),
                                        _ptr(out)))
     return out
+
+
+class PolicyForward:
+    """Per-preference-group policy forward (BASELINE config 2): G preference
+    vectors, R observations each, through the weights the hypernetwork
+    generates for each preference (policy_forward nn.cpp:162-190 over
+    hypernet_forward hypernet.cpp:69-90). forward() returns the Gaussian mean
+    before the tanh squash, [G*R][out]."""
+
+    def __init__(self, spec: HypernetSpec, groups: int, rows_per_group: int):
+        self.spec, self.G, self.R = spec, groups, rows_per_group
+        h = C.c_void_p()
+        _check(LIB.morlax_policy_create(C.byref(spec.c()), groups, rows_per_group, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.morlax_policy_destroy(self._h)
+            self._h = None
+
+    def set_params(self, flat):
+        f = _f64(flat)
+        if f.size != self.spec.param_count:
+            raise ShapeError("policy forward: flat parameter vector has the wrong length")
+        _check(LIB.morlax_policy_set_params(self._h, _ptr(f)))
+
+    def forward(self, w, obs) -> np.ndarray:
+        w = _f64(w).reshape(self.G, self.spec.m)
+        od, out = self.spec.target_sizes[0], self.spec.target_sizes[-1]
+        o = np.ascontiguousarray(obs, np.float32).reshape(self.G * self.R, od)
+        pre = np.zeros((self.G * self.R, out), np.float32)
+        _check(LIB.morlax_policy_forward(self._h, _ptr(w), _ptr(o), _ptr(pre)))
+        return pre
+
+    def forward_device(self, w_ptr: int, obs_ptr: int, pre_ptr: int, stream: int = 0):
+        _check(LIB.morlax_policy_forward_device(self._h, C.c_void_p(w_ptr), C.c_void_p(obs_ptr),
+                                                C.c_void_p(pre_ptr), C.c_void_p(stream)))
+
+    @property
+    def flops(self) -> float:
+        return float(LIB.morlax_policy_flops(self._h))
 
 
 def hypernet_backward(spec: HypernetSpec, flat, w, gtheta) -> np.ndarray:

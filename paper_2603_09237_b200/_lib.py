@@ -46,6 +46,12 @@ def _load():
     lib.morlax_trainer_kernel_launches.argtypes = [C.c_void_p]
     lib.morlax_trainer_stream.restype = C.c_void_p
     lib.morlax_trainer_stream.argtypes = [C.c_void_p]
+    lib.morlax_policy_destroy.argtypes = [C.c_void_p]
+    lib.morlax_policy_set_params.argtypes = [C.c_void_p, C.c_void_p]
+    lib.morlax_policy_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.morlax_policy_forward_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.morlax_policy_flops.restype = C.c_double
+    lib.morlax_policy_flops.argtypes = [C.c_void_p]
     for name in ("morlax_env_reset", "morlax_env_step", "morlax_env_current_obs",
                  "morlax_env_step_device", "morlax_trainer_iteration", "morlax_trainer_phase",
                  "morlax_trainer_sizes", "morlax_trainer_get_params", "morlax_trainer_set_params",

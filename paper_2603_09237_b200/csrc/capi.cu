@@ -8,6 +8,7 @@
 
 #include "../../include/morlax_b200.h"
 #include "comm.h"
+#include "policy.h"
 #include "trainer.h"
 
 using namespace mb200;
@@ -97,6 +98,11 @@ struct morlax_env {
 
 struct morlax_trainer {
     Trainer* t = nullptr;
+};
+
+struct morlax_policy {
+    GroupPolicy* p = nullptr;
+    int m = 0;
 };
 
 extern "C" {
@@ -259,6 +265,53 @@ int morlax_hypernet_forward(const morlax_hypernet_spec* s, const double* flat, c
         }
     });
 }
+int morlax_policy_create(const morlax_hypernet_spec* s, int groups, int rows_per_group, morlax_policy** out) {
+    return guarded([&] {
+        if (s->n_target_sizes < 2 || s->n_target_sizes > 9) throw ShapeError("MlpSpec needs at least input and output sizes");
+        auto* h = new morlax_policy;
+        try {
+            h->p = new GroupPolicy(s->m, s->F, vec(s->n_feature_hidden, s->feature_hidden),
+                                   vec(s->n_target_sizes, s->target_sizes), s->target_tanh != 0, s->has_log_std != 0,
+                                   groups, rows_per_group);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        h->m = s->m;
+        *out = h;
+    });
+}
+void morlax_policy_destroy(morlax_policy* h) {
+    if (!h) return;
+    delete h->p;
+    delete h;
+}
+int morlax_policy_set_params(morlax_policy* h, const double* flat) {
+    return guarded([&] {
+        HyperNet& hn = h->p->h;
+        std::vector<float> f(flat, flat + hn.n);
+        MB_CUDA(cudaMemcpy(hn.p, f.data(), sizeof(float) * hn.n, cudaMemcpyHostToDevice));
+        hn.refresh_images(0);
+        MB_CUDA(cudaDeviceSynchronize());
+    });
+}
+int morlax_policy_forward(morlax_policy* h, const double* w, const float* obs, float* pre) {
+    return guarded([&] {
+        GroupPolicy& gp = *h->p;
+        for (int g = 0; g < gp.G; ++g) check_simplex(h->m, w + (size_t)g * h->m);
+        const int od = gp.h.tgt.sz[0], out = gp.h.tgt.sz[gp.h.tgt.L];
+        std::vector<float> wf(w, w + (size_t)gp.G * h->m);
+        DBuf<float> dw(wf.data(), wf.size()), dobs(obs, (size_t)gp.G * gp.R * od), dpre((size_t)gp.G * gp.R * out);
+        gp.forward(dw.p, dobs.p, dpre.p, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        dpre.get(pre);
+    });
+}
+int morlax_policy_forward_device(morlax_policy* h, const float* d_w, const float* d_obs, float* d_pre,
+                                 void* stream) {
+    return guarded([&] { h->p->forward(d_w, d_obs, d_pre, (cudaStream_t)stream); });
+}
+double morlax_policy_flops(morlax_policy* h) { return h ? h->p->flops() : 0.0; }
 int morlax_hypernet_backward(const morlax_hypernet_spec* s, const double* flat, const double* w, int G,
                              const double* gtheta, double* out) {
     return guarded([&] {
@@ -384,6 +437,7 @@ int morlax_trainer_phase(morlax_trainer* t, int it, int phase, int max_mb, morla
             case 2: t->t->phase_advantages(); break;
             case 3: t->t->phase_update(it, max_mb); break;
             case 4: t->t->finish(&st); break;
+            case 5: t->t->phase_plans(it); break;
             default: throw ConfigError("unknown phase");
         }
     });

@@ -672,6 +672,17 @@ void Trainer::phase_rollout(int it) {
     prepare_perms(it);  // host work overlaps the rollout on the GPU
 }
 
+// the update of an externally provided batch (set via the field setters):
+// only the iteration's minibatch plans and the per-iteration resets; the
+// clusters are whatever set_clusters() left (train.cpp:156-169)
+void Trainer::phase_plans(int it) {
+    g_prof = &prof_;
+    MB_CUDA(cudaMemsetAsync(d_retsum, 0, sizeof(double) * Nl_, s_));
+    MB_CUDA(cudaMemsetAsync(d_retcnt, 0, sizeof(int) * Nl_, s_));
+    MB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s_));
+    prepare_perms(it);
+}
+
 void Trainer::build_plan(PermPlan& p, int it, const std::vector<int>& perm_before, long version) {
     if (p.uploaded) MB_CUDA(cudaEventSynchronize(p.uploaded));  // pinned buffers free again
     p.it = -1;

@@ -113,6 +113,7 @@ public:
     void iteration(int it, IterStats* st);
 
     // phases (for tests / bench breakdowns); iteration() runs all of them
+    void phase_plans(int it);  // minibatch plans only (update of an externally set batch)
     void phase_rollout(int it);
     void phase_advantages();
     void phase_update(int it, int max_minibatches = -1);

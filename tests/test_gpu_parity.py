@@ -111,6 +111,47 @@ def test_hypernet_forward_backward(mb, o, F, fh, ah, od, ad, m):
     assert_normwise(gr, gr_o, REL_BF16, what="hypernet grad")
 
 
+def _mlp_pre(theta, sizes, x):
+    """nn.cpp:60-92 mlp_forward restated in numpy (fp64): tanh hidden layers,
+    identity output (the pre-squash Gaussian mean)."""
+    off = 0
+    a = x
+    L = len(sizes) - 1
+    for l in range(L):
+        i, o_ = sizes[l], sizes[l + 1]
+        W = theta[off:off + i * o_].reshape(o_, i)
+        b = theta[off + i * o_:off + i * o_ + o_]
+        off += (i + 1) * o_
+        a = a @ W.T + b
+        if l < L - 1:
+            a = np.tanh(a)
+    return a
+
+
+@pytest.mark.parametrize("F,fh,ah,od,ad,m,G,R", [(16, [16], [32, 32], 4, 2, 2, 3, 50),
+                                                 (256, [256], [256, 256], 48, 12, 3, 8, 256)])
+def test_group_policy_forward(mb, o, F, fh, ah, od, ad, m, G, R):
+    """Per-preference-group policy forward (config-2 shapes scaled down):
+    theta from the oracle's hypernet_forward, then the reference MLP."""
+    from pyoracle import HSpec
+    sizes = [od] + ah + [ad]
+    spec_o = HSpec(m, F, fh, sizes, True, True)
+    spec = mb.HypernetSpec(m, F, fh, sizes, True, True)
+    flat = r32(o.init_hypernet(spec_o, 0x51))
+    rng = np.random.default_rng(1)
+    W = rng.dirichlet(np.ones(m), size=G)
+    obs = r32(rng.normal(size=(G * R, od)))
+    pf = mb.PolicyForward(spec, G, R)
+    pf.set_params(flat)
+    pre = pf.forward(W, obs)
+    ref = np.concatenate([_mlp_pre(o.hypernet_forward(spec_o, flat, W[g]), sizes, obs[g * R:(g + 1) * R])
+                          for g in range(G)])
+    assert pre.shape == ref.shape
+    assert_normwise(pre, ref, REL_BF16, what="policy pre-activation")
+    with pytest.raises(mb.DomainError):
+        pf.forward(np.full((G, m), 0.9), obs)
+
+
 # ------------------------------------------------------------------ GAE / normalise (K4)
 @pytest.mark.parametrize("T", [1, 16, 32, 64, 100])
 def test_gae_scan_parity(mb, o, T):
