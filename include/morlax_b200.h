@@ -196,6 +196,10 @@ int morlax_gemm_bench(int M, int N, int K, int a_view, int b_view, int act, int 
 /* survivors of nondominated_filter as a mask over the input order */
 int morlax_pareto_mask(int n, int m, const double* points, uint8_t* mask_out);
 int morlax_pareto_mask_device(int n, int m, const double* d_points, uint8_t* d_mask, void* stream);
+/* survivors of linear_dominance_filter (pareto.cpp:79-139) as a mask over
+ * the input order: nondominated points that attain max_w w.J (m == 2: the
+ * upper hull, collinear kept; m >= 3: the simplex_grid(m, 60) sweep) */
+int morlax_linear_dominance_mask(int n, int m, const double* points, uint8_t* mask_out);
 int morlax_hypervolume_mc(int n, int m, const double* points, const double* reference, uint64_t samples,
                           uint64_t key, uint64_t ctr, double* value, double* stderr_out, uint64_t* hits);
 /* hypervolume_detailed (pareto.cpp:209-230): exact for m <= 4 (device WFG

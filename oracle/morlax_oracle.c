@@ -1301,6 +1301,88 @@ int mo_hypervolume_detailed(int n, int m, const double* pts, const double* ref, 
     return MO_OK;
 }
 
+/* ---- linear_dominance_filter (pareto.cpp:79-139) as a mask over the input:
+ * nd = nondominated_filter; |nd| <= 2 or m == 1 -> nd; m == 2 -> upper hull
+ * of nd sorted by J1 ascending, collinear points kept (cross > 0 pops);
+ * m >= 3 -> a point survives if w.p >= best - 1e-9 max(1, |best|) for some
+ * w on simplex_grid(m, 60) (simplex.cpp:108-117; w_j = k_j / 60, dot in
+ * coordinate order, simplex.cpp:10-16). */
+static const double* g_ldf_pts;
+static int cmp_j1_asc(const void* a, const void* b) {
+    const double x = g_ldf_pts[(size_t)(*(const int*)a) * 2], y = g_ldf_pts[(size_t)(*(const int*)b) * 2];
+    return x < y ? -1 : x > y ? 1 : 0;
+}
+static void ldf_grid_rec(int m, int res, int remaining, int depth, int* k, const double* nd, int nn,
+                         uint8_t* keep) {
+    if (depth == m - 1) {
+        k[depth] = remaining;
+        double best = -INFINITY;
+        for (int i = 0; i < nn; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < m; ++j) acc += ((double)k[j] / res) * nd[(size_t)i * m + j];
+            best = acc > best ? acc : best;
+        }
+        const double tol = 1e-9 * (fabs(best) > 1.0 ? fabs(best) : 1.0);
+        for (int i = 0; i < nn; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < m; ++j) acc += ((double)k[j] / res) * nd[(size_t)i * m + j];
+            if (acc >= best - tol) keep[i] = 1;
+        }
+        return;
+    }
+    for (int v = remaining; v >= 0; --v) {
+        k[depth] = v;
+        ldf_grid_rec(m, res, remaining - v, depth + 1, k, nd, nn, keep);
+    }
+}
+int mo_linear_dominance_mask(int n, int m, const double* pts, uint8_t* mask) {
+    if (n <= 0) return MO_OK;
+    if (m < 1) return fail(MO_ERR, "linear_dominance_filter: empty points");
+    mo_nondominated_mask(n, m, pts, mask);
+    int nn = 0;
+    for (int i = 0; i < n; ++i) nn += mask[i] != 0;
+    if (nn <= 2 || m == 1) return MO_OK;
+    int* idx = (int*)malloc(sizeof(int) * nn);
+    double* nd = (double*)malloc(sizeof(double) * (size_t)nn * m);
+    for (int i = 0, q = 0; i < n; ++i)
+        if (mask[i]) {
+            idx[q] = i;
+            memcpy(nd + (size_t)q * m, pts + (size_t)i * m, sizeof(double) * m);
+            ++q;
+        }
+    uint8_t* keep = (uint8_t*)calloc(nn, 1);
+    if (m == 2) {
+        int* order = (int*)malloc(sizeof(int) * nn);
+        int* hull = (int*)malloc(sizeof(int) * nn);
+        for (int q = 0; q < nn; ++q) order[q] = q;
+        g_ldf_pts = nd;
+        qsort(order, nn, sizeof(int), cmp_j1_asc);  /* J1 values are distinct in nd */
+        int h = 0;
+        for (int q = 0; q < nn; ++q) {
+            const int id = order[q];
+            while (h >= 2) {
+                const double* p1 = nd + (size_t)hull[h - 2] * 2;
+                const double* p2 = nd + (size_t)hull[h - 1] * 2;
+                const double* p3 = nd + (size_t)id * 2;
+                const double cross = (p2[0] - p1[0]) * (p3[1] - p2[1]) - (p2[1] - p1[1]) * (p3[0] - p2[0]);
+                if (cross > 0.0) --h; else break;
+            }
+            hull[h++] = id;
+        }
+        for (int q = 0; q < h; ++q) keep[hull[q]] = 1;
+        free(order);
+        free(hull);
+    } else {
+        int k[64];
+        ldf_grid_rec(m, 60, 60, 0, k, nd, nn, keep);
+    }
+    for (int q = 0; q < nn; ++q) mask[idx[q]] = keep[q];
+    free(keep);
+    free(nd);
+    free(idx);
+    return MO_OK;
+}
+
 /* ---- WFG exact hypervolume (any m). New algorithm, not in the reference:
  * hv(S) = sum_k [ inclhv(s_k) - hv(nd(limit(s_k, S[k+1:]))) ] with points
  * sorted by the last objective descending; m == 2 base case is the sweep

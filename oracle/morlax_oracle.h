@@ -178,6 +178,9 @@ int mo_hypervolume_mc(int n, int m, const double* pts, const double* ref,
 int mo_hypervolume_detailed(int n, int m, const double* pts, const double* ref,
                             uint64_t samples, uint64_t seed, double* value,
                             double* stderr_out, int* exact, int* clipped);
+/* linear_dominance_filter (pareto.cpp:79-139) as a survivor mask over the
+ * input order (duplicates: first occurrence) */
+int mo_linear_dominance_mask(int n, int m, const double* pts, uint8_t* mask);
 /* New exact algorithm for any m (WFG-style exclusive-volume recursion). Not
  * in the reference (which has no exact algorithm above m = 4). */
 int mo_hypervolume_wfg(int n, int m, const double* pts, const double* ref, double* value);

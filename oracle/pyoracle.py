@@ -395,6 +395,13 @@ class Oracle:
         self.check(self.fn("nondominated_mask")(n, m, _p(pts), _p(mask, C.c_uint8)))
         return mask
 
+    def linear_dominance_mask(self, pts):
+        pts = np.ascontiguousarray(pts, np.float64)
+        n, m = pts.shape
+        mask = np.zeros(n, np.uint8)
+        self.check(self.fn("linear_dominance_mask")(n, m, _p(pts), _p(mask, C.c_uint8)))
+        return mask
+
     def hypervolume_detailed(self, pts, ref, samples=1_000_000, seed=0x9E3779B9):
         pts = np.ascontiguousarray(pts, np.float64).reshape(-1, len(ref))
         ref = np.ascontiguousarray(ref, np.float64)

@@ -480,6 +480,21 @@ void mref_trainer_perm(void* tp, int32_t* out) {
     std::copy(t.perm.begin(), t.perm.end(), out);
 }
 
+int mref_linear_dominance_mask(int n, int m, const double* pts, uint8_t* mask) {
+    return guarded([&] {
+        std::vector<ObjectiveVector> p;
+        for (int i = 0; i < n; ++i) p.emplace_back(pts + (size_t)i * m, pts + (size_t)(i + 1) * m);
+        auto out = linear_dominance_filter(p);
+        size_t k = 0;
+        for (int i = 0; i < n; ++i) {
+            mask[i] = 0;
+            if (k < out.size() && out[k] == p[i]) {
+                mask[i] = 1;
+                ++k;
+            }
+        }
+    });
+}
 int mref_nondominated_mask(int n, int m, const double* pts, uint8_t* mask) {
     return guarded([&] {
         std::vector<ObjectiveVector> p;

@@ -29,7 +29,7 @@ __all__ = [
     "ConfigError", "ShapeError", "NumericError", "DomainError", "CudaError", "EnvSpec", "env_spec",
     "BatchedEnv", "make_env", "HypernetSpec", "PolicyForward", "init_hypernet", "hypernet_forward", "hypernet_backward",
     "gae_per_objective", "normalize_and_scalarize", "adam_apply", "TrainConfig", "Trainer",
-    "nondominated_mask", "nondominated_filter", "hypervolume_mc", "hypervolume_detailed", "hypervolume_exact",
+    "nondominated_mask", "nondominated_filter", "linear_dominance_mask", "linear_dominance_filter", "hypervolume_mc", "hypervolume_detailed", "hypervolume_exact",
     "rng_words", "rng_gaussians", "shard_minibatch", "LIB_PATH",
 ]
 
@@ -494,6 +494,20 @@ def nondominated_mask(points) -> np.ndarray:
 def nondominated_filter(points) -> np.ndarray:
     p = _f64(points)
     return p[nondominated_mask(p).astype(bool)]
+
+
+def linear_dominance_mask(points) -> np.ndarray:
+    """linear_dominance_filter (pareto.cpp:79-139) survivors as a mask."""
+    p = _f64(points)
+    n, m = p.shape
+    mask = np.zeros(n, np.uint8)
+    _check(LIB.morlax_linear_dominance_mask(n, m, _ptr(p), _ptr(mask)))
+    return mask
+
+
+def linear_dominance_filter(points) -> np.ndarray:
+    p = _f64(points)
+    return p[linear_dominance_mask(p).astype(bool)]
 
 
 def hypervolume_mc(points, reference, samples, key, ctr=0):

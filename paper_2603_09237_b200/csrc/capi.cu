@@ -688,6 +688,33 @@ int morlax_pareto_mask(int n, int m, const double* pts, uint8_t* mask) {
         mk.get(mask);
     });
 }
+int morlax_linear_dominance_mask(int n, int m, const double* pts, uint8_t* mask) {
+    return guarded([&] {  // pareto.cpp:79-139
+        if (m < 1 || m > 8) throw ShapeError("linear_dominance_filter: objective count must be in [1, 8]");
+        if (n <= 0) return;
+        DBuf<double> p(pts, (size_t)n * m);
+        DBuf<uint8_t> mk(n), uq(n);
+        DBuf<double> sums(n);
+        pareto_mask(n, m, p.p, mk.p, uq.p, sums.p, 0);  // nd = nondominated_filter(points)
+        MB_CUDA(cudaDeviceSynchronize());
+        mk.get(mask);
+        std::vector<int> idx;
+        for (int i = 0; i < n; ++i)
+            if (mask[i]) idx.push_back(i);
+        const int nn = (int)idx.size();
+        if (nn <= 2 || m == 1) return;
+        std::vector<double> nd((size_t)nn * m);
+        for (int q = 0; q < nn; ++q) std::memcpy(&nd[(size_t)q * m], pts + (size_t)idx[q] * m, sizeof(double) * m);
+        DBuf<double> dnd(nd.data(), nd.size());
+        DBuf<uint8_t> keep(nn);
+        DBuf<int> scratch(2 * (size_t)nn);
+        linear_dominance(nn, m, dnd.p, keep.p, scratch.p, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        std::vector<uint8_t> k(nn);
+        keep.get(k.data());
+        for (int q = 0; q < nn; ++q) mask[idx[q]] = k[q];
+    });
+}
 int morlax_hypervolume_mc(int n, int m, const double* pts, const double* ref, uint64_t samples, uint64_t key,
                           uint64_t ctr, double* value, double* se, uint64_t* hits_out) {
     return guarded([&] {

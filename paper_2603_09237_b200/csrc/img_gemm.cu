@@ -8,7 +8,7 @@
 //     (full[s] expect_tx, empty[s] released by tcgen05.commit);
 //   * warp 1 / lane 0 = MMA issuer: 8 x (K = 16) tcgen05.mma per B chunk
 //     into TMEM accumulator buffer (tile & 1); tcgen05.commit -> tfull;
-//   * warps 4..11 = epilogue (TMEM lanes 32*(w%4).., column half (w-4)/4): tcgen05.ld 16 columns at
+//   * warps 4.. = epilogue (8 or 16; TMEM lanes 32*(w%4).., column part (w-4)/4): tcgen05.ld 16 columns at
 //     a time, fused bias / tanh / tanh' / fp32 + bf16-image stores, then
 //     arrive tempty so the MMA warp can reuse the buffer -- the epilogue of
 //     tile i overlaps the loads and MMAs of tile i+1.
@@ -23,11 +23,10 @@
 namespace mb200 {
 
 namespace {
-constexpr int NT = 384;  // warps 0-3: producer / MMA / spare, 4-11: epilogue
 constexpr int CHUNK = 32768;
 constexpr int EPI_WARP0 = 4;
 
-template <int BN>
+template <int BN, int EPI>
 struct Cfg {
     static constexpr int NB = BN > 128 ? 2 : 1;      // B chunks per stage
     static constexpr int STAGE = CHUNK * (1 + NB);
@@ -35,7 +34,13 @@ struct Cfg {
     static constexpr int NMMA = BN > 128 ? 128 : BN;  // N per MMA instruction
     static constexpr int ACC = BN < 32 ? 32 : BN;     // TMEM columns per accumulator buffer
     static constexpr int TCOLS = 2 * ACC;             // double buffered (<= 512)
-    static constexpr int SMEM = STAGES * STAGE + 1024 + 4 * BN + 16 * BN + 8 * 512 * 4;
+    // epilogue warps: 4 lane quadrants x NEPI/4 column parts. The image
+    // epilogues (tanh / tanh') are issue-latency bound with 2 warps per
+    // SMSP, so wide tiles get 16 warps; fp32-output tiles keep 8 and the
+    // smem staging area of their transposed stores
+    static constexpr int NEPI = (EPI == 1 && BN >= 64) ? 16 : 8;
+    static constexpr int NT = 128 + 32 * NEPI;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 4 * BN + 16 * BN + (EPI == 0 ? 8 * 512 * 4 : 0);
 };
 
 __device__ __forceinline__ long chunk_index(int view, int mt, int kc, int CT) {
@@ -72,8 +77,9 @@ __device__ __forceinline__ TileInfo tile_info(const IGemm& d, int t, int ntn, in
 // EPI: 0 = fp32 out (bias optional), 1 = tanh -> image (+ optional fp32 pre-act),
 //      2 = tanh' (aux image) -> image
 template <int BN, int EPI>
-__global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn, int ntm) {
-    using C = Cfg<BN>;
+__global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn, int ntm) {
+    using C = Cfg<BN, EPI>;
+    constexpr int NEPI = C::NEPI, ET = 32 * NEPI;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
     uint64_t* empty = full + C::STAGES;
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
         }
         for (int b = 0; b < 2; ++b) {
             umma::mbar_init(&tfull[b], 1);
-            umma::mbar_init(&tempty[b], 256);
+            umma::mbar_init(&tempty[b], ET);
         }
         umma::fence_barrier_init();
     }
@@ -164,12 +170,13 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             }
         }
         __syncwarp();
-    } else if (warp >= EPI_WARP0) {  // ---------------- epilogue (8 warps)
-        const int ew = warp - EPI_WARP0;           // 0..7
-        const int lg = ew & 3, half = ew >> 2;     // TMEM lane quadrant, column half
-        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..255
-        constexpr int HALF = BN >= 32 ? BN / 2 : BN;
-        const bool active = BN >= 32 || half == 0;
+    } else if (warp >= EPI_WARP0) {  // ---------------- epilogue (NEPI warps)
+        const int ew = warp - EPI_WARP0;           // 0..NEPI-1
+        const int lg = ew & 3, half = ew >> 2;     // TMEM lane quadrant, column part
+        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..ET-1
+        constexpr int NPART = NEPI / 4;
+        constexpr int HALF = BN >= 16 * NPART ? BN / NPART : BN;  // columns per part
+        const bool active = BN >= 16 * NPART || half == 0;
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const TileInfo ti = tile_info(d, t, ntn, ntm);
@@ -177,10 +184,10 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             const int acc = it & 1;
             const float* bias = d.bias ? d.bias + (d.gmode != 2 ? ti.z * d.bias_gs : 0) : nullptr;
             // per-n bias -> smem (the previous tile's readers passed this barrier already)
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(ET) : "memory");
             if (d.bias_mode == 1)
-                for (int j = et; j < BN; j += 256) sbias[j] = (ti.n0 + j < d.N) ? bias[ti.n0 + j] : 0.f;
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+                for (int j = et; j < BN; j += ET) sbias[j] = (ti.n0 + j < d.N) ? bias[ti.n0 + j] : 0.f;
+            asm volatile("bar.sync 1, %0;" ::"r"(ET) : "memory");
             const int m = ti.m0 + lg * 32 + lane;
             const bool mrow = m < ti.m_hi;
             const float bm = (d.bias_mode == 2 && mrow) ? bias[m] : 0.f;
@@ -428,8 +435,8 @@ __global__ void __launch_bounds__(NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn
             umma::fence_before_sync();
             umma::mbar_arrive(&tempty[acc]);
             if (EPI == 2 && d.psum) {  // psum[m-tile][n] = sum over the tile's 128 rows
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-                for (int j = et; j < BN; j += 256)
+                asm volatile("bar.sync 1, %0;" ::"r"(ET) : "memory");
+                for (int j = et; j < BN; j += ET)
                     if (ti.n0 + j < d.N)
                         d.psum[(long)(ti.m0 >> 7) * d.psum_ld + ti.n0 + j] =
                             sred[j] + sred[BN + j] + sred[2 * BN + j] + sred[3 * BN + j];
@@ -446,7 +453,7 @@ void launch(IGemm d, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
         MB_CUDA(cudaFuncSetAttribute(k_img_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Cfg<BN>::SMEM));
+                                     Cfg<BN, EPI>::SMEM));
         configured = true;
     }
     d.N_tile = BN;
@@ -454,7 +461,7 @@ void launch(IGemm d, cudaStream_t s) {
     const int ntn = (d.N + BN - 1) / BN, ntm = (mext + 127) / 128;
     const int ntiles = ntn * ntm * d.Z;
     const int grid = ntiles < 148 ? ntiles : 148;
-    k_img_gemm<BN, EPI><<<grid, NT, Cfg<BN>::SMEM, s>>>(d, ntiles, ntn, ntm);
+    k_img_gemm<BN, EPI><<<grid, Cfg<BN, EPI>::NT, Cfg<BN, EPI>::SMEM, s>>>(d, ntiles, ntn, ntm);
     MB_LAUNCH();
 }
 

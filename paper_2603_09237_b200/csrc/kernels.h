@@ -222,6 +222,9 @@ void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, floa
 // ---------------------------------------------------------------- Pareto (K8/K9)
 void pareto_mask(int n, int m, const double* pts, uint8_t* mask, uint8_t* uniq, double* sums,
                  cudaStream_t s);
+// linear_dominance_filter's selection on the nondominated set nd [nn][m]
+// (device): keep[q] = 1 for survivors; scratch >= 2 nn ints (m == 2)
+void linear_dominance(int nn, int m, const double* nd, uint8_t* keep, int* scratch, cudaStream_t s);
 // exact hypervolume (WFG recursion, any m <= 8) of the points >= ref;
 // value and clipped count written to host memory (synchronises `s`)
 void hv_exact(int n, int m, const double* d_pts, const double* d_ref, double* value, int* clipped, cudaStream_t s);

@@ -10,6 +10,9 @@
 // hypervolume_mc (pareto.cpp:236-277): sample s uses words s*m+j+1 of the
 // stream; coordinates use explicit __dmul_rn/__dadd_rn (no FMA) so every
 // sample point and the hit count are bit-identical to the reference.
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -62,6 +65,119 @@ void pareto_mask(int n, int m, const double* pts, uint8_t* mask, uint8_t* uniq, 
     k_pareto_prep<<<(n + 127) / 128, 128, 0, s>>>(n, m, pts, uniq, sums);
     MB_LAUNCH();
     k_pareto_mask<<<(n + 127) / 128, 128, 0, s>>>(n, m, pts, uniq, sums, mask);
+    MB_LAUNCH();
+}
+
+// ---- linear_dominance_filter (pareto.cpp:79-139) on the nondominated set
+// nd [nn][m] (input order). m == 2: one block sorts by J1 (rank scatter;
+// J1 values are distinct in nd) and thread 0 runs the upper-hull scan with
+// the reference's cross product (explicit _rn ops: no FMA contraction).
+// m >= 3: every weight of simplex_grid(m, 60) (simplex.cpp:108-117) is
+// unranked from its index (stars and bars, grid_rec order), w_j = k_j / 60,
+// dots in coordinate order (simplex.cpp:10-16); the points within
+// 1e-9 max(1, |best|) of the best are kept. Bit-identical keep decisions.
+__global__ void k_ldf_hull2(int nn, const double* __restrict__ nd, int* order, uint8_t* keep) {
+    for (int q = threadIdx.x; q < nn; q += blockDim.x) {
+        const double x = nd[2 * q];
+        int rank = 0;
+        for (int r = 0; r < nn; ++r) rank += nd[2 * r] < x || (nd[2 * r] == x && r < q);
+        order[rank] = q;
+        keep[q] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    int h = 0;
+    int* hull = order + nn;
+    for (int q = 0; q < nn; ++q) {
+        const int id = order[q];
+        while (h >= 2) {
+            const double* p1 = nd + 2 * hull[h - 2];
+            const double* p2 = nd + 2 * hull[h - 1];
+            const double* p3 = nd + 2 * id;
+            const double cross = __dsub_rn(__dmul_rn(__dsub_rn(p2[0], p1[0]), __dsub_rn(p3[1], p2[1])),
+                                           __dmul_rn(__dsub_rn(p2[1], p1[1]), __dsub_rn(p3[0], p2[0])));
+            if (cross > 0.0) --h;
+            else break;
+        }
+        hull[h++] = id;
+    }
+    for (int q = 0; q < h; ++q) keep[hull[q]] = 1;
+}
+
+constexpr int kLdfRes = 60;
+constexpr int kLdfThreads = 256;
+__device__ __forceinline__ double ldf_dot(const int* k, const double* p, int m) {
+    double acc = 0.0;
+    for (int j = 0; j < m; ++j) acc = __dadd_rn(acc, __dmul_rn(__ddiv_rn((double)k[j], (double)kLdfRes), p[j]));
+    return acc;
+}
+// binom[n][r] for n <= kLdfRes + 8, r <= 8 (uint64, exact)
+__global__ void __launch_bounds__(kLdfThreads) k_ldf_sweep(int nn, int m, const double* __restrict__ nd,
+                                                           const unsigned long long* __restrict__ binom,
+                                                           unsigned long long nw, uint8_t* keep_g) {
+    extern __shared__ double sp[];  // [nn][m]
+    uint8_t* keep = reinterpret_cast<uint8_t*>(sp + (size_t)nn * m);
+    for (int e = threadIdx.x; e < nn * m; e += blockDim.x) sp[e] = nd[e];
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) keep[e] = 0;
+    __syncthreads();
+    for (unsigned long long w = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; w < nw;
+         w += (unsigned long long)gridDim.x * blockDim.x) {
+        // unrank: grid_rec enumerates k_0 from R down to 0, then recurses
+        int k[8];
+        unsigned long long idx = w;
+        int R = kLdfRes;
+        for (int j = 0; j < m - 1; ++j) {
+            const int q = m - j;  // parts left including this one
+            int v = R;
+            for (;; --v) {
+                const unsigned long long cnt = binom[(R - v + q - 2) * 9 + (q - 2)];  // compositions of R-v into q-1
+                if (idx < cnt) break;
+                idx -= cnt;
+            }
+            k[j] = v;
+            R -= v;
+        }
+        k[m - 1] = R;
+        double best = -INFINITY;
+        for (int i = 0; i < nn; ++i) best = fmax(best, ldf_dot(k, sp + i * m, m));
+        const double tol = __dmul_rn(1e-9, fmax(1.0, fabs(best)));
+        const double thr = __dsub_rn(best, tol);
+        for (int i = 0; i < nn; ++i)
+            if (ldf_dot(k, sp + i * m, m) >= thr) keep[i] = 1;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nn; e += blockDim.x)
+        if (keep[e]) keep_g[e] = 1;
+}
+
+void linear_dominance(int nn, int m, const double* nd, uint8_t* keep, int* scratch, cudaStream_t s) {
+    if (m == 2) {
+        k_ldf_hull2<<<1, 256, 0, s>>>(nn, nd, scratch, keep);
+        MB_LAUNCH();
+        return;
+    }
+    // compositions of r into q parts = C(r + q - 1, q - 1); table over n <= 68, r <= 8
+    static unsigned long long* d_binom = nullptr;
+    std::vector<unsigned long long> b(69 * 9, 0);
+    for (int n = 0; n <= 68; ++n) {
+        b[n * 9] = 1;
+        for (int r = 1; r <= 8 && r <= n; ++r) b[n * 9 + r] = b[(n - 1) * 9 + r - 1] + (r <= n - 1 ? b[(n - 1) * 9 + r] : 0);
+    }
+    if (!d_binom) {
+        MB_CUDA(cudaMalloc(&d_binom, sizeof(unsigned long long) * b.size()));
+        MB_CUDA(cudaMemcpy(d_binom, b.data(), sizeof(unsigned long long) * b.size(), cudaMemcpyHostToDevice));
+    }
+    const unsigned long long nw = b[(kLdfRes + m - 1) * 9 + (m - 1)];  // C(60 + m - 1, m - 1)
+    MB_CUDA(cudaMemsetAsync(keep, 0, nn, s));
+    const size_t smem = sizeof(double) * (size_t)nn * m + nn;
+    if (smem > 200 * 1024) throw ShapeError("linear_dominance_filter: too many nondominated points for the device sweep");
+    static size_t configured = 0;
+    if (smem > configured) {
+        MB_CUDA(cudaFuncSetAttribute(k_ldf_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    const unsigned long long blocks = std::min<unsigned long long>((nw + kLdfThreads - 1) / kLdfThreads, 148ull * 8);
+    k_ldf_sweep<<<(unsigned)blocks, kLdfThreads, smem, s>>>(nn, m, nd, d_binom, nw, keep);
     MB_LAUNCH();
 }
 

@@ -114,6 +114,20 @@ def main():
     g["hv_pts6"] = q6
     v, se, ex, clp = r.hypervolume_detailed(q6, np.zeros(6), samples=200_000)
     g["hv_mc6"] = np.array([v, se])
+    # ---- linear_dominance_filter (pareto.cpp:79-139): 2-D hull with a
+    # collinear triple, m = 3 / 4 / 6 grid sweeps with a duplicate point
+    lrng = np.random.default_rng(77)
+    for m, n in ((2, 40), (3, 60), (4, 40), (6, 16)):
+        w = lrng.dirichlet(np.ones(m), size=n)
+        q = w / np.linalg.norm(w, axis=1, keepdims=True) + lrng.normal(0, 0.05, (n, m))
+        q[5] = q[2]
+        if m == 2:
+            q[7] = [0.0, 1.0]
+            q[8] = [0.5, 0.5 + 0.5]
+            q[9] = [1.0, 0.0]
+            q[10] = [0.25, 0.75 + 0.25 * 0.5]
+        g[f"ldf_pts{m}"] = q
+        g[f"ldf_mask{m}"] = r.linear_dominance_mask(q)
     np.savez_compressed(os.path.join(HERE, "golden_ref.npz"), **g)
     print("wrote", len(g), "arrays")
 

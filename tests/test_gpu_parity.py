@@ -395,3 +395,21 @@ def test_hypervolume_exact_edge_cases(mb):
     assert v == vd
     with pytest.raises(mb.ShapeError):
         mb.hypervolume_exact(np.zeros((3, 9)), np.zeros(9))
+
+
+# ------------------------------------------------------------------ linear dominance filter (pareto.cpp:79-139)
+@pytest.mark.parametrize("m", [2, 3, 4, 6])
+def test_linear_dominance_bit_exact(mb, o, g, m):
+    assert np.array_equal(mb.linear_dominance_mask(g[f"ldf_pts{m}"]), g[f"ldf_mask{m}"])
+
+
+def test_linear_dominance_edge_cases(mb, o):
+    line = np.array([[0.0, 1.0], [0.25, 0.75], [0.5, 0.5], [1.0, 0.0], [0.2, 0.2]])  # collinear: all kept
+    assert list(mb.linear_dominance_mask(line)) == [1, 1, 1, 1, 0]
+    q = np.round(np.random.default_rng(8).normal(size=(300, 2)), 1)  # ties / duplicates
+    assert np.array_equal(mb.linear_dominance_mask(q), o.linear_dominance_mask(q))
+    p3 = _front(200, 3, 9)
+    p3[10] = p3[4]
+    assert np.array_equal(mb.linear_dominance_mask(p3), o.linear_dominance_mask(p3))
+    assert list(mb.linear_dominance_mask(np.array([[1.0, 2.0], [2.0, 1.0]]))) == [1, 1]  # |nd| <= 2
+    assert mb.linear_dominance_mask(np.zeros((0, 3))).size == 0

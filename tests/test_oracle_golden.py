@@ -122,3 +122,9 @@ def test_wfg_exact_matches_reference_exact_for_small_m(o, g):
     # m = 6: exact within 4 stderr of the reference Monte-Carlo
     v = o.hypervolume_wfg(g["hv_pts6"], np.zeros(6))
     assert abs(v - g["hv_mc6"][0]) <= 4 * g["hv_mc6"][1]
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 6])
+def test_linear_dominance_oracle_matches_reference(o, g, m):
+    # golden: the reference's linear_dominance_filter (pareto.cpp:79-139)
+    assert np.array_equal(o.linear_dominance_mask(g[f"ldf_pts{m}"]), g[f"ldf_mask{m}"])
