@@ -97,6 +97,17 @@ int morlax_policy_forward_device(morlax_policy* p, const float* d_w, const float
 /* algorithmic FLOPs of one forward (feature MLP + theta GEMM + per-row MLP) */
 double morlax_policy_flops(morlax_policy* p);
 
+/* ---- Evaluation (replaces evaluate_params / eval_point,
+ *      src/evaluate.cpp:17-101, and simplex_grid_size, simplex.cpp:119) --- */
+int64_t morlax_simplex_grid_size(int m, int resolution);
+/* for every w of simplex_grid(m, resolution) (reference order) the
+ * deterministic policy (tanh of the mean) of the actor hypernet `flat` runs
+ * episodes_per_point fresh instances reset from Rng(key).split(g) for one
+ * episode each; w_out / mean_return_out are [n_points][m] */
+int morlax_evaluate_params(const morlax_hypernet_spec* actor_spec, const double* flat, const char* env_name,
+                           int grid_resolution, int episodes_per_point, uint64_t key, double* w_out,
+                           double* mean_return_out, int64_t* n_points);
+
 /* ---- Advantage estimation (replaces gae_per_objective /
  *      normalize_and_scalarize, include/morlax/trainer.hpp:154-161) ------ */
 int morlax_gae(int N, int T, int m, const float* reward, const float* value, const float* next_value,

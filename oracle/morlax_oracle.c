@@ -1301,6 +1301,97 @@ int mo_hypervolume_detailed(int n, int m, const double* pts, const double* ref, 
     return MO_OK;
 }
 
+/* ---- simplex_grid (simplex.cpp:88-117): compositions of `res` into m parts,
+ * first coordinate from res down to 0, recursively; entries k / res. */
+static void grid_rec_c(int m, int res, int remaining, int depth, double* prefix, double* out, int64_t* n) {
+    if (depth == m - 1) {
+        prefix[depth] = (double)remaining / res;
+        memcpy(out + (size_t)(*n) * m, prefix, sizeof(double) * m);
+        (*n)++;
+        return;
+    }
+    for (int k = remaining; k >= 0; --k) {
+        prefix[depth] = (double)k / res;
+        grid_rec_c(m, res, remaining - k, depth + 1, prefix, out, n);
+    }
+}
+int64_t mo_simplex_grid_size(int m, int res) {
+    int64_t r = 1;
+    for (int i = 1; i <= m - 1; ++i) r = r * (res + i) / i;
+    return r;
+}
+int mo_simplex_grid(int m, int res, double* out) {
+    if (m < 1 || res < 1) return fail(MO_ERR, "simplex_grid: bad arguments");
+    if (m == 1) { out[0] = 1.0; return MO_OK; }
+    double prefix[64];
+    int64_t n = 0;
+    grid_rec_c(m, res, res, 0, prefix, out, &n);
+    return MO_OK;
+}
+
+/* ---- evaluate_params / eval_point (evaluate.cpp:17-101): for every simplex
+ * grid point g, a fresh env of `episodes` instances reset from
+ * Rng(key).split(g); the deterministic policy (tanh of the mean, the
+ * target MLP's output activation) steps the still-alive instances for up to
+ * max_episode_steps; first-episode undiscounted returns, averaged. Dead
+ * instances are stepped too (their own streams only) and masked out. */
+int mo_evaluate_params(const mo_hspec* h, const double* flat, int env_kind, int res, int episodes,
+                       uint64_t key, double* w_out, double* mean_out, int64_t* n_points) {
+    mo_envspec es;
+    if (mo_env_spec(env_kind, &es)) return MO_ERR;
+    if (episodes < 1) return fail(MO_ERR, "evaluate: episodes_per_point must be >= 1");
+    if (h->m != es.m) return fail(MO_ERR, "evaluate: hypernet trade-off dim does not match env");
+    if (es.m > 1 && res < 1) return fail(MO_ERR, "evaluate: grid_resolution must be >= 1");
+    const int64_t ng = es.m == 1 ? 1 : mo_simplex_grid_size(es.m, res);
+    if (es.m == 1) w_out[0] = 1.0; else mo_simplex_grid(es.m, res, w_out);
+    const int64_t P = mo_hspec_target_count(h);
+    double* theta = (double*)malloc(sizeof(double) * P);
+    double* obs = (double*)malloc(sizeof(double) * (size_t)episodes * es.obs_dim);
+    double* act = (double*)calloc((size_t)episodes * es.act_dim, sizeof(double));
+    double* nobs = (double*)malloc(sizeof(double) * (size_t)episodes * es.obs_dim);
+    double* rew = (double*)malloc(sizeof(double) * (size_t)episodes * es.m);
+    uint8_t* term = (uint8_t*)malloc(episodes);
+    uint8_t* trunc = (uint8_t*)malloc(episodes);
+    uint8_t* alive = (uint8_t*)malloc(episodes);
+    double* tot = (double*)malloc(sizeof(double) * (size_t)episodes * es.m);
+    int rc = MO_OK;
+    for (int64_t g = 0; g < ng && rc == MO_OK; ++g) {
+        rc = mo_hypernet_forward(h, flat, w_out + (size_t)g * es.m, theta);
+        if (rc) break;
+        mo_env* env = mo_env_create(env_kind, episodes);
+        mo_rng root = {key, 0};
+        mo_env_reset(env, mo_rng_split(root, (uint64_t)g).key, 0, NULL);
+        for (int i = 0; i < episodes; ++i) alive[i] = 1;
+        memset(tot, 0, sizeof(double) * (size_t)episodes * es.m);
+        for (int t = 0; t < es.max_steps; ++t) {
+            int any = 0;
+            mo_env_current_obs(env, obs);
+            for (int i = 0; i < episodes; ++i) {
+                if (!alive[i]) continue;
+                any = 1;
+                mo_mlp_forward(&h->target, theta, obs + (size_t)i * es.obs_dim, act + (size_t)i * es.act_dim);
+            }
+            if (!any) break;
+            rc = mo_env_step(env, act, nobs, rew, term, trunc);
+            if (rc) break;
+            for (int i = 0; i < episodes; ++i) {
+                if (!alive[i]) continue;
+                for (int k = 0; k < es.m; ++k) tot[(size_t)i * es.m + k] += rew[(size_t)i * es.m + k];
+                if (term[i] || trunc[i]) alive[i] = 0;
+            }
+        }
+        for (int k = 0; k < es.m; ++k) {
+            double mean = 0.0;
+            for (int i = 0; i < episodes; ++i) mean += tot[(size_t)i * es.m + k];
+            mean_out[(size_t)g * es.m + k] = mean / (double)episodes;
+        }
+        mo_env_destroy(env);
+    }
+    *n_points = ng;
+    free(theta); free(obs); free(act); free(nobs); free(rew); free(term); free(trunc); free(alive); free(tot);
+    return rc;
+}
+
 /* ---- linear_dominance_filter (pareto.cpp:79-139) as a mask over the input:
  * nd = nondominated_filter; |nd| <= 2 or m == 1 -> nd; m == 2 -> upper hull
  * of nd sorted by J1 ascending, collinear points kept (cross > 0 pops);

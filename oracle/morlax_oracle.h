@@ -178,6 +178,12 @@ int mo_hypervolume_mc(int n, int m, const double* pts, const double* ref,
 int mo_hypervolume_detailed(int n, int m, const double* pts, const double* ref,
                             uint64_t samples, uint64_t seed, double* value,
                             double* stderr_out, int* exact, int* clipped);
+/* ---- simplex_grid (simplex.cpp:108-130) and evaluate_params
+ * (evaluate.cpp:17-101): w_out [n_points][m], mean_out [n_points][m] */
+int64_t mo_simplex_grid_size(int m, int res);
+int mo_simplex_grid(int m, int res, double* out);
+int mo_evaluate_params(const mo_hspec* h, const double* flat, int env_kind, int res, int episodes,
+                       uint64_t key, double* w_out, double* mean_out, int64_t* n_points);
 /* linear_dominance_filter (pareto.cpp:79-139) as a survivor mask over the
  * input order (duplicates: first occurrence) */
 int mo_linear_dominance_mask(int n, int m, const double* pts, uint8_t* mask);

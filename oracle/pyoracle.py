@@ -395,6 +395,19 @@ class Oracle:
         self.check(self.fn("nondominated_mask")(n, m, _p(pts), _p(mask, C.c_uint8)))
         return mask
 
+    def evaluate_params(self, spec, flat, env_kind, res, episodes, key):
+        m = spec.m
+        f = self.fn("simplex_grid_size")
+        f.restype = C.c_int64
+        n = 1 if m == 1 else int(f(m, res))
+        W = np.zeros((n, m))
+        R = np.zeros((n, m))
+        npts = C.c_int64()
+        flat = np.ascontiguousarray(flat, np.float64)
+        self.check(self.fn("evaluate_params")(C.byref(spec.c()), _p(flat), env_kind, res, episodes,
+                                              C.c_uint64(key), _p(W), _p(R), C.byref(npts)))
+        return W[:npts.value], R[:npts.value]
+
     def linear_dominance_mask(self, pts):
         pts = np.ascontiguousarray(pts, np.float64)
         n, m = pts.shape

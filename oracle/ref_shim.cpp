@@ -480,6 +480,21 @@ void mref_trainer_perm(void* tp, int32_t* out) {
     std::copy(t.perm.begin(), t.perm.end(), out);
 }
 
+int64_t mref_simplex_grid_size(int m, int res) { return (int64_t)simplex_grid_size(m, res); }
+int mref_evaluate_params(const mo_hspec* h, const double* flat, int env_kind, int res, int episodes,
+                         uint64_t key, double* w_out, double* mean_out, int64_t* n_points) {
+    return guarded([&] {  // the reference registry: lqr / pointmass / dst only
+        const HypernetSpec s = to_spec(h);
+        const auto hp = unflatten_hypernet(s, {flat, (size_t)hypernet_param_count(s)});
+        const EvalTable tab = evaluate_params(s, hp, env_name(env_kind), res, episodes, Rng::from_state(key, 0), 1);
+        for (size_t g = 0; g < tab.rows.size(); ++g)
+            for (int k = 0; k < tab.m; ++k) {
+                w_out[g * tab.m + k] = tab.rows[g].w.weights[k];
+                mean_out[g * tab.m + k] = tab.rows[g].mean_return[k];
+            }
+        *n_points = (int64_t)tab.rows.size();
+    });
+}
 int mref_linear_dominance_mask(int n, int m, const double* pts, uint8_t* mask) {
     return guarded([&] {
         std::vector<ObjectiveVector> p;

@@ -27,7 +27,7 @@ from ._lib import LIB, LIB_PATH  # noqa: F401  (loads / builds the CUDA library)
 
 __all__ = [
     "ConfigError", "ShapeError", "NumericError", "DomainError", "CudaError", "EnvSpec", "env_spec",
-    "BatchedEnv", "make_env", "HypernetSpec", "PolicyForward", "init_hypernet", "hypernet_forward", "hypernet_backward",
+    "BatchedEnv", "make_env", "HypernetSpec", "PolicyForward", "evaluate_params", "simplex_grid_size", "init_hypernet", "hypernet_forward", "hypernet_backward",
     "gae_per_objective", "normalize_and_scalarize", "adam_apply", "TrainConfig", "Trainer",
     "nondominated_mask", "nondominated_filter", "linear_dominance_mask", "linear_dominance_filter", "hypervolume_mc", "hypervolume_detailed", "hypervolume_exact",
     "rng_words", "rng_gaussians", "shard_minibatch", "LIB_PATH",
@@ -263,6 +263,23 @@ class PolicyForward:
     @property
     def flops(self) -> float:
         return float(LIB.morlax_policy_flops(self._h))
+
+
+def simplex_grid_size(m: int, resolution: int) -> int:
+    return int(LIB.morlax_simplex_grid_size(m, resolution))
+
+
+def evaluate_params(spec: HypernetSpec, flat, env_name: str, grid_resolution: int, episodes_per_point: int,
+                    key: int):
+    """evaluate_params (evaluate.cpp:68-101) on the device: returns (W, mean_return),
+    both [n_points][m], W in simplex_grid order; Rng(key).split(g) resets point g."""
+    n = 1 if spec.m == 1 else simplex_grid_size(spec.m, grid_resolution)
+    W = np.zeros((max(n, 1), spec.m))
+    R = np.zeros((max(n, 1), spec.m))
+    npts = C.c_int64()
+    _check(LIB.morlax_evaluate_params(C.byref(spec.c()), _ptr(_f64(flat)), env_name.encode(), grid_resolution,
+                                      episodes_per_point, C.c_uint64(key), _ptr(W), _ptr(R), C.byref(npts)))
+    return W[:npts.value], R[:npts.value]
 
 
 def hypernet_backward(spec: HypernetSpec, flat, w, gtheta) -> np.ndarray:

@@ -52,6 +52,7 @@ def _load():
     lib.morlax_policy_forward_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.morlax_policy_flops.restype = C.c_double
     lib.morlax_policy_flops.argtypes = [C.c_void_p]
+    lib.morlax_simplex_grid_size.restype = C.c_int64
     for name in ("morlax_env_reset", "morlax_env_step", "morlax_env_current_obs",
                  "morlax_env_step_device", "morlax_trainer_iteration", "morlax_trainer_phase",
                  "morlax_trainer_sizes", "morlax_trainer_get_params", "morlax_trainer_set_params",

@@ -2,6 +2,7 @@
 // reference's C++ exceptions to the CLI's status codes
 // (tools/commands.hpp:12-32) and records a thread-local message.
 #include <cmath>
+#include <functional>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -312,6 +313,67 @@ int morlax_policy_forward_device(morlax_policy* h, const float* d_w, const float
     return guarded([&] { h->p->forward(d_w, d_obs, d_pre, (cudaStream_t)stream); });
 }
 double morlax_policy_flops(morlax_policy* h) { return h ? h->p->flops() : 0.0; }
+int64_t morlax_simplex_grid_size(int m, int res) {  // simplex.cpp:119-130
+    if (m < 1 || res < 1) return 0;
+    int64_t r = 1;
+    for (int i = 1; i <= m - 1; ++i) r = r * (res + i) / i;
+    return r;
+}
+int morlax_evaluate_params(const morlax_hypernet_spec* s, const double* flat, const char* env_name,
+                           int grid_resolution, int episodes, uint64_t key, double* w_out, double* mean_out,
+                           int64_t* n_points) {
+    return guarded([&] {  // evaluate.cpp:68-101
+        if (episodes < 1) throw ConfigError("evaluate: episodes_per_point must be >= 1");
+        const EnvSpecB es = env_spec_of(env_kind_of(env_name));
+        if (s->m != es.m) throw ShapeError("evaluate: hypernet trade-off dim does not match env");
+        if (s->n_target_sizes < 2 || s->target_sizes[0] != es.obs_dim ||
+            s->target_sizes[s->n_target_sizes - 1] != es.act_dim)
+            throw ShapeError("evaluate: policy spec does not match the environment");
+        // simplex_grid (simplex.cpp:88-117): compositions of res into m parts,
+        // first coordinate from res down to 0
+        std::vector<double> W;
+        if (es.m == 1) {
+            W.push_back(1.0);
+        } else {
+            if (grid_resolution < 1) throw ConfigError("evaluate: grid_resolution must be >= 1");
+            std::vector<int> k(es.m, 0);
+            std::function<void(int, int)> rec = [&](int depth, int rem) {
+                if (depth == es.m - 1) {
+                    k[depth] = rem;
+                    for (int j = 0; j < es.m; ++j) W.push_back((double)k[j] / grid_resolution);
+                    return;
+                }
+                for (int v = rem; v >= 0; --v) {
+                    k[depth] = v;
+                    rec(depth + 1, rem - v);
+                }
+            };
+            rec(0, grid_resolution);
+        }
+        const int ng = (int)(W.size() / es.m);
+        HyperHandle hh(s, ng);
+        hh.load(flat);
+        std::vector<float> wf(W.begin(), W.end());
+        DBuf<float> dw(wf.data(), wf.size());
+        hh.h.forward(dw.p, 0, ng, 0);  // theta for every grid point (hypernet.cpp:69-90)
+        const int cpp = (episodes + 15) / 16;
+        DBuf<double> part((size_t)ng * cpp * es.m), mean((size_t)ng * es.m);
+        DBuf<int> err(1);
+        MB_CUDA(cudaMemset(err.p, 0, sizeof(int)));
+        EvalArgs a;
+        a.kind = es.kind; a.od = es.obs_dim; a.ad = es.act_dim; a.m = es.m; a.sdim = es.state_dim;
+        a.max_steps = es.max_steps; a.episodes = episodes; a.pol = hh.h.tgt;
+        a.theta = hh.h.theta; a.ld = hh.h.ld; a.key = key; a.part = part.p; a.err = err.p;
+        evaluate(a, ng, mean.p, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        int e = 0;
+        err.get(&e);
+        if (e) throw NumericError("evaluate: non-finite action");
+        std::copy(W.begin(), W.end(), w_out);
+        mean.get(mean_out);
+        *n_points = ng;
+    });
+}
 int morlax_hypernet_backward(const morlax_hypernet_spec* s, const double* flat, const double* w, int G,
                              const double* gtheta, double* out) {
     return guarded([&] {

@@ -136,6 +136,21 @@ struct NetDims {
     long mlp_n, P;
     int out_tanh, has_log_std;
 };
+// evaluate_params (evaluate.cu): deterministic first-episode returns per
+// simplex-grid preference; theta [n_points][ld] from the hypernet forward
+struct EvalArgs {
+    int kind = 0, od = 0, ad = 0, m = 0, sdim = 0, max_steps = 0;
+    int episodes = 0;
+    int cpp = 0, maxw = 0, nbias = 0;  // set by evaluate()
+    NetDims pol{};
+    const float* theta = nullptr;
+    long ld = 0;
+    uint64_t key = 0;                  // Rng(key): point g resets from split(g)
+    double* part = nullptr;            // [n_points][ceil(episodes / 16)][m] scratch
+    int* err = nullptr;
+};
+void evaluate(EvalArgs a, int n_points, double* d_mean, cudaStream_t s);
+
 struct RolloutArgs {
     int kind, N, T, K, reps, od, ad, m, sdim, max_steps;
     const float* theta;  // [K][theta_ld] (first Pa used)

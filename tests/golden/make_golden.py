@@ -128,6 +128,13 @@ def main():
             q[10] = [0.25, 0.75 + 0.25 * 0.5]
         g[f"ldf_pts{m}"] = q
         g[f"ldf_mask{m}"] = r.linear_dominance_mask(q)
+    # ---- evaluate_params (evaluate.cpp:17-101): reference envs only
+    from pyoracle import HSpec
+    for env, od, ad, res, eps in (("mo-pointmass", 4, 2, 4, 3), ("mo-lqr1d", 1, 1, 3, 2)):
+        spec = HSpec(2, 16, [16], [od, 32, 32, ad], True, True)
+        flat = r.init_hypernet(spec, 0x77)
+        W, R = r.evaluate_params(spec, flat, ENV_KINDS[env], res, eps, 0x1234)
+        g[f"eval_{env}_flat"], g[f"eval_{env}_W"], g[f"eval_{env}_R"] = flat, W, R
     np.savez_compressed(os.path.join(HERE, "golden_ref.npz"), **g)
     print("wrote", len(g), "arrays")
 

@@ -413,3 +413,44 @@ def test_linear_dominance_edge_cases(mb, o):
     assert np.array_equal(mb.linear_dominance_mask(p3), o.linear_dominance_mask(p3))
     assert list(mb.linear_dominance_mask(np.array([[1.0, 2.0], [2.0, 1.0]]))) == [1, 1]  # |nd| <= 2
     assert mb.linear_dominance_mask(np.zeros((0, 3))).size == 0
+
+
+# ------------------------------------------------------------------ evaluate_params (evaluate.cpp:17-101)
+@pytest.mark.parametrize("env,od,ad,res,eps", [("mo-pointmass", 4, 2, 4, 3), ("mo-lqr1d", 1, 1, 3, 2)])
+def test_evaluate_params_matches_reference(mb, g, env, od, ad, res, eps):
+    """Deterministic first-episode returns over the simplex grid: bf16
+    generated weights on the device vs the fp64 reference (chain tolerance:
+    200-step trajectories through the policy)."""
+    spec = mb.HypernetSpec(2, 16, [16], [od, 32, 32, ad], True, True)
+    W, R = mb.evaluate_params(spec, r32(g[f"eval_{env}_flat"]), env, res, eps, 0x1234)
+    assert np.array_equal(W, g[f"eval_{env}_W"])
+    assert_normwise(R, g[f"eval_{env}_R"], REL_CHAIN, what=f"{env} mean returns")
+
+
+def test_evaluate_params_oracle_envs(mb, o):
+    """DST (terminal treasures) and mo-humanoid6 against the C oracle, and
+    more episodes than one CTA holds (partial sums across CTAs)."""
+    from pyoracle import ENV_KINDS, HSpec
+    spec_o = HSpec(2, 16, [16], [1, 32, 32, 1], True, True)
+    spec = mb.HypernetSpec(2, 16, [16], [1, 32, 32, 1], True, True)
+    flat = r32(o.init_hypernet(spec_o, 0x99))
+    W, R = mb.evaluate_params(spec, flat, "mo-dst-continuous", 5, 20, 7)
+    Wo, Ro = o.evaluate_params(spec_o, flat, ENV_KINDS["mo-dst-continuous"], 5, 20, 7)
+    assert np.array_equal(W, Wo)
+    assert_normwise(R, Ro, REL_CHAIN, what="dst mean returns")
+    spec_o = HSpec(6, 32, [32], [45, 64, 64, 12], True, True)
+    spec = mb.HypernetSpec(6, 32, [32], [45, 64, 64, 12], True, True)
+    flat = r32(o.init_hypernet(spec_o, 0x98))
+    W, R = mb.evaluate_params(spec, flat, "mo-humanoid6", 1, 2, 5)
+    Wo, Ro = o.evaluate_params(spec_o, flat, ENV_KINDS["mo-humanoid6"], 1, 2, 5)
+    assert np.array_equal(W, Wo) and len(W) == 6
+    assert_normwise(R, Ro, REL_CHAIN, what="humanoid6 mean returns")
+
+
+def test_evaluate_params_errors(mb):
+    spec = mb.HypernetSpec(2, 16, [16], [4, 32, 32, 2], True, True)
+    flat = mb.init_hypernet(spec, 1)
+    with pytest.raises(mb.ConfigError):
+        mb.evaluate_params(spec, flat, "mo-pointmass", 4, 0, 1)
+    with pytest.raises(mb.ShapeError):
+        mb.evaluate_params(spec, flat, "mo-humanoid6", 4, 1, 1)

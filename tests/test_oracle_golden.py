@@ -128,3 +128,13 @@ def test_wfg_exact_matches_reference_exact_for_small_m(o, g):
 def test_linear_dominance_oracle_matches_reference(o, g, m):
     # golden: the reference's linear_dominance_filter (pareto.cpp:79-139)
     assert np.array_equal(o.linear_dominance_mask(g[f"ldf_pts{m}"]), g[f"ldf_mask{m}"])
+
+
+@pytest.mark.parametrize("env,od,ad,res,eps", [("mo-pointmass", 4, 2, 4, 3), ("mo-lqr1d", 1, 1, 3, 2)])
+def test_evaluate_params_oracle_matches_reference(o, g, env, od, ad, res, eps):
+    # golden: the reference's evaluate_params (evaluate.cpp:17-101)
+    from pyoracle import ENV_KINDS, HSpec
+    spec = HSpec(2, 16, [16], [od, 32, 32, ad], True, True)
+    W, R = o.evaluate_params(spec, g[f"eval_{env}_flat"], ENV_KINDS[env], res, eps, 0x1234)
+    assert np.array_equal(W, g[f"eval_{env}_W"])
+    assert np.array_equal(R, g[f"eval_{env}_R"])
