@@ -356,7 +356,15 @@ def main():
         ach = top[2] / (top[1] / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": tflops, "unit": "TFLOP/s",
                 "frac": ach / tflops}
-    roof.update({"traffic": None, "kernel": top[0], "launches_per_iter": top[4],
+    traffic, tsrc = None, None
+    tpath = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    if os.path.exists(tpath):  # dram__bytes_read + write per launch from an ncu --set full capture
+        tj = json.load(open(tpath)).get(top[0])
+        if tj:
+            traffic, tsrc = tj["dram_bytes_per_launch"], tj["capture"]
+    roof.update({"traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": tsrc,
+                 "algorithmic_bytes_per_launch": top[3] / top[4] if top[4] else None,
+                 "kernel": top[0], "launches_per_iter": top[4],
                  "share_of_step": top[1] / sum(p[1] for p in prof),
                  "peak_source": peak_src + (" bf16 sustained" if roof["bound"] == "tensor" else " copy")})
     breakdown = {p[0]: {"ms": round(p[1], 3), "launches": p[4],

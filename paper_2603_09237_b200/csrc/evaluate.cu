@@ -6,12 +6,12 @@
 // every instance finished its first episode or max_episode_steps; the
 // undiscounted returns of that first episode are averaged per objective.
 //
-// One CTA per (grid point, block of <= 16 instances): the point's generated
+// One CTA per (grid point, block of 8 or 16 instances): the point's generated
 // weights theta_g (from the hypernet GEMM) are staged ONCE into shared
 // memory as bf16 (transposed, [in][out], so thread j reads W[k][j]
 // conflict-free) and stay resident for all steps; activations ping-pong in
 // shared memory as [k][instance]; env state lives in shared memory. Each
-// step: thread j computes output j of a layer for all 16 instances (the
+// step: thread j computes output j of a layer for all the CTA's instances (the
 // instance values are shared-memory broadcasts), then the instance threads
 // step the environment. fp32 arithmetic, fp64 return sums.
 #include <algorithm>
@@ -22,25 +22,26 @@
 namespace mb200 {
 
 namespace {
-constexpr int kEvalE = 16;  // instances per CTA
+constexpr int kEvalE = 16;  // max instances per CTA
 constexpr int kEvalThreads = 256;
 
+template <int E>  // instances per CTA (8 or 16)
 __global__ void __launch_bounds__(kEvalThreads) k_eval(EvalArgs a) {
     extern __shared__ __align__(16) uint8_t sm[];
     const NetDims& nd = a.pol;
     const int g = blockIdx.x / a.cpp, cb = blockIdx.x % a.cpp;
-    const int i0 = cb * kEvalE, n = min(kEvalE, a.episodes - i0);
+    const int i0 = cb * E, n = min(E, a.episodes - i0);
     const float* th = a.theta + (long)g * a.ld;
     // ---- shared-memory carve-up (host sizes the same)
     uint8_t* p = sm;
-    float* S = reinterpret_cast<float*>(p); p += sizeof(float) * a.sdim * kEvalE;
+    float* S = reinterpret_cast<float*>(p); p += sizeof(float) * a.sdim * E;
     float* act[2];
-    act[0] = reinterpret_cast<float*>(p); p += sizeof(float) * a.maxw * kEvalE;
-    act[1] = reinterpret_cast<float*>(p); p += sizeof(float) * a.maxw * kEvalE;
-    double* tot = reinterpret_cast<double*>(p); p += sizeof(double) * kEvalE * 8;
+    act[0] = reinterpret_cast<float*>(p); p += sizeof(float) * a.maxw * E;
+    act[1] = reinterpret_cast<float*>(p); p += sizeof(float) * a.maxw * E;
+    double* tot = reinterpret_cast<double*>(p); p += sizeof(double) * E * 8;
     float* bias = reinterpret_cast<float*>(p); p += sizeof(float) * a.nbias;
     __nv_bfloat16* WT = reinterpret_cast<__nv_bfloat16*>(p);  // per layer [in][out]
-    __shared__ int alive[kEvalE], steps[kEvalE];
+    __shared__ int alive[E], steps[E];
     // ---- weights: theta (fp32, W_l [out][in] then b_l) -> WT_l (bf16, [in][out])
     {
         long wo = 0, bo = 0;
@@ -57,23 +58,23 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(EvalArgs a) {
     }
     // ---- fresh instances: BatchedEnv::reset(rng.split(g)) (env.cpp:51-58)
     const uint64_t gkey = split_key(a.key, (uint64_t)g);
-    if (threadIdx.x < kEvalE) {
+    if (threadIdx.x < E) {
         const int r = threadIdx.x;
         alive[r] = r < n;
         steps[r] = 0;
         for (int k = 0; k < 8; ++k) tot[r * 8 + k] = 0.0;
         if (r < n) {
             uint64_t ctr = 0;
-            env_do_reset(a.kind, S + r, kEvalE, split_key(gkey, (uint64_t)(i0 + r)), &ctr);
+            env_do_reset(a.kind, S + r, E, split_key(gkey, (uint64_t)(i0 + r)), &ctr);
         } else {
-            for (int k = 0; k < a.sdim; ++k) S[k * kEvalE + r] = 0.f;
+            for (int k = 0; k < a.sdim; ++k) S[k * E + r] = 0.f;
         }
     }
     __syncthreads();
     for (int t = 0; t < a.max_steps; ++t) {
-        const int any = __syncthreads_or(threadIdx.x < kEvalE ? alive[threadIdx.x] : 0);
+        const int any = __syncthreads_or(threadIdx.x < E ? alive[threadIdx.x] : 0);
         if (!any) break;  // evaluate.cpp:57
-        for (int e = threadIdx.x; e < a.od * kEvalE; e += blockDim.x) act[0][e] = S[e];  // obs = state[0:od]
+        for (int e = threadIdx.x; e < a.od * E; e += blockDim.x) act[0][e] = S[e];  // obs = state[0:od]
         __syncthreads();
         int cur = 0;
         long wo = 0, bo = 0;
@@ -82,14 +83,15 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(EvalArgs a) {
             const float* ai = act[cur];
             float* ao = act[cur ^ 1];
             for (int j = threadIdx.x; j < out; j += blockDim.x) {
-                float z[kEvalE];
+                float z[E];
 #pragma unroll
-                for (int r = 0; r < kEvalE; ++r) z[r] = bias[bo + j];
+                for (int r = 0; r < E; ++r) z[r] = bias[bo + j];
+#pragma unroll 4
                 for (int k = 0; k < in; ++k) {
                     const float w = __bfloat162float(WT[wo + (long)k * out + j]);
-                    const float4* x4 = reinterpret_cast<const float4*>(ai + k * kEvalE);
+                    const float4* x4 = reinterpret_cast<const float4*>(ai + k * E);
 #pragma unroll
-                    for (int q = 0; q < kEvalE / 4; ++q) {
+                    for (int q = 0; q < E / 4; ++q) {
                         const float4 x = x4[q];
                         z[4 * q + 0] = fmaf(w, x.x, z[4 * q + 0]);
                         z[4 * q + 1] = fmaf(w, x.y, z[4 * q + 1]);
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(EvalArgs a) {
                 }
                 const bool squash = l < nd.L - 1 || nd.out_tanh;
 #pragma unroll
-                for (int r = 0; r < kEvalE; ++r) ao[j * kEvalE + r] = squash ? tanhf(z[r]) : z[r];
+                for (int r = 0; r < E; ++r) ao[j * E + r] = squash ? tanhf(z[r]) : z[r];
             }
             __syncthreads();
             cur ^= 1;
@@ -111,11 +113,11 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(EvalArgs a) {
             const int r = threadIdx.x;
             float ac[16], rw[8];
             for (int d = 0; d < a.ad; ++d) {
-                const float x = act[cur][d * kEvalE + r];
+                const float x = act[cur][d * E + r];
                 if (!isfinite(x)) atomicExch(a.err, 3);
                 ac[d] = fminf(fmaxf(x, -1.f), 1.f);
             }
-            const bool tm = env_do_step(a.kind, S + r, kEvalE, ac, rw);
+            const bool tm = env_do_step(a.kind, S + r, E, ac, rw);
             const int st = steps[r] + 1;
             steps[r] = st;
             const bool tr = !tm && st >= a.max_steps;
@@ -141,28 +143,26 @@ __global__ void k_eval_mean(const double* part, int ng, int cpp, int m, int epis
 }
 }  // namespace
 
-size_t eval_smem(const EvalArgs& a) {
+size_t eval_smem(const EvalArgs& a, int E) {
     size_t w = 0;
     for (int l = 0; l < a.pol.L; ++l) w += (size_t)a.pol.sz[l] * a.pol.sz[l + 1];
-    return sizeof(float) * a.sdim * kEvalE + 2 * sizeof(float) * a.maxw * kEvalE + sizeof(double) * kEvalE * 8 +
+    return sizeof(float) * a.sdim * E + 2 * sizeof(float) * a.maxw * E + sizeof(double) * E * 8 +
            sizeof(float) * a.nbias + 2 * w;
 }
 
 void evaluate(EvalArgs a, int n_points, double* d_mean, cudaStream_t s) {
-    a.cpp = (a.episodes + kEvalE - 1) / kEvalE;
+    const int E = a.episodes <= 8 ? 8 : kEvalE;
+    a.cpp = (a.episodes + E - 1) / E;
     a.maxw = 0;
     a.nbias = 0;
     for (int l = 0; l <= a.pol.L; ++l) a.maxw = std::max(a.maxw, (a.pol.sz[l] + 3) / 4 * 4);
     for (int l = 0; l < a.pol.L; ++l) a.nbias += a.pol.sz[l + 1];
     if (a.ad > 16 || a.m > 8) throw ShapeError("evaluate: act_dim <= 16 and m <= 8 on the device");
-    const size_t smem = (eval_smem(a) + 15) / 16 * 16;
+    const size_t smem = (eval_smem(a, E) + 15) / 16 * 16;
     if (smem > 220 * 1024) throw ShapeError("evaluate: the policy does not fit in shared memory (bf16)");
-    static size_t configured = 0;
-    if (smem > configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
-    k_eval<<<n_points * a.cpp, kEvalThreads, smem, s>>>(a);
+    auto kern = E == 8 ? k_eval<8> : k_eval<16>;
+    MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<n_points * a.cpp, kEvalThreads, smem, s>>>(a);
     MB_LAUNCH();
     const int n = n_points * a.m;
     k_eval_mean<<<(n + 255) / 256, 256, 0, s>>>(a.part, n_points, a.cpp, a.m, a.episodes, d_mean);
