@@ -70,8 +70,8 @@ void comm_destroy(Comm* c) {
     if (c && c->comm) nccl().commDestroy(c->comm);
     delete c;
 }
-void comm_allgather_f32(Comm* c, float* buf, size_t count, cudaStream_t s) {
-    check(nccl().allGather(buf + count * c->rank, buf, count, ncclFloat32, c->comm, s), "ncclAllGather");
+void comm_allreduce_f32(Comm* c, float* buf, size_t count, cudaStream_t s) {
+    check(nccl().allReduce(buf, buf, count, ncclFloat32, ncclSum, c->comm, s), "ncclAllReduce");
 }
 void comm_allreduce_f64(Comm* c, double* buf, size_t count, cudaStream_t s) {
     check(nccl().allReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, s), "ncclAllReduce");

@@ -34,7 +34,8 @@ struct Dense16 {
     long cr, cc;
     int ones_col;       // column N of the output = sum_k A(r, k) -> Cb[r]
     float* Cb;
-    Img img;            // optional bf16 image copy of the output (row r, col c)
+    Img img;            // optional bf16 image copy of the output (row r - img_r0, col c)
+    int img_r0, img_rn; // rows [img_r0, img_r0 + img_rn) go to the image
 };
 
 __global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
@@ -83,8 +84,8 @@ __global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
         v *= 1.f - a * a;
     }
     d.C[r * d.cr + c * d.cc] = v;
-    if (d.img.p)
-        *reinterpret_cast<__nv_bfloat16*>(d.img.p + img_off(r, c, img_ct(d.img.C))) = __float2bfloat16_rn(v);
+    if (d.img.p && r >= d.img_r0 && r < d.img_r0 + d.img_rn)
+        *reinterpret_cast<__nv_bfloat16*>(d.img.p + img_off(r - d.img_r0, c, img_ct(d.img.C))) = __float2bfloat16_rn(v);
 }
 
 void dense16(const Dense16& d, cudaStream_t s) {
@@ -122,7 +123,8 @@ __global__ void __launch_bounds__(256) k_split_dtanh(const float* __restrict__ p
 }
 }  // namespace
 
-void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, cudaStream_t s) {
+void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, int r0, int rn,
+                     cudaStream_t s) {
     for (int l = 0; l < fd.L; ++l) {
         Dense16 d{};
         d.A = l == 0 ? w : fd.act[l];  // act[0] is not materialised: w is the input
@@ -132,7 +134,11 @@ void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, 
         d.bias = p + fd.boff[l];
         d.act = 1;
         d.C = fd.act[l + 1]; d.cr = fd.sz[l + 1]; d.cc = 1;
-        if (l == fd.L - 1) d.img = fimg;
+        if (l == fd.L - 1) {
+            d.img = fimg;
+            d.img_r0 = r0;
+            d.img_rn = rn;
+        }
         dense16(d, s);
     }
 }

@@ -223,8 +223,10 @@ struct FeatDims {
     float* act[kMaxFeatLayers + 1] = {};   // activations [G][sz[l]] (act[0] = w)
     float* gz[kMaxFeatLayers] = {};        // pre-activation gradients [G][sz[l+1]]
 };
-// act[1..L], fimg (bf16 image of f) for all G rows of the cluster weights w [G][m]
-void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, cudaStream_t s);
+// act[1..L] for all G rows of the cluster weights w [G][m]; fimg (bf16 image
+// of f) gets rows [r0, r0 + rn) as image rows 0..rn-1
+void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, int r0, int rn,
+                     cudaStream_t s);
 // df = sum of the split-K partials [splits][G][F]; writes dW/db of every layer into gout (flat layout)
 void feature_backward(const FeatDims& fd, const float* p, const float* w, const float* parts, int splits, int G,
                       float* gout, cudaStream_t s);

@@ -303,21 +303,23 @@ static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
 
 // feature map f(w) for all G groups (SIMT: K = m is tiny), then on the tensor
 // cores theta[g][p] = b[p] + sum_k M[p][k] f[g][k] (hypernet.cpp:73-88) for
-// all groups; [g0, g0+ng) are this rank's clusters.
+// this rank's clusters [g0, g0+ng) only (theta rows keep global indices).
 void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
     {
         double fl = 0;
         for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 2.0 * G * fsz[l] * fsz[l + 1];
         ProfScope ps("feature_fwd", fl, 0, s);
         w_last = w;
-        feature_forward(fd, p, w, G, fimg, s);  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
+        fg0 = g0;
+        fng = ng;
+        feature_forward(fd, p, w, G, fimg, g0, ng, s);  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
     }
     IGemm d;  // theta[g][p] = b[p] + sum_k f[g][k] M[p][k]: rows = clusters, contiguous theta rows
     d.A = fimg; d.a_view = 0;          // (m = g, k = f)
     d.B = mimg; d.b_view = 0;          // (n = p, k = f)
-    d.M = G; d.N = (int)P; d.K = F;
+    d.M = ng; d.N = (int)P; d.K = F;
     d.bias = p + nf + P * F; d.bias_mode = 1;
-    d.C = theta; d.cm = ld; d.cn = 1;
+    d.C = theta + (long)g0 * ld; d.cm = ld; d.cn = 1;
     igemm("hyper_theta", d, s);
     PackDims pd;  // generated weights of this rank's clusters -> per-layer bf16 images
     pd.L = tgt.L;
@@ -334,20 +336,20 @@ void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
 
 void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, mimg, 1, s); }
 
-// hypernet_backward (hypernet.cpp:92-122) summed over all groups:
-// db = sum_g gtheta_g, dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then
-// the feature-map backward. Writes (not accumulates) the flat grad g.
-// hypernet_backward (hypernet.cpp:92-122) summed over all groups:
-// db = sum_g gtheta_g, dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then
-// the feature-map backward. Writes (not accumulates) the flat grad g.
+// hypernet_backward (hypernet.cpp:92-122) summed over the clusters of the
+// last forward ([fg0, fg0 + fng), this rank's): db = sum_g gtheta_g,
+// dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then the feature-map
+// backward. Writes (not accumulates) the flat grad g; with several ranks it
+// is the rank's partial sum, all-reduced by the trainer before Adam.
 void HyperNet::backward(cudaStream_t s) {
     const long nM = P * F;
-    gtheta_prep(gtheta, ld, G, (int)P, gimg, g + nf + nM, s);  // gimg + db in one pass
+    const int ng = fng;
+    gtheta_prep(gtheta + (long)fg0 * ld, ld, ng, (int)P, gimg, g + nf + nM, s);  // gimg + db in one pass
     {
         IGemm d;  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
         d.A = gimg; d.a_view = 1;  // (m = p, k = g)
         d.B = fimg; d.b_view = 1;  // (n = f, k = g)
-        d.M = (int)P; d.N = F; d.K = G;
+        d.M = (int)P; d.N = F; d.K = ng;
         d.C = g + nf; d.cm = F; d.cn = 1;
         igemm("hyper_dM", d, s);
     }
@@ -355,16 +357,18 @@ void HyperNet::backward(cudaStream_t s) {
         IGemm d;  // gf[g][k] = sum_p gtheta[g][p] M[p][k], split-K over 128-aligned P ranges
         d.A = gimg; d.a_view = 0;  // (m = g, k = p)
         d.B = mimg; d.b_view = 1;  // (n = f, k = p)
-        d.M = G; d.N = F; d.K = (int)P; d.Z = splits;
+        d.M = ng; d.N = F; d.K = (int)P; d.Z = splits;
         d.gmode = 2; d.goff = d_split_bounds;
-        d.C = parts; d.cm = F; d.cn = 1; d.c_gs = (long)G * F;
+        d.C = parts; d.cm = F; d.cn = 1; d.c_gs = (long)ng * F;
         igemm("hyper_df", d, s);
     }
-    {  // df reduction + feature-map backward (all layers' dW, db)
+    {  // df reduction + feature-map backward (all layers' dW, db) over the local rows
         double fl = 0;
-        for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 4.0 * G * fsz[l] * fsz[l + 1];
+        for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 4.0 * ng * fsz[l] * fsz[l + 1];
         ProfScope ps("feature_bwd", fl, 0, s);
-        feature_backward(fd, p, w_last, parts, splits, G, g, s);
+        FeatDims fl_d = fd;
+        for (int l = 0; l <= fd.L; ++l) fl_d.act[l] = fd.act[l] + (long)fg0 * fd.sz[l];
+        feature_backward(fl_d, p, w_last + (long)fg0 * m, parts, splits, ng, g, s);
     }
 }
 
@@ -445,7 +449,7 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     Rl_ = (long)Nl_ * cfg.T;
     MB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
     MB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_c_done_})
+    for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_c_done_, &ev_cb_, &ev_cr_})
         MB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     MB_CUDA(cudaEventRecord(ev_c_done_, s2_));
     if (world > 1) comm_ = comm_create(world, rank, nccl_id);
@@ -486,7 +490,7 @@ Trainer::~Trainer() {
         cudaFree(u.psls);
         cudaFree(u.lossrows);
     }
-    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_c_done_})
+    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_c_done_, ev_cb_, ev_cr_})
         if (e) cudaEventDestroy(e);
     if (s2_) cudaStreamDestroy(s2_);
     for (auto& u : ub_) cudaFree(u.Zf);
@@ -878,8 +882,10 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
     }
 }
 
-void Trainer::allgather_gtheta(HyperNet& h) {
-    if (comm_) comm_allgather_f32(comm_, h.gtheta, (size_t)Kl_ * h.ld, s_);
+void Trainer::allreduce_grad(HyperNet& h, cudaStream_t s) {
+    // the per-minibatch hypernetwork-gradient all-reduce: each rank's
+    // backward summed over its own clusters (linear in gtheta)
+    if (comm_) comm_allreduce_f32(comm_, h.g, (size_t)h.n, s);
 }
 
 // One PPO minibatch (train.cpp:163-180). The actor chain runs on s_, the
@@ -913,13 +919,24 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     actor_.forward(d_cw, g_lo_, Kl_, s_);
     net_step(actor_, true, Bp, inv_B, maxg, rows, goff, slot, s_);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_net_, 0));
-    allgather_gtheta(actor_);
-    allgather_gtheta(critic_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
     MB_CUDA(cudaEventRecord(ev_chk_, s_));
     MB_CUDA(cudaStreamWaitEvent(sc, ev_chk_, 0));
     critic_.backward(sc);
+    if (comm_) {  // every NCCL call goes on s_: one stream per communicator, device order = host order
+        MB_CUDA(cudaEventRecord(ev_cb_, sc));
+        actor_.backward(s_);
+        MB_CUDA(cudaStreamWaitEvent(s_, ev_cb_, 0));
+        allreduce_grad(critic_, s_);
+        MB_CUDA(cudaEventRecord(ev_cr_, s_));
+        MB_CUDA(cudaStreamWaitEvent(sc, ev_cr_, 0));
+        critic_.adam_step(cfg_.critic_lr, d_err, sc);
+        MB_CUDA(cudaEventRecord(ev_c_done_, sc));
+        allreduce_grad(actor_, s_);
+        actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
+        return;
+    }
     critic_.adam_step(cfg_.critic_lr, d_err, sc);
     MB_CUDA(cudaEventRecord(ev_c_done_, sc));
     actor_.backward(s_);
@@ -1013,11 +1030,11 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
     }
     net_step(actor_, true, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
     net_step(critic_, false, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
-    allgather_gtheta(actor_);
-    allgather_gtheta(critic_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss, 2, s_);
     actor_.backward(s_);
     critic_.backward(s_);
+    allreduce_grad(actor_, s_);
+    allreduce_grad(critic_, s_);
     double l[2];
     int err = 0;
     MB_CUDA(cudaMemcpyAsync(l, d_mbloss, sizeof(l), cudaMemcpyDeviceToHost, s_));

@@ -68,6 +68,7 @@ struct HyperNet {
     std::vector<float*> fgz;   // feature pre-activation gradients [G][fsz[l+1]]
     FeatDims fd{};             // device view of the feature MLP (feature.cu)
     const float* w_last = nullptr;  // cluster weights of the last forward (feature-map input)
+    int fg0 = 0, fng = 0;           // clusters [fg0, fg0 + fng) of the last forward (this rank's)
     int splits = 1;
     int* d_split_bounds = nullptr;
     // bf16 tiled images (img.cuh) feeding the tcgen05 GEMMs
@@ -171,7 +172,7 @@ private:
     void minibatch(int slot, int B, int Bglob, int maxg, const int* d_rows, const int* d_goff);
     void net_step(HyperNet& h, bool actor, int Bp, float inv_B, int maxg, const int* rows, const int* d_goff,
                   int slot, cudaStream_t st);
-    void allgather_gtheta(HyperNet& h);
+    void allreduce_grad(HyperNet& h, cudaStream_t s);
 
     TrainConfig cfg_;
     EnvSpecB es_{};
@@ -201,6 +202,7 @@ private:
     } ub_[2];
     cudaStream_t s2_ = nullptr;  // critic chain of the update
     cudaEvent_t ev_gather_ = nullptr, ev_c_net_ = nullptr, ev_chk_ = nullptr, ev_c_done_ = nullptr;
+    cudaEvent_t ev_cb_ = nullptr, ev_cr_ = nullptr;  // multi-GPU: critic backward done / its all-reduce done
     Img Xi_;                    // [Bp][obs] gathered observations (bf16 image)
     std::vector<uint8_t*> img_allocs_;
     std::vector<int> rows_tmp_;

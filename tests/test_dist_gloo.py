@@ -6,8 +6,10 @@ trainer uses (trainer.cu: Trainer::phase_advantages / minibatch):
   * a minibatch is the global perm slice, each rank keeps its own rows
     (shard_minibatch, the C-ABI host helper) and scales by the GLOBAL 1/B;
   * the hypernetwork gradient is linear in the per-cluster theta gradients,
-    so summing the per-rank gradients (what the NCCL all-gather of gtheta +
-    replicated hypernet backward computes) equals the single-process one.
+    so each rank's hypernet backward over its own clusters, summed across
+    ranks (the per-minibatch NCCL gradient all-reduce, Trainer::allreduce_grad),
+    equals the single-process gradient; Adam then runs replicated on the
+    identical all-reduced gradient.
 
 Each rank computes with the fp64 C oracle; results are compared with the
 single-process oracle on the same seeded inputs."""
