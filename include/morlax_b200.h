@@ -148,7 +148,9 @@ typedef struct {
 
 typedef struct morlax_trainer morlax_trainer;
 /* world > 1: one trainer per GPU/rank; nccl_id = 128 bytes from
- * morlax_nccl_unique_id() on rank 0, broadcast by the caller. */
+ * morlax_nccl_unique_id() on rank 0, broadcast by the caller. A non-NULL
+ * nccl_id with world == 1 builds a single-rank communicator (the
+ * multi-GPU code path on one GPU; results identical to nccl_id == NULL). */
 int morlax_nccl_unique_id(void* out128);
 int morlax_trainer_create(const morlax_train_config* cfg, int world, int rank, const void* nccl_id,
                           morlax_trainer** out);

@@ -452,7 +452,9 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_c_done_, &ev_cb_, &ev_cr_})
         MB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     MB_CUDA(cudaEventRecord(ev_c_done_, s2_));
-    if (world > 1) comm_ = comm_create(world, rank, nccl_id);
+    // a communicator whenever an NCCL id is given (world == 1 included: the
+    // single-rank collectives exercise the multi-GPU code path on one GPU)
+    if (world > 1 || nccl_id) comm_ = comm_create(world, rank, nccl_id);
     root_ = HostRng::seeded(cfg.seed);
     std::vector<int> as{es_.obs_dim}, cs{es_.obs_dim};
     for (int h : cfg.actor_hidden) as.push_back(h);

@@ -454,3 +454,18 @@ def test_evaluate_params_errors(mb):
         mb.evaluate_params(spec, flat, "mo-pointmass", 4, 0, 1)
     with pytest.raises(mb.ShapeError):
         mb.evaluate_params(spec, flat, "mo-humanoid6", 4, 1, 1)
+
+
+def test_single_rank_nccl_path_matches(mb):
+    """The multi-GPU code path (NCCL all-reduces of the normalisation sums,
+    the losses and the hypernet gradients, all on one stream) with a
+    single-rank communicator gives bit-identical results to the no-NCCL run."""
+    cfg = mb.TrainConfig(env_name="mo-pointmass", N=64, K=4, T=16, epochs=2, minibatch_count=2, seed=5, F=16,
+                         feature_hidden=[16], actor_hidden=[32, 32], critic_hidden=[32, 32])
+    a = mb.Trainer(cfg)
+    b = mb.Trainer(cfg, 1, 0, mb.nccl_unique_id())
+    for it in range(2):
+        sa, sb = a.iteration(it), b.iteration(it)
+        assert sa.actor_loss == sb.actor_loss and sa.critic_loss == sb.critic_loss
+    assert np.array_equal(a.params("actor"), b.params("actor"))
+    assert np.array_equal(a.params("critic"), b.params("critic"))
