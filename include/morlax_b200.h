@@ -171,6 +171,25 @@ int morlax_trainer_set_params(morlax_trainer* t, int which, const double* in);
 /* flat hypernet gradient of the last backward pass (morlax_trainer_losses
  * or the last minibatch of an iteration) */
 int morlax_trainer_get_grad(morlax_trainer* t, int which, double* out);
+/* Checkpoint wire format of the reference (save_checkpoint / load_checkpoint,
+ * src/checkpoint.cpp:15-241; "MRLXCKPT" v1, little-endian fixed width): the
+ * trainer's RunConfig, specs, fp64 params in flatten_hypernet order,
+ * `iteration`, root Rng(seed) key / counter. The RunConfig fields the
+ * trainer does not hold come from `extra` (NULL = the reference defaults:
+ * iterations 300, eval grid 10 / 8 episodes / interval 10, empty pareto
+ * reference). Loading checks magic, version, architecture and counts
+ * (ConfigError) and sets both hypernets' params (like the reference, no
+ * Adam state is stored). */
+typedef struct {
+    int iterations;
+    int grid_resolution, episodes_per_point, log_interval;
+    int n_pareto_reference;
+    const double* pareto_reference;
+} morlax_checkpoint_extra;
+int morlax_trainer_save_checkpoint(morlax_trainer* t, const char* path, int64_t iteration,
+                                   const morlax_checkpoint_extra* extra);
+int morlax_trainer_load_checkpoint(morlax_trainer* t, const char* path, int64_t* iteration_out);
+
 int morlax_trainer_get_theta(morlax_trainer* t, int which, float* out /* local K x P */);
 /* field: obs action_pre logprob reward value next_value advantages
  * value_targets scalar_advantage (float) | terminated truncated (uint8) |

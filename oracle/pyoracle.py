@@ -408,6 +408,14 @@ class Oracle:
                                               C.c_uint64(key), _p(W), _p(R), C.byref(npts)))
         return W[:npts.value], R[:npts.value]
 
+    def checkpoint_resave(self, src, dst, n_actor, n_critic):
+        """The reference's load_checkpoint(src) + save_checkpoint(dst) (ref lib only)."""
+        a, c = np.zeros(n_actor), np.zeros(n_critic)
+        it = C.c_int64()
+        self.check(self.lib.mref_checkpoint_resave(src.encode(), dst.encode(), _p(a), C.c_int64(n_actor), _p(c),
+                                                   C.c_int64(n_critic), C.byref(it)))
+        return a, c, it.value
+
     def linear_dominance_mask(self, pts):
         pts = np.ascontiguousarray(pts, np.float64)
         n, m = pts.shape

@@ -480,6 +480,20 @@ void mref_trainer_perm(void* tp, int32_t* out) {
     std::copy(t.perm.begin(), t.perm.end(), out);
 }
 
+// load_checkpoint + save_checkpoint of the reference (checkpoint.cpp:200-241):
+// reads `in`, returns the params and iteration, writes the same checkpoint to `out`
+int mref_checkpoint_resave(const char* in, const char* out, double* actor_out, int64_t cap_a, double* critic_out,
+                           int64_t cap_c, int64_t* iteration) {
+    return guarded([&] {
+        const Checkpoint ck = load_checkpoint(in);
+        if ((int64_t)ck.actor_params.size() > cap_a || (int64_t)ck.critic_params.size() > cap_c)
+            throw ShapeError("checkpoint_resave: output buffers too small");
+        std::copy(ck.actor_params.begin(), ck.actor_params.end(), actor_out);
+        std::copy(ck.critic_params.begin(), ck.critic_params.end(), critic_out);
+        *iteration = ck.iteration;
+        save_checkpoint(ck, out);
+    });
+}
 int64_t mref_simplex_grid_size(int m, int res) { return (int64_t)simplex_grid_size(m, res); }
 int mref_evaluate_params(const mo_hspec* h, const double* flat, int env_kind, int res, int episodes,
                          uint64_t key, double* w_out, double* mean_out, int64_t* n_points) {

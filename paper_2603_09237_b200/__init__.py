@@ -398,6 +398,12 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class _CkExtraC(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("grid_resolution", C.c_int), ("episodes_per_point", C.c_int),
+                ("log_interval", C.c_int), ("n_pareto_reference", C.c_int),
+                ("pareto_reference", C.POINTER(C.c_double))]
+
+
 class Trainer:
     """The reference train() loop body on the GPU (train.cpp:118-184).
     world > 1: one Trainer per GPU/rank (environments and preference clusters
@@ -477,6 +483,20 @@ class Trainer:
               else np.uint64 if name == "env_ctr" else np.int32)
         v = np.ascontiguousarray(value, dt).reshape(self._shape(name))
         _check(LIB.morlax_trainer_set(self._h, name.encode(), _ptr(v)))
+
+    def save_checkpoint(self, path: str, iteration: int, iterations: int = 300, grid_resolution: int = 10,
+                        episodes_per_point: int = 8, log_interval: int = 10, pareto_reference=None):
+        """save_checkpoint (checkpoint.cpp:200-213): the reference's MRLXCKPT v1 bytes."""
+        ref = _f64(pareto_reference if pareto_reference is not None else [])
+        x = _CkExtraC(iterations, grid_resolution, episodes_per_point, log_interval, len(ref),
+                      ref.ctypes.data_as(C.POINTER(C.c_double)) if len(ref) else None)
+        _check(LIB.morlax_trainer_save_checkpoint(self._h, path.encode(), C.c_int64(iteration), C.byref(x)))
+
+    def load_checkpoint(self, path: str) -> int:
+        """load_checkpoint (checkpoint.cpp:215-241) into this trainer's hypernets; returns the iteration."""
+        it = C.c_int64()
+        _check(LIB.morlax_trainer_load_checkpoint(self._h, path.encode(), C.byref(it)))
+        return it.value
 
     def losses(self, rows):
         r = np.ascontiguousarray(rows, np.int32)

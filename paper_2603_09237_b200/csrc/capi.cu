@@ -2,6 +2,7 @@
 // reference's C++ exceptions to the CLI's status codes
 // (tools/commands.hpp:12-32) and records a thread-local message.
 #include <cmath>
+#include <cstdio>
 #include <functional>
 #include <cstring>
 #include <string>
@@ -105,6 +106,66 @@ struct morlax_policy {
     GroupPolicy* p = nullptr;
     int m = 0;
 };
+
+namespace mb200 {
+// ---- checkpoint wire format (checkpoint.cpp:15-241): "MRLXCKPT", u32 v1,
+// RunConfig, actor / critic HypernetSpec, fp64 params (flatten_hypernet
+// order), i64 iteration, root Rng key / counter; little-endian fixed width
+namespace {
+const char* env_name_of(int kind) {
+    switch (kind) {
+        case ENV_LQR: return "mo-lqr1d";
+        case ENV_LQR_M1: return "mo-lqr1d-m1";
+        case ENV_POINTMASS: return "mo-pointmass";
+        case ENV_DST: return "mo-dst-continuous";
+    }
+    return "mo-humanoid6";
+}
+struct CkWriter {
+    std::string buf;
+    void raw(const void* p, size_t n) { buf.append(static_cast<const char*>(p), n); }
+    template <typename T>
+    void put(T v) { raw(&v, sizeof(T)); }
+    void str(const std::string& s) { put<uint64_t>(s.size()); raw(s.data(), s.size()); }
+    void vec_i32(const std::vector<int>& v) { put<uint64_t>(v.size()); for (int x : v) put<int32_t>(x); }
+    void vec_f64(const std::vector<double>& v) { put<uint64_t>(v.size()); raw(v.data(), v.size() * 8); }
+};
+struct CkReader {
+    const std::string& b;
+    size_t o = 0;
+    std::string path;
+    void raw(void* p, size_t n) {
+        if (o + n > b.size()) throw ConfigError("checkpoint truncated: " + path);
+        std::memcpy(p, b.data() + o, n);
+        o += n;
+    }
+    template <typename T>
+    T get() { T v; raw(&v, sizeof(T)); return v; }
+    uint64_t len(uint64_t cap) {
+        const uint64_t n = get<uint64_t>();
+        if (n > cap) throw ConfigError("checkpoint corrupt (oversized field): " + path);
+        return n;
+    }
+    std::string str() { const uint64_t n = len(1u << 20); std::string s(n, '\0'); raw(&s[0], n); return s; }
+    std::vector<int> vec_i32() { const uint64_t n = len(1u << 20); std::vector<int> v(n); for (auto& x : v) x = get<int32_t>(); return v; }
+    std::vector<double> vec_f64() { const uint64_t n = len(1u << 28); std::vector<double> v(n); raw(v.data(), n * 8); return v; }
+};
+void write_spec(CkWriter& w, const HyperNet& h, const std::vector<int>& fh) {  // write_hypernet_spec
+    w.put<int32_t>(h.m);
+    w.put<int32_t>(h.F);
+    w.vec_i32(fh);
+    w.vec_i32(std::vector<int>(h.tgt.sz, h.tgt.sz + h.tgt.L + 1));
+    w.put<uint8_t>(h.tgt.out_tanh ? 1 : 0);
+    w.put<uint8_t>(h.tgt.has_log_std ? 1 : 0);
+}
+std::vector<double> params_f64(const HyperNet& h, cudaStream_t s) {
+    std::vector<float> f(h.n);
+    MB_CUDA(cudaStreamSynchronize(s));
+    MB_CUDA(cudaMemcpy(f.data(), h.p, sizeof(float) * h.n, cudaMemcpyDeviceToHost));
+    return std::vector<double>(f.begin(), f.end());
+}
+}  // namespace
+}  // namespace mb200
 
 extern "C" {
 
@@ -516,6 +577,96 @@ int morlax_trainer_sizes(morlax_trainer* t, int64_t* ap, int64_t* cp, int* le, i
         if (rows) *rows = tr.local_envs() * tr.config().T;
     });
 }
+
+int morlax_trainer_save_checkpoint(morlax_trainer* t, const char* path, int64_t iteration,
+                                   const morlax_checkpoint_extra* x) {
+    return guarded([&] {
+        Trainer& tr = *t->t;
+        const TrainConfig& c = tr.config();
+        const morlax_checkpoint_extra def{300, 10, 8, 10, 0, nullptr};  // trainer.hpp:39, 59-62 defaults
+        const morlax_checkpoint_extra& e = x ? *x : def;
+        CkWriter w;
+        w.raw("MRLXCKPT", 8);
+        w.put<uint32_t>(1);
+        w.str(env_name_of(c.env_kind));  // write_run_config (checkpoint.cpp:137-163)
+        w.put<int32_t>(c.N); w.put<int32_t>(c.K); w.put<int32_t>(c.kappa); w.put<int32_t>(c.T);
+        w.put<double>(c.gamma); w.put<double>(c.lambda); w.put<double>(c.clip_eps);
+        w.put<int32_t>(c.epochs); w.put<int32_t>(c.minibatch_count);
+        w.put<double>(c.actor_lr); w.put<double>(c.critic_lr); w.put<double>(c.entropy_coef);
+        w.put<int32_t>(e.iterations);
+        w.put<uint64_t>(c.seed);
+        w.put<int32_t>(c.F);
+        w.vec_i32(c.feat_hidden); w.vec_i32(c.actor_hidden); w.vec_i32(c.critic_hidden);
+        w.put<int32_t>(e.grid_resolution); w.put<int32_t>(e.episodes_per_point); w.put<int32_t>(e.log_interval);
+        w.vec_f64(std::vector<double>(e.pareto_reference, e.pareto_reference + (e.pareto_reference ? e.n_pareto_reference : 0)));
+        write_spec(w, tr.actor(), c.feat_hidden);
+        write_spec(w, tr.critic(), c.feat_hidden);
+        w.vec_f64(params_f64(tr.actor(), tr.stream()));
+        w.vec_f64(params_f64(tr.critic(), tr.stream()));
+        w.put<int64_t>(iteration);
+        w.put<uint64_t>(seed_key(c.seed));  // the root Rng(seed) is only ever split: counter 0
+        w.put<uint64_t>(0);
+        FILE* f = std::fopen(path, "wb");
+        if (!f) throw ConfigError(std::string("cannot open checkpoint for writing: ") + path);
+        const size_t n = std::fwrite(w.buf.data(), 1, w.buf.size(), f);
+        if (std::fclose(f) != 0 || n != w.buf.size()) throw ConfigError(std::string("failed writing checkpoint: ") + path);
+    });
+}
+
+int morlax_trainer_load_checkpoint(morlax_trainer* t, const char* path, int64_t* iteration) {
+    return guarded([&] {  // load_checkpoint (checkpoint.cpp:215-241) + the params into the trainer
+        FILE* f = std::fopen(path, "rb");
+        if (!f) throw ConfigError(std::string("cannot open checkpoint: ") + path);
+        std::string b;
+        char tmp[1 << 16];
+        size_t k;
+        while ((k = std::fread(tmp, 1, sizeof(tmp), f)) > 0) b.append(tmp, k);
+        std::fclose(f);
+        CkReader r{b, 0, path};
+        char magic[8];
+        r.raw(magic, 8);
+        if (std::memcmp(magic, "MRLXCKPT", 8) != 0) throw ConfigError(std::string("not a checkpoint file: ") + path);
+        const uint32_t ver = r.get<uint32_t>();
+        if (ver != 1) throw ConfigError("unsupported checkpoint version " + std::to_string(ver) + ": " + path);
+        r.str();
+        for (int i = 0; i < 4; ++i) r.get<int32_t>();
+        for (int i = 0; i < 3; ++i) r.get<double>();
+        for (int i = 0; i < 2; ++i) r.get<int32_t>();
+        for (int i = 0; i < 3; ++i) r.get<double>();
+        r.get<int32_t>();
+        r.get<uint64_t>();
+        r.get<int32_t>();
+        for (int i = 0; i < 3; ++i) r.vec_i32();
+        for (int i = 0; i < 3; ++i) r.get<int32_t>();
+        r.vec_f64();
+        Trainer& tr = *t->t;
+        for (HyperNet* h : {&tr.actor(), &tr.critic()}) {  // read_hypernet_spec, checked against the trainer
+            const int m = r.get<int32_t>(), F = r.get<int32_t>();
+            const std::vector<int> fh = r.vec_i32(), ts = r.vec_i32();
+            r.get<uint8_t>();
+            r.get<uint8_t>();
+            const std::vector<int> mine(h->tgt.sz, h->tgt.sz + h->tgt.L + 1);
+            std::vector<int> fmine(h->fsz.begin() + 1, h->fsz.end() - 1);
+            if (m != h->m || F != h->F || ts != mine || fh != fmine)
+                throw ConfigError(std::string("checkpoint architecture does not match the trainer: ") + path);
+        }
+        const std::vector<double> a = r.vec_f64(), c = r.vec_f64();
+        if ((long)a.size() != tr.actor().n || (long)c.size() != tr.critic().n)
+            throw ConfigError(std::string("checkpoint parameter count mismatch: ") + path);
+        const int64_t it = r.get<int64_t>();
+        if (iteration) *iteration = it;
+        MB_CUDA(cudaStreamSynchronize(tr.stream()));
+        for (int w = 0; w < 2; ++w) {
+            HyperNet& h = w ? tr.critic() : tr.actor();
+            const std::vector<double>& v = w ? c : a;
+            std::vector<float> fl(v.begin(), v.end());
+            MB_CUDA(cudaMemcpy(h.p, fl.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+            h.refresh_images(tr.stream());
+        }
+        MB_CUDA(cudaStreamSynchronize(tr.stream()));
+    });
+}
+
 int morlax_trainer_get_params(morlax_trainer* t, int which, double* out) {
     return guarded([&] {
         HyperNet& h = which ? t->t->critic() : t->t->actor();

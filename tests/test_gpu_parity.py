@@ -469,3 +469,32 @@ def test_single_rank_nccl_path_matches(mb):
         assert sa.actor_loss == sb.actor_loss and sa.critic_loss == sb.critic_loss
     assert np.array_equal(a.params("actor"), b.params("actor"))
     assert np.array_equal(a.params("critic"), b.params("critic"))
+
+
+# ------------------------------------------------------------------ checkpoint wire format (checkpoint.cpp)
+def test_checkpoint_is_the_reference_format(mb, tmp_path):
+    from helpers import ref_available
+    cfg = mb.TrainConfig(env_name="mo-pointmass", N=32, K=4, T=8, epochs=1, minibatch_count=2, seed=3, F=16,
+                         feature_hidden=[16], actor_hidden=[32, 32], critic_hidden=[32, 32])
+    t = mb.Trainer(cfg)
+    t.iteration(0)
+    path = str(tmp_path / "ck.bin")
+    t.save_checkpoint(path, 1, iterations=7, pareto_reference=[-1.0, -2.0])
+    u = mb.Trainer(cfg)
+    assert u.load_checkpoint(path) == 1
+    assert np.array_equal(u.params("actor"), t.params("actor"))
+    assert np.array_equal(u.params("critic"), t.params("critic"))
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"NOTACKPT" + open(path, "rb").read()[8:])
+    with pytest.raises(mb.ConfigError):
+        u.load_checkpoint(str(bad))
+    trunc = tmp_path / "trunc.bin"
+    trunc.write_bytes(open(path, "rb").read()[:100])
+    with pytest.raises(mb.ConfigError):
+        u.load_checkpoint(str(trunc))
+    if ref_available():  # the compiled reference reads it and writes back the identical bytes
+        r = Oracle("ref")
+        out = str(tmp_path / "ref.bin")
+        a, c, it = r.checkpoint_resave(path, out, t.n_actor, t.n_critic)
+        assert it == 1 and np.array_equal(a, t.params("actor")) and np.array_equal(c, t.params("critic"))
+        assert open(out, "rb").read() == open(path, "rb").read()
