@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
                                             (reinterpret_cast<uintptr_t>(d.C) & 15) == 0)) &&
                               (EPI != 1 || !d.C2);
             if (active && fast) {
-                constexpr int NCH = HALF / 16, PF = NCH < 4 ? NCH : 4;
+                constexpr int NCH = HALF / 16;
                 // image byte offset of (row m, column n0 + half * HALF); + chunk offset below
                 const long rowo_x = ((long)(m >> 7) * CTx) * 32768 + ((m & 127) >> 3) * 2048 + (m & 7) * 16;
                 const long rowo_o = ((long)(m >> 7) * CTo) * 32768 + ((m & 127) >> 3) * 2048 + (m & 7) * 16;
@@ -232,18 +232,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
                 // chunk ci = columns cb + 16 ci .. +15, inside one 128-column chunk
                 // for every BN ((cb & 127) + 16 ci <= 112): 2 core-matrix columns
                 auto coff = [](int ci) -> long { return (long)ci * 256; };
-                uint4 ring[PF][2];
-                if (EPI == 2) {
-#pragma unroll
-                    for (int q = 0; q < PF; ++q) {
-                        ring[q][0] = *reinterpret_cast<const uint4*>(xb + coff(q));
-                        ring[q][1] = *reinterpret_cast<const uint4*>(xb + coff(q) + 128);
-                    }
-                }
-                umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
-                umma::fence_after_sync();
-#pragma unroll
-                for (int ci = 0; ci < NCH; ++ci) {
+                // one 16-column chunk: TMEM -> bias -> activation -> bf16 image (or
+                // fp32 via the staging transpose); ax = this chunk's tanh' operand
+                auto chunk = [&](int ci, const uint4* ax) {
                     const int c0 = half * HALF + ci * 16;
                     float v[16];
                     if (ti.nk > 0) {
@@ -261,17 +252,12 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
                     }
                     if (EPI == 0) {
                         stage_store(d.C + wofs + ci * 16, v);
-                        continue;
+                        return;
                     }
                     if (EPI == 1) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) v[i] = umma::tanh_approx(v[i]);
                     } else {
-                        uint4 ax[2] = {ring[ci % PF][0], ring[ci % PF][1]};
-                        if (ci + PF < NCH) {
-                            ring[ci % PF][0] = *reinterpret_cast<const uint4*>(xb + coff(ci + PF));
-                            ring[ci % PF][1] = *reinterpret_cast<const uint4*>(xb + coff(ci + PF) + 128);
-                        }
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&ax[h]);
@@ -313,12 +299,33 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
                     q1.w = umma::pack_bf16(v[14], v[15]);
                     *reinterpret_cast<uint4*>(ob + coff(ci)) = q0;
                     *reinterpret_cast<uint4*>(ob + coff(ci) + 128) = q1;
+                };
+                // pairs of chunks, the next pair's tanh' operands in flight under
+                // this pair's math; kept rolled (the fully unrolled epilogue did
+                // not fit the instruction cache: "no_instructions" stalls)
+                auto aux = [&](int ci, uint4* dst) {
+                    if (EPI == 2 && ci < NCH) {
+                        dst[0] = *reinterpret_cast<const uint4*>(xb + coff(ci));
+                        dst[1] = *reinterpret_cast<const uint4*>(xb + coff(ci) + 128);
+                    }
+                };
+                uint4 cur[4], nxt[4];
+                aux(0, cur);
+                aux(1, cur + 2);
+                umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+                umma::fence_after_sync();
+#pragma unroll 1
+                for (int ci = 0; ci < NCH; ci += 2) {
+                    aux(ci + 2, nxt);
+                    aux(ci + 3, nxt + 2);
+                    chunk(ci, cur);
+                    if (ci + 1 < NCH) chunk(ci + 1, cur + 2);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
                 }
             } else if (active) {
-                // tanh' operand: 4-deep register prefetch ring (loads issued up to
-                // four 16-column chunks ahead, the first four before the tfull wait)
-                constexpr int NCH = HALF / 16, PF = NCH < 4 ? NCH : 4;
-                uint4 ring[PF][2];
+                // partial tiles (edges of M or N): guarded, rolled
+                constexpr int NCH = HALF / 16;
                 auto aux_load = [&](int ci, uint4* dst) {
                     const int nb2 = ti.n0 + half * HALF + ci * 16;
                     dst[0] = dst[1] = make_uint4(0, 0, 0, 0);
@@ -327,24 +334,16 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
                         if (nb2 + 8 < d.N) dst[1] = *reinterpret_cast<const uint4*>(d.aux.p + img_off(m, nb2 + 8, CTx));
                     }
                 };
-                if (EPI == 2) {
-#pragma unroll
-                    for (int q = 0; q < PF; ++q) aux_load(q, ring[q]);
-                }
                 umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));  // committed even when nk == 0
                 umma::fence_after_sync();
-#pragma unroll
+#pragma unroll 1
                 for (int ci = 0; ci < NCH; ++ci) {
                     const int c0 = half * HALF + ci * 16;
                     const int nb = ti.n0 + c0;
                     const bool full = mrow && nb + 16 <= d.N;
                     const bool any = mrow && nb < d.N;
-                    uint4 ax[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-                    if (EPI == 2) {
-                        ax[0] = ring[ci % PF][0];
-                        ax[1] = ring[ci % PF][1];
-                        if (ci + PF < NCH) aux_load(ci + PF, ring[ci % PF]);
-                    }
+                    uint4 ax[2];
+                    aux_load(ci, ax);
                     float v[16];
                     if (ti.nk > 0) {
                         umma::tmem_ld16(tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * C::ACC + c0), v);
