@@ -501,6 +501,39 @@ void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, 
     MB_LAUNCH();
 }
 
+// every per-cluster segment sum of one net's minibatch step in one launch:
+// block z < G sums job j's tiles of cluster z (fixed order), block G sums
+// the per-tile loss partials (fp64, fixed tree) into *loss_out
+__global__ void k_segsum_multi(SegJobs jb, const int* goff, int G) {
+    const int z = blockIdx.x;
+    if (z == G) {
+        __shared__ double red[256];
+        double s = 0.0;
+        for (long i = threadIdx.x; i < jb.n_loss; i += blockDim.x) s += jb.loss_tiles[i];
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+            if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) *jb.loss_out = red[0];
+        return;
+    }
+    const int t0 = goff[z] >> 7, t1 = goff[z + 1] >> 7;
+    for (int q = 0; q < jb.n; ++q) {
+        const SegJob& j = jb.job[q];
+        for (int c = threadIdx.x; c < j.width; c += blockDim.x) {
+            float acc = 0.f;
+            for (int t = t0; t < t1; ++t) acc += j.psum[(long)t * j.ld + c];
+            j.out[(long)z * j.out_gs + c] = acc;
+        }
+    }
+}
+void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s) {
+    k_segsum_multi<<<G + (jb.loss_out ? 1 : 0), 256, 0, s>>>(jb, goff, G);
+    MB_LAUNCH();
+}
+
 // ---- image packing / unpacking helpers ------------------------------------
 // dst image (row r, col c) <- src[r * ld + c] (fp32), r < R, c < C
 __global__ void k_to_img(const float* __restrict__ src, long ld, long src_gs, int R, int C, Img dst) {

@@ -67,6 +67,22 @@ struct IGemm {
 void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, float* out, long out_gs,
                  cudaStream_t s);
 void img_gemm(const IGemm& d, cudaStream_t s);
+// several tile_segsum jobs (+ the per-tile loss partials) in one launch
+struct SegJob {
+    const float* psum = nullptr;
+    long ld = 0;
+    int width = 0;
+    float* out = nullptr;
+    long out_gs = 0;
+};
+struct SegJobs {
+    int n = 0;
+    SegJob job[10];
+    const double* loss_tiles = nullptr;  // [n_loss] -> *loss_out
+    long n_loss = 0;
+    double* loss_out = nullptr;
+};
+void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s);
 // dst(r, c) <- src[z*src_gs + r*ld + c] for z < G (dst.gs per z)
 void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
 void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,

@@ -487,8 +487,7 @@ Trainer::~Trainer() {
         if (p) cudaFree(p);
     for (auto* p : img_allocs_) cudaFree(p);
     for (auto& u : ub_) {
-        cudaFree(u.psum);
-        cudaFree(u.psum2);
+        for (float* q : u.pbias) cudaFree(q);
         cudaFree(u.psls);
         cudaFree(u.lossrows);
     }
@@ -572,8 +571,8 @@ void Trainer::alloc() {
         for (int l = 1; l <= actor_.tgt.L; ++l) wmax = std::max(wmax, actor_.tgt.sz[l]);
         for (int l = 1; l <= critic_.tgt.L; ++l) wmax = std::max(wmax, critic_.tgt.sz[l]);
         for (auto& u : ub_) {
-            u.psum = dalloc<float>((size_t)(Bpmax_ / 128) * wmax);
-            u.psum2 = dalloc<float>((size_t)(Bpmax_ / 128) * wmax);
+            const int L = (&u == &ub_[0] ? actor_ : critic_).tgt.L;
+            for (int l = 0; l < L; ++l) u.pbias.push_back(dalloc<float>((size_t)(Bpmax_ / 128) * wmax));
             u.psls = dalloc<float>((size_t)(Bpmax_ / 128) * 16);
             u.lossrows = dalloc<double>(Bpmax_);
         }
@@ -797,7 +796,7 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
     const int L = nd.L;
     UpdBufs& u = ub_[is_actor ? 0 : 1];
     float* gth = h.gtheta + (long)g_lo_ * h.ld;
-    float *d_psum = u.psum, *d_psls = u.psls;
+    float* d_psls = u.psls;
     double* d_lossrows = u.lossrows;
     if (Bp == 0) {
         MB_CUDA(cudaMemsetAsync(gth, 0, sizeof(float) * Kl_ * h.ld, s_));
@@ -841,25 +840,20 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         ha.z = d_Z; ha.lp_old = d_lpo; ha.sadv = d_sa; ha.clip = (float)cfg_.clip_eps;
         ha.ent = (float)cfg_.entropy_coef; ha.err = d_err;
         ha.tgt = d_tg; ha.inv_B = inv_B;
-        ha.psum = d_psum; ha.psls = d_psls; ha.psum_prev = u.psum2; ha.psum_prev_ld = nd.sz[L - 1];
+        ha.psum = u.pbias[L - 1]; ha.psls = d_psls; ha.psum_prev = u.pbias[L - 2]; ha.psum_prev_ld = nd.sz[L - 1];
         ha.loss_rows = d_lossrows;
         {
             const double fl = 4.0 * Bp * nd.sz[L - 1] * nd.sz[L];  // forward + backward of the output layer
             ProfScope ps("mlp_head", fl, 0, s_);
             head(ha, is_actor, s_);
         }
-        if (is_actor) tile_segsum(d_psls, 16, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.ld, s_);  // log-std grads
-        tile_segsum(u.psum2, nd.sz[L - 1], nd.sz[L - 1], goff, Kl_, gth + nd.boff[L - 2], h.ld, s_);
     } else if (is_actor) {  // losses.cpp:87-129
         actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, th, h.ld, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
-                       (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], d_psum, d_psls, d_lossrows,
-                       d_err, s_);
-        tile_segsum(d_psls, 16, es_.act_dim, goff, Kl_, gth + nd.mlp_n, h.ld, s_);  // log-std grads
+                       (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], u.pbias[L - 1], d_psls,
+                       d_lossrows, d_err, s_);
     } else {  // losses.cpp:170-185
-        critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], d_psum, d_lossrows, s_);
+        critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], u.pbias[L - 1], d_lossrows, s_);
     }
-    tile_segsum(d_psum, 16, nd.sz[L], goff, Kl_, gth + nd.boff[L - 1], h.ld, s_);  // output-layer bias grads
-    sum_f64(d_lossrows, Bp / 128, d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, s_);  // tile partials
     for (int l = L - 1; l >= 0; --l) {  // backward (nn.cpp:111-160)
         const Img& ain = l == 0 ? Xi_ : u.A[l - 1];
         IGemm d;  // dW_l[z][j][i] = sum_{q in z} G_l[q][j] A_{l-1}[q][i]
@@ -877,11 +871,20 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
             e.gmode = 1; e.goff = goff; e.max_group = maxg;
             e.act = 2; e.aux = u.A[l - 1];
             e.O = u.G[l - 1]; e.o_mode = 1;
-            e.psum = d_psum; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
+            e.psum = u.pbias[l - 1]; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
             igemm("mlp_dX", e, s_);
-            tile_segsum(d_psum, nd.sz[l], nd.sz[l], goff, Kl_, gth + nd.boff[l - 1], h.ld, s_);
         }
     }
+    // every bias gradient (per-tile column sums of G_l -> per cluster), the
+    // log-std gradients and the minibatch loss: one launch
+    SegJobs jb;
+    for (int l = 0; l < L; ++l)  // output layer partials are written with a row stride of 16
+        jb.job[jb.n++] = SegJob{u.pbias[l], l == L - 1 ? 16 : nd.sz[l + 1], nd.sz[l + 1], gth + nd.boff[l], h.ld};
+    if (is_actor) jb.job[jb.n++] = SegJob{d_psls, 16, es_.act_dim, gth + nd.mlp_n, h.ld};
+    jb.loss_tiles = d_lossrows;
+    jb.n_loss = Bp / 128;
+    jb.loss_out = d_mbloss + slot * 2 + (is_actor ? 0 : 1);
+    segsum_multi(jb, goff, Kl_, s_);
 }
 
 void Trainer::allreduce_grad(HyperNet& h, cudaStream_t s) {

@@ -196,8 +196,8 @@ private:
         std::vector<Img> A;     // [Bp][h_l] hidden activations (post-tanh)
         std::vector<Img> G;     // [Bp][out_l] gradient at the pre-activation of layer l
         float* Zf = nullptr;    // [Bp][16] output layer (policy mean / values), fp32
-        float *psum = nullptr, *psls = nullptr;  // per-128-row-tile column sums (bias / log-std grads)
-        float* psum2 = nullptr;                  // same for the last hidden layer (k_head)
+        float* psls = nullptr;      // per-128-row-tile column sums of the log-std gradient terms
+        std::vector<float*> pbias;  // per layer l: per-tile column sums of G_l (bias grads of layer l)
         double* lossrows = nullptr;
     } ub_[2];
     cudaStream_t s2_ = nullptr;  // critic chain of the update
