@@ -38,11 +38,9 @@ struct Dense16 {
     int img_r0, img_rn; // rows [img_r0, img_r0 + img_rn) go to the image
 };
 
-__global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
-    __shared__ float As[16][KC + 1];
-    __shared__ float Bs[16][KC + 1];
+__device__ void dense16_tile(const Dense16& d, int bx, int by, float (*As)[KC + 1], float (*Bs)[KC + 1]) {
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int r0 = blockIdx.y * 16, c0 = blockIdx.x * 16;
+    const int r0 = by * 16, c0 = bx * 16;
     const int ncols = d.N + (d.ones_col ? 1 : 0);
     float acc0 = 0.f, acc1 = 0.f;
     for (int k0 = 0; k0 < d.K; k0 += KC) {
@@ -86,6 +84,27 @@ __global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
     d.C[r * d.cr + c * d.cc] = v;
     if (d.img.p && r >= d.img_r0 && r < d.img_r0 + d.img_rn)
         *reinterpret_cast<__nv_bfloat16*>(d.img.p + img_off(r - d.img_r0, c, img_ct(d.img.C))) = __float2bfloat16_rn(v);
+}
+
+__global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
+    __shared__ float As[16][KC + 1];
+    __shared__ float Bs[16][KC + 1];
+    dense16_tile(d, blockIdx.x, blockIdx.y, As, Bs);
+}
+
+// two independent contractions in one launch (the tiles of d0, then d1)
+__global__ void __launch_bounds__(256) k_dense16_pair(Dense16 d0, Dense16 d1, int t0, int nx0, int nx1) {
+    __shared__ float As[16][KC + 1];
+    __shared__ float Bs[16][KC + 1];
+    const int t = blockIdx.x;
+    if (t < t0) dense16_tile(d0, t % nx0, t / nx0, As, Bs);
+    else dense16_tile(d1, (t - t0) % nx1, (t - t0) / nx1, As, Bs);
+}
+void dense16_pair(const Dense16& d0, const Dense16& d1, cudaStream_t s) {
+    const int nx0 = (d0.N + (d0.ones_col ? 1 : 0) + 15) / 16, ny0 = (d0.R + 15) / 16;
+    const int nx1 = (d1.N + (d1.ones_col ? 1 : 0) + 15) / 16, ny1 = (d1.R + 15) / 16;
+    k_dense16_pair<<<nx0 * ny0 + nx1 * ny1, 256, 0, s>>>(d0, d1, nx0 * ny0, nx0, nx1);
+    MB_LAUNCH();
 }
 
 void dense16(const Dense16& d, cudaStream_t s) {
@@ -158,15 +177,16 @@ void feature_backward(const FeatDims& fd, const float* p, const float* w, const 
         d.R = out; d.N = in; d.K = G;
         d.C = gout + fd.woff[l]; d.cr = in; d.cc = 1;
         d.ones_col = 1; d.Cb = gout + fd.boff[l];
-        dense16(d, s);
-        if (l > 0) {
+        if (l > 0) {  // independent of dW_l: one launch for both
             Dense16 e{};  // gz_{l-1}[g][i] = (sum_j gz_l[g][j] W[j][i]) (1 - a_l[g][i]^2)
             e.A = fd.gz[l]; e.ar = out; e.ak = 1;
             e.B = p + fd.woff[l]; e.bc = 1; e.bk = in;
             e.R = G; e.N = in; e.K = out;
             e.act = 2; e.aux = fd.act[l]; e.xr = in;
             e.C = fd.gz[l - 1]; e.cr = in; e.cc = 1;
-            dense16(e, s);
+            dense16_pair(d, e, s);
+        } else {
+            dense16(d, s);
         }
     }
 }

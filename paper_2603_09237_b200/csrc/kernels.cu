@@ -780,10 +780,22 @@ void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, floa
 // the next theta-generation and df GEMMs. 4 parameters per thread; m_lo and
 // F are multiples of 4 so a quad never straddles an 8-column image group.
 __global__ void k_adam_img(long n4, float4* p, const float4* g, float4* m1, float4* m2, float lr, float ibc1,
-                           float ibc2, const int* err, long m_lo, long m_hi, int F, Img mimg) {
+                           float ibc2, const int* err, long m_lo, long m_hi, int F, Img mimg, long n) {
     if (*err) return;
     const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (i >= n4) return;
+    if (i >= n4) {  // the n % 4 scalar tail (never inside the M block: it ends at b, after M)
+        const long e = 4 * n4 + (i - n4);
+        if (i - n4 < 4 && e < n) {
+            float* ps = reinterpret_cast<float*>(p);
+            const float* gs = reinterpret_cast<const float*>(g);
+            float* as = reinterpret_cast<float*>(m1);
+            float* bs = reinterpret_cast<float*>(m2);
+            as[e] = 0.9f * as[e] + 0.1f * gs[e];
+            bs[e] = 0.999f * bs[e] + 0.001f * gs[e] * gs[e];
+            ps[e] -= lr * (as[e] * ibc1) / (sqrtf(bs[e] * ibc2) + 1e-8f);
+        }
+        return;
+    }
     float4 pp = p[i], gg = g[i], a = m1[i], b = m2[i];
     float* P = &pp.x;
     const float* G = &gg.x;
@@ -811,16 +823,11 @@ void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, 
               long m_lo, int F, const Img& mimg, cudaStream_t s) {
     const long m_hi = m_lo + (long)mimg.R * F;
     if (m_lo % 4 || F % 8) throw ShapeError("adam_img: M block must be 4-aligned with F % 8 == 0");
-    const long n4 = n / 4;
-    if (n4)
-        k_adam_img<<<(unsigned)((n4 + 255) / 256), 256, 0, s>>>(n4, (float4*)p, (const float4*)g, (float4*)m1,
-                                                               (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi,
-                                                               F, mimg);
+    const long n4 = n / 4, threads = n4 + (n - 4 * n4);
+    k_adam_img<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(n4, (float4*)p, (const float4*)g, (float4*)m1,
+                                                                (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi,
+                                                                F, mimg, n);
     MB_LAUNCH();
-    if (n4 * 4 < n) {  // tail (never inside the M block: it ends at b, after M)
-        k_adam_tail<<<1, 32, 0, s>>>(n4 * 4, n, p, g, m1, m2, lr, 1.f / bc1, 1.f / bc2, err);
-        MB_LAUNCH();
-    }
 }
 
 // =========================================================================
