@@ -599,10 +599,12 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
 
 // gtheta [G][ld] (fp32) -> bf16 image (row g, col p) for the dM / df GEMMs and
 // db[p] = sum_g gtheta[g][p] (hypernet.cpp:92-122) in one read. A block covers
-// 64 8-column units x 4 row slices; the slices' sums combine in a fixed order.
-__global__ void __launch_bounds__(256) k_gtheta_prep(const float* __restrict__ gt, long ld, int G, int P, Img gimg,
-                                                     float* db) {
-    __shared__ float part[4][64][9];
+// 64 8-column units x 16 row slices (1024 threads: enough loads in flight to
+// stream at HBM rate); the slices' sums combine in a fixed order.
+constexpr int kGtSlices = 16;
+__global__ void __launch_bounds__(64 * kGtSlices) k_gtheta_prep(const float* __restrict__ gt, long ld, int G, int P,
+                                                               Img gimg, float* db) {
+    __shared__ float part[kGtSlices][64][9];
     const int ul = threadIdx.x & 63, sl = threadIdx.x >> 6;
     const long u = blockIdx.x * 64L + ul;
     const int p0 = (int)(u * 8);
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(256) k_gtheta_prep(const float* __restrict__ g
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (p0 < P) {
         const bool full = p0 + 8 <= P;
-        const int rs = (G + 3) / 4, r0 = sl * rs, r1 = min(G, r0 + rs);
+        const int rs = (G + kGtSlices - 1) / kGtSlices, r0 = sl * rs, r1 = min(G, r0 + rs);
 #pragma unroll 4
         for (int g = r0; g < r1; ++g) {
             const float* src = gt + (long)g * ld + p0;
@@ -638,13 +640,16 @@ __global__ void __launch_bounds__(256) k_gtheta_prep(const float* __restrict__ g
     for (int e = 0; e < 8; ++e) part[sl][ul][e] = acc[e];
     __syncthreads();
     if (sl == 0 && p0 < P)
-        for (int e = 0; e < 8 && p0 + e < P; ++e)
-            db[p0 + e] = (part[0][ul][e] + part[1][ul][e]) + (part[2][ul][e] + part[3][ul][e]);
+        for (int e = 0; e < 8 && p0 + e < P; ++e) {
+            float t = 0.f;
+            for (int q = 0; q < kGtSlices; ++q) t += part[q][ul][e];
+            db[p0 + e] = t;
+        }
 }
 void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s) {
     if (ld % 4) throw ShapeError("gtheta_prep: row stride must be a multiple of 4");
     const long units = (P + 7) / 8;
-    k_gtheta_prep<<<(unsigned)((units + 63) / 64), 256, 0, s>>>(gt, ld, G, P, gimg, db);
+    k_gtheta_prep<<<(unsigned)((units + 63) / 64), 64 * kGtSlices, 0, s>>>(gt, ld, G, P, gimg, db);
     MB_LAUNCH();
 }
 
