@@ -564,7 +564,7 @@ void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst
 
 // generated weights theta[g0 + z][woff_l + j * in_l + i] -> layer images of
 // group z (row j, col i), every layer of every group in one launch; one thread
-// per 8-column unit (coalesced fp32 reads, one 16-byte image store)
+// per 8-column unit (32-byte fp32 reads, one 16-byte image store)
 __global__ void k_pack_weights(const float* __restrict__ theta, long ld, int g0, int ng, PackDims pd, uint8_t* wimg,
                                long gs) {
     const long per = pd.ustart[pd.L];
@@ -575,7 +575,12 @@ __global__ void k_pack_weights(const float* __restrict__ theta, long ld, int g0,
         while (r >= pd.ustart[l + 1]) ++l;
         const int in = pd.in[l], cpr = (in + 7) >> 3;
         const int e = (int)(r - pd.ustart[l]);
-        const int j = e / cpr, c = (e - j * cpr) * 8;
+        // 8 consecutive threads = 8 consecutive rows of one 8-column unit: the
+        // image stores (row % 8 innermost) are 128 contiguous bytes
+        const int jr = e & 7, rest = e >> 3;
+        const int jg = rest / cpr, c = (rest - jg * cpr) * 8;
+        const int j = jg * 8 + jr;
+        if (j >= pd.out[l]) continue;  // rows padded to a multiple of 8
         const float* src = theta + (long)(g0 + z) * ld + pd.woff[l] + (long)j * in + c;
         float v[8];
 #pragma unroll

@@ -39,7 +39,7 @@ struct PackDims {
     int L = 0;
     int in[8] = {}, out[8] = {};
     long woff[8] = {}, ioff[8] = {};
-    long ustart[9] = {};  // 8-column units per group before layer l
+    long ustart[9] = {};  // (8-row-padded) 8-column units per group before layer l
 };
 
 // ---------------------------------------------------------------- tcgen05 GEMM v2

@@ -328,7 +328,7 @@ void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
         pd.out[l] = tgt.sz[l + 1];
         pd.woff[l] = tgt.woff[l];
         pd.ioff[l] = wimg_off[l];
-        pd.ustart[l + 1] = pd.ustart[l] + (long)tgt.sz[l + 1] * ((tgt.sz[l] + 7) / 8);
+        pd.ustart[l + 1] = pd.ustart[l] + (long)((tgt.sz[l + 1] + 7) / 8 * 8) * ((tgt.sz[l] + 7) / 8);
     }
     ProfScope ps("pack_weights", 0, 6.0 * ng * tgt.mlp_n, s);
     pack_weights(theta, ld, g0, ng, pd, wimg.p, wimg.gs, s);
