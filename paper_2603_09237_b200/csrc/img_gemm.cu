@@ -15,6 +15,9 @@
 // Grouped modes: gmode 1 = rows grouped (A/output rows start at goff[z],
 // 128-aligned; B / bias per group), gmode 2 = K grouped (K range
 // [goff[z], goff[z+1]), 128-aligned; output per group).
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "img.cuh"
 #include "kernels.h"
@@ -74,10 +77,21 @@ __device__ __forceinline__ TileInfo tile_info(const IGemm& d, int t, int ntn, in
     return ti;
 }
 
+// up to 3 independent GEMMs of the same epilogue kind in one persistent
+// launch: tile t belongs to g[k] with base[k] <= t < base[k+1]
+struct GemmBatch {
+    IGemm g[3];
+    int n = 1;
+    int base[4] = {0, 0, 0, 0};
+    int ntn[3] = {1, 1, 1}, ntm[3] = {1, 1, 1};
+};
+__device__ __forceinline__ int batch_of(const GemmBatch& bt, int t) { return t < bt.base[1] ? 0 : t < bt.base[2] ? 1 : 2; }
+
 // EPI: 0 = fp32 out (bias optional), 1 = tanh -> image (+ optional fp32 pre-act),
 //      2 = tanh' (aux image) -> image
 template <int BN, int EPI>
-__global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int ntiles, int ntn, int ntm) {
+__global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_constant__ GemmBatch bt) {
+    const int ntiles = bt.base[bt.n];
     using C = Cfg<BN, EPI>;
     constexpr int NEPI = C::NEPI, ET = 32 * NEPI;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -107,44 +121,54 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tbase = *tslot;
-    const int CTa = img_ct(d.A.C), CTb = img_ct(d.B.C);
+    // the descriptor and tile coordinates of batch tile t
+#define MB_TILE(t)                                  \
+    const int bk_ = batch_of(bt, t);                \
+    const IGemm& d = bt.g[bk_];                     \
+    const TileInfo ti = tile_info(d, t - bt.base[bk_], bt.ntn[bk_], bt.ntm[bk_])
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- producer
-            const uint32_t bbytes = (d.b_view == 0 && BN < 128) ? (uint32_t)BN * 256 : (uint32_t)CHUNK;
             long g = 0;  // global chunk counter
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const TileInfo ti = tile_info(d, t, ntn, ntm);
+                MB_TILE(t);
                 if (!ti.valid) continue;
+                const int CTa = img_ct(d.A.C), CTb = img_ct(d.B.C);
+                const uint32_t bbytes = (d.b_view == 0 && BN < 128) ? (uint32_t)BN * 256 : (uint32_t)CHUNK;
                 const uint8_t* Ab = d.A.p + (d.gmode == 0 ? ti.z * d.A.gs : 0);
                 const uint8_t* Bb = d.B.p + (d.gmode != 2 ? ti.z * d.B.gs : 0);
                 const int mt = ti.m0 >> 7, nt0 = ti.n0 >> 7, kc0 = ti.k_lo >> 7;
+                // B chunks that exist for this N tile (a narrow GEMM batched with BN > N)
+                const int nbv = min(C::NB, (d.b_view ? CTb : img_rt(d.B.R)) - nt0);
                 for (int kc = 0; kc < ti.nk; ++kc, ++g) {
                     const int s = (int)(g % C::STAGES);
                     umma::mbar_wait(&empty[s], (uint32_t)(((g / C::STAGES) & 1) ^ 1));
                     uint8_t* st = smem + s * C::STAGE;
-                    umma::mbar_arrive_expect_tx(&full[s], CHUNK + C::NB * bbytes);
+                    umma::mbar_arrive_expect_tx(&full[s], CHUNK + nbv * bbytes);
                     umma::bulk_g2s(st, Ab + chunk_index(d.a_view, mt, kc0 + kc, CTa) * CHUNK, CHUNK, &full[s]);
 #pragma unroll
                     for (int j = 0; j < C::NB; ++j)
-                        umma::bulk_g2s(st + CHUNK * (1 + j),
-                                       Bb + chunk_index(d.b_view, nt0 + j, kc0 + kc, CTb) * CHUNK, bbytes, &full[s]);
+                        if (j < nbv)
+                            umma::bulk_g2s(st + CHUNK * (1 + j),
+                                           Bb + chunk_index(d.b_view, nt0 + j, kc0 + kc, CTb) * CHUNK, bbytes,
+                                           &full[s]);
                 }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t idesc = umma::idesc_bf16(128, C::NMMA, d.a_view == 1, d.b_view == 1);
-            const uint32_t a_lbo = d.a_view ? 2048 : 128, a_sbo = d.a_view ? 128 : 2048;
-            const uint32_t a_step = d.a_view ? 4096 : 256;
-            const uint32_t b_lbo = d.b_view ? 2048 : 128, b_sbo = d.b_view ? 128 : 2048;
-            const uint32_t b_step = d.b_view ? 4096 : 256;
             long g = 0;
             int it = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const TileInfo ti = tile_info(d, t, ntn, ntm);
+                MB_TILE(t);
                 if (!ti.valid) continue;
+                const uint32_t idesc = umma::idesc_bf16(128, C::NMMA, d.a_view == 1, d.b_view == 1);
+                const uint32_t a_lbo = d.a_view ? 2048 : 128, a_sbo = d.a_view ? 128 : 2048;
+                const uint32_t a_step = d.a_view ? 4096 : 256;
+                const uint32_t b_lbo = d.b_view ? 2048 : 128, b_sbo = d.b_view ? 128 : 2048;
+                const uint32_t b_step = d.b_view ? 4096 : 256;
+                const int nbv = min(C::NB, (d.b_view ? img_ct(d.B.C) : img_rt(d.B.R)) - (ti.n0 >> 7));
                 const int acc = it & 1;
                 umma::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
                 umma::fence_after_sync();
@@ -156,6 +180,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
                     const uint32_t a0 = umma::smem_u32(smem + s * C::STAGE);
 #pragma unroll
                     for (int j = 0; j < C::NB; ++j) {
+                        if (j >= nbv) break;
                         const uint32_t b0 = a0 + CHUNK * (1 + j);
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk)
@@ -179,7 +204,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
         const bool active = BN >= 16 * NPART || half == 0;
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const TileInfo ti = tile_info(d, t, ntn, ntm);
+            MB_TILE(t);
             if (!ti.valid) continue;
             const int acc = it & 1;
             const float* bias = d.bias ? d.bias + (d.gmode != 2 ? ti.z * d.bias_gs : 0) : nullptr;
@@ -445,47 +470,70 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(IGemm d, int n
     }
     __syncthreads();
     if (warp == 0) umma::tmem_free(tbase, C::TCOLS);
+#undef MB_TILE
 }
 
 template <int BN, int EPI>
-void launch(IGemm d, cudaStream_t s) {
+void launch(const IGemm* ds, int n, cudaStream_t s) {
+    using C = Cfg<BN, EPI>;
     static bool configured = false;
     if (!configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_img_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Cfg<BN, EPI>::SMEM));
+        MB_CUDA(cudaFuncSetAttribute(k_img_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         configured = true;
     }
-    d.N_tile = BN;
-    const int mext = d.gmode == 1 ? d.max_group : d.M;
-    const int ntn = (d.N + BN - 1) / BN, ntm = (mext + 127) / 128;
-    const int ntiles = ntn * ntm * d.Z;
+    GemmBatch bt;
+    bt.n = n;
+    for (int k = 0; k < n; ++k) {
+        IGemm d = ds[k];
+        d.N_tile = BN;
+        const int mext = d.gmode == 1 ? d.max_group : d.M;
+        bt.ntn[k] = (d.N + BN - 1) / BN;
+        bt.ntm[k] = (mext + 127) / 128;
+        bt.base[k + 1] = bt.base[k] + bt.ntn[k] * bt.ntm[k] * d.Z;
+        bt.g[k] = d;
+    }
+    const int ntiles = bt.base[n];
+    if (ntiles == 0) return;
     const int grid = ntiles < 148 ? ntiles : 148;
-    k_img_gemm<BN, EPI><<<grid, Cfg<BN, EPI>::NT, Cfg<BN, EPI>::SMEM, s>>>(d, ntiles, ntn, ntm);
+    k_img_gemm<BN, EPI><<<grid, C::NT, C::SMEM, s>>>(bt);
     MB_LAUNCH();
 }
 
 template <int EPI>
-void dispatch_bn(const IGemm& d, cudaStream_t s) {
-    if (d.N <= 16) launch<16, EPI>(d, s);
-    else if (d.N <= 32) launch<32, EPI>(d, s);
-    else if (d.N <= 64) launch<64, EPI>(d, s);
-    else if (d.N <= 128) launch<128, EPI>(d, s);
-    else launch<256, EPI>(d, s);
+void dispatch_bn(const IGemm* ds, int n, cudaStream_t s) {
+    int N = 0;
+    for (int k = 0; k < n; ++k) N = std::max(N, ds[k].N);
+    if (N <= 16) launch<16, EPI>(ds, n, s);
+    else if (N <= 32) launch<32, EPI>(ds, n, s);
+    else if (N <= 64) launch<64, EPI>(ds, n, s);
+    else if (N <= 128) launch<128, EPI>(ds, n, s);
+    else launch<256, EPI>(ds, n, s);
 }
 }  // namespace
 
-void img_gemm(const IGemm& d, cudaStream_t s) {
-    if (d.M <= 0 || d.N <= 0 || d.Z <= 0) return;
-    if (d.gmode == 1 && d.max_group <= 0) return;
-    if (d.act == 0) {
-        if (d.o_mode != 0) throw ShapeError("img_gemm: image output needs an activation epilogue");
-        dispatch_bn<0>(d, s);
-    } else if (d.act == 1) {
-        dispatch_bn<1>(d, s);
+void img_gemm_batch(const IGemm* ds, int n, cudaStream_t s) {
+    if (n < 1 || n > 3) throw ShapeError("img_gemm_batch: 1 to 3 GEMMs per launch");
+    std::vector<IGemm> live;
+    for (int k = 0; k < n; ++k) {
+        const IGemm& d = ds[k];
+        if (d.M <= 0 || d.N <= 0 || d.Z <= 0 || (d.gmode == 1 && d.max_group <= 0)) continue;
+        if (d.act != ds[0].act || d.o_mode != ds[0].o_mode)
+            throw ShapeError("img_gemm_batch: the batched GEMMs must share the epilogue kind");
+        live.push_back(d);
+    }
+    if (live.empty()) return;
+    const IGemm& d0 = live[0];
+    if (d0.act == 0) {
+        if (d0.o_mode != 0) throw ShapeError("img_gemm: image output needs an activation epilogue");
+        dispatch_bn<0>(live.data(), (int)live.size(), s);
+    } else if (d0.act == 1) {
+        dispatch_bn<1>(live.data(), (int)live.size(), s);
     } else {
-        dispatch_bn<2>(d, s);
+        dispatch_bn<2>(live.data(), (int)live.size(), s);
     }
 }
+
+void img_gemm(const IGemm& d, cudaStream_t s) { img_gemm_batch(&d, 1, s); }
 
 __global__ void k_tile_segsum(const float* psum, long ld, int width, const int* goff, float* out, long out_gs) {
     const int z = blockIdx.x;

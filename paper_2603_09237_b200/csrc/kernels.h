@@ -67,6 +67,8 @@ struct IGemm {
 void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, float* out, long out_gs,
                  cudaStream_t s);
 void img_gemm(const IGemm& d, cudaStream_t s);
+// 1-3 independent GEMMs with the same epilogue kind in one persistent launch
+void img_gemm_batch(const IGemm* ds, int n, cudaStream_t s);
 // several tile_segsum jobs (+ the per-tile loss partials) in one launch
 struct SegJob {
     const float* psum = nullptr;

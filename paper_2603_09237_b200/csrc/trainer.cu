@@ -854,7 +854,23 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
     } else {  // losses.cpp:170-185
         critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], u.pbias[L - 1], d_lossrows, s_);
     }
-    for (int l = L - 1; l >= 0; --l) {  // backward (nn.cpp:111-160)
+    // backward (nn.cpp:111-160): the data-gradient chain first (each dX needs
+    // the previous one), then every layer's weight gradient -- independent
+    // of each other -- batched three per launch
+    for (int l = L - 1; l > 0; --l) {
+        if (fused_head && l == L - 1) continue;  // k_head produced G_{L-2}
+        IGemm e;  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
+        e.A = u.G[l]; e.a_view = 0;  // (m = q, k = j)
+        e.B = wl(l); e.b_view = 1;   // (n = i, k = j)
+        e.M = Bp; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
+        e.gmode = 1; e.goff = goff; e.max_group = maxg;
+        e.act = 2; e.aux = u.A[l - 1];
+        e.O = u.G[l - 1]; e.o_mode = 1;
+        e.psum = u.pbias[l - 1]; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
+        igemm("mlp_dX", e, s_);
+    }
+    std::vector<IGemm> dws;
+    for (int l = L - 1; l >= 0; --l) {
         const Img& ain = l == 0 ? Xi_ : u.A[l - 1];
         IGemm d;  // dW_l[z][j][i] = sum_{q in z} G_l[q][j] A_{l-1}[q][i]
         d.A = u.G[l]; d.a_view = 1;  // (m = j, k = q)
@@ -862,18 +878,14 @@ void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg
         d.M = nd.sz[l + 1]; d.N = nd.sz[l]; d.K = Bp; d.Z = Kl_;
         d.gmode = 2; d.goff = goff;
         d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = h.ld;
-        igemm("mlp_dW", d, s_);
-        if (l > 0 && !(fused_head && l == L - 1)) {
-            IGemm e;  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
-            e.A = u.G[l]; e.a_view = 0;  // (m = q, k = j)
-            e.B = wl(l); e.b_view = 1;   // (n = i, k = j)
-            e.M = Bp; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
-            e.gmode = 1; e.goff = goff; e.max_group = maxg;
-            e.act = 2; e.aux = u.A[l - 1];
-            e.O = u.G[l - 1]; e.o_mode = 1;
-            e.psum = u.pbias[l - 1]; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
-            igemm("mlp_dX", e, s_);
-        }
+        dws.push_back(d);
+    }
+    for (size_t k0 = 0; k0 < dws.size(); k0 += 3) {
+        const int nb = (int)std::min<size_t>(3, dws.size() - k0);
+        double fl = 0;
+        for (int k = 0; k < nb; ++k) fl += 2.0 * dws[k0 + k].M * dws[k0 + k].N * dws[k0 + k].K;
+        ProfScope ps("mlp_dW", fl, 0, s_);
+        img_gemm_batch(&dws[k0], nb, s_);
     }
     // every bias gradient (per-tile column sums of G_l -> per cluster), the
     // log-std gradients and the minibatch loss: one launch
