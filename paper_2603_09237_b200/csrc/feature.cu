@@ -92,18 +92,32 @@ __global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
     dense16_tile(d, blockIdx.x, blockIdx.y, As, Bs);
 }
 
-// two independent contractions in one launch (the tiles of d0, then d1)
-__global__ void __launch_bounds__(256) k_dense16_pair(Dense16 d0, Dense16 d1, int t0, int nx0, int nx1) {
+// up to 4 independent contractions in one launch (tile ranges per descriptor)
+struct DenseBatch {
+    Dense16 d[4];
+    int n = 0;
+    int base[5] = {0, 0, 0, 0, 0};
+    int nx[4] = {1, 1, 1, 1};
+};
+__global__ void __launch_bounds__(256) k_dense16_multi(const __grid_constant__ DenseBatch b) {
     __shared__ float As[16][KC + 1];
     __shared__ float Bs[16][KC + 1];
     const int t = blockIdx.x;
-    if (t < t0) dense16_tile(d0, t % nx0, t / nx0, As, Bs);
-    else dense16_tile(d1, (t - t0) % nx1, (t - t0) / nx1, As, Bs);
+    int k = 0;
+    while (k + 1 < b.n && t >= b.base[k + 1]) ++k;
+    const int u = t - b.base[k];
+    dense16_tile(b.d[k], u % b.nx[k], u / b.nx[k], As, Bs);
 }
-void dense16_pair(const Dense16& d0, const Dense16& d1, cudaStream_t s) {
-    const int nx0 = (d0.N + (d0.ones_col ? 1 : 0) + 15) / 16, ny0 = (d0.R + 15) / 16;
-    const int nx1 = (d1.N + (d1.ones_col ? 1 : 0) + 15) / 16, ny1 = (d1.R + 15) / 16;
-    k_dense16_pair<<<nx0 * ny0 + nx1 * ny1, 256, 0, s>>>(d0, d1, nx0 * ny0, nx0, nx1);
+void dense16_multi(const Dense16* ds, int n, cudaStream_t s) {
+    DenseBatch b;
+    b.n = n;
+    for (int k = 0; k < n; ++k) {
+        b.d[k] = ds[k];
+        b.nx[k] = (ds[k].N + (ds[k].ones_col ? 1 : 0) + 15) / 16;
+        b.base[k + 1] = b.base[k] + b.nx[k] * ((ds[k].R + 15) / 16);
+    }
+    if (b.base[n] == 0) return;
+    k_dense16_multi<<<b.base[n], 256, 0, s>>>(b);
     MB_LAUNCH();
 }
 
@@ -142,53 +156,82 @@ __global__ void __launch_bounds__(256) k_split_dtanh(const float* __restrict__ p
 }
 }  // namespace
 
+void feature_forward_multi(const FeatJob* jobs, int nj, cudaStream_t s) {
+    const int L = jobs[0].fd->L;
+    for (int k = 1; k < nj; ++k)
+        if (jobs[k].fd->L != L) throw ShapeError("feature_forward_multi: the feature maps must have equal depth");
+    for (int l = 0; l < L; ++l) {
+        Dense16 ds[4];
+        for (int k = 0; k < nj; ++k) {
+            const FeatJob& j = jobs[k];
+            const FeatDims& fd = *j.fd;
+            Dense16 d{};
+            d.A = l == 0 ? j.w : fd.act[l];  // act[0] is not materialised: w is the input
+            d.ar = fd.sz[l]; d.ak = 1;
+            d.B = j.p + fd.woff[l]; d.bc = fd.sz[l]; d.bk = 1;  // W [out][in]
+            d.R = j.G; d.N = fd.sz[l + 1]; d.K = fd.sz[l];
+            d.bias = j.p + fd.boff[l];
+            d.act = 1;
+            d.C = fd.act[l + 1]; d.cr = fd.sz[l + 1]; d.cc = 1;
+            if (l == L - 1) {
+                d.img = j.fimg;
+                d.img_r0 = j.r0;
+                d.img_rn = j.rn;
+            }
+            ds[k] = d;
+        }
+        dense16_multi(ds, nj, s);
+    }
+}
+
 void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, int r0, int rn,
                      cudaStream_t s) {
-    for (int l = 0; l < fd.L; ++l) {
-        Dense16 d{};
-        d.A = l == 0 ? w : fd.act[l];  // act[0] is not materialised: w is the input
-        d.ar = fd.sz[l]; d.ak = 1;
-        d.B = p + fd.woff[l]; d.bc = fd.sz[l]; d.bk = 1;  // W [out][in]
-        d.R = G; d.N = fd.sz[l + 1]; d.K = fd.sz[l];
-        d.bias = p + fd.boff[l];
-        d.act = 1;
-        d.C = fd.act[l + 1]; d.cr = fd.sz[l + 1]; d.cc = 1;
-        if (l == fd.L - 1) {
-            d.img = fimg;
-            d.img_r0 = r0;
-            d.img_rn = rn;
+    FeatJob j{&fd, p, w, G, fimg, r0, rn, nullptr, 0, nullptr};
+    feature_forward_multi(&j, 1, s);
+}
+
+void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s) {
+    const int L = jobs[0].fd->L;
+    for (int k = 0; k < nj; ++k) {
+        const FeatJob& j = jobs[k];
+        if (j.fd->L != L) throw ShapeError("feature_backward_multi: the feature maps must have equal depth");
+        const long n = (long)j.G * j.fd->sz[L];
+        k_split_dtanh<<<(unsigned)((n + 63) / 64), 256, 0, s>>>(j.parts, j.splits, n, j.fd->act[L], j.fd->gz[L - 1]);
+        MB_LAUNCH();
+    }
+    for (int l = L - 1; l >= 0; --l) {
+        Dense16 ds[4];
+        int nd = 0;
+        for (int k = 0; k < nj; ++k) {
+            const FeatJob& j = jobs[k];
+            const FeatDims& fd = *j.fd;
+            const int in = fd.sz[l], out = fd.sz[l + 1];
+            const float* a_in = l == 0 ? j.w : fd.act[l];
+            Dense16 d{};  // dW[j][i] = sum_g gz[g][j] a[g][i]; db[j] = sum_g gz[g][j]
+            d.A = fd.gz[l]; d.ar = 1; d.ak = out;
+            d.B = a_in; d.bc = 1; d.bk = in;
+            d.R = out; d.N = in; d.K = j.G;
+            d.C = j.gout + fd.woff[l]; d.cr = in; d.cc = 1;
+            d.ones_col = 1; d.Cb = j.gout + fd.boff[l];
+            ds[nd++] = d;
+            if (l > 0) {  // independent of dW_l: same launch
+                Dense16 e{};  // gz_{l-1}[g][i] = (sum_j gz_l[g][j] W[j][i]) (1 - a_l[g][i]^2)
+                e.A = fd.gz[l]; e.ar = out; e.ak = 1;
+                e.B = j.p + fd.woff[l]; e.bc = 1; e.bk = in;
+                e.R = j.G; e.N = in; e.K = out;
+                e.act = 2; e.aux = fd.act[l]; e.xr = in;
+                e.C = fd.gz[l - 1]; e.cr = in; e.cc = 1;
+                ds[nd++] = e;
+            }
         }
-        dense16(d, s);
+        dense16_multi(ds, nd, s);
     }
 }
 
 void feature_backward(const FeatDims& fd, const float* p, const float* w, const float* parts, int splits, int G,
                       float* gout, cudaStream_t s) {
-    const int L = fd.L;
-    const long n = (long)G * fd.sz[L];
-    k_split_dtanh<<<(unsigned)((n + 63) / 64), 256, 0, s>>>(parts, splits, n, fd.act[L], fd.gz[L - 1]);
-    MB_LAUNCH();
-    for (int l = L - 1; l >= 0; --l) {
-        const int in = fd.sz[l], out = fd.sz[l + 1];
-        const float* a_in = l == 0 ? w : fd.act[l];
-        Dense16 d{};  // dW[j][i] = sum_g gz[g][j] a[g][i]; db[j] = sum_g gz[g][j]
-        d.A = fd.gz[l]; d.ar = 1; d.ak = out;
-        d.B = a_in; d.bc = 1; d.bk = in;
-        d.R = out; d.N = in; d.K = G;
-        d.C = gout + fd.woff[l]; d.cr = in; d.cc = 1;
-        d.ones_col = 1; d.Cb = gout + fd.boff[l];
-        if (l > 0) {  // independent of dW_l: one launch for both
-            Dense16 e{};  // gz_{l-1}[g][i] = (sum_j gz_l[g][j] W[j][i]) (1 - a_l[g][i]^2)
-            e.A = fd.gz[l]; e.ar = out; e.ak = 1;
-            e.B = p + fd.woff[l]; e.bc = 1; e.bk = in;
-            e.R = G; e.N = in; e.K = out;
-            e.act = 2; e.aux = fd.act[l]; e.xr = in;
-            e.C = fd.gz[l - 1]; e.cr = in; e.cc = 1;
-            dense16_pair(d, e, s);
-        } else {
-            dense16(d, s);
-        }
-    }
+    FeatJob j{&fd, p, w, G, Img{}, 0, 0, parts, splits, gout};
+    feature_backward_multi(&j, 1, s);
 }
 
 }  // namespace mb200

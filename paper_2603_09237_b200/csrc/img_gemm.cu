@@ -552,19 +552,20 @@ void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, 
 // every per-cluster segment sum of one net's minibatch step in one launch:
 // block z < G sums job j's tiles of cluster z (fixed order), block G sums
 // the per-tile loss partials (fp64, fixed tree) into *loss_out
-__global__ void k_segsum_multi(SegJobs jb, const int* goff, int G) {
+__global__ void k_segsum_multi(const __grid_constant__ SegJobs jb, const int* goff, int G) {
     const int z = blockIdx.x;
-    if (z == G) {
+    if (z >= G) {  // one block per loss
+        const SegLoss& L = jb.loss[z - G];
         __shared__ double red[256];
         double s = 0.0;
-        for (long i = threadIdx.x; i < jb.n_loss; i += blockDim.x) s += jb.loss_tiles[i];
+        for (long i = threadIdx.x; i < L.n; i += blockDim.x) s += L.tiles[i];
         red[threadIdx.x] = s;
         __syncthreads();
         for (int k = blockDim.x / 2; k > 0; k >>= 1) {
             if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
             __syncthreads();
         }
-        if (threadIdx.x == 0) *jb.loss_out = red[0];
+        if (threadIdx.x == 0) *L.out = red[0];
         return;
     }
     const int t0 = goff[z] >> 7, t1 = goff[z + 1] >> 7;
@@ -578,7 +579,7 @@ __global__ void k_segsum_multi(SegJobs jb, const int* goff, int G) {
     }
 }
 void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s) {
-    k_segsum_multi<<<G + (jb.loss_out ? 1 : 0), 256, 0, s>>>(jb, goff, G);
+    k_segsum_multi<<<G + jb.nloss, 256, 0, s>>>(jb, goff, G);
     MB_LAUNCH();
 }
 

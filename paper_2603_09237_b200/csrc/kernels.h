@@ -77,12 +77,16 @@ struct SegJob {
     float* out = nullptr;
     long out_gs = 0;
 };
+struct SegLoss {
+    const double* tiles = nullptr;  // [n] per-tile loss partials -> *out
+    long n = 0;
+    double* out = nullptr;
+};
 struct SegJobs {
     int n = 0;
-    SegJob job[10];
-    const double* loss_tiles = nullptr;  // [n_loss] -> *loss_out
-    long n_loss = 0;
-    double* loss_out = nullptr;
+    SegJob job[16];
+    int nloss = 0;
+    SegLoss loss[2];
 };
 void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s);
 // dst(r, c) <- src[z*src_gs + r*ld + c] for z < G (dst.gs per z)
@@ -248,6 +252,20 @@ void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, 
 // df = sum of the split-K partials [splits][G][F]; writes dW/db of every layer into gout (flat layout)
 void feature_backward(const FeatDims& fd, const float* p, const float* w, const float* parts, int splits, int G,
                       float* gout, cudaStream_t s);
+// the same for up to two feature maps of equal depth in lockstep (one launch per layer)
+struct FeatJob {
+    const FeatDims* fd;
+    const float* p;
+    const float* w;
+    int G;
+    Img fimg;  // forward: image rows [r0, r0 + rn)
+    int r0, rn;
+    const float* parts;  // backward: split-K partials of M^T gtheta
+    int splits;
+    float* gout;
+};
+void feature_forward_multi(const FeatJob* jobs, int nj, cudaStream_t s);
+void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s);
 void mul_dtanh(float* g, const float* a, long n, cudaStream_t s);
 
 // ---------------------------------------------------------------- Adam (K7)

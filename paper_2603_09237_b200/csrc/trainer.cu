@@ -305,33 +305,57 @@ static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
 // cores theta[g][p] = b[p] + sum_k M[p][k] f[g][k] (hypernet.cpp:73-88) for
 // this rank's clusters [g0, g0+ng) only (theta rows keep global indices).
 void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
+    HyperNet* self = this;
+    forward_multi(&self, 1, w, g0, ng, s);
+}
+
+// the forward of one or two hypernetworks (actor and critic) in lockstep:
+// each stage is one launch covering both
+void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s) {
     {
         double fl = 0;
-        for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 2.0 * G * fsz[l] * fsz[l + 1];
+        FeatJob jobs[2];
+        for (int k = 0; k < nh; ++k) {
+            HyperNet& h = *hs[k];
+            for (size_t l = 0; l + 1 < h.fsz.size(); ++l) fl += 2.0 * h.G * h.fsz[l] * h.fsz[l + 1];
+            h.w_last = w;
+            h.fg0 = g0;
+            h.fng = ng;
+            jobs[k] = FeatJob{&h.fd, h.p, w, h.G, h.fimg, g0, ng, nullptr, 0, nullptr};
+        }
         ProfScope ps("feature_fwd", fl, 0, s);
-        w_last = w;
-        fg0 = g0;
-        fng = ng;
-        feature_forward(fd, p, w, G, fimg, g0, ng, s);  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
+        feature_forward_multi(jobs, nh, s);  // tanh MLP incl. tanh output (hypernet.cpp:10-17)
     }
-    IGemm d;  // theta[g][p] = b[p] + sum_k f[g][k] M[p][k]: rows = clusters, contiguous theta rows
-    d.A = fimg; d.a_view = 0;          // (m = g, k = f)
-    d.B = mimg; d.b_view = 0;          // (n = p, k = f)
-    d.M = ng; d.N = (int)P; d.K = F;
-    d.bias = p + nf + P * F; d.bias_mode = 1;
-    d.C = theta + (long)g0 * ld; d.cm = ld; d.cn = 1;
-    igemm("hyper_theta", d, s);
-    PackDims pd;  // generated weights of this rank's clusters -> per-layer bf16 images
-    pd.L = tgt.L;
-    for (int l = 0; l < tgt.L; ++l) {
-        pd.in[l] = tgt.sz[l];
-        pd.out[l] = tgt.sz[l + 1];
-        pd.woff[l] = tgt.woff[l];
-        pd.ioff[l] = wimg_off[l];
-        pd.ustart[l + 1] = pd.ustart[l] + (long)((tgt.sz[l + 1] + 7) / 8 * 8) * ((tgt.sz[l] + 7) / 8);
+    {
+        IGemm ds[2];
+        double fl = 0;
+        for (int k = 0; k < nh; ++k) {
+            HyperNet& h = *hs[k];
+            IGemm& d = ds[k];  // theta[g][p] = b[p] + sum_k f[g][k] M[p][k]: rows = clusters
+            d.A = h.fimg; d.a_view = 0;  // (m = g, k = f)
+            d.B = h.mimg; d.b_view = 0;  // (n = p, k = f)
+            d.M = ng; d.N = (int)h.P; d.K = h.F;
+            d.bias = h.p + h.nf + h.P * h.F; d.bias_mode = 1;
+            d.C = h.theta + (long)g0 * h.ld; d.cm = h.ld; d.cn = 1;
+            fl += 2.0 * d.M * d.N * d.K;
+        }
+        ProfScope ps("hyper_theta", fl, 0, s);
+        img_gemm_batch(ds, nh, s);
     }
-    ProfScope ps("pack_weights", 0, 6.0 * ng * tgt.mlp_n, s);
-    pack_weights(theta, ld, g0, ng, pd, wimg.p, wimg.gs, s);
+    for (int k = 0; k < nh; ++k) {
+        HyperNet& h = *hs[k];
+        PackDims pd;  // generated weights of this rank's clusters -> per-layer bf16 images
+        pd.L = h.tgt.L;
+        for (int l = 0; l < h.tgt.L; ++l) {
+            pd.in[l] = h.tgt.sz[l];
+            pd.out[l] = h.tgt.sz[l + 1];
+            pd.woff[l] = h.tgt.woff[l];
+            pd.ioff[l] = h.wimg_off[l];
+            pd.ustart[l + 1] = pd.ustart[l] + (long)((h.tgt.sz[l + 1] + 7) / 8 * 8) * ((h.tgt.sz[l] + 7) / 8);
+        }
+        ProfScope ps("pack_weights", 0, 6.0 * ng * h.tgt.mlp_n, s);
+        pack_weights(h.theta, h.ld, g0, ng, pd, h.wimg.p, h.wimg.gs, s);
+    }
 }
 
 void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, mimg, 1, s); }
@@ -342,33 +366,59 @@ void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, 
 // backward. Writes (not accumulates) the flat grad g; with several ranks it
 // is the rank's partial sum, all-reduced by the trainer before Adam.
 void HyperNet::backward(cudaStream_t s) {
-    const long nM = P * F;
-    const int ng = fng;
-    gtheta_prep(gtheta + (long)fg0 * ld, ld, ng, (int)P, gimg, g + nf + nM, s);  // gimg + db in one pass
-    {
-        IGemm d;  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
-        d.A = gimg; d.a_view = 1;  // (m = p, k = g)
-        d.B = fimg; d.b_view = 1;  // (n = f, k = g)
-        d.M = (int)P; d.N = F; d.K = ng;
-        d.C = g + nf; d.cm = F; d.cn = 1;
-        igemm("hyper_dM", d, s);
+    HyperNet* self = this;
+    backward_multi(&self, 1, s);
+}
+
+void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
+    for (int k = 0; k < nh; ++k) {  // gimg + db in one pass
+        HyperNet& h = *hs[k];
+        gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg, h.g + h.nf + h.P * h.F, s);
     }
     {
-        IGemm d;  // gf[g][k] = sum_p gtheta[g][p] M[p][k], split-K over 128-aligned P ranges
-        d.A = gimg; d.a_view = 0;  // (m = g, k = p)
-        d.B = mimg; d.b_view = 1;  // (n = f, k = p)
-        d.M = ng; d.N = F; d.K = (int)P; d.Z = splits;
-        d.gmode = 2; d.goff = d_split_bounds;
-        d.C = parts; d.cm = F; d.cn = 1; d.c_gs = (long)ng * F;
-        igemm("hyper_df", d, s);
+        IGemm ds[2];
+        double fl = 0;
+        for (int k = 0; k < nh; ++k) {
+            HyperNet& h = *hs[k];
+            IGemm& d = ds[k];  // gf[g][k] = sum_p gtheta[g][p] M[p][k], split-K over 128-aligned P ranges
+            d.A = h.gimg; d.a_view = 0;  // (m = g, k = p)
+            d.B = h.mimg; d.b_view = 1;  // (n = f, k = p)
+            d.M = h.fng; d.N = h.F; d.K = (int)h.P; d.Z = h.splits;
+            d.gmode = 2; d.goff = h.d_split_bounds;
+            d.C = h.parts; d.cm = h.F; d.cn = 1; d.c_gs = (long)h.fng * h.F;
+            fl += 2.0 * d.M * d.N * d.K;
+        }
+        ProfScope ps("hyper_df", fl, 0, s);
+        img_gemm_batch(ds, nh, s);
+    }
+    {
+        IGemm ds[2];
+        double fl = 0;
+        for (int k = 0; k < nh; ++k) {
+            HyperNet& h = *hs[k];
+            IGemm& d = ds[k];  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
+            d.A = h.gimg; d.a_view = 1;  // (m = p, k = g)
+            d.B = h.fimg; d.b_view = 1;  // (n = f, k = g)
+            d.M = (int)h.P; d.N = h.F; d.K = h.fng;
+            d.C = h.g + h.nf; d.cm = h.F; d.cn = 1;
+            fl += 2.0 * d.M * d.N * d.K;
+        }
+        ProfScope ps("hyper_dM", fl, 0, s);
+        img_gemm_batch(ds, nh, s);
     }
     {  // df reduction + feature-map backward (all layers' dW, db) over the local rows
         double fl = 0;
-        for (size_t l = 0; l + 1 < fsz.size(); ++l) fl += 4.0 * ng * fsz[l] * fsz[l + 1];
+        FeatDims fl_d[2];
+        FeatJob jobs[2];
+        for (int k = 0; k < nh; ++k) {
+            HyperNet& h = *hs[k];
+            for (size_t l = 0; l + 1 < h.fsz.size(); ++l) fl += 4.0 * h.fng * h.fsz[l] * h.fsz[l + 1];
+            fl_d[k] = h.fd;
+            for (int l = 0; l <= h.fd.L; ++l) fl_d[k].act[l] = h.fd.act[l] + (long)h.fg0 * h.fd.sz[l];
+            jobs[k] = FeatJob{&fl_d[k], h.p, h.w_last + (long)h.fg0 * h.m, h.fng, Img{}, 0, 0, h.parts, h.splits, h.g};
+        }
         ProfScope ps("feature_bwd", fl, 0, s);
-        FeatDims fl_d = fd;
-        for (int l = 0; l <= fd.L; ++l) fl_d.act[l] = fd.act[l] + (long)fg0 * fd.sz[l];
-        feature_backward(fl_d, p, w_last + (long)fg0 * m, parts, splits, ng, g, s);
+        feature_backward_multi(jobs, nh, s);
     }
 }
 
@@ -637,8 +687,10 @@ void Trainer::phase_rollout(int it) {
     MB_CUDA(cudaMemsetAsync(d_retsum, 0, sizeof(double) * Nl_, s_));
     MB_CUDA(cudaMemsetAsync(d_retcnt, 0, sizeof(int) * Nl_, s_));
     MB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s_));
-    actor_.forward(d_cw, g_lo_, Kl_, s_);
-    critic_.forward(d_cw, g_lo_, Kl_, s_);
+    {
+        HyperNet* both[2] = {&actor_, &critic_};
+        HyperNet::forward_multi(both, 2, d_cw, g_lo_, Kl_, s_);
+    }
     {
         ProfScope ps("pack_theta", 0, (double)Kl_ * (actor_.P * 4 + pol_plan_.blob_bytes + critic_.P * 4 +
                                                        cri_plan_.blob_bytes), s_);
@@ -790,112 +842,163 @@ void Trainer::phase_advantages() {
 // images: forward Z_l = A_{l-1} W_l^T (grouped rows), per-row loss head,
 // dW_l = G_l^T A_{l-1} (K = the cluster's rows), dX = (G_l W_l) * tanh'.
 // Leaves gtheta [local clusters][P] (fp32, reference flat layout) complete.
-void Trainer::net_step(HyperNet& h, bool is_actor, int Bp, float inv_B, int maxg, const int* rows, const int* goff,
-                       int slot, cudaStream_t s_) {
-    const NetDims& nd = h.tgt;
-    const int L = nd.L;
-    UpdBufs& u = ub_[is_actor ? 0 : 1];
-    float* gth = h.gtheta + (long)g_lo_ * h.ld;
-    float* d_psls = u.psls;
-    double* d_lossrows = u.lossrows;
-    if (Bp == 0) {
-        MB_CUDA(cudaMemsetAsync(gth, 0, sizeof(float) * Kl_ * h.ld, s_));
-        MB_CUDA(cudaMemsetAsync(d_mbloss + slot * 2 + (is_actor ? 0 : 1), 0, sizeof(double), s_));
-        return;
+// One or two nets' loss + backward through their generated weights on one
+// minibatch (losses.cpp:46-189); with two nets (actor + critic) every stage
+// is one launch covering both. Contractions on the tensor cores over bf16
+// images: forward Z_l = A_{l-1} W_l^T (grouped rows), per-row loss head,
+// dW_l = G_l^T A_{l-1} (K = the cluster's rows), dX = (G_l W_l) * tanh'.
+// Leaves gtheta [local clusters][P] (fp32, reference flat layout) complete.
+void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, float inv_B, int maxg, const int* rows,
+                       const int* goff, int slot, cudaStream_t s_) {
+    struct Net {
+        HyperNet* h;
+        bool actor;
+        UpdBufs* u;
+        float* gth;
+        const float* th;
+        bool fused_head;
+        int Lg;
+    } N[2];
+    for (int k = 0; k < nn; ++k) {
+        Net& n = N[k];
+        n.h = hs[k];
+        n.actor = actor[k];
+        n.u = &ub_[n.actor ? 0 : 1];
+        n.gth = n.h->gtheta + (long)g_lo_ * n.h->ld;
+        n.th = n.h->theta + (long)g_lo_ * n.h->ld;
+        const NetDims& nd = n.h->tgt;
+        const int L = nd.L;
+        // the output layer, the loss and the output layer's backward run fused
+        // in k_head on the CUDA cores when there is a hidden layer to feed it
+        n.fused_head = L >= 2 && nd.sz[L - 1] % 16 == 0 && nd.sz[L - 1] <= 256 && nd.sz[L] <= 16;
+        n.Lg = n.fused_head ? L - 1 : L;  // layers run as tensor-core GEMMs in the forward
+        if (Bp == 0) {
+            MB_CUDA(cudaMemsetAsync(n.gth, 0, sizeof(float) * Kl_ * n.h->ld, s_));
+            MB_CUDA(cudaMemsetAsync(d_mbloss + slot * 2 + (n.actor ? 0 : 1), 0, sizeof(double), s_));
+        }
     }
-    const float* th = h.theta + (long)g_lo_ * h.ld;
-    // the generated weight images (h.wimg) were written by h.forward's theta GEMM
-    auto wl = [&](int l) {
+    if (Bp == 0) return;
+    // the generated weight images (h.wimg) were written by the forward's theta GEMM
+    auto wl = [](const HyperNet& h, int l) {
         Img w = h.wimg;
         w.p = h.wimg.p + h.wimg_off[l];
-        w.R = nd.sz[l + 1];
-        w.C = nd.sz[l];
+        w.R = h.tgt.sz[l + 1];
+        w.C = h.tgt.sz[l];
         return w;
     };
-    // the output layer, the loss and the output layer's backward run fused in
-    // k_head on the CUDA cores when there is a hidden layer to feed it
-    const bool fused_head = L >= 2 && nd.sz[L - 1] % 16 == 0 && nd.sz[L - 1] <= 256 && nd.sz[L] <= 16;
-    const int Lg = fused_head ? L - 1 : L;  // layers run as tensor-core GEMMs in the forward
-    for (int l = 0; l < Lg; ++l) {  // forward
-        const bool last = (l == L - 1);
-        IGemm d;
-        d.A = l == 0 ? Xi_ : u.A[l - 1]; d.a_view = 0;  // (m = row, k = in)
-        d.B = wl(l); d.b_view = 0;                     // (n = out, k = in)
-        d.M = Bp; d.N = nd.sz[l + 1]; d.K = nd.sz[l]; d.Z = Kl_;
-        d.gmode = 1; d.goff = goff; d.max_group = maxg;
-        d.bias = th + nd.boff[l]; d.bias_gs = h.ld; d.bias_mode = 1;
-        if (last) {
-            d.C = u.Zf; d.cm = 16; d.cn = 1;  // Gaussian mean / values (pre-activation)
-        } else {
-            d.act = 1; d.O = u.A[l]; d.o_mode = 1;
+    auto batch = [&](const char* cls, const IGemm* ds, int n) {
+        double fl = 0;
+        for (int k = 0; k < n; ++k) fl += 2.0 * ds[k].M * ds[k].N * ds[k].K * (ds[k].gmode == 0 ? ds[k].Z : 1);
+        ProfScope ps(cls, fl, 0, s_);
+        img_gemm_batch(ds, n, s_);
+    };
+    const int Lmax = std::max(N[0].h->tgt.L, nn > 1 ? N[1].h->tgt.L : 0);
+    for (int l = 0; l < Lmax; ++l) {  // forward, layer by layer over the nets
+        IGemm ds[2];
+        int n = 0;
+        for (int k = 0; k < nn; ++k) {
+            const Net& t = N[k];
+            const NetDims& nd = t.h->tgt;
+            if (l >= t.Lg) continue;
+            const bool last = (l == nd.L - 1);
+            IGemm& d = ds[n++];
+            d.A = l == 0 ? Xi_ : t.u->A[l - 1]; d.a_view = 0;  // (m = row, k = in)
+            d.B = wl(*t.h, l); d.b_view = 0;                   // (n = out, k = in)
+            d.M = Bp; d.N = nd.sz[l + 1]; d.K = nd.sz[l]; d.Z = Kl_;
+            d.gmode = 1; d.goff = goff; d.max_group = maxg;
+            d.bias = t.th + nd.boff[l]; d.bias_gs = t.h->ld; d.bias_mode = 1;
+            if (last) {
+                d.C = t.u->Zf; d.cm = 16; d.cn = 1;  // Gaussian mean / values (pre-activation)
+            } else {
+                d.act = 1; d.O = t.u->A[l]; d.o_mode = 1;
+            }
         }
-        igemm("mlp_fwd", d, s_);
+        // a tanh layer and a plain output layer cannot share a launch
+        if (n == 2 && ds[0].act != ds[1].act) {
+            batch("mlp_fwd", &ds[0], 1);
+            batch("mlp_fwd", &ds[1], 1);
+        } else if (n) {
+            batch("mlp_fwd", ds, n);
+        }
     }
-    if (fused_head) {
-        HeadArgs ha;
-        ha.Bp = Bp; ha.H = nd.sz[L - 1]; ha.out = nd.sz[L];
-        ha.rows = rows; ha.rg = d_rowgroup;
-        ha.theta = th; ha.ld = h.ld; ha.woff = nd.woff[L - 1]; ha.boff = nd.boff[L - 1]; ha.mlp_n = nd.mlp_n;
-        ha.A = u.A[L - 2]; ha.Gout = u.G[L - 1]; ha.Gprev = u.G[L - 2];
-        ha.z = d_Z; ha.lp_old = d_lpo; ha.sadv = d_sa; ha.clip = (float)cfg_.clip_eps;
-        ha.ent = (float)cfg_.entropy_coef; ha.err = d_err;
-        ha.tgt = d_tg; ha.inv_B = inv_B;
-        ha.psum = u.pbias[L - 1]; ha.psls = d_psls; ha.psum_prev = u.pbias[L - 2]; ha.psum_prev_ld = nd.sz[L - 1];
-        ha.loss_rows = d_lossrows;
-        {
+    for (int k = 0; k < nn; ++k) {
+        const Net& t = N[k];
+        const NetDims& nd = t.h->tgt;
+        const int L = nd.L;
+        UpdBufs& u = *t.u;
+        if (t.fused_head) {
+            HeadArgs ha;
+            ha.Bp = Bp; ha.H = nd.sz[L - 1]; ha.out = nd.sz[L];
+            ha.rows = rows; ha.rg = d_rowgroup;
+            ha.theta = t.th; ha.ld = t.h->ld; ha.woff = nd.woff[L - 1]; ha.boff = nd.boff[L - 1]; ha.mlp_n = nd.mlp_n;
+            ha.A = u.A[L - 2]; ha.Gout = u.G[L - 1]; ha.Gprev = u.G[L - 2];
+            ha.z = d_Z; ha.lp_old = d_lpo; ha.sadv = d_sa; ha.clip = (float)cfg_.clip_eps;
+            ha.ent = (float)cfg_.entropy_coef; ha.err = d_err;
+            ha.tgt = d_tg; ha.inv_B = inv_B;
+            ha.psum = u.pbias[L - 1]; ha.psls = u.psls; ha.psum_prev = u.pbias[L - 2]; ha.psum_prev_ld = nd.sz[L - 1];
+            ha.loss_rows = u.lossrows;
             const double fl = 4.0 * Bp * nd.sz[L - 1] * nd.sz[L];  // forward + backward of the output layer
             ProfScope ps("mlp_head", fl, 0, s_);
-            head(ha, is_actor, s_);
+            head(ha, t.actor, s_);
+        } else if (t.actor) {  // losses.cpp:87-129
+            actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, t.th, t.h->ld, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
+                           (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], u.pbias[L - 1], u.psls,
+                           u.lossrows, d_err, s_);
+        } else {  // losses.cpp:170-185
+            critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], u.pbias[L - 1], u.lossrows, s_);
         }
-    } else if (is_actor) {  // losses.cpp:87-129
-        actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, th, h.ld, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
-                       (float)cfg_.clip_eps, (float)cfg_.entropy_coef, inv_B, u.G[L - 1], u.pbias[L - 1], d_psls,
-                       d_lossrows, d_err, s_);
-    } else {  // losses.cpp:170-185
-        critic_rows_img(Bp, es_.m, rows, u.Zf, 16, d_tg, inv_B, u.G[L - 1], u.pbias[L - 1], d_lossrows, s_);
     }
     // backward (nn.cpp:111-160): the data-gradient chain first (each dX needs
     // the previous one), then every layer's weight gradient -- independent
     // of each other -- batched three per launch
-    for (int l = L - 1; l > 0; --l) {
-        if (fused_head && l == L - 1) continue;  // k_head produced G_{L-2}
-        IGemm e;  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
-        e.A = u.G[l]; e.a_view = 0;  // (m = q, k = j)
-        e.B = wl(l); e.b_view = 1;   // (n = i, k = j)
-        e.M = Bp; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
-        e.gmode = 1; e.goff = goff; e.max_group = maxg;
-        e.act = 2; e.aux = u.A[l - 1];
-        e.O = u.G[l - 1]; e.o_mode = 1;
-        e.psum = u.pbias[l - 1]; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
-        igemm("mlp_dX", e, s_);
+    for (int l = Lmax - 1; l > 0; --l) {
+        IGemm ds[2];
+        int n = 0;
+        for (int k = 0; k < nn; ++k) {
+            const Net& t = N[k];
+            const NetDims& nd = t.h->tgt;
+            if (l >= nd.L || (t.fused_head && l == nd.L - 1)) continue;  // k_head produced G_{L-2}
+            IGemm& e = ds[n++];  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
+            e.A = t.u->G[l]; e.a_view = 0;  // (m = q, k = j)
+            e.B = wl(*t.h, l); e.b_view = 1;  // (n = i, k = j)
+            e.M = Bp; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
+            e.gmode = 1; e.goff = goff; e.max_group = maxg;
+            e.act = 2; e.aux = t.u->A[l - 1];
+            e.O = t.u->G[l - 1]; e.o_mode = 1;
+            e.psum = t.u->pbias[l - 1]; e.psum_ld = nd.sz[l];  // per-tile column sums -> bias grads of layer l-1
+        }
+        if (n) batch("mlp_dX", ds, n);
     }
     std::vector<IGemm> dws;
-    for (int l = L - 1; l >= 0; --l) {
-        const Img& ain = l == 0 ? Xi_ : u.A[l - 1];
-        IGemm d;  // dW_l[z][j][i] = sum_{q in z} G_l[q][j] A_{l-1}[q][i]
-        d.A = u.G[l]; d.a_view = 1;  // (m = j, k = q)
-        d.B = ain; d.b_view = 1;     // (n = i, k = q)
-        d.M = nd.sz[l + 1]; d.N = nd.sz[l]; d.K = Bp; d.Z = Kl_;
-        d.gmode = 2; d.goff = goff;
-        d.C = gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = h.ld;
-        dws.push_back(d);
+    for (int k = 0; k < nn; ++k) {
+        const Net& t = N[k];
+        const NetDims& nd = t.h->tgt;
+        for (int l = nd.L - 1; l >= 0; --l) {
+            const Img& ain = l == 0 ? Xi_ : t.u->A[l - 1];
+            IGemm d;  // dW_l[z][j][i] = sum_{q in z} G_l[q][j] A_{l-1}[q][i]
+            d.A = t.u->G[l]; d.a_view = 1;  // (m = j, k = q)
+            d.B = ain; d.b_view = 1;        // (n = i, k = q)
+            d.M = nd.sz[l + 1]; d.N = nd.sz[l]; d.K = Bp; d.Z = Kl_;
+            d.gmode = 2; d.goff = goff;
+            d.C = t.gth + nd.woff[l]; d.cm = nd.sz[l]; d.cn = 1; d.c_gs = t.h->ld;
+            dws.push_back(d);
+        }
     }
-    for (size_t k0 = 0; k0 < dws.size(); k0 += 3) {
-        const int nb = (int)std::min<size_t>(3, dws.size() - k0);
-        double fl = 0;
-        for (int k = 0; k < nb; ++k) fl += 2.0 * dws[k0 + k].M * dws[k0 + k].N * dws[k0 + k].K;
-        ProfScope ps("mlp_dW", fl, 0, s_);
-        img_gemm_batch(&dws[k0], nb, s_);
-    }
+    for (size_t k0 = 0; k0 < dws.size(); k0 += 3) batch("mlp_dW", &dws[k0], (int)std::min<size_t>(3, dws.size() - k0));
     // every bias gradient (per-tile column sums of G_l -> per cluster), the
-    // log-std gradients and the minibatch loss: one launch
+    // log-std gradients and the minibatch losses: one launch
     SegJobs jb;
-    for (int l = 0; l < L; ++l)  // output layer partials are written with a row stride of 16
-        jb.job[jb.n++] = SegJob{u.pbias[l], l == L - 1 ? 16 : nd.sz[l + 1], nd.sz[l + 1], gth + nd.boff[l], h.ld};
-    if (is_actor) jb.job[jb.n++] = SegJob{d_psls, 16, es_.act_dim, gth + nd.mlp_n, h.ld};
-    jb.loss_tiles = d_lossrows;
-    jb.n_loss = Bp / 128;
-    jb.loss_out = d_mbloss + slot * 2 + (is_actor ? 0 : 1);
+    for (int k = 0; k < nn; ++k) {
+        const Net& t = N[k];
+        const NetDims& nd = t.h->tgt;
+        const int L = nd.L;
+        for (int l = 0; l < L; ++l)  // output layer partials are written with a row stride of 16
+            jb.job[jb.n++] = SegJob{t.u->pbias[l], l == L - 1 ? 16 : nd.sz[l + 1], nd.sz[l + 1], t.gth + nd.boff[l],
+                                    t.h->ld};
+        if (t.actor) jb.job[jb.n++] = SegJob{t.u->psls, 16, es_.act_dim, t.gth + nd.mlp_n, t.h->ld};
+        jb.loss[k] = SegLoss{t.u->lossrows, Bp / 128, d_mbloss + slot * 2 + (t.actor ? 0 : 1)};
+    }
+    jb.nloss = nn;
     segsum_multi(jb, goff, Kl_, s_);
 }
 
@@ -910,15 +1013,20 @@ void Trainer::allreduce_grad(HyperNet& h, cudaStream_t s) {
 // independent, so their many small kernels overlap. Joins: both losses are
 // checked for finiteness before either Adam (train.cpp:174-178), and the
 // next minibatch's gather waits for the critic to release the shared inputs.
+// One PPO minibatch (train.cpp:163-180). Default: one stream per net (actor
+// on s_, critic on s2_) joined for the finiteness check, so one net's
+// HBM-bound Adam overlaps the other net's GEMMs (measured 26.5 ms/iter).
+// MORLAX_FUSED_NETS=1: both nets in lockstep on one stream, every stage one
+// launch covering both (fewer, fuller launches but no overlap: 29.9 ms/iter).
+// Both losses are checked for finiteness before either Adam (train.cpp:174-178).
 void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, const int* goff) {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
-    // MORLAX_ONE_STREAM=1 serialises the two chains (profiling: per-class times without overlap)
-    static const bool one = [] {
-        const char* e = std::getenv("MORLAX_ONE_STREAM");
-        return e && e[0] == '1';
+    static const bool two = [] {
+        const char* e = std::getenv("MORLAX_FUSED_NETS");
+        return !(e && e[0] == '1');
     }();
-    cudaStream_t sc = one ? s_ : s2_;
+    cudaStream_t sc = two ? s2_ : s_;
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
     if (Bp > 0) {
         MbGather ga;
@@ -928,13 +1036,28 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         ga.Xi = Xi_; ga.act_o = d_Z; ga.lp_o = d_lpo; ga.sadv_o = d_sa; ga.tgt_o = d_tg; ga.rg = d_rowgroup;
         gather_minibatch(ga, s_);
     }
+    HyperNet* both[2] = {&actor_, &critic_};
+    const bool roles[2] = {true, false};
+    if (!two) {
+        HyperNet::forward_multi(both, 2, d_cw, g_lo_, Kl_, s_);  // hypernet_forward per loss (losses.cpp:79,167)
+        net_step(both, roles, 2, Bp, inv_B, maxg, rows, goff, slot, s_);
+        if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
+        check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
+        HyperNet::backward_multi(both, 2, s_);
+        allreduce_grad(actor_, s_);
+        allreduce_grad(critic_, s_);
+        actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
+        critic_.adam_step(cfg_.critic_lr, d_err, s_);
+        MB_CUDA(cudaEventRecord(ev_c_done_, s_));
+        return;
+    }
     MB_CUDA(cudaEventRecord(ev_gather_, s_));
     MB_CUDA(cudaStreamWaitEvent(sc, ev_gather_, 0));
-    critic_.forward(d_cw, g_lo_, Kl_, sc);  // hypernet_forward per loss (losses.cpp:79,167)
-    net_step(critic_, false, Bp, inv_B, maxg, rows, goff, slot, sc);
+    critic_.forward(d_cw, g_lo_, Kl_, sc);
+    net_step(&both[1], &roles[1], 1, Bp, inv_B, maxg, rows, goff, slot, sc);
     MB_CUDA(cudaEventRecord(ev_c_net_, sc));
     actor_.forward(d_cw, g_lo_, Kl_, s_);
-    net_step(actor_, true, Bp, inv_B, maxg, rows, goff, slot, s_);
+    net_step(&both[0], &roles[0], 1, Bp, inv_B, maxg, rows, goff, slot, s_);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_net_, 0));
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
@@ -1033,8 +1156,10 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
     MB_CUDA(cudaMemcpyAsync(d_rows, h_rows_pinned, sizeof(int) * (Bp ? Bp : 1), cudaMemcpyHostToDevice, s_));
     MB_CUDA(cudaMemcpyAsync(d_goff, h_goff_pinned, sizeof(int) * (Kl_ + 1), cudaMemcpyHostToDevice, s_));
     MB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), s_));
-    actor_.forward(d_cw, g_lo_, Kl_, s_);
-    critic_.forward(d_cw, g_lo_, Kl_, s_);
+    {
+        HyperNet* both[2] = {&actor_, &critic_};
+        HyperNet::forward_multi(both, 2, d_cw, g_lo_, Kl_, s_);
+    }
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)n);
     if (Bp > 0) {
@@ -1045,8 +1170,9 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
         ga.Xi = Xi_; ga.act_o = d_Z; ga.lp_o = d_lpo; ga.sadv_o = d_sa; ga.tgt_o = d_tg; ga.rg = d_rowgroup;
         gather_minibatch(ga, s_);
     }
-    net_step(actor_, true, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
-    net_step(critic_, false, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
+    HyperNet* both[2] = {&actor_, &critic_};
+    const bool roles[2] = {true, false};
+    net_step(both, roles, 2, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss, 2, s_);
     actor_.backward(s_);
     critic_.backward(s_);

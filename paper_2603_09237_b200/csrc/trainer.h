@@ -85,6 +85,9 @@ struct HyperNet {
     void init_params(uint64_t key, cudaStream_t s);  // init_hypernet (hypernet.cpp:124-145)
     // f, theta for groups [g0, g0+ng) of the G cluster weights w[G][m]
     void forward(const float* w, int g0, int ng, cudaStream_t s);
+    // the same for nh (1 or 2) hypernetworks in lockstep, one launch per stage
+    static void forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s);
+    static void backward_multi(HyperNet* const* hs, int nh, cudaStream_t s);
     // grads from gtheta [G][P] (all groups) -> g
     void backward(cudaStream_t s);
     void adam_step(double lr, const int* err, cudaStream_t s);
@@ -170,8 +173,8 @@ private:
     int worker_plan_ = -1;
     long perm_version_ = 0;
     void minibatch(int slot, int B, int Bglob, int maxg, const int* d_rows, const int* d_goff);
-    void net_step(HyperNet& h, bool actor, int Bp, float inv_B, int maxg, const int* rows, const int* d_goff,
-                  int slot, cudaStream_t st);
+    void net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, float inv_B, int maxg, const int* rows,
+                  const int* d_goff, int slot, cudaStream_t s);
     void allreduce_grad(HyperNet& h, cudaStream_t s);
 
     TrainConfig cfg_;
