@@ -543,13 +543,15 @@ void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, co
 // and of g_prev (bias grads of the last hidden layer), and the tile's loss.
 // Padded rows (rows[q] < 0) contribute zeros.
 // =========================================================================
-template <bool ACTOR>
+// OUT = output width (compile time: the per-row arrays stay in registers)
+template <bool ACTOR, int OUT>
 __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
     __shared__ __align__(16) float sw[16 * 256];
     __shared__ float sb[16];
     __shared__ float red[64];
     __shared__ float red2[4 * 256];
-    const int H = a.H, out = a.out;
+    const int H = a.H;
+    constexpr int out = OUT;
     const int q = blockIdx.x * 128 + threadIdx.x;
     const int z = a.rg[blockIdx.x * 128];  // groups are 128-row padded: one cluster per tile
     const float* th = a.theta + (long)z * a.ld;
@@ -559,9 +561,9 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
     const bool live = a.rows[q] >= 0;
     const int CTa = img_ct(a.A.C), CTg = img_ct(a.Gprev.C), CTo = img_ct(a.Gout.C);
     // ---- forward of the output layer
-    float o[16];
+    float o[OUT];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) o[j] = 0.f;
+    for (int j = 0; j < OUT; ++j) o[j] = 0.f;
     // activation row: 4 16-byte units (32 columns) in flight per step
     auto fwd8 = [&](const uint4& u, int c) {
         const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -573,8 +575,7 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
             x[2 * e + 1] = f.y;
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (j >= out) break;
+        for (int j = 0; j < OUT; ++j) {
             const float4 w0 = *reinterpret_cast<const float4*>(sw + j * H + c);
             const float4 w1 = *reinterpret_cast<const float4*>(sw + j * H + c + 4);
             o[j] = fmaf(x[0], w0.x, o[j]);
@@ -596,17 +597,16 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
         for (int k = 0; k < 4; ++k) fwd8(u[k], c + 8 * k);
     }
     for (; c < H; c += 8) fwd8(*reinterpret_cast<const uint4*>(a.A.p + img_off(q, c, CTa)), c);
-    float g[16], gl[16];
+    float g[16], gl[16];  // 16: the image / column-sum code below works in 8-wide groups
 #pragma unroll
     for (int j = 0; j < 16; ++j) g[j] = gl[j] = 0.f;
     double lrow = 0.0;
     if (live) {
         if (ACTOR) {  // losses.cpp:87-129 (action_logprob nn.cpp:204-219)
             const float* ls_raw = th + a.mlp_n;
-            float lp = 0.f, zn[16], sig[16], ent_h = 0.f;
+            float lp = 0.f, zn[OUT], sig[OUT], ent_h = 0.f;
 #pragma unroll
-            for (int d = 0; d < 16; ++d) {
-                if (d >= out) break;
+            for (int d = 0; d < OUT; ++d) {
                 const float ls = fminf(fmaxf(ls_raw[d], -5.f), 1.f);
                 sig[d] = __expf(ls);
                 const float zz = a.z[(long)q * out + d];
@@ -623,16 +623,14 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
             lrow = (double)(-fminf(unc, clp) * a.inv_B) - (double)(a.ent * ent_h * a.inv_B);
             const float glp = unc <= clp ? -ratio * adv * a.inv_B : 0.f;  // losses.cpp:116
 #pragma unroll
-            for (int d = 0; d < 16; ++d) {
-                if (d >= out) break;
+            for (int d = 0; d < OUT; ++d) {
                 g[d] = glp * zn[d] / sig[d];
                 const float raw = ls_raw[d];  // clamp mask (losses.cpp:124-128)
                 gl[d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - a.ent * a.inv_B : 0.f;
             }
         } else {  // losses.cpp:170-185: sum_k (v - tgt)^2 / B, grad 2 e / B
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (k >= out) break;
+            for (int k = 0; k < OUT; ++k) {
                 const float e = (o[k] + sb[k]) - a.tgt[(long)q * out + k];
                 lrow += (double)e * e * a.inv_B;
                 g[k] = 2.f * e * a.inv_B;
@@ -648,8 +646,31 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
         w.w = umma::pack_bf16(g[8 * h + 6], g[8 * h + 7]);
         *reinterpret_cast<uint4*>(a.Gout.p + img_off(q, 8 * h, CTo)) = w;
     }
-    tile_colsum(g, out, red, a.psum + blockIdx.x * 16);
-    if (ACTOR) tile_colsum(gl, out, red, a.psls + blockIdx.x * 16);
+    {  // per-tile column sums of the output gradient (bias) and the log-std terms, fixed order
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int d = 0; d < OUT; ++d) {
+            float x1 = g[d], x2 = gl[d];
+#pragma unroll
+            for (int k = 16; k > 0; k >>= 1) {
+                x1 += __shfl_xor_sync(0xffffffffu, x1, k);
+                if (ACTOR) x2 += __shfl_xor_sync(0xffffffffu, x2, k);
+            }
+            if (lane == 0) {
+                red[warp * 16 + d] = x1;
+                if (ACTOR) red2[warp * 16 + d] = x2;  // red2 is free until the backward below
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < OUT) {
+            a.psum[blockIdx.x * 16 + threadIdx.x] =
+                red[threadIdx.x] + red[16 + threadIdx.x] + red[32 + threadIdx.x] + red[48 + threadIdx.x];
+            if (ACTOR)
+                a.psls[blockIdx.x * 16 + threadIdx.x] =
+                    red2[threadIdx.x] + red2[16 + threadIdx.x] + red2[32 + threadIdx.x] + red2[48 + threadIdx.x];
+        }
+        __syncthreads();
+    }
     // ---- backward of the output layer into the last hidden layer
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint4 nxt[2];
@@ -665,8 +686,7 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] = 0.f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {  // W_L^T g: rows of W_L as float4 broadcasts
-            if (j >= out) break;
+        for (int j = 0; j < OUT; ++j) {  // W_L^T g: rows of W_L as float4 broadcasts
             const float4* w4 = reinterpret_cast<const float4*>(sw + j * H + c);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -720,10 +740,17 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
 void head(const HeadArgs& a, bool actor, cudaStream_t s) {
     if (a.Bp <= 0) return;
     if (a.H > 256 || a.H % 16 || a.out > 16) throw ShapeError("head: needs hidden width % 16 == 0 (<= 256), out <= 16");
-    if (actor)
-        k_head<true><<<a.Bp / 128, 128, 0, s>>>(a);
-    else
-        k_head<false><<<a.Bp / 128, 128, 0, s>>>(a);
+#define MB_HEAD(O)                                                              \
+    case O:                                                                     \
+        if (actor) k_head<true, O><<<a.Bp / 128, 128, 0, s>>>(a);               \
+        else k_head<false, O><<<a.Bp / 128, 128, 0, s>>>(a);                    \
+        break;
+    switch (a.out) {
+        MB_HEAD(1) MB_HEAD(2) MB_HEAD(3) MB_HEAD(4) MB_HEAD(5) MB_HEAD(6) MB_HEAD(7) MB_HEAD(8)
+        MB_HEAD(9) MB_HEAD(10) MB_HEAD(11) MB_HEAD(12) MB_HEAD(13) MB_HEAD(14) MB_HEAD(15) MB_HEAD(16)
+        default: throw ShapeError("head: output width must be in [1, 16]");
+    }
+#undef MB_HEAD
     MB_LAUNCH();
 }
 
