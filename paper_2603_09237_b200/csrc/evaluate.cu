@@ -26,7 +26,7 @@ constexpr int kEvalE = 16;  // max instances per CTA
 constexpr int kEvalThreads = 256;
 
 template <int E>  // instances per CTA (8 or 16)
-__global__ void __launch_bounds__(kEvalThreads) k_eval(EvalArgs a) {
+__global__ void __launch_bounds__(kEvalThreads) k_eval(const __grid_constant__ EvalArgs a) {
     extern __shared__ __align__(16) uint8_t sm[];
     const NetDims& nd = a.pol;
     const int g = blockIdx.x / a.cpp, cb = blockIdx.x % a.cpp;

@@ -37,9 +37,11 @@ __device__ __forceinline__ float sech2(float z) {
 }
 
 struct Ctx {
-    uint8_t* ring[2];
+    uint8_t* ring0;  // 2 weight slots: ring0 + slot * ring_stride (no indexed pointer array: registers)
+    int ring_stride;
     uint8_t* xb;     // layer-0 operand (MN-major, env x obs_pad)
-    uint8_t* hb[2];  // hidden activations (MN-major, env x hpad)
+    uint8_t* hb0;  // 2 hidden-activation buffers (MN-major, env x hpad): hb0 + i * hb_stride
+    int hb_stride;
     uint64_t* fullb;
     uint64_t* mmad;
     uint32_t tbase;
@@ -67,7 +69,7 @@ struct Issuer {
     int step, pos;
 };
 
-__device__ void issue_next(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* vflags, int group) {
+__device__ __forceinline__ void issue_next(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* vflags, int group) {
     if (is.step >= a.T) return;
     int net, c;
     chunk_at(a, vflags[is.step & 1], is.pos, &net, &c);
@@ -75,7 +77,7 @@ __device__ void issue_next(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int
     const uint8_t* src = (net ? a.cri_blob : a.pol_blob) + (long)group * pl.blob_bytes + pl.chunk_off[c];
     const int slot = (int)(x.issued & 1);
     umma::mbar_arrive_expect_tx(&x.fullb[slot], (uint32_t)pl.chunk_bytes[c]);
-    umma::bulk_g2s(x.ring[slot], src, (uint32_t)pl.chunk_bytes[c], &x.fullb[slot]);
+    umma::bulk_g2s(x.ring0 + slot * x.ring_stride, src, (uint32_t)pl.chunk_bytes[c], &x.fullb[slot]);
     x.issued++;
     if (++is.pos >= step_len(a, vflags[is.step & 1])) {
         is.pos = 0;
@@ -85,7 +87,7 @@ __device__ void issue_next(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int
 
 // Run one net (all chunks) on the layer-0 operand xb. Result: output layer
 // accumulators in TMEM columns [OUT_COL, OUT_COL+16) (M = 64 env layout).
-__device__ void run_net(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* vflags, int group, int net,
+__device__ __forceinline__ void run_net(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* vflags, int group, int net,
                         const float* theta) {
     const NetPlan& pl = net ? a.cri_plan : a.pol_plan;
     const NetDims& nd = net ? a.cri : a.pol;
@@ -96,14 +98,14 @@ __device__ void run_net(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* v
         const bool last = (l == nd.L - 1);
         const int kin = pl.kin_pad[l];
         const uint32_t sbo = (uint32_t)kin * 16;  // 8-row block stride of every operand of this layer
-        const uint8_t* inb = cur < 0 ? x.xb : x.hb[cur];
+        const uint8_t* inb = cur < 0 ? x.xb : x.hb0 + cur * x.hb_stride;
         const int ntiles = last ? 1 : pl.tiles[l];
         for (int t = 0; t < ntiles; ++t, ++c) {
             if (threadIdx.x == 0) {
                 const int slot = (int)(x.consumed & 1);
                 umma::mbar_wait(&x.fullb[slot], (uint32_t)((x.consumed >> 1) & 1));
                 umma::fence_after_sync();
-                const uint32_t w0 = umma::smem_u32(x.ring[slot]), i0 = umma::smem_u32(inb);
+                const uint32_t w0 = umma::smem_u32(x.ring0 + slot * x.ring_stride), i0 = umma::smem_u32(inb);
                 if (!last) {
                     const uint32_t idesc = umma::idesc_bf16(128, x.nepad, false, true);
                     for (int k = 0; k < kin / 16; ++k)
@@ -125,7 +127,7 @@ __device__ void run_net(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* v
         umma::fence_after_sync();
         if (!last) {  // epilogue: bias + tanh -> next operand (MN-major, env x hpad)
             const int nxt = cur < 0 ? 0 : (cur ^ 1);
-            uint8_t* ob = x.hb[nxt];
+            uint8_t* ob = x.hb0 + nxt * x.hb_stride;
             const uint32_t osbo = (uint32_t)pl.kin_pad[l + 1] * 16;
             const int tile = warp >> 2, lg = warp & 3;
             const int out = nd.sz[l + 1];
@@ -158,7 +160,7 @@ __device__ void run_net(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* v
     }
 }
 
-__global__ void __launch_bounds__(RNT, 1) k_rollout_tc(RolloutTcArgs a) {
+__global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ RolloutTcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int cpg = (a.reps + RE - 1) / RE;
     const int c = blockIdx.x / cpg, ch = blockIdx.x % cpg;
@@ -169,11 +171,9 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(RolloutTcArgs a) {
     // ---- shared memory carve-up (host computes the same total)
     Ctx x;
     uint8_t* p = smem;
-    x.ring[0] = p; p += a.slot_bytes;
-    x.ring[1] = p; p += a.slot_bytes;
+    x.ring0 = p; x.ring_stride = a.slot_bytes; p += 2 * a.slot_bytes;
     x.xb = p; p += a.xb_bytes;
-    x.hb[0] = p; p += a.hb_bytes;
-    x.hb[1] = p; p += a.hb_bytes;
+    x.hb0 = p; x.hb_stride = a.hb_bytes; p += 2 * a.hb_bytes;
     float* S = reinterpret_cast<float*>(p); p += sizeof(float) * sd * RE;      // env state [k][env]
     float* MU = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 16;     // policy mean
     float* ZS = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 16;     // pre-tanh sample
@@ -294,14 +294,20 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(RolloutTcArgs a) {
         for (int r = tid; r < nr; r += RNT) {
             const long row = (long)(i0 + r) * a.T + t;
             for (int k = 0; k < m; ++k) a.value[row * m + k] = NEED[r] ? VV[r * 8 + k] : NV[r * 8 + k];
-            float act[16], rw[8];
+            float act[16], rw[8];  // compile-time indexed (predicated): registers, not local memory
             bool anyc = false;
-            for (int d = 0; d < ad; ++d) {
-                const float xx = tanhf(ZS[r * 16 + d]);
-                if (!isfinite(xx)) atomicExch(a.err, 3);
-                act[d] = fminf(fmaxf(xx, -1.f), 1.f);
-                anyc |= act[d] != xx;
+#pragma unroll
+            for (int d = 0; d < 16; ++d) {
+                act[d] = 0.f;
+                if (d < ad) {
+                    const float xx = tanhf(ZS[r * 16 + d]);
+                    if (!isfinite(xx)) atomicExch(a.err, 3);
+                    act[d] = fminf(fmaxf(xx, -1.f), 1.f);
+                    anyc |= act[d] != xx;
+                }
             }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) rw[k] = 0.f;
             if (anyc) atomicAdd(a.clamp_count, 1ULL);
             float* s = S + r;
             const bool tm = env_do_step(a.kind, s, RE, act, rw);
@@ -309,10 +315,12 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(RolloutTcArgs a) {
             const bool tr = !tm && st >= a.max_steps;
             a.term[row] = tm;
             a.trunc[row] = tr;
-            for (int k = 0; k < m; ++k) {
-                a.reward[row * m + k] = rw[k];
-                TRK[r * 8 + k] += rw[k];
-            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < m) {
+                    a.reward[row * m + k] = rw[k];
+                    TRK[r * 8 + k] += rw[k];
+                }
             for (int k = 0; k < od; ++k)  // pre-reset final obs -> critic operand
                 *reinterpret_cast<__nv_bfloat16*>(x.xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 +
                                                   (r & 7) * 2) = __float2bfloat16_rn(s[k * RE]);
