@@ -210,14 +210,17 @@ __global__ void k_hv_prep(int n, int m, const double* p, const double* ref, doub
 }
 
 constexpr int kHvThreads = 256;
-__global__ void __launch_bounds__(kHvThreads) k_hv_mc(int m, const double* __restrict__ cp, const int* kp,
+template <int M>  // objectives (compile time: the sample point stays in registers)
+__global__ void __launch_bounds__(kHvThreads) k_hv_mc(const double* __restrict__ cp, const int* kp,
                                                       const double* __restrict__ ref,
                                                       const double* __restrict__ hi, uint64_t samples,
                                                       uint64_t key, uint64_t ctr, unsigned long long* hits) {
+    constexpr int m = M;
     extern __shared__ double pts[];  // [k][m]
     const int k = *kp;
     for (int e = threadIdx.x; e < k * m; e += blockDim.x) pts[e] = cp[e];
-    double r[8], span[8];
+    double r[M], span[M];
+#pragma unroll
     for (int j = 0; j < m; ++j) {
         r[j] = ref[j];
         span[j] = __dsub_rn(hi[j], ref[j]);
@@ -226,14 +229,15 @@ __global__ void __launch_bounds__(kHvThreads) k_hv_mc(int m, const double* __res
     unsigned long long local = 0;
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < samples;
          s += (uint64_t)gridDim.x * blockDim.x) {
-        double x[8];
+        double x[M];
+#pragma unroll
         for (int j = 0; j < m; ++j)
             x[j] = __dadd_rn(r[j], __dmul_rn(span[j], word_double(rng_word(key, ctr + s * m + j + 1))));
         for (int i = 0; i < k; ++i) {
             const double* pi = pts + i * m;
             bool inside = true;
-            for (int j = 0; j < m; ++j)
-                if (x[j] > pi[j]) { inside = false; break; }
+#pragma unroll
+            for (int j = 0; j < m; ++j) inside = inside && !(x[j] > pi[j]);
             if (inside) { ++local; break; }
         }
     }
@@ -258,12 +262,16 @@ void hv_mc(int n, int m, const double* pts, const double* ref, uint64_t samples,
     MB_LAUNCH();
     MB_CUDA(cudaMemsetAsync(hits, 0, sizeof(unsigned long long), s));
     const size_t smem = (size_t)n * m * sizeof(double);
-    static size_t configured = 0;
-    if (smem > configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_hv_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
+#define MB_HV(M_)                                                                                      \
+    case M_:                                                                                           \
+        MB_CUDA(cudaFuncSetAttribute(k_hv_mc<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_hv_mc<M_><<<148 * 8, kHvThreads, smem, s>>>(cp, kp, ref, hi_out, samples, key, ctr, hits);       \
+        break;
+    switch (m) {
+        MB_HV(1) MB_HV(2) MB_HV(3) MB_HV(4) MB_HV(5) MB_HV(6) MB_HV(7) MB_HV(8)
+        default: throw ShapeError("hypervolume: objective count must be in [1, 8]");
     }
-    k_hv_mc<<<148 * 8, kHvThreads, smem, s>>>(m, cp, kp, ref, hi_out, samples, key, ctr, hits);
+#undef MB_HV
     MB_LAUNCH();
 }
 
