@@ -96,17 +96,32 @@ __device__ int block_nd_sort(const double* raw, int c, int m, int key, double* d
     return n;
 }
 
-// ---- warp-wide version; bits: per-warp keep mask (c <= kHvMaxN)
-__device__ int warp_nd_sort(const double* raw, int c, int m, int key, double* dst, unsigned* bits) {
+// ---- warp-wide version (M objectives at compile time: the tested point in
+// registers); bits: per-warp keep mask (c <= kHvMaxN)
+template <int M>
+__device__ int warp_nd_sort(const double* raw, int c, int key, double* dst, unsigned* bits) {
+    constexpr int m = M;
     const int lane = threadIdx.x & 31;
     const int words = (c + 31) >> 5;
     for (int w = 0; w < words; ++w) {
         const int q = w * 32 + lane;
         bool keep = q < c;
         if (keep) {
-            const double* pq = raw + (long)q * m;
-            for (int r = 0; r < c && keep; ++r)
-                if (r != q && dropped_by(raw + (long)r * m, pq, m, r < q)) keep = false;
+            double pq[M];
+#pragma unroll
+            for (int d = 0; d < M; ++d) pq[d] = raw[(long)q * m + d];
+            for (int r = 0; r < c && keep; ++r) {
+                if (r == q) continue;
+                const double* pr = raw + (long)r * m;
+                bool ge = true, ne = false;
+#pragma unroll
+                for (int d = 0; d < M; ++d) {
+                    const double x = pr[d];
+                    ge = ge && x >= pq[d];
+                    ne = ne || x != pq[d];
+                }
+                if (ge && (ne || r < q)) keep = false;
+            }
         }
         const unsigned b = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) bits[w] = b;
@@ -202,6 +217,7 @@ __global__ void k_hv_offsets(const int* s0p, const int* sz1, int* off, int* nsub
 
 // 3. subtask (k, j): incl(L1_k[j]) - hv(nd(limit(L1_k[j], L1_k[j+1:]))),
 // one warp each, depth-first over an explicit frame stack
+template <int M>
 __global__ void __launch_bounds__(kSubWarps * 32) k_hv_sub(const double* __restrict__ L1, const int* s0p,
                                                             const int* __restrict__ sz1,
                                                             const int* __restrict__ off, const int* nsubp, int m,
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(kSubWarps * 32) k_hv_sub(const double* __restr
             for (int q = lane; q < cc0; q += 32)
                 for (int d = 0; d < m; ++d) raw[(long)q * m + d] = fmin(X0[(long)(j + 1 + q) * m + d], p0[d]);
             __syncwarp();
-            const int n1 = warp_nd_sort(raw, cc0, m, key, arena, bits);
+            const int n1 = warp_nd_sort<M>(raw, cc0, key, arena, bits);
             if (n1 == 1) {
                 hv = box_vol(arena, ref, m);
             } else if (n1 > 1) {
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(kSubWarps * 32) k_hv_sub(const double* __restr
                             for (int d = 0; d < m; ++d)
                                 raw2[(long)q * m + d] = fmin(X[(long)(F.k + 1 + q) * m + d], p[d]);
                         __syncwarp();
-                        n2 = warp_nd_sort(raw2, cc, m, key, arena + child, bits);
+                        n2 = warp_nd_sort<M>(raw2, cc, key, arena + child, bits);
                     }
                     if (n2 >= 2) {
                         if (lane == 0) {
@@ -340,11 +356,27 @@ __global__ void k_hv_small(const double* top, const int* s0p, int m, const doubl
     }
 }
 
+// device scratch reused across calls (grown on demand, never shrunk): the
+// recursion arenas are hundreds of MB and cudaMalloc / cudaFree of that size
+// per call cost more than the computation
+struct ScratchPool {
+    void* p[16] = {};
+    size_t cap[16] = {};
+    void* get(int slot, size_t bytes) {
+        if (bytes == 0) bytes = 1;
+        if (bytes > cap[slot]) {
+            if (p[slot]) cudaFree(p[slot]);
+            MB_CUDA(cudaMalloc(&p[slot], bytes));
+            cap[slot] = bytes;
+        }
+        return p[slot];
+    }
+};
+ScratchPool g_pool;
 template <typename T>
 struct DevScratch {
     T* p = nullptr;
-    explicit DevScratch(size_t n) { MB_CUDA(cudaMalloc(&p, sizeof(T) * (n ? n : 1))); }
-    ~DevScratch() { cudaFree(p); }
+    DevScratch(int slot, size_t n) { p = static_cast<T*>(g_pool.get(slot, sizeof(T) * (n ? n : 1))); }
 };
 }  // namespace
 
@@ -353,8 +385,8 @@ void hv_exact(int n, int m, const double* d_pts, const double* d_ref, double* va
     if (m < 1 || m > kHvMaxM) throw ShapeError("hypervolume: objective count must be in [1, 8]");
     if (n > kHvMaxN) throw ShapeError("exact hypervolume: at most 4096 points");
     const long nn = n > 0 ? n : 1;
-    DevScratch<double> raw(nn * m), top(nn * m), out(1);
-    DevScratch<int> ints(8), flag(nn);
+    DevScratch<double> raw(0, nn * m), top(1, nn * m), out(2, 1);
+    DevScratch<int> ints(3, 8), flag(4, nn);
     int *s0p = ints.p, *clp = ints.p + 1, *ctr = ints.p + 2, *ovf = ints.p + 3, *nsubp = ints.p + 4,
         *cmaxp = ints.p + 5;
     MB_CUDA(cudaMemsetAsync(ints.p, 0, sizeof(int) * 8, s));
@@ -372,8 +404,8 @@ void hv_exact(int n, int m, const double* d_pts, const double* d_ref, double* va
         return;
     }
     // 2. level-1 limit sets (worst case s0 points each)
-    DevScratch<double> L1((size_t)s0 * s0 * m), raw1((size_t)s0 * s0 * m);
-    DevScratch<int> sz1(s0), off(s0 + 1), flag1((size_t)s0 * s0);
+    DevScratch<double> L1(5, (size_t)s0 * s0 * m), raw1(6, (size_t)s0 * s0 * m);
+    DevScratch<int> sz1(7, s0), off(8, s0 + 1), flag1(9, (size_t)s0 * s0);
     k_hv_level1<<<s0, 256, 0, s>>>(top.p, s0p, m, L1.p, raw1.p, sz1.p, flag1.p);
     MB_LAUNCH();
     k_hv_offsets<<<1, 32, 0, s>>>(s0p, sz1.p, off.p, nsubp, cmaxp);
@@ -382,7 +414,7 @@ void hv_exact(int n, int m, const double* d_pts, const double* d_ref, double* va
     MB_CUDA(cudaMemcpyAsync(&nsub, nsubp, sizeof(int), cudaMemcpyDeviceToHost, s));
     MB_CUDA(cudaMemcpyAsync(&cmax, cmaxp, sizeof(int), cudaMemcpyDeviceToHost, s));
     MB_CUDA(cudaStreamSynchronize(s));
-    DevScratch<double> sub(nsub), term(s0);
+    DevScratch<double> sub(10, nsub), term(11, s0);
     // 3. warp subtasks; arena per warp: sets on the recursion path + scratch
     int dev = 0, sms = 148;
     MB_CUDA(cudaGetDevice(&dev));
@@ -392,10 +424,12 @@ void hv_exact(int n, int m, const double* d_pts, const double* d_ref, double* va
     int blocks = std::max(1, std::min(sms * 4, (nsub + kSubWarps - 1) / kSubWarps));
     for (int attempt = 0; attempt < 2; ++attempt) {
         const long warps = (long)blocks * kSubWarps;
-        DevScratch<double> arena((size_t)(cap > 0 ? cap : 1) * warps);
-        DevScratch<HvFrame> frames((size_t)warps * (cmax + 1));
+        DevScratch<double> arena(12, (size_t)(cap > 0 ? cap : 1) * warps);
+        DevScratch<HvFrame> frames(13, (size_t)warps * (cmax + 1));
         MB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * 2, s));
-        k_hv_sub<<<blocks, kSubWarps * 32, 0, s>>>(L1.p, s0p, sz1.p, off.p, nsubp, m, d_ref, arena.p, cap,
+        auto sub_kernel = m == 3 ? k_hv_sub<3> : m == 4 ? k_hv_sub<4> : m == 5 ? k_hv_sub<5> : m == 6 ? k_hv_sub<6>
+                        : m == 7 ? k_hv_sub<7> : k_hv_sub<8>;
+        sub_kernel<<<blocks, kSubWarps * 32, 0, s>>>(L1.p, s0p, sz1.p, off.p, nsubp, m, d_ref, arena.p, cap,
                                                     frames.p, cmax + 1, ctr, sub.p, ovf);
         MB_LAUNCH();
         int of = 0;
