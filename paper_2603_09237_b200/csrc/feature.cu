@@ -3,7 +3,7 @@
 // tiny (K = 128 rows, widths of a few hundred) and sits on the critical path
 // of every minibatch, so the limit is L2 latency, not bandwidth or flops:
 // every contraction is one launch of k_dense16, a 16 x 16 output tile per
-// CTA (>= 128 CTAs per layer) that stages its whole K extent (in 128-wide
+// CTA (>= 128 CTAs per layer) that stages its whole K extent (in 256-wide
 // slices) of both operands in shared memory with one round of loads, then
 // one FMA chain per thread. fp32 throughout.
 //   forward : per layer Y = tanh(X W^T + b); the last layer also writes the
@@ -18,7 +18,7 @@
 namespace mb200 {
 
 namespace {
-constexpr int KC = 128;  // K slice staged per round
+constexpr int KC = 256;  // K slice staged per round
 
 struct Dense16 {
     const float* A;  // A(r, k) = A[r * ar + k * ak]
@@ -38,38 +38,57 @@ struct Dense16 {
     int img_r0, img_rn; // rows [img_r0, img_r0 + img_rn) go to the image
 };
 
-__device__ void dense16_tile(const Dense16& d, int bx, int by, float (*As)[KC + 1], float (*Bs)[KC + 1]) {
+// 16 rows x kn (<= KC) of one operand into smem, all 16 loads in flight
+// before the stores; k-fast thread mapping when k is the unit-stride index
+// (coalesced), row-fast when the row is (the transposed operands of dW)
+__device__ __forceinline__ void stage16(const float* __restrict__ P, long pr, long pk, int r0, int rlim, int k0,
+                                        int kn, int ones_row, float (*S)[KC + 4]) {
+    float v[16];
+    const bool kfast = pk == 1 || pr != 1;
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int rr = kfast ? i : (t & 15), kk = kfast ? t : (t >> 4) + 16 * i;
+        const int r = r0 + rr;
+        float x = 0.f;
+        if (kk < kn) {
+            if (r < rlim) x = P[r * pr + (long)(k0 + kk) * pk];
+            else if (r == ones_row) x = 1.f;
+        }
+        v[i] = x;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int rr = kfast ? i : (t & 15), kk = kfast ? t : (t >> 4) + 16 * i;
+        S[rr][kk] = v[i];
+    }
+}
+
+__device__ void dense16_tile(const Dense16& d, int bx, int by, float (*As)[KC + 4], float (*Bs)[KC + 4]) {
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int r0 = by * 16, c0 = bx * 16;
     const int ncols = d.N + (d.ones_col ? 1 : 0);
-    float acc0 = 0.f, acc1 = 0.f;
+    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
     for (int k0 = 0; k0 < d.K; k0 += KC) {
         const int kn = min(KC, d.K - k0);
-        // 16 rows x kn of each operand: thread t loads k = t % KC.., row = t / KC..
-        for (int e = threadIdx.x; e < 16 * KC; e += 256) {
-            const int rr = e / KC, kk = e % KC;
-            const int r = r0 + rr, c = c0 + rr, k = k0 + kk;
-            float a = 0.f, b = 0.f;
-            if (kk < kn) {
-                if (r < d.R) a = d.A[r * d.ar + k * d.ak];
-                if (c < d.N) b = d.B[c * d.bc + k * d.bk];
-                else if (c == d.N && d.ones_col) b = 1.f;
-            }
-            As[rr][kk] = a;
-            Bs[rr][kk] = b;
-        }
+        stage16(d.A, d.ar, d.ak, r0, d.R, k0, kn, -1, As);
+        stage16(d.B, d.bc, d.bk, c0, d.N, k0, kn, d.ones_col ? d.N : -1, Bs);
         __syncthreads();
-        int kk = 0;
-        for (; kk + 2 <= kn; kk += 2) {
-            acc0 = fmaf(As[ty][kk], Bs[tx][kk], acc0);
-            acc1 = fmaf(As[ty][kk + 1], Bs[tx][kk + 1], acc1);
+        const float4* a4 = reinterpret_cast<const float4*>(As[ty]);
+        const float4* b4 = reinterpret_cast<const float4*>(Bs[tx]);
+        for (int q = 0; q < (kn + 3) / 4; ++q) {  // zero-filled past kn
+            const float4 a = a4[q], b = b4[q];
+            acc0 = fmaf(a.x, b.x, acc0);
+            acc1 = fmaf(a.y, b.y, acc1);
+            acc2 = fmaf(a.z, b.z, acc2);
+            acc3 = fmaf(a.w, b.w, acc3);
         }
-        if (kk < kn) acc0 = fmaf(As[ty][kk], Bs[tx][kk], acc0);
         __syncthreads();
     }
+    const float acc = (acc0 + acc1) + (acc2 + acc3);
     const int r = r0 + ty, c = c0 + tx;
     if (r >= d.R || c >= ncols) return;
-    float v = acc0 + acc1;
+    float v = acc;
     if (c == d.N) {  // ones column: row sums of A (bias gradients)
         d.Cb[r] = v;
         return;
@@ -87,8 +106,8 @@ __device__ void dense16_tile(const Dense16& d, int bx, int by, float (*As)[KC + 
 }
 
 __global__ void __launch_bounds__(256) k_dense16(Dense16 d) {
-    __shared__ float As[16][KC + 1];
-    __shared__ float Bs[16][KC + 1];
+    __shared__ __align__(16) float As[16][KC + 4];
+    __shared__ __align__(16) float Bs[16][KC + 4];
     dense16_tile(d, blockIdx.x, blockIdx.y, As, Bs);
 }
 
@@ -100,8 +119,8 @@ struct DenseBatch {
     int nx[4] = {1, 1, 1, 1};
 };
 __global__ void __launch_bounds__(256) k_dense16_multi(const __grid_constant__ DenseBatch b) {
-    __shared__ float As[16][KC + 1];
-    __shared__ float Bs[16][KC + 1];
+    __shared__ __align__(16) float As[16][KC + 4];
+    __shared__ __align__(16) float Bs[16][KC + 4];
     const int t = blockIdx.x;
     int k = 0;
     while (k + 1 < b.n && t >= b.base[k + 1]) ++k;

@@ -14,6 +14,8 @@ struct GroupPolicy {
     float* out_pad = nullptr;  // [G*Rp][16] output layer (pre-squash means)
     int* rowmap = nullptr;     // padded row -> input row (-1 = padding)
     int* goff = nullptr;       // group row offsets (g * Rp)
+    cudaStream_t s2 = nullptr;  // side stream: the observation image while theta is generated
+    cudaEvent_t ev_in = nullptr, ev_x = nullptr;
     GroupPolicy(int m, int F, const std::vector<int>& fh, const std::vector<int>& sizes, bool out_tanh,
                 bool has_log_std, int G, int R);
     ~GroupPolicy();
