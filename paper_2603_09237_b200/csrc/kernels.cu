@@ -807,11 +807,13 @@ void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, floa
 // the next theta-generation and df GEMMs. 4 parameters per thread; m_lo and
 // F are multiples of 4 so a quad never straddles an 8-column image group.
 __global__ void k_adam_img(long n4, float4* p, const float4* g, float4* m1, float4* m2, float lr, float ibc1,
-                           float ibc2, const int* err, long m_lo, long m_hi, int F, Img mimg, long n) {
+                           float ibc2, const int* err, long m_lo, long m_hi, int F, Img mimg, long n, long hole_lo,
+                           long hole_len) {
     if (*err) return;
-    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (i >= n4) {  // the n % 4 scalar tail (never inside the M block: it ends at b, after M)
-        const long e = 4 * n4 + (i - n4);
+        long e = 4 * n4 + (i - n4);
+        if (e >= hole_lo) e += hole_len;
         if (i - n4 < 4 && e < n) {
             float* ps = reinterpret_cast<float*>(p);
             const float* gs = reinterpret_cast<const float*>(g);
@@ -823,6 +825,7 @@ __global__ void k_adam_img(long n4, float4* p, const float4* g, float4* m1, floa
         }
         return;
     }
+    if (4 * i >= hole_lo) i += hole_len / 4;  // the skipped range (4-aligned)
     float4 pp = p[i], gg = g[i], a = m1[i], b = m2[i];
     float* P = &pp.x;
     const float* G = &gg.x;
@@ -847,13 +850,16 @@ __global__ void k_adam_img(long n4, float4* p, const float4* g, float4* m1, floa
     }
 }
 void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2, const int* err,
-              long m_lo, int F, const Img& mimg, cudaStream_t s) {
+              long m_lo, int F, const Img& mimg, cudaStream_t s, long hole_lo, long hole_len) {
     const long m_hi = m_lo + (long)mimg.R * F;
     if (m_lo % 4 || F % 8) throw ShapeError("adam_img: M block must be 4-aligned with F % 8 == 0");
+    if (hole_lo % 4 || hole_len % 4 || hole_len < 0 || (hole_len && mimg.R))
+        throw ShapeError("adam_img: the skipped range must be 4-aligned (and excludes the image)");
+    n -= hole_len;  // elements updated
     const long n4 = n / 4, threads = n4 + (n - 4 * n4);
     k_adam_img<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(n4, (float4*)p, (const float4*)g, (float4*)m1,
                                                                 (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi,
-                                                                F, mimg, n);
+                                                                F, mimg, n, hole_lo, hole_len);
     MB_LAUNCH();
 }
 

@@ -139,8 +139,21 @@ struct HeadArgs {
     double* loss_rows = nullptr;
 };
 void head(const HeadArgs& a, bool actor, cudaStream_t s);
+// Adam over n elements (minus the 4-aligned range [hole_lo, hole_lo + hole_len),
+// left untouched); elements in the M block [m_lo, m_lo + mimg.R * F) also
+// refresh the bf16 image
 void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2, const int* err,
-              long m_lo, int F, const Img& mimg, cudaStream_t s);
+              long m_lo, int F, const Img& mimg, cudaStream_t s, long hole_lo = 0, long hole_len = 0);
+// dM = gtheta^T f consumed in registers by Adam on the M block (dm_adam.cu)
+struct DmAdam {
+    Img gimg, fimg;        // gtheta (rows g, cols p), f (rows g, cols f)
+    int G = 0, P = 0, F = 0;
+    float *p = nullptr, *m1 = nullptr, *m2 = nullptr;  // M block [P][F] fp32
+    Img mimg;              // bf16 image of M (rows p, cols f)
+    float lr = 0.f, ibc1 = 0.f, ibc2 = 0.f;
+    const int* err = nullptr;
+};
+void dm_adam(const DmAdam& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- env (K1)
 void env_reset(int kind, int N, float* state, uint64_t* keys, uint64_t* ctrs, int* steps,

@@ -28,47 +28,87 @@ __global__ void k_unpad(const float* __restrict__ src, int ld, int R, int Rp, in
     const long g = row / R, r = row - g * R;
     dst[e] = src[(g * Rp + r) * ld + j];
 }
-// output layer on the CUDA cores (OUT <= 16 outputs: too narrow for a
-// 128-wide MMA tile): one 128-row tile of one group per block, W_L (fp32,
-// from theta) in shared memory, the last hidden activation row from its bf16
-// image; writes the unpadded pre-squash means directly
-template <int OUT>
+// output layer (OUT <= 16 outputs: too narrow for a 128-wide tcgen05 tile)
+// on mma.sync m16n8k16: one 128-row tile of one group per 4-warp block, each
+// warp two 16-row m-tiles; A fragments straight from the bf16 image (one
+// 8 x 16 B core matrix = one coalesced 128 B warp load per fragment pair),
+// W_L (bf16-rounded from theta, as the weight image) staged in shared memory in
+// fragment order; writes the unpadded pre-squash means plus bias directly
+template <int NT>
 __global__ void __launch_bounds__(128) k_out_forward(const float* __restrict__ theta, long ld, long woff, long boff,
-                                                     int H, Img A, int R, int Rp, float* __restrict__ pre) {
-    __shared__ __align__(16) float sw[OUT * 256];
-    __shared__ float sb[OUT];
-    const int q = blockIdx.x * 128 + threadIdx.x;
-    const int g = (blockIdx.x * 128) / Rp, r = q - g * Rp;
+                                                     int H, Img A, int R, int Rp, int OUT, float* __restrict__ pre) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile_r = blockIdx.x * 128;
+    const int g = tile_r / Rp;
     const float* th = theta + (long)g * ld;
-    for (int e = threadIdx.x; e < OUT * H; e += 128) sw[e] = th[woff + e];
-    if (threadIdx.x < OUT) sb[threadIdx.x] = th[boff + threadIdx.x];
-    __syncthreads();
-    if (r >= R) return;
-    const int CT = img_ct(A.C);
-    float o[OUT];
-#pragma unroll
-    for (int j = 0; j < OUT; ++j) o[j] = sb[j];
-    for (int c = 0; c < H; c += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(A.p + img_off(q, c, CT));
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-        float x[8];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(b2[e]);
-            x[2 * e] = f.x;
-            x[2 * e + 1] = f.y;
+    const int KS = H >> 4, kq = 2 * (lane & 3), rq = lane >> 2;
+    // W_L fragments in mma order: sb[s][j][lane] = {k pair, k pair + 8} of row n
+    __shared__ uint2 sb[16][NT][32];
+    for (int e = threadIdx.x; e < KS * NT * 32; e += 128) {
+        const int l = e & 31, j = (e >> 5) % NT, st = e / (32 * NT);
+        const int n = j * 8 + (l >> 2), k = st * 16 + 2 * (l & 3);
+        float2 lo = make_float2(0.f, 0.f), hi = lo;
+        if (n < OUT) {
+            const float* w = th + woff + (long)n * H + k;
+            lo = make_float2(w[0], w[1]);
+            hi = make_float2(w[8], w[9]);
         }
+        const __nv_bfloat162 l2 = __float22bfloat162_rn(lo), h2 = __float22bfloat162_rn(hi);
+        sb[st][j][l] = make_uint2(*reinterpret_cast<const uint32_t*>(&l2), *reinterpret_cast<const uint32_t*>(&h2));
+    }
+    float bias[NT][2];
 #pragma unroll
-        for (int j = 0; j < OUT; ++j) {
-            const float4 w0 = *reinterpret_cast<const float4*>(sw + j * H + c);
-            const float4 w1 = *reinterpret_cast<const float4*>(sw + j * H + c + 4);
-            o[j] = fmaf(x[0], w0.x, fmaf(x[1], w0.y, fmaf(x[2], w0.z, fmaf(x[3], w0.w, o[j]))));
-            o[j] = fmaf(x[4], w1.x, fmaf(x[5], w1.y, fmaf(x[6], w1.z, fmaf(x[7], w1.w, o[j]))));
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int n = j * 8 + kq + e;
+            bias[j][e] = n < OUT ? th[boff + n] : 0.f;
+        }
+    const int CT = img_ct(A.C);
+    __syncthreads();
+#pragma unroll 1
+    for (int mt = 0; mt < 2; ++mt) {
+        const int row = tile_r + warp * 32 + mt * 16 + rq;  // and row + 8
+        uint32_t af[16][4];
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            if (s < KS) {
+                const uint8_t* p0 = A.p + img_off(row, s * 16, CT) + kq * 2;
+                const uint8_t* p1 = A.p + img_off(row, s * 16 + 8, CT) + kq * 2;
+                af[s][0] = *reinterpret_cast<const uint32_t*>(p0);
+                af[s][1] = *reinterpret_cast<const uint32_t*>(p0 + 2048);  // row + 8: next core-matrix row group
+                af[s][2] = *reinterpret_cast<const uint32_t*>(p1);
+                af[s][3] = *reinterpret_cast<const uint32_t*>(p1 + 2048);
+            }
+        float c[NT][4];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            if (s < KS)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    const uint2 b = sb[s][j][lane];
+                    asm volatile(
+                        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+                        "{%8,%9}, {%0,%1,%2,%3};\n"
+                        : "+f"(c[j][0]), "+f"(c[j][1]), "+f"(c[j][2]), "+f"(c[j][3])
+                        : "r"(af[s][0]), "r"(af[s][1]), "r"(af[s][2]), "r"(af[s][3]), "r"(b.x), "r"(b.y));
+                }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = row + 8 * h - g * Rp;
+            if (r >= R) continue;
+            float* dst = pre + ((long)g * R + r) * OUT;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int n = j * 8 + kq + e;
+                    if (n < OUT) dst[n] = c[j][2 * h + e] + bias[j][e];
+                }
         }
     }
-    float* dst = pre + ((long)g * R + r) * OUT;
-#pragma unroll
-    for (int j = 0; j < OUT; ++j) dst[j] = o[j];
 }
 
 // group-padded row map: q = g*Rp + r -> g*R + r (r < R), -1 for padding
@@ -135,8 +175,8 @@ void GroupPolicy::forward(const float* d_w, const float* d_obs, float* d_pre, cu
     h.forward(d_w, 0, G, s);                                    // theta + per-layer weight images
     MB_CUDA(cudaStreamWaitEvent(s, ev_x, 0));
     const int H = nd.sz[nd.L - 1], out = nd.sz[nd.L];
-    const bool simt_out = nd.L >= 2 && H % 8 == 0 && H <= 256 && out <= 16;
-    for (int l = 0; l < nd.L - (simt_out ? 1 : 0); ++l) {
+    const bool mma_out = nd.L >= 2 && H % 16 == 0 && H <= 256 && out <= 16;
+    for (int l = 0; l < nd.L - (mma_out ? 1 : 0); ++l) {
         const bool last = l == nd.L - 1;
         IGemm d;
         d.A = l == 0 ? X : A[l - 1]; d.a_view = 0;
@@ -151,17 +191,14 @@ void GroupPolicy::forward(const float* d_w, const float* d_obs, float* d_pre, cu
         }
         img_gemm(d, s);
     }
-    if (simt_out) {
+    if (mma_out) {
         const long woff = nd.woff[nd.L - 1], boff = nd.boff[nd.L - 1];
         const Img& a = A[nd.L - 2];
         const unsigned tiles = (unsigned)((long)G * Rp / 128);
-#define MB_OUT(O) \
-    case O: k_out_forward<O><<<tiles, 128, 0, s>>>(h.theta, h.ld, woff, boff, H, a, R, Rp, d_pre); break;
-        switch (out) {
-            MB_OUT(1) MB_OUT(2) MB_OUT(3) MB_OUT(4) MB_OUT(5) MB_OUT(6) MB_OUT(7) MB_OUT(8)
-            MB_OUT(9) MB_OUT(10) MB_OUT(11) MB_OUT(12) MB_OUT(13) MB_OUT(14) MB_OUT(15) MB_OUT(16)
-        }
-#undef MB_OUT
+        if (out <= 8)
+            k_out_forward<1><<<tiles, 128, 0, s>>>(h.theta, h.ld, woff, boff, H, a, R, Rp, out, d_pre);
+        else
+            k_out_forward<2><<<tiles, 128, 0, s>>>(h.theta, h.ld, woff, boff, H, a, R, Rp, out, d_pre);
         MB_LAUNCH();
         return;
     }

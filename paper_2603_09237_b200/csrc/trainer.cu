@@ -394,17 +394,32 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
     {
         IGemm ds[2];
         double fl = 0;
+        int nd = 0;
         for (int k = 0; k < nh; ++k) {
             HyperNet& h = *hs[k];
-            IGemm& d = ds[k];  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
+            if (h.adam_fused) continue;
+            IGemm& d = ds[nd++];  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
             d.A = h.gimg; d.a_view = 1;  // (m = p, k = g)
             d.B = h.fimg; d.b_view = 1;  // (n = f, k = g)
             d.M = (int)h.P; d.N = h.F; d.K = h.fng;
             d.C = h.g + h.nf; d.cm = h.F; d.cn = 1;
             fl += 2.0 * d.M * d.N * d.K;
         }
-        ProfScope ps("hyper_dM", fl, 0, s);
-        img_gemm_batch(ds, nh, s);
+        if (nd) {
+            ProfScope ps("hyper_dM", fl, 0, s);
+            img_gemm_batch(ds, nd, s);
+        }
+    }
+    for (int k = 0; k < nh; ++k) {  // single rank: dM consumed by Adam in registers (dm_adam.cu)
+        HyperNet& h = *hs[k];
+        if (!h.adam_fused) continue;
+        DmAdam a;
+        a.gimg = h.gimg; a.fimg = h.fimg; a.G = h.fng; a.P = (int)h.P; a.F = h.F;
+        a.p = h.p + h.nf; a.m1 = h.m1 + h.nf; a.m2 = h.m2 + h.nf; a.mimg = h.mimg;
+        a.lr = h.ad_lr; a.ibc1 = h.ad_ibc1; a.ibc2 = h.ad_ibc2; a.err = h.ad_err;
+        // HBM-bound: p, m1, m2 in + out (fp32), M image out (bf16), gtheta image in
+        ProfScope ps("dm_adam", 0, 26.0 * h.P * h.F + 2.0 * h.P * h.fng, s);
+        dm_adam(a, s);
     }
     {  // df reduction + feature-map backward (all layers' dW, db) over the local rows
         double fl = 0;
@@ -422,9 +437,30 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
     }
 }
 
+void HyperNet::adam_begin(double lr, const int* err) {
+    for (long& st : steps) ++st;
+    const double bc1 = 1.0 - std::pow(0.9, (double)steps[0]);
+    const double bc2 = 1.0 - std::pow(0.999, (double)steps[0]);
+    ad_lr = (float)lr;
+    ad_ibc1 = 1.f / (float)bc1;  // as adam_img
+    ad_ibc2 = 1.f / (float)bc2;
+    ad_err = err;
+    adam_fused = true;
+}
+
 void HyperNet::adam_step(double lr, const int* err, cudaStream_t s) {
     // three blocks (feature, M, b) with their own step counters (train.cpp:28-39);
     // they always advance together, so one launch covers the flat vector.
+    if (adam_fused) {  // M was updated in the dM epilogue: the feature and b blocks remain
+        adam_fused = false;
+        const double bc1 = 1.0 - std::pow(0.9, (double)steps[0]);
+        const double bc2 = 1.0 - std::pow(0.999, (double)steps[0]);
+        const long b0 = nf + P * F;
+        ProfScope ps("adam", 0, 28.0 * (nf + P), s);
+        Img none;
+        adam_img(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, 0, F, none, s, nf, b0 - nf);
+        return;
+    }
     for (long& st : steps) ++st;
     const double bc1 = 1.0 - std::pow(0.9, (double)steps[0]);
     const double bc2 = 1.0 - std::pow(0.999, (double)steps[0]);
@@ -1027,6 +1063,10 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         return !(e && e[0] == '1');
     }();
     cudaStream_t sc = two ? s2_ : s_;
+    const char* fe = std::getenv("MORLAX_FUSED_ADAM");  // "0": the unfused dM GEMM + Adam (A/B, tests)
+    const bool fuse_env = !(fe && fe[0] == '0');
+    // no gradient exchange between backward and Adam; dm_adam's tile shape
+    const bool fuse = fuse_env && !comm_ && actor_.F % 64 == 0 && critic_.F % 64 == 0 && Kl_ <= 128;
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
     if (Bp > 0) {
         MbGather ga;
@@ -1043,6 +1083,10 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         net_step(both, roles, 2, Bp, inv_B, maxg, rows, goff, slot, s_);
         if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
         check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
+        if (fuse) {
+            actor_.adam_begin(cfg_.actor_lr, d_err);
+            critic_.adam_begin(cfg_.critic_lr, d_err);
+        }
         HyperNet::backward_multi(both, 2, s_);
         allreduce_grad(actor_, s_);
         allreduce_grad(critic_, s_);
@@ -1063,6 +1107,10 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
     MB_CUDA(cudaEventRecord(ev_chk_, s_));
     MB_CUDA(cudaStreamWaitEvent(sc, ev_chk_, 0));
+    if (fuse) {
+        actor_.adam_begin(cfg_.actor_lr, d_err);
+        critic_.adam_begin(cfg_.critic_lr, d_err);
+    }
     critic_.backward(sc);
     if (comm_) {  // every NCCL call goes on s_: one stream per communicator, device order = host order
         MB_CUDA(cudaEventRecord(ev_cb_, sc));

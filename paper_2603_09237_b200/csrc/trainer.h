@@ -91,6 +91,13 @@ struct HyperNet {
     // grads from gtheta [G][P] (all groups) -> g
     void backward(cudaStream_t s);
     void adam_step(double lr, const int* err, cudaStream_t s);
+    // fused update (single rank, no gradient exchange): called before
+    // backward, which then applies Adam to the M block inside the dM GEMM
+    // epilogue (dM is never stored); adam_step finishes the feature / b blocks
+    void adam_begin(double lr, const int* err);
+    bool adam_fused = false;
+    float ad_lr = 0.f, ad_ibc1 = 0.f, ad_ibc2 = 0.f;
+    const int* ad_err = nullptr;
 };
 
 NetDims make_dims(const std::vector<int>& sizes, bool out_tanh, bool has_log_std);

@@ -275,8 +275,12 @@ def test_rollout_and_advantages_parity(mb, o, env):
         assert_normwise(t.get(name), b[key], REL_CHAIN, what=name)
 
 
-def test_full_iteration_parity(mb, o):
-    c = _tiny(N=32, K=4, T=16, epochs=2, minibatch_count=2, F=16, feat_hidden=[16],
+@pytest.mark.parametrize("F,fused", [(16, "1"), (64, "1"), (64, "0")])
+def test_full_iteration_parity(mb, o, monkeypatch, F, fused):
+    """F = 64 takes the single-rank fused dM + Adam kernel (dm_adam.cu) unless
+    MORLAX_FUSED_ADAM=0 (the tcgen05 dM GEMM + separate Adam)."""
+    monkeypatch.setenv("MORLAX_FUSED_ADAM", fused)
+    c = _tiny(N=32, K=4, T=16, epochs=2, minibatch_count=2, F=F, feat_hidden=[16],
               actor_hidden=[32, 32], critic_hidden=[32, 32])
     t = mb.Trainer(_mbcfg(mb, c))
     ot = OracleTrainer(o, c)
@@ -298,8 +302,9 @@ def test_full_iteration_parity(mb, o):
         assert err.max() <= 2.5 * lr * 4, which
 
 
-def test_iteration_is_deterministic(mb):
-    c = _tiny(N=32, K=4, T=16)
+@pytest.mark.parametrize("F", [8, 64])
+def test_iteration_is_deterministic(mb, F):
+    c = _tiny(N=32, K=4, T=16, F=F)
     t1, t2 = mb.Trainer(_mbcfg(mb, c)), mb.Trainer(_mbcfg(mb, c))
     for it in range(2):
         s1, s2 = t1.iteration(it), t2.iteration(it)
