@@ -532,225 +532,302 @@ void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, co
 // K5 head: the output layer of the generated MLP, the per-row loss and the
 // output layer's backward in one pass over a 128-row tile of one cluster
 // (losses.cpp:87-132 / 165-185 with nn.cpp:60-92, 111-160 for the last
-// layer). The output layer is only act_dim (12) or m (6) wide -- too narrow
-// for the tensor cores -- so it runs on the CUDA cores in fp32 from the
-// fp32 generated weights W_L [out][H] (staged in shared memory):
+// layer):
 //   o      = b_L + W_L a          (a = last hidden activation row, bf16 image)
 //   g      = dloss/do             (actor: clipped surrogate + entropy;
 //                                  critic: 2 e / B)
 //   g_prev = (W_L^T g) * (1 - a^2)  -> bf16 image (input of the dW / dX GEMMs)
 // plus per-tile column sums of g (output bias grads), of the log-std terms
 // and of g_prev (bias grads of the last hidden layer), and the tile's loss.
-// Padded rows (rows[q] < 0) contribute zeros.
+// The output layer is only act_dim / m (<= 16) wide: both contractions run
+// on mma.sync m16n8k16 (bf16 operands, fp32 accumulation; a 16-column MMA
+// is below the tcgen05 minimum tile), each warp owning two 16-row m-tiles.
+// The accumulator fragment of the forward (rows x out) is exactly the A
+// fragment of the backward (rows x K = out), and the forward's A fragments
+// (the activations) are exactly the tanh' operands of the backward's
+// accumulator, so the activations are read once and nothing is staged.
+// W_L (bf16-rounded from the fp32 theta) sits in shared memory in fragment
+// order for both products. Padded rows (rows[q] < 0) contribute zeros.
 // =========================================================================
-// OUT = output width (compile time: the per-row arrays stay in registers)
-template <bool ACTOR, int OUT>
+__device__ __forceinline__ void mma_bf16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t bf2_pack(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ float2 bf2_unpack(uint32_t u) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+}
+
+// NT = n-tiles of the output (out <= 8 * NT)
+template <bool ACTOR, int NT>
 __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
-    __shared__ __align__(16) float sw[16 * 256];
-    __shared__ float sb[16];
-    __shared__ float red[64];
-    __shared__ float red2[4 * 256];
-    const int H = a.H;
-    constexpr int out = OUT;
-    const int q = blockIdx.x * 128 + threadIdx.x;
+    __shared__ uint2 swf[16][NT][32];  // forward B: (k = h pair, n = d) per k-step / n-tile / lane
+    __shared__ uint2 swb[32][32];      // backward B: (k = d pair, n = h) per h n-tile / lane
+    __shared__ float sb[16], red[4][16], redl[4][16];
+    __shared__ float red2[4][256];
+    const int H = a.H, out = a.out, KS = H >> 4, HT = H >> 3;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, rq = lane >> 2, q = lane & 3;
     const int z = a.rg[blockIdx.x * 128];  // groups are 128-row padded: one cluster per tile
     const float* th = a.theta + (long)z * a.ld;
-    for (int e = threadIdx.x; e < out * H; e += 128) sw[e] = th[a.woff + e];
-    if (threadIdx.x < out) sb[threadIdx.x] = th[a.boff + threadIdx.x];
+    const float* W = th + a.woff;  // W_L [out][H] fp32
+    for (int e = threadIdx.x; e < KS * NT * 32; e += 128) {
+        const int l = e & 31, j = (e >> 5) % NT, st = e / (32 * NT);
+        const int n = j * 8 + (l >> 2), k = st * 16 + 2 * (l & 3);
+        float w0 = 0.f, w1 = 0.f, w8 = 0.f, w9 = 0.f;
+        if (n < out) {
+            w0 = W[(long)n * H + k]; w1 = W[(long)n * H + k + 1];
+            w8 = W[(long)n * H + k + 8]; w9 = W[(long)n * H + k + 9];
+        }
+        swf[st][j][l] = make_uint2(bf2_pack(w0, w1), bf2_pack(w8, w9));
+    }
+    for (int e = threadIdx.x; e < HT * 32; e += 128) {
+        const int l = e & 31, nt = e >> 5;
+        const int hcol = nt * 8 + (l >> 2), d = 2 * (l & 3);
+        auto w = [&](int dd) { return dd < out ? W[(long)dd * H + hcol] : 0.f; };
+        swb[nt][l] = make_uint2(bf2_pack(w(d), w(d + 1)), bf2_pack(w(d + 8), w(d + 9)));
+    }
+    __shared__ float sinv[16], smask[16], sconst[2];  // actor: 1 / sigma_d, clamp mask; sum_d lp / entropy terms
+    if (threadIdx.x < 16) {
+        const int d = threadIdx.x;
+        sb[d] = d < out ? th[a.boff + d] : 0.f;
+        if (ACTOR) {
+            const float raw = d < out ? th[a.mlp_n + d] : 0.f;
+            const float ls = fminf(fmaxf(raw, -5.f), 1.f);
+            sinv[d] = d < out ? __expf(-ls) : 0.f;
+            smask[d] = (d < out && raw >= -5.f && raw <= 1.f) ? 1.f : 0.f;
+            float c1 = d < out ? -ls - 0.9189385332046727f : 0.f;
+            float c2 = d < out ? ls + 0.5f * (1.f + 1.8378770664093453f) : 0.f;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {  // fixed-order sums over d (lanes 0-15)
+                c1 += __shfl_xor_sync(0x0000ffffu, c1, o);
+                c2 += __shfl_xor_sync(0x0000ffffu, c2, o);
+            }
+            if (d == 0) {
+                sconst[0] = c1;
+                sconst[1] = c2;
+            }
+        }
+    }
     __syncthreads();
-    const bool live = a.rows[q] >= 0;
     const int CTa = img_ct(a.A.C), CTg = img_ct(a.Gprev.C), CTo = img_ct(a.Gout.C);
-    // ---- forward of the output layer
-    float o[OUT];
+    float cs[NT][2], csl[NT][2];  // this lane's column sums (lanes rq == 0 hold the warp's)
 #pragma unroll
-    for (int j = 0; j < OUT; ++j) o[j] = 0.f;
-    // activation row: 4 16-byte units (32 columns) in flight per step
-    auto fwd8 = [&](const uint4& u, int c) {
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-        float x[8];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(b2[e]);
-            x[2 * e] = f.x;
-            x[2 * e + 1] = f.y;
-        }
-#pragma unroll
-        for (int j = 0; j < OUT; ++j) {
-            const float4 w0 = *reinterpret_cast<const float4*>(sw + j * H + c);
-            const float4 w1 = *reinterpret_cast<const float4*>(sw + j * H + c + 4);
-            o[j] = fmaf(x[0], w0.x, o[j]);
-            o[j] = fmaf(x[1], w0.y, o[j]);
-            o[j] = fmaf(x[2], w0.z, o[j]);
-            o[j] = fmaf(x[3], w0.w, o[j]);
-            o[j] = fmaf(x[4], w1.x, o[j]);
-            o[j] = fmaf(x[5], w1.y, o[j]);
-            o[j] = fmaf(x[6], w1.z, o[j]);
-            o[j] = fmaf(x[7], w1.w, o[j]);
-        }
-    };
-    int c = 0;
-    for (; c + 32 <= H; c += 32) {
-        uint4 u[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, c + 8 * k, CTa));
-#pragma unroll
-        for (int k = 0; k < 4; ++k) fwd8(u[k], c + 8 * k);
-    }
-    for (; c < H; c += 8) fwd8(*reinterpret_cast<const uint4*>(a.A.p + img_off(q, c, CTa)), c);
-    float g[16], gl[16];  // 16: the image / column-sum code below works in 8-wide groups
-#pragma unroll
-    for (int j = 0; j < 16; ++j) g[j] = gl[j] = 0.f;
+    for (int j = 0; j < NT; ++j) cs[j][0] = cs[j][1] = csl[j][0] = csl[j][1] = 0.f;
     double lrow = 0.0;
-    if (live) {
-        if (ACTOR) {  // losses.cpp:87-129 (action_logprob nn.cpp:204-219)
-            const float* ls_raw = th + a.mlp_n;
-            float lp = 0.f, zn[OUT], sig[OUT], ent_h = 0.f;
+#pragma unroll 1
+    for (int mt = 0; mt < 2; ++mt) {
+        const int r0 = blockIdx.x * 128 + warp * 32 + mt * 16 + rq;  // rows r0, r0 + 8
+        uint32_t af[16][4];
 #pragma unroll
-            for (int d = 0; d < OUT; ++d) {
-                const float ls = fminf(fmaxf(ls_raw[d], -5.f), 1.f);
-                sig[d] = __expf(ls);
-                const float zz = a.z[(long)q * out + d];
-                zn[d] = (zz - (o[d] + sb[d])) / sig[d];
-                lp += -0.5f * zn[d] * zn[d] - ls - 0.9189385332046727f;
-                lp -= __logf(sech2_f(zz) + 1e-6f);
-                ent_h += ls + 0.5f * (1.f + 1.8378770664093453f);
+        for (int s = 0; s < 16; ++s)
+            if (s < KS) {
+                const uint8_t* p0 = a.A.p + img_off(r0, s * 16, CTa) + q * 4;
+                const uint8_t* p1 = a.A.p + img_off(r0, s * 16 + 8, CTa) + q * 4;
+                af[s][0] = *reinterpret_cast<const uint32_t*>(p0);
+                af[s][1] = *reinterpret_cast<const uint32_t*>(p0 + 2048);  // row + 8: next core-matrix row group
+                af[s][2] = *reinterpret_cast<const uint32_t*>(p1);
+                af[s][3] = *reinterpret_cast<const uint32_t*>(p1 + 2048);
             }
-            const float ratio = __expf(lp - a.lp_old[q]);
-            if (!isfinite(ratio)) atomicExch(a.err, 3);
-            const float adv = a.sadv[q];
-            const float unc = ratio * adv;
-            const float clp = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip) * adv;
-            lrow = (double)(-fminf(unc, clp) * a.inv_B) - (double)(a.ent * ent_h * a.inv_B);
-            const float glp = unc <= clp ? -ratio * adv * a.inv_B : 0.f;  // losses.cpp:116
+        // per-row loss inputs of this lane's (row, column) slots, in flight under the MMAs
+        bool live[2];
+        float zin[2][NT][2], lpo[2], adv[2];
 #pragma unroll
-            for (int d = 0; d < OUT; ++d) {
-                g[d] = glp * zn[d] / sig[d];
-                const float raw = ls_raw[d];  // clamp mask (losses.cpp:124-128)
-                gl[d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - a.ent * a.inv_B : 0.f;
-            }
-        } else {  // losses.cpp:170-185: sum_k (v - tgt)^2 / B, grad 2 e / B
+        for (int h = 0; h < 2; ++h) {
+            const int r = r0 + 8 * h;
+            live[h] = a.rows[r] >= 0;
+            lpo[h] = ACTOR ? a.lp_old[r] : 0.f;
+            adv[h] = ACTOR ? a.sadv[r] : 0.f;
+            const float* src = ACTOR ? a.z : a.tgt;
 #pragma unroll
-            for (int k = 0; k < OUT; ++k) {
-                const float e = (o[k] + sb[k]) - a.tgt[(long)q * out + k];
-                lrow += (double)e * e * a.inv_B;
-                g[k] = 2.f * e * a.inv_B;
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int d = 8 * j + 2 * q + e;
+                    zin[h][j][e] = d < out ? src[(long)r * out + d] : 0.f;
+                }
+        }
+        // ---- forward of the output layer: c[j] = (rows r0 / r0 + 8, columns 8j + 2q, + 1)
+        float c[NT][4];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            c[j][0] = c[j][2] = sb[8 * j + 2 * q];
+            c[j][1] = c[j][3] = sb[8 * j + 2 * q + 1];
+        }
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            if (s < KS)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    const uint2 b = swf[s][j][lane];
+                    mma_bf16_16816(c[j], af[s][0], af[s][1], af[s][2], af[s][3], b.x, b.y);
+                }
+        // ---- per-row loss and dloss/do (the row's columns are spread over the 4 q-lanes)
+        float g[2][NT][2], gl[2][NT][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const bool lv = live[h];
+            if (ACTOR) {  // losses.cpp:87-129 (action_logprob nn.cpp:204-219)
+                // lp = sum_d [-zn^2 / 2 - ls_d - log sqrt(2 pi) - log(sech^2 z_d + 1e-6)]; the
+                // sigma / entropy terms depend on the cluster only (sconst)
+                float lp = 0.f, zn[NT][2];
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int d = 8 * j + 2 * q + e;
+                        zn[j][e] = 0.f;
+                        if (d < out && lv) {
+                            const float zz = zin[h][j][e];
+                            zn[j][e] = (zz - c[j][2 * h + e]) * sinv[d];
+                            lp += -0.5f * zn[j][e] * zn[j][e] - __logf(sech2_f(zz) + 1e-6f);
+                        }
+                    }
+                lp += __shfl_xor_sync(0xffffffffu, lp, 1);
+                lp += __shfl_xor_sync(0xffffffffu, lp, 2);
+                lp += sconst[0];
+                const float ent_h = sconst[1];
+                float glp = 0.f;
+                if (lv) {
+                    const float ratio = __expf(lp - lpo[h]);
+                    if (!isfinite(ratio)) atomicExch(a.err, 3);
+                    const float unc = ratio * adv[h];
+                    const float clp = fminf(fmaxf(ratio, 1.f - a.clip), 1.f + a.clip) * adv[h];
+                    if (q == 0) lrow += (double)(-fminf(unc, clp) * a.inv_B) - (double)(a.ent * ent_h * a.inv_B);
+                    glp = unc <= clp ? -ratio * adv[h] * a.inv_B : 0.f;  // losses.cpp:116
+                }
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int d = 8 * j + 2 * q + e;
+                        const bool ok = d < out && lv;
+                        g[h][j][e] = ok ? glp * zn[j][e] * sinv[d] : 0.f;
+                        // clamp mask (losses.cpp:124-128)
+                        gl[h][j][e] = ok ? smask[d] * (glp * (zn[j][e] * zn[j][e] - 1.f) - a.ent * a.inv_B) : 0.f;
+                    }
+            } else {  // losses.cpp:170-185: sum_k (v - tgt)^2 / B, grad 2 e / B
+                float sq = 0.f;
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int d = 8 * j + 2 * q + e;
+                        const bool ok = d < out && lv;
+                        const float er = ok ? c[j][2 * h + e] - zin[h][j][e] : 0.f;
+                        sq += er * er;
+                        g[h][j][e] = 2.f * er * a.inv_B;
+                        gl[h][j][e] = 0.f;
+                    }
+                sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+                sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+                if (q == 0 && lv) lrow += (double)sq * a.inv_B;
             }
+        }
+        // ---- output-layer gradient image (dW_L GEMM operand) and its column sums
+        uint32_t ga[2][2];  // backward A fragment: (row h, k = 8j + 2q pair)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                ga[j][h] = j < NT ? bf2_pack(g[h][j < NT ? j : 0][0], g[h][j < NT ? j : 0][1]) : 0u;
+                if (j < NT) *reinterpret_cast<uint32_t*>(a.Gout.p + img_off(r0 + 8 * h, 8 * j + 2 * q, CTo)) = ga[j][h];
+            }
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                float x = g[0][j][e] + g[1][j][e], y = gl[0][j][e] + gl[1][j][e];
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) {
+                    x += __shfl_xor_sync(0xffffffffu, x, o);
+                    if (ACTOR) y += __shfl_xor_sync(0xffffffffu, y, o);
+                }
+                cs[j][e] += x;
+                csl[j][e] += y;
+            }
+        // ---- backward: (rows x out) g times W_L -> (rows x H), times tanh'(a);
+        // groups of 4 n-tiles (32 columns): this lane's 8 row-pair sums are
+        // reduce-scattered over the 8 lanes sharing q (xor 16, 8, 4: 7 shuffles),
+        // leaving lane (rq, q) with the warp's sum of column 8 (rq >> 1) + 2q + (rq & 1)
+        uint8_t* gp0 = a.Gprev.p + img_off(r0, 2 * q, CTg);  // + 128 B per n-tile, + 32 KB per 128 columns
+#pragma unroll
+        for (int n4 = 0; n4 < 8; ++n4) {
+            if (4 * n4 >= HT) break;
+            float cs8[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int nt = 4 * n4 + u;
+                const uint2 b = swb[nt][lane];
+                float v[4] = {0.f, 0.f, 0.f, 0.f};
+                mma_bf16_16816(v, ga[0][0], ga[0][1], ga[1][0], ga[1][1], b.x, b.y);
+                // activations at (rows r0 / r0 + 8, columns 8 nt + 2q, + 1): the forward's A fragments
+                const float2 x0 = bf2_unpack(af[nt >> 1][(nt & 1) ? 2 : 0]);
+                const float2 x1 = bf2_unpack(af[nt >> 1][(nt & 1) ? 3 : 1]);
+                v[0] *= 1.f - x0.x * x0.x;
+                v[1] *= 1.f - x0.y * x0.y;
+                v[2] *= 1.f - x1.x * x1.x;
+                v[3] *= 1.f - x1.y * x1.y;
+                uint8_t* gp = gp0 + (nt >> 4) * 32768 + (nt & 15) * 128;
+                *reinterpret_cast<uint32_t*>(gp) = bf2_pack(v[0], v[1]);
+                *reinterpret_cast<uint32_t*>(gp + 2048) = bf2_pack(v[2], v[3]);
+                cs8[2 * u] = v[0] + v[2];
+                cs8[2 * u + 1] = v[1] + v[3];
+            }
+            // slot k = 2u + e (column 8 (4 n4 + u) + 2q + e); halve the slots per step
+#pragma unroll
+            for (int w = 4; w >= 1; w >>= 1) {
+                const int bit = w == 4 ? 16 : w == 2 ? 8 : 4;  // lane bit paired at this step
+                const bool up = (lane & bit) != 0;
+#pragma unroll
+                for (int i = 0; i < w; ++i) {
+                    const float mine = up ? cs8[w + i] : cs8[i];
+                    const float other = up ? cs8[i] : cs8[w + i];
+                    cs8[i] = mine + __shfl_xor_sync(0xffffffffu, other, bit);
+                }
+            }
+            // lane keeps slot k = 4 (lane>>4 & 1) + 2 (lane>>3 & 1) + (lane>>2 & 1) = rq bit-reversed
+            const int k = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+            const int col = 8 * (4 * n4 + (k >> 1)) + 2 * q + (k & 1);
+            if (mt == 0) red2[warp][col] = cs8[0];
+            else red2[warp][col] += cs8[0];
         }
     }
-    tile_sum_f64(lrow, a.loss_rows + blockIdx.x);
-    for (int h = 0; h < (out + 7) / 8; ++h) {  // output-layer gradient image (dW_L GEMM operand)
-        uint4 w;
-        w.x = umma::pack_bf16(g[8 * h + 0], g[8 * h + 1]);
-        w.y = umma::pack_bf16(g[8 * h + 2], g[8 * h + 3]);
-        w.z = umma::pack_bf16(g[8 * h + 4], g[8 * h + 5]);
-        w.w = umma::pack_bf16(g[8 * h + 6], g[8 * h + 7]);
-        *reinterpret_cast<uint4*>(a.Gout.p + img_off(q, 8 * h, CTo)) = w;
+    if (rq == 0)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                red[warp][8 * j + 2 * q + e] = cs[j][e];
+                redl[warp][8 * j + 2 * q + e] = csl[j][e];
+            }
+    tile_sum_f64(lrow, a.loss_rows + blockIdx.x);  // includes a __syncthreads
+    if (threadIdx.x < out) {
+        const int d = threadIdx.x;
+        a.psum[blockIdx.x * 16 + d] = (red[0][d] + red[1][d]) + (red[2][d] + red[3][d]);
+        if (ACTOR) a.psls[blockIdx.x * 16 + d] = (redl[0][d] + redl[1][d]) + (redl[2][d] + redl[3][d]);
     }
-    {  // per-tile column sums of the output gradient (bias) and the log-std terms, fixed order
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int d = 0; d < OUT; ++d) {
-            float x1 = g[d], x2 = gl[d];
-#pragma unroll
-            for (int k = 16; k > 0; k >>= 1) {
-                x1 += __shfl_xor_sync(0xffffffffu, x1, k);
-                if (ACTOR) x2 += __shfl_xor_sync(0xffffffffu, x2, k);
-            }
-            if (lane == 0) {
-                red[warp * 16 + d] = x1;
-                if (ACTOR) red2[warp * 16 + d] = x2;  // red2 is free until the backward below
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < OUT) {
-            a.psum[blockIdx.x * 16 + threadIdx.x] =
-                red[threadIdx.x] + red[16 + threadIdx.x] + red[32 + threadIdx.x] + red[48 + threadIdx.x];
-            if (ACTOR)
-                a.psls[blockIdx.x * 16 + threadIdx.x] =
-                    red2[threadIdx.x] + red2[16 + threadIdx.x] + red2[32 + threadIdx.x] + red2[48 + threadIdx.x];
-        }
-        __syncthreads();
-    }
-    // ---- backward of the output layer into the last hidden layer
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint4 nxt[2];
-    nxt[0] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, 0, CTa));
-    nxt[1] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, 8, CTa));
-    for (int c = 0; c < H; c += 16) {
-        const uint4 cur[2] = {nxt[0], nxt[1]};
-        if (c + 16 < H) {  // next 16 columns' activations load under this step's FMAs
-            nxt[0] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, c + 16, CTa));
-            nxt[1] = *reinterpret_cast<const uint4*>(a.A.p + img_off(q, c + 24, CTa));
-        }
-        float v[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = 0.f;
-#pragma unroll
-        for (int j = 0; j < OUT; ++j) {  // W_L^T g: rows of W_L as float4 broadcasts
-            const float4* w4 = reinterpret_cast<const float4*>(sw + j * H + c);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float4 w = w4[k];
-                v[4 * k + 0] = fmaf(g[j], w.x, v[4 * k + 0]);
-                v[4 * k + 1] = fmaf(g[j], w.y, v[4 * k + 1]);
-                v[4 * k + 2] = fmaf(g[j], w.z, v[4 * k + 2]);
-                v[4 * k + 3] = fmaf(g[j], w.w, v[4 * k + 3]);
-            }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&cur[hh]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(b2[e]);
-                v[8 * hh + 2 * e] *= 1.f - f.x * f.x;
-                v[8 * hh + 2 * e + 1] *= 1.f - f.y * f.y;
-            }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            uint4 w;
-            w.x = umma::pack_bf16(v[8 * hh + 0], v[8 * hh + 1]);
-            w.y = umma::pack_bf16(v[8 * hh + 2], v[8 * hh + 3]);
-            w.z = umma::pack_bf16(v[8 * hh + 4], v[8 * hh + 5]);
-            w.w = umma::pack_bf16(v[8 * hh + 6], v[8 * hh + 7]);
-            *reinterpret_cast<uint4*>(a.Gprev.p + img_off(q, c + 8 * hh, CTg)) = w;
-        }
-        // warp reduce-scatter of 16 columns over 32 rows (deterministic order)
-        int col = 0;
-#pragma unroll
-        for (int w = 8; w >= 1; w >>= 1) {
-            const bool up = (lane & (2 * w)) != 0;
-            col += up ? w : 0;
-#pragma unroll
-            for (int i = 0; i < w; ++i) {
-                const float mine = up ? v[w + i] : v[i];
-                const float other = up ? v[i] : v[w + i];
-                v[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * w);
-            }
-        }
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-        if ((lane & 1) == 0) red2[warp * 256 + c + col] = v[0];
-    }
-    __syncthreads();
     for (int j = threadIdx.x; j < H; j += 128)
-        a.psum_prev[(long)blockIdx.x * a.psum_prev_ld + j] =
-            (red2[j] + red2[256 + j]) + (red2[512 + j] + red2[768 + j]);
+        a.psum_prev[(long)blockIdx.x * a.psum_prev_ld + j] = (red2[0][j] + red2[1][j]) + (red2[2][j] + red2[3][j]);
 }
 void head(const HeadArgs& a, bool actor, cudaStream_t s) {
     if (a.Bp <= 0) return;
-    if (a.H > 256 || a.H % 16 || a.out > 16) throw ShapeError("head: needs hidden width % 16 == 0 (<= 256), out <= 16");
-#define MB_HEAD(O)                                                              \
-    case O:                                                                     \
-        if (actor) k_head<true, O><<<a.Bp / 128, 128, 0, s>>>(a);               \
-        else k_head<false, O><<<a.Bp / 128, 128, 0, s>>>(a);                    \
-        break;
-    switch (a.out) {
-        MB_HEAD(1) MB_HEAD(2) MB_HEAD(3) MB_HEAD(4) MB_HEAD(5) MB_HEAD(6) MB_HEAD(7) MB_HEAD(8)
-        MB_HEAD(9) MB_HEAD(10) MB_HEAD(11) MB_HEAD(12) MB_HEAD(13) MB_HEAD(14) MB_HEAD(15) MB_HEAD(16)
-        default: throw ShapeError("head: output width must be in [1, 16]");
+    if (a.H > 256 || a.H % 16 || a.out > 16 || a.out < 1)
+        throw ShapeError("head: needs hidden width % 16 == 0 (<= 256), 1 <= out <= 16");
+    const unsigned tiles = (unsigned)(a.Bp / 128);
+    if (a.out <= 8) {
+        if (actor) k_head<true, 1><<<tiles, 128, 0, s>>>(a);
+        else k_head<false, 1><<<tiles, 128, 0, s>>>(a);
+    } else {
+        if (actor) k_head<true, 2><<<tiles, 128, 0, s>>>(a);
+        else k_head<false, 2><<<tiles, 128, 0, s>>>(a);
     }
-#undef MB_HEAD
     MB_LAUNCH();
 }
 
