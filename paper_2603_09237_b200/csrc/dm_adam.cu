@@ -180,8 +180,8 @@ void dm_adam(const DmAdam& a, cudaStream_t s) {
         configured = true;
     }
     const int ntf = a.F / TF, ntiles = (a.P + TP - 1) / TP * ntf;
-    int sms = 148;
-    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    static int sms = 0;
+    if (!sms) MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int grid = std::min(ntiles, 2 * sms);  // two 108 KB blocks per SM
     k_dm_adam<<<grid, 128, SMEM, s>>>(a, ntiles, ntf);
     MB_LAUNCH();

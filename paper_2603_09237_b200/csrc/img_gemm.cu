@@ -624,16 +624,20 @@ __global__ void k_pack_weights(const float* __restrict__ theta, long ld, int g0,
         while (r >= pd.ustart[l + 1]) ++l;
         const int in = pd.in[l], cpr = (in + 7) >> 3;
         const int e = (int)(r - pd.ustart[l]);
-        // 8 consecutive threads = 8 consecutive rows of one 8-column unit: the
-        // image stores (row % 8 innermost) are 128 contiguous bytes
-        const int jr = e & 7, rest = e >> 3;
-        const int jg = rest / cpr, c = (rest - jg * cpr) * 8;
-        const int j = jg * 8 + jr;
+        // consecutive threads = consecutive 8-column units of one row: each
+        // warp reads a contiguous 1 KB of theta (two float4 per thread)
+        const int j = e / cpr, c = (e - j * cpr) * 8;
         if (j >= pd.out[l]) continue;  // rows padded to a multiple of 8
         const float* src = theta + (long)(g0 + z) * ld + pd.woff[l] + (long)j * in + c;
         float v[8];
+        if (c + 8 <= in && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = c + q < in ? src[q] : 0.f;
+            for (int q = 0; q < 8; ++q) v[q] = c + q < in ? src[q] : 0.f;
+        }
         uint4 w;
         w.x = umma::pack_bf16(v[0], v[1]);
         w.y = umma::pack_bf16(v[2], v[3]);
@@ -652,58 +656,65 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
 }
 
 // gtheta [G][ld] (fp32) -> bf16 image (row g, col p) for the dM / df GEMMs and
-// db[p] = sum_g gtheta[g][p] (hypernet.cpp:92-122) in one read. A block covers
-// 64 8-column units x 16 row slices (1024 threads: enough loads in flight to
-// stream at HBM rate); the slices' sums combine in a fixed order.
-constexpr int kGtSlices = 16;
-__global__ void __launch_bounds__(64 * kGtSlices) k_gtheta_prep(const float* __restrict__ gt, long ld, int G, int P,
-                                                               Img gimg, float* db) {
-    __shared__ float part[kGtSlices][64][9];
-    const int ul = threadIdx.x & 63, sl = threadIdx.x >> 6;
-    const long u = blockIdx.x * 64L + ul;
-    const int p0 = (int)(u * 8);
+// db[p] = sum_g gtheta[g][p] (hypernet.cpp:92-122) in one read. A block step
+// covers 32 8-column units x 32 row slices (1024 threads, <= 32 registers: two
+// blocks fill an SM, so 64 warps x 32 B per lane keep enough bytes in flight);
+// persistent over the unit groups (no tail wave); the slices' sums combine in
+// a fixed order.
+constexpr int kGtSlices = 32, kGtUnits = 32;
+__global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const float* __restrict__ gt, long ld, int G,
+                                                                         int P, Img gimg, float* db) {
+    __shared__ float part[kGtSlices][kGtUnits][9];
+    const int ul = threadIdx.x % kGtUnits, sl = threadIdx.x / kGtUnits;
     const int CT = img_ct(gimg.C);
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (p0 < P) {
-        const bool full = p0 + 8 <= P;
-        const int rs = (G + kGtSlices - 1) / kGtSlices, r0 = sl * rs, r1 = min(G, r0 + rs);
-#pragma unroll 4
-        for (int g = r0; g < r1; ++g) {
-            const float* src = gt + (long)g * ld + p0;
-            float v[8];
-            if (full) {
-                const float4 a = *reinterpret_cast<const float4*>(src);
-                const float4 b = *reinterpret_cast<const float4*>(src + 4);
-                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-                v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-            } else {
+    const int rs = (G + kGtSlices - 1) / kGtSlices, r0 = sl * rs, r1 = min(G, r0 + rs);
+    const long ngroups = ((P + 7) / 8 + kGtUnits - 1) / kGtUnits;
+    for (long ug = blockIdx.x; ug < ngroups; ug += gridDim.x) {
+        const int p0 = (int)((ug * kGtUnits + ul) * 8);
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (p0 < P) {
+            const bool full = p0 + 8 <= P;
+            for (int g = r0; g < r1; ++g) {
+                const float* src = gt + (long)g * ld + p0;
+                float v[8];
+                if (full) {
+                    const float4 a = *reinterpret_cast<const float4*>(src);
+                    const float4 b = *reinterpret_cast<const float4*>(src + 4);
+                    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+                } else {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = p0 + e < P ? src[e] : 0.f;
+                    for (int e = 0; e < 8; ++e) v[e] = p0 + e < P ? src[e] : 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] += v[e];
+                uint4 w;
+                w.x = umma::pack_bf16(v[0], v[1]);
+                w.y = umma::pack_bf16(v[2], v[3]);
+                w.z = umma::pack_bf16(v[4], v[5]);
+                w.w = umma::pack_bf16(v[6], v[7]);
+                *reinterpret_cast<uint4*>(gimg.p + img_off(g, p0, CT)) = w;
             }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] += v[e];
-            uint4 w;
-            w.x = umma::pack_bf16(v[0], v[1]);
-            w.y = umma::pack_bf16(v[2], v[3]);
-            w.z = umma::pack_bf16(v[4], v[5]);
-            w.w = umma::pack_bf16(v[6], v[7]);
-            *reinterpret_cast<uint4*>(gimg.p + img_off(g, p0, CT)) = w;
         }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) part[sl][ul][e] = acc[e];
+        __syncthreads();
+        if (sl == 0 && p0 < P)
+            for (int e = 0; e < 8 && p0 + e < P; ++e) {
+                float t = 0.f;
+                for (int q = 0; q < kGtSlices; ++q) t += part[q][ul][e];
+                db[p0 + e] = t;
+            }
+        __syncthreads();
     }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) part[sl][ul][e] = acc[e];
-    __syncthreads();
-    if (sl == 0 && p0 < P)
-        for (int e = 0; e < 8 && p0 + e < P; ++e) {
-            float t = 0.f;
-            for (int q = 0; q < kGtSlices; ++q) t += part[q][ul][e];
-            db[p0 + e] = t;
-        }
 }
 void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s) {
     if (ld % 4) throw ShapeError("gtheta_prep: row stride must be a multiple of 4");
-    const long units = (P + 7) / 8;
-    k_gtheta_prep<<<(unsigned)((units + 63) / 64), 64 * kGtSlices, 0, s>>>(gt, ld, G, P, gimg, db);
+    const long ngroups = ((P + 7) / 8 + kGtUnits - 1) / kGtUnits;
+    static int sms = 0;
+    if (!sms) MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    k_gtheta_prep<<<(unsigned)std::min<long>(ngroups, 2L * sms), kGtUnits * kGtSlices, 0, s>>>(gt, ld, G, P, gimg,
+                                                                                               db);
     MB_LAUNCH();
 }
 
@@ -733,42 +744,79 @@ void gather_img(const int* rows, int Bp, const float* src, int width, const Img&
     MB_LAUNCH();
 }
 
-// the whole minibatch in one launch (losses.cpp:21-33 row selection): thread
-// per padded row q (row map rows[q], -1 = padding -> zeros): observation row ->
-// bf16 image, actions / old log-prob / scalar advantage / value targets -> fp32
-// rows, and the row's cluster (goff search) -> rg
-__global__ void k_gather_minibatch(MbGather a) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= a.Bp) return;
+// the whole minibatch in one launch (losses.cpp:21-33 row selection), one
+// block per 128-row tile (groups are 128-row padded: a tile is one cluster,
+// found once by a warp-wide count of the offsets <= the tile start). Per padded
+// row q (row map rows[q], -1 = padding -> zeros): observation row -> bf16
+// image (threads walk the tile's 8-column units row-major: coalesced 32 B
+// reads, 16 B image stores), actions / old log-prob / scalar advantage / value
+// targets -> fp32 rows, the cluster -> rg
+__global__ void __launch_bounds__(128) k_gather_minibatch(const __grid_constant__ MbGather a) {
+    __shared__ int srow[128], sz;
+    const int q0 = blockIdx.x * 128, t = threadIdx.x;
+    const int q = q0 + t;
     const int r = a.rows[q];
+    srow[t] = r;
+    if (t < 32) {
+        int cnt = 0;
+        for (int b = 0; b < a.G; b += 32) {
+            const int i = b + t;
+            cnt += __popc(__ballot_sync(0xffffffffu, i < a.G && a.goff[i] <= q0));
+        }
+        if (t == 0) sz = cnt - 1;
+    }
     const bool ok = r >= 0;
-    int lo = 0, hi = a.G;  // goff[lo] <= q < goff[hi]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (a.goff[mid] <= q) lo = mid;
-        else hi = mid;
-    }
-    a.rg[q] = lo;
-    const int CT = img_ct(a.od);
-    for (int c = 0; c < a.od; c += 8) {
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = (ok && c + e < a.od) ? a.obs[(long)r * a.od + c + e] : 0.f;
-        uint4 w;
-        w.x = umma::pack_bf16(v[0], v[1]);
-        w.y = umma::pack_bf16(v[2], v[3]);
-        w.z = umma::pack_bf16(v[4], v[5]);
-        w.w = umma::pack_bf16(v[6], v[7]);
-        *reinterpret_cast<uint4*>(a.Xi.p + img_off(q, c, CT)) = w;
-    }
-    for (int e = 0; e < a.ad; ++e) a.act_o[(long)q * a.ad + e] = ok ? a.act[(long)r * a.ad + e] : 0.f;
-    for (int e = 0; e < a.m; ++e) a.tgt_o[(long)q * a.m + e] = ok ? a.tgt[(long)r * a.m + e] : 0.f;
     a.lp_o[q] = ok ? a.lp[r] : 0.f;
     a.sadv_o[q] = ok ? a.sadv[r] : 0.f;
+    __syncthreads();
+    a.rg[q] = sz;
+    const int CT = img_ct(a.od), cpr = (a.od + 7) >> 3;
+    const bool vec = (a.od & 3) == 0;
+    // 4 units per thread per round: all 8 loads in flight before the stores
+    for (int u0 = t; u0 < 128 * cpr; u0 += 4 * 128) {
+        float v[4][8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int u = u0 + k * 128;
+            const int rl = u / cpr, c = (u - rl * cpr) * 8;
+            const int rr = u < 128 * cpr ? srow[rl] : -1;
+            const float* src = a.obs + (long)(rr >= 0 ? rr : 0) * a.od;
+            if (rr >= 0 && vec && c + 8 <= a.od) {
+                const float4 x = *reinterpret_cast<const float4*>(src + c);
+                const float4 y = *reinterpret_cast<const float4*>(src + c + 4);
+                v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
+                v[k][4] = y.x; v[k][5] = y.y; v[k][6] = y.z; v[k][7] = y.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[k][e] = (rr >= 0 && c + e < a.od) ? src[c + e] : 0.f;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int u = u0 + k * 128;
+            if (u >= 128 * cpr) break;
+            const int rl = u / cpr, c = (u - rl * cpr) * 8;
+            uint4 w;
+            w.x = umma::pack_bf16(v[k][0], v[k][1]);
+            w.y = umma::pack_bf16(v[k][2], v[k][3]);
+            w.z = umma::pack_bf16(v[k][4], v[k][5]);
+            w.w = umma::pack_bf16(v[k][6], v[k][7]);
+            *reinterpret_cast<uint4*>(a.Xi.p + img_off(q0 + rl, c, CT)) = w;
+        }
+    }
+    for (int u = t; u < 128 * a.ad; u += 128) {
+        const int rl = u / a.ad, e = u - rl * a.ad, rr = srow[rl];
+        a.act_o[(long)q0 * a.ad + u] = rr >= 0 ? a.act[(long)rr * a.ad + e] : 0.f;
+    }
+    for (int u = t; u < 128 * a.m; u += 128) {
+        const int rl = u / a.m, e = u - rl * a.m, rr = srow[rl];
+        a.tgt_o[(long)q0 * a.m + u] = rr >= 0 ? a.tgt[(long)rr * a.m + e] : 0.f;
+    }
 }
 void gather_minibatch(const MbGather& a, cudaStream_t s) {
     if (a.Bp <= 0) return;
-    k_gather_minibatch<<<(a.Bp + 127) / 128, 128, 0, s>>>(a);
+    if (a.Bp % 128) throw ShapeError("gather_minibatch: rows must be 128-padded per cluster");
+    k_gather_minibatch<<<a.Bp / 128, 128, 0, s>>>(a);
     MB_LAUNCH();
 }
 
