@@ -190,6 +190,36 @@ int morlax_trainer_save_checkpoint(morlax_trainer* t, const char* path, int64_t 
                                    const morlax_checkpoint_extra* extra);
 int morlax_trainer_load_checkpoint(morlax_trainer* t, const char* path, int64_t* iteration_out);
 
+/* ---- Training loop (replaces train(RunConfig, TrainOptions,
+ *      IterationCallback), include/morlax/trainer.hpp:237-257 and
+ *      src/train.cpp:55-229, single rank): iterations of the device loop
+ *      body; every log_interval (and the last) iteration evaluate_params ->
+ *      archive -> nondominated_filter -> hypervolume; out_dir/metrics.csv
+ *      (iteration,wall_ms,cluster_<c>_return...,archive_hypervolume; "%.17g")
+ *      and out_dir/checkpoint.bin (MRLXCKPT v1: the final params, or on a
+ *      NumericError the last healthy iteration's, then status 3). `out`
+ *      (optional) receives the trained trainer (free with
+ *      morlax_trainer_destroy); NULL destroys it. */
+typedef struct {
+    const char* out_dir; /* NULL / "" disables checkpoint.bin and metrics.csv (TrainOptions::out_dir) */
+    int iterations;      /* TrainerConfig::iterations */
+    int grid_resolution, episodes_per_point, log_interval; /* EvalConfig */
+    int n_pareto_reference;
+    const double* pareto_reference; /* NULL: the env's hv_reference */
+    int deterministic;   /* wall_ms logged as 0 (TrainOptions::deterministic) */
+} morlax_run_options;
+typedef struct {         /* IterationStats (trainer.hpp:243-249) */
+    int iteration;
+    double actor_loss, critic_loss, archive_hypervolume;
+    int n_clusters;
+    const double* cluster_returns; /* valid during the callback */
+} morlax_iteration_stats;
+/* a non-zero return stops training (train() propagates a callback's
+ * exception): morlax_train returns 1, last error "iteration callback failed" */
+typedef int (*morlax_iteration_callback)(const morlax_iteration_stats* stats, void* user);
+int morlax_train(const morlax_train_config* cfg, const morlax_run_options* opts, morlax_iteration_callback cb,
+                 void* user, morlax_trainer** out);
+
 int morlax_trainer_get_theta(morlax_trainer* t, int which, float* out /* local K x P */);
 /* field: obs action_pre logprob reward value next_value advantages
  * value_targets scalar_advantage (float) | terminated truncated (uint8) |

@@ -416,6 +416,14 @@ class Oracle:
                                                    C.c_int64(n_critic), C.byref(it)))
         return a, c, it.value
 
+    def train_run(self, cfg, iterations, grid, episodes, log_interval, out_dir, n_actor, n_critic):
+        """The reference train() with out_dir, evaluation and the archive
+        (train.cpp:55-229; ref lib only): per-iteration archive HV, final params."""
+        hv, a, c = np.zeros(iterations), np.zeros(n_actor), np.zeros(n_critic)
+        self.check(self.lib.mref_train_run(C.byref(cfg.c()), iterations, grid, episodes, log_interval,
+                                           out_dir.encode(), _p(hv), _p(a), _p(c)))
+        return hv, a, c
+
     def linear_dominance_mask(self, pts):
         pts = np.ascontiguousarray(pts, np.float64)
         n, m = pts.shape

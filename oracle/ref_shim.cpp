@@ -346,6 +346,39 @@ int mref_train(const mo_train_cfg* c, int iterations, double* actor_out, double*
     });
 }
 
+// The reference train() with files and evaluation (train.cpp:55-229):
+// out_dir gets metrics.csv / checkpoint.bin; archive_hv_out[it] from the
+// callback; final params out.
+int mref_train_run(const mo_train_cfg* c, int iterations, int grid, int episodes, int log_interval,
+                   const char* out_dir, double* archive_hv_out, double* actor_out, double* critic_out) {
+    return guarded([&] {
+        RunConfig cfg;
+        cfg.env_name = env_name(c->env_kind);
+        TrainerConfig& t = cfg.trainer;
+        t.N = c->N; t.K = c->K; t.kappa = c->kappa; t.T = c->T;
+        t.gamma = c->gamma; t.gae_lambda = c->lambda; t.clip_eps = c->clip_eps;
+        t.epochs = c->epochs; t.minibatch_count = c->minibatch_count;
+        t.actor_lr = c->actor_lr; t.critic_lr = c->critic_lr; t.entropy_coef = c->entropy_coef;
+        t.iterations = iterations; t.seed = c->seed;
+        cfg.hypernet.F = c->F;
+        cfg.hypernet.feature_hidden.assign(c->feat_hidden, c->feat_hidden + c->n_feat_hidden);
+        cfg.hypernet.actor_hidden.assign(c->actor_hidden, c->actor_hidden + c->n_actor_hidden);
+        cfg.hypernet.critic_hidden.assign(c->critic_hidden, c->critic_hidden + c->n_critic_hidden);
+        cfg.eval.grid_resolution = grid;
+        cfg.eval.episodes_per_point = episodes;
+        cfg.eval.log_interval = log_interval;
+        TrainOptions opts;
+        opts.threads = 1;
+        opts.deterministic = true;
+        opts.out_dir = out_dir ? out_dir : "";
+        Checkpoint ck = train(cfg, opts, [&](const IterationStats& s) {
+            archive_hv_out[s.iteration] = s.archive_hypervolume;
+        });
+        std::copy(ck.actor_params.begin(), ck.actor_params.end(), actor_out);
+        std::copy(ck.critic_params.begin(), ck.critic_params.end(), critic_out);
+    });
+}
+
 // ---- Timed harness: exactly the train() loop body (train.cpp:118-184) on
 // reference functions, any env including mo-humanoid6, `threads` rollout
 // workers. Used by bench.py --impl reference / cpu_baseline.

@@ -412,12 +412,16 @@ class Trainer:
     _F32 = {"obs", "action_pre", "logprob", "reward", "value", "next_value", "advantages",
             "value_targets", "scalar_advantage", "env_state", "tracker", "clusters"}
 
-    def __init__(self, cfg: TrainConfig, world: int = 1, rank: int = 0, nccl_id: bytes = None):
+    def __init__(self, cfg: TrainConfig, world: int = 1, rank: int = 0, nccl_id: bytes = None,
+                 _handle=None):
         self.cfg = cfg
         self._c = cfg.c()
         h = C.c_void_p()
-        idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        _check(LIB.morlax_trainer_create(C.byref(self._c), world, rank, idb, C.byref(h)))
+        if _handle is not None:  # adopt a trainer made by morlax_train
+            h = _handle
+        else:
+            idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+            _check(LIB.morlax_trainer_create(C.byref(self._c), world, rank, idb, C.byref(h)))
         self._h = h
         self.es = env_spec(cfg.env_name)
         ap, cp = C.c_int64(), C.c_int64()
@@ -576,3 +580,84 @@ def hypervolume_detailed(points, reference, samples=1_000_000, seed=0x9E3779B9):
                                            C.c_uint64(seed), C.byref(v), C.byref(se), C.byref(ex),
                                            C.byref(cl)))
     return v.value, se.value, bool(ex.value), cl.value
+
+
+# ---------------------------------------------------------------- train()
+@dataclass
+class RunOptions:
+    """TrainOptions + EvalConfig + TrainerConfig::iterations + the Pareto
+    reference of RunConfig (trainer.hpp:59-77, 237-241); defaults = the
+    reference's."""
+    out_dir: str = ""
+    iterations: int = 300
+    grid_resolution: int = 10
+    episodes_per_point: int = 8
+    log_interval: int = 10
+    pareto_reference: list = None
+    deterministic: bool = False
+
+
+@dataclass
+class IterationRecord:
+    """IterationStats (trainer.hpp:243-249)."""
+    iteration: int
+    actor_loss: float
+    critic_loss: float
+    archive_hypervolume: float
+    cluster_returns: np.ndarray
+
+
+class _RunOptsC(C.Structure):
+    _fields_ = [("out_dir", C.c_char_p), ("iterations", C.c_int), ("grid_resolution", C.c_int),
+                ("episodes_per_point", C.c_int), ("log_interval", C.c_int),
+                ("n_pareto_reference", C.c_int), ("pareto_reference", C.POINTER(C.c_double)),
+                ("deterministic", C.c_int)]
+
+
+class _IterRecC(C.Structure):
+    _fields_ = [("iteration", C.c_int), ("actor_loss", C.c_double), ("critic_loss", C.c_double),
+                ("archive_hypervolume", C.c_double), ("n_clusters", C.c_int),
+                ("cluster_returns", C.POINTER(C.c_double))]
+
+
+_ITER_CB = C.CFUNCTYPE(C.c_int, C.POINTER(_IterRecC), C.c_void_p)
+
+
+def train(cfg: TrainConfig, opts: RunOptions = None, callback=None) -> "Trainer":
+    """train(RunConfig, TrainOptions, IterationCallback) (train.cpp:55-229) on
+    one GPU: returns the trained Trainer (params(), save_checkpoint(), ...).
+    With opts.out_dir, writes metrics.csv and checkpoint.bin there like the
+    reference (on a NumericError: the last healthy checkpoint, then raises).
+    An exception raised by `callback(IterationRecord)` stops training and
+    propagates."""
+    opts = opts or RunOptions()
+    ref = None
+    if opts.pareto_reference is not None:
+        ref = np.ascontiguousarray(opts.pareto_reference, dtype=np.float64)
+    o = _RunOptsC(opts.out_dir.encode() if opts.out_dir else None, opts.iterations, opts.grid_resolution,
+                  opts.episodes_per_point, opts.log_interval, 0 if ref is None else len(ref),
+                  None if ref is None else ref.ctypes.data_as(C.POINTER(C.c_double)),
+                  1 if opts.deterministic else 0)
+    err = []
+
+    def _cb(p, _user):
+        if callback is None:
+            return 0
+        r = p.contents
+        rec = IterationRecord(r.iteration, r.actor_loss, r.critic_loss, r.archive_hypervolume,
+                              np.ctypeslib.as_array(r.cluster_returns, (r.n_clusters,)).copy())
+        try:
+            callback(rec)
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err.append(e)
+            return 1
+        return 0
+
+    cb = _ITER_CB(_cb)
+    h = C.c_void_p()
+    c = cfg.c()
+    rc = LIB.morlax_train(C.byref(c), C.byref(o), cb, None, C.byref(h))
+    if err:
+        raise err[0]
+    _check(rc)
+    return Trainer(cfg, _handle=h)

@@ -4,7 +4,9 @@
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <chrono>
 #include <cstring>
+#include <filesystem>
 #include <string>
 #include <vector>
 
@@ -158,11 +160,45 @@ void write_spec(CkWriter& w, const HyperNet& h, const std::vector<int>& fh) {  /
     w.put<uint8_t>(h.tgt.out_tanh ? 1 : 0);
     w.put<uint8_t>(h.tgt.has_log_std ? 1 : 0);
 }
-std::vector<double> params_f64(const HyperNet& h, cudaStream_t s) {
+std::vector<double> params_f64(const HyperNet& h, const float* dev, cudaStream_t s) {
     std::vector<float> f(h.n);
     MB_CUDA(cudaStreamSynchronize(s));
-    MB_CUDA(cudaMemcpy(f.data(), h.p, sizeof(float) * h.n, cudaMemcpyDeviceToHost));
+    MB_CUDA(cudaMemcpy(f.data(), dev, sizeof(float) * h.n, cudaMemcpyDeviceToHost));
     return std::vector<double>(f.begin(), f.end());
+}
+// save_checkpoint (checkpoint.cpp:200-213) of the trainer's config with the
+// params read from the device buffers actor_dev / critic_dev (the live
+// params, or train()'s last-healthy snapshot)
+void write_checkpoint(Trainer& tr, const char* path, int64_t iteration, const morlax_checkpoint_extra* x,
+                      const float* actor_dev, const float* critic_dev) {
+    const TrainConfig& c = tr.config();
+    const morlax_checkpoint_extra def{300, 10, 8, 10, 0, nullptr};  // trainer.hpp:39, 59-62 defaults
+    const morlax_checkpoint_extra& e = x ? *x : def;
+    CkWriter w;
+    w.raw("MRLXCKPT", 8);
+    w.put<uint32_t>(1);
+    w.str(env_name_of(c.env_kind));  // write_run_config (checkpoint.cpp:137-163)
+    w.put<int32_t>(c.N); w.put<int32_t>(c.K); w.put<int32_t>(c.kappa); w.put<int32_t>(c.T);
+    w.put<double>(c.gamma); w.put<double>(c.lambda); w.put<double>(c.clip_eps);
+    w.put<int32_t>(c.epochs); w.put<int32_t>(c.minibatch_count);
+    w.put<double>(c.actor_lr); w.put<double>(c.critic_lr); w.put<double>(c.entropy_coef);
+    w.put<int32_t>(e.iterations);
+    w.put<uint64_t>(c.seed);
+    w.put<int32_t>(c.F);
+    w.vec_i32(c.feat_hidden); w.vec_i32(c.actor_hidden); w.vec_i32(c.critic_hidden);
+    w.put<int32_t>(e.grid_resolution); w.put<int32_t>(e.episodes_per_point); w.put<int32_t>(e.log_interval);
+    w.vec_f64(std::vector<double>(e.pareto_reference, e.pareto_reference + (e.pareto_reference ? e.n_pareto_reference : 0)));
+    write_spec(w, tr.actor(), c.feat_hidden);
+    write_spec(w, tr.critic(), c.feat_hidden);
+    w.vec_f64(params_f64(tr.actor(), actor_dev, tr.stream()));
+    w.vec_f64(params_f64(tr.critic(), critic_dev, tr.stream()));
+    w.put<int64_t>(iteration);
+    w.put<uint64_t>(seed_key(c.seed));  // the root Rng(seed) is only ever split: counter 0
+    w.put<uint64_t>(0);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw ConfigError(std::string("cannot open checkpoint for writing: ") + path);
+    const size_t n = std::fwrite(w.buf.data(), 1, w.buf.size(), f);
+    if (std::fclose(f) != 0 || n != w.buf.size()) throw ConfigError(std::string("failed writing checkpoint: ") + path);
 }
 }  // namespace
 }  // namespace mb200
@@ -582,35 +618,146 @@ int morlax_trainer_save_checkpoint(morlax_trainer* t, const char* path, int64_t 
                                    const morlax_checkpoint_extra* x) {
     return guarded([&] {
         Trainer& tr = *t->t;
-        const TrainConfig& c = tr.config();
-        const morlax_checkpoint_extra def{300, 10, 8, 10, 0, nullptr};  // trainer.hpp:39, 59-62 defaults
-        const morlax_checkpoint_extra& e = x ? *x : def;
-        CkWriter w;
-        w.raw("MRLXCKPT", 8);
-        w.put<uint32_t>(1);
-        w.str(env_name_of(c.env_kind));  // write_run_config (checkpoint.cpp:137-163)
-        w.put<int32_t>(c.N); w.put<int32_t>(c.K); w.put<int32_t>(c.kappa); w.put<int32_t>(c.T);
-        w.put<double>(c.gamma); w.put<double>(c.lambda); w.put<double>(c.clip_eps);
-        w.put<int32_t>(c.epochs); w.put<int32_t>(c.minibatch_count);
-        w.put<double>(c.actor_lr); w.put<double>(c.critic_lr); w.put<double>(c.entropy_coef);
-        w.put<int32_t>(e.iterations);
-        w.put<uint64_t>(c.seed);
-        w.put<int32_t>(c.F);
-        w.vec_i32(c.feat_hidden); w.vec_i32(c.actor_hidden); w.vec_i32(c.critic_hidden);
-        w.put<int32_t>(e.grid_resolution); w.put<int32_t>(e.episodes_per_point); w.put<int32_t>(e.log_interval);
-        w.vec_f64(std::vector<double>(e.pareto_reference, e.pareto_reference + (e.pareto_reference ? e.n_pareto_reference : 0)));
-        write_spec(w, tr.actor(), c.feat_hidden);
-        write_spec(w, tr.critic(), c.feat_hidden);
-        w.vec_f64(params_f64(tr.actor(), tr.stream()));
-        w.vec_f64(params_f64(tr.critic(), tr.stream()));
-        w.put<int64_t>(iteration);
-        w.put<uint64_t>(seed_key(c.seed));  // the root Rng(seed) is only ever split: counter 0
-        w.put<uint64_t>(0);
-        FILE* f = std::fopen(path, "wb");
-        if (!f) throw ConfigError(std::string("cannot open checkpoint for writing: ") + path);
-        const size_t n = std::fwrite(w.buf.data(), 1, w.buf.size(), f);
-        if (std::fclose(f) != 0 || n != w.buf.size()) throw ConfigError(std::string("failed writing checkpoint: ") + path);
+        write_checkpoint(tr, path, iteration, x, tr.actor().p, tr.critic().p);
     });
+}
+
+// train() (train.cpp:55-229) over the device trainer: per iteration the
+// device loop body (sampling, rollout, GAE, PPO update), every log_interval
+// (and the last iteration) evaluate_params of the actor -> archive ->
+// nondominated_filter -> hypervolume (exact m <= 4, else MC 1e6 / seed
+// 0x9E3779B9), one metrics.csv row ("%.17g", wall_ms 0 when deterministic),
+// the callback, and a last-healthy snapshot (device copy of both hypernets'
+// params, taken after each iteration). On NumericError the snapshot is saved
+// as checkpoint.bin and the error returned (3); at the end the final params.
+int morlax_train(const morlax_train_config* cfg, const morlax_run_options* o, morlax_iteration_callback cb,
+                 void* user, morlax_trainer** out) {
+    morlax_trainer* t = nullptr;
+    int rc = morlax_trainer_create(cfg, 1, 0, nullptr, &t);
+    if (rc) return rc;
+    float *snap_a = nullptr, *snap_c = nullptr;
+    rc = guarded([&] {
+        Trainer& tr = *t->t;
+        const TrainConfig& c = tr.config();
+        const morlax_run_options def{nullptr, 300, 10, 8, 10, 0, nullptr, 0};  // trainer.hpp:39, 59-62
+        const morlax_run_options& op = o ? *o : def;
+        if (op.iterations < 1) throw ConfigError("trainer.iterations must be >= 1");
+        if (op.grid_resolution < 1 || op.episodes_per_point < 1 || op.log_interval < 1)
+            throw ConfigError("eval: grid_resolution, episodes_per_point and log_interval must be >= 1");
+        const EnvSpecB es = env_spec_of(c.env_kind);
+        std::vector<double> ref(op.pareto_reference, op.pareto_reference + (op.pareto_reference ? op.n_pareto_reference : 0));
+        if (ref.empty()) {  // EnvSpec::hv_reference (env_lqr.cpp:15, env_pointmass.cpp:14, env_deepsea.cpp:31)
+            switch (c.env_kind) {
+                case ENV_LQR: ref = {-50.0, -20.0}; break;
+                case ENV_LQR_M1: ref = {-50.0}; break;
+                case ENV_POINTMASS: ref = {-1100.0, -450.0}; break;
+                case ENV_DST: ref = {-1.0, -55.0}; break;
+                default: ref = H6_HV_REF; break;
+            }
+        }
+        if ((int)ref.size() != es.m) throw ConfigError("pareto_reference length must equal the number of objectives");
+        const morlax_checkpoint_extra ex{op.iterations, op.grid_resolution, op.episodes_per_point, op.log_interval,
+                                         op.pareto_reference ? op.n_pareto_reference : 0, op.pareto_reference};
+        const bool files = op.out_dir && op.out_dir[0];
+        std::string dir = files ? std::string(op.out_dir) : std::string();
+        FILE* metrics = nullptr;
+        if (files) {
+            std::filesystem::create_directories(dir);
+            metrics = std::fopen((dir + "/metrics.csv").c_str(), "w");
+            if (!metrics) throw ConfigError("cannot open metrics log in '" + dir + "'");
+            std::fprintf(metrics, "iteration,wall_ms");
+            for (int k = 0; k < c.K; ++k) std::fprintf(metrics, ",cluster_%d_return", k);
+            std::fprintf(metrics, ",archive_hypervolume\n");
+        }
+        struct Closer {
+            FILE*& f;
+            ~Closer() { if (f) std::fclose(f); }
+        } closer{metrics};
+        const HyperNet& A = tr.actor();
+        const HyperNet& Cn = tr.critic();
+        MB_CUDA(cudaMalloc(&snap_a, sizeof(float) * A.n));
+        MB_CUDA(cudaMalloc(&snap_c, sizeof(float) * Cn.n));
+        auto snapshot = [&] {
+            MB_CUDA(cudaMemcpyAsync(snap_a, A.p, sizeof(float) * A.n, cudaMemcpyDeviceToDevice, tr.stream()));
+            MB_CUDA(cudaMemcpyAsync(snap_c, Cn.p, sizeof(float) * Cn.n, cudaMemcpyDeviceToDevice, tr.stream()));
+        };
+        snapshot();
+        int64_t last_it = 0;
+        // actor spec for evaluate_params (HypernetArch::actor_spec)
+        morlax_hypernet_spec as{};
+        as.m = A.m; as.F = A.F;
+        as.n_feature_hidden = (int)c.feat_hidden.size();
+        for (size_t k = 0; k < c.feat_hidden.size(); ++k) as.feature_hidden[k] = c.feat_hidden[k];
+        as.n_target_sizes = A.tgt.L + 1;
+        for (int k = 0; k <= A.tgt.L; ++k) as.target_sizes[k] = A.tgt.sz[k];
+        as.target_tanh = A.tgt.out_tanh ? 1 : 0;
+        as.has_log_std = A.tgt.has_log_std ? 1 : 0;
+        std::vector<double> archive;  // [n][m]
+        double archive_hv = 0.0;
+        const HostRng root = HostRng::seeded(c.seed);
+        for (int it = 0; it < op.iterations; ++it) {
+            const auto t0 = std::chrono::steady_clock::now();
+            IterStats st;
+            try {
+                tr.iteration(it, &st);
+                if (it % op.log_interval == 0 || it == op.iterations - 1) {
+                    const std::vector<double> flat = params_f64(A, A.p, tr.stream());
+                    const int64_t np = morlax_simplex_grid_size(es.m, op.grid_resolution);
+                    std::vector<double> w((size_t)np * es.m), mr((size_t)np * es.m);
+                    int64_t n = 0;
+                    const uint64_t key = root.split(0x20000000ULL + (uint64_t)it).key;  // kLaneEvalBase + it
+                    if (morlax_evaluate_params(&as, flat.data(), env_name_of(c.env_kind), op.grid_resolution,
+                                               op.episodes_per_point, key, w.data(), mr.data(), &n))
+                        throw std::runtime_error(g_err);
+                    archive.insert(archive.end(), mr.begin(), mr.begin() + n * es.m);
+                    const int na = (int)(archive.size() / es.m);
+                    std::vector<uint8_t> keep(na);
+                    if (morlax_pareto_mask(na, es.m, archive.data(), keep.data())) throw std::runtime_error(g_err);
+                    std::vector<double> kept;
+                    for (int i = 0; i < na; ++i)
+                        if (keep[i]) kept.insert(kept.end(), archive.begin() + (size_t)i * es.m, archive.begin() + (size_t)(i + 1) * es.m);
+                    archive.swap(kept);
+                    double se = 0;
+                    int exact = 0, clipped = 0;
+                    if (morlax_hypervolume_detailed((int)(archive.size() / es.m), es.m, archive.data(), ref.data(),
+                                                    1000000, 0x9E3779B9ULL, &archive_hv, &se, &exact, &clipped))
+                        throw std::runtime_error(g_err);
+                }
+            } catch (const NumericError&) {  // keep the last healthy state on disk, then rethrow
+                if (files) {
+                    write_checkpoint(tr, (dir + "/checkpoint.bin").c_str(), last_it, &ex, snap_a, snap_c);
+                    std::fflush(metrics);
+                }
+                throw;
+            }
+            const double wall_ms =
+                op.deterministic ? 0.0
+                                 : std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (metrics) {
+                std::fprintf(metrics, "%d,%.17g", it, wall_ms);
+                for (double r : st.cluster_returns) std::fprintf(metrics, ",%.17g", r);
+                std::fprintf(metrics, ",%.17g\n", archive_hv);
+                std::fflush(metrics);
+            }
+            if (cb) {
+                morlax_iteration_stats s{it, st.actor_loss, st.critic_loss, archive_hv, (int)st.cluster_returns.size(),
+                                         st.cluster_returns.data()};
+                if (cb(&s, user)) throw std::runtime_error("iteration callback failed");
+            }
+            snapshot();
+            last_it = it + 1;
+        }
+        if (files) write_checkpoint(tr, (dir + "/checkpoint.bin").c_str(), last_it, &ex, A.p, Cn.p);
+    });
+    cudaFree(snap_a);
+    cudaFree(snap_c);
+    if (rc == 0 && out) {
+        *out = t;
+    } else {
+        morlax_trainer_destroy(t);
+        if (out) *out = nullptr;
+    }
+    return rc;
 }
 
 int morlax_trainer_load_checkpoint(morlax_trainer* t, const char* path, int64_t* iteration) {

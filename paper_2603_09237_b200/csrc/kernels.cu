@@ -546,8 +546,12 @@ void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, co
 // fragment of the backward (rows x K = out), and the forward's A fragments
 // (the activations) are exactly the tanh' operands of the backward's
 // accumulator, so the activations are read once and nothing is staged.
-// W_L (bf16-rounded from the fp32 theta) sits in shared memory in fragment
-// order for both products. Padded rows (rows[q] < 0) contribute zeros.
+// In the forward W_L enters as a two-term bf16 split (hi + lo: ~16 mantissa
+// bits, the accuracy of the fp32 SIMT form this replaced -- the PPO ratio is
+// sensitive to the output mean; the activations are the bf16 image either
+// way); the backward uses bf16 g and W_L like the other data-gradient GEMMs.
+// W_L sits in shared memory in fragment order for both products. Padded rows
+// (rows[q] < 0) contribute zeros.
 // =========================================================================
 __device__ __forceinline__ void mma_bf16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                uint32_t b0, uint32_t b1) {
@@ -561,15 +565,19 @@ __device__ __forceinline__ uint32_t bf2_pack(float lo, float hi) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<const uint32_t*>(&v);
 }
+// the bf16 residual x - bf16(x) (the "lo" half of a two-term bf16 split)
+__device__ __forceinline__ float bf_lo(float x) { return x - __bfloat162float(__float2bfloat16_rn(x)); }
 __device__ __forceinline__ float2 bf2_unpack(uint32_t u) {
     return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
 }
 
 // NT = n-tiles of the output (out <= 8 * NT)
 template <bool ACTOR, int NT>
-__global__ void __launch_bounds__(128) k_head(HeadArgs a) {
-    __shared__ uint2 swf[16][NT][32];  // forward B: (k = h pair, n = d) per k-step / n-tile / lane
-    __shared__ uint2 swb[32][32];      // backward B: (k = d pair, n = h) per h n-tile / lane
+__global__ void __launch_bounds__(128, 4) k_head(HeadArgs a) {
+    // forward W_L = hi + lo (two bf16 terms: ~16 mantissa bits, as the fp32
+    // form this replaced: the PPO ratio is sensitive to the output mean)
+    __shared__ uint2 swf[2][16][NT][32];  // forward B: (k = h pair, n = d) per k-step / n-tile / lane
+    __shared__ uint2 swb[32][32];         // backward B: (k = d pair, n = h) per h n-tile / lane
     __shared__ float sb[16], red[4][16], redl[4][16];
     __shared__ float red2[4][256];
     const int H = a.H, out = a.out, KS = H >> 4, HT = H >> 3;
@@ -585,7 +593,8 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
             w0 = W[(long)n * H + k]; w1 = W[(long)n * H + k + 1];
             w8 = W[(long)n * H + k + 8]; w9 = W[(long)n * H + k + 9];
         }
-        swf[st][j][l] = make_uint2(bf2_pack(w0, w1), bf2_pack(w8, w9));
+        swf[0][st][j][l] = make_uint2(bf2_pack(w0, w1), bf2_pack(w8, w9));
+        swf[1][st][j][l] = make_uint2(bf2_pack(bf_lo(w0), bf_lo(w1)), bf2_pack(bf_lo(w8), bf_lo(w9)));
     }
     for (int e = threadIdx.x; e < HT * 32; e += 128) {
         const int l = e & 31, nt = e >> 5;
@@ -665,8 +674,9 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
             if (s < KS)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) {
-                    const uint2 b = swf[s][j][lane];
+                    const uint2 b = swf[0][s][j][lane], bl = swf[1][s][j][lane];
                     mma_bf16_16816(c[j], af[s][0], af[s][1], af[s][2], af[s][3], b.x, b.y);
+                    mma_bf16_16816(c[j], af[s][0], af[s][1], af[s][2], af[s][3], bl.x, bl.y);
                 }
         // ---- per-row loss and dloss/do (the row's columns are spread over the 4 q-lanes)
         float g[2][NT][2], gl[2][NT][2];
@@ -764,6 +774,10 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int nt = 4 * n4 + u;
+                if (nt >= HT) {  // H % 32 == 16: the last group is half full
+                    cs8[2 * u] = cs8[2 * u + 1] = 0.f;
+                    continue;
+                }
                 const uint2 b = swb[nt][lane];
                 float v[4] = {0.f, 0.f, 0.f, 0.f};
                 mma_bf16_16816(v, ga[0][0], ga[0][1], ga[1][0], ga[1][1], b.x, b.y);
@@ -795,8 +809,10 @@ __global__ void __launch_bounds__(128) k_head(HeadArgs a) {
             // lane keeps slot k = 4 (lane>>4 & 1) + 2 (lane>>3 & 1) + (lane>>2 & 1) = rq bit-reversed
             const int k = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
             const int col = 8 * (4 * n4 + (k >> 1)) + 2 * q + (k & 1);
-            if (mt == 0) red2[warp][col] = cs8[0];
-            else red2[warp][col] += cs8[0];
+            if (col < H) {
+                if (mt == 0) red2[warp][col] = cs8[0];
+                else red2[warp][col] += cs8[0];
+            }
         }
     }
     if (rq == 0)

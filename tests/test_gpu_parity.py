@@ -275,13 +275,15 @@ def test_rollout_and_advantages_parity(mb, o, env):
         assert_normwise(t.get(name), b[key], REL_CHAIN, what=name)
 
 
-@pytest.mark.parametrize("F,fused", [(16, "1"), (64, "1"), (64, "0")])
-def test_full_iteration_parity(mb, o, monkeypatch, F, fused):
+@pytest.mark.parametrize("F,fused,H", [(16, "1", 32), (64, "1", 32), (64, "0", 32), (16, "1", 48), (16, "1", 16)])
+def test_full_iteration_parity(mb, o, monkeypatch, F, fused, H):
     """F = 64 takes the single-rank fused dM + Adam kernel (dm_adam.cu) unless
-    MORLAX_FUSED_ADAM=0 (the tcgen05 dM GEMM + separate Adam)."""
+    MORLAX_FUSED_ADAM=0 (the tcgen05 dM GEMM + separate Adam); H = 48 / 16
+    cover the head kernel's partial 32-column group of the output layer's
+    backward."""
     monkeypatch.setenv("MORLAX_FUSED_ADAM", fused)
     c = _tiny(N=32, K=4, T=16, epochs=2, minibatch_count=2, F=F, feat_hidden=[16],
-              actor_hidden=[32, 32], critic_hidden=[32, 32])
+              actor_hidden=[H, H], critic_hidden=[H, H])
     t = mb.Trainer(_mbcfg(mb, c))
     ot = OracleTrainer(o, c)
     a0 = t.params("actor")
@@ -503,3 +505,80 @@ def test_checkpoint_is_the_reference_format(mb, tmp_path):
         a, c, it = r.checkpoint_resave(path, out, t.n_actor, t.n_critic)
         assert it == 1 and np.array_equal(a, t.params("actor")) and np.array_equal(c, t.params("critic"))
         assert open(out, "rb").read() == open(path, "rb").read()
+
+
+# ------------------------------------------------------------------ train() loop (train.cpp:55-229)
+def _train_cfg():
+    return _tiny(N=16, K=2, T=12, epochs=2, minibatch_count=2, F=16, feat_hidden=[16],
+                 actor_hidden=[16, 16], critic_hidden=[16, 16])
+
+
+def test_train_loop_drives_the_iteration_loop(mb, tmp_path):
+    """train() = Trainer.iteration(0..n-1) (bit-identical params) + the
+    evaluation / archive / files / callback around it."""
+    c = _train_cfg()
+    recs = []
+    t = mb.train(_mbcfg(mb, c), mb.RunOptions(out_dir=str(tmp_path), iterations=3, grid_resolution=3,
+                                              episodes_per_point=2, log_interval=2, deterministic=True),
+                 callback=recs.append)
+    u = mb.Trainer(_mbcfg(mb, c))
+    for it in range(3):
+        su = u.iteration(it)
+        assert recs[it].iteration == it
+        assert recs[it].actor_loss == su.actor_loss and recs[it].critic_loss == su.critic_loss
+    assert np.array_equal(t.params("actor"), u.params("actor"))
+    assert np.array_equal(t.params("critic"), u.params("critic"))
+    lines = (tmp_path / "metrics.csv").read_text().splitlines()
+    assert lines[0] == "iteration,wall_ms,cluster_0_return,cluster_1_return,archive_hypervolume"
+    assert [ln.split(",")[:2] for ln in lines[1:]] == [[str(i), "0"] for i in range(3)]
+    assert recs[0].archive_hypervolume > 0 and recs[1].archive_hypervolume == recs[0].archive_hypervolume
+    v = mb.Trainer(_mbcfg(mb, c))
+    assert v.load_checkpoint(str(tmp_path / "checkpoint.bin")) == 3
+    assert np.array_equal(v.params("actor"), t.params("actor"))
+
+    class Stop(Exception):
+        pass
+
+    def boom(r):
+        if r.iteration == 1:
+            raise Stop()
+    with pytest.raises(Stop):
+        mb.train(_mbcfg(mb, c), mb.RunOptions(iterations=3, log_interval=5), callback=boom)
+    with pytest.raises(mb.ConfigError):
+        mb.train(_mbcfg(mb, c), mb.RunOptions(iterations=1, pareto_reference=[0.0]))
+
+
+def test_train_loop_matches_the_reference_train(mb, tmp_path):
+    """metrics.csv (layout, iteration / wall_ms columns, cluster returns,
+    archive hypervolume) and checkpoint.bin of train() vs the compiled
+    reference train() on the same config (fp32 device path vs fp64)."""
+    from helpers import ref_available
+    if not ref_available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    c = _train_cfg()
+    its = 3
+    recs = []
+    t = mb.train(_mbcfg(mb, c), mb.RunOptions(out_dir=str(tmp_path / "gpu"), iterations=its, grid_resolution=3,
+                                              episodes_per_point=2, log_interval=2, deterministic=True),
+                 callback=recs.append)
+    r = Oracle("ref")
+    hv_ref, a_ref, c_ref = r.train_run(c, its, 3, 2, 2, str(tmp_path / "ref"), t.n_actor, t.n_critic)
+    g = (tmp_path / "gpu" / "metrics.csv").read_text().splitlines()
+    q = (tmp_path / "ref" / "metrics.csv").read_text().splitlines()
+    assert g[0] == q[0] and len(g) == len(q) == its + 1
+    for lg, lq in zip(g[1:], q[1:]):
+        fg, fq = lg.split(","), lq.split(",")
+        assert fg[:2] == fq[:2]
+        vg, vq = np.array(fg[2:], float), np.array(fq[2:], float)
+        assert np.array_equal(np.isnan(vg), np.isnan(vq))
+        ok = ~np.isnan(vq)
+        assert np.allclose(vg[ok], vq[ok], rtol=2e-2, atol=1e-2)
+    assert np.allclose([x.archive_hypervolume for x in recs], hv_ref, rtol=2e-2)
+    a, cc, it = r.checkpoint_resave(str(tmp_path / "gpu" / "checkpoint.bin"), str(tmp_path / "re.bin"),
+                                    t.n_actor, t.n_critic)
+    assert it == its
+    for p, ref, lr in ((a, a_ref, c.actor_lr), (cc, c_ref, c.critic_lr)):
+        err = np.abs(p - ref)  # Adam moves a weight by <= ~lr per step (see test_full_iteration_parity)
+        steps = its * c.epochs * c.minibatch_count
+        assert np.quantile(err, 0.99) <= 0.05 * lr * steps
+        assert err.max() <= 2.5 * lr * steps
