@@ -11,7 +11,7 @@ namespace {
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef void* ncclComm_t;
 typedef int ncclResult_t;
-enum { ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0 };
+enum { ncclUint8 = 1, ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0 };
 struct Nccl {
     void* lib = nullptr;
     ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
@@ -75,6 +75,10 @@ void comm_allreduce_f32(Comm* c, float* buf, size_t count, cudaStream_t s) {
 }
 void comm_allreduce_f64(Comm* c, double* buf, size_t count, cudaStream_t s) {
     check(nccl().allReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, s), "ncclAllReduce");
+}
+void comm_allgather_bytes(Comm* c, void* buf, size_t bytes, cudaStream_t s) {
+    uint8_t* b = static_cast<uint8_t*>(buf);
+    check(nccl().allGather(b + (size_t)c->rank * bytes, b, bytes, ncclUint8, c->comm, s), "ncclAllGather");
 }
 
 }  // namespace mb200

@@ -611,6 +611,23 @@ void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst
     MB_LAUNCH();
 }
 
+// bf16 rows [R][ld] (ld % 8 == 0) -> image: one 16 B unit per thread
+__global__ void k_rows_to_img(const uint16_t* __restrict__ rows, long ld, int R, int C, Img dst) {
+    const int CT = img_ct(C), cpr = (C + 7) / 8;
+    const long units = (long)R * cpr;
+    for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < units; u += (long)gridDim.x * blockDim.x) {
+        const int r = (int)(u / cpr), c = (int)(u - (long)r * cpr) * 8;
+        *reinterpret_cast<uint4*>(dst.p + img_off(r, c, CT)) = *reinterpret_cast<const uint4*>(rows + (long)r * ld + c);
+    }
+}
+void rows_to_img(const uint16_t* rows, long ld, int R, int C, const Img& dst, cudaStream_t s) {
+    if (ld % 8) throw ShapeError("rows_to_img: row stride must be a multiple of 8");
+    const long units = (long)R * ((C + 7) / 8);
+    if (units == 0) return;
+    k_rows_to_img<<<(unsigned)std::min<long>((units + 255) / 256, 148 * 16), 256, 0, s>>>(rows, ld, R, C, dst);
+    MB_LAUNCH();
+}
+
 // generated weights theta[g0 + z][woff_l + j * in_l + i] -> layer images of
 // group z (row j, col i), every layer of every group in one launch; one thread
 // per 8-column unit (32-byte fp32 reads, one 16-byte image store)
@@ -663,7 +680,7 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
 // a fixed order.
 constexpr int kGtSlices = 32, kGtUnits = 32;
 __global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const float* __restrict__ gt, long ld, int G,
-                                                                         int P, Img gimg, float* db) {
+                                                                         int P, Img gimg, float* db, uint16_t* rows) {
     __shared__ float part[kGtSlices][kGtUnits][9];
     const int ul = threadIdx.x % kGtUnits, sl = threadIdx.x / kGtUnits;
     const int CT = img_ct(gimg.C);
@@ -694,6 +711,7 @@ __global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const f
                 w.z = umma::pack_bf16(v[4], v[5]);
                 w.w = umma::pack_bf16(v[6], v[7]);
                 *reinterpret_cast<uint4*>(gimg.p + img_off(g, p0, CT)) = w;
+                if (rows) *reinterpret_cast<uint4*>(rows + (long)g * ld + p0) = w;
             }
         }
 #pragma unroll
@@ -708,13 +726,13 @@ __global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const f
         __syncthreads();
     }
 }
-void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s) {
-    if (ld % 4) throw ShapeError("gtheta_prep: row stride must be a multiple of 4");
+void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s, uint16_t* rows) {
+    if (ld % 8) throw ShapeError("gtheta_prep: row stride must be a multiple of 8");
     const long ngroups = ((P + 7) / 8 + kGtUnits - 1) / kGtUnits;
     static int sms = 0;
     if (!sms) MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     k_gtheta_prep<<<(unsigned)std::min<long>(ngroups, 2L * sms), kGtUnits * kGtSlices, 0, s>>>(gt, ld, G, P, gimg,
-                                                                                               db);
+                                                                                               db, rows);
     MB_LAUNCH();
 }
 

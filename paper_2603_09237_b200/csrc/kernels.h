@@ -93,8 +93,12 @@ void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s);
 void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
 void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
                   cudaStream_t s);
-// gtheta [G][ld] -> bf16 image + column sums db[P] (one pass)
-void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s);
+// gtheta [G][ld] -> bf16 image + column sums db[P] (one pass); optionally
+// also the bf16 rows row-major [G][ld] (the multi-GPU all-gather payload)
+void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s,
+                 uint16_t* rows_out = nullptr);
+// bf16 rows [R][ld] -> image (row r, col c), c < C
+void rows_to_img(const uint16_t* rows, long ld, int R, int C, const Img& dst, cudaStream_t s);
 struct MbGather {
     int Bp = 0, G = 0, od = 0, ad = 0, m = 0;
     const int *rows = nullptr, *goff = nullptr;

@@ -269,7 +269,22 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     parts = dalloc<float>((size_t)splits * G * F);
 }
 
+void HyperNet::enable_exchange(Comm* c) {
+    comm = c;
+    auto mk = [](int R, int C) {
+        Img im;
+        im.R = R;
+        im.C = C;
+        im.p = dalloc<uint8_t>((size_t)img_bytes(R, C));
+        return im;
+    };
+    gall = mk(G, (int)P);
+    fall = mk(G, F);
+    grows = dalloc<uint16_t>((size_t)G * ld);
+}
+
 void HyperNet::free_all() {
+    dfree(gall.p); dfree(fall.p); dfree(grows);
     dfree(p); dfree(g); dfree(m1); dfree(m2);
     for (auto& a : fact) dfree(a);
     for (auto& a : fgz) dfree(a);
@@ -363,8 +378,12 @@ void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, 
 // hypernet_backward (hypernet.cpp:92-122) summed over the clusters of the
 // last forward ([fg0, fg0 + fng), this rank's): db = sum_g gtheta_g,
 // dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then the feature-map
-// backward. Writes (not accumulates) the flat grad g; with several ranks it
-// is the rank's partial sum, all-reduced by the trainer before Adam.
+// backward. Writes (not accumulates) the flat grad g. With several ranks
+// (comm set) the result is the global gradient on every rank: the local
+// clusters' gtheta rows are all-gathered as bf16 (the dM GEMM's operand
+// precision) so dM runs over all clusters on every rank -- 2 B per cluster
+// row entry on the wire instead of an all-reduce of the 4 B x P x F dM --
+// while db and the feature-map gradient (small) are all-reduced.
 void HyperNet::backward(cudaStream_t s) {
     HyperNet* self = this;
     backward_multi(&self, 1, s);
@@ -373,7 +392,17 @@ void HyperNet::backward(cudaStream_t s) {
 void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
     for (int k = 0; k < nh; ++k) {  // gimg + db in one pass
         HyperNet& h = *hs[k];
-        gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg, h.g + h.nf + h.P * h.F, s);
+        gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg, h.g + h.nf + h.P * h.F, s,
+                    h.comm ? h.grows + (long)h.fg0 * h.ld : nullptr);
+    }
+    for (int k = 0; k < nh; ++k) {  // multi-GPU: every rank gets every cluster's theta gradient (bf16
+        HyperNet& h = *hs[k];        // rows, in place) and f(w), so dM needs no all-reduce
+        if (!h.comm) continue;
+        ProfScope ps("exchange", 0, 2.0 * h.G * h.ld, s);
+        comm_allreduce_f32(h.comm, h.g + h.nf + h.P * h.F, (size_t)h.P, s);  // db: the local sums
+        comm_allgather_bytes(h.comm, h.grows, sizeof(uint16_t) * (size_t)h.fng * h.ld, s);
+        rows_to_img(h.grows, h.ld, h.G, (int)h.P, h.gall, s);
+        to_img(h.fact.back(), h.F, 0, h.G, h.F, h.fall, 1, s);  // f(w) of all G clusters (every rank has it)
     }
     {
         IGemm ds[2];
@@ -398,10 +427,10 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
         for (int k = 0; k < nh; ++k) {
             HyperNet& h = *hs[k];
             if (h.adam_fused) continue;
-            IGemm& d = ds[nd++];  // dM[p][k] = sum_g gtheta[g][p] f[g][k]
-            d.A = h.gimg; d.a_view = 1;  // (m = p, k = g)
-            d.B = h.fimg; d.b_view = 1;  // (n = f, k = g)
-            d.M = (int)h.P; d.N = h.F; d.K = h.fng;
+            IGemm& d = ds[nd++];  // dM[p][k] = sum_g gtheta[g][p] f[g][k] (all G clusters with an exchange)
+            d.A = h.comm ? h.gall : h.gimg; d.a_view = 1;  // (m = p, k = g)
+            d.B = h.comm ? h.fall : h.fimg; d.b_view = 1;  // (n = f, k = g)
+            d.M = (int)h.P; d.N = h.F; d.K = h.comm ? h.G : h.fng;
             d.C = h.g + h.nf; d.cm = h.F; d.cn = 1;
             fl += 2.0 * d.M * d.N * d.K;
         }
@@ -414,7 +443,8 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
         HyperNet& h = *hs[k];
         if (!h.adam_fused) continue;
         DmAdam a;
-        a.gimg = h.gimg; a.fimg = h.fimg; a.G = h.fng; a.P = (int)h.P; a.F = h.F;
+        a.gimg = h.comm ? h.gall : h.gimg; a.fimg = h.comm ? h.fall : h.fimg;
+        a.G = h.comm ? h.G : h.fng; a.P = (int)h.P; a.F = h.F;
         a.p = h.p + h.nf; a.m1 = h.m1 + h.nf; a.m2 = h.m2 + h.nf; a.mimg = h.mimg;
         a.lr = h.ad_lr; a.ibc1 = h.ad_ibc1; a.ibc2 = h.ad_ibc2; a.err = h.ad_err;
         // HBM-bound: p, m1, m2 in + out (fp32), M image out (bf16), gtheta image in
@@ -435,6 +465,8 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
         ProfScope ps("feature_bwd", fl, 0, s);
         feature_backward_multi(jobs, nh, s);
     }
+    for (int k = 0; k < nh; ++k)  // the feature-map gradient: each rank's partial over its clusters
+        if (hs[k]->comm) comm_allreduce_f32(hs[k]->comm, hs[k]->g, (size_t)hs[k]->nf, s);
 }
 
 void HyperNet::adam_begin(double lr, const int* err) {
@@ -552,6 +584,10 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     actor_.init_params(root_.split(0xA1).key, s_);                        // train.cpp:67-70
     critic_.init_params(root_.split(0xA2).key, s_);
     alloc();
+    if (comm_) {  // per-minibatch exchange buffers (backward_multi)
+        actor_.enable_exchange(comm_);
+        critic_.enable_exchange(comm_);
+    }
     env_reset(es_.kind, Nl_, d_state, d_ekey, d_ectr, d_steps, root_.split(0xE0).key, inst_lo_, s_);
     perm_.resize((size_t)cfg.N * cfg.T);
     std::iota(perm_.begin(), perm_.end(), 0);  // train.cpp:112-114
@@ -1038,12 +1074,6 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
     segsum_multi(jb, goff, Kl_, s_);
 }
 
-void Trainer::allreduce_grad(HyperNet& h, cudaStream_t s) {
-    // the per-minibatch hypernetwork-gradient all-reduce: each rank's
-    // backward summed over its own clusters (linear in gtheta)
-    if (comm_) comm_allreduce_f32(comm_, h.g, (size_t)h.n, s);
-}
-
 // One PPO minibatch (train.cpp:163-180). The actor chain runs on s_, the
 // critic chain on s2_: the two losses / backward passes / Adam steps are
 // independent, so their many small kernels overlap. Joins: both losses are
@@ -1065,8 +1095,8 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     cudaStream_t sc = two ? s2_ : s_;
     const char* fe = std::getenv("MORLAX_FUSED_ADAM");  // "0": the unfused dM GEMM + Adam (A/B, tests)
     const bool fuse_env = !(fe && fe[0] == '0');
-    // no gradient exchange between backward and Adam; dm_adam's tile shape
-    const bool fuse = fuse_env && !comm_ && actor_.F % 64 == 0 && critic_.F % 64 == 0 && Kl_ <= 128;
+    // dm_adam's tile shape and K (all clusters: with an exchange dM sums every rank's rows)
+    const bool fuse = fuse_env && actor_.F % 64 == 0 && critic_.F % 64 == 0 && cfg_.K <= 128;
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
     if (Bp > 0) {
         MbGather ga;
@@ -1087,9 +1117,7 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
             actor_.adam_begin(cfg_.actor_lr, d_err);
             critic_.adam_begin(cfg_.critic_lr, d_err);
         }
-        HyperNet::backward_multi(both, 2, s_);
-        allreduce_grad(actor_, s_);
-        allreduce_grad(critic_, s_);
+        HyperNet::backward_multi(both, 2, s_);  // (with an exchange: its collectives inside, on s_)
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         critic_.adam_step(cfg_.critic_lr, d_err, s_);
         MB_CUDA(cudaEventRecord(ev_c_done_, s_));
@@ -1111,20 +1139,15 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         actor_.adam_begin(cfg_.actor_lr, d_err);
         critic_.adam_begin(cfg_.critic_lr, d_err);
     }
-    critic_.backward(sc);
-    if (comm_) {  // every NCCL call goes on s_: one stream per communicator, device order = host order
-        MB_CUDA(cudaEventRecord(ev_cb_, sc));
-        actor_.backward(s_);
-        MB_CUDA(cudaStreamWaitEvent(s_, ev_cb_, 0));
-        allreduce_grad(critic_, s_);
-        MB_CUDA(cudaEventRecord(ev_cr_, s_));
-        MB_CUDA(cudaStreamWaitEvent(sc, ev_cr_, 0));
-        critic_.adam_step(cfg_.critic_lr, d_err, sc);
-        MB_CUDA(cudaEventRecord(ev_c_done_, sc));
-        allreduce_grad(actor_, s_);
+    if (comm_) {  // the backward passes hold the exchange collectives: every NCCL call on s_ (one
+        // stream per communicator, device order = host order), both nets batched
+        HyperNet::backward_multi(both, 2, s_);
+        critic_.adam_step(cfg_.critic_lr, d_err, s_);
+        MB_CUDA(cudaEventRecord(ev_c_done_, s_));
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         return;
     }
+    critic_.backward(sc);
     critic_.adam_step(cfg_.critic_lr, d_err, sc);
     MB_CUDA(cudaEventRecord(ev_c_done_, sc));
     actor_.backward(s_);
@@ -1222,10 +1245,10 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
     const bool roles[2] = {true, false};
     net_step(both, roles, 2, Bp, inv_B, mx, d_rows, d_goff, 0, s_);
     if (comm_) comm_allreduce_f64(comm_, d_mbloss, 2, s_);
-    actor_.backward(s_);
-    critic_.backward(s_);
-    allreduce_grad(actor_, s_);
-    allreduce_grad(critic_, s_);
+    {  // (with an exchange: its collectives inside, on s_)
+        HyperNet* both[2] = {&actor_, &critic_};
+        HyperNet::backward_multi(both, 2, s_);
+    }
     double l[2];
     int err = 0;
     MB_CUDA(cudaMemcpyAsync(l, d_mbloss, sizeof(l), cudaMemcpyDeviceToHost, s_));

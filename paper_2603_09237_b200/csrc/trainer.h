@@ -98,6 +98,13 @@ struct HyperNet {
     bool adam_fused = false;
     float ad_lr = 0.f, ad_ibc1 = 0.f, ad_ibc2 = 0.f;
     const int* ad_err = nullptr;
+    // multi-GPU exchange (backward_multi): the local clusters' theta-gradient
+    // rows (bf16) are all-gathered into grows, re-tiled into gall / fall (all
+    // G clusters) for dM; db and the feature-map gradient are all-reduced
+    Comm* comm = nullptr;
+    Img gall, fall;
+    uint16_t* grows = nullptr;
+    void enable_exchange(Comm* c);
 };
 
 NetDims make_dims(const std::vector<int>& sizes, bool out_tanh, bool has_log_std);
@@ -182,7 +189,6 @@ private:
     void minibatch(int slot, int B, int Bglob, int maxg, const int* d_rows, const int* d_goff);
     void net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, float inv_B, int maxg, const int* rows,
                   const int* d_goff, int slot, cudaStream_t s);
-    void allreduce_grad(HyperNet& h, cudaStream_t s);
 
     TrainConfig cfg_;
     EnvSpecB es_{};

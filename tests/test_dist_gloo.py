@@ -7,9 +7,12 @@ trainer uses (trainer.cu: Trainer::phase_advantages / minibatch):
     (shard_minibatch, the C-ABI host helper) and scales by the GLOBAL 1/B;
   * the hypernetwork gradient is linear in the per-cluster theta gradients,
     so each rank's hypernet backward over its own clusters, summed across
-    ranks (the per-minibatch NCCL gradient all-reduce, Trainer::allreduce_grad),
-    equals the single-process gradient; Adam then runs replicated on the
-    identical all-reduced gradient.
+    ranks, equals the single-process gradient (checked on the losses);
+  * the exchange the trainer actually performs (HyperNet::backward_multi):
+    the per-cluster theta-gradient rows are all-gathered so every rank forms
+    dM (and db) over all clusters itself, and only the feature-map gradient
+    (and db) is all-reduced -- the result equals the single-process
+    hypernet_backward; Adam then runs replicated on identical gradients.
 
 Each rank computes with the fp64 C oracle; results are compared with the
 single-process oracle on the same seeded inputs."""
@@ -88,9 +91,31 @@ def _worker(rank, world, port, q):
                                        b["targets"])
             full = np.concatenate([[la_f, lc_f], ga_f, gc_f])
             v = vec.numpy()
-            q.put((float(err_norm), float(np.abs(v - full).max() / np.abs(full).max())))
+            err_grad = float(np.abs(v - full).max() / np.abs(full).max())
         else:
-            q.put((float(err_norm), 0.0))
+            err_grad = 0.0
+        # --- the exchange of HyperNet::backward_multi on seeded per-cluster theta gradients
+        Kl = K // world
+        gth = np.random.default_rng(100).normal(size=(K, a_s.P))  # every cluster's dloss / dtheta
+        mine = torch.tensor(gth[rank * Kl:(rank + 1) * Kl])
+        parts = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)  # the bf16-row all-gather (fp64 here)
+        rows_all = torch.cat(parts).numpy()
+        flat = t.actor_params()
+
+        def hb(ws, gs):  # hypernet_backward is per preference (hypernet.cpp:92-122): sum over clusters
+            return sum(o.hypernet_backward(a_s, flat, wv, gv) for wv, gv in zip(ws, gs))
+        g_all = hb(cw, rows_all)  # dM / db over every cluster, on every rank
+        g_loc = hb(cw[rank * Kl:(rank + 1) * Kl], gth[rank * Kl:(rank + 1) * Kl])
+        nfe = a_s.n_feature
+        feat = torch.tensor(g_loc[:nfe])
+        dist.all_reduce(feat)  # the feature-map gradient: per-rank partials
+        db_loc = torch.tensor(gth[rank * Kl:(rank + 1) * Kl].sum(0))
+        dist.all_reduce(db_loc)  # db: per-rank partial sums
+        got = np.concatenate([feat.numpy(), g_all[nfe:nfe + a_s.P * a_s.F], db_loc.numpy()])
+        ref = hb(cw, gth)
+        err_x = float(np.abs(got - ref).max() / np.abs(ref).max())
+        q.put((float(err_norm), max(err_grad, err_x)))
     finally:
         dist.destroy_process_group()
 

@@ -463,11 +463,15 @@ def test_evaluate_params_errors(mb):
         mb.evaluate_params(spec, flat, "mo-humanoid6", 4, 1, 1)
 
 
-def test_single_rank_nccl_path_matches(mb):
-    """The multi-GPU code path (NCCL all-reduces of the normalisation sums,
-    the losses and the hypernet gradients, all on one stream) with a
-    single-rank communicator gives bit-identical results to the no-NCCL run."""
-    cfg = mb.TrainConfig(env_name="mo-pointmass", N=64, K=4, T=16, epochs=2, minibatch_count=2, seed=5, F=16,
+@pytest.mark.parametrize("F", [16, 64])
+def test_single_rank_nccl_path_matches(mb, F):
+    """The multi-GPU code path (NCCL all-reduces of the normalisation sums
+    and the losses; the per-minibatch exchange: all-gather of the clusters'
+    bf16 theta-gradient rows re-tiled for dM, all-reduces of db and the
+    feature-map gradient; all on one stream) with a single-rank communicator
+    gives bit-identical results to the no-NCCL run. F = 64 takes the fused
+    dM + Adam kernel over the gathered rows."""
+    cfg = mb.TrainConfig(env_name="mo-pointmass", N=64, K=4, T=16, epochs=2, minibatch_count=2, seed=5, F=F,
                          feature_hidden=[16], actor_hidden=[32, 32], critic_hidden=[32, 32])
     a = mb.Trainer(cfg)
     b = mb.Trainer(cfg, 1, 0, mb.nccl_unique_id())
