@@ -38,6 +38,32 @@ extern std::atomic<long> g_kernel_launches;
         MB_CUDA(cudaGetLastError());                                       \
     } while (0)
 
+// ---- programmatic dependent launch ------------------------------------------
+// The update chain's kernels are launched with programmatic stream
+// serialization (launch_pdl): a kernel's launch is processed while its
+// predecessor drains (the predecessor's implicit trigger at completion), and
+// the kernel waits for the predecessor's completion and memory
+// (griddepcontrol.wait) only after its prologue. Measured: 22.9 vs 23.5 ms /
+// iteration. An early explicit trigger (griddepcontrol.launch_dependents at
+// kernel entry) was slower (24.0): waiting CTAs hold SMs the other update
+// stream could use. Without the launch attribute the wait is a no-op.
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();  // MORLAX_PDL != "0" (kernels.cu)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MB_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
 // ---- RNG: include/morlax/rng.hpp:18-93 -----------------------------------
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t kSeedTag = 0x5851F42D4C957F2DULL;

@@ -94,6 +94,7 @@ __device__ __forceinline__ void load_tile(const DmAdam& a, int t, int ntf, int K
 // state stream in while this tile's MMAs and updates run
 __global__ void __launch_bounds__(128) k_dm_adam(const __grid_constant__ DmAdam a, int ntiles, int ntf) {
     extern __shared__ __align__(128) uint8_t smem[];
+    pdl_enter();
     if (*a.err) return;  // non-finite loss: no update (k_adam_img)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rq = lane >> 2, q = lane & 3, mi = lane >> 3, mr = lane & 7;
@@ -183,7 +184,7 @@ void dm_adam(const DmAdam& a, cudaStream_t s) {
     static int sms = 0;
     if (!sms) MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int grid = std::min(ntiles, 2 * sms);  // two 108 KB blocks per SM
-    k_dm_adam<<<grid, 128, SMEM, s>>>(a, ntiles, ntf);
+    launch_pdl(k_dm_adam, dim3(grid), dim3(128), SMEM, s, a, ntiles, ntf);
     MB_LAUNCH();
 }
 

@@ -119,6 +119,7 @@ struct DenseBatch {
     int nx[4] = {1, 1, 1, 1};
 };
 __global__ void __launch_bounds__(256) k_dense16_multi(const __grid_constant__ DenseBatch b) {
+    pdl_enter();
     __shared__ __align__(16) float As[16][KC + 4];
     __shared__ __align__(16) float Bs[16][KC + 4];
     const int t = blockIdx.x;
@@ -136,7 +137,7 @@ void dense16_multi(const Dense16* ds, int n, cudaStream_t s) {
         b.base[k + 1] = b.base[k] + b.nx[k] * ((ds[k].R + 15) / 16);
     }
     if (b.base[n] == 0) return;
-    k_dense16_multi<<<b.base[n], 256, 0, s>>>(b);
+    launch_pdl(k_dense16_multi, dim3(b.base[n]), dim3(256), 0, s, b);
     MB_LAUNCH();
 }
 
@@ -151,6 +152,7 @@ void dense16(const Dense16& d, cudaStream_t s) {
 // (split slices) so 4x more loads are in flight, combined in a fixed order
 __global__ void __launch_bounds__(256) k_split_dtanh(const float* __restrict__ parts, int splits, long n,
                                                      const float* __restrict__ f, float* gz) {
+    pdl_enter();
     __shared__ float part[4][64];
     const int ol = threadIdx.x & 63, sl = threadIdx.x >> 6;
     const long i = blockIdx.x * 64L + ol;
@@ -215,7 +217,8 @@ void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s) {
         const FeatJob& j = jobs[k];
         if (j.fd->L != L) throw ShapeError("feature_backward_multi: the feature maps must have equal depth");
         const long n = (long)j.G * j.fd->sz[L];
-        k_split_dtanh<<<(unsigned)((n + 63) / 64), 256, 0, s>>>(j.parts, j.splits, n, j.fd->act[L], j.fd->gz[L - 1]);
+        launch_pdl(k_split_dtanh, dim3((unsigned)((n + 63) / 64)), dim3(256), 0, s, j.parts, j.splits, n,
+                   (const float*)j.fd->act[L], j.fd->gz[L - 1]);
         MB_LAUNCH();
     }
     for (int l = L - 1; l >= 0; --l) {

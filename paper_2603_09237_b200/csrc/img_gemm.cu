@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
+    pdl_enter();  // prologue done: wait for the predecessor's data
     const uint32_t tbase = *tslot;
     // the descriptor and tile coordinates of batch tile t
 #define MB_TILE(t)                                  \
@@ -495,7 +496,7 @@ void launch(const IGemm* ds, int n, cudaStream_t s) {
     const int ntiles = bt.base[n];
     if (ntiles == 0) return;
     const int grid = ntiles < 148 ? ntiles : 148;
-    k_img_gemm<BN, EPI><<<grid, C::NT, C::SMEM, s>>>(bt);
+    launch_pdl(k_img_gemm<BN, EPI>, dim3(grid), dim3(C::NT), C::SMEM, s, bt);
     MB_LAUNCH();
 }
 
@@ -553,6 +554,7 @@ void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, 
 // block z < G sums job j's tiles of cluster z (fixed order), block G sums
 // the per-tile loss partials (fp64, fixed tree) into *loss_out
 __global__ void k_segsum_multi(const __grid_constant__ SegJobs jb, const int* goff, int G) {
+    pdl_enter();
     const int z = blockIdx.x;
     if (z >= G) {  // one block per loss
         const SegLoss& L = jb.loss[z - G];
@@ -579,7 +581,7 @@ __global__ void k_segsum_multi(const __grid_constant__ SegJobs jb, const int* go
     }
 }
 void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s) {
-    k_segsum_multi<<<G + jb.nloss, 256, 0, s>>>(jb, goff, G);
+    launch_pdl(k_segsum_multi, dim3(G + jb.nloss), dim3(256), 0, s, jb, goff, G);
     MB_LAUNCH();
 }
 
@@ -633,6 +635,7 @@ void rows_to_img(const uint16_t* rows, long ld, int R, int C, const Img& dst, cu
 // per 8-column unit (32-byte fp32 reads, one 16-byte image store)
 __global__ void k_pack_weights(const float* __restrict__ theta, long ld, int g0, int ng, PackDims pd, uint8_t* wimg,
                                long gs) {
+    pdl_enter();
     const long per = pd.ustart[pd.L];
     for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < per * ng; u += (long)gridDim.x * blockDim.x) {
         const int z = (int)(u / per);
@@ -667,8 +670,8 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
                   cudaStream_t s) {
     const long n = pd.ustart[pd.L] * ng;
     if (n == 0) return;
-    k_pack_weights<<<(unsigned)std::min<long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(theta, ld, g0, ng, pd, wimg,
-                                                                                     gs);
+    launch_pdl(k_pack_weights, dim3((unsigned)std::min<long>((n + 255) / 256, 148 * 16)), dim3(256), 0, s, theta, ld,
+               g0, ng, pd, wimg, gs);
     MB_LAUNCH();
 }
 
@@ -681,6 +684,7 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
 constexpr int kGtSlices = 32, kGtUnits = 32;
 __global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const float* __restrict__ gt, long ld, int G,
                                                                          int P, Img gimg, float* db, uint16_t* rows) {
+    pdl_enter();
     __shared__ float part[kGtSlices][kGtUnits][9];
     const int ul = threadIdx.x % kGtUnits, sl = threadIdx.x / kGtUnits;
     const int CT = img_ct(gimg.C);
@@ -731,8 +735,8 @@ void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float*
     const long ngroups = ((P + 7) / 8 + kGtUnits - 1) / kGtUnits;
     static int sms = 0;
     if (!sms) MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    k_gtheta_prep<<<(unsigned)std::min<long>(ngroups, 2L * sms), kGtUnits * kGtSlices, 0, s>>>(gt, ld, G, P, gimg,
-                                                                                               db, rows);
+    launch_pdl(k_gtheta_prep, dim3((unsigned)std::min<long>(ngroups, 2L * sms)), dim3(kGtUnits * kGtSlices), 0, s, gt,
+               ld, G, P, gimg, db, rows);
     MB_LAUNCH();
 }
 
@@ -771,6 +775,7 @@ void gather_img(const int* rows, int Bp, const float* src, int width, const Img&
 // targets -> fp32 rows, the cluster -> rg
 __global__ void __launch_bounds__(128) k_gather_minibatch(const __grid_constant__ MbGather a) {
     __shared__ int srow[128], sz;
+    pdl_enter();
     const int q0 = blockIdx.x * 128, t = threadIdx.x;
     const int q = q0 + t;
     const int r = a.rows[q];
@@ -834,7 +839,7 @@ __global__ void __launch_bounds__(128) k_gather_minibatch(const __grid_constant_
 void gather_minibatch(const MbGather& a, cudaStream_t s) {
     if (a.Bp <= 0) return;
     if (a.Bp % 128) throw ShapeError("gather_minibatch: rows must be 128-padded per cluster");
-    k_gather_minibatch<<<a.Bp / 128, 128, 0, s>>>(a);
+    launch_pdl(k_gather_minibatch, dim3(a.Bp / 128), dim3(128), 0, s, a);
     MB_LAUNCH();
 }
 

@@ -11,6 +11,13 @@
 namespace mb200 {
 
 std::atomic<long> g_kernel_launches{0};
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MORLAX_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 // =========================================================================
 // K1: BatchedEnv reset / step (env.cpp:44-106). SoA state [sdim][N].
@@ -580,6 +587,7 @@ __global__ void __launch_bounds__(128, 4) k_head(HeadArgs a) {
     __shared__ uint2 swb[32][32];         // backward B: (k = d pair, n = h) per h n-tile / lane
     __shared__ float sb[16], red[4][16], redl[4][16];
     __shared__ float red2[4][256];
+    pdl_enter();
     const int H = a.H, out = a.out, KS = H >> 4, HT = H >> 3;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, rq = lane >> 2, q = lane & 3;
     const int z = a.rg[blockIdx.x * 128];  // groups are 128-row padded: one cluster per tile
@@ -838,11 +846,11 @@ void head(const HeadArgs& a, bool actor, cudaStream_t s) {
         throw ShapeError("head: needs hidden width % 16 == 0 (<= 256), 1 <= out <= 16");
     const unsigned tiles = (unsigned)(a.Bp / 128);
     if (a.out <= 8) {
-        if (actor) k_head<true, 1><<<tiles, 128, 0, s>>>(a);
-        else k_head<false, 1><<<tiles, 128, 0, s>>>(a);
+        if (actor) launch_pdl(k_head<true, 1>, dim3(tiles), dim3(128), 0, s, a);
+        else launch_pdl(k_head<false, 1>, dim3(tiles), dim3(128), 0, s, a);
     } else {
-        if (actor) k_head<true, 2><<<tiles, 128, 0, s>>>(a);
-        else k_head<false, 2><<<tiles, 128, 0, s>>>(a);
+        if (actor) launch_pdl(k_head<true, 2>, dim3(tiles), dim3(128), 0, s, a);
+        else launch_pdl(k_head<false, 2>, dim3(tiles), dim3(128), 0, s, a);
     }
     MB_LAUNCH();
 }
@@ -902,6 +910,7 @@ void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, floa
 __global__ void k_adam_img(long n4, float4* p, const float4* g, float4* m1, float4* m2, float lr, float ibc1,
                            float ibc2, const int* err, long m_lo, long m_hi, int F, Img mimg, long n, long hole_lo,
                            long hole_len) {
+    pdl_enter();
     if (*err) return;
     long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (i >= n4) {  // the n % 4 scalar tail (never inside the M block: it ends at b, after M)
@@ -950,9 +959,9 @@ void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, 
         throw ShapeError("adam_img: the skipped range must be 4-aligned (and excludes the image)");
     n -= hole_len;  // elements updated
     const long n4 = n / 4, threads = n4 + (n - 4 * n4);
-    k_adam_img<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(n4, (float4*)p, (const float4*)g, (float4*)m1,
-                                                                (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi,
-                                                                F, mimg, n, hole_lo, hole_len);
+    launch_pdl(k_adam_img, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, n4, (float4*)p,
+               (const float4*)g, (float4*)m1, (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi, F, mimg, n,
+               hole_lo, hole_len);
     MB_LAUNCH();
 }
 
