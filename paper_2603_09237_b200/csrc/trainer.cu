@@ -567,9 +567,10 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     Rl_ = (long)Nl_ * cfg.T;
     MB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
     MB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_c_done_, &ev_cb_, &ev_cr_})
+    for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_cd_[0], &ev_cd_[1], &ev_cb_, &ev_cr_})
         MB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    MB_CUDA(cudaEventRecord(ev_c_done_, s2_));
+    MB_CUDA(cudaEventRecord(ev_cd_[0], s2_));
+    MB_CUDA(cudaEventRecord(ev_cd_[1], s2_));
     // a communicator whenever an NCCL id is given (world == 1 included: the
     // single-rank collectives exercise the multi-GPU code path on one GPU)
     if (world > 1 || nccl_id) comm_ = comm_create(world, rank, nccl_id);
@@ -605,20 +606,22 @@ Trainer::~Trainer() {
     actor_.free_all();
     critic_.free_all();
     for (auto* p : {d_obs, d_act, d_lp, d_rew, d_val, d_nval, d_adv, d_tgt, d_sadv, d_state, d_tracker, d_cw,
-                    d_Z, d_lpo, d_sa, d_tg, d_lsg})
+                    d_lsg, mbb_[0].Z, mbb_[0].lpo, mbb_[0].sa, mbb_[0].tg, mbb_[1].Z, mbb_[1].lpo, mbb_[1].sa,
+                    mbb_[1].tg})
         if (p) cudaFree(p);
+    for (auto& b : mbb_) cudaFree(b.rg);
     for (auto* p : img_allocs_) cudaFree(p);
     for (auto& u : ub_) {
         for (float* q : u.pbias) cudaFree(q);
         cudaFree(u.psls);
         cudaFree(u.lossrows);
     }
-    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_c_done_, ev_cb_, ev_cr_})
+    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_cd_[0], ev_cd_[1], ev_cb_, ev_cr_})
         if (e) cudaEventDestroy(e);
     if (s2_) cudaStreamDestroy(s2_);
     for (auto& u : ub_) cudaFree(u.Zf);
     for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
-                    (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_rowgroup, (void*)d_lossrows,
+                    (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_lossrows,
                     (void*)d_mbloss, (void*)d_stats, (void*)d_scratch, (void*)d_retsum, (void*)d_retcnt,
                     (void*)d_pol_blob, (void*)d_cri_blob})
         if (p) cudaFree(p);
@@ -671,14 +674,17 @@ void Trainer::alloc() {
     cudaFree(d_rows);
     d_rows = dalloc<int>((size_t)slots * Bpmax_);
     cudaFree(d_rowgroup);
-    d_rowgroup = dalloc<int>(Bpmax_);
     for (float** f : {&d_Z, &d_lpo, &d_sa, &d_tg, &d_lsg}) cudaFree(*f);
-    d_Z = dalloc<float>((size_t)Bpmax_ * ad);
-    d_lpo = dalloc<float>(Bpmax_);
-    d_sa = dalloc<float>(Bpmax_);
-    d_tg = dalloc<float>((size_t)Bpmax_ * m);
+    for (auto& b : mbb_) {  // double-buffered minibatch inputs (see mbb_)
+        b.rg = dalloc<int>(Bpmax_);
+        b.Z = dalloc<float>((size_t)Bpmax_ * ad);
+        b.lpo = dalloc<float>(Bpmax_);
+        b.sa = dalloc<float>(Bpmax_);
+        b.tg = dalloc<float>((size_t)Bpmax_ * m);
+        b.Xi = new_img(Bpmax_, od);
+    }
     d_lsg = dalloc<float>((size_t)Bpmax_ * ad);
-    Xi_ = new_img(Bpmax_, od);
+    use_mb_bufs(0);
     for (int w = 0; w < 2; ++w) {
         const NetDims& nd = w == 0 ? actor_.tgt : critic_.tgt;
         for (int l = 0; l < nd.L; ++l) {
@@ -1085,6 +1091,11 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
 // MORLAX_FUSED_NETS=1: both nets in lockstep on one stream, every stage one
 // launch covering both (fewer, fuller launches but no overlap: 29.9 ms/iter).
 // Both losses are checked for finiteness before either Adam (train.cpp:174-178).
+void Trainer::use_mb_bufs(int p) {
+    const MbBufs& b = mbb_[p];
+    Xi_ = b.Xi; d_Z = b.Z; d_lpo = b.lpo; d_sa = b.sa; d_tg = b.tg; d_rowgroup = b.rg;
+}
+
 void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, const int* goff) {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
@@ -1097,7 +1108,9 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     const bool fuse_env = !(fe && fe[0] == '0');
     // dm_adam's tile shape and K (all clusters: with an exchange dM sums every rank's rows)
     const bool fuse = fuse_env && actor_.F % 64 == 0 && critic_.F % 64 == 0 && cfg_.K <= 128;
-    MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
+    mb_par_ ^= 1;  // this minibatch's input buffers were last read by the critic two minibatches back
+    use_mb_bufs(mb_par_);
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_cd_[mb_par_], 0));
     if (Bp > 0) {
         MbGather ga;
         ga.Bp = Bp; ga.G = Kl_; ga.od = od; ga.ad = ad; ga.m = m;
@@ -1120,7 +1133,7 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         HyperNet::backward_multi(both, 2, s_);  // (with an exchange: its collectives inside, on s_)
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         critic_.adam_step(cfg_.critic_lr, d_err, s_);
-        MB_CUDA(cudaEventRecord(ev_c_done_, s_));
+        MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], s_));
         return;
     }
     MB_CUDA(cudaEventRecord(ev_gather_, s_));
@@ -1143,13 +1156,13 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         // stream per communicator, device order = host order), both nets batched
         HyperNet::backward_multi(both, 2, s_);
         critic_.adam_step(cfg_.critic_lr, d_err, s_);
-        MB_CUDA(cudaEventRecord(ev_c_done_, s_));
+        MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], s_));
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         return;
     }
     critic_.backward(sc);
     critic_.adam_step(cfg_.critic_lr, d_err, sc);
-    MB_CUDA(cudaEventRecord(ev_c_done_, sc));
+    MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], sc));
     actor_.backward(s_);
     actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
 }
@@ -1172,7 +1185,8 @@ void Trainer::phase_update(int it, int max_minibatches) {
 }
 
 void Trainer::finish(IterStats* st) {
-    MB_CUDA(cudaStreamWaitEvent(s_, ev_c_done_, 0));
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_cd_[0], 0));
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_cd_[1], 0));
     const int slots = cfg_.epochs * cfg_.minibatch_count;
     std::vector<double> losses((size_t)slots * 2);
     std::vector<double> rs(Nl_);

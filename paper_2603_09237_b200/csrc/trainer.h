@@ -217,7 +217,18 @@ private:
         double* lossrows = nullptr;
     } ub_[2];
     cudaStream_t s2_ = nullptr;  // critic chain of the update
-    cudaEvent_t ev_gather_ = nullptr, ev_c_net_ = nullptr, ev_chk_ = nullptr, ev_c_done_ = nullptr;
+    cudaEvent_t ev_gather_ = nullptr, ev_c_net_ = nullptr, ev_chk_ = nullptr;
+    // the minibatch inputs (gathered rows) are double-buffered by minibatch
+    // parity, so the actor chain of minibatch i+1 only waits for the critic
+    // chain of minibatch i-1 (ev_cd_[parity]) before overwriting them
+    cudaEvent_t ev_cd_[2] = {nullptr, nullptr};
+    int mb_par_ = 0;
+    struct MbBufs {
+        Img Xi;
+        float *Z = nullptr, *lpo = nullptr, *sa = nullptr, *tg = nullptr;
+        int* rg = nullptr;
+    } mbb_[2];
+    void use_mb_bufs(int parity);  // point Xi_ / d_Z / ... at buffer set `parity`
     cudaEvent_t ev_cb_ = nullptr, ev_cr_ = nullptr;  // multi-GPU: critic backward done / its all-reduce done
     Img Xi_;                    // [Bp][obs] gathered observations (bf16 image)
     std::vector<uint8_t*> img_allocs_;
