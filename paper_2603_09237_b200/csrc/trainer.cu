@@ -389,84 +389,88 @@ void HyperNet::backward(cudaStream_t s) {
     backward_multi(&self, 1, s);
 }
 
-void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s) {
-    for (int k = 0; k < nh; ++k) {  // gimg + db in one pass
-        HyperNet& h = *hs[k];
-        gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg, h.g + h.nf + h.P * h.F, s,
-                    h.comm ? h.grows + (long)h.fg0 * h.ld : nullptr);
-    }
-    for (int k = 0; k < nh; ++k) {  // multi-GPU: every rank gets every cluster's theta gradient (bf16
-        HyperNet& h = *hs[k];        // rows, in place) and f(w), so dM needs no all-reduce
-        if (!h.comm) continue;
-        ProfScope ps("exchange", 0, 2.0 * h.G * h.ld, s);
-        comm_allreduce_f32(h.comm, h.g + h.nf + h.P * h.F, (size_t)h.P, s);  // db: the local sums
-        comm_allgather_bytes(h.comm, h.grows, sizeof(uint16_t) * (size_t)h.fng * h.ld, s);
-        rows_to_img(h.grows, h.ld, h.G, (int)h.P, h.gall, s);
-        to_img(h.fact.back(), h.F, 0, h.G, h.F, h.fall, 1, s);  // f(w) of all G clusters (every rank has it)
-    }
-    {
-        IGemm ds[2];
-        double fl = 0;
-        for (int k = 0; k < nh; ++k) {
+void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int part) {
+    if (part != 2) {  // the gradient passes (no parameter is written)
+        for (int k = 0; k < nh; ++k) {  // gimg + db in one pass
             HyperNet& h = *hs[k];
-            IGemm& d = ds[k];  // gf[g][k] = sum_p gtheta[g][p] M[p][k], split-K over 128-aligned P ranges
-            d.A = h.gimg; d.a_view = 0;  // (m = g, k = p)
-            d.B = h.mimg; d.b_view = 1;  // (n = f, k = p)
-            d.M = h.fng; d.N = h.F; d.K = (int)h.P; d.Z = h.splits;
-            d.gmode = 2; d.goff = h.d_split_bounds;
-            d.C = h.parts; d.cm = h.F; d.cn = 1; d.c_gs = (long)h.fng * h.F;
-            fl += 2.0 * d.M * d.N * d.K;
+            gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg, h.g + h.nf + h.P * h.F, s,
+                        h.comm ? h.grows + (long)h.fg0 * h.ld : nullptr);
         }
-        ProfScope ps("hyper_df", fl, 0, s);
-        img_gemm_batch(ds, nh, s);
+        for (int k = 0; k < nh; ++k) {  // multi-GPU: every rank gets every cluster's theta gradient (bf16
+            HyperNet& h = *hs[k];        // rows, in place) and f(w), so dM needs no all-reduce
+            if (!h.comm) continue;
+            ProfScope ps("exchange", 0, 2.0 * h.G * h.ld, s);
+            comm_allreduce_f32(h.comm, h.g + h.nf + h.P * h.F, (size_t)h.P, s);  // db: the local sums
+            comm_allgather_bytes(h.comm, h.grows, sizeof(uint16_t) * (size_t)h.fng * h.ld, s);
+            rows_to_img(h.grows, h.ld, h.G, (int)h.P, h.gall, s);
+            to_img(h.fact.back(), h.F, 0, h.G, h.F, h.fall, 1, s);  // f(w) of all G clusters (every rank has it)
+        }
+        {
+            IGemm ds[2];
+            double fl = 0;
+            for (int k = 0; k < nh; ++k) {
+                HyperNet& h = *hs[k];
+                IGemm& d = ds[k];  // gf[g][k] = sum_p gtheta[g][p] M[p][k], split-K over 128-aligned P ranges
+                d.A = h.gimg; d.a_view = 0;  // (m = g, k = p)
+                d.B = h.mimg; d.b_view = 1;  // (n = f, k = p)
+                d.M = h.fng; d.N = h.F; d.K = (int)h.P; d.Z = h.splits;
+                d.gmode = 2; d.goff = h.d_split_bounds;
+                d.C = h.parts; d.cm = h.F; d.cn = 1; d.c_gs = (long)h.fng * h.F;
+                fl += 2.0 * d.M * d.N * d.K;
+            }
+            ProfScope ps("hyper_df", fl, 0, s);
+            img_gemm_batch(ds, nh, s);
+        }
+        {  // df reduction + feature-map backward (all layers' dW, db) over the local rows
+            double fl = 0;
+            FeatDims fl_d[2];
+            FeatJob jobs[2];
+            for (int k = 0; k < nh; ++k) {
+                HyperNet& h = *hs[k];
+                for (size_t l = 0; l + 1 < h.fsz.size(); ++l) fl += 4.0 * h.fng * h.fsz[l] * h.fsz[l + 1];
+                fl_d[k] = h.fd;
+                for (int l = 0; l <= h.fd.L; ++l) fl_d[k].act[l] = h.fd.act[l] + (long)h.fg0 * h.fd.sz[l];
+                jobs[k] = FeatJob{&fl_d[k], h.p, h.w_last + (long)h.fg0 * h.m, h.fng, Img{}, 0, 0, h.parts, h.splits, h.g};
+            }
+            ProfScope ps("feature_bwd", fl, 0, s);
+            feature_backward_multi(jobs, nh, s);
+        }
+        for (int k = 0; k < nh; ++k)  // the feature-map gradient: each rank's partial over its clusters
+            if (hs[k]->comm) comm_allreduce_f32(hs[k]->comm, hs[k]->g, (size_t)hs[k]->nf, s);
     }
-    {
-        IGemm ds[2];
-        double fl = 0;
-        int nd = 0;
-        for (int k = 0; k < nh; ++k) {
+    if (part != 1) {  // dM and, fused, the M-block Adam (after the losses' finiteness check)
+        {
+            IGemm ds[2];
+            double fl = 0;
+            int nd = 0;
+            for (int k = 0; k < nh; ++k) {
+                HyperNet& h = *hs[k];
+                if (h.adam_fused) continue;
+                IGemm& d = ds[nd++];  // dM[p][k] = sum_g gtheta[g][p] f[g][k] (all G clusters with an exchange)
+                d.A = h.comm ? h.gall : h.gimg; d.a_view = 1;  // (m = p, k = g)
+                d.B = h.comm ? h.fall : h.fimg; d.b_view = 1;  // (n = f, k = g)
+                d.M = (int)h.P; d.N = h.F; d.K = h.comm ? h.G : h.fng;
+                d.C = h.g + h.nf; d.cm = h.F; d.cn = 1;
+                fl += 2.0 * d.M * d.N * d.K;
+            }
+            if (nd) {
+                ProfScope ps("hyper_dM", fl, 0, s);
+                img_gemm_batch(ds, nd, s);
+            }
+        }
+        for (int k = 0; k < nh; ++k) {  // single rank: dM consumed by Adam in registers (dm_adam.cu)
             HyperNet& h = *hs[k];
-            if (h.adam_fused) continue;
-            IGemm& d = ds[nd++];  // dM[p][k] = sum_g gtheta[g][p] f[g][k] (all G clusters with an exchange)
-            d.A = h.comm ? h.gall : h.gimg; d.a_view = 1;  // (m = p, k = g)
-            d.B = h.comm ? h.fall : h.fimg; d.b_view = 1;  // (n = f, k = g)
-            d.M = (int)h.P; d.N = h.F; d.K = h.comm ? h.G : h.fng;
-            d.C = h.g + h.nf; d.cm = h.F; d.cn = 1;
-            fl += 2.0 * d.M * d.N * d.K;
-        }
-        if (nd) {
-            ProfScope ps("hyper_dM", fl, 0, s);
-            img_gemm_batch(ds, nd, s);
+            if (!h.adam_fused) continue;
+            DmAdam a;
+            a.gimg = h.comm ? h.gall : h.gimg; a.fimg = h.comm ? h.fall : h.fimg;
+            a.G = h.comm ? h.G : h.fng; a.P = (int)h.P; a.F = h.F;
+            a.p = h.p + h.nf; a.m1 = h.m1 + h.nf; a.m2 = h.m2 + h.nf; a.mimg = h.mimg;
+            a.lr = h.ad_lr; a.ibc1 = h.ad_ibc1; a.ibc2 = h.ad_ibc2; a.err = h.ad_err;
+            // HBM-bound: p, m1, m2 in + out (fp32), M image out (bf16), gtheta image in
+            ProfScope ps("dm_adam", 0, 26.0 * h.P * h.F + 2.0 * h.P * h.fng, s);
+            dm_adam(a, s);
         }
     }
-    for (int k = 0; k < nh; ++k) {  // single rank: dM consumed by Adam in registers (dm_adam.cu)
-        HyperNet& h = *hs[k];
-        if (!h.adam_fused) continue;
-        DmAdam a;
-        a.gimg = h.comm ? h.gall : h.gimg; a.fimg = h.comm ? h.fall : h.fimg;
-        a.G = h.comm ? h.G : h.fng; a.P = (int)h.P; a.F = h.F;
-        a.p = h.p + h.nf; a.m1 = h.m1 + h.nf; a.m2 = h.m2 + h.nf; a.mimg = h.mimg;
-        a.lr = h.ad_lr; a.ibc1 = h.ad_ibc1; a.ibc2 = h.ad_ibc2; a.err = h.ad_err;
-        // HBM-bound: p, m1, m2 in + out (fp32), M image out (bf16), gtheta image in
-        ProfScope ps("dm_adam", 0, 26.0 * h.P * h.F + 2.0 * h.P * h.fng, s);
-        dm_adam(a, s);
-    }
-    {  // df reduction + feature-map backward (all layers' dW, db) over the local rows
-        double fl = 0;
-        FeatDims fl_d[2];
-        FeatJob jobs[2];
-        for (int k = 0; k < nh; ++k) {
-            HyperNet& h = *hs[k];
-            for (size_t l = 0; l + 1 < h.fsz.size(); ++l) fl += 4.0 * h.fng * h.fsz[l] * h.fsz[l + 1];
-            fl_d[k] = h.fd;
-            for (int l = 0; l <= h.fd.L; ++l) fl_d[k].act[l] = h.fd.act[l] + (long)h.fg0 * h.fd.sz[l];
-            jobs[k] = FeatJob{&fl_d[k], h.p, h.w_last + (long)h.fg0 * h.m, h.fng, Img{}, 0, 0, h.parts, h.splits, h.g};
-        }
-        ProfScope ps("feature_bwd", fl, 0, s);
-        feature_backward_multi(jobs, nh, s);
-    }
-    for (int k = 0; k < nh; ++k)  // the feature-map gradient: each rank's partial over its clusters
-        if (hs[k]->comm) comm_allreduce_f32(hs[k]->comm, hs[k]->g, (size_t)hs[k]->nf, s);
 }
 
 void HyperNet::adam_begin(double lr, const int* err) {
@@ -1141,8 +1145,13 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     critic_.forward(d_cw, g_lo_, Kl_, sc);
     net_step(&both[1], &roles[1], 1, Bp, inv_B, maxg, rows, goff, slot, sc);
     MB_CUDA(cudaEventRecord(ev_c_net_, sc));
+    // the gradient passes of the backward write no parameter: each chain runs
+    // them before the finiteness join (with an exchange they hold NCCL calls:
+    // below, on s_)
+    if (!comm_) HyperNet::backward_multi(&both[1], 1, sc, 1);
     actor_.forward(d_cw, g_lo_, Kl_, s_);
     net_step(&both[0], &roles[0], 1, Bp, inv_B, maxg, rows, goff, slot, s_);
+    if (!comm_) HyperNet::backward_multi(&both[0], 1, s_, 1);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_net_, 0));
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
@@ -1160,10 +1169,10 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         return;
     }
-    critic_.backward(sc);
+    HyperNet::backward_multi(&both[1], 1, sc, 2);
     critic_.adam_step(cfg_.critic_lr, d_err, sc);
     MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], sc));
-    actor_.backward(s_);
+    HyperNet::backward_multi(&both[0], 1, s_, 2);
     actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
 }
 

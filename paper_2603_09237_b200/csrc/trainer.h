@@ -87,7 +87,9 @@ struct HyperNet {
     void forward(const float* w, int g0, int ng, cudaStream_t s);
     // the same for nh (1 or 2) hypernetworks in lockstep, one launch per stage
     static void forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s);
-    static void backward_multi(HyperNet* const* hs, int nh, cudaStream_t s);
+    // part 0: all; 1: the gradient passes (gtheta image, exchange, df,
+    // feature map); 2: dM (+ the fused M-block Adam), after part 1
+    static void backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int part = 0);
     // grads from gtheta [G][P] (all groups) -> g
     void backward(cudaStream_t s);
     void adam_step(double lr, const int* err, cudaStream_t s);
