@@ -571,10 +571,12 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     Rl_ = (long)Nl_ * cfg.T;
     MB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
     MB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_cd_[0], &ev_cd_[1], &ev_cb_, &ev_cr_})
+    MB_CUDA(cudaStreamCreateWithFlags(&s3_, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_cd_[0], &ev_cd_[1], &ev_ad_[0], &ev_ad_[1],
+                           &ev_cfin_, &ev_cb_, &ev_cr_})
         MB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    MB_CUDA(cudaEventRecord(ev_cd_[0], s2_));
-    MB_CUDA(cudaEventRecord(ev_cd_[1], s2_));
+    for (cudaEvent_t e : {ev_cd_[0], ev_cd_[1], ev_cfin_}) MB_CUDA(cudaEventRecord(e, s2_));
+    for (cudaEvent_t e : {ev_ad_[0], ev_ad_[1]}) MB_CUDA(cudaEventRecord(e, s_));
     // a communicator whenever an NCCL id is given (world == 1 included: the
     // single-rank collectives exercise the multi-GPU code path on one GPU)
     if (world > 1 || nccl_id) comm_ = comm_create(world, rank, nccl_id);
@@ -620,9 +622,11 @@ Trainer::~Trainer() {
         cudaFree(u.psls);
         cudaFree(u.lossrows);
     }
-    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_cd_[0], ev_cd_[1], ev_cb_, ev_cr_})
+    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_cd_[0], ev_cd_[1], ev_ad_[0], ev_ad_[1], ev_cfin_, ev_cb_,
+                   ev_cr_})
         if (e) cudaEventDestroy(e);
     if (s2_) cudaStreamDestroy(s2_);
+    if (s3_) cudaStreamDestroy(s3_);
     for (auto& u : ub_) cudaFree(u.Zf);
     for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
                     (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_lossrows,
@@ -1112,66 +1116,74 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     const bool fuse_env = !(fe && fe[0] == '0');
     // dm_adam's tile shape and K (all clusters: with an exchange dM sums every rank's rows)
     const bool fuse = fuse_env && actor_.F % 64 == 0 && critic_.F % 64 == 0 && cfg_.K <= 128;
-    mb_par_ ^= 1;  // this minibatch's input buffers were last read by the critic two minibatches back
+    if (fuse) {  // host-side Adam step counters / bias corrections for the fused M-block update
+        actor_.adam_begin(cfg_.actor_lr, d_err);
+        critic_.adam_begin(cfg_.critic_lr, d_err);
+    }
+    // the minibatch rows are gathered on their own stream into the input
+    // buffer set of this parity, once both chains' losses of two minibatches
+    // back (the set's last readers) are done; each chain waits only for it
+    mb_par_ ^= 1;
     use_mb_bufs(mb_par_);
-    MB_CUDA(cudaStreamWaitEvent(s_, ev_cd_[mb_par_], 0));
+    MB_CUDA(cudaStreamWaitEvent(s3_, ev_ad_[mb_par_], 0));
+    MB_CUDA(cudaStreamWaitEvent(s3_, ev_cd_[mb_par_], 0));
     if (Bp > 0) {
         MbGather ga;
         ga.Bp = Bp; ga.G = Kl_; ga.od = od; ga.ad = ad; ga.m = m;
         ga.rows = rows; ga.goff = goff;
         ga.obs = d_obs; ga.act = d_act; ga.lp = d_lp; ga.sadv = d_sadv; ga.tgt = d_tgt;
         ga.Xi = Xi_; ga.act_o = d_Z; ga.lp_o = d_lpo; ga.sadv_o = d_sa; ga.tgt_o = d_tg; ga.rg = d_rowgroup;
-        gather_minibatch(ga, s_);
+        gather_minibatch(ga, s3_);
     }
+    MB_CUDA(cudaEventRecord(ev_gather_, s3_));
     HyperNet* both[2] = {&actor_, &critic_};
     const bool roles[2] = {true, false};
     if (!two) {
         HyperNet::forward_multi(both, 2, d_cw, g_lo_, Kl_, s_);  // hypernet_forward per loss (losses.cpp:79,167)
+        MB_CUDA(cudaStreamWaitEvent(s_, ev_gather_, 0));
         net_step(both, roles, 2, Bp, inv_B, maxg, rows, goff, slot, s_);
+        MB_CUDA(cudaEventRecord(ev_ad_[mb_par_], s_));
+        MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], s_));
         if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
         check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
-        if (fuse) {
-            actor_.adam_begin(cfg_.actor_lr, d_err);
-            critic_.adam_begin(cfg_.critic_lr, d_err);
-        }
         HyperNet::backward_multi(both, 2, s_);  // (with an exchange: its collectives inside, on s_)
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         critic_.adam_step(cfg_.critic_lr, d_err, s_);
-        MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], s_));
+        MB_CUDA(cudaEventRecord(ev_cfin_, s_));
         return;
     }
-    MB_CUDA(cudaEventRecord(ev_gather_, s_));
-    MB_CUDA(cudaStreamWaitEvent(sc, ev_gather_, 0));
+    // the forwards (feature map, theta, weight packing) need no minibatch rows
     critic_.forward(d_cw, g_lo_, Kl_, sc);
+    MB_CUDA(cudaStreamWaitEvent(sc, ev_gather_, 0));
     net_step(&both[1], &roles[1], 1, Bp, inv_B, maxg, rows, goff, slot, sc);
     MB_CUDA(cudaEventRecord(ev_c_net_, sc));
+    MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], sc));
     // the gradient passes of the backward write no parameter: each chain runs
     // them before the finiteness join (with an exchange they hold NCCL calls:
     // below, on s_)
     if (!comm_) HyperNet::backward_multi(&both[1], 1, sc, 1);
     actor_.forward(d_cw, g_lo_, Kl_, s_);
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_gather_, 0));
     net_step(&both[0], &roles[0], 1, Bp, inv_B, maxg, rows, goff, slot, s_);
+    MB_CUDA(cudaEventRecord(ev_ad_[mb_par_], s_));
     if (!comm_) HyperNet::backward_multi(&both[0], 1, s_, 1);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_net_, 0));
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
     MB_CUDA(cudaEventRecord(ev_chk_, s_));
     MB_CUDA(cudaStreamWaitEvent(sc, ev_chk_, 0));
-    if (fuse) {
-        actor_.adam_begin(cfg_.actor_lr, d_err);
-        critic_.adam_begin(cfg_.critic_lr, d_err);
-    }
     if (comm_) {  // the backward passes hold the exchange collectives: every NCCL call on s_ (one
         // stream per communicator, device order = host order), both nets batched
         HyperNet::backward_multi(both, 2, s_);
         critic_.adam_step(cfg_.critic_lr, d_err, s_);
-        MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], s_));
+        MB_CUDA(cudaEventRecord(ev_cfin_, s_));
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
+        MB_CUDA(cudaStreamWaitEvent(sc, ev_cfin_, 0));  // the critic's next forward reads its new params
         return;
     }
     HyperNet::backward_multi(&both[1], 1, sc, 2);
     critic_.adam_step(cfg_.critic_lr, d_err, sc);
-    MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], sc));
+    MB_CUDA(cudaEventRecord(ev_cfin_, sc));
     HyperNet::backward_multi(&both[0], 1, s_, 2);
     actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
 }
@@ -1181,6 +1193,10 @@ void Trainer::phase_update(int it, int max_minibatches) {
     (void)it;
     const int mbs = cfg_.minibatch_count;
     mb_done_ = 0;
+    // the gathers (stream s3_) read the rollout / advantages and the uploaded
+    // minibatch index lists, all produced on s_
+    MB_CUDA(cudaEventRecord(ev_gather_, s_));
+    MB_CUDA(cudaStreamWaitEvent(s3_, ev_gather_, 0));
     // every rank refreshes theta for its clusters from the current params
     for (int e = 0; e < cfg_.epochs; ++e)
         for (int s = 0; s < mbs; ++s) {
@@ -1194,8 +1210,7 @@ void Trainer::phase_update(int it, int max_minibatches) {
 }
 
 void Trainer::finish(IterStats* st) {
-    MB_CUDA(cudaStreamWaitEvent(s_, ev_cd_[0], 0));
-    MB_CUDA(cudaStreamWaitEvent(s_, ev_cd_[1], 0));
+    MB_CUDA(cudaStreamWaitEvent(s_, ev_cfin_, 0));  // the critic chain's last Adam
     const int slots = cfg_.epochs * cfg_.minibatch_count;
     std::vector<double> losses((size_t)slots * 2);
     std::vector<double> rs(Nl_);

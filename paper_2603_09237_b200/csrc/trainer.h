@@ -221,9 +221,11 @@ private:
     cudaStream_t s2_ = nullptr;  // critic chain of the update
     cudaEvent_t ev_gather_ = nullptr, ev_c_net_ = nullptr, ev_chk_ = nullptr;
     // the minibatch inputs (gathered rows) are double-buffered by minibatch
-    // parity, so the actor chain of minibatch i+1 only waits for the critic
-    // chain of minibatch i-1 (ev_cd_[parity]) before overwriting them
-    cudaEvent_t ev_cd_[2] = {nullptr, nullptr};
+    // parity: the gather of minibatch i+1 (stream s3_) waits only for the two
+    // chains' losses of minibatch i-1 (ev_ad_ / ev_cd_[parity])
+    cudaEvent_t ev_cd_[2] = {nullptr, nullptr}, ev_ad_[2] = {nullptr, nullptr};  // critic / actor done with set p
+    cudaEvent_t ev_cfin_ = nullptr;  // the critic chain's last Adam
+    cudaStream_t s3_ = nullptr;      // the minibatch gathers
     int mb_par_ = 0;
     struct MbBufs {
         Img Xi;
