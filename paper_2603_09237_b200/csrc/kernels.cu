@@ -154,9 +154,95 @@ __global__ void k_gae(int N, int T, int m, const float* __restrict__ rew, const 
     }
 }
 
+// The same recurrence for short horizons, one block per kGaeInst instances:
+// their T x m blocks of every input (contiguous in the row-major [row][m]
+// layout) are staged through shared memory with coalesced loads, then one
+// thread per (instance, objective) runs the backward recurrence
+// sequentially from shared memory (instance stride padded so the m x
+// kGaeInst threads hit distinct banks), and advantages / targets leave with
+// coalesced stores. (The warp-scan kernel above reads m-strided words and
+// spends its issue slots on shuffles; at T = 64 the sequential pass is
+// shorter than the scan.) Same arithmetic per (instance, objective).
+constexpr int kGaeInst = 8;
+__global__ void __launch_bounds__(256) k_gae_inst(int N, int T, int m, int stride, const float* __restrict__ rew,
+                                                   const float* __restrict__ val, const float* __restrict__ nval,
+                                                   const uint8_t* __restrict__ term,
+                                                   const uint8_t* __restrict__ trunc, float gamma, float lambda,
+                                                   float* adv, float* tgt) {
+    extern __shared__ float gsm[];
+    const int tm = T * m;
+    float* R = gsm;  // rew -> adv
+    float* V = R + kGaeInst * stride;
+    float* X = V + kGaeInst * stride;  // next value -> target
+    uint8_t* FL = reinterpret_cast<uint8_t*>(X + kGaeInst * stride);  // bit 0 term, bit 1 trunc
+    const int i0 = blockIdx.x * kGaeInst;
+    const int ni = min(kGaeInst, N - i0);
+    const long b = (long)i0 * tm;
+    const int n = ni * tm;
+    for (int e0 = 0; e0 < n; e0 += 256 * 4) {  // 12 loads in flight per thread before the smem stores
+        float lr[4], lv[4], lx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * 256 + threadIdx.x;
+            if (e < n) {
+                lr[u] = rew[b + e];
+                lv[u] = val[b + e];
+                lx[u] = nval[b + e];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * 256 + threadIdx.x;
+            if (e < n) {
+                const int w = e / tm, o = w * stride + (e - w * tm);
+                R[o] = lr[u];
+                V[o] = lv[u];
+                X[o] = lx[u];
+            }
+        }
+    }
+    for (int e = threadIdx.x; e < ni * T; e += blockDim.x)
+        FL[e] = (term[(long)i0 * T + e] ? 1 : 0) | (trunc[(long)i0 * T + e] ? 2 : 0);
+    __syncthreads();
+    if (threadIdx.x < ni * m) {
+        const int w = threadIdx.x / m, k = threadIdx.x - w * m;
+        float* r = R + w * stride + k;
+        const float* v = V + w * stride + k;
+        float* x = X + w * stride + k;
+        const uint8_t* fl = FL + w * T;
+        const float gl = gamma * lambda;
+        float carry = 0.f;  // gae.cpp:40-60
+#pragma unroll 8
+        for (int t = T - 1; t >= 0; --t) {
+            const int f = fl[t];
+            const float boot = (f & 1) ? 0.f : 1.f;
+            const float cont = f ? 0.f : 1.f;
+            const float vt = v[t * m];
+            const float delta = r[t * m] + gamma * x[t * m] * boot - vt;
+            carry = delta + gl * cont * carry;
+            r[t * m] = carry;
+            x[t * m] = carry + vt;
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < ni * tm; e += blockDim.x) {
+        const int w = e / tm, o = w * stride + (e - w * tm);
+        adv[b + e] = R[o];
+        tgt[b + e] = X[o];
+    }
+}
+
 void gae_scan(int N, int T, int m, const float* reward, const float* value, const float* next_value,
               const uint8_t* term, const uint8_t* trunc, float gamma, float lambda, float* adv,
               float* targets, cudaStream_t s) {
+    const int tm = T * m, stride = tm + ((m - tm) % 32 + 32) % 32;  // stride = m (mod 32)
+    const size_t sm = sizeof(float) * 3 * (size_t)kGaeInst * stride + (size_t)kGaeInst * T;
+    if (T <= 256 && m * kGaeInst <= 256 && sm <= 48 * 1024) {
+        k_gae_inst<<<(N + kGaeInst - 1) / kGaeInst, 256, sm, s>>>(N, T, m, stride, reward, value, next_value, term,
+                                                                   trunc, gamma, lambda, adv, targets);
+        MB_LAUNCH();
+        return;
+    }
     const long warps = (long)N * m;
     k_gae<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(N, T, m, reward, value, next_value, term,
                                                           trunc, gamma, lambda, adv, targets);

@@ -3,6 +3,8 @@
 // generation -> fused rollout -> GAE / normalise / scalarise -> epochs x
 // minibatches of {actor loss, critic loss through the hypernetwork, Adam}.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1299,10 +1301,26 @@ void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
 
 void Trainer::iteration(int it, IterStats* st) {
     g_prof = &prof_;
+    static const bool host_timing = [] {  // MORLAX_HOST_TIMING=1: host enqueue time per phase (stderr)
+        const char* e = std::getenv("MORLAX_HOST_TIMING");
+        return e && e[0] == '1';
+    }();
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     phase_rollout(it);
+    const auto t1 = clk::now();
     phase_advantages();
+    const auto t2 = clk::now();
     phase_update(it);
+    const auto t3 = clk::now();
     finish(st);
+    if (host_timing) {
+        const auto ms = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        std::fprintf(stderr, "host enqueue ms: rollout %.3f advantages %.3f update %.3f | total with sync %.3f\n",
+                     ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t0, clk::now()));
+    }
 }
 
 }  // namespace mb200
