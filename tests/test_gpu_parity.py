@@ -153,10 +153,12 @@ def test_group_policy_forward(mb, o, F, fh, ah, od, ad, m, G, R):
 
 
 # ------------------------------------------------------------------ GAE / normalise (K4)
-@pytest.mark.parametrize("T", [1, 16, 32, 64, 100])
-def test_gae_scan_parity(mb, o, T):
+# (T <= 256 with the staged blocks under 48 KB: the per-instance staged
+# kernel; T = 300 and the m = 8, T = 64 case: the warp-scan kernel)
+@pytest.mark.parametrize("T,m", [(1, 6), (16, 6), (32, 6), (64, 6), (100, 6), (300, 6), (64, 2), (64, 8)])
+def test_gae_scan_parity(mb, o, T, m):
     rng = np.random.default_rng(T)
-    N, m = 37, 6
+    N = 37
     r, v, nv = (r32(rng.normal(size=(N * T, m))) for _ in range(3))
     u = rng.random(N * T)
     te = (u < 0.03).astype(np.uint8)
