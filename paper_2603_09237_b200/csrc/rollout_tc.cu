@@ -30,6 +30,22 @@ constexpr int RNT = 256;  // threads
 constexpr int RE = 64;    // instances per CTA
 constexpr int OUT_COL = 128;
 
+#ifdef MB_ROLL_PROF  // phase timing of CTA 0 (debug builds only: NVCC="nvcc -DMB_ROLL_PROF")
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define RPROF(k)                                            \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {              \
+        const unsigned long long now_ = gtimer();           \
+        prof_[k] += now_ - prof_last_;                      \
+        prof_last_ = now_;                                  \
+    }
+#else
+#define RPROF(k)
+#endif
+
 __device__ __forceinline__ float sech2(float z) {
     const float e = __expf(-2.f * fabsf(z));
     const float d = 1.f + e;
@@ -233,6 +249,9 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
     const int warp = tid >> 5, lane = tid & 31;
     const uint32_t xsbo = (uint32_t)a.pol_plan.kin_pad[0] * 16;
 
+#ifdef MB_ROLL_PROF
+    unsigned long long prof_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, prof_last_ = gtimer();
+#endif
     for (int t = 0; t < a.T; ++t) {
         // ---- observation -> layer-0 operand (bf16, MN-major) + batch.obs
         for (int e = tid; e < nr * od; e += RNT) {
@@ -244,8 +263,10 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         }
         umma::fence_proxy_async();
         __syncthreads();
+        RPROF(0);
         // ---- policy
         run_net(a, x, is, VF, c, 0, th);
+        RPROF(1);
         if (warp < 4) {  // M = 64 output layout: env = 16*warp + lane (lanes < 16)
             float v[16];
             umma::tmem_ld16(x.tbase + ((uint32_t)(warp * 32) << 16) + OUT_COL, v);
@@ -255,27 +276,30 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         }
         umma::fence_before_sync();
         __syncthreads();
+        RPROF(2);
         // ---- Gaussian sample, 2 words per dim (nn.cpp:192-202, rng.hpp:55-60)
         for (int e = tid; e < nr * ad; e += RNT) {
             const int r = e / ad, d = e % ad;
             const uint64_t base = 2ull * ((uint64_t)t * ad + d);
             const double eps = box_muller(rng_word(RK[r], base + 1), rng_word(RK[r], base + 2));
-            const float z = MU[r * 16 + d] + __expf(LS[d]) * (float)eps;
-            ZS[r * 16 + d] = z;
+            const float sig = __expf(LS[d]);
+            const float mu = MU[r * 16 + d];
+            const float z = mu + sig * (float)eps;
             a.act_pre[((long)(i0 + r) * a.T + t) * ad + d] = z;
+            // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
+            // squashed action tanh(z) for the env step: both per (env, dim) item here
+            // rather than in the one-thread-per-env loops
+            const float zn = (z - mu) / sig;
+            MU[r * 16 + d] = (-0.5f * zn * zn - LS[d] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
+            ZS[r * 16 + d] = tanhf(z);
         }
         __syncthreads();
-        for (int r = tid; r < nr; r += RNT) {  // action_logprob (nn.cpp:204-219)
+        for (int r = tid; r < nr; r += RNT) {  // action_logprob: the dims' terms in order
             float lp = 0.f;
-            for (int d = 0; d < ad; ++d) {
-                const float sig = __expf(LS[d]);
-                const float z = ZS[r * 16 + d];
-                const float zn = (z - MU[r * 16 + d]) / sig;
-                lp += -0.5f * zn * zn - LS[d] - 0.9189385332046727f;
-                lp -= __logf(sech2(z) + 1e-6f);
-            }
+            for (int d = 0; d < ad; ++d) lp += MU[r * 16 + d];
             a.logprob[(long)(i0 + r) * a.T + t] = lp;
         }
+        RPROF(3);
         // ---- critic at the current obs, only if some instance reset (or t = 0)
         if (VF[t & 1]) {
             run_net(a, x, is, VF, c, 1, ph);
@@ -289,6 +313,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             umma::fence_before_sync();
         }
         __syncthreads();
+        RPROF(4);
         // ---- value, env step (env.cpp:60-92), tracker (rollout.cpp:143-148)
         int any_reset = 0;
         for (int r = tid; r < nr; r += RNT) {
@@ -300,7 +325,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             for (int d = 0; d < 16; ++d) {
                 act[d] = 0.f;
                 if (d < ad) {
-                    const float xx = tanhf(ZS[r * 16 + d]);
+                    const float xx = ZS[r * 16 + d];  // tanh(z), from the sampling pass
                     if (!isfinite(xx)) atomicExch(a.err, 3);
                     act[d] = fminf(fmaxf(xx, -1.f), 1.f);
                     anyc |= act[d] != xx;
@@ -347,8 +372,10 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         if (tid == 0) VF[(t + 1) & 1] = any_reset;
         umma::fence_proxy_async();
         __syncthreads();
+        RPROF(5);
         // ---- critic at the pre-reset final obs -> next_value
         run_net(a, x, is, VF, c, 1, ph);
+        RPROF(6);
         if (warp < 4) {
             float v[16];
             umma::tmem_ld16(x.tbase + ((uint32_t)(warp * 32) << 16) + OUT_COL, v);
@@ -363,6 +390,14 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         umma::fence_before_sync();
         __syncthreads();
     }
+#ifdef MB_ROLL_PROF
+    if (blockIdx.x == 0 && tid == 0)
+        printf("rollout CTA0 us (thread 0's clock): obs %.1f policy %.1f pol_out %.1f sample+logprob(own rows) %.1f "
+               "critic_cur(+wait) %.1f env %.1f "
+               "critic_final %.1f tail %.1f\n",
+               prof_[0] * 1e-3, prof_[1] * 1e-3, prof_[2] * 1e-3, prof_[3] * 1e-3, prof_[4] * 1e-3, prof_[5] * 1e-3,
+               prof_[6] * 1e-3, prof_[7] * 1e-3);
+#endif
     for (int e = tid; e < sd * nr; e += RNT) {
         const int k = e / nr, r = e % nr;
         a.state[(long)k * a.N + i0 + r] = S[k * RE + r];
