@@ -254,13 +254,13 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
 #endif
     for (int t = 0; t < a.T; ++t) {
         // ---- observation -> layer-0 operand (bf16, MN-major) + batch.obs
-        for (int e = tid; e < nr * od; e += RNT) {
-            const int r = e / od, k = e % od;
-            const float v = S[k * RE + r];
-            a.obs[((long)(i0 + r) * a.T + t) * od + k] = v;
-            *reinterpret_cast<__nv_bfloat16*>(x.xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2) =
-                __float2bfloat16_rn(v);
-        }
+        for (int q = tid; q < nr * 4; q += RNT)  // 4 threads per instance (no div / mod)
+            for (int r = q >> 2, k = q & 3; k < od; k += 4) {
+                const float v = S[k * RE + r];
+                a.obs[((long)(i0 + r) * a.T + t) * od + k] = v;
+                *reinterpret_cast<__nv_bfloat16*>(x.xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 +
+                                                  (r & 7) * 2) = __float2bfloat16_rn(v);
+            }
         umma::fence_proxy_async();
         __syncthreads();
         RPROF(0);
@@ -346,9 +346,6 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                     a.reward[row * m + k] = rw[k];
                     TRK[r * 8 + k] += rw[k];
                 }
-            for (int k = 0; k < od; ++k)  // pre-reset final obs -> critic operand
-                *reinterpret_cast<__nv_bfloat16*>(x.xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 +
-                                                  (r & 7) * 2) = __float2bfloat16_rn(s[k * RE]);
             if (tm || tr) {
                 double ret = 0.0;
                 for (int k = 0; k < m; ++k) {
@@ -357,10 +354,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 }
                 a.ret_sum[i0 + r] += ret;
                 a.ret_cnt[i0 + r] += 1;
-                uint64_t cc = EC[r];
-                env_do_reset(a.kind, s, RE, EK[r], &cc);
-                EC[r] = cc;
-                STP[r] = 0;
+                STP[r] = 0;  // (the reset itself after the final-obs operand pass below)
                 NEED[r] = 1;
                 any_reset = 1;
             } else {
@@ -370,6 +364,20 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         }
         any_reset = __syncthreads_or(any_reset);
         if (tid == 0) VF[(t + 1) & 1] = any_reset;
+        // pre-reset final obs -> critic operand, 4 threads per instance
+        for (int r = tid >> 2; r < nr; r += RNT / 4)
+            for (int k = tid & 3; k < od; k += 4)
+                *reinterpret_cast<__nv_bfloat16*>(x.xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 +
+                                                  (r & 7) * 2) = __float2bfloat16_rn(S[k * RE + r]);
+        if (any_reset) {  // auto-reset from the instance's persistent stream (env.cpp:84-92)
+            __syncthreads();
+            for (int r = tid; r < nr; r += RNT)
+                if (NEED[r]) {
+                    uint64_t cc = EC[r];
+                    env_do_reset(a.kind, S + r, RE, EK[r], &cc);
+                    EC[r] = cc;
+                }
+        }
         umma::fence_proxy_async();
         __syncthreads();
         RPROF(5);
