@@ -138,7 +138,7 @@ def reference_sample(base, cores):
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     base = dict(BASE[args.config])
     base["N"] *= world
     base["K"] *= world
@@ -259,6 +259,18 @@ def leg_c4(mb):
 
 
 # ---------------------------------------------------------------- GPU arm
+def self_launch(args):
+    """--gpus N without a launcher: re-exec this script as N ranks under
+    torch.distributed.run on this node (one process per GPU, NCCL)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -272,6 +284,11 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}: "
+                         "launch one rank per GPU (torchrun --nproc-per-node N) or let bench.py self-launch")
 
     import torch
     import torch.distributed as dist

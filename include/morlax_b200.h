@@ -155,6 +155,19 @@ int morlax_nccl_unique_id(void* out128);
 int morlax_trainer_create(const morlax_train_config* cfg, int world, int rank, const void* nccl_id,
                           morlax_trainer** out);
 void morlax_trainer_destroy(morlax_trainer* t);
+/* In-process loopback group: `world` ranks as host threads of ONE process
+ * on ONE device (comm.h). Each rank's trainer runs the sharded multi-GPU
+ * data plane (all-to-all of the per-cluster gradient shards, sharded dM +
+ * Adam, all-gathers of the M image / b / feature gradients) with
+ * device-to-device copies in place of NCCL; every rank must drive its
+ * trainer from its own thread (the collectives meet at host barriers).
+ * Results equal the single-rank trainer's bit for bit (tests only: it
+ * measures nothing about NVLink). */
+typedef struct morlax_loopback morlax_loopback;
+int morlax_loopback_create(int world, morlax_loopback** out);
+void morlax_loopback_destroy(morlax_loopback* g); /* after every trainer of the group */
+int morlax_trainer_create_loopback(const morlax_train_config* cfg, morlax_loopback* group, int rank,
+                                   morlax_trainer** out);
 /* one full training iteration `it` (host-facing: H2D of sampled
  * preferences and minibatch indices, D2H of the stats, inside the call) */
 int morlax_trainer_iteration(morlax_trainer* t, int it, morlax_iter_stats* stats);
@@ -251,6 +264,12 @@ int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, cons
                      float* C, int use_tc);
 
 /* microbenchmark hook for the tcgen05 GEMM (tools/gemm_bench.py): ms per launch */
+/* test hook: fused hypernet M-block gradient + Adam (dm_adam.cu) on host
+ * arrays: dM = gtheta^T f (bf16 operands, fp32 accumulation; G groups in
+ * 128-group K chunks) and Adam on p / m1 / m2 [P][F] (hypernet.cpp:92-122 dM,
+ * adam.cpp:8-26); also returns the bf16 bits of the refreshed M image rows */
+int morlax_dm_adam_test(int G, int P, int F, const float* gtheta, const float* f, float* p, float* m1, float* m2,
+                        float lr, float ibc1, float ibc2, uint16_t* mimg_rows);
 int morlax_gemm_bench(int M, int N, int K, int a_view, int b_view, int act, int iters, double* ms);
 
 /* ---- Pareto (replaces nondominated_filter / hypervolume_mc /

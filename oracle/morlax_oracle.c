@@ -614,6 +614,24 @@ void mo_env_get_streams(const mo_env* e, uint64_t* keys, uint64_t* ctrs, int32_t
     }
 }
 
+/* Test hook (teacher forcing; not a reference entry point): overwrite every
+ * instance's state, step counter and stream position, so a parity test can
+ * restart the oracle from the device's recorded observation each step
+ * (obs == state for every env, write_obs above). Streams keep their keys
+ * unless keys is non-NULL. */
+void mo_env_set_instances(mo_env* e, const double* state, const int32_t* steps, const uint64_t* keys,
+                          const uint64_t* ctrs) {
+    for (int i = 0; i < e->n; ++i) {
+        if (state) {
+            memcpy(e->state + (size_t)i * e->sdim, state + (size_t)i * e->sdim, sizeof(double) * e->sdim);
+            write_obs(e, i, e->cur_obs + (size_t)i * e->spec.obs_dim);
+        }
+        if (steps) e->steps[i] = steps[i];
+        if (keys) e->streams[i].key = keys[i];
+        if (ctrs) e->streams[i].ctr = ctrs[i];
+    }
+}
+
 /* ========================================================================= */
 /* Rollout: src/rollout.cpp:37-161                                            */
 /* ========================================================================= */

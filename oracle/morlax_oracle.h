@@ -99,6 +99,9 @@ void mo_env_current_obs(const mo_env* e, double* out);
 uint64_t mo_env_clamp_count(const mo_env* e);
 /* streams (key, ctr) and step counters per instance */
 void mo_env_get_streams(const mo_env* e, uint64_t* keys, uint64_t* ctrs, int32_t* steps);
+/* test hook: restart instances from given states / counters (teacher forcing) */
+void mo_env_set_instances(mo_env* e, const double* state, const int32_t* steps, const uint64_t* keys,
+                          const uint64_t* ctrs);
 
 /* ---- Rollout (rollout.cpp:37-161) ---------------------------------------- */
 typedef struct {

@@ -218,6 +218,7 @@ class Oracle:
             L.mo_trainer_iteration.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
             L.mo_trainer_destroy.argtypes = [C.c_void_p]
             L.mo_env_get_streams.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.mo_env_set_instances.argtypes = [C.c_void_p] * 5
             L.mo_hypervolume_wfg.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         else:
             L.mref_trainer_create.restype = C.c_void_p
@@ -507,6 +508,15 @@ class OracleEnv:
         steps = np.zeros(self.n, np.int32)
         self.o.lib.mo_env_get_streams(self.h, keys.ctypes.data, ctrs.ctypes.data, steps.ctypes.data)
         return keys, ctrs, steps
+
+    def set_instances(self, state=None, steps=None, keys=None, ctrs=None):
+        """Teacher-forcing test hook: restart every instance from the given
+        state (obs == state) / step counter / stream position."""
+        assert self.o.kind == "oracle"
+        arrs = []
+        for v, dt in ((state, np.float64), (steps, np.int32), (keys, np.uint64), (ctrs, np.uint64)):
+            arrs.append(None if v is None else np.ascontiguousarray(v, dt))
+        self.o.lib.mo_env_set_instances(self.h, *[None if a is None else a.ctypes.data for a in arrs])
 
 
 class OracleTrainer:

@@ -404,6 +404,24 @@ class _CkExtraC(C.Structure):
                 ("pareto_reference", C.POINTER(C.c_double))]
 
 
+class LoopbackGroup:
+    """W ranks of the sharded data plane as host threads on ONE device
+    (morlax_loopback_create): each rank's Trainer(cfg, W, r, loopback=group)
+    must be driven from its own thread; results equal the single-rank
+    trainer's bit for bit. For tests of the multi-GPU code path."""
+
+    def __init__(self, world: int):
+        self.world = world
+        h = C.c_void_p()
+        _check(LIB.morlax_loopback_create(world, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.morlax_loopback_destroy(self._h)
+            self._h = None
+
+
 class Trainer:
     """The reference train() loop body on the GPU (train.cpp:118-184).
     world > 1: one Trainer per GPU/rank (environments and preference clusters
@@ -413,12 +431,17 @@ class Trainer:
             "value_targets", "scalar_advantage", "env_state", "tracker", "clusters"}
 
     def __init__(self, cfg: TrainConfig, world: int = 1, rank: int = 0, nccl_id: bytes = None,
-                 _handle=None):
+                 _handle=None, loopback: "LoopbackGroup" = None):
         self.cfg = cfg
         self._c = cfg.c()
         h = C.c_void_p()
+        self._group = loopback  # keeps the group alive while this rank exists
         if _handle is not None:  # adopt a trainer made by morlax_train
             h = _handle
+        elif loopback is not None:
+            if world != loopback.world:
+                raise ConfigError("world must equal the loopback group's size")
+            _check(LIB.morlax_trainer_create_loopback(C.byref(self._c), loopback._h, rank, C.byref(h)))
         else:
             idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
             _check(LIB.morlax_trainer_create(C.byref(self._c), world, rank, idb, C.byref(h)))
@@ -458,6 +481,14 @@ class Trainer:
         _check(LIB.morlax_trainer_set_params(self._h, 0 if which == "actor" else 1,
                                              _ptr(_f64(flat))))
 
+    def theta(self, which: str = "actor") -> np.ndarray:
+        """Generated target-net weights of the local clusters (last hypernet
+        forward), fp32 [local K][P] in the reference flat layout."""
+        P = self.cfg.specs()[0 if which == "actor" else 1].target_param_count
+        out = np.zeros((self.local_clusters, P), np.float32)
+        _check(LIB.morlax_trainer_get_theta(self._h, 0 if which == "actor" else 1, _ptr(out)))
+        return out
+
     def grad(self, which: str = "actor") -> np.ndarray:
         n = self.n_actor if which == "actor" else self.n_critic
         out = np.zeros(n)
@@ -471,21 +502,26 @@ class Trainer:
                 "advantages": (R, es.m), "value_targets": (R, es.m), "scalar_advantage": (R,),
                 "terminated": (R,), "truncated": (R,), "clusters": (self.cfg.K, es.m),
                 "perm": (self.cfg.N * self.cfg.T,), "env_ctr": (N,), "env_steps": (N,),
-                "tracker": (N, es.m)}[name]
+                "env_key": (N,), "ret_sum": (N,), "ret_cnt": (N,), "tracker": (N, es.m),
+                "env_state": (es.obs_dim, N)}[name]  # obs == state for every env
+
+    def _dtype(self, name):
+        if name in self._F32:
+            return np.float32
+        if name in ("terminated", "truncated"):
+            return np.uint8
+        if name in ("env_ctr", "env_key"):
+            return np.uint64
+        return np.float64 if name == "ret_sum" else np.int32
 
     def get(self, name: str) -> np.ndarray:
-        if name == "env_state":
-            raise ShapeError("use env_state()")
-        dt = (np.float32 if name in self._F32 else np.uint8 if name in ("terminated", "truncated")
-              else np.uint64 if name == "env_ctr" else np.int32)
-        out = np.zeros(self._shape(name), dt)
+        """Device field -> host copy. env_state is the SoA [state_dim][N] layout."""
+        out = np.zeros(self._shape(name), self._dtype(name))
         _check(LIB.morlax_trainer_get(self._h, name.encode(), _ptr(out)))
         return out
 
     def set(self, name: str, value):
-        dt = (np.float32 if name in self._F32 else np.uint8 if name in ("terminated", "truncated")
-              else np.uint64 if name == "env_ctr" else np.int32)
-        v = np.ascontiguousarray(value, dt).reshape(self._shape(name))
+        v = np.ascontiguousarray(value, self._dtype(name)).reshape(self._shape(name))
         _check(LIB.morlax_trainer_set(self._h, name.encode(), _ptr(v)))
 
     def save_checkpoint(self, path: str, iteration: int, iterations: int = 300, grid_resolution: int = 10,

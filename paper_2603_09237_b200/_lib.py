@@ -40,6 +40,8 @@ def _load():
     lib.morlax_env_clamp_count.argtypes = [C.c_void_p]
     lib.morlax_env_destroy.argtypes = [C.c_void_p]
     lib.morlax_trainer_destroy.argtypes = [C.c_void_p]
+    lib.morlax_loopback_destroy.argtypes = [C.c_void_p]
+    lib.morlax_trainer_create_loopback.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.morlax_hypernet_param_count.restype = C.c_int64
     lib.morlax_hypernet_target_count.restype = C.c_int64
     lib.morlax_trainer_kernel_launches.restype = C.c_int64
@@ -53,6 +55,7 @@ def _load():
     lib.morlax_policy_flops.restype = C.c_double
     lib.morlax_policy_flops.argtypes = [C.c_void_p]
     lib.morlax_simplex_grid_size.restype = C.c_int64
+    lib.morlax_dm_adam_test.argtypes = [C.c_int] * 3 + [C.c_void_p] * 5 + [C.c_float] * 3 + [C.c_void_p]
     for name in ("morlax_env_reset", "morlax_env_step", "morlax_env_current_obs",
                  "morlax_env_step_device", "morlax_trainer_iteration", "morlax_trainer_phase",
                  "morlax_trainer_sizes", "morlax_trainer_get_params", "morlax_trainer_set_params",

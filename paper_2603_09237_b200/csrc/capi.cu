@@ -512,10 +512,12 @@ int morlax_normalize_scalarize(int N, int T, int m, const float* adv, const doub
         DBuf<float> a(adv, R * m), o(R);
         std::vector<float> twf(tw, tw + (size_t)N * m);
         DBuf<float> w(twf.data(), twf.size());
-        DBuf<double> st(32), scratch(148 * 2 * 8);
-        channel_sums(a.p, R, m, nullptr, st.p, scratch.p, 0);
+        DBuf<double> st(32), part((size_t)N * 8);  // partials per instance (T rows each)
+        channel_partials(a.p, N, T, m, nullptr, part.p, 0);
+        channel_total(part.p, N, m, st.p, 0);
         stats_finalize(st.p, (double)R, m, st.p + 8, 0, 0);
-        channel_sums(a.p, R, m, st.p + 8, st.p + 16, scratch.p, 0);
+        channel_partials(a.p, N, T, m, st.p + 8, part.p, 0);
+        channel_total(part.p, N, m, st.p + 16, 0);
         stats_finalize(st.p + 16, (double)R, m, st.p + 24, 1, 0);
         scalarize(N, T, m, a.p, w.p, 1, st.p + 8, st.p + 24, o.p, 0);  // reps = 1: per-instance weights
         MB_CUDA(cudaDeviceSynchronize());
@@ -547,7 +549,32 @@ int morlax_adam(int64_t n, double* p, const double* g, double* m1, double* m2, i
 int morlax_nccl_unique_id(void* out) {
     return guarded([&] { comm_unique_id(out); });
 }
+struct morlax_loopback {
+    LoopGroup* g = nullptr;
+};
+int morlax_loopback_create(int world, morlax_loopback** out) {
+    return guarded([&] {
+        auto* h = new morlax_loopback;
+        h->g = loop_group_create(world);
+        *out = h;
+    });
+}
+void morlax_loopback_destroy(morlax_loopback* g) {
+    if (!g) return;
+    loop_group_destroy(g->g);
+    delete g;
+}
+static int trainer_create(const morlax_train_config* c, int world, int rank, const void* id, LoopGroup* loop,
+                          morlax_trainer** out);
 int morlax_trainer_create(const morlax_train_config* c, int world, int rank, const void* id, morlax_trainer** out) {
+    return trainer_create(c, world, rank, id, nullptr, out);
+}
+int morlax_trainer_create_loopback(const morlax_train_config* c, morlax_loopback* g, int rank, morlax_trainer** out) {
+    if (!g) return guarded([] { throw ConfigError("loopback group is null"); });
+    return trainer_create(c, comm_world_of(g->g), rank, nullptr, g->g, out);
+}
+static int trainer_create(const morlax_train_config* c, int world, int rank, const void* id, LoopGroup* loop,
+                          morlax_trainer** out) {
     return guarded([&] {
         TrainConfig tc;
         tc.env_kind = env_kind_of(c->env_name ? c->env_name : "");
@@ -561,7 +588,7 @@ int morlax_trainer_create(const morlax_train_config* c, int world, int rank, con
         tc.critic_hidden = vec(c->n_critic_hidden, c->critic_hidden);
         auto* h = new morlax_trainer;
         try {
-            h->t = new Trainer(tc, world, rank, id);
+            h->t = new Trainer(tc, world, rank, id, loop);
         } catch (...) {
             delete h;
             throw;
@@ -618,6 +645,9 @@ int morlax_trainer_save_checkpoint(morlax_trainer* t, const char* path, int64_t 
                                    const morlax_checkpoint_extra* x) {
     return guarded([&] {
         Trainer& tr = *t->t;
+        MB_CUDA(cudaStreamSynchronize(tr.stream()));
+        tr.actor().gather_params(tr.stream());  // sharded optimizer: every rank's M rows (collective)
+        tr.critic().gather_params(tr.stream());
         write_checkpoint(tr, path, iteration, x, tr.actor().p, tr.critic().p);
     });
 }
@@ -819,6 +849,7 @@ int morlax_trainer_get_params(morlax_trainer* t, int which, double* out) {
         HyperNet& h = which ? t->t->critic() : t->t->actor();
         std::vector<float> f(h.n);
         MB_CUDA(cudaStreamSynchronize(t->t->stream()));
+        h.gather_params(t->t->stream());  // sharded optimizer: every rank's M rows (collective)
         MB_CUDA(cudaMemcpy(f.data(), h.p, sizeof(float) * h.n, cudaMemcpyDeviceToHost));
         for (long i = 0; i < h.n; ++i) out[i] = f[i];
     });
@@ -838,6 +869,7 @@ int morlax_trainer_get_grad(morlax_trainer* t, int which, double* out) {
         HyperNet& h = which ? t->t->critic() : t->t->actor();
         std::vector<float> f(h.n);
         MB_CUDA(cudaStreamSynchronize(t->t->stream()));
+        h.gather_params(t->t->stream());  // sharded optimizer: every rank's M rows (collective)
         MB_CUDA(cudaMemcpy(f.data(), h.g, sizeof(float) * h.n, cudaMemcpyDeviceToHost));
         for (long i = 0; i < h.n; ++i) out[i] = f[i];
     });
@@ -872,6 +904,9 @@ static void field_info(Trainer& tr, const std::string& f, void** dev, size_t* by
     else if (f == "tracker") { *dev = tr.d_tracker; *bytes = sizeof(float) * es.m * tr.local_envs(); }
     else if (f == "env_ctr") { *dev = tr.d_ectr; *bytes = sizeof(uint64_t) * tr.local_envs(); }
     else if (f == "env_steps") { *dev = tr.d_steps; *bytes = sizeof(int) * tr.local_envs(); }
+    else if (f == "env_key") { *dev = tr.d_ekey; *bytes = sizeof(uint64_t) * tr.local_envs(); }
+    else if (f == "ret_sum") { *dev = tr.d_retsum; *bytes = sizeof(double) * tr.local_envs(); }
+    else if (f == "ret_cnt") { *dev = tr.d_retcnt; *bytes = sizeof(int) * tr.local_envs(); }
     else if (f != "clusters" && f != "perm") throw ConfigError("unknown field: " + f);
 }
 int morlax_trainer_get(morlax_trainer* t, const char* field, void* out) {
@@ -991,6 +1026,46 @@ int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, cons
         }
         MB_CUDA(cudaDeviceSynchronize());
         dc.get(C);
+    });
+}
+
+// test hook: the fused hypernet M-block gradient + Adam (dm_adam.cu) on host
+// arrays at any (G, P, F): dM = gtheta^T f over the bf16 images of gtheta
+// [G][P] and f [G][F], Adam on p / m1 / m2 [P][F]; returns the updated
+// fp32 state and the bf16 bits of the refreshed M image as rows [P][F]
+int morlax_dm_adam_test(int G, int P, int F, const float* gtheta, const float* f, float* p, float* m1, float* m2,
+                        float lr, float ibc1, float ibc2, uint16_t* mimg_rows) {
+    return guarded([&] {
+        DBuf<float> dg(gtheta, (size_t)G * P), dfv(f, (size_t)G * F), dp(p, (size_t)P * F), da(m1, (size_t)P * F),
+            db(m2, (size_t)P * F);
+        DBuf<uint8_t> gi(img_bytes(G, P)), fi(img_bytes(G, F)), mi(img_bytes(P, F));
+        DBuf<int> err(1);
+        MB_CUDA(cudaMemset(gi.p, 0, img_bytes(G, P)));
+        MB_CUDA(cudaMemset(fi.p, 0, img_bytes(G, F)));
+        MB_CUDA(cudaMemset(mi.p, 0, img_bytes(P, F)));
+        MB_CUDA(cudaMemset(err.p, 0, sizeof(int)));
+        DmAdam a;
+        a.gimg = Img{gi.p, G, P, 0};
+        a.fimg = Img{fi.p, G, F, 0};
+        a.mimg = Img{mi.p, P, F, 0};
+        to_img(dg.p, P, 0, G, P, a.gimg, 1, 0);
+        to_img(dfv.p, F, 0, G, F, a.fimg, 1, 0);
+        a.G = G; a.P = P; a.F = F;
+        a.p = dp.p; a.m1 = da.p; a.m2 = db.p;
+        a.lr = lr; a.ibc1 = ibc1; a.ibc2 = ibc2; a.err = err.p;
+        dm_adam(a, 0);
+        MB_CUDA(cudaDeviceSynchronize());
+        dp.get(p);
+        da.get(m1);
+        db.get(m2);
+        if (mimg_rows) {
+            std::vector<uint8_t> im(img_bytes(P, F));
+            MB_CUDA(cudaMemcpy(im.data(), mi.p, im.size(), cudaMemcpyDeviceToHost));
+            const int CT = img_ct(F);
+            for (long r = 0; r < P; ++r)
+                for (int c = 0; c < F; ++c)
+                    std::memcpy(mimg_rows + r * F + c, im.data() + img_off(r, c, CT), 2);
+        }
     });
 }
 

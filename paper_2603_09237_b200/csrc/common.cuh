@@ -38,6 +38,14 @@ extern std::atomic<long> g_kernel_launches;
         MB_CUDA(cudaGetLastError());                                       \
     } while (0)
 
+// ---- per-device launch facts ---------------------------------------------------
+// The SM count and the one-time cudaFuncSetAttribute(MaxDynamicSharedMemory)
+// of the >48 KB kernels are cached per CUDA device (keyed by cudaGetDevice, a
+// mutex around the cache): one process may drive several GPUs from several
+// host threads (kernels.cu).
+int device_sms();
+void ensure_smem(const void* func, size_t bytes);
+
 // ---- programmatic dependent launch ------------------------------------------
 // The update chain's kernels are launched with programmatic stream
 // serialization (launch_pdl): a kernel's launch is processed while its

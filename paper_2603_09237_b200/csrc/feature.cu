@@ -211,16 +211,18 @@ void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, 
     feature_forward_multi(&j, 1, s);
 }
 
-void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s) {
+void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s, int stage) {
     const int L = jobs[0].fd->L;
     for (int k = 0; k < nj; ++k) {
         const FeatJob& j = jobs[k];
         if (j.fd->L != L) throw ShapeError("feature_backward_multi: the feature maps must have equal depth");
+        if (stage == 2) continue;
         const long n = (long)j.G * j.fd->sz[L];
         launch_pdl(k_split_dtanh, dim3((unsigned)((n + 63) / 64)), dim3(256), 0, s, j.parts, j.splits, n,
                    (const float*)j.fd->act[L], j.fd->gz[L - 1]);
         MB_LAUNCH();
     }
+    if (stage == 1) return;
     for (int l = L - 1; l >= 0; --l) {
         Dense16 ds[4];
         int nd = 0;
@@ -253,7 +255,7 @@ void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s) {
 void feature_backward(const FeatDims& fd, const float* p, const float* w, const float* parts, int splits, int G,
                       float* gout, cudaStream_t s) {
     FeatJob j{&fd, p, w, G, Img{}, 0, 0, parts, splits, gout};
-    feature_backward_multi(&j, 1, s);
+    feature_backward_multi(&j, 1, s, 0);
 }
 
 }  // namespace mb200

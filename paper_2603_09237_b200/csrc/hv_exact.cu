@@ -29,6 +29,8 @@
 // Every sum is in a fixed order, so the value is deterministic. A warp
 // arena overflow (adversarial fronts whose limit sets do not shrink) sets a
 // flag and the host re-runs step 3 with the worst-case arena.
+#include <map>
+#include <mutex>
 #include <algorithm>
 
 #include "common.cuh"
@@ -372,11 +374,18 @@ struct ScratchPool {
         return p[slot];
     }
 };
-ScratchPool g_pool;
+// one pool per device; hv_exact holds the pool's mutex for the whole call
+// (it is synchronous), so concurrent host threads never share scratch
+struct DevicePools {
+    std::mutex mu;
+    std::map<int, ScratchPool> pools;
+};
+DevicePools g_pools;
+thread_local ScratchPool* t_pool = nullptr;
 template <typename T>
 struct DevScratch {
     T* p = nullptr;
-    DevScratch(int slot, size_t n) { p = static_cast<T*>(g_pool.get(slot, sizeof(T) * (n ? n : 1))); }
+    DevScratch(int slot, size_t n) { p = static_cast<T*>(t_pool->get(slot, sizeof(T) * (n ? n : 1))); }
 };
 }  // namespace
 
@@ -384,6 +393,10 @@ void hv_exact(int n, int m, const double* d_pts, const double* d_ref, double* va
               cudaStream_t s) {
     if (m < 1 || m > kHvMaxM) throw ShapeError("hypervolume: objective count must be in [1, 8]");
     if (n > kHvMaxN) throw ShapeError("exact hypervolume: at most 4096 points");
+    int cur_dev = 0;
+    MB_CUDA(cudaGetDevice(&cur_dev));
+    std::lock_guard<std::mutex> lk(g_pools.mu);
+    t_pool = &g_pools.pools[cur_dev];
     const long nn = n > 0 ? n : 1;
     DevScratch<double> raw(0, nn * m), top(1, nn * m), out(2, 1);
     DevScratch<int> ints(3, 8), flag(4, nn);

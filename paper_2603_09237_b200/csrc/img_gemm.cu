@@ -477,11 +477,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
 template <int BN, int EPI>
 void launch(const IGemm* ds, int n, cudaStream_t s) {
     using C = Cfg<BN, EPI>;
-    static bool configured = false;
-    if (!configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_img_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        configured = true;
-    }
+    ensure_smem((const void*)k_img_gemm<BN, EPI>, C::SMEM);
     GemmBatch bt;
     bt.n = n;
     for (int k = 0; k < n; ++k) {
@@ -495,7 +491,8 @@ void launch(const IGemm* ds, int n, cudaStream_t s) {
     }
     const int ntiles = bt.base[n];
     if (ntiles == 0) return;
-    const int grid = ntiles < 148 ? ntiles : 148;
+    const int sms = device_sms();
+    const int grid = ntiles < sms ? ntiles : sms;
     launch_pdl(k_img_gemm<BN, EPI>, dim3(grid), dim3(C::NT), C::SMEM, s, bt);
     MB_LAUNCH();
 }
@@ -613,20 +610,26 @@ void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst
     MB_LAUNCH();
 }
 
-// bf16 rows [R][ld] (ld % 8 == 0) -> image: one 16 B unit per thread
-__global__ void k_rows_to_img(const uint16_t* __restrict__ rows, long ld, int R, int C, Img dst) {
-    const int CT = img_ct(C), cpr = (C + 7) / 8;
-    const long units = (long)R * cpr;
+// local clusters' gtheta rows [Kl][ld] -> send[W][Kl][S]: destination
+// rank d gets columns [d S, d S + S) of every local row (the all-to-all
+// payload of the sharded optimizer); one float4 per thread
+__global__ void k_pack_shards(const float* __restrict__ gt, long ld, int Kl, long S, int W, float* __restrict__ send) {
+    pdl_enter();
+    const long s4 = S / 4, units = (long)W * Kl * s4;
     for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < units; u += (long)gridDim.x * blockDim.x) {
-        const int r = (int)(u / cpr), c = (int)(u - (long)r * cpr) * 8;
-        *reinterpret_cast<uint4*>(dst.p + img_off(r, c, CT)) = *reinterpret_cast<const uint4*>(rows + (long)r * ld + c);
+        const long d = u / ((long)Kl * s4), rem = u - d * Kl * s4;
+        const long k = rem / s4, c = d * S + (rem - k * s4) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < ld) v = *reinterpret_cast<const float4*>(gt + k * ld + c);
+        reinterpret_cast<float4*>(send)[u] = v;
     }
 }
-void rows_to_img(const uint16_t* rows, long ld, int R, int C, const Img& dst, cudaStream_t s) {
-    if (ld % 8) throw ShapeError("rows_to_img: row stride must be a multiple of 8");
-    const long units = (long)R * ((C + 7) / 8);
+void pack_shards(const float* gt, long ld, int Kl, long S, int W, float* send, cudaStream_t s) {
+    if (ld % 8 || S % 128) throw ShapeError("pack_shards: row stride % 8 and shard width % 128 required");
+    const long units = (long)W * Kl * (S / 4);
     if (units == 0) return;
-    k_rows_to_img<<<(unsigned)std::min<long>((units + 255) / 256, 148 * 16), 256, 0, s>>>(rows, ld, R, C, dst);
+    launch_pdl(k_pack_shards, dim3((unsigned)std::min<long>((units + 255) / 256, 148L * 8)), dim3(256), 0, s, gt, ld,
+               Kl, S, W, send);
     MB_LAUNCH();
 }
 
@@ -683,7 +686,7 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
 // a fixed order.
 constexpr int kGtSlices = 32, kGtUnits = 32;
 __global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const float* __restrict__ gt, long ld, int G,
-                                                                         int P, Img gimg, float* db, uint16_t* rows) {
+                                                                         int P, Img gimg, float* db) {
     pdl_enter();
     __shared__ float part[kGtSlices][kGtUnits][9];
     const int ul = threadIdx.x % kGtUnits, sl = threadIdx.x / kGtUnits;
@@ -715,13 +718,12 @@ __global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const f
                 w.z = umma::pack_bf16(v[4], v[5]);
                 w.w = umma::pack_bf16(v[6], v[7]);
                 *reinterpret_cast<uint4*>(gimg.p + img_off(g, p0, CT)) = w;
-                if (rows) *reinterpret_cast<uint4*>(rows + (long)g * ld + p0) = w;
             }
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) part[sl][ul][e] = acc[e];
         __syncthreads();
-        if (sl == 0 && p0 < P)
+        if (db && sl == 0 && p0 < P)
             for (int e = 0; e < 8 && p0 + e < P; ++e) {
                 float t = 0.f;
                 for (int q = 0; q < kGtSlices; ++q) t += part[q][ul][e];
@@ -730,13 +732,12 @@ __global__ void __launch_bounds__(kGtUnits * kGtSlices, 2) k_gtheta_prep(const f
         __syncthreads();
     }
 }
-void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s, uint16_t* rows) {
+void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s) {
     if (ld % 8) throw ShapeError("gtheta_prep: row stride must be a multiple of 8");
     const long ngroups = ((P + 7) / 8 + kGtUnits - 1) / kGtUnits;
-    static int sms = 0;
-    if (!sms) MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int sms = device_sms();
     launch_pdl(k_gtheta_prep, dim3((unsigned)std::min<long>(ngroups, 2L * sms)), dim3(kGtUnits * kGtSlices), 0, s, gt,
-               ld, G, P, gimg, db, rows);
+               ld, G, P, gimg, db);
     MB_LAUNCH();
 }
 

@@ -2,6 +2,8 @@
 // GEMMs and Pareto): K1 env step, K3 fused rollout, K4 GAE scan +
 // normalise/scalarise, K5 per-row PPO losses, K7 Adam, reductions.
 // Reference semantics are cited per kernel (paths under /root/reference/proj).
+#include <map>
+#include <mutex>
 #include <cfloat>
 
 #include "common.cuh"
@@ -11,6 +13,30 @@
 namespace mb200 {
 
 std::atomic<long> g_kernel_launches{0};
+int device_sms() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 0;
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev] = sms;
+    return sms;
+}
+void ensure_smem(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> cache;
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = cache[{dev, func}];
+    if (bytes <= have) return;
+    MB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+}
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("MORLAX_PDL");
@@ -249,43 +275,61 @@ void gae_scan(int N, int T, int m, const float* reward, const float* value, cons
     MB_LAUNCH();
 }
 
-// Normalisation statistics (gae.cpp:79-96): deterministic two-level fp64
-// reductions. pass 1 (mean == nullptr): sum x; pass 2: sum (x - mean)^2.
-constexpr int kRedBlocks = 148 * 2;
-__global__ void k_chan_partial(const float* x, long rows, int m, const double* mean, double* part) {
-    extern __shared__ double red[];  // [blockDim][m]
+// Normalisation statistics (gae.cpp:79-96): deterministic fp64 reductions in
+// a fixed two-level order that does not depend on how the rows are spread
+// over GPUs: one partial per group of consecutive rows (a preference
+// cluster's reps * T rows in the trainer: whole clusters live on one rank),
+// then the group partials summed in group order. pass 1 (mean == nullptr):
+// sum x; pass 2: sum (x - mean)^2.
+__global__ void __launch_bounds__(256) k_chan_part(const float* __restrict__ x, long rows_per_group, int m,
+                                                   const double* mean, double* part) {
+    __shared__ double red[256 * 8];
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (long r = blockIdx.x * (long)blockDim.x + threadIdx.x; r < rows; r += (long)gridDim.x * blockDim.x)
-        for (int k = 0; k < m; ++k) {
-            double v = x[r * m + k];
-            if (mean) {
-                v -= mean[k];
-                v *= v;
+    const float* xg = x + (long)blockIdx.x * rows_per_group * m;
+    double mu[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mu[k] = (mean && k < m) ? mean[k] : 0.0;
+    for (long r = threadIdx.x; r < rows_per_group; r += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < m) {
+                double v = xg[r * m + k];
+                if (mean) {
+                    v -= mu[k];
+                    v *= v;
+                }
+                acc[k] += v;
             }
-            acc[k] += v;
-        }
-    for (int k = 0; k < m; ++k) red[threadIdx.x * m + k] = acc[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red[k * 256 + threadIdx.x] = acc[k];
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    for (int s = 128; s > 0; s >>= 1) {
         if (threadIdx.x < s)
-            for (int k = 0; k < m; ++k) red[threadIdx.x * m + k] += red[(threadIdx.x + s) * m + k];
+            for (int k = 0; k < m; ++k) red[k * 256 + threadIdx.x] += red[k * 256 + threadIdx.x + s];
         __syncthreads();
     }
-    if (threadIdx.x == 0)
-        for (int k = 0; k < m; ++k) part[blockIdx.x * m + k] = red[k];
+    if (threadIdx.x < 8) part[blockIdx.x * 8 + threadIdx.x] = threadIdx.x < m ? red[threadIdx.x * 256] : 0.0;
 }
-__global__ void k_chan_final(const double* part, int nb, int m, double* out) {
-    const int k = threadIdx.x;
+// out[k] = sum_g part[g][k]: warp k, lane-strided partial sums in g order,
+// then a fixed butterfly (the same order for any group count split)
+__global__ void k_chan_total(const double* __restrict__ part, int groups, int m, double* out) {
+    const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (k >= m) return;
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part[b * m + k];
-    out[k] = s;
+    for (int g = lane; g < groups; g += 32) s += part[g * 8 + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[k] = s;
 }
-void channel_sums(const float* x, long rows, int m, const double* mean, double* out, double* scratch,
-                  cudaStream_t s) {
-    k_chan_partial<<<kRedBlocks, 256, 256 * m * sizeof(double), s>>>(x, rows, m, mean, scratch);
+void channel_partials(const float* x, int groups, long rows_per_group, int m, const double* mean, double* part,
+                      cudaStream_t s) {
+    if (m > 8) throw ShapeError("normalize: at most 8 objectives on the device");
+    if (groups <= 0) return;
+    k_chan_part<<<groups, 256, 0, s>>>(x, rows_per_group, m, mean, part);
     MB_LAUNCH();
-    k_chan_final<<<1, 32, 0, s>>>(scratch, kRedBlocks, m, out);
+}
+void channel_total(const double* part, int groups, int m, double* out, cudaStream_t s) {
+    k_chan_total<<<1, 256, 0, s>>>(part, groups, m, out);
     MB_LAUNCH();
 }
 
@@ -1043,10 +1087,12 @@ void adam_img(long n, float* p, const float* g, float* m1, float* m2, float lr, 
     if (m_lo % 4 || F % 8) throw ShapeError("adam_img: M block must be 4-aligned with F % 8 == 0");
     if (hole_lo % 4 || hole_len % 4 || hole_len < 0 || (hole_len && mimg.R))
         throw ShapeError("adam_img: the skipped range must be 4-aligned (and excludes the image)");
-    n -= hole_len;  // elements updated
+    const long n_all = n;  // the tail's bound is in unshifted element indices
+    n -= hole_len;         // elements updated
+    if (n <= 0) return;
     const long n4 = n / 4, threads = n4 + (n - 4 * n4);
     launch_pdl(k_adam_img, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, n4, (float4*)p,
-               (const float4*)g, (float4*)m1, (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi, F, mimg, n,
+               (const float4*)g, (float4*)m1, (float4*)m2, lr, 1.f / bc1, 1.f / bc2, err, m_lo, m_hi, F, mimg, n_all,
                hole_lo, hole_len);
     MB_LAUNCH();
 }

@@ -93,12 +93,11 @@ void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s);
 void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
 void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
                   cudaStream_t s);
-// gtheta [G][ld] -> bf16 image + column sums db[P] (one pass); optionally
-// also the bf16 rows row-major [G][ld] (the multi-GPU all-gather payload)
-void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s,
-                 uint16_t* rows_out = nullptr);
-// bf16 rows [R][ld] -> image (row r, col c), c < C
-void rows_to_img(const uint16_t* rows, long ld, int R, int C, const Img& dst, cudaStream_t s);
+// gtheta [G][ld] -> bf16 image + column sums db[P] in one pass (db may be null)
+void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s);
+// sharded optimizer: the local clusters' gtheta rows [Kl][ld] split by
+// column shard into send[W][Kl][S] (columns past ld zero-filled)
+void pack_shards(const float* gt, long ld, int Kl, long S, int W, float* send, cudaStream_t s);
 struct MbGather {
     int Bp = 0, G = 0, od = 0, ad = 0, m = 0;
     const int *rows = nullptr, *goff = nullptr;
@@ -228,9 +227,12 @@ void rollout_tc(RolloutTcArgs a, cudaStream_t s);
 void gae_scan(int N, int T, int m, const float* reward, const float* value, const float* next_value,
               const uint8_t* term, const uint8_t* trunc, float gamma, float lambda, float* adv,
               float* targets, cudaStream_t s);
-// partial sums: out[m] (fp64) of x[r*m+k] (pass 1) or (x - mean)^2 (pass 2)
-void channel_sums(const float* x, long rows, int m, const double* mean, double* out,
-                  double* scratch, cudaStream_t s);
+// per-group partial sums part[g][8] (fp64) of x[r*m+k] (pass 1) or
+// (x - mean)^2 (pass 2) over the group's consecutive rows; channel_total sums
+// the partials in group order (rank-count invariant: gae.cpp:79-96)
+void channel_partials(const float* x, int groups, long rows_per_group, int m, const double* mean, double* part,
+                      cudaStream_t s);
+void channel_total(const double* part, int groups, int m, double* out, cudaStream_t s);
 // mean[k] = sums[k] / rows (mode 0); inv[k] = 1/(sqrt(sums[k]/rows) + 1e-8) (mode 1)
 void stats_finalize(const double* sums, double rows, int m, double* out, int mode, cudaStream_t s);
 void scalarize(int N, int T, int m, const float* adv, const float* cluster_w, int reps,
@@ -282,7 +284,9 @@ struct FeatJob {
     float* gout;
 };
 void feature_forward_multi(const FeatJob* jobs, int nj, cudaStream_t s);
-void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s);
+// stage 0: df split-K sum * tanh' (gz of the last layer) and the dense
+// backward; 1: the first part only; 2: the dense backward only
+void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s, int stage = 0);
 void mul_dtanh(float* g, const float* a, long n, cudaStream_t s);
 
 // ---------------------------------------------------------------- Adam (K7)

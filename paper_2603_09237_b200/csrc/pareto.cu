@@ -171,11 +171,7 @@ void linear_dominance(int nn, int m, const double* nd, uint8_t* keep, int* scrat
     MB_CUDA(cudaMemsetAsync(keep, 0, nn, s));
     const size_t smem = sizeof(double) * (size_t)nn * m + nn;
     if (smem > 200 * 1024) throw ShapeError("linear_dominance_filter: too many nondominated points for the device sweep");
-    static size_t configured = 0;
-    if (smem > configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_ldf_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
+    ensure_smem((const void*)k_ldf_sweep, smem);
     const unsigned long long blocks = std::min<unsigned long long>((nw + kLdfThreads - 1) / kLdfThreads, 148ull * 8);
     k_ldf_sweep<<<(unsigned)blocks, kLdfThreads, smem, s>>>(nn, m, nd, d_binom, nw, keep);
     MB_LAUNCH();

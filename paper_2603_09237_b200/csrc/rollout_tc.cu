@@ -507,11 +507,7 @@ void rollout_tc(RolloutTcArgs a, cudaStream_t s) {
     a.nepad = pad16(ne);
     const size_t bytes = rollout_tc_smem(a);
     if (bytes > 227 * 1024) throw ShapeError("tensor-core rollout: shared-memory plan exceeds 227 KB");
-    static size_t configured = 0;
-    if (bytes > configured) {
-        MB_CUDA(cudaFuncSetAttribute(k_rollout_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        configured = bytes;
-    }
+    ensure_smem((const void*)k_rollout_tc, bytes);
     const int cpg = (a.reps + RE - 1) / RE;
     k_rollout_tc<<<a.K * cpg, RNT, bytes, s>>>(a);
     MB_LAUNCH();

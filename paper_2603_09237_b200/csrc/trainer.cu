@@ -183,10 +183,14 @@ static void gemm(const char* cls, const GemmDesc& d, cudaStream_t s) {  // tiny 
 
 // ------------------------------------------------------------------ HyperNet
 void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vector<int>& ts, bool out_tanh,
-                    bool has_log_std, int G_) {
+                    bool has_log_std, int G_, Comm* comm_, int Kl_) {
     m = m_;
     F = F_;
     G = G_;
+    comm = comm_;
+    world = comm ? comm_world(comm) : 1;
+    rank = comm ? comm_rank(comm) : 0;
+    Kl = comm ? Kl_ : G_;
     fsz.clear();
     fsz.push_back(m);
     for (int h : fh) fsz.push_back(h);
@@ -203,10 +207,18 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     P = tgt.P;
     ld = (P + 7) / 8 * 8;
     n = nf + P * F + P;
-    p = dalloc<float>(n);
-    g = dalloc<float>(n);
-    m1 = dalloc<float>(n);
-    m2 = dalloc<float>(n);
+    // optimizer shards: whole 128-row chunks of the M image per rank
+    const long rt = (P + 127) / 128;
+    S = ((rt + world - 1) / world) * 128;
+    row_lo = std::min<long>(P, (long)rank * S);
+    row_hi = std::min<long>(P, row_lo + S);
+    if (comm && (nf % 4 || (P * F) % 4))
+        throw ShapeError("sharded optimizer: feature-map and M block sizes must be multiples of 4");
+    const long pad = comm ? (long)world * S - P : 0;  // b is all-gathered in place (rank r at b + r S)
+    p = dalloc<float>(n + pad);
+    g = dalloc<float>(n + pad);
+    m1 = dalloc<float>(n + pad);
+    m2 = dalloc<float>(n + pad);
     fact.assign(fsz.size(), nullptr);
     int maxw = 0;
     for (size_t l = 0; l < fsz.size(); ++l) {
@@ -246,8 +258,15 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
         im.p = dalloc<uint8_t>((size_t)(groups > 1 ? gs * groups : img_bytes(R, C)));
         return im;
     };
-    mimg = mk((int)P, F, 0, 1);
+    mimg = mk((int)(comm ? world * S : P), F, 0, 1);  // rows [r S, r S + S): rank r's all-gather block
+    mimg.R = (int)P;
     fimg = mk(G, F, 0, 1);
+    if (comm) {
+        gsend = dalloc<float>((size_t)world * Kl * S);
+        grecv = dalloc<float>((size_t)world * Kl * S);
+        gshard = mk(G, (int)S, 0, 1);
+        fall = mk(G, F, 0, 1);
+    }
     gimg = mk(G, (int)P, 0, 1);
     wimg_off.clear();
     long ws = 0;
@@ -275,22 +294,8 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     parts = dalloc<float>((size_t)splits * G * F);
 }
 
-void HyperNet::enable_exchange(Comm* c) {
-    comm = c;
-    auto mk = [](int R, int C) {
-        Img im;
-        im.R = R;
-        im.C = C;
-        im.p = dalloc<uint8_t>((size_t)img_bytes(R, C));
-        return im;
-    };
-    gall = mk(G, (int)P);
-    fall = mk(G, F);
-    grows = dalloc<uint16_t>((size_t)G * ld);
-}
-
 void HyperNet::free_all() {
-    dfree(gall.p); dfree(fall.p); dfree(grows);
+    dfree(gshard.p); dfree(fall.p); dfree(gsend); dfree(grecv);
     dfree(p); dfree(g); dfree(m1); dfree(m2);
     for (auto& a : fact) dfree(a);
     for (auto& a : fgz) dfree(a);
@@ -381,35 +386,35 @@ void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0
 
 void HyperNet::refresh_images(cudaStream_t s) { to_img(p + nf, F, 0, (int)P, F, mimg, 1, s); }
 
-// hypernet_backward (hypernet.cpp:92-122) summed over the clusters of the
-// last forward ([fg0, fg0 + fng), this rank's): db = sum_g gtheta_g,
-// dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then the feature-map
-// backward. Writes (not accumulates) the flat grad g. With several ranks
-// (comm set) the result is the global gradient on every rank: the local
-// clusters' gtheta rows are all-gathered as bf16 (the dM GEMM's operand
-// precision) so dM runs over all clusters on every rank -- 2 B per cluster
-// row entry on the wire instead of an all-reduce of the 4 B x P x F dM --
-// while db and the feature-map gradient (small) are all-reduced.
+// hypernet_backward (hypernet.cpp:92-122) summed over the clusters:
+// db = sum_g gtheta_g, dM = sum_g gtheta_g f_g^T, df_g = M^T gtheta_g, then
+// the feature-map backward. Writes (not accumulates) the flat grad g. This
+// rank's clusters are [fg0, fg0 + fng) (all of them without a communicator).
+// Sharded (comm set): the local gtheta rows are exchanged all-to-all by
+// column shard, so db and dM of this rank's M rows [row_lo, row_hi) sum over
+// every cluster in the single-rank order; each cluster's df-derived feature
+// gradient (gz) is all-gathered and the feature-map backward runs over all
+// clusters on every rank. No collective sums floating-point partials, so the
+// result is the single-rank one bit for bit.
 void HyperNet::backward(cudaStream_t s) {
     HyperNet* self = this;
     backward_multi(&self, 1, s);
 }
 
+static Img img_rows(const Img& im, long r0, int R) {  // rows [r0, r0 + R) of an image (r0 % 128 == 0)
+    Img v = im;
+    v.p = im.p + (r0 / 128) * (long)img_ct(im.C) * 32768;
+    v.R = R;
+    return v;
+}
+
 void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int part) {
     if (part != 2) {  // the gradient passes (no parameter is written)
-        for (int k = 0; k < nh; ++k) {  // gimg + db in one pass
+        for (int k = 0; k < nh; ++k) {  // local gimg (df operand) + db (single rank) in one pass
             HyperNet& h = *hs[k];
-            gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg, h.g + h.nf + h.P * h.F, s,
-                        h.comm ? h.grows + (long)h.fg0 * h.ld : nullptr);
-        }
-        for (int k = 0; k < nh; ++k) {  // multi-GPU: every rank gets every cluster's theta gradient (bf16
-            HyperNet& h = *hs[k];        // rows, in place) and f(w), so dM needs no all-reduce
-            if (!h.comm) continue;
-            ProfScope ps("exchange", 0, 2.0 * h.G * h.ld, s);
-            comm_allreduce_f32(h.comm, h.g + h.nf + h.P * h.F, (size_t)h.P, s);  // db: the local sums
-            comm_allgather_bytes(h.comm, h.grows, sizeof(uint16_t) * (size_t)h.fng * h.ld, s);
-            rows_to_img(h.grows, h.ld, h.G, (int)h.P, h.gall, s);
-            to_img(h.fact.back(), h.F, 0, h.G, h.F, h.fall, 1, s);  // f(w) of all G clusters (every rank has it)
+            gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg,
+                        h.comm ? nullptr : h.g + h.nf + h.P * h.F, s);
+            if (h.comm) pack_shards(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, h.S, h.world, h.gsend, s);
         }
         {
             IGemm ds[2];
@@ -427,36 +432,60 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
             ProfScope ps("hyper_df", fl, 0, s);
             img_gemm_batch(ds, nh, s);
         }
-        {  // df reduction + feature-map backward (all layers' dW, db) over the local rows
+        FeatDims loc[2], all[2];
+        FeatJob jl[2], ja[2];
+        bool any_comm = false;
+        for (int k = 0; k < nh; ++k) {
+            HyperNet& h = *hs[k];
+            any_comm |= h.comm != nullptr;
+            loc[k] = h.fd;  // this rank's clusters: df split-K sum * tanh' -> gz rows [fg0, fg0 + fng)
+            for (int l = 0; l <= h.fd.L; ++l) loc[k].act[l] = h.fd.act[l] + (long)h.fg0 * h.fd.sz[l];
+            for (int l = 0; l < h.fd.L; ++l) loc[k].gz[l] = h.fd.gz[l] + (long)h.fg0 * h.fd.sz[l + 1];
+            jl[k] = FeatJob{&loc[k], h.p, h.w_last + (long)h.fg0 * h.m, h.fng, Img{}, 0, 0, h.parts, h.splits, h.g};
+            all[k] = h.fd;  // all clusters: the feature map's weight gradients
+            ja[k] = FeatJob{&all[k], h.p, h.w_last, h.G, Img{}, 0, 0, h.parts, h.splits, h.g};
+        }
+        if (!any_comm) {
             double fl = 0;
-            FeatDims fl_d[2];
-            FeatJob jobs[2];
+            for (int k = 0; k < nh; ++k)
+                for (size_t l = 0; l + 1 < hs[k]->fsz.size(); ++l) fl += 4.0 * hs[k]->G * hs[k]->fsz[l] * hs[k]->fsz[l + 1];
+            ProfScope ps("feature_bwd", fl, 0, s);
+            feature_backward_multi(jl, nh, s, 0);
+        } else {
+            feature_backward_multi(jl, nh, s, 1);
             for (int k = 0; k < nh; ++k) {
                 HyperNet& h = *hs[k];
-                for (size_t l = 0; l + 1 < h.fsz.size(); ++l) fl += 4.0 * h.fng * h.fsz[l] * h.fsz[l + 1];
-                fl_d[k] = h.fd;
-                for (int l = 0; l <= h.fd.L; ++l) fl_d[k].act[l] = h.fd.act[l] + (long)h.fg0 * h.fd.sz[l];
-                jobs[k] = FeatJob{&fl_d[k], h.p, h.w_last + (long)h.fg0 * h.m, h.fng, Img{}, 0, 0, h.parts, h.splits, h.g};
+                ProfScope ps("exchange", 0, 4.0 * h.world * h.Kl * h.S + 4.0 * h.G * h.F, s);
+                // every cluster's gtheta on this rank's shard, then its image and db (all clusters, in order)
+                comm_alltoall_bytes(h.comm, h.gsend, h.grecv, sizeof(float) * (size_t)h.Kl * h.S, s);
+                if (h.row_hi > h.row_lo)
+                    gtheta_prep(h.grecv, h.S, h.G, (int)(h.row_hi - h.row_lo), h.gshard, h.g + h.nf + h.P * h.F + h.row_lo, s);
+                comm_allgather_bytes(h.comm, h.fd.gz[h.fd.L - 1], sizeof(float) * (size_t)h.Kl * h.F, s);
             }
+            double fl = 0;
+            for (int k = 0; k < nh; ++k)
+                for (size_t l = 0; l + 1 < hs[k]->fsz.size(); ++l) fl += 4.0 * hs[k]->G * hs[k]->fsz[l] * hs[k]->fsz[l + 1];
             ProfScope ps("feature_bwd", fl, 0, s);
-            feature_backward_multi(jobs, nh, s);
+            feature_backward_multi(ja, nh, s, 2);
         }
-        for (int k = 0; k < nh; ++k)  // the feature-map gradient: each rank's partial over its clusters
-            if (hs[k]->comm) comm_allreduce_f32(hs[k]->comm, hs[k]->g, (size_t)hs[k]->nf, s);
     }
     if (part != 1) {  // dM and, fused, the M-block Adam (after the losses' finiteness check)
+        for (int k = 0; k < nh; ++k) {
+            HyperNet& h = *hs[k];
+            if (h.comm) to_img(h.fact.back(), h.F, 0, h.G, h.F, h.fall, 1, s);  // f(w) of every cluster
+        }
         {
             IGemm ds[2];
             double fl = 0;
             int nd = 0;
             for (int k = 0; k < nh; ++k) {
                 HyperNet& h = *hs[k];
-                if (h.adam_fused) continue;
-                IGemm& d = ds[nd++];  // dM[p][k] = sum_g gtheta[g][p] f[g][k] (all G clusters with an exchange)
-                d.A = h.comm ? h.gall : h.gimg; d.a_view = 1;  // (m = p, k = g)
-                d.B = h.comm ? h.fall : h.fimg; d.b_view = 1;  // (n = f, k = g)
-                d.M = (int)h.P; d.N = h.F; d.K = h.comm ? h.G : h.fng;
-                d.C = h.g + h.nf; d.cm = h.F; d.cn = 1;
+                if (h.adam_fused || h.row_hi <= h.row_lo) continue;
+                IGemm& d = ds[nd++];  // dM[p][k] = sum_g gtheta[g][p] f[g][k] over this rank's rows
+                d.A = h.comm ? h.gshard : h.gimg; d.a_view = 1;  // (m = p, k = g)
+                d.B = h.comm ? h.fall : h.fimg; d.b_view = 1;    // (n = f, k = g)
+                d.M = (int)(h.row_hi - h.row_lo); d.N = h.F; d.K = h.comm ? h.G : h.fng;
+                d.C = h.g + h.nf + h.row_lo * h.F; d.cm = h.F; d.cn = 1;
                 fl += 2.0 * d.M * d.N * d.K;
             }
             if (nd) {
@@ -464,16 +493,18 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
                 img_gemm_batch(ds, nd, s);
             }
         }
-        for (int k = 0; k < nh; ++k) {  // single rank: dM consumed by Adam in registers (dm_adam.cu)
+        for (int k = 0; k < nh; ++k) {  // dM consumed by Adam in registers (dm_adam.cu)
             HyperNet& h = *hs[k];
-            if (!h.adam_fused) continue;
+            if (!h.adam_fused || h.row_hi <= h.row_lo) continue;
             DmAdam a;
-            a.gimg = h.comm ? h.gall : h.gimg; a.fimg = h.comm ? h.fall : h.fimg;
-            a.G = h.comm ? h.G : h.fng; a.P = (int)h.P; a.F = h.F;
-            a.p = h.p + h.nf; a.m1 = h.m1 + h.nf; a.m2 = h.m2 + h.nf; a.mimg = h.mimg;
+            a.gimg = h.comm ? h.gshard : h.gimg; a.fimg = h.comm ? h.fall : h.fimg;
+            a.G = h.comm ? h.G : h.fng; a.P = (int)(h.row_hi - h.row_lo); a.F = h.F;
+            const long off = h.nf + h.row_lo * h.F;
+            a.p = h.p + off; a.m1 = h.m1 + off; a.m2 = h.m2 + off;
+            a.mimg = img_rows(h.mimg, h.row_lo, a.P);
             a.lr = h.ad_lr; a.ibc1 = h.ad_ibc1; a.ibc2 = h.ad_ibc2; a.err = h.ad_err;
             // HBM-bound: p, m1, m2 in + out (fp32), M image out (bf16), gtheta image in
-            ProfScope ps("dm_adam", 0, 26.0 * h.P * h.F + 2.0 * h.P * h.fng, s);
+            ProfScope ps("dm_adam", 0, 26.0 * a.P * h.F + 2.0 * a.P * a.G, s);
             dm_adam(a, s);
         }
     }
@@ -493,21 +524,55 @@ void HyperNet::adam_begin(double lr, const int* err) {
 void HyperNet::adam_step(double lr, const int* err, cudaStream_t s) {
     // three blocks (feature, M, b) with their own step counters (train.cpp:28-39);
     // they always advance together, so one launch covers the flat vector.
-    if (adam_fused) {  // M was updated in the dM epilogue: the feature and b blocks remain
-        adam_fused = false;
-        const double bc1 = 1.0 - std::pow(0.9, (double)steps[0]);
-        const double bc2 = 1.0 - std::pow(0.999, (double)steps[0]);
-        const long b0 = nf + P * F;
-        ProfScope ps("adam", 0, 28.0 * (nf + P), s);
-        Img none;
-        adam_img(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, 0, F, none, s, nf, b0 - nf);
-        return;
-    }
-    for (long& st : steps) ++st;
+    if (!adam_fused)
+        for (long& st : steps) ++st;
     const double bc1 = 1.0 - std::pow(0.9, (double)steps[0]);
     const double bc2 = 1.0 - std::pow(0.999, (double)steps[0]);
-    ProfScope ps("adam", 0, 28.0 * n + 2.0 * P * F, s);  // p,g,m1,m2 in; p,m1,m2 out (fp32); M image (bf16)
-    adam_img(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, nf, F, mimg, s);
+    const long b0 = nf + P * F;
+    Img none;
+    if (!comm) {
+        if (adam_fused) {  // M was updated inside the dM kernel: the feature and b blocks remain
+            ProfScope ps("adam", 0, 28.0 * (nf + P), s);
+            adam_img(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, 0, F, none, s, nf, b0 - nf);
+        } else {
+            ProfScope ps("adam", 0, 28.0 * n + 2.0 * P * F, s);  // p,g,m1,m2 in; p,m1,m2 out; M image (bf16)
+            adam_img(n, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, nf, F, mimg, s);
+        }
+        adam_fused = false;
+        return;
+    }
+    // sharded: the replicated feature block and this rank's M rows / b entries
+    {
+        ProfScope ps("adam", 0, 28.0 * (nf + (row_hi - row_lo) * (adam_fused ? 1 : F + 1)), s);
+        if (adam_fused) {  // feature block + b shard (M shard done in dm_adam)
+            adam_img(b0 + row_hi, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, 0, F, none, s, nf,
+                     b0 + row_lo - nf);
+        } else {
+            adam_img(nf + row_hi * F, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, 0, F, none, s, nf,
+                     row_lo * F);  // feature block + M shard
+            if (row_hi > row_lo)
+                to_img(p + nf + row_lo * F, F, 0, (int)(row_hi - row_lo), F, img_rows(mimg, row_lo, (int)(row_hi - row_lo)),
+                       1, s);
+            adam_img(b0 + row_hi, p, g, m1, m2, (float)lr, (float)bc1, (float)bc2, err, 0, F, none, s, 0,
+                     b0 + row_lo);  // b shard
+        }
+    }
+    adam_fused = false;
+    ProfScope ps("exchange", 0, 2.0 * world * S * F + 4.0 * world * S, s);
+    // every rank's refreshed M image rows and b entries (rank r's block at row / entry r S)
+    comm_allgather_bytes(comm, mimg.p, (size_t)(S / 128) * img_ct(F) * 32768, s);
+    comm_allgather_bytes(comm, p + b0, sizeof(float) * (size_t)S, s);
+}
+
+void HyperNet::gather_params(cudaStream_t s) {
+    if (!comm) return;
+    float* tmp = dalloc<float>((size_t)world * S * F);
+    MB_CUDA(cudaMemcpyAsync(tmp + (size_t)rank * S * F, p + nf + row_lo * F, sizeof(float) * (row_hi - row_lo) * F,
+                            cudaMemcpyDeviceToDevice, s));
+    comm_allgather_bytes(comm, tmp, sizeof(float) * (size_t)S * F, s);
+    MB_CUDA(cudaMemcpyAsync(p + nf, tmp, sizeof(float) * P * F, cudaMemcpyDeviceToDevice, s));
+    MB_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
 }
 
 // ------------------------------------------------------------------ sharding
@@ -557,7 +622,7 @@ int pad_groups(const int* rows, int* goff, int G, int* rows_out, int* n_out) {
 }
 
 // ------------------------------------------------------------------ Trainer
-Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_id)
+Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_id, LoopGroup* loop)
     : cfg_(cfg), world_(world), rank_(rank) {
     es_ = env_spec_of(cfg.env_kind);
     cfg_.validate(es_.m);
@@ -579,28 +644,31 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     MB_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
     MB_CUDA(cudaStreamCreateWithFlags(&s3_, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_cd_[0], &ev_cd_[1], &ev_ad_[0], &ev_ad_[1],
-                           &ev_cfin_, &ev_cb_, &ev_cr_})
+                           &ev_cfin_})
         MB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (cudaEvent_t e : {ev_cd_[0], ev_cd_[1], ev_cfin_}) MB_CUDA(cudaEventRecord(e, s2_));
     for (cudaEvent_t e : {ev_ad_[0], ev_ad_[1]}) MB_CUDA(cudaEventRecord(e, s_));
-    // a communicator whenever an NCCL id is given (world == 1 included: the
-    // single-rank collectives exercise the multi-GPU code path on one GPU)
-    if (world > 1 || nccl_id) comm_ = comm_create(world, rank, nccl_id);
+    // a communicator whenever an NCCL id or a loopback group is given (world
+    // == 1 included: the single-rank collectives run the sharded code path
+    // on one GPU); one per update chain so the two chains' exchanges overlap
+    if (loop) {
+        comm_ = comm_create_loopback(loop, rank);
+        if (comm_world(comm_) != world) throw ConfigError("loopback group size != world");
+    } else if (world > 1 || nccl_id) {
+        comm_ = comm_create(world, rank, nccl_id);
+    }
+    if (comm_) comm2_ = comm_split(comm_);
     root_ = HostRng::seeded(cfg.seed);
     std::vector<int> as{es_.obs_dim}, cs{es_.obs_dim};
     for (int h : cfg.actor_hidden) as.push_back(h);
     as.push_back(es_.act_dim);
     for (int h : cfg.critic_hidden) cs.push_back(h);
     cs.push_back(es_.m);
-    actor_.init(es_.m, cfg.F, cfg.feat_hidden, as, true, true, cfg.K);    // config.cpp:59-70
-    critic_.init(es_.m, cfg.F, cfg.feat_hidden, cs, false, false, cfg.K); // config.cpp:72-83
+    actor_.init(es_.m, cfg.F, cfg.feat_hidden, as, true, true, cfg.K, comm_, Kl_);     // config.cpp:59-70
+    critic_.init(es_.m, cfg.F, cfg.feat_hidden, cs, false, false, cfg.K, comm2_, Kl_); // config.cpp:72-83
     actor_.init_params(root_.split(0xA1).key, s_);                        // train.cpp:67-70
     critic_.init_params(root_.split(0xA2).key, s_);
     alloc();
-    if (comm_) {  // per-minibatch exchange buffers (backward_multi)
-        actor_.enable_exchange(comm_);
-        critic_.enable_exchange(comm_);
-    }
     env_reset(es_.kind, Nl_, d_state, d_ekey, d_ectr, d_steps, root_.split(0xE0).key, inst_lo_, s_);
     perm_.resize((size_t)cfg.N * cfg.T);
     std::iota(perm_.begin(), perm_.end(), 0);  // train.cpp:112-114
@@ -628,20 +696,20 @@ Trainer::~Trainer() {
         cudaFree(u.psls);
         cudaFree(u.lossrows);
     }
-    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_cd_[0], ev_cd_[1], ev_ad_[0], ev_ad_[1], ev_cfin_, ev_cb_,
-                   ev_cr_})
+    for (auto e : {ev_gather_, ev_c_net_, ev_chk_, ev_cd_[0], ev_cd_[1], ev_ad_[0], ev_ad_[1], ev_cfin_})
         if (e) cudaEventDestroy(e);
     if (s2_) cudaStreamDestroy(s2_);
     if (s3_) cudaStreamDestroy(s3_);
     for (auto& u : ub_) cudaFree(u.Zf);
     for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
                     (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_lossrows,
-                    (void*)d_mbloss, (void*)d_stats, (void*)d_scratch, (void*)d_retsum, (void*)d_retcnt,
+                    (void*)d_mbloss, (void*)d_stats, (void*)d_scratch, (void*)d_part, (void*)d_retsum, (void*)d_retcnt,
                     (void*)d_pol_blob, (void*)d_cri_blob})
         if (p) cudaFree(p);
     if (h_cw_pinned) cudaFreeHost(h_cw_pinned);
     if (h_rows_pinned) cudaFreeHost(h_rows_pinned);
     if (h_goff_pinned) cudaFreeHost(h_goff_pinned);
+    if (comm2_) comm_destroy(comm2_);
     if (comm_) comm_destroy(comm_);
     if (s_) cudaStreamDestroy(s_);
 }
@@ -731,6 +799,7 @@ void Trainer::alloc() {
     }
     d_mbloss = dalloc<double>((size_t)slots * 2 + 2);
     d_stats = dalloc<double>(4 * 8);
+    d_part = dalloc<double>((size_t)cfg_.K * 8);
     d_scratch = dalloc<double>(148 * 2 * 8);
     d_retsum = dalloc<double>(Nl_);
     pol_plan_ = make_plan(actor_.tgt);
@@ -914,17 +983,21 @@ void Trainer::phase_advantages() {
         gae_scan(Nl_, cfg_.T, m, d_rew, d_val, d_nval, d_term, d_trunc, (float)cfg_.gamma, (float)cfg_.lambda,
                  d_adv, d_tgt, s_);
     }
-    // global per-channel statistics (gae.cpp:79-96): sums all-reduced across ranks
+    // global per-channel statistics (gae.cpp:79-96): one partial per cluster
+    // (whole clusters live on one rank), all-gathered, summed in cluster order
     const double rows = (double)cfg_.N * cfg_.T;
     double* sum1 = d_stats;
     double* mean = d_stats + 8;
     double* sum2 = d_stats + 16;
     double* inv = d_stats + 24;
-    channel_sums(d_adv, Rl_, m, nullptr, sum1, d_scratch, s_);
-    if (comm_) comm_allreduce_f64(comm_, sum1, m, s_);
+    const long rpg = (long)reps_ * cfg_.T;
+    channel_partials(d_adv, Kl_, rpg, m, nullptr, d_part + (size_t)g_lo_ * 8, s_);
+    if (comm_) comm_allgather_bytes(comm_, d_part, sizeof(double) * 8 * Kl_, s_);
+    channel_total(d_part, cfg_.K, m, sum1, s_);
     stats_finalize(sum1, rows, m, mean, 0, s_);
-    channel_sums(d_adv, Rl_, m, mean, sum2, d_scratch, s_);
-    if (comm_) comm_allreduce_f64(comm_, sum2, m, s_);
+    channel_partials(d_adv, Kl_, rpg, m, mean, d_part + (size_t)g_lo_ * 8, s_);
+    if (comm_) comm_allgather_bytes(comm_, d_part, sizeof(double) * 8 * Kl_, s_);
+    channel_total(d_part, cfg_.K, m, sum2, s_);
     stats_finalize(sum2, rows, m, inv, 1, s_);
     scalarize(Nl_, cfg_.T, m, d_adv, d_cw + (size_t)g_lo_ * m, reps_, mean, inv, d_sadv, s_);
 }
@@ -1120,8 +1193,8 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     cudaStream_t sc = two ? s2_ : s_;
     const char* fe = std::getenv("MORLAX_FUSED_ADAM");  // "0": the unfused dM GEMM + Adam (A/B, tests)
     const bool fuse_env = !(fe && fe[0] == '0');
-    // dm_adam's tile shape and K (all clusters: with an exchange dM sums every rank's rows)
-    const bool fuse = fuse_env && actor_.F % 64 == 0 && critic_.F % 64 == 0 && cfg_.K <= 128;
+    // dm_adam's tile width (K: any cluster count, in 128-cluster chunks)
+    const bool fuse = fuse_env && actor_.F % 64 == 0 && critic_.F % 64 == 0;
     if (fuse) {  // host-side Adam step counters / bias corrections for the fused M-block update
         actor_.adam_begin(cfg_.actor_lr, d_err);
         critic_.adam_begin(cfg_.critic_lr, d_err);
@@ -1164,31 +1237,22 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     net_step(&both[1], &roles[1], 1, Bp, inv_B, maxg, rows, goff, slot, sc);
     MB_CUDA(cudaEventRecord(ev_c_net_, sc));
     MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], sc));
-    // the gradient passes of the backward write no parameter: each chain runs
-    // them before the finiteness join (with an exchange they hold NCCL calls:
-    // below, on s_)
-    if (!comm_) HyperNet::backward_multi(&both[1], 1, sc, 1);
+    // the gradient passes of the backward write no parameter (with a
+    // communicator they hold the chain's exchange collectives): each chain
+    // runs them before the finiteness join
+    HyperNet::backward_multi(&both[1], 1, sc, 1);
     actor_.forward(d_cw, g_lo_, Kl_, s_);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_gather_, 0));
     net_step(&both[0], &roles[0], 1, Bp, inv_B, maxg, rows, goff, slot, s_);
     MB_CUDA(cudaEventRecord(ev_ad_[mb_par_], s_));
-    if (!comm_) HyperNet::backward_multi(&both[0], 1, s_, 1);
+    HyperNet::backward_multi(&both[0], 1, s_, 1);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_c_net_, 0));
     if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 2, s_);
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
     MB_CUDA(cudaEventRecord(ev_chk_, s_));
     MB_CUDA(cudaStreamWaitEvent(sc, ev_chk_, 0));
-    if (comm_) {  // the backward passes hold the exchange collectives: every NCCL call on s_ (one
-        // stream per communicator, device order = host order), both nets batched
-        HyperNet::backward_multi(both, 2, s_);
-        critic_.adam_step(cfg_.critic_lr, d_err, s_);
-        MB_CUDA(cudaEventRecord(ev_cfin_, s_));
-        actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
-        MB_CUDA(cudaStreamWaitEvent(sc, ev_cfin_, 0));  // the critic's next forward reads its new params
-        return;
-    }
     HyperNet::backward_multi(&both[1], 1, sc, 2);
-    critic_.adam_step(cfg_.critic_lr, d_err, sc);
+    critic_.adam_step(cfg_.critic_lr, d_err, sc);  // (+ the critic chain's all-gathers on comm2_)
     MB_CUDA(cudaEventRecord(ev_cfin_, sc));
     HyperNet::backward_multi(&both[0], 1, s_, 2);
     actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180

@@ -17,7 +17,8 @@
 
 namespace mb200 {
 
-struct Comm;  // NCCL communicator (nccl.cu), null when world == 1
+struct Comm;       // communicator of one rank (comm.cu), null when single-GPU without one
+struct LoopGroup;  // in-process loopback group (comm.cu)
 
 // Per-kernel-class device timing with CUDA events on the launching stream,
 // plus the algorithmic FLOPs / bytes of every launch (for the roofline).
@@ -79,34 +80,45 @@ struct HyperNet {
     std::vector<long> wimg_off;
     void refresh_images(cudaStream_t s);                 // p (M block) -> mimg after external loads
 
+    // world > 1 (or a single-rank communicator): the optimizer is sharded --
+    // this rank owns M rows and b entries [row_lo, row_hi)
     void init(int m_, int F_, const std::vector<int>& fh, const std::vector<int>& target_sizes,
-              bool out_tanh, bool has_log_std, int G_);
+              bool out_tanh, bool has_log_std, int G_, Comm* comm_ = nullptr, int Kl_ = 0);
     void free_all();
     void init_params(uint64_t key, cudaStream_t s);  // init_hypernet (hypernet.cpp:124-145)
-    // f, theta for groups [g0, g0+ng) of the G cluster weights w[G][m]
+    // f (all G clusters), theta for groups [g0, g0+ng) of the G cluster weights w[G][m]
     void forward(const float* w, int g0, int ng, cudaStream_t s);
     // the same for nh (1 or 2) hypernetworks in lockstep, one launch per stage
     static void forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s);
-    // part 0: all; 1: the gradient passes (gtheta image, exchange, df,
-    // feature map); 2: dM (+ the fused M-block Adam), after part 1
+    // part 0: all; 1: the gradient passes (gtheta image, shard exchange, df,
+    // feature map: no parameter is written); 2: dM (+ the fused M-block Adam)
     static void backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int part = 0);
     // grads from gtheta [G][P] (all groups) -> g
     void backward(cudaStream_t s);
     void adam_step(double lr, const int* err, cudaStream_t s);
-    // fused update (single rank, no gradient exchange): called before
-    // backward, which then applies Adam to the M block inside the dM GEMM
-    // epilogue (dM is never stored); adam_step finishes the feature / b blocks
+    // fused update: called before backward, which then applies Adam to the
+    // M block inside the dM kernel (dM is never stored); adam_step finishes
+    // the feature / b blocks
     void adam_begin(double lr, const int* err);
     bool adam_fused = false;
     float ad_lr = 0.f, ad_ibc1 = 0.f, ad_ibc2 = 0.f;
     const int* ad_err = nullptr;
-    // multi-GPU exchange (backward_multi): the local clusters' theta-gradient
-    // rows (bf16) are all-gathered into grows, re-tiled into gall / fall (all
-    // G clusters) for dM; db and the feature-map gradient are all-reduced
+    // ---- sharded optimizer, comm != null:
+    // per minibatch the local clusters' fp32 gtheta rows are split by column
+    // shard and exchanged all-to-all (grecv = every cluster's gtheta on this
+    // rank's shard), db and dM + Adam run on the shard only, and the
+    // refreshed bf16 M image rows and b entries are all-gathered. The
+    // feature-map gradient of each cluster (gz) is all-gathered and the
+    // feature map's backward + Adam run replicated over all clusters. Every
+    // reduction keeps the single-rank order, so any rank count gives the
+    // single-rank result bit for bit.
     Comm* comm = nullptr;
-    Img gall, fall;
-    uint16_t* grows = nullptr;
-    void enable_exchange(Comm* c);
+    int world = 1, rank = 0, Kl = 0;
+    long S = 0, row_lo = 0, row_hi = 0;  // shard width (multiple of 128) and this rank's rows
+    float *gsend = nullptr, *grecv = nullptr;  // [W][Kl][S] fp32
+    Img gshard;                                 // bf16 [G][S]: this shard's gtheta, all clusters
+    Img fall;                                   // bf16 [G][F]: f(w) of all clusters
+    void gather_params(cudaStream_t s);         // all-gather the fp32 M rows (export / checkpoints)
 };
 
 NetDims make_dims(const std::vector<int>& sizes, bool out_tanh, bool has_log_std);
@@ -128,7 +140,8 @@ int pad_groups(const int* rows, int* goff, int G, int* rows_out, int* n_out);
 
 class Trainer {
 public:
-    Trainer(const TrainConfig& cfg, int world = 1, int rank = 0, const void* nccl_id = nullptr);
+    Trainer(const TrainConfig& cfg, int world = 1, int rank = 0, const void* nccl_id = nullptr,
+            LoopGroup* loop = nullptr);
     ~Trainer();
     void iteration(int it, IterStats* st);
 
@@ -164,6 +177,8 @@ public:
     float* d_tracker = nullptr;
     int* d_err = nullptr;
     unsigned long long* d_clamps = nullptr;
+    double* d_retsum = nullptr;  // per instance: sum of completed-episode scalarised returns (rollout.cpp:150-159)
+    int* d_retcnt = nullptr;     // per instance: completed episodes this iteration
     long kernel_launches() const { return g_kernel_launches.load(); }  // process-wide
     Profiler& profiler() { return prof_; }
 
@@ -195,7 +210,8 @@ private:
     TrainConfig cfg_;
     EnvSpecB es_{};
     int world_ = 1, rank_ = 0;
-    Comm* comm_ = nullptr;
+    Comm* comm_ = nullptr;   // actor chain + per-iteration collectives (stream s_)
+    Comm* comm2_ = nullptr;  // critic chain (stream s2_): the two chains' exchanges overlap
     int Nl_ = 0, Kl_ = 0, reps_ = 0, inst_lo_ = 0, g_lo_ = 0;
     long Rl_ = 0;
     HostRng root_;
@@ -233,7 +249,6 @@ private:
         int* rg = nullptr;
     } mbb_[2];
     void use_mb_bufs(int parity);  // point Xi_ / d_Z / ... at buffer set `parity`
-    cudaEvent_t ev_cb_ = nullptr, ev_cr_ = nullptr;  // multi-GPU: critic backward done / its all-reduce done
     Img Xi_;                    // [Bp][obs] gathered observations (bf16 image)
     std::vector<uint8_t*> img_allocs_;
     std::vector<int> rows_tmp_;
@@ -242,8 +257,7 @@ private:
     float *d_Z = nullptr, *d_lpo = nullptr, *d_sa = nullptr, *d_tg = nullptr;
     float *d_lsg = nullptr;
     double *d_lossrows = nullptr, *d_mbloss = nullptr, *d_stats = nullptr, *d_scratch = nullptr;
-    double* d_retsum = nullptr;
-    int* d_retcnt = nullptr;
+    double* d_part = nullptr;  // [K][8] per-cluster normalisation partials (all ranks' after the all-gather)
     NetPlan pol_plan_{}, cri_plan_{};
     uint8_t *d_pol_blob = nullptr, *d_cri_blob = nullptr;
     int mb_done_ = 0;
