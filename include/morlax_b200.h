@@ -254,6 +254,10 @@ void* morlax_trainer_stream(morlax_trainer* t);
 
 /* host-side sharding helper (pure): rows of perm[lo:hi) that belong to
  * instances [inst_lo, inst_lo+n_inst), local row ids grouped by cluster */
+/* host helper: the sharded optimizer's partition of the P hypernet rows
+ * (M rows and b entries): shard width S (a multiple of 128), rank's rows
+ * [row_lo, row_hi) */
+int morlax_shard_rows(int64_t P, int world, int rank, int64_t* S, int64_t* row_lo, int64_t* row_hi);
 int morlax_shard_minibatch(const int32_t* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps,
                            int n_groups, int32_t* rows_out, int32_t* goff_out, int* n_rows_out,
                            int* max_group_out);

@@ -549,6 +549,14 @@ class Trainer:
         return int(LIB.morlax_trainer_kernel_launches(self._h))
 
 
+def shard_rows(P: int, world: int, rank: int):
+    """The sharded optimizer's partition of the P hypernet rows (M rows / b
+    entries): (S, row_lo, row_hi), S a multiple of 128 (trainer.cu shard_rows)."""
+    S, lo, hi = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(LIB.morlax_shard_rows(C.c_int64(P), world, rank, C.byref(S), C.byref(lo), C.byref(hi)))
+    return S.value, lo.value, hi.value
+
+
 def shard_minibatch(perm, lo, hi, T, inst_lo, n_inst, reps, n_groups):
     perm = np.ascontiguousarray(perm, np.int32)
     rows = np.zeros(max(hi - lo, 1), np.int32)

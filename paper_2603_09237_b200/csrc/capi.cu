@@ -985,6 +985,16 @@ int morlax_trainer_profile_get(morlax_trainer* t, int i, char* name64, double* m
 }
 void* morlax_trainer_stream(morlax_trainer* t) { return (void*)t->t->stream(); }
 
+int morlax_shard_rows(int64_t P, int world, int rank, int64_t* S, int64_t* row_lo, int64_t* row_hi) {
+    return guarded([&] {
+        if (P < 1 || world < 1 || rank < 0 || rank >= world) throw ConfigError("shard_rows: bad arguments");
+        long s = 0, lo = 0, hi = 0;
+        shard_rows(P, world, rank, &s, &lo, &hi);
+        *S = s;
+        *row_lo = lo;
+        *row_hi = hi;
+    });
+}
 int morlax_shard_minibatch(const int32_t* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps,
                            int n_groups, int32_t* rows_out, int32_t* goff_out, int* n_rows, int* max_group) {
     return guarded([&] {

@@ -207,11 +207,7 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     P = tgt.P;
     ld = (P + 7) / 8 * 8;
     n = nf + P * F + P;
-    // optimizer shards: whole 128-row chunks of the M image per rank
-    const long rt = (P + 127) / 128;
-    S = ((rt + world - 1) / world) * 128;
-    row_lo = std::min<long>(P, (long)rank * S);
-    row_hi = std::min<long>(P, row_lo + S);
+    shard_rows(P, world, rank, &S, &row_lo, &row_hi);
     if (comm && (nf % 4 || (P * F) % 4))
         throw ShapeError("sharded optimizer: feature-map and M block sizes must be multiples of 4");
     const long pad = comm ? (long)world * S - P : 0;  // b is all-gathered in place (rank r at b + r S)
@@ -576,6 +572,15 @@ void HyperNet::gather_params(cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ sharding
+// optimizer shards: whole 128-row chunks of the M image per rank; rank r
+// owns rows [r S, r S + S) clipped to P (the last ranks may own none)
+void shard_rows(long P, int world, int rank, long* S, long* lo, long* hi) {
+    const long rt = (P + 127) / 128;
+    *S = ((rt + world - 1) / world) * 128;
+    *lo = std::min<long>(P, (long)rank * *S);
+    *hi = std::min<long>(P, *lo + *S);
+}
+
 void shard_minibatch(const int* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps, int n_groups,
                      int* rows_out, int* goff_out, int* n_rows_out, int* max_group) {
     // stable counting sort by (local) cluster id; rows keep minibatch order

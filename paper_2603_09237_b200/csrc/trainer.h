@@ -137,6 +137,8 @@ struct IterStats {
 void shard_minibatch(const int* perm, int lo, int hi, int T, int inst_lo, int n_inst, int reps,
                      int n_groups, int* rows_out, int* goff_out, int* n_rows_out, int* max_group);
 int pad_groups(const int* rows, int* goff, int G, int* rows_out, int* n_out);
+// the sharded optimizer's M-row partition (HyperNet::init)
+void shard_rows(long P, int world, int rank, long* S, long* lo, long* hi);
 
 class Trainer {
 public:
