@@ -258,6 +258,30 @@ def leg_c4(mb):
             "value": R / (ms / 1e3), "ms_per_step": ms}
 
 
+# ---------------------------------------------------------------- roofline of the whole iteration
+def iteration_roofline(prof, hbm_gbs, tflops, iter_ms):
+    """roofline time per iteration = sum over phases of
+    max(FLOP_phase / bf16 peak, bytes_phase / HBM peak), with the algorithmic
+    FLOPs and bytes of every launch of the phase as the dataflow moves them
+    (GEMM operand / activation / gradient images, theta and its packing,
+    optimizer state, rollout batch writes) from the per-launch profile pass.
+    frac = roofline time / measured time per iteration."""
+    phases = {}
+    for name, _ms, fl, by, _n in prof:
+        ph = name.split("/")[0]
+        f, b = phases.get(ph, (0.0, 0.0))
+        phases[ph] = (f + fl, b + by)
+    out, total = {}, 0.0
+    for ph, (f, b) in phases.items():
+        t_f = f / (tflops * 1e12) * 1e3
+        t_b = b / (hbm_gbs * 1e9) * 1e3
+        out[ph] = {"gflop": round(f / 1e9, 2), "gbytes": round(b / 1e9, 3), "ms_tensor": round(t_f, 4),
+                   "ms_hbm": round(t_b, 4), "bound": "tensor" if t_f >= t_b else "hbm"}
+        total += max(t_f, t_b)
+    return {"roofline_ms": round(total, 4), "measured_ms": round(iter_ms, 4), "frac": total / iter_ms,
+            "phases": out}
+
+
 # ---------------------------------------------------------------- GPU arm
 def self_launch(args):
     """--gpus N without a launcher: re-exec this script as N ranks under
@@ -366,6 +390,7 @@ def main():
     hbm, tflops, peak_src = peaks()
     top = prof[0]
     iter_ms = ms / args.steps
+    iteration_roof = iteration_roofline(prof, hbm, tflops, iter_ms)
     if top[3] > 0 and top[2] == 0:
         ach = top[3] / (top[1] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
@@ -374,14 +399,16 @@ def main():
         roof = {"bound": "tensor", "achieved": ach, "peak": tflops, "unit": "TFLOP/s",
                 "frac": ach / tflops}
     traffic, tsrc = None, None
-    tpath = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
-    if os.path.exists(tpath):  # dram__bytes_read + write per launch from an ncu --set full capture
-        tj = json.load(open(tpath)).get(top[0])
-        if tj:
-            traffic, tsrc = tj["dram_bytes_per_launch"], tj["capture"]
+    kname = top[0].split("/")[-1]
+    for tfile in ("r2_ncu_traffic.json", "r1_ncu_traffic.json"):  # the newest capture that has the kernel
+        tpath = os.path.join(ROOT, "profiles", tfile)
+        if traffic is None and os.path.exists(tpath):  # dram__bytes_read + write per launch, ncu --set full
+            tj = json.load(open(tpath)).get(kname)
+            if tj:
+                traffic, tsrc = tj["dram_bytes_per_launch"], tj["capture"]
     roof.update({"traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": tsrc,
                  "algorithmic_bytes_per_launch": top[3] / top[4] if top[4] else None,
-                 "kernel": top[0], "launches_per_iter": top[4],
+                 "kernel": kname, "class": top[0], "launches_per_iter": top[4],
                  "share_of_step": top[1] / sum(p[1] for p in prof),
                  "peak_source": peak_src + (" bf16 sustained" if roof["bound"] == "tensor" else " copy")})
     breakdown = {p[0]: {"ms": round(p[1], 3), "launches": p[4],
@@ -404,6 +431,21 @@ def main():
         pareto = {"points": 1024, "nondominated": int(mask.sum()), "mask_ms": round((t1 - t0) * 1e3, 3),
                   "hv_mc_ms": round((t2 - t1) * 1e3, 3), "hv": hv[0], "hv_stderr": hv[1],
                   "hv_samples": 1_000_000, "hv_exact": hv_ex, "hv_exact_ms": round((t3 - t2) * 1e3, 3)}
+        try:  # the reference's own nondominated_filter / hypervolume_detailed (pareto.cpp:38-77, 209-277)
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            from pyoracle import Oracle
+            r = Oracle("ref")
+            t0 = time.perf_counter()
+            rmask = r.nondominated_mask(pts)
+            t1 = time.perf_counter()
+            rhv = r.hypervolume_detailed(pts[rmask.astype(bool)], -np.ones(6))
+            t2 = time.perf_counter()
+            pareto["reference"] = {"mask_ms": round((t1 - t0) * 1e3, 3), "hv_mc_ms": round((t2 - t1) * 1e3, 3),
+                                   "mask_equal": bool(np.array_equal(rmask, mask)),
+                                   "hv_equal": bool(rhv[0] == hv[0] and rhv[1] == hv[1]), "threads": 1,
+                                   "kind": "reference (oracle/_ref, Release flags)"}
+        except Exception as ex:  # reported, never silently replaced
+            pareto["reference"] = {"unavailable": str(ex)}
     # ---- CPU baseline (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -435,7 +477,9 @@ def main():
                        "parallelism": f"dp{world}", "l2": "working set > L2 (Adam state 666 MB/iter)"},
             "e2e": {"value": e2e, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": launches, "roofline": {**roof, "iteration_frac": iteration_roof["frac"],
+                                                   "iteration": iteration_roof},
+            "cpu_baseline": cpu, "clocks": clk.summary(),
             "breakdown_ms_per_iter": breakdown, "pareto": pareto, "other_configs": legs,
         }))
     if world > 1:

@@ -219,9 +219,15 @@ struct RolloutTcArgs : RolloutArgs {
     NetPlan pol_plan, cri_plan;
     const uint8_t* pol_blob;  // [K][pol_plan.blob_bytes]
     const uint8_t* cri_blob;
+    const float* eps;         // [T][N][ad] the rollout's N(0,1) draws (rollout_noise)
     int slot_bytes, xb_bytes, hb_bytes, nepad;  // filled by rollout_tc
 };
 void rollout_tc(RolloutTcArgs a, cudaStream_t s);
+// the N(0,1) draws of a whole rollout, ahead of it and in parallel:
+// eps[t][i][d] = (float) Box-Muller of words 2 (t ad + d) + 1, + 2 of instance
+// i's stream roll_key.split(inst_base + i) (rollout.cpp:101, nn.cpp:192-202,
+// rng.hpp:55-60) -- the exact value the sequential sampler adds to the mean
+void rollout_noise(uint64_t roll_key, int inst_base, int N, int T, int ad, float* eps, cudaStream_t s);
 
 // ---------------------------------------------------------------- GAE + normalise (K4)
 void gae_scan(int N, int T, int m, const float* reward, const float* value, const float* next_value,

@@ -16,9 +16,15 @@
 // * Output layer: D[env][out] = act (A, MN-major, M = 64 envs) x W_out^T
 //   (B, K-major, N = 16), so each env-owning thread gets its own outputs
 //   and goes straight on to sampling / the env step.
+// * The N(0,1) draws do not depend on the policy: k_rollout_noise computes
+//   all T steps' fp64 Box-Muller draws ahead at full occupancy (bit-identical
+//   words, rounded to fp32 exactly where the sequential sampler rounds), and
+//   the sampler only reads them.
 // * Critic: once per step at the pre-reset final observation; at the
 //   current observation only when the previous step reset an instance (or
 //   t = 0), because V(o_{t+1}) = next_value_t otherwise.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "umma.cuh"
@@ -199,7 +205,6 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
     float* LS = reinterpret_cast<float*>(p); p += sizeof(float) * 16;
     uint64_t* EK = reinterpret_cast<uint64_t*>(p); p += 8 * RE;
     uint64_t* EC = reinterpret_cast<uint64_t*>(p); p += 8 * RE;
-    uint64_t* RK = reinterpret_cast<uint64_t*>(p); p += 8 * RE;
     int* STP = reinterpret_cast<int*>(p); p += 4 * RE;
     int* NEED = reinterpret_cast<int*>(p); p += 4 * RE;
     int* VF = reinterpret_cast<int*>(p); p += 16;   // vflag of step t (index t & 1)
@@ -224,7 +229,6 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             EK[r] = a.env_key[i0 + r];
             EC[r] = a.env_ctr[i0 + r];
             STP[r] = a.steps[i0 + r];
-            RK[r] = split_key(a.roll_key, (uint64_t)(a.roll_inst_base + i0 + r));  // rollout.cpp:101
             for (int k = 0; k < m; ++k) TRK[r * 8 + k] = a.tracker[(long)(i0 + r) * m + k];
         }
     }
@@ -277,14 +281,13 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         umma::fence_before_sync();
         __syncthreads();
         RPROF(2);
-        // ---- Gaussian sample, 2 words per dim (nn.cpp:192-202, rng.hpp:55-60)
+        // ---- Gaussian sample (nn.cpp:192-202): the precomputed draw of (t, instance, dim)
+        const float* eps_t = a.eps + ((long)t * a.N + i0) * ad;
         for (int e = tid; e < nr * ad; e += RNT) {
-            const int r = e / ad, d = e % ad;
-            const uint64_t base = 2ull * ((uint64_t)t * ad + d);
-            const double eps = box_muller(rng_word(RK[r], base + 1), rng_word(RK[r], base + 2));
+            const int r = e / ad, d = e - r * ad;
             const float sig = __expf(LS[d]);
             const float mu = MU[r * 16 + d];
-            const float z = mu + sig * (float)eps;
+            const float z = mu + sig * eps_t[e];
             a.act_pre[((long)(i0 + r) * a.T + t) * ad + d] = z;
             // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
             // squashed action tanh(z) for the env step: both per (env, dim) item here
@@ -453,6 +456,20 @@ __global__ void k_pack_theta(const float* __restrict__ theta, long P, NetDims nd
         *reinterpret_cast<uint4*>(out + byte) = q;
     }
 }
+
+// one thread per (step, instance, dim): the fp64 Box-Muller draw of words
+// 2 (t ad + d) + 1, + 2 of the instance's rollout stream, rounded to fp32
+__global__ void k_rollout_noise(uint64_t roll_key, int inst_base, int N, int T, int ad, float* __restrict__ eps) {
+    const long n = (long)T * N * ad;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const long ti = e / ad;
+        const int d = (int)(e - ti * ad);
+        const int t = (int)(ti / N), i = (int)(ti - (long)t * N);
+        const uint64_t key = split_key(roll_key, (uint64_t)(inst_base + i));  // rollout.cpp:101
+        const uint64_t base = 2ull * ((uint64_t)t * ad + d);
+        eps[e] = (float)box_muller(rng_word(key, base + 1), rng_word(key, base + 2));
+    }
+}
 }  // namespace
 
 static int pad16(int x) { return (x + 15) / 16 * 16; }
@@ -488,9 +505,17 @@ void pack_theta(const float* theta, long ld, int G, const NetDims& nd, const Net
     MB_LAUNCH();
 }
 
+void rollout_noise(uint64_t roll_key, int inst_base, int N, int T, int ad, float* eps, cudaStream_t s) {
+    const long n = (long)T * N * ad;
+    if (n == 0) return;
+    k_rollout_noise<<<(unsigned)std::min<long>((n + 255) / 256, (long)device_sms() * 16), 256, 0, s>>>(
+        roll_key, inst_base, N, T, ad, eps);
+    MB_LAUNCH();
+}
+
 size_t rollout_tc_smem(const RolloutTcArgs& a) {
     return 2ull * a.slot_bytes + a.xb_bytes + 2ull * a.hb_bytes + sizeof(float) * a.sdim * RE +
-           sizeof(float) * RE * (16 + 16 + 8 + 8 + 8) + 64 + 3 * 8 * RE + 2 * 4 * RE + 16 + 16 + 8 + 16;
+           sizeof(float) * RE * (16 + 16 + 8 + 8 + 8) + 64 + 2 * 8 * RE + 2 * 4 * RE + 16 + 16 + 8 + 16;
 }
 
 void rollout_tc(RolloutTcArgs a, cudaStream_t s) {

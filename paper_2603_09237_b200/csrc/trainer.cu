@@ -118,11 +118,12 @@ static InitLayers init_layers(const std::vector<int>& s) {
 // ------------------------------------------------------------------ profiler
 int Profiler::begin(const char* name, double flops, double bytes, cudaStream_t s) {
     if (!on) return -1;
+    const std::string key = phase + "/" + name;  // the iteration phase the launch belongs to
     int c = -1;
     for (size_t i = 0; i < cls.size(); ++i)
-        if (cls[i].name == name) c = (int)i;
+        if (cls[i].name == key) c = (int)i;
     if (c < 0) {
-        cls.push_back(Cls{name});
+        cls.push_back(Cls{key});
         c = (int)cls.size() - 1;
     }
     cls[c].flops += flops;
@@ -317,9 +318,22 @@ void HyperNet::init_params(uint64_t key, cudaStream_t s) {  // hypernet.cpp:124-
     to_img(p + nf, F, 0, (int)P, F, mimg, 1, s);
 }
 
+// algorithmic bytes of one tcgen05 GEMM of this dataflow: the bf16 operand
+// images (B once per group for the row-grouped GEMMs), the tanh' operand,
+// and the output (bf16 image or fp32, per group for the K-grouped ones)
+static double igemm_bytes(const IGemm& d) {
+    const double M = d.M, N = d.N, K = d.K, Z = d.Z;
+    double b = 2.0 * M * K;                        // A
+    b += 2.0 * N * K * (d.gmode == 1 ? Z : 1.0);   // B (per group weights when rows are grouped)
+    if (d.act == 2) b += 2.0 * M * N;              // tanh' operand image
+    const double outs = M * N * (d.gmode == 2 ? Z : (d.gmode == 0 ? Z : 1.0));
+    if (d.o_mode) b += 2.0 * outs;
+    if (d.C) b += 4.0 * outs;
+    return b;
+}
 static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
     const double f = 2.0 * d.M * d.N * d.K * (d.gmode == 0 ? d.Z : 1);
-    ProfScope p(cls, f, 0, s);
+    ProfScope p(cls, f, igemm_bytes(d), s);
     img_gemm(d, s);
 }
 
@@ -350,7 +364,7 @@ void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0
     }
     {
         IGemm ds[2];
-        double fl = 0;
+        double fl = 0, by = 0;
         for (int k = 0; k < nh; ++k) {
             HyperNet& h = *hs[k];
             IGemm& d = ds[k];  // theta[g][p] = b[p] + sum_k f[g][k] M[p][k]: rows = clusters
@@ -360,8 +374,9 @@ void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0
             d.bias = h.p + h.nf + h.P * h.F; d.bias_mode = 1;
             d.C = h.theta + (long)g0 * h.ld; d.cm = h.ld; d.cn = 1;
             fl += 2.0 * d.M * d.N * d.K;
+            by += igemm_bytes(d);
         }
-        ProfScope ps("hyper_theta", fl, 0, s);
+        ProfScope ps("hyper_theta", fl, by, s);
         img_gemm_batch(ds, nh, s);
     }
     for (int k = 0; k < nh; ++k) {
@@ -408,13 +423,14 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
     if (part != 2) {  // the gradient passes (no parameter is written)
         for (int k = 0; k < nh; ++k) {  // local gimg (df operand) + db (single rank) in one pass
             HyperNet& h = *hs[k];
+            ProfScope ps("gtheta_prep", 0, 6.0 * h.fng * h.P + (h.comm ? 8.0 * h.world * h.Kl * h.S : 4.0 * h.P), s);
             gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg,
                         h.comm ? nullptr : h.g + h.nf + h.P * h.F, s);
             if (h.comm) pack_shards(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, h.S, h.world, h.gsend, s);
         }
         {
             IGemm ds[2];
-            double fl = 0;
+            double fl = 0, by = 0;
             for (int k = 0; k < nh; ++k) {
                 HyperNet& h = *hs[k];
                 IGemm& d = ds[k];  // gf[g][k] = sum_p gtheta[g][p] M[p][k], split-K over 128-aligned P ranges
@@ -424,8 +440,9 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
                 d.gmode = 2; d.goff = h.d_split_bounds;
                 d.C = h.parts; d.cm = h.F; d.cn = 1; d.c_gs = (long)h.fng * h.F;
                 fl += 2.0 * d.M * d.N * d.K;
+                by += igemm_bytes(d);
             }
-            ProfScope ps("hyper_df", fl, 0, s);
+            ProfScope ps("hyper_df", fl, by, s);
             img_gemm_batch(ds, nh, s);
         }
         FeatDims loc[2], all[2];
@@ -472,7 +489,7 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
         }
         {
             IGemm ds[2];
-            double fl = 0;
+            double fl = 0, by = 0;
             int nd = 0;
             for (int k = 0; k < nh; ++k) {
                 HyperNet& h = *hs[k];
@@ -483,9 +500,10 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
                 d.M = (int)(h.row_hi - h.row_lo); d.N = h.F; d.K = h.comm ? h.G : h.fng;
                 d.C = h.g + h.nf + h.row_lo * h.F; d.cm = h.F; d.cn = 1;
                 fl += 2.0 * d.M * d.N * d.K;
+                by += igemm_bytes(d);
             }
             if (nd) {
-                ProfScope ps("hyper_dM", fl, 0, s);
+                ProfScope ps("hyper_dM", fl, by, s);
                 img_gemm_batch(ds, nd, s);
             }
         }
@@ -690,7 +708,7 @@ Trainer::~Trainer() {
     if (g_prof == &prof_) g_prof = nullptr;
     actor_.free_all();
     critic_.free_all();
-    for (auto* p : {d_obs, d_act, d_lp, d_rew, d_val, d_nval, d_adv, d_tgt, d_sadv, d_state, d_tracker, d_cw,
+    for (auto* p : {d_obs, d_act, d_eps, d_lp, d_rew, d_val, d_nval, d_adv, d_tgt, d_sadv, d_state, d_tracker, d_cw,
                     d_lsg, mbb_[0].Z, mbb_[0].lpo, mbb_[0].sa, mbb_[0].tg, mbb_[1].Z, mbb_[1].lpo, mbb_[1].sa,
                     mbb_[1].tg})
         if (p) cudaFree(p);
@@ -723,6 +741,7 @@ void Trainer::alloc() {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     d_obs = dalloc<float>(Rl_ * od);
     d_act = dalloc<float>(Rl_ * ad);
+    d_eps = dalloc<float>(Rl_ * ad);
     d_lp = dalloc<float>(Rl_);
     d_rew = dalloc<float>(Rl_ * m);
     d_val = dalloc<float>(Rl_ * m);
@@ -829,6 +848,7 @@ Img Trainer::new_img(int R, int C) {
 
 void Trainer::phase_rollout(int it) {
     g_prof = &prof_;
+    prof_.phase = "rollout";
     const int m = es_.m, K = cfg_.K;
     const HostRng iter = root_.split(0x10000000ULL + (uint64_t)it);  // train.cpp:120
     cw_h_.assign((size_t)K * m, 0.f);
@@ -878,6 +898,11 @@ void Trainer::phase_rollout(int it) {
     a.state = d_state; a.env_key = d_ekey; a.env_ctr = d_ectr; a.steps = d_steps;
     a.roll_key = iter.split(1).key;  // train.cpp:146
     a.roll_inst_base = inst_lo_;
+    {
+        ProfScope ps("noise", 0, 4.0 * Rl_ * es_.act_dim, s_);
+        rollout_noise(a.roll_key, inst_lo_, Nl_, cfg_.T, es_.act_dim, d_eps, s_);
+    }
+    a.eps = d_eps;
     a.obs = d_obs; a.act_pre = d_act; a.logprob = d_lp; a.reward = d_rew; a.value = d_val; a.next_value = d_nval;
     a.term = d_term; a.trunc = d_trunc; a.tracker = d_tracker;
     a.cluster_w = d_cw + (size_t)g_lo_ * m;
@@ -889,7 +914,9 @@ void Trainer::phase_rollout(int it) {
         double macs = 0;
         for (int l = 0; l < a.pol.L; ++l) macs += (double)a.pol.sz[l] * a.pol.sz[l + 1];
         for (int l = 0; l < a.cri.L; ++l) macs += (double)a.cri.sz[l] * a.cri.sz[l + 1];
-        ProfScope ps("rollout", 2.0 * macs * Rl_, 0, s_);
+        // batch writes (obs, pre-tanh action, log-prob, reward / value / next value, flags)
+        const double by = (double)Rl_ * (4.0 * (a.od + a.ad + 1 + 3 * m) + 2);
+        ProfScope ps("rollout", 2.0 * macs * Rl_, by, s_);
         rollout_tc(a, s_);
     }
     prepare_perms(it);  // host work overlaps the rollout on the GPU
@@ -982,6 +1009,7 @@ void Trainer::prepare_perms(int it) {
 
 void Trainer::phase_advantages() {
     g_prof = &prof_;
+    prof_.phase = "advantages";
     const int m = es_.m;
     {
         ProfScope ps("gae", 0, (double)Rl_ * (5.0 * m * 4 + 2), s_);  // r,V,V' in; A,target out; flags
@@ -1057,9 +1085,12 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
         return w;
     };
     auto batch = [&](const char* cls, const IGemm* ds, int n) {
-        double fl = 0;
-        for (int k = 0; k < n; ++k) fl += 2.0 * ds[k].M * ds[k].N * ds[k].K * (ds[k].gmode == 0 ? ds[k].Z : 1);
-        ProfScope ps(cls, fl, 0, s_);
+        double fl = 0, by = 0;
+        for (int k = 0; k < n; ++k) {
+            fl += 2.0 * ds[k].M * ds[k].N * ds[k].K * (ds[k].gmode == 0 ? ds[k].Z : 1);
+            by += igemm_bytes(ds[k]);
+        }
+        ProfScope ps(cls, fl, by, s_);
         img_gemm_batch(ds, n, s_);
     };
     const int Lmax = std::max(N[0].h->tgt.L, nn > 1 ? N[1].h->tgt.L : 0);
@@ -1108,7 +1139,9 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
             ha.psum = u.pbias[L - 1]; ha.psls = u.psls; ha.psum_prev = u.pbias[L - 2]; ha.psum_prev_ld = nd.sz[L - 1];
             ha.loss_rows = u.lossrows;
             const double fl = 4.0 * Bp * nd.sz[L - 1] * nd.sz[L];  // forward + backward of the output layer
-            ProfScope ps("mlp_head", fl, 0, s_);
+            // last hidden activation image in, its gradient image out, the row inputs and output-layer gradient
+            const double by = 4.0 * Bp * nd.sz[L - 1] + 4.0 * Bp * (nd.sz[L] + 4) + 2.0 * Bp * nd.sz[L];
+            ProfScope ps("mlp_head", fl, by, s_);
             head(ha, t.actor, s_);
         } else if (t.actor) {  // losses.cpp:87-129
             actor_rows_img(Bp, es_.act_dim, rows, d_rowgroup, t.th, t.h->ld, nd.mlp_n, u.Zf, 16, d_Z, d_lpo, d_sa,
@@ -1169,7 +1202,10 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
         jb.loss[k] = SegLoss{t.u->lossrows, Bp / 128, d_mbloss + slot * 2 + (t.actor ? 0 : 1)};
     }
     jb.nloss = nn;
-    segsum_multi(jb, goff, Kl_, s_);
+    {
+        ProfScope ps("segsum", 0, 4.0 * (Bp / 128) * 16 * 2 * 8 + 8.0 * Bp, s_);  // per-tile partials -> per cluster
+        segsum_multi(jb, goff, Kl_, s_);
+    }
 }
 
 // One PPO minibatch (train.cpp:163-180). The actor chain runs on s_, the
@@ -1217,6 +1253,7 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         ga.rows = rows; ga.goff = goff;
         ga.obs = d_obs; ga.act = d_act; ga.lp = d_lp; ga.sadv = d_sadv; ga.tgt = d_tgt;
         ga.Xi = Xi_; ga.act_o = d_Z; ga.lp_o = d_lpo; ga.sadv_o = d_sa; ga.tgt_o = d_tg; ga.rg = d_rowgroup;
+        ProfScope ps("gather", 0, (double)Bp * (4.0 * od + 2.0 * od + 8.0 * ad + 16.0 + 8.0 * m + 4.0), s3_);
         gather_minibatch(ga, s3_);
     }
     MB_CUDA(cudaEventRecord(ev_gather_, s3_));
@@ -1234,6 +1271,37 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         critic_.adam_step(cfg_.critic_lr, d_err, s_);
         MB_CUDA(cudaEventRecord(ev_cfin_, s_));
+        return;
+    }
+    static const bool decouple = [] {  // MORLAX_DECOUPLE=1: A/B of per-chain finiteness checks
+        const char* e = std::getenv("MORLAX_DECOUPLE");
+        return e && e[0] == '1';
+    }();
+    if (decouple) {
+        // each chain checks its own loss and applies its Adam without waiting
+        // for the other chain; a non-finite loss of either sets the shared
+        // error flag, every later Adam of the iteration is skipped and the
+        // iteration raises NumericError (train() then keeps the last healthy
+        // parameters, as the reference's train() does)
+        critic_.forward(d_cw, g_lo_, Kl_, sc);
+        MB_CUDA(cudaStreamWaitEvent(sc, ev_gather_, 0));
+        net_step(&both[1], &roles[1], 1, Bp, inv_B, maxg, rows, goff, slot, sc);
+        MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], sc));
+        HyperNet::backward_multi(&both[1], 1, sc, 1);
+        if (comm2_) comm_allreduce_f64(comm2_, d_mbloss + slot * 2 + 1, 1, sc);
+        check_finite_f64(d_mbloss + slot * 2 + 1, 1, d_err, 3, sc);
+        HyperNet::backward_multi(&both[1], 1, sc, 2);
+        critic_.adam_step(cfg_.critic_lr, d_err, sc);
+        MB_CUDA(cudaEventRecord(ev_cfin_, sc));
+        actor_.forward(d_cw, g_lo_, Kl_, s_);
+        MB_CUDA(cudaStreamWaitEvent(s_, ev_gather_, 0));
+        net_step(&both[0], &roles[0], 1, Bp, inv_B, maxg, rows, goff, slot, s_);
+        MB_CUDA(cudaEventRecord(ev_ad_[mb_par_], s_));
+        HyperNet::backward_multi(&both[0], 1, s_, 1);
+        if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 1, s_);
+        check_finite_f64(d_mbloss + slot * 2, 1, d_err, 3, s_);
+        HyperNet::backward_multi(&both[0], 1, s_, 2);
+        actor_.adam_step(cfg_.actor_lr, d_err, s_);
         return;
     }
     // the forwards (feature map, theta, weight packing) need no minibatch rows
@@ -1265,6 +1333,7 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
 
 void Trainer::phase_update(int it, int max_minibatches) {
     g_prof = &prof_;
+    prof_.phase = "update";
     (void)it;
     const int mbs = cfg_.minibatch_count;
     mb_done_ = 0;

@@ -29,6 +29,7 @@ struct Profiler {
         long count = 0;
     };
     bool on = false;
+    std::string phase = "iteration";  // class key prefix: the phase being enqueued
     std::vector<Cls> cls;
     std::vector<cudaEvent_t> pool;
     struct Pending { int c; cudaEvent_t a, b; };
@@ -174,6 +175,7 @@ public:
           *d_nval = nullptr, *d_adv = nullptr, *d_tgt = nullptr, *d_sadv = nullptr;
     uint8_t *d_term = nullptr, *d_trunc = nullptr;
     float* d_state = nullptr;
+    float* d_eps = nullptr;  // [T][local N][act_dim] the rollout's N(0,1) draws
     uint64_t *d_ekey = nullptr, *d_ectr = nullptr;
     int* d_steps = nullptr;
     float* d_tracker = nullptr;

@@ -1,6 +1,9 @@
-# A/B of an environment knob: VAR=name VALUES="a b c" bash tools/gpu_ab_env.sh
-for v in $VALUES; do
-  export $VAR=$v
-  timeout 300 python tools/profile_step.py c3 4 >/dev/null 2>&1
-  MORLAX_HOST_TIMING=1 timeout 300 python tools/profile_step.py c3 6 2>&1 | grep "host enqueue" | tail -4 | awk -v v=$v '{print v, $NF}'
+# A/B of env settings on the bench (in-situ): each argument is an env assignment list ("X=1 Y=2" or "none")
+for v in "$@"; do
+  if [ "$v" = none ]; then vv=""; else vv="$v"; fi
+  for rep in 1 2; do
+    env $vv timeout 300 python bench.py --no-legs --no-cpu-baseline --steps 10 > gpurun_out/ab.json 2>/dev/null
+    python -c "
+import json; d=json.load(open('gpurun_out/ab.json')); print('== $v', 'iter_ms %.3f' % d['ms_per_step'])"
+  done
 done
