@@ -250,6 +250,11 @@ int morlax_trainer_profile_enable(morlax_trainer* t, int on);
 int morlax_trainer_profile_count(morlax_trainer* t);
 int morlax_trainer_profile_get(morlax_trainer* t, int i, char* name64, double* ms, double* flops, double* bytes,
                                int64_t* count);
+/* per-launch timeline of the profiled iteration (class, stream index,
+ * start / end in ms from its first launch; CUDA events around each launch) */
+int morlax_trainer_profile_timeline_count(morlax_trainer* t);
+int morlax_trainer_profile_timeline(morlax_trainer* t, int i, char* name64, int* stream, double* t0_ms,
+                                    double* t1_ms);
 void* morlax_trainer_stream(morlax_trainer* t);
 
 /* host-side sharding helper (pure): rows of perm[lo:hi) that belong to

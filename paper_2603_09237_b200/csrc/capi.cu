@@ -983,6 +983,28 @@ int morlax_trainer_profile_get(morlax_trainer* t, int i, char* name64, double* m
         *count = c.count;
     });
 }
+int morlax_trainer_profile_timeline(morlax_trainer* t, int i, char* name64, int* stream, double* t0_ms,
+                                    double* t1_ms) {
+    return guarded([&] {
+        Profiler& p = t->t->profiler();
+        p.collect();
+        if (i < 0 || i >= (int)p.timeline.size()) throw ShapeError("timeline index out of range");
+        const auto& sp = p.timeline[i];
+        std::strncpy(name64, p.cls[sp.c].name.c_str(), 63);
+        name64[63] = 0;
+        *stream = sp.stream;
+        *t0_ms = sp.t0;
+        *t1_ms = sp.t1;
+    });
+}
+int morlax_trainer_profile_timeline_count(morlax_trainer* t) {
+    int n = 0;
+    guarded([&] {
+        t->t->profiler().collect();
+        n = (int)t->t->profiler().timeline.size();
+    });
+    return n;
+}
 void* morlax_trainer_stream(morlax_trainer* t) { return (void*)t->t->stream(); }
 
 int morlax_shard_rows(int64_t P, int world, int rank, int64_t* S, int64_t* row_lo, int64_t* row_hi) {

@@ -533,20 +533,6 @@ void img_gemm_batch(const IGemm* ds, int n, cudaStream_t s) {
 
 void img_gemm(const IGemm& d, cudaStream_t s) { img_gemm_batch(&d, 1, s); }
 
-__global__ void k_tile_segsum(const float* psum, long ld, int width, const int* goff, float* out, long out_gs) {
-    const int z = blockIdx.x;
-    const int j = threadIdx.x;
-    if (j >= width) return;
-    float acc = 0.f;
-    for (int t = goff[z] >> 7; t < (goff[z + 1] >> 7); ++t) acc += psum[(long)t * ld + j];
-    out[(long)z * out_gs + j] = acc;
-}
-void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, float* out, long out_gs,
-                 cudaStream_t s) {
-    k_tile_segsum<<<G, ((width + 31) / 32) * 32, 0, s>>>(psum, ld, width, goff, out, out_gs);
-    MB_LAUNCH();
-}
-
 // every per-cluster segment sum of one net's minibatch step in one launch:
 // block z < G sums job j's tiles of cluster z (fixed order), block G sums
 // the per-tile loss partials (fp64, fixed tree) into *loss_out
@@ -841,61 +827,6 @@ void gather_minibatch(const MbGather& a, cudaStream_t s) {
     if (a.Bp <= 0) return;
     if (a.Bp % 128) throw ShapeError("gather_minibatch: rows must be 128-padded per cluster");
     launch_pdl(k_gather_minibatch, dim3(a.Bp / 128), dim3(128), 0, s, a);
-    MB_LAUNCH();
-}
-
-// fp32 gather with padding (-1 -> 0)
-__global__ void k_gather_pad(const int* rows, int Bp, const float* __restrict__ src, int width, float* dst) {
-    const long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (e >= (long)Bp * width) return;
-    const int q = (int)(e / width), j = (int)(e % width);
-    const int r = rows[q];
-    dst[e] = r >= 0 ? src[(long)r * width + j] : 0.f;
-}
-void gather_pad(const int* rows, int Bp, const float* src, int width, float* dst, cudaStream_t s) {
-    const long n = (long)Bp * width;
-    if (n == 0) return;
-    k_gather_pad<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rows, Bp, src, width, dst);
-    MB_LAUNCH();
-}
-
-// per-group column sums of an image's rows [goff[z], goff[z+1]) for columns
-// [0, width): out fp32 [z*out_gs + j] and, if gimg.p, the gtheta image at
-// (row z, col c0 + j)
-__global__ void k_img_segcolsum(Img x, int width, const int* goff, float* out, long out_gs, Img gimg, long c0) {
-    const int z = blockIdx.y;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= width) return;
-    const int CT = img_ct(x.C);
-    float s = 0.f;
-    for (int q = goff[z]; q < goff[z + 1]; ++q)
-        s += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(x.p + img_off(q, j, CT)));
-    out[z * out_gs + j] = s;
-    if (gimg.p)
-        *reinterpret_cast<__nv_bfloat16*>(gimg.p + img_off(z, c0 + j, img_ct(gimg.C))) = __float2bfloat16_rn(s);
-}
-void img_segcolsum(const Img& x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg, long c0,
-                   cudaStream_t s) {
-    dim3 grid((width + 127) / 128, G);
-    k_img_segcolsum<<<grid, 128, 0, s>>>(x, width, goff, out, out_gs, gimg, c0);
-    MB_LAUNCH();
-}
-
-// fp32 per-group column sums (log-std gradients) -> fp32 flat + image
-__global__ void k_segcolsum_f32(const float* x, int width, const int* goff, float* out, long out_gs, Img gimg,
-                                long c0) {
-    const int z = blockIdx.y;
-    const int j = threadIdx.x;
-    if (j >= width) return;
-    float s = 0.f;
-    for (int q = goff[z]; q < goff[z + 1]; ++q) s += x[(long)q * width + j];
-    out[z * out_gs + j] = s;
-    if (gimg.p)
-        *reinterpret_cast<__nv_bfloat16*>(gimg.p + img_off(z, c0 + j, img_ct(gimg.C))) = __float2bfloat16_rn(s);
-}
-void segcolsum_f32(const float* x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg,
-                   long c0, cudaStream_t s) {
-    k_segcolsum_f32<<<dim3(1, G), 32, 0, s>>>(x, width, goff, out, out_gs, gimg, c0);
     MB_LAUNCH();
 }
 

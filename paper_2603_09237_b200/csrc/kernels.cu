@@ -360,159 +360,6 @@ void scalarize(int N, int T, int m, const float* adv, const float* cluster_w, in
     MB_LAUNCH();
 }
 
-// =========================================================================
-// K5 pieces: minibatch gather and per-row loss heads (losses.cpp:87-129,
-// 170-185).
-// =========================================================================
-__global__ void k_gather(const int* rows, int B, const float* src, int width, float* dst) {
-    const long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (e >= (long)B * width) return;
-    const int q = e / width, j = e % width;
-    dst[e] = src[(long)rows[q] * width + j];
-}
-void gather_rows(const int* rows, int B, const float* src, int width, float* dst, cudaStream_t s) {
-    const long n = (long)B * width;
-    if (n == 0) return;
-    k_gather<<<(int)((n + 255) / 256), 256, 0, s>>>(rows, B, src, width, dst);
-    MB_LAUNCH();
-}
-
-__global__ void k_fill_row_group(const int* goff, int G, int* rg) {
-    const int g = blockIdx.x;
-    for (int q = goff[g] + threadIdx.x; q < goff[g + 1]; q += blockDim.x) rg[q] = g;
-}
-void fill_row_group(const int* goff, int G, int* row_group, int B, cudaStream_t s) {
-    (void)B;
-    k_fill_row_group<<<G, 256, 0, s>>>(goff, G, row_group);
-    MB_LAUNCH();
-}
-
-__global__ void k_actor_rows(int B, int ad, const int* rg, const float* theta, long P, long mlp_n,
-                             const float* mu, const float* z, const float* lp_old, const float* sadv,
-                             float clip, float ent, float inv_B, float* g_mu, float* lsg, double* loss_rows,
-                             int* err) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= B) return;
-    const float* th = theta + (long)rg[q] * P + mlp_n;
-    float lp = 0.f, ls[16], zn[16], sig[16];
-    float ent_h = 0.f;
-    for (int d = 0; d < ad; ++d) {  // action_logprob (nn.cpp:204-219) with the recomputed mean
-        const float raw = th[d];
-        ls[d] = fminf(fmaxf(raw, -5.f), 1.f);
-        sig[d] = __expf(ls[d]);
-        const float zz = z[(long)q * ad + d];
-        zn[d] = (zz - mu[(long)q * ad + d]) / sig[d];
-        lp += -0.5f * zn[d] * zn[d] - ls[d] - 0.9189385332046727f;
-        lp -= __logf(sech2_f(zz) + 1e-6f);
-        ent_h += ls[d] + 0.5f * (1.f + 1.8378770664093453f);  // gaussian_entropy
-    }
-    const float ratio = __expf(lp - lp_old[q]);
-    if (!isfinite(ratio)) atomicExch(err, 3);  // losses.cpp:103-105
-    const float adv = sadv[q];
-    const float unc = ratio * adv;
-    const float clp = fminf(fmaxf(ratio, 1.f - clip), 1.f + clip) * adv;
-    loss_rows[q] = (double)(-fminf(unc, clp) * inv_B) - (double)(ent * ent_h * inv_B);
-    const float glp = unc <= clp ? -ratio * adv * inv_B : 0.f;  // losses.cpp:116
-    for (int d = 0; d < ad; ++d) {
-        g_mu[(long)q * ad + d] = glp * zn[d] / sig[d];  // pre-activation gradient (no tanh')
-        const float raw = th[d];
-        lsg[(long)q * ad + d] = (raw >= -5.f && raw <= 1.f) ? glp * (zn[d] * zn[d] - 1.f) - ent * inv_B : 0.f;
-    }
-}
-void actor_rows(int B, int ad, const int* row_group, const float* theta, long P, long mlp_n,
-                const float* mu, const float* z, const float* lp_old, const float* sadv, float clip,
-                float ent, float inv_B, float* g_mu, float* lsg, double* loss_rows, int* err,
-                cudaStream_t s) {
-    k_actor_rows<<<(B + 255) / 256, 256, 0, s>>>(B, ad, row_group, theta, P, mlp_n, mu, z, lp_old, sadv,
-                                                 clip, ent, inv_B, g_mu, lsg, loss_rows, err);
-    MB_LAUNCH();
-}
-
-__global__ void k_critic_rows(int B, int m, const float* v, const float* tgt, float inv_B, float* g,
-                              double* loss_rows) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= B) return;
-    double l = 0.0;
-    for (int k = 0; k < m; ++k) {
-        const float e = v[(long)q * m + k] - tgt[(long)q * m + k];
-        l += (double)e * e * inv_B;
-        g[(long)q * m + k] = 2.f * e * inv_B;  // losses.cpp:179-181 (no 1/2)
-    }
-    loss_rows[q] = l;
-}
-void critic_rows(int B, int m, const float* v, const float* tgt, float inv_B, float* g_out,
-                 double* loss_rows, cudaStream_t s) {
-    k_critic_rows<<<(B + 255) / 256, 256, 0, s>>>(B, m, v, tgt, inv_B, g_out, loss_rows);
-    MB_LAUNCH();
-}
-
-// out[z][j] (+)= sum_{q in [goff[z], goff[z+1])} x[q][j]; one block per (z, 128-col tile)
-__global__ void k_segcolsum(const float* x, int width, const int* goff, float* out, long out_bz, int acc) {
-    const int z = blockIdx.y;
-    const int j = blockIdx.x * 128 + (threadIdx.x & 127);
-    const int half = threadIdx.x >> 7;  // 2 row-halves
-    __shared__ float red[256];
-    const int lo = goff[z], hi = goff[z + 1];
-    float s = 0.f;
-    if (j < width)
-        for (int q = lo + half; q < hi; q += 2) s += x[(long)q * width + j];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    if (half == 0 && j < width) {
-        const float v = red[threadIdx.x] + red[threadIdx.x + 128];
-        float* o = out + z * out_bz + j;
-        *o = acc ? *o + v : v;
-    }
-}
-void segmented_colsum(const float* x, int width, const int* goff, int G, float* out, long out_bz,
-                      int accumulate, cudaStream_t s) {
-    dim3 grid((width + 127) / 128, G);
-    k_segcolsum<<<grid, 256, 0, s>>>(x, width, goff, out, out_bz, accumulate);
-    MB_LAUNCH();
-}
-
-// out[j] = sum_r x[r][j]
-__global__ void k_colsum(const float* __restrict__ x, int rows, long width, long ld, float* out) {
-    const long j = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (j >= width) return;
-    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 8 independent chains: loads stay in flight
-    int r = 0;
-    for (; r + 8 <= rows; r += 8)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] += x[(long)(r + u) * ld + j];
-    for (; r < rows; ++r) a[0] += x[(long)r * ld + j];
-    out[j] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-}
-void colsum_rows(const float* x, int rows, long width, long ld, float* out, cudaStream_t s) {
-    k_colsum<<<(int)((width + 255) / 256), 256, 0, s>>>(x, rows, width, ld, out);
-    MB_LAUNCH();
-}
-
-__global__ void k_sum_f64(const double* __restrict__ x, long n, double* out, int acc) {
-    __shared__ double red[1024];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    long i = threadIdx.x;
-    for (; i + 3 * (long)blockDim.x < n; i += 4 * (long)blockDim.x) {
-        s0 += x[i];
-        s1 += x[i + blockDim.x];
-        s2 += x[i + 2 * (long)blockDim.x];
-        s3 += x[i + 3 * (long)blockDim.x];
-    }
-    for (; i < n; i += blockDim.x) s0 += x[i];
-    double s = (s0 + s1) + (s2 + s3);
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
-        if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *out = acc ? *out + red[0] : red[0];
-}
-void sum_f64(const double* x, long n, double* out, int accumulate, cudaStream_t s) {
-    k_sum_f64<<<1, 1024, 0, s>>>(x, n, out, accumulate);
-    MB_LAUNCH();
-}
-
 __global__ void k_check_finite(const double* x, int n, int* err, int code) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && !isfinite(x[i])) atomicExch(err, code);
@@ -522,35 +369,10 @@ void check_finite_f64(const double* x, int n, int* err, int code, cudaStream_t s
     MB_LAUNCH();
 }
 
-__global__ void k_reduce_splits(const float* __restrict__ parts, int S, long n, float* out) {
-    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int k = 0;
-    for (; k + 8 <= S; k += 8)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] += parts[(long)(k + u) * n + i];
-    for (; k < S; ++k) a[0] += parts[(long)k * n + i];
-    out[i] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-}
-void reduce_splits(const float* parts, int S, long n, float* out, cudaStream_t s) {
-    k_reduce_splits<<<(int)((n + 255) / 256), 256, 0, s>>>(parts, S, n, out);
-    MB_LAUNCH();
-}
-
-__global__ void k_mul_dtanh(float* g, const float* a, long n) {
-    const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (i < n) g[i] *= 1.f - a[i] * a[i];
-}
-void mul_dtanh(float* g, const float* a, long n, cudaStream_t s) {
-    k_mul_dtanh<<<(int)((n + 255) / 256), 256, 0, s>>>(g, a, n);
-    MB_LAUNCH();
-}
-
 // image-output variants (tcgen05 update path): one block = one 128-row tile;
 // padded rows (rows[q] < 0) get zero loss and zero gradient. Per-tile column
 // sums of the output gradient (bias grads) and of the log-std terms go to
-// psum / psls [tile][16] (deterministic, summed per cluster by tile_segsum);
+// psum / psls [tile][16] (deterministic, summed per cluster by k_segsum_multi);
 // loss_rows[tile] = the tile's loss sum (fp64).
 __device__ __forceinline__ void tile_colsum(const float* g, int width, float* red, float* out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -64,12 +64,10 @@ struct IGemm {
     long psum_ld = 0;
 };
 // out[z*out_gs + j] = sum over row tiles t of group z (goff/128) of psum[t*ld + j]
-void tile_segsum(const float* psum, long ld, int width, const int* goff, int G, float* out, long out_gs,
-                 cudaStream_t s);
 void img_gemm(const IGemm& d, cudaStream_t s);
 // 1-3 independent GEMMs with the same epilogue kind in one persistent launch
 void img_gemm_batch(const IGemm* ds, int n, cudaStream_t s);
-// several tile_segsum jobs (+ the per-tile loss partials) in one launch
+// several per-cluster segment-sum jobs (+ the per-tile loss partials) in one launch
 struct SegJob {
     const float* psum = nullptr;
     long ld = 0;
@@ -108,11 +106,6 @@ struct MbGather {
 };
 void gather_minibatch(const MbGather& a, cudaStream_t s);
 void gather_img(const int* rows, int Bp, const float* src, int width, const Img& dst, cudaStream_t s);
-void gather_pad(const int* rows, int Bp, const float* src, int width, float* dst, cudaStream_t s);
-void img_segcolsum(const Img& x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg, long c0,
-                   cudaStream_t s);
-void segcolsum_f32(const float* x, int width, const int* goff, int G, float* out, long out_gs, const Img& gimg,
-                   long c0, cudaStream_t s);
 // per-row loss heads writing the output-layer gradient into an image
 // psum / psls: per-128-row-tile column sums [Bp/128][16] of the output
 // gradient (bias grads) and of the log-std gradient terms
@@ -245,21 +238,8 @@ void scalarize(int N, int T, int m, const float* adv, const float* cluster_w, in
                const double* mean, const double* inv_std, float* sadv, cudaStream_t s);
 
 // ---------------------------------------------------------------- PPO (K5)
-void gather_rows(const int* rows, int B, const float* src, int width, float* dst, cudaStream_t s);
-void actor_rows(int B, int ad, const int* row_group, const float* theta, long P, long mlp_n,
-                const float* mu, const float* z, const float* lp_old, const float* sadv,
-                float clip, float ent, float inv_B, float* g_mu, float* lsg, double* loss_rows,
-                int* err, cudaStream_t s);
-void critic_rows(int B, int m, const float* v, const float* tgt, float inv_B, float* g_out,
-                 double* loss_rows, cudaStream_t s);
 // out[z*out_bz + j] (+)= sum_{rows in group z} x[row*width + j]
-void segmented_colsum(const float* x, int width, const int* goff, int G, float* out, long out_bz,
-                      int accumulate, cudaStream_t s);
-void colsum_rows(const float* x, int rows, long width, long ld, float* out, cudaStream_t s);
-void sum_f64(const double* x, long n, double* out, int accumulate, cudaStream_t s);
-void fill_row_group(const int* goff, int G, int* row_group, int B, cudaStream_t s);
 void check_finite_f64(const double* x, int n, int* err, int code, cudaStream_t s);
-void reduce_splits(const float* parts, int S, long n, float* out, cudaStream_t s);
 
 // hypernetwork feature map (feature.cu): fused tanh MLP over the cluster rows
 constexpr int kMaxFeatLayers = 8;
@@ -272,11 +252,7 @@ struct FeatDims {
 };
 // act[1..L] for all G rows of the cluster weights w [G][m]; fimg (bf16 image
 // of f) gets rows [r0, r0 + rn) as image rows 0..rn-1
-void feature_forward(const FeatDims& fd, const float* p, const float* w, int G, const Img& fimg, int r0, int rn,
-                     cudaStream_t s);
 // df = sum of the split-K partials [splits][G][F]; writes dW/db of every layer into gout (flat layout)
-void feature_backward(const FeatDims& fd, const float* p, const float* w, const float* parts, int splits, int G,
-                      float* gout, cudaStream_t s);
 // the same for up to two feature maps of equal depth in lockstep (one launch per layer)
 struct FeatJob {
     const FeatDims* fd;
@@ -293,7 +269,6 @@ void feature_forward_multi(const FeatJob* jobs, int nj, cudaStream_t s);
 // stage 0: df split-K sum * tanh' (gz of the last layer) and the dense
 // backward; 1: the first part only; 2: the dense backward only
 void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s, int stage = 0);
-void mul_dtanh(float* g, const float* a, long n, cudaStream_t s);
 
 // ---------------------------------------------------------------- Adam (K7)
 void adam(long n, float* p, const float* g, float* m1, float* m2, float lr, float bc1, float bc2,

@@ -134,7 +134,7 @@ int Profiler::begin(const char* name, double flops, double bytes, cudaStream_t s
         MB_CUDA(cudaEventCreate(&e));
         pool.push_back(e);
     }
-    Pending p{c, pool[used], pool[used + 1]};
+    Pending p{c, pool[used], pool[used + 1], s};
     used += 2;
     MB_CUDA(cudaEventRecord(p.a, s));
     pending.push_back(p);
@@ -144,11 +144,22 @@ void Profiler::end(int h, cudaStream_t s) {
     if (h >= 0) MB_CUDA(cudaEventRecord(pending[h].b, s));
 }
 void Profiler::collect() {
+    if (!pending.empty()) timeline.clear();
     for (auto& p : pending) {
         MB_CUDA(cudaEventSynchronize(p.b));
         float ms = 0;
         MB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
         cls[p.c].ms += ms;
+        float t0 = 0;
+        MB_CUDA(cudaEventElapsedTime(&t0, pending[0].a, p.a));
+        int sid = -1;
+        for (size_t i = 0; i < streams.size(); ++i)
+            if (streams[i] == p.s) sid = (int)i;
+        if (sid < 0) {
+            streams.push_back(p.s);
+            sid = (int)streams.size() - 1;
+        }
+        timeline.push_back(Span{p.c, sid, t0, t0 + ms});
     }
     pending.clear();
     used = 0;
@@ -172,15 +183,6 @@ struct ProfScope {
         if (g_prof) g_prof->end(h, s);
     }
 };
-static double gemm_flops(const GemmDesc& d) {
-    if (d.gmode == 1) return 2.0 * d.M * d.N * d.K;        // M = total grouped rows
-    if (d.gmode == 2) return 2.0 * d.M * d.N * d.K;        // K = total grouped rows
-    return 2.0 * d.M * d.N * d.K * d.Z;
-}
-static void gemm(const char* cls, const GemmDesc& d, cudaStream_t s) {  // tiny feature-map GEMMs
-    ProfScope p(cls, gemm_flops(d), 0, s);
-    gemm_simt(d, s);
-}
 
 // ------------------------------------------------------------------ HyperNet
 void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vector<int>& ts, bool out_tanh,
@@ -1271,37 +1273,6 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
         critic_.adam_step(cfg_.critic_lr, d_err, s_);
         MB_CUDA(cudaEventRecord(ev_cfin_, s_));
-        return;
-    }
-    static const bool decouple = [] {  // MORLAX_DECOUPLE=1: A/B of per-chain finiteness checks
-        const char* e = std::getenv("MORLAX_DECOUPLE");
-        return e && e[0] == '1';
-    }();
-    if (decouple) {
-        // each chain checks its own loss and applies its Adam without waiting
-        // for the other chain; a non-finite loss of either sets the shared
-        // error flag, every later Adam of the iteration is skipped and the
-        // iteration raises NumericError (train() then keeps the last healthy
-        // parameters, as the reference's train() does)
-        critic_.forward(d_cw, g_lo_, Kl_, sc);
-        MB_CUDA(cudaStreamWaitEvent(sc, ev_gather_, 0));
-        net_step(&both[1], &roles[1], 1, Bp, inv_B, maxg, rows, goff, slot, sc);
-        MB_CUDA(cudaEventRecord(ev_cd_[mb_par_], sc));
-        HyperNet::backward_multi(&both[1], 1, sc, 1);
-        if (comm2_) comm_allreduce_f64(comm2_, d_mbloss + slot * 2 + 1, 1, sc);
-        check_finite_f64(d_mbloss + slot * 2 + 1, 1, d_err, 3, sc);
-        HyperNet::backward_multi(&both[1], 1, sc, 2);
-        critic_.adam_step(cfg_.critic_lr, d_err, sc);
-        MB_CUDA(cudaEventRecord(ev_cfin_, sc));
-        actor_.forward(d_cw, g_lo_, Kl_, s_);
-        MB_CUDA(cudaStreamWaitEvent(s_, ev_gather_, 0));
-        net_step(&both[0], &roles[0], 1, Bp, inv_B, maxg, rows, goff, slot, s_);
-        MB_CUDA(cudaEventRecord(ev_ad_[mb_par_], s_));
-        HyperNet::backward_multi(&both[0], 1, s_, 1);
-        if (comm_) comm_allreduce_f64(comm_, d_mbloss + slot * 2, 1, s_);
-        check_finite_f64(d_mbloss + slot * 2, 1, d_err, 3, s_);
-        HyperNet::backward_multi(&both[0], 1, s_, 2);
-        actor_.adam_step(cfg_.actor_lr, d_err, s_);
         return;
     }
     // the forwards (feature map, theta, weight packing) need no minibatch rows

@@ -32,9 +32,14 @@ struct Profiler {
     std::string phase = "iteration";  // class key prefix: the phase being enqueued
     std::vector<Cls> cls;
     std::vector<cudaEvent_t> pool;
-    struct Pending { int c; cudaEvent_t a, b; };
+    struct Pending { int c; cudaEvent_t a, b; cudaStream_t s; };
     std::vector<Pending> pending;
     size_t used = 0;
+    // per-launch timeline of the last collect(): class, stream, start / end
+    // (ms from the first recorded launch)
+    struct Span { int c; int stream; double t0, t1; };
+    std::vector<Span> timeline;
+    std::vector<cudaStream_t> streams;
     int begin(const char* name, double flops, double bytes, cudaStream_t s);
     void end(int h, cudaStream_t s);
     void collect();  // synchronises the recorded events
