@@ -9,7 +9,12 @@ col = {h: i for i, h in enumerate(hdr)}
 M = [("time_us", "gpu__time_duration.sum"),
      ("dram_rd_MB", "dram__bytes_read.sum"),
      ("dram_wr_MB", "dram__bytes_write.sum"),
-     ("tensor_pct", "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+     # tcgen05-aware: tensor-memory (TMEM) activity of the UTC (tcgen05) pipe, and
+     # the tcgen05.mma instruction count; the legacy pipe_tensor counter only sees
+     # mma.sync (HMMA) and reads ~1-5 % for tcgen05 kernels
+     ("tcgen05_tmem_pct", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+     ("utcmma_inst", "smsp__sass_inst_executed_op_utcmma.sum"),
+     ("hmma_pct", "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
      ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
      ("sm_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
      ("regs", "launch__registers_per_thread"),
