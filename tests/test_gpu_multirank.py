@@ -93,6 +93,23 @@ def test_sharded_ranks_match_single_gpu_bit_exact(mb, F, W):
             assert abs(st.critic_loss - ref_st[it].critic_loss) <= 1e-6 * max(1.0, abs(ref_st[it].critic_loss))
 
 
+def test_eight_ranks_with_k_chunked_optimizer(mb):
+    """W = 8 ranks, 256 clusters (more than one 128-cluster K chunk of the
+    fused dM + Adam: the K-chunked walker on every rank's M-row shard),
+    mo-humanoid6 (obs 45, act 12, m 6): bit-exact against one GPU."""
+    cfg = _cfg(mb, 64, env="mo-humanoid6", N=512, K=256, T=4, epochs=1, minibatch_count=2, feature_hidden=[32],
+               actor_hidden=[64, 64], critic_hidden=[64, 64])
+    ref = mb.Trainer(cfg)
+    ref.iteration(0)
+    res = _sharded(mb, cfg, 8, 1)
+    for r in range(8):
+        _, _, pa, pc = res[r]
+        assert np.array_equal(pa, ref.params("actor")), f"rank {r} actor params"
+        assert np.array_equal(pc, ref.params("critic")), f"rank {r} critic params"
+    got = np.concatenate([r[1]["scalar_advantage"] for r in res])
+    assert np.array_equal(got, ref.get("scalar_advantage"))
+
+
 def test_single_rank_loopback_is_the_single_gpu_path(mb):
     """W = 1 with a communicator runs every sharded code path (exchanges are
     self-copies) and must equal the no-communicator trainer bit for bit."""
