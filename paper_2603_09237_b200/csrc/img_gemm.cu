@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
     const TileInfo ti = tile_info(d, t - bt.base[bk_], bt.ntn[bk_], bt.ntm[bk_])
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- producer
+        {  // ---------------- producer (converged warp; one elected lane issues)
             long g = 0;  // global chunk counter
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 MB_TILE(t);
@@ -145,20 +145,23 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                     const int s = (int)(g % C::STAGES);
                     umma::mbar_wait(&empty[s], (uint32_t)(((g / C::STAGES) & 1) ^ 1));
                     uint8_t* st = smem + s * C::STAGE;
-                    umma::mbar_arrive_expect_tx(&full[s], CHUNK + nbv * bbytes);
-                    umma::bulk_g2s(st, Ab + chunk_index(d.a_view, mt, kc0 + kc, CTa) * CHUNK, CHUNK, &full[s]);
+                    if (umma::elect_one()) {
+                        umma::mbar_arrive_expect_tx(&full[s], CHUNK + nbv * bbytes);
+                        umma::bulk_g2s(st, Ab + chunk_index(d.a_view, mt, kc0 + kc, CTa) * CHUNK, CHUNK, &full[s]);
 #pragma unroll
-                    for (int j = 0; j < C::NB; ++j)
-                        if (j < nbv)
-                            umma::bulk_g2s(st + CHUNK * (1 + j),
-                                           Bb + chunk_index(d.b_view, nt0 + j, kc0 + kc, CTb) * CHUNK, bbytes,
-                                           &full[s]);
+                        for (int j = 0; j < C::NB; ++j)
+                            if (j < nbv)
+                                umma::bulk_g2s(st + CHUNK * (1 + j),
+                                               Bb + chunk_index(d.b_view, nt0 + j, kc0 + kc, CTb) * CHUNK, bbytes,
+                                               &full[s]);
+                    }
+                    __syncwarp();
                 }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
+        {  // ---------------- MMA issuer (converged warp; one elected lane issues)
             long g = 0;
             int it = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -174,24 +177,31 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 umma::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
                 umma::fence_after_sync();
                 const uint32_t dcol = tbase + (uint32_t)(acc * C::ACC);
+                // descriptors of stage 0's A and first B chunk; a stage / chunk / K step
+                // only moves the start address (+bytes >> 4 in the low field)
+                const uint64_t a_desc0 = umma::smem_desc(umma::smem_u32(smem), a_lbo, a_sbo);
+                const uint64_t b_desc0 = umma::smem_desc(umma::smem_u32(smem) + CHUNK, b_lbo, b_sbo);
                 for (int kc = 0; kc < ti.nk; ++kc, ++g) {
                     const int s = (int)(g % C::STAGES);
                     umma::mbar_wait(&full[s], (uint32_t)((g / C::STAGES) & 1));
                     umma::fence_after_sync();
-                    const uint32_t a0 = umma::smem_u32(smem + s * C::STAGE);
+                    if (umma::elect_one()) {
+                        const uint64_t ad = a_desc0 + (uint64_t)((s * C::STAGE) >> 4);
 #pragma unroll
-                    for (int j = 0; j < C::NB; ++j) {
-                        if (j >= nbv) break;
-                        const uint32_t b0 = a0 + CHUNK * (1 + j);
+                        for (int j = 0; j < C::NB; ++j) {
+                            if (j >= nbv) break;
+                            const uint64_t bd = b_desc0 + (uint64_t)((s * C::STAGE + j * CHUNK) >> 4);
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)
-                            umma::mma_bf16(dcol + j * 128, umma::smem_desc(a0 + kk * a_step, a_lbo, a_sbo),
-                                           umma::smem_desc(b0 + kk * b_step, b_lbo, b_sbo), idesc,
-                                           (kc | kk) ? 1u : 0u);
+                            for (int kk = 0; kk < 8; ++kk)
+                                umma::mma_bf16(dcol + j * 128, ad + (uint64_t)(kk * (a_step >> 4)),
+                                               bd + (uint64_t)(kk * (b_step >> 4)), idesc, (kc | kk) ? 1u : 0u);
+                        }
+                        umma::commit(&empty[s]);
                     }
-                    umma::commit(&empty[s]);
+                    __syncwarp();
                 }
-                umma::commit(&tfull[acc]);
+                if (umma::elect_one()) umma::commit(&tfull[acc]);
+                __syncwarp();
                 ++it;
             }
         }

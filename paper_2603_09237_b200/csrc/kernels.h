@@ -200,11 +200,15 @@ struct RolloutArgs {
 };
 
 // tensor-core rollout (rollout_tc.cu): per-cluster weights packed as bf16
-// UMMA images, streamed per step by the bulk-copy engine
+// UMMA images, streamed per step by the bulk-copy engine. A chunk is one
+// bulk copy: rows [128 tile, +128) (16 for the output layer) x K columns
+// [k0, k0 + kw) of layer `layer`, K-major core matrices with SBO = kw * 16.
+constexpr int ROLL_MAX_CHUNKS = 48;
 struct NetPlan {
-    int nchunks, blob_bytes;
+    int nchunks, blob_bytes, max_chunk;
     int kin_pad[8], tiles[8];
-    int chunk_off[24], chunk_bytes[24], chunk_layer[24], chunk_tile[24];
+    int chunk_off[ROLL_MAX_CHUNKS], chunk_bytes[ROLL_MAX_CHUNKS], chunk_layer[ROLL_MAX_CHUNKS],
+        chunk_tile[ROLL_MAX_CHUNKS], chunk_k0[ROLL_MAX_CHUNKS], chunk_kw[ROLL_MAX_CHUNKS];
 };
 NetPlan make_plan(const NetDims& nd);
 void pack_theta(const float* theta, long ld, int G, const NetDims& nd, const NetPlan& pl, uint8_t* blob, cudaStream_t s);
@@ -213,7 +217,8 @@ struct RolloutTcArgs : RolloutArgs {
     const uint8_t* pol_blob;  // [K][pol_plan.blob_bytes]
     const uint8_t* cri_blob;
     const float* eps;         // [T][N][ad] the rollout's N(0,1) draws (rollout_noise)
-    int slot_bytes, xb_bytes, hb_bytes, nepad;  // filled by rollout_tc
+    // filled by rollout_tc: ring slot size and slots per net, operand buffer sizes, padded env count
+    int slot_bytes, pol_slots, cri_slots, xb_bytes, hb_bytes, nepad;
 };
 void rollout_tc(RolloutTcArgs a, cudaStream_t s);
 // the N(0,1) draws of a whole rollout, ahead of it and in parallel:

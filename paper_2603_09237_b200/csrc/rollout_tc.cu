@@ -5,17 +5,27 @@
 //   all T steps; env state stays in shared memory.
 // * The cluster's generated weights theta_c (fp32, from the hypernet GEMM)
 //   are packed once per iteration by k_pack_theta into bf16 "blobs" already
-//   in the UMMA K-major core-matrix image, one contiguous chunk per
-//   128-feature tile of each hidden layer plus one chunk for the output
-//   layer. Every step the CTA streams its chunks L2 -> SMEM with the TMA
-//   bulk-copy engine (cp.async.bulk, mbarrier complete_tx) through a 2-slot
-//   ring, two chunks ahead of the MMA.
+//   in the UMMA K-major core-matrix image, one contiguous <= 16 KB chunk per
+//   (128-feature tile, 64-wide K piece) of each hidden layer plus one chunk
+//   for the output layer. Every step the CTA streams its chunks L2 -> SMEM
+//   with the TMA bulk-copy engine (cp.async.bulk, mbarrier complete_tx).
 // * Hidden layers: D[feature][env] = W_l (A, K-major) x act^T (B, MN-major),
 //   M = 128 features per tile, N = envs; the epilogue (tcgen05.ld) adds the
-//   fp32 bias, applies tanh and writes the next layer's bf16 operand.
+//   fp32 bias, applies tanh and writes the next layer's bf16 operand, in
+//   place (the layer's MMAs have consumed their input when it runs).
 // * Output layer: D[env][out] = act (A, MN-major, M = 64 envs) x W_out^T
-//   (B, K-major, N = 16), so each env-owning thread gets its own outputs
-//   and goes straight on to sampling / the env step.
+//   (B, K-major, N = 16), so each env-owning thread gets its own outputs.
+// * Warp-specialised, two independent chains per CTA:
+//     warps 0-3  policy group: policy epilogues, Gaussian sample, log-prob,
+//                env step, auto-reset, operand writes (the critical path);
+//     warps 4-7  critic group: critic epilogues, value / next value;
+//     warp 8 / 9   policy bulk-copy producer / policy MMA issuer;
+//     warp 10 / 11 critic bulk-copy producer / critic MMA issuer.
+//   Each net has its own weight ring and TMEM columns, so the critic at the
+//   final observation of step t runs while the policy chain goes on to step
+//   t + 1 (both depend only on the env step), and weights of the next pass
+//   stream in while the current one computes. All hand-offs are mbarriers
+//   (parity-tracked; every buffer a chain reuses is released explicitly).
 // * The N(0,1) draws do not depend on the policy: k_rollout_noise computes
 //   all T steps' fp64 Box-Muller draws ahead at full occupancy (bit-identical
 //   words, rounded to fp32 exactly where the sequential sampler rounds), and
@@ -32,25 +42,62 @@
 namespace mb200 {
 
 namespace {
-constexpr int RNT = 256;  // threads
-constexpr int RE = 64;    // instances per CTA
-constexpr int OUT_COL = 128;
+constexpr int RE = 64;           // instances per CTA
+constexpr int GROUP = 128;       // threads per epilogue warp group
+constexpr int RNT = 3 * GROUP;   // policy group, critic group, 4 issue warps
+constexpr int MAX_SLOTS = 4;     // weight-ring slots per net
+constexpr int SLOT_MAX = 16384;  // bytes per ring slot (largest chunk)
+constexpr uint32_t POL_COL = 0, CRI_COL = 256, OUT_OFF = 128;  // TMEM columns (512 allocated)
+constexpr int BAR_POL = 1, BAR_CRI = 2;                        // named barriers of the two groups
 
-#ifdef MB_ROLL_PROF  // phase timing of CTA 0 (debug builds only: NVCC="nvcc -DMB_ROLL_PROF")
+#ifdef MB_ROLL_PROF  // phase timing in CTA 0 (debug builds only: NVCC="nvcc -DMB_ROLL_PROF")
+__shared__ unsigned long long g_rp[4][16], g_rp_last[4];  // (CTA 0 prints them)
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define RPROF(k)                                            \
-    if (blockIdx.x == 0 && threadIdx.x == 0) {              \
-        const unsigned long long now_ = gtimer();           \
-        prof_[k] += now_ - prof_last_;                      \
-        prof_last_ = now_;                                  \
+// thread slot j: 0 policy group thread 0, 2 critic group thread 0
+__device__ __forceinline__ int rprof_slot() {
+    if (blockIdx.x != 0) return -1;
+    return threadIdx.x == 0 ? 0 : threadIdx.x == 128 ? 2 : -1;
+}
+#define RPROF(k)                                          \
+    {                                                     \
+        const int j_ = rprof_slot();                      \
+        if (j_ >= 0) {                                    \
+            const unsigned long long now_ = gtimer();     \
+            if (g_rp_last[j_]) g_rp[j_][k] += now_ - g_rp_last[j_]; \
+            g_rp_last[j_] = now_;                         \
+        }                                                 \
     }
 #else
 #define RPROF(k)
 #endif
+
+struct Bars {
+    uint64_t pfull[MAX_SLOTS], pempty[MAX_SLOTS], cfull[MAX_SLOTS], cempty[MAX_SLOTS];
+    uint64_t pacc, cacc;               // MMA issuer -> group: a layer's accumulators are complete
+    uint64_t php, chp;                 // group -> MMA issuer: a layer's epilogue wrote the next operand
+    uint64_t xp_ready[2], xp_free[2];  // observation operand of step t (buffer t & 1)
+    uint64_t xc_ready, xc_free;        // final-observation operand
+    uint64_t vf_ready[2];              // NEED / VF of step s (s & 1) published
+    uint64_t cdone[2];                 // critic group done reading NEED / VF of step s
+};
+
+struct Ring {
+    uint8_t* base;
+    uint64_t* full;
+    uint64_t* empty;
+    int nslots, slot_bytes;
+    int slot, round;  // position of the issuing thread
+    __device__ __forceinline__ void advance() {
+        if (++slot == nslots) {
+            slot = 0;
+            ++round;
+        }
+    }
+};
 
 __device__ __forceinline__ float sech2(float z) {
     const float e = __expf(-2.f * fabsf(z));
@@ -58,128 +105,152 @@ __device__ __forceinline__ float sech2(float z) {
     return 4.f * e / (d * d);
 }
 
-struct Ctx {
-    uint8_t* ring0;  // 2 weight slots: ring0 + slot * ring_stride (no indexed pointer array: registers)
-    int ring_stride;
-    uint8_t* xb;     // layer-0 operand (MN-major, env x obs_pad)
-    uint8_t* hb0;  // 2 hidden-activation buffers (MN-major, env x hpad): hb0 + i * hb_stride
-    int hb_stride;
-    uint64_t* fullb;
-    uint64_t* mmad;
-    uint32_t tbase;
-    int nepad;
-    // issue state (thread 0 only)
-    long issued;  // chunks issued so far
-    long consumed;
-};
+__device__ __forceinline__ void wait_phase(uint64_t* b, int n) { umma::mbar_wait(b, (uint32_t)(n & 1)); }
 
-__device__ __forceinline__ void chunk_at(const RolloutTcArgs& a, int vflag, int pos, int* net, int* c) {
-    if (pos < a.pol_plan.nchunks) { *net = 0; *c = pos; return; }
-    pos -= a.pol_plan.nchunks;
-    *net = 1;
-    *c = vflag ? (pos % a.cri_plan.nchunks) : pos;
-}
-__device__ __forceinline__ int step_len(const RolloutTcArgs& a, int vflag) {
-    return a.pol_plan.nchunks + (vflag ? 2 : 1) * a.cri_plan.nchunks;
-}
-
-// thread 0: issue the bulk copy of the J-th chunk of the CTA's sequence.
-// The sequence position is tracked by (step, pos); vflag of the issuing
-// step is known because the issuer runs at most 2 chunks ahead and every
-// step starts with >= 2 policy chunks.
-struct Issuer {
-    int step, pos;
-};
-
-__device__ __forceinline__ void issue_next(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* vflags, int group) {
-    if (is.step >= a.T) return;
-    int net, c;
-    chunk_at(a, vflags[is.step & 1], is.pos, &net, &c);
-    const NetPlan& pl = net ? a.cri_plan : a.pol_plan;
-    const uint8_t* src = (net ? a.cri_blob : a.pol_blob) + (long)group * pl.blob_bytes + pl.chunk_off[c];
-    const int slot = (int)(x.issued & 1);
-    umma::mbar_arrive_expect_tx(&x.fullb[slot], (uint32_t)pl.chunk_bytes[c]);
-    umma::bulk_g2s(x.ring0 + slot * x.ring_stride, src, (uint32_t)pl.chunk_bytes[c], &x.fullb[slot]);
-    x.issued++;
-    if (++is.pos >= step_len(a, vflags[is.step & 1])) {
-        is.pos = 0;
-        is.step++;
+// producer warp (converged; one elected lane issues): the bulk copies of
+// one pass of a net, in chunk order
+__device__ __forceinline__ void produce_pass(const NetPlan& pl, const uint8_t* blob, Ring& r) {
+    for (int c = 0; c < pl.nchunks; ++c) {
+        if (r.round > 0) wait_phase(&r.empty[r.slot], r.round - 1);  // the MMAs of the slot's last chunk are done
+        if (umma::elect_one()) {
+            umma::mbar_arrive_expect_tx(&r.full[r.slot], (uint32_t)pl.chunk_bytes[c]);
+            umma::bulk_g2s(r.base + r.slot * r.slot_bytes, blob + pl.chunk_off[c], (uint32_t)pl.chunk_bytes[c],
+                           &r.full[r.slot]);
+        }
+        __syncwarp();
+        r.advance();
     }
 }
 
-// Run one net (all chunks) on the layer-0 operand xb. Result: output layer
-// accumulators in TMEM columns [OUT_COL, OUT_COL+16) (M = 64 env layout).
-__device__ __forceinline__ void run_net(const RolloutTcArgs& a, Ctx& x, Issuer& is, const int* vflags, int group, int net,
-                        const float* theta) {
-    const NetPlan& pl = net ? a.cri_plan : a.pol_plan;
-    const NetDims& nd = net ? a.cri : a.pol;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// MMA warp (converged; one elected lane issues): one pass of a net on the
+// operand at smem address `in0`. Layer l > 0 waits for the group's epilogue
+// of layer l - 1 (`hready`); each layer ends with a commit to `acc`; the
+// layer-0 MMAs also release the input operand through `xfree` (when given).
+// Descriptors are built once per chunk and advanced by 256 B (+16 in the
+// address field) per K = 16 step.
+__device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint32_t tbase, uint32_t in0,
+                                         uint32_t hb0, int nepad, uint64_t* acc, uint64_t* hready, int& hph,
+                                         uint64_t* xfree) {
     int c = 0;
-    int cur = -1;  // -1: input is xb, else hb[cur]
-    for (int l = 0; l < nd.L; ++l) {
-        const bool last = (l == nd.L - 1);
-        const int kin = pl.kin_pad[l];
-        const uint32_t sbo = (uint32_t)kin * 16;  // 8-row block stride of every operand of this layer
-        const uint8_t* inb = cur < 0 ? x.xb : x.hb0 + cur * x.hb_stride;
-        const int ntiles = last ? 1 : pl.tiles[l];
-        for (int t = 0; t < ntiles; ++t, ++c) {
-            if (threadIdx.x == 0) {
-                const int slot = (int)(x.consumed & 1);
-                umma::mbar_wait(&x.fullb[slot], (uint32_t)((x.consumed >> 1) & 1));
-                umma::fence_after_sync();
-                const uint32_t w0 = umma::smem_u32(x.ring0 + slot * x.ring_stride), i0 = umma::smem_u32(inb);
-                if (!last) {
-                    const uint32_t idesc = umma::idesc_bf16(128, x.nepad, false, true);
-                    for (int k = 0; k < kin / 16; ++k)
-                        umma::mma_bf16(x.tbase + (uint32_t)(t * x.nepad), umma::smem_desc(w0 + k * 256, 128, sbo),
-                                       umma::smem_desc(i0 + k * 256, 128, sbo), idesc, k ? 1u : 0u);
-                } else {
-                    const uint32_t idesc = umma::idesc_bf16(64, 16, true, false);
-                    for (int k = 0; k < kin / 16; ++k)
-                        umma::mma_bf16(x.tbase + OUT_COL, umma::smem_desc(i0 + k * 256, 128, sbo),
-                                       umma::smem_desc(w0 + k * 256, 128, sbo), idesc, k ? 1u : 0u);
-                }
-                umma::commit(x.mmad);
-                umma::mbar_wait(x.mmad, (uint32_t)(x.consumed & 1));
-                x.consumed++;
-                issue_next(a, x, is, vflags, group);  // slot is free again
-            }
+    for (int l = 0; l < L; ++l) {
+        if (l > 0) {
+            wait_phase(hready, hph++);
+            umma::fence_after_sync();
         }
-        __syncthreads();
-        umma::fence_after_sync();
-        if (!last) {  // epilogue: bias + tanh -> next operand (MN-major, env x hpad)
-            const int nxt = cur < 0 ? 0 : (cur ^ 1);
-            uint8_t* ob = x.hb0 + nxt * x.hb_stride;
-            const uint32_t osbo = (uint32_t)pl.kin_pad[l + 1] * 16;
-            const int tile = warp >> 2, lg = warp & 3;
-            const int out = nd.sz[l + 1];
-            if (tile < ntiles && tile * 128 + lg * 32 < out) {
-                const int j = tile * 128 + lg * 32 + lane;
-                const float bj = j < out ? theta[nd.boff[l] + j] : 0.f;
-                for (int n0 = 0; n0 < x.nepad; n0 += 16) {
-                    float v[16];
-                    umma::tmem_ld16(x.tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(tile * x.nepad + n0), v);
-                    if (j < out) {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            uint4 q;
-                            // MUFU tanh (rel err < 2^-10.99): below the bf16 rounding of the operand
-                            q.x = umma::pack_bf16(umma::tanh_approx(v[8 * h + 0] + bj), umma::tanh_approx(v[8 * h + 1] + bj));
-                            q.y = umma::pack_bf16(umma::tanh_approx(v[8 * h + 2] + bj), umma::tanh_approx(v[8 * h + 3] + bj));
-                            q.z = umma::pack_bf16(umma::tanh_approx(v[8 * h + 4] + bj), umma::tanh_approx(v[8 * h + 5] + bj));
-                            q.w = umma::pack_bf16(umma::tanh_approx(v[8 * h + 6] + bj), umma::tanh_approx(v[8 * h + 7] + bj));
-                            const int nb = (n0 >> 3) + h;
-                            *reinterpret_cast<uint4*>(ob + nb * osbo + (j >> 3) * 128 + (j & 7) * 16) = q;
-                        }
-                    }
+        const bool last = l == L - 1;
+        // input operand at K = 0; its 8-env block stride is this layer's padded K
+        const uint64_t in_desc = umma::smem_desc(l == 0 ? in0 : hb0, 128, (uint32_t)pl.kin_pad[l] * 16);
+        const uint32_t idesc =
+            last ? umma::idesc_bf16(64, 16, true, false) : umma::idesc_bf16(128, nepad, false, true);
+        for (; c < pl.nchunks && pl.chunk_layer[c] == l; ++c) {
+            wait_phase(&r.full[r.slot], r.round);
+            umma::fence_after_sync();
+            const int kw = pl.chunk_kw[c], k0 = pl.chunk_k0[c];
+            const uint64_t w_desc =
+                umma::smem_desc(umma::smem_u32(r.base + r.slot * r.slot_bytes), 128, (uint32_t)kw * 16);
+            const uint64_t x_desc = in_desc + (uint64_t)k0;  // (k0 / 16) steps of 16
+            const int nk = kw / 16;
+            if (umma::elect_one()) {
+                if (!last) {
+                    const uint32_t d = tbase + (uint32_t)(pl.chunk_tile[c] * nepad);
+#pragma unroll 4
+                    for (int kk = 0; kk < nk; ++kk)
+                        umma::mma_bf16(d, w_desc + 16 * kk, x_desc + 16 * kk, idesc, (k0 | kk) ? 1u : 0u);
+                } else {
+#pragma unroll 4
+                    for (int kk = 0; kk < nk; ++kk)
+                        umma::mma_bf16(tbase + OUT_OFF, x_desc + 16 * kk, w_desc + 16 * kk, idesc,
+                                       (k0 | kk) ? 1u : 0u);
                 }
+                umma::commit(&r.empty[r.slot]);
             }
-            umma::fence_before_sync();
-            umma::fence_proxy_async();
-            __syncthreads();
-            cur = nxt;
+            __syncwarp();
+            r.advance();
+        }
+        if (umma::elect_one()) {
+            if (l == 0 && xfree) umma::commit(xfree);
+            umma::commit(acc);
+        }
+        __syncwarp();
+    }
+}
+
+// group epilogue of hidden layer l: bias + tanh -> the next layer's bf16
+// operand (MN-major, env x kin_pad(l+1)); zeros in the padded features
+__device__ __forceinline__ void hidden_epi(const NetPlan& pl, const NetDims& nd, int l, const float* theta,
+                                           uint8_t* hb, uint32_t tacc, int nepad, int gw, int lane) {
+    const uint32_t osbo = (uint32_t)pl.kin_pad[l + 1] * 16;
+    const int out = nd.sz[l + 1];
+    for (int tile = 0; tile < pl.tiles[l]; ++tile) {
+        const int j = tile * 128 + gw * 32 + lane;
+        const bool live = j < out;
+        const float bj = live ? theta[nd.boff[l] + j] : 0.f;
+        const uint32_t ta = tacc + ((uint32_t)(gw * 32) << 16) + (uint32_t)(tile * nepad);
+        uint8_t* ob = hb + (j >> 3) * 128 + (j & 7) * 16;
+        for (int n0 = 0; n0 < nepad; n0 += 32) {
+            uint32_t v[32];
+            const bool two = n0 + 16 < nepad;  // warp-uniform
+            umma::tmem_ld16_async(ta + n0, v);
+            if (two) umma::tmem_ld16_async(ta + n0 + 16, v + 16);
+            umma::tmem_wait_ld();
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                if (h >= 2 && !two) break;
+                uint4 q = make_uint4(0, 0, 0, 0);
+                if (live) {
+                    // MUFU tanh (rel err < 2^-10.99): below the bf16 rounding of the operand
+                    float f[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) f[e] = umma::tanh_approx(__uint_as_float(v[8 * h + e]) + bj);
+                    q.x = umma::pack_bf16(f[0], f[1]);
+                    q.y = umma::pack_bf16(f[2], f[3]);
+                    q.z = umma::pack_bf16(f[4], f[5]);
+                    q.w = umma::pack_bf16(f[6], f[7]);
+                }
+                *reinterpret_cast<uint4*>(ob + ((n0 >> 3) + h) * osbo) = q;
+            }
         }
     }
+}
+
+// the group's hidden layers of one pass; returns the output layer's 16
+// accumulators of env (gw * 16 + lane) (lanes < 16) in v
+__device__ __forceinline__ void group_pass(const NetPlan& pl, const NetDims& nd, const float* theta, uint8_t* hb,
+                                           uint32_t tacc, int nepad, uint64_t* acc, int& aph, uint64_t* hready,
+                                           int gw, int lane, float* v) {
+    for (int l = 0; l + 1 < nd.L; ++l) {
+        RPROF(5);
+        wait_phase(acc, aph++);
+        RPROF(6);
+        umma::fence_after_sync();
+        hidden_epi(pl, nd, l, theta, hb, tacc, nepad, gw, lane);
+        umma::fence_proxy_async();  // generic-proxy operand writes -> the MMA's async proxy
+        umma::fence_before_sync();
+        umma::mbar_arrive(hready);
+    }
+    RPROF(5);
+    wait_phase(acc, aph++);
+    RPROF(6);
+    umma::fence_after_sync();
+    uint32_t r[16];
+    umma::tmem_ld16_async(tacc + OUT_OFF + ((uint32_t)(gw * 32) << 16), r);
+    umma::tmem_wait_ld();
+    umma::fence_before_sync();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// observation of the instances (state in S) -> bf16 MN-major operand xb (and
+// optionally the batch's obs rows), 2 threads per instance
+__device__ __forceinline__ void write_operand(const float* S, int nr, int od, uint8_t* xb, uint32_t xsbo,
+                                              float* obs_out, long T, long t, long i0, int gtid) {
+    for (int r = gtid >> 1; r < nr; r += GROUP / 2)
+        for (int k = gtid & 1; k < od; k += 2) {
+            const float v = S[k * RE + r];
+            if (obs_out) obs_out[((i0 + r) * T + t) * od + k] = v;
+            *reinterpret_cast<__nv_bfloat16*>(xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2) =
+                __float2bfloat16_rn(v);
+        }
 }
 
 __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ RolloutTcArgs a) {
@@ -188,43 +259,50 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
     const int c = blockIdx.x / cpg, ch = blockIdx.x % cpg;
     const int i0 = c * a.reps + ch * RE;
     const int nr = min(RE, a.reps - ch * RE);
-    const int od = a.od, ad = a.ad, m = a.m, sd = a.sdim;
-    const int tid = threadIdx.x;
+    const int od = a.od, ad = a.ad, m = a.m, sd = a.sdim, T = a.T, nepad = a.nepad;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // ---- shared memory carve-up (host computes the same total)
-    Ctx x;
     uint8_t* p = smem;
-    x.ring0 = p; x.ring_stride = a.slot_bytes; p += 2 * a.slot_bytes;
-    x.xb = p; p += a.xb_bytes;
-    x.hb0 = p; x.hb_stride = a.hb_bytes; p += 2 * a.hb_bytes;
-    float* S = reinterpret_cast<float*>(p); p += sizeof(float) * sd * RE;      // env state [k][env]
-    float* MU = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 16;     // policy mean
-    float* ZS = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 16;     // pre-tanh sample
-    float* VV = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 8;      // value
-    float* NV = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 8;      // next value
-    float* TRK = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 8;     // running returns
+    uint8_t* pring = p; p += a.pol_slots * a.slot_bytes;
+    uint8_t* cring = p; p += a.cri_slots * a.slot_bytes;
+    uint8_t* xp = p; p += 2 * a.xb_bytes;  // observation operand, by step parity
+    uint8_t* xc = p; p += a.xb_bytes;      // final-observation operand
+    uint8_t* hp = p; p += a.hb_bytes;      // policy hidden activations (in place across layers)
+    uint8_t* hc = p; p += a.hb_bytes;      // critic hidden activations
+    float* S = reinterpret_cast<float*>(p); p += sizeof(float) * sd * RE;  // env state [k][env]
+    float* TRK = reinterpret_cast<float*>(p); p += sizeof(float) * RE * 8;  // running returns
     float* LS = reinterpret_cast<float*>(p); p += sizeof(float) * 16;
     uint64_t* EK = reinterpret_cast<uint64_t*>(p); p += 8 * RE;
     uint64_t* EC = reinterpret_cast<uint64_t*>(p); p += 8 * RE;
     int* STP = reinterpret_cast<int*>(p); p += 4 * RE;
-    int* NEED = reinterpret_cast<int*>(p); p += 4 * RE;
-    int* VF = reinterpret_cast<int*>(p); p += 16;   // vflag of step t (index t & 1)
-    x.fullb = reinterpret_cast<uint64_t*>(p); p += 16;
-    x.mmad = reinterpret_cast<uint64_t*>(p); p += 8;
+    int* NEED = reinterpret_cast<int*>(p); p += 4 * 2 * RE;  // [s & 1][env]: reset before step s
+    int* VF = reinterpret_cast<int*>(p); p += 16;            // [s & 1]: any NEED at step s
+    Bars* B = reinterpret_cast<Bars*>(p); p += sizeof(Bars);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(p);
-    x.nepad = a.nepad;
-    x.issued = x.consumed = 0;
+    // the policy group's sampling scratch lives in its hidden buffer, idle
+    // between the output layer and the next layer-0 epilogue
+    float* MU = reinterpret_cast<float*>(hp);
+    float* ZS = MU + RE * 16;
 
+#ifdef MB_ROLL_PROF
+    if (rprof_slot() >= 0) {
+        for (int k = 0; k < 16; ++k) g_rp[rprof_slot()][k] = 0;
+        g_rp_last[rprof_slot()] = 0;
+    }
+#endif
     const float* th = a.theta + (long)c * a.theta_ld;
     const float* ph = a.phi + (long)c * a.phi_ld;
+    const uint32_t xsbo = (uint32_t)a.pol_plan.kin_pad[0] * 16;
     // zero the operand buffers once: padded K rows / env columns stay zero
-    for (int e = tid; e < (a.xb_bytes + 2 * a.hb_bytes) / 16; e += RNT)
-        reinterpret_cast<uint4*>(x.xb)[e] = make_uint4(0, 0, 0, 0);
+    for (int e = tid; e < (3 * a.xb_bytes + 2 * a.hb_bytes) / 16; e += RNT)
+        reinterpret_cast<uint4*>(xp)[e] = make_uint4(0, 0, 0, 0);
     for (int e = tid; e < sd * nr; e += RNT) {
         const int k = e / nr, r = e % nr;
         S[k * RE + r] = a.state[(long)k * a.N + i0 + r];
     }
     for (int r = tid; r < RE; r += RNT) {
         NEED[r] = 1;
+        NEED[RE + r] = 0;
         if (r < nr) {
             EK[r] = a.env_key[i0 + r];
             EC[r] = a.env_ctr[i0 + r];
@@ -233,199 +311,269 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         }
     }
     if (tid < ad) LS[tid] = fminf(fmaxf(th[a.pol.mlp_n + tid], -5.f), 1.f);  // nn.cpp:185-188
-    if (tid == 0) { VF[0] = 1; VF[1] = 1; }
-    if ((tid >> 5) == 0) umma::tmem_alloc(tslot, 256);
+    if (tid == 0) { VF[0] = 1; VF[1] = 0; }
+    if (warp == 0) umma::tmem_alloc(tslot, 512);
     if (tid == 32) {
-        umma::mbar_init(&x.fullb[0], 1);
-        umma::mbar_init(&x.fullb[1], 1);
-        umma::mbar_init(x.mmad, 1);
+        for (int i = 0; i < MAX_SLOTS; ++i) {
+            umma::mbar_init(&B->pfull[i], 1);
+            umma::mbar_init(&B->pempty[i], 1);
+            umma::mbar_init(&B->cfull[i], 1);
+            umma::mbar_init(&B->cempty[i], 1);
+        }
+        umma::mbar_init(&B->pacc, 1);
+        umma::mbar_init(&B->cacc, 1);
+        umma::mbar_init(&B->php, GROUP);
+        umma::mbar_init(&B->chp, GROUP);
+        for (int i = 0; i < 2; ++i) {
+            umma::mbar_init(&B->xp_ready[i], GROUP);
+            umma::mbar_init(&B->xp_free[i], 1);
+            umma::mbar_init(&B->vf_ready[i], 1);
+            umma::mbar_init(&B->cdone[i], GROUP);
+        }
+        umma::mbar_init(&B->xc_ready, GROUP);
+        umma::mbar_init(&B->xc_free, 1);
         umma::fence_barrier_init();
     }
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
-    x.tbase = *tslot;
-    Issuer is{0, 0};
-    if (tid == 0) {
-        issue_next(a, x, is, VF, c);
-        issue_next(a, x, is, VF, c);
-    }
-    const int warp = tid >> 5, lane = tid & 31;
-    const uint32_t xsbo = (uint32_t)a.pol_plan.kin_pad[0] * 16;
+    const uint32_t tbase = *tslot;
+    const NetPlan& PP = a.pol_plan;
+    const NetPlan& CP = a.cri_plan;
+    const uint8_t* pblob = a.pol_blob + (long)c * PP.blob_bytes;
+    const uint8_t* cblob = a.cri_blob + (long)c * CP.blob_bytes;
 
-#ifdef MB_ROLL_PROF
-    unsigned long long prof_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, prof_last_ = gtimer();
-#endif
-    for (int t = 0; t < a.T; ++t) {
-        // ---- observation -> layer-0 operand (bf16, MN-major) + batch.obs
-        for (int q = tid; q < nr * 4; q += RNT)  // 4 threads per instance (no div / mod)
-            for (int r = q >> 2, k = q & 3; k < od; k += 4) {
-                const float v = S[k * RE + r];
-                a.obs[((long)(i0 + r) * a.T + t) * od + k] = v;
-                *reinterpret_cast<__nv_bfloat16*>(x.xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 +
-                                                  (r & 7) * 2) = __float2bfloat16_rn(v);
+    if (warp >= 8) {
+        // ================= issue warps (converged; elected lanes issue)
+        {
+            Ring pr{pring, B->pfull, B->pempty, a.pol_slots, a.slot_bytes, 0, 0};
+            Ring cr{cring, B->cfull, B->cempty, a.cri_slots, a.slot_bytes, 0, 0};
+            if (warp == 8) {  // policy producer: P(0..T-1)
+                for (int t = 0; t < T; ++t) produce_pass(PP, pblob, pr);
+            } else if (warp == 9) {  // policy MMA
+                int hph = 0;
+                for (int t = 0; t < T; ++t) {
+                    wait_phase(&B->xp_ready[t & 1], t >> 1);
+                    umma::fence_after_sync();
+                    mma_pass(PP, a.pol.L, pr, tbase + POL_COL, umma::smem_u32(xp + (t & 1) * a.xb_bytes),
+                             umma::smem_u32(hp), nepad, &B->pacc, &B->php, hph, nullptr);
+                }
+            } else if (warp == 10) {  // critic producer: [C_final(s-1)], [C_cur(s) if VF(s)], ..., C_final(T-1)
+                for (int s = 0; s < T; ++s) {
+                    if (s > 0) produce_pass(CP, cblob, cr);
+                    wait_phase(&B->vf_ready[s & 1], s >> 1);
+                    if (VF[s & 1]) produce_pass(CP, cblob, cr);
+                }
+                produce_pass(CP, cblob, cr);
+            } else {  // critic MMA, same sequence
+                int hph = 0;
+                for (int s = 0; s <= T; ++s) {
+                    if (s > 0) {
+                        wait_phase(&B->xc_ready, s - 1);
+                        umma::fence_after_sync();
+                        mma_pass(CP, a.cri.L, cr, tbase + CRI_COL, umma::smem_u32(xc), umma::smem_u32(hc), nepad,
+                                 &B->cacc, &B->chp, hph, &B->xc_free);
+                    }
+                    if (s == T) break;
+                    wait_phase(&B->vf_ready[s & 1], s >> 1);
+                    if (VF[s & 1]) {
+                        wait_phase(&B->xp_ready[s & 1], s >> 1);
+                        umma::fence_after_sync();
+                        mma_pass(CP, a.cri.L, cr, tbase + CRI_COL, umma::smem_u32(xp + (s & 1) * a.xb_bytes),
+                                 umma::smem_u32(hc), nepad, &B->cacc, &B->chp, hph, &B->xp_free[s & 1]);
+                    } else {
+                        if (umma::elect_one()) umma::mbar_arrive(&B->xp_free[s & 1]);
+                        __syncwarp();
+                    }
+                }
             }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ================= critic group: epilogues, value / next value
+        const int gw = warp & 3;
+        const int rr = gw * 16 + lane;  // env of this lane in the M = 64 output layout
+        const bool own = lane < 16 && rr < nr;
+        const float* cb = ph + a.cri.boff[a.cri.L - 1];
+        int aph = 0;
+        float v[16];
+        for (int s = 0; s <= T; ++s) {
+            if (s < T) wait_phase(&B->vf_ready[s & 1], s >> 1);  // NEED / VF of step s
+            if (s > 0) {  // C_final(s-1) -> next_value[s-1]; value[s] where no reset
+                group_pass(CP, a.cri, ph, hc, tbase + CRI_COL, nepad, &B->cacc, aph, &B->chp, gw, lane, v);
+                if (own) {
+                    const long row = (long)(i0 + rr) * T + (s - 1);
+                    const bool cont = s < T && !NEED[(s & 1) * RE + rr];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)  // compile-time indices: v stays in registers
+                        if (k < m) {
+                            const float nv = v[k] + cb[k];
+                            a.next_value[row * m + k] = nv;
+                            if (cont) a.value[(row + 1) * m + k] = nv;
+                        }
+                }
+            }
+            if (s == T) break;
+            if (VF[s & 1]) {  // C_cur(s) -> value[s] of the instances reset before step s
+                group_pass(CP, a.cri, ph, hc, tbase + CRI_COL, nepad, &B->cacc, aph, &B->chp, gw, lane, v);
+                if (own && NEED[(s & 1) * RE + rr]) {
+                    const long row = (long)(i0 + rr) * T + s;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k < m) a.value[row * m + k] = v[k] + cb[k];
+                }
+            }
+            umma::mbar_arrive(&B->cdone[s & 1]);
+        }
+    } else {
+        // ================= policy group: the critical path
+        const int gtid = tid, gw = warp;
+        const int rr = gw * 16 + lane;
+        const float* pb = th + a.pol.boff[a.pol.L - 1];
+        int aph = 0;
+        float v[16];
+        write_operand(S, nr, od, xp, xsbo, a.obs, T, 0, i0, gtid);
         umma::fence_proxy_async();
-        __syncthreads();
-        RPROF(0);
-        // ---- policy
-        run_net(a, x, is, VF, c, 0, th);
-        RPROF(1);
-        if (warp < 4) {  // M = 64 output layout: env = 16*warp + lane (lanes < 16)
-            float v[16];
-            umma::tmem_ld16(x.tbase + ((uint32_t)(warp * 32) << 16) + OUT_COL, v);
-            const int r = warp * 16 + lane;
-            if (lane < 16 && r < nr)
-                for (int d = 0; d < ad; ++d) MU[r * 16 + d] = v[d] + th[a.pol.boff[a.pol.L - 1] + d];
-        }
-        umma::fence_before_sync();
-        __syncthreads();
-        RPROF(2);
-        // ---- Gaussian sample (nn.cpp:192-202): the precomputed draw of (t, instance, dim)
-        const float* eps_t = a.eps + ((long)t * a.N + i0) * ad;
-        for (int e = tid; e < nr * ad; e += RNT) {
-            const int r = e / ad, d = e - r * ad;
-            const float sig = __expf(LS[d]);
-            const float mu = MU[r * 16 + d];
-            const float z = mu + sig * eps_t[e];
-            a.act_pre[((long)(i0 + r) * a.T + t) * ad + d] = z;
-            // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
-            // squashed action tanh(z) for the env step: both per (env, dim) item here
-            // rather than in the one-thread-per-env loops
-            const float zn = (z - mu) / sig;
-            MU[r * 16 + d] = (-0.5f * zn * zn - LS[d] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
-            ZS[r * 16 + d] = tanhf(z);
-        }
-        __syncthreads();
-        for (int r = tid; r < nr; r += RNT) {  // action_logprob: the dims' terms in order
-            float lp = 0.f;
-            for (int d = 0; d < ad; ++d) lp += MU[r * 16 + d];
-            a.logprob[(long)(i0 + r) * a.T + t] = lp;
-        }
-        RPROF(3);
-        // ---- critic at the current obs, only if some instance reset (or t = 0)
-        if (VF[t & 1]) {
-            run_net(a, x, is, VF, c, 1, ph);
-            if (warp < 4) {
-                float v[16];
-                umma::tmem_ld16(x.tbase + ((uint32_t)(warp * 32) << 16) + OUT_COL, v);
-                const int r = warp * 16 + lane;
-                if (lane < 16 && r < nr)
-                    for (int k = 0; k < m; ++k) VV[r * 8 + k] = v[k] + ph[a.cri.boff[a.cri.L - 1] + k];
-            }
-            umma::fence_before_sync();
-        }
-        __syncthreads();
-        RPROF(4);
-        // ---- value, env step (env.cpp:60-92), tracker (rollout.cpp:143-148)
-        int any_reset = 0;
-        for (int r = tid; r < nr; r += RNT) {
-            const long row = (long)(i0 + r) * a.T + t;
-            for (int k = 0; k < m; ++k) a.value[row * m + k] = NEED[r] ? VV[r * 8 + k] : NV[r * 8 + k];
-            float act[16], rw[8];  // compile-time indexed (predicated): registers, not local memory
-            bool anyc = false;
+        umma::mbar_arrive(&B->xp_ready[0]);
+        if (gtid == 0) umma::mbar_arrive(&B->vf_ready[0]);  // NEED / VF of step 0 were set before the sync
+        for (int t = 0; t < T; ++t) {
+            // ---- policy(obs_t)
+            group_pass(PP, a.pol, th, hp, tbase + POL_COL, nepad, &B->pacc, aph, &B->php, gw, lane, v);
+            if (lane < 16 && rr < nr)
 #pragma unroll
-            for (int d = 0; d < 16; ++d) {
-                act[d] = 0.f;
-                if (d < ad) {
-                    const float xx = ZS[r * 16 + d];  // tanh(z), from the sampling pass
-                    if (!isfinite(xx)) atomicExch(a.err, 3);
-                    act[d] = fminf(fmaxf(xx, -1.f), 1.f);
-                    anyc |= act[d] != xx;
-                }
+                for (int d = 0; d < 16; ++d)
+                    if (d < ad) MU[rr * 16 + d] = v[d] + pb[d];
+            umma::bar_sync(BAR_POL, GROUP);
+            RPROF(1);
+            // ---- Gaussian sample (nn.cpp:192-202): the precomputed draw of (t, instance, dim)
+            const float* eps_t = a.eps + ((long)t * a.N + i0) * ad;
+            for (int e = gtid; e < nr * ad; e += GROUP) {
+                const int r = e / ad, d = e - r * ad;
+                const float sig = __expf(LS[d]);
+                const float mu = MU[r * 16 + d];
+                const float z = mu + sig * eps_t[e];
+                a.act_pre[((long)(i0 + r) * T + t) * ad + d] = z;
+                // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
+                // squashed action tanh(z) for the env step
+                const float zn = (z - mu) / sig;
+                MU[r * 16 + d] = (-0.5f * zn * zn - LS[d] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
+                ZS[r * 16 + d] = tanhf(z);
             }
+            umma::bar_sync(BAR_POL, GROUP);
+            RPROF(2);
+            // NEED / VF of step t - 1 are reused for step t + 1: the critic group must be done with them
+            if (t > 0) wait_phase(&B->cdone[(t - 1) & 1], (t - 1) >> 1);
+            int any_reset = 0;
+            for (int r = gtid; r < nr; r += GROUP) {
+                float lp = 0.f;  // action_logprob: the dims' terms in order
+                for (int d = 0; d < ad; ++d) lp += MU[r * 16 + d];
+                const long row = (long)(i0 + r) * T + t;
+                a.logprob[row] = lp;
+                // ---- env step (env.cpp:60-92), tracker (rollout.cpp:143-148)
+                float act[16], rw[8];  // compile-time indexed (predicated): registers, not local memory
+                bool anyc = false;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) rw[k] = 0.f;
-            if (anyc) atomicAdd(a.clamp_count, 1ULL);
-            float* s = S + r;
-            const bool tm = env_do_step(a.kind, s, RE, act, rw);
-            const int st = STP[r] + 1;
-            const bool tr = !tm && st >= a.max_steps;
-            a.term[row] = tm;
-            a.trunc[row] = tr;
+                for (int d = 0; d < 16; ++d) {
+                    act[d] = 0.f;
+                    if (d < ad) {
+                        const float xx = ZS[r * 16 + d];  // tanh(z), from the sampling pass
+                        if (!isfinite(xx)) atomicExch(a.err, 3);
+                        act[d] = fminf(fmaxf(xx, -1.f), 1.f);
+                        anyc |= act[d] != xx;
+                    }
+                }
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (k < m) {
-                    a.reward[row * m + k] = rw[k];
-                    TRK[r * 8 + k] += rw[k];
+                for (int k = 0; k < 8; ++k) rw[k] = 0.f;
+                if (anyc) atomicAdd(a.clamp_count, 1ULL);
+                const bool tm = env_do_step(a.kind, S + r, RE, act, rw);
+                const int st = STP[r] + 1;
+                const bool tr = !tm && st >= a.max_steps;
+                a.term[row] = tm;
+                a.trunc[row] = tr;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (k < m) {
+                        a.reward[row * m + k] = rw[k];
+                        TRK[r * 8 + k] += rw[k];
+                    }
+                const bool done = tm || tr;
+                if (done) {
+                    double ret = 0.0;
+                    for (int k = 0; k < m; ++k) {
+                        ret += (double)a.cluster_w[c * m + k] * TRK[r * 8 + k];
+                        TRK[r * 8 + k] = 0.f;
+                    }
+                    a.ret_sum[i0 + r] += ret;
+                    a.ret_cnt[i0 + r] += 1;
                 }
-            if (tm || tr) {
-                double ret = 0.0;
-                for (int k = 0; k < m; ++k) {
-                    ret += (double)a.cluster_w[c * m + k] * TRK[r * 8 + k];
-                    TRK[r * 8 + k] = 0.f;
-                }
-                a.ret_sum[i0 + r] += ret;
-                a.ret_cnt[i0 + r] += 1;
-                STP[r] = 0;  // (the reset itself after the final-obs operand pass below)
-                NEED[r] = 1;
-                any_reset = 1;
-            } else {
-                STP[r] = st;
-                NEED[r] = 0;
+                STP[r] = done ? 0 : st;  // (the reset itself after the final-obs operand pass below)
+                NEED[((t + 1) & 1) * RE + r] = done;
+                any_reset |= done;
             }
+            any_reset = umma::bar_sync_or(BAR_POL, GROUP, any_reset);
+            RPROF(3);
+            // ---- pre-reset final obs -> critic operand, once C_final(t-1) has consumed it
+            if (t > 0) wait_phase(&B->xc_free, t - 1);
+            if (gtid == 0) {
+                VF[(t + 1) & 1] = any_reset;
+                umma::mbar_arrive(&B->vf_ready[(t + 1) & 1]);
+            }
+            write_operand(S, nr, od, xc, xsbo, nullptr, T, t, i0, gtid);
+            umma::fence_proxy_async();
+            umma::mbar_arrive(&B->xc_ready);
+            if (any_reset) {  // auto-reset from the instance's persistent stream (env.cpp:84-92)
+                umma::bar_sync(BAR_POL, GROUP);
+                for (int r = gtid; r < nr; r += GROUP)
+                    if (NEED[((t + 1) & 1) * RE + r]) {
+                        uint64_t cc = EC[r];
+                        env_do_reset(a.kind, S + r, RE, EK[r], &cc);
+                        EC[r] = cc;
+                    }
+                umma::bar_sync(BAR_POL, GROUP);
+            }
+            // ---- obs_{t+1} -> policy operand (buffer (t+1) & 1, once step t-1's readers are done)
+            if (t + 1 < T) {
+                if (t + 1 >= 2) wait_phase(&B->xp_free[(t + 1) & 1], ((t + 1) >> 1) - 1);
+                write_operand(S, nr, od, xp + ((t + 1) & 1) * a.xb_bytes, xsbo, a.obs, T, t + 1, i0, gtid);
+                umma::fence_proxy_async();
+                umma::mbar_arrive(&B->xp_ready[(t + 1) & 1]);
+            }
+            RPROF(4);
         }
-        any_reset = __syncthreads_or(any_reset);
-        if (tid == 0) VF[(t + 1) & 1] = any_reset;
-        // pre-reset final obs -> critic operand, 4 threads per instance
-        for (int r = tid >> 2; r < nr; r += RNT / 4)
-            for (int k = tid & 3; k < od; k += 4)
-                *reinterpret_cast<__nv_bfloat16*>(x.xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 +
-                                                  (r & 7) * 2) = __float2bfloat16_rn(S[k * RE + r]);
-        if (any_reset) {  // auto-reset from the instance's persistent stream (env.cpp:84-92)
-            __syncthreads();
-            for (int r = tid; r < nr; r += RNT)
-                if (NEED[r]) {
-                    uint64_t cc = EC[r];
-                    env_do_reset(a.kind, S + r, RE, EK[r], &cc);
-                    EC[r] = cc;
-                }
-        }
-        umma::fence_proxy_async();
-        __syncthreads();
-        RPROF(5);
-        // ---- critic at the pre-reset final obs -> next_value
-        run_net(a, x, is, VF, c, 1, ph);
-        RPROF(6);
-        if (warp < 4) {
-            float v[16];
-            umma::tmem_ld16(x.tbase + ((uint32_t)(warp * 32) << 16) + OUT_COL, v);
-            const int r = warp * 16 + lane;
-            if (lane < 16 && r < nr)
-                for (int k = 0; k < m; ++k) {
-                    const float nv = v[k] + ph[a.cri.boff[a.cri.L - 1] + k];
-                    NV[r * 8 + k] = nv;
-                    a.next_value[((long)(i0 + r) * a.T + t) * m + k] = nv;
-                }
-        }
-        umma::fence_before_sync();
-        __syncthreads();
-    }
 #ifdef MB_ROLL_PROF
-    if (blockIdx.x == 0 && tid == 0)
-        printf("rollout CTA0 us (thread 0's clock): obs %.1f policy %.1f pol_out %.1f sample+logprob(own rows) %.1f "
-               "critic_cur(+wait) %.1f env %.1f "
-               "critic_final %.1f tail %.1f\n",
-               prof_[0] * 1e-3, prof_[1] * 1e-3, prof_[2] * 1e-3, prof_[3] * 1e-3, prof_[4] * 1e-3, prof_[5] * 1e-3,
-               prof_[6] * 1e-3, prof_[7] * 1e-3);
+        if (blockIdx.x == 0 && gtid == 0) {
+            const unsigned long long* q = g_rp[0];
+            printf("rollout CTA0 policy group us: out+MU %.1f sample %.1f env %.1f final-obs+reset+obs %.1f "
+                   "epilogues %.1f wait-acc %.1f\n",
+                   q[1] * 1e-3, q[2] * 1e-3, q[3] * 1e-3, q[4] * 1e-3, q[5] * 1e-3, q[6] * 1e-3);
+        }
 #endif
-    for (int e = tid; e < sd * nr; e += RNT) {
-        const int k = e / nr, r = e % nr;
-        a.state[(long)k * a.N + i0 + r] = S[k * RE + r];
+        umma::bar_sync(BAR_POL, GROUP);
+        for (int e = gtid; e < sd * nr; e += GROUP) {
+            const int k = e / nr, r = e % nr;
+            a.state[(long)k * a.N + i0 + r] = S[k * RE + r];
+        }
+        for (int r = gtid; r < nr; r += GROUP) {
+            a.env_ctr[i0 + r] = EC[r];
+            a.steps[i0 + r] = STP[r];
+            for (int k = 0; k < m; ++k) a.tracker[(long)(i0 + r) * m + k] = TRK[r * 8 + k];
+        }
     }
-    for (int r = tid; r < nr; r += RNT) {
-        a.env_ctr[i0 + r] = EC[r];
-        a.steps[i0 + r] = STP[r];
-        for (int k = 0; k < m; ++k) a.tracker[(long)(i0 + r) * m + k] = TRK[r * 8 + k];
-    }
+    umma::fence_before_sync();
     __syncthreads();
-    if (warp == 0) umma::tmem_free(x.tbase, 256);
+    umma::fence_after_sync();
+#ifdef MB_ROLL_PROF
+    if (blockIdx.x == 0 && tid == 0) {
+        const unsigned long long* q = g_rp[2];
+        printf("rollout CTA0 critic group us: epilogues+rest %.1f wait-acc %.1f\n", q[5] * 1e-3, q[6] * 1e-3);
+    }
+#endif
+    if (warp == 0) umma::tmem_free(tbase, 512);
 }
 
-// theta (fp32, reference flat layout) -> bf16 blob in the UMMA K-major image:
-// hidden layer l, tile t: rows [128t, 128t+128) x kin_pad(l); output layer:
-// 16 rows x kin_pad(L-1). Element (r, k) of a chunk at
-// (r/8)*kin_pad*16 + (k/8)*128 + (r%8)*16 + (k%8)*2.
+// theta (fp32, reference flat layout) -> bf16 blob in the UMMA K-major image.
+// Chunk c holds rows [128 tile, +rows) x K columns [k0, k0 + kw) of its
+// layer; element (r, k0 + kk) at (r/8)*kw*16 + (kk/8)*128 + (r%8)*16 + (kk%8)*2.
 __global__ void k_pack_theta(const float* __restrict__ theta, long P, NetDims nd, NetPlan pl, uint8_t* blob) {
     const int g = blockIdx.y;
     const float* th = theta + (long)g * P;
@@ -433,19 +581,23 @@ __global__ void k_pack_theta(const float* __restrict__ theta, long P, NetDims nd
     const long units = pl.blob_bytes / 16;
     for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < units; u += (long)gridDim.x * blockDim.x) {
         const long byte = u * 16;
-        int c = 0;
-        while (c + 1 < pl.nchunks && byte >= pl.chunk_off[c + 1]) ++c;
+        int lo = 0, hi = pl.nchunks - 1;  // last chunk with chunk_off <= byte
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pl.chunk_off[mid] <= byte) lo = mid; else hi = mid - 1;
+        }
+        const int c = lo;
         const int l = pl.chunk_layer[c], tile = pl.chunk_tile[c];
-        const int kin = pl.kin_pad[l];
+        const int kw = pl.chunk_kw[c], k0 = pl.chunk_k0[c];
         const int within = (int)(byte - pl.chunk_off[c]);
-        const int rblk = within / (kin * 16), rem = within % (kin * 16);
+        const int rblk = within / (kw * 16), rem = within % (kw * 16);
         const int kb = rem / 128, r8 = (rem % 128) / 16;
         const int row = tile * 128 + rblk * 8 + r8;
         const int in = nd.sz[l], outd = nd.sz[l + 1];
         float v[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const int k = kb * 8 + e;
+            const int k = k0 + kb * 8 + e;
             v[e] = (row < outd && k < in) ? th[nd.woff[l] + (long)row * in + k] : 0.f;
         }
         uint4 q;
@@ -485,14 +637,22 @@ NetPlan make_plan(const NetDims& nd) {
         pl.kin_pad[l] = l == 0 ? pad16(nd.sz[0]) : pad128(nd.sz[l]);
         if (nd.sz[l + 1] > 256 && l < nd.L - 1) throw ShapeError("tensor-core rollout supports hidden widths <= 256");
         const bool last = l == nd.L - 1;
+        const int rows = last ? 16 : 128;
+        const int kwmax = SLOT_MAX / (rows * 2);  // a chunk fills at most one ring slot
         pl.tiles[l] = last ? 1 : pad128(nd.sz[l + 1]) / 128;
-        for (int t = 0; t < pl.tiles[l]; ++t, ++c) {
-            pl.chunk_off[c] = (int)off;
-            pl.chunk_bytes[c] = (last ? 16 : 128) * pl.kin_pad[l] * 2;
-            pl.chunk_layer[c] = l;
-            pl.chunk_tile[c] = t;
-            off += pl.chunk_bytes[c];
-        }
+        for (int t = 0; t < pl.tiles[l]; ++t)
+            for (int k0 = 0; k0 < pl.kin_pad[l]; k0 += kwmax, ++c) {
+                if (c >= ROLL_MAX_CHUNKS) throw ShapeError("tensor-core rollout: too many weight chunks");
+                const int kw = std::min(kwmax, pl.kin_pad[l] - k0);
+                pl.chunk_off[c] = (int)off;
+                pl.chunk_bytes[c] = rows * kw * 2;
+                pl.chunk_layer[c] = l;
+                pl.chunk_tile[c] = t;
+                pl.chunk_k0[c] = k0;
+                pl.chunk_kw[c] = kw;
+                pl.max_chunk = std::max(pl.max_chunk, pl.chunk_bytes[c]);
+                off += pl.chunk_bytes[c];
+            }
     }
     pl.nchunks = c;
     pl.blob_bytes = (int)off;
@@ -513,25 +673,30 @@ void rollout_noise(uint64_t roll_key, int inst_base, int N, int T, int ad, float
     MB_LAUNCH();
 }
 
-size_t rollout_tc_smem(const RolloutTcArgs& a) {
-    return 2ull * a.slot_bytes + a.xb_bytes + 2ull * a.hb_bytes + sizeof(float) * a.sdim * RE +
-           sizeof(float) * RE * (16 + 16 + 8 + 8 + 8) + 64 + 2 * 8 * RE + 2 * 4 * RE + 16 + 16 + 8 + 16;
+// everything but the two weight rings
+static size_t rollout_fixed_smem(const RolloutTcArgs& a) {
+    return 3ull * a.xb_bytes + 2ull * a.hb_bytes + sizeof(float) * a.sdim * RE + sizeof(float) * RE * 8 +
+           sizeof(float) * 16 + 2 * 8 * RE + 4 * RE + 4 * 2 * RE + 16 + sizeof(Bars) + 16;
 }
 
 void rollout_tc(RolloutTcArgs a, cudaStream_t s) {
-    int slot = 0;
-    for (int c = 0; c < a.pol_plan.nchunks; ++c) slot = slot > a.pol_plan.chunk_bytes[c] ? slot : a.pol_plan.chunk_bytes[c];
-    for (int c = 0; c < a.cri_plan.nchunks; ++c) slot = slot > a.cri_plan.chunk_bytes[c] ? slot : a.cri_plan.chunk_bytes[c];
-    a.slot_bytes = slot;
+    if (a.T <= 0 || a.K <= 0) return;
+    if (a.pol_plan.kin_pad[0] != a.cri_plan.kin_pad[0])
+        throw ShapeError("tensor-core rollout: policy and critic inputs differ");
+    a.slot_bytes = std::max(a.pol_plan.max_chunk, a.cri_plan.max_chunk);
     a.xb_bytes = RE * a.pol_plan.kin_pad[0] * 2;
     int hmax = 128;
-    for (int l = 1; l < a.pol.L; ++l) hmax = hmax > a.pol_plan.kin_pad[l] ? hmax : a.pol_plan.kin_pad[l];
-    for (int l = 1; l < a.cri.L; ++l) hmax = hmax > a.cri_plan.kin_pad[l] ? hmax : a.cri_plan.kin_pad[l];
+    for (int l = 1; l < a.pol.L; ++l) hmax = std::max(hmax, a.pol_plan.kin_pad[l]);
+    for (int l = 1; l < a.cri.L; ++l) hmax = std::max(hmax, a.cri_plan.kin_pad[l]);
     a.hb_bytes = RE * hmax * 2;
     const int ne = a.reps < RE ? a.reps : RE;
     a.nepad = pad16(ne);
-    const size_t bytes = rollout_tc_smem(a);
-    if (bytes > 227 * 1024) throw ShapeError("tensor-core rollout: shared-memory plan exceeds 227 KB");
+    const size_t limit = 227 * 1024, fixed = rollout_fixed_smem(a);
+    const int slots = fixed < limit ? (int)((limit - fixed) / a.slot_bytes) : 0;
+    a.pol_slots = std::min(MAX_SLOTS, (slots + 1) / 2);  // the policy chain is the critical path
+    a.cri_slots = std::min(MAX_SLOTS, slots - a.pol_slots);
+    if (a.cri_slots < 2) throw ShapeError("tensor-core rollout: shared-memory plan exceeds 227 KB");
+    const size_t bytes = fixed + (size_t)(a.pol_slots + a.cri_slots) * a.slot_bytes;
     ensure_smem((const void*)k_rollout_tc, bytes);
     const int cpg = (a.reps + RE - 1) / RE;
     k_rollout_tc<<<a.K * cpg, RNT, bytes, s>>>(a);
