@@ -16,11 +16,12 @@
 // * Output layer: D[env][out] = act (A, MN-major, M = 64 envs) x W_out^T
 //   (B, K-major, N = 16), so each env-owning thread gets its own outputs.
 // * Warp-specialised, two independent chains per CTA:
-//     warps 0-3  policy group: policy epilogues, Gaussian sample, log-prob,
-//                env step, auto-reset, operand writes (the critical path);
-//     warps 4-7  critic group: critic epilogues, value / next value;
-//     warp 8 / 9   policy bulk-copy producer / policy MMA issuer;
-//     warp 10 / 11 critic bulk-copy producer / critic MMA issuer.
+//     warps 0-7    policy group: policy epilogues (one 128-feature tile per
+//                  warp quadrant pair), Gaussian sample, log-prob, env step,
+//                  auto-reset, operand writes (the critical path);
+//     warps 8-11   critic group: critic epilogues, value / next value;
+//     warps 12/13  policy bulk-copy producer / policy MMA issuer;
+//     warps 14/15  critic bulk-copy producer / critic MMA issuer.
 //   Each net has its own weight ring and TMEM columns, so the critic at the
 //   final observation of step t runs while the policy chain goes on to step
 //   t + 1 (both depend only on the env step), and weights of the next pass
@@ -43,8 +44,10 @@ namespace mb200 {
 
 namespace {
 constexpr int RE = 64;           // instances per CTA
-constexpr int GROUP = 128;       // threads per epilogue warp group
-constexpr int RNT = 3 * GROUP;   // policy group, critic group, 4 issue warps
+constexpr int PGROUP = 256;      // policy group: 8 warps (two per TMEM lane quadrant, one tile each)
+constexpr int CGROUP = 128;      // critic group: 4 warps
+constexpr int RNT = PGROUP + CGROUP + 128;  // + 4 issue warps
+constexpr int W_CRI = PGROUP / 32, W_ISSUE = W_CRI + CGROUP / 32;  // first warp of each role
 constexpr int MAX_SLOTS = 4;     // weight-ring slots per net
 constexpr int SLOT_MAX = 16384;  // bytes per ring slot (largest chunk)
 constexpr uint32_t POL_COL = 0, CRI_COL = 256, OUT_OFF = 128;  // TMEM columns (512 allocated)
@@ -60,7 +63,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // thread slot j: 0 policy group thread 0, 2 critic group thread 0
 __device__ __forceinline__ int rprof_slot() {
     if (blockIdx.x != 0) return -1;
-    return threadIdx.x == 0 ? 0 : threadIdx.x == 128 ? 2 : -1;
+    return threadIdx.x == 0 ? 0 : threadIdx.x == PGROUP ? 2 : threadIdx.x == (W_ISSUE + 1) * 32 ? 1 : -1;
 }
 #define RPROF(k)                                          \
     {                                                     \
@@ -131,10 +134,19 @@ __device__ __forceinline__ void produce_pass(const NetPlan& pl, const uint8_t* b
 __device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint32_t tbase, uint32_t in0,
                                          uint32_t hb0, int nepad, uint64_t* acc, uint64_t* hready, int& hph,
                                          uint64_t* xfree) {
+#ifdef MB_ROLL_PROF
+    long long cw_h = 0, cw_f = 0, c_all = clock64();
+#endif
     int c = 0;
     for (int l = 0; l < L; ++l) {
         if (l > 0) {
+#ifdef MB_ROLL_PROF
+            const long long q0 = clock64();
+#endif
             wait_phase(hready, hph++);
+#ifdef MB_ROLL_PROF
+            cw_h += clock64() - q0;
+#endif
             umma::fence_after_sync();
         }
         const bool last = l == L - 1;
@@ -143,7 +155,13 @@ __device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint
         const uint32_t idesc =
             last ? umma::idesc_bf16(64, 16, true, false) : umma::idesc_bf16(128, nepad, false, true);
         for (; c < pl.nchunks && pl.chunk_layer[c] == l; ++c) {
+#ifdef MB_ROLL_PROF
+            const long long q0 = clock64();
+#endif
             wait_phase(&r.full[r.slot], r.round);
+#ifdef MB_ROLL_PROF
+            cw_f += clock64() - q0;
+#endif
             umma::fence_after_sync();
             const int kw = pl.chunk_kw[c], k0 = pl.chunk_k0[c];
             const uint64_t w_desc =
@@ -173,15 +191,24 @@ __device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint
         }
         __syncwarp();
     }
+#ifdef MB_ROLL_PROF
+    if (rprof_slot() == 1) {
+        g_rp[1][0] += clock64() - c_all;
+        g_rp[1][1] += cw_h;
+        g_rp[1][2] += cw_f;
+        g_rp[1][3] += 1;
+    }
+#endif
 }
 
 // group epilogue of hidden layer l: bias + tanh -> the next layer's bf16
 // operand (MN-major, env x kin_pad(l+1)); zeros in the padded features
 __device__ __forceinline__ void hidden_epi(const NetPlan& pl, const NetDims& nd, int l, const float* theta,
-                                           uint8_t* hb, uint32_t tacc, int nepad, int gw, int lane) {
+                                           uint8_t* hb, uint32_t tacc, int nepad, int gw, int lane, int tile0,
+                                           int tstep) {
     const uint32_t osbo = (uint32_t)pl.kin_pad[l + 1] * 16;
     const int out = nd.sz[l + 1];
-    for (int tile = 0; tile < pl.tiles[l]; ++tile) {
+    for (int tile = tile0; tile < pl.tiles[l]; tile += tstep) {
         const int j = tile * 128 + gw * 32 + lane;
         const bool live = j < out;
         const float bj = live ? theta[nd.boff[l] + j] : 0.f;
@@ -213,44 +240,60 @@ __device__ __forceinline__ void hidden_epi(const NetPlan& pl, const NetDims& nd,
     }
 }
 
-// the group's hidden layers of one pass; returns the output layer's 16
+// the group's hidden layers of one pass (warp quadrant gw; tiles tile0,
+// tile0 + tstep, ...); warps with out_reader get the output layer's 16
 // accumulators of env (gw * 16 + lane) (lanes < 16) in v
 __device__ __forceinline__ void group_pass(const NetPlan& pl, const NetDims& nd, const float* theta, uint8_t* hb,
                                            uint32_t tacc, int nepad, uint64_t* acc, int& aph, uint64_t* hready,
-                                           int gw, int lane, float* v) {
+                                           int gw, int lane, int tile0, int tstep, bool out_reader, int bar,
+                                           int nthr, bool leader, float* v) {
     for (int l = 0; l + 1 < nd.L; ++l) {
         RPROF(5);
         wait_phase(acc, aph++);
         RPROF(6);
         umma::fence_after_sync();
-        hidden_epi(pl, nd, l, theta, hb, tacc, nepad, gw, lane);
+        hidden_epi(pl, nd, l, theta, hb, tacc, nepad, gw, lane, tile0, tstep);
         umma::fence_proxy_async();  // generic-proxy operand writes -> the MMA's async proxy
         umma::fence_before_sync();
-        umma::mbar_arrive(hready);
+        umma::bar_sync(bar, nthr);  // the whole group's writes, then one arrival
+        if (leader) umma::mbar_arrive(hready);
     }
     RPROF(5);
     wait_phase(acc, aph++);
     RPROF(6);
-    umma::fence_after_sync();
-    uint32_t r[16];
-    umma::tmem_ld16_async(tacc + OUT_OFF + ((uint32_t)(gw * 32) << 16), r);
-    umma::tmem_wait_ld();
-    umma::fence_before_sync();
+    if (out_reader) {
+        umma::fence_after_sync();
+        uint32_t r[16];
+        umma::tmem_ld16_async(tacc + OUT_OFF + ((uint32_t)(gw * 32) << 16), r);
+        umma::tmem_wait_ld();
+        umma::fence_before_sync();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    }
 }
 
-// observation of the instances (state in S) -> bf16 MN-major operand xb (and
-// optionally the batch's obs rows), 2 threads per instance
-__device__ __forceinline__ void write_operand(const float* S, int nr, int od, uint8_t* xb, uint32_t xsbo,
-                                              float* obs_out, long T, long t, long i0, int gtid) {
-    for (int r = gtid >> 1; r < nr; r += GROUP / 2)
-        for (int k = gtid & 1; k < od; k += 2) {
+// observation of the instances (state in S) -> bf16 MN-major operands,
+// PGROUP / RE threads per instance: xa (all instances, if given) and xb
+// plus the batch's obs rows at step t (if given) for the instances whose
+// need[] flag equals `sel` (all instances when need is null)
+__device__ __forceinline__ void write_operands(const float* S, int nr, int od, uint8_t* xa, uint8_t* xb,
+                                               const int* need, int sel, uint32_t xsbo, float* obs_out, long T,
+                                               long t, long i0, int gtid) {
+    constexpr int TPI = PGROUP / RE;
+    for (int r = gtid / TPI; r < nr; r += RE) {
+        const bool wb = xb && (!need || need[r] == sel);
+        if (!xa && !wb) continue;
+        for (int k = gtid % TPI; k < od; k += TPI) {
             const float v = S[k * RE + r];
-            if (obs_out) obs_out[((i0 + r) * T + t) * od + k] = v;
-            *reinterpret_cast<__nv_bfloat16*>(xb + (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2) =
-                __float2bfloat16_rn(v);
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            const int off = (r >> 3) * xsbo + (k >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2;
+            if (xa) *reinterpret_cast<__nv_bfloat16*>(xa + off) = h;
+            if (wb) {
+                *reinterpret_cast<__nv_bfloat16*>(xb + off) = h;
+                if (obs_out) obs_out[((i0 + r) * T + t) * od + k] = v;
+            }
         }
+    }
 }
 
 __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ RolloutTcArgs a) {
@@ -322,15 +365,15 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         }
         umma::mbar_init(&B->pacc, 1);
         umma::mbar_init(&B->cacc, 1);
-        umma::mbar_init(&B->php, GROUP);
-        umma::mbar_init(&B->chp, GROUP);
+        umma::mbar_init(&B->php, 1);
+        umma::mbar_init(&B->chp, 1);
         for (int i = 0; i < 2; ++i) {
-            umma::mbar_init(&B->xp_ready[i], GROUP);
+            umma::mbar_init(&B->xp_ready[i], 1);
             umma::mbar_init(&B->xp_free[i], 1);
             umma::mbar_init(&B->vf_ready[i], 1);
-            umma::mbar_init(&B->cdone[i], GROUP);
+            umma::mbar_init(&B->cdone[i], 1);
         }
-        umma::mbar_init(&B->xc_ready, GROUP);
+        umma::mbar_init(&B->xc_ready, 1);
         umma::mbar_init(&B->xc_free, 1);
         umma::fence_barrier_init();
     }
@@ -343,14 +386,14 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
     const uint8_t* pblob = a.pol_blob + (long)c * PP.blob_bytes;
     const uint8_t* cblob = a.cri_blob + (long)c * CP.blob_bytes;
 
-    if (warp >= 8) {
+    if (warp >= W_ISSUE) {
         // ================= issue warps (converged; elected lanes issue)
         {
             Ring pr{pring, B->pfull, B->pempty, a.pol_slots, a.slot_bytes, 0, 0};
             Ring cr{cring, B->cfull, B->cempty, a.cri_slots, a.slot_bytes, 0, 0};
-            if (warp == 8) {  // policy producer: P(0..T-1)
+            if (warp == W_ISSUE) {  // policy producer: P(0..T-1)
                 for (int t = 0; t < T; ++t) produce_pass(PP, pblob, pr);
-            } else if (warp == 9) {  // policy MMA
+            } else if (warp == W_ISSUE + 1) {  // policy MMA
                 int hph = 0;
                 for (int t = 0; t < T; ++t) {
                     wait_phase(&B->xp_ready[t & 1], t >> 1);
@@ -358,7 +401,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                     mma_pass(PP, a.pol.L, pr, tbase + POL_COL, umma::smem_u32(xp + (t & 1) * a.xb_bytes),
                              umma::smem_u32(hp), nepad, &B->pacc, &B->php, hph, nullptr);
                 }
-            } else if (warp == 10) {  // critic producer: [C_final(s-1)], [C_cur(s) if VF(s)], ..., C_final(T-1)
+            } else if (warp == W_ISSUE + 2) {  // critic producer: [C_final(s-1)], [C_cur(s) if VF(s)], ..., C_final(T-1)
                 for (int s = 0; s < T; ++s) {
                     if (s > 0) produce_pass(CP, cblob, cr);
                     wait_phase(&B->vf_ready[s & 1], s >> 1);
@@ -389,9 +432,10 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (warp >= W_CRI) {
         // ================= critic group: epilogues, value / next value
         const int gw = warp & 3;
+        const bool cleader = tid == PGROUP;
         const int rr = gw * 16 + lane;  // env of this lane in the M = 64 output layout
         const bool own = lane < 16 && rr < nr;
         const float* cb = ph + a.cri.boff[a.cri.L - 1];
@@ -400,7 +444,8 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         for (int s = 0; s <= T; ++s) {
             if (s < T) wait_phase(&B->vf_ready[s & 1], s >> 1);  // NEED / VF of step s
             if (s > 0) {  // C_final(s-1) -> next_value[s-1]; value[s] where no reset
-                group_pass(CP, a.cri, ph, hc, tbase + CRI_COL, nepad, &B->cacc, aph, &B->chp, gw, lane, v);
+                group_pass(CP, a.cri, ph, hc, tbase + CRI_COL, nepad, &B->cacc, aph, &B->chp, gw, lane, 0, 1, true, BAR_CRI,
+                           CGROUP, cleader, v);
                 if (own) {
                     const long row = (long)(i0 + rr) * T + (s - 1);
                     const bool cont = s < T && !NEED[(s & 1) * RE + rr];
@@ -415,7 +460,8 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             }
             if (s == T) break;
             if (VF[s & 1]) {  // C_cur(s) -> value[s] of the instances reset before step s
-                group_pass(CP, a.cri, ph, hc, tbase + CRI_COL, nepad, &B->cacc, aph, &B->chp, gw, lane, v);
+                group_pass(CP, a.cri, ph, hc, tbase + CRI_COL, nepad, &B->cacc, aph, &B->chp, gw, lane, 0, 1, true, BAR_CRI,
+                           CGROUP, cleader, v);
                 if (own && NEED[(s & 1) * RE + rr]) {
                     const long row = (long)(i0 + rr) * T + s;
 #pragma unroll
@@ -423,48 +469,70 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                         if (k < m) a.value[row * m + k] = v[k] + cb[k];
                 }
             }
-            umma::mbar_arrive(&B->cdone[s & 1]);
+            umma::bar_sync(BAR_CRI, CGROUP);  // the group is done with NEED / VF of step s
+            if (cleader) umma::mbar_arrive(&B->cdone[s & 1]);
         }
     } else {
         // ================= policy group: the critical path
-        const int gtid = tid, gw = warp;
-        const int rr = gw * 16 + lane;
+        const int gtid = tid, gw = warp & 3;
+        const int rr = gw * 16 + lane;  // env of this lane in the M = 64 output layout (warps 0-3)
         const float* pb = th + a.pol.boff[a.pol.L - 1];
         int aph = 0;
         float v[16];
-        write_operand(S, nr, od, xp, xsbo, a.obs, T, 0, i0, gtid);
+        write_operands(S, nr, od, nullptr, xp, nullptr, 0, xsbo, a.obs, T, 0, i0, gtid);
         umma::fence_proxy_async();
-        umma::mbar_arrive(&B->xp_ready[0]);
-        if (gtid == 0) umma::mbar_arrive(&B->vf_ready[0]);  // NEED / VF of step 0 were set before the sync
+        umma::bar_sync(BAR_POL, PGROUP);
+        if (gtid == 0) {
+            umma::mbar_arrive(&B->xp_ready[0]);
+            umma::mbar_arrive(&B->vf_ready[0]);
+        }  // NEED / VF of step 0 were set before the sync
+        constexpr int EPT = RE * 16 / PGROUP;  // sampling items per thread
+        float epsr[EPT];
+        auto load_eps = [&](int t) {
+            const float* eps_t = a.eps + ((long)t * a.N + i0) * ad;
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                const int e = gtid + k * PGROUP;
+                epsr[k] = e < nr * ad ? __ldg(eps_t + e) : 0.f;
+            }
+        };
+        load_eps(0);
         for (int t = 0; t < T; ++t) {
             // ---- policy(obs_t)
-            group_pass(PP, a.pol, th, hp, tbase + POL_COL, nepad, &B->pacc, aph, &B->php, gw, lane, v);
-            if (lane < 16 && rr < nr)
+            group_pass(PP, a.pol, th, hp, tbase + POL_COL, nepad, &B->pacc, aph, &B->php, gw, lane, warp >> 2, 2,
+                       warp < 4, BAR_POL, PGROUP, gtid == 0, v);
+            if (warp < 4 && lane < 16 && rr < nr)
 #pragma unroll
                 for (int d = 0; d < 16; ++d)
                     if (d < ad) MU[rr * 16 + d] = v[d] + pb[d];
-            umma::bar_sync(BAR_POL, GROUP);
+            umma::bar_sync(BAR_POL, PGROUP);
             RPROF(1);
-            // ---- Gaussian sample (nn.cpp:192-202): the precomputed draw of (t, instance, dim)
-            const float* eps_t = a.eps + ((long)t * a.N + i0) * ad;
-            for (int e = gtid; e < nr * ad; e += GROUP) {
-                const int r = e / ad, d = e - r * ad;
-                const float sig = __expf(LS[d]);
-                const float mu = MU[r * 16 + d];
-                const float z = mu + sig * eps_t[e];
-                a.act_pre[((long)(i0 + r) * T + t) * ad + d] = z;
-                // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
-                // squashed action tanh(z) for the env step
-                const float zn = (z - mu) / sig;
-                MU[r * 16 + d] = (-0.5f * zn * zn - LS[d] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
-                ZS[r * 16 + d] = tanhf(z);
+            // ---- Gaussian sample (nn.cpp:192-202): the precomputed draw of (t, instance, dim),
+            // loaded into registers one step ahead
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                const int e = gtid + k * PGROUP;
+                if (e < nr * ad) {
+                    const int r = e / ad, d = e - r * ad;
+                    const float sig = __expf(LS[d]);
+                    const float mu = MU[r * 16 + d];
+                    const float z = mu + sig * epsr[k];
+                    a.act_pre[((long)(i0 + r) * T + t) * ad + d] = z;
+                    // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
+                    // squashed action tanh(z) for the env step
+                    const float zn = (z - mu) / sig;
+                    MU[r * 16 + d] = (-0.5f * zn * zn - LS[d] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
+                    ZS[r * 16 + d] = tanhf(z);
+                }
             }
-            umma::bar_sync(BAR_POL, GROUP);
+            if (t + 1 < T) load_eps(t + 1);
+            umma::bar_sync(BAR_POL, PGROUP);
             RPROF(2);
             // NEED / VF of step t - 1 are reused for step t + 1: the critic group must be done with them
             if (t > 0) wait_phase(&B->cdone[(t - 1) & 1], (t - 1) >> 1);
+            RPROF(7);
             int any_reset = 0;
-            for (int r = gtid; r < nr; r += GROUP) {
+            for (int r = gtid; r < nr; r += PGROUP) {
                 float lp = 0.f;  // action_logprob: the dims' terms in order
                 for (int d = 0; d < ad; ++d) lp += MU[r * 16 + d];
                 const long row = (long)(i0 + r) * T + t;
@@ -510,50 +578,60 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 NEED[((t + 1) & 1) * RE + r] = done;
                 any_reset |= done;
             }
-            any_reset = umma::bar_sync_or(BAR_POL, GROUP, any_reset);
+            any_reset = umma::bar_sync_or(BAR_POL, PGROUP, any_reset);
             RPROF(3);
-            // ---- pre-reset final obs -> critic operand, once C_final(t-1) has consumed it
+            // ---- pre-reset final obs -> critic operand (once C_final(t-1) has consumed the
+            // buffer) and, for the instances that did not reset, obs_{t+1} -> policy operand
+            // (buffer (t+1) & 1, once step t-1's readers are done) in the same pass
+            const bool nxt = t + 1 < T;
             if (t > 0) wait_phase(&B->xc_free, t - 1);
+            if (nxt && t + 1 >= 2) wait_phase(&B->xp_free[(t + 1) & 1], ((t + 1) >> 1) - 1);
+            RPROF(8);
             if (gtid == 0) {
                 VF[(t + 1) & 1] = any_reset;
                 umma::mbar_arrive(&B->vf_ready[(t + 1) & 1]);
             }
-            write_operand(S, nr, od, xc, xsbo, nullptr, T, t, i0, gtid);
+            const int* need = NEED + ((t + 1) & 1) * RE;
+            uint8_t* xpn = nxt ? xp + ((t + 1) & 1) * a.xb_bytes : nullptr;
+            write_operands(S, nr, od, xc, xpn, need, 0, xsbo, a.obs, T, t + 1, i0, gtid);
             umma::fence_proxy_async();
-            umma::mbar_arrive(&B->xc_ready);
+            umma::bar_sync(BAR_POL, PGROUP);
+            if (gtid == 0) {
+                umma::mbar_arrive(&B->xc_ready);
+                if (nxt && !any_reset) umma::mbar_arrive(&B->xp_ready[(t + 1) & 1]);
+            }
             if (any_reset) {  // auto-reset from the instance's persistent stream (env.cpp:84-92)
-                umma::bar_sync(BAR_POL, GROUP);
-                for (int r = gtid; r < nr; r += GROUP)
-                    if (NEED[((t + 1) & 1) * RE + r]) {
+                for (int r = gtid; r < nr; r += PGROUP)
+                    if (need[r]) {
                         uint64_t cc = EC[r];
                         env_do_reset(a.kind, S + r, RE, EK[r], &cc);
                         EC[r] = cc;
                     }
-                umma::bar_sync(BAR_POL, GROUP);
-            }
-            // ---- obs_{t+1} -> policy operand (buffer (t+1) & 1, once step t-1's readers are done)
-            if (t + 1 < T) {
-                if (t + 1 >= 2) wait_phase(&B->xp_free[(t + 1) & 1], ((t + 1) >> 1) - 1);
-                write_operand(S, nr, od, xp + ((t + 1) & 1) * a.xb_bytes, xsbo, a.obs, T, t + 1, i0, gtid);
-                umma::fence_proxy_async();
-                umma::mbar_arrive(&B->xp_ready[(t + 1) & 1]);
+                umma::bar_sync(BAR_POL, PGROUP);
+                if (nxt) {
+                    write_operands(S, nr, od, nullptr, xpn, need, 1, xsbo, a.obs, T, t + 1, i0, gtid);
+                    umma::fence_proxy_async();
+                    umma::bar_sync(BAR_POL, PGROUP);
+                    if (gtid == 0) umma::mbar_arrive(&B->xp_ready[(t + 1) & 1]);
+                }
             }
             RPROF(4);
         }
 #ifdef MB_ROLL_PROF
         if (blockIdx.x == 0 && gtid == 0) {
             const unsigned long long* q = g_rp[0];
-            printf("rollout CTA0 policy group us: out+MU %.1f sample %.1f env %.1f final-obs+reset+obs %.1f "
-                   "epilogues %.1f wait-acc %.1f\n",
-                   q[1] * 1e-3, q[2] * 1e-3, q[3] * 1e-3, q[4] * 1e-3, q[5] * 1e-3, q[6] * 1e-3);
+            printf("rollout CTA0 policy group us: out+MU %.1f sample %.1f wait-cdone %.1f env %.1f "
+                   "wait-free %.1f operands+reset %.1f epilogues %.1f wait-acc %.1f\n",
+                   q[1] * 1e-3, q[2] * 1e-3, q[7] * 1e-3, q[3] * 1e-3, q[8] * 1e-3, q[4] * 1e-3, q[5] * 1e-3,
+                   q[6] * 1e-3);
         }
 #endif
-        umma::bar_sync(BAR_POL, GROUP);
-        for (int e = gtid; e < sd * nr; e += GROUP) {
+        umma::bar_sync(BAR_POL, PGROUP);
+        for (int e = gtid; e < sd * nr; e += PGROUP) {
             const int k = e / nr, r = e % nr;
             a.state[(long)k * a.N + i0 + r] = S[k * RE + r];
         }
-        for (int r = gtid; r < nr; r += GROUP) {
+        for (int r = gtid; r < nr; r += PGROUP) {
             a.env_ctr[i0 + r] = EC[r];
             a.steps[i0 + r] = STP[r];
             for (int k = 0; k < m; ++k) a.tracker[(long)(i0 + r) * m + k] = TRK[r * 8 + k];
@@ -566,6 +644,10 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
     if (blockIdx.x == 0 && tid == 0) {
         const unsigned long long* q = g_rp[2];
         printf("rollout CTA0 critic group us: epilogues+rest %.1f wait-acc %.1f\n", q[5] * 1e-3, q[6] * 1e-3);
+        q = g_rp[1];
+        printf("rollout CTA0 policy MMA warp, cycles per pass: total %.0f wait-epilogue %.0f wait-weights %.0f "
+               "issue %.0f (%llu passes)\n", (double)q[0] / q[3], (double)q[1] / q[3], (double)q[2] / q[3],
+               (double)(q[0] - q[1] - q[2]) / q[3], q[3]);
     }
 #endif
     if (warp == 0) umma::tmem_free(tbase, 512);

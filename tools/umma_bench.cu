@@ -1,0 +1,100 @@
+// Microbenchmark: tcgen05.mma (kind::f16, cta_group::1) issue-to-completion
+// cycles per instruction for the operand layouts the rollout and the GEMMs
+// use. One CTA per SM issues NI back-to-back MMAs on resident SMEM operands
+// (contents irrelevant), commits, waits; reports cycles / MMA.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2603_09237_b200/csrc tools/umma_bench.cu -o /tmp/umma_bench
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "umma.cuh"
+
+using namespace mb200;
+
+__device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t swz) {
+    uint64_t d = umma::smem_desc(saddr, lbo, sbo);
+    d |= (uint64_t)swz << 61;
+    return d;
+}
+
+struct Cfg {
+    int M, N, a_mn, b_mn, swz, nthreads_issue;
+};
+
+__global__ void k_bench(Cfg c, int NI, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) umma::tmem_alloc(&tslot, 512);
+    if (threadIdx.x == 32) {
+        umma::mbar_init(&bar, 1);
+        umma::fence_barrier_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tb = tslot;
+    if (warp == 1) {
+        const uint32_t a0 = umma::smem_u32(smem), b0 = a0 + 65536;
+        // SWIZZLE_NONE: interleaved core matrices (LBO 128 between K blocks, SBO 1024 between 8-row groups)
+        // SWIZZLE_128B K-major: 8-row x 128 B atoms, SBO 1024, K step +32 B
+        const uint32_t swz = c.swz ? 2u : 0u;
+        const uint32_t kstep = c.swz ? 32 : 256;
+        const uint64_t ad = desc_sw(a0, c.swz ? 16 : 128, 1024, swz);
+        const uint64_t bd = desc_sw(b0, c.swz ? 16 : 128, 1024, swz);
+        const uint32_t idesc = umma::idesc_bf16(c.M, c.N, c.a_mn, c.b_mn);
+        long long t0 = 0, t1 = 0;
+        for (int rep = 0; rep < 2; ++rep) {
+            __syncwarp();
+            t0 = clock64();
+            if (umma::elect_one()) {
+                for (int i = 0; i < NI; ++i) {
+                    const int kk = i & 3;
+                    umma::mma_bf16(tb, ad + (uint64_t)((kk * kstep) >> 4), bd + (uint64_t)((kk * kstep) >> 4), idesc,
+                                   i ? 1u : 0u);
+                }
+                umma::commit(&bar);
+            }
+            __syncwarp();
+            umma::mbar_wait(&bar, (uint32_t)rep);
+            t1 = clock64();
+        }
+        if (threadIdx.x == 32 && blockIdx.x == 0) out[0] = t1 - t0;
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(tb, 512);
+}
+
+int main() {
+    long long* d_out;
+    cudaMalloc(&d_out, 8);
+    cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const Cfg cfgs[] = {
+        {128, 64, 0, 1, 0, 1},   // rollout hidden layer: A K-major, B MN-major, no swizzle
+        {128, 64, 0, 0, 0, 1},   // both K-major, no swizzle
+        {128, 64, 0, 0, 1, 1},   // both K-major, 128B swizzle
+        {64, 16, 1, 0, 0, 1},    // rollout output layer
+        {128, 128, 0, 0, 0, 1},  // GEMM N = 128, no swizzle
+        {128, 128, 0, 0, 1, 1},  // GEMM N = 128, 128B swizzle
+        {128, 128, 1, 1, 0, 1},  // GEMM N = 128, both MN-major, no swizzle
+        {128, 256, 0, 0, 0, 1},  // N = 256, no swizzle
+        {128, 256, 0, 0, 1, 1},  // N = 256, 128B swizzle
+    };
+    for (const Cfg& c : cfgs) {
+        for (int grid : {1, 148}) {
+            const int NI = 512;
+            k_bench<<<grid, 128, 200 * 1024>>>(c, NI, d_out);
+            cudaError_t e = cudaDeviceSynchronize();
+            long long cyc = 0;
+            cudaMemcpy(&cyc, d_out, 8, cudaMemcpyDeviceToHost);
+            const double flop_per = 2.0 * c.M * c.N * 16;
+            printf("M %3d N %3d a_mn %d b_mn %d swz %d grid %3d: %.1f cycles/MMA (floor %d) %s\n", c.M, c.N, c.a_mn,
+                   c.b_mn, c.swz, grid, (double)cyc / NI, (c.M < 128 ? 128 : c.M) * c.N / 256,
+                   e == cudaSuccess ? "" : cudaGetErrorString(e));
+            (void)flop_per;
+        }
+    }
+    return 0;
+}
