@@ -173,6 +173,64 @@ __device__ __forceinline__ void env_do_reset(int kind, float* s, int ss, uint64_
     }
 }
 
+// mo-humanoid6 step, split so the twelve joints can run on several threads
+// (csrc/humanoid6_params.h): joint j's actuator / joint update; returns the
+// new actuator state e, joint velocity qd and s_j = tanh(qd)
+__device__ __forceinline__ void h6_joint(float* s, int ss, int j, float aj, float* e_out, float* qd_out,
+                                         float* sj_out) {
+    const float dt = (float)H6_DT;
+    float e = s[(24 + j) * ss], qd = s[(12 + j) * ss], q = s[j * ss];
+    e = __fadd_rn(e, __fmul_rn((float)H6_ALPHA, __fsub_rn(aj, e)));
+    qd = __fadd_rn(qd, __fmul_rn(dt, __fsub_rn(__fsub_rn(__fmul_rn((float)H6_KT, e), __fmul_rn((float)H6_KP, q)),
+                                               __fmul_rn((float)H6_KD, qd))));
+    q = __fadd_rn(q, __fmul_rn(dt, qd));
+    s[(24 + j) * ss] = e;
+    s[(12 + j) * ss] = qd;
+    s[j * ss] = q;
+    *e_out = e;
+    *qd_out = qd;
+    *sj_out = tanhf(qd);
+}
+// the body update from the twelve joints' (s_j, e_j, a_j, qd_j) (element j at
+// [j * stride]), summed in joint order; writes the 6 rewards, returns fallen
+__device__ __forceinline__ bool h6_body(float* s, int ss, const float* sjv, const float* ev, const float* av,
+                                        const float* qdv, int stride, float* r) {
+    const float dt = (float)H6_DT;
+    float sx = 0, sy = 0, sz = 0, sr = 0, sp = 0, sw = 0, asq = 0, qsq = 0;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+        const float sj = sjv[j * stride], e = ev[j * stride], aj = av[j * stride], qd = qdv[j * stride];
+        sx += c_h6[0][j] * sj;
+        sy += c_h6[1][j] * sj;
+        sw += c_h6[5][j] * sj;
+        sz += c_h6[2][j] * e;
+        sr += c_h6[3][j] * e;
+        sp += c_h6[4][j] * e;
+        asq += aj * aj;
+        qsq += qd * qd;
+    }
+    float h = s[36 * ss], vx = s[37 * ss], vy = s[38 * ss], vz = s[39 * ss];
+    float roll = s[40 * ss], pitch = s[41 * ss], wx = s[42 * ss], wy = s[43 * ss], wz = s[44 * ss];
+    vx += dt * (sx - (float)H6_DRAG * vx);
+    vy += dt * (sy - (float)H6_DRAG * vy);
+    vz += dt * (sz - (float)H6_KH * h - (float)H6_DZ * vz);
+    h += dt * vz;
+    wx += dt * (sr - (float)H6_KA * roll - (float)H6_DA * wx);
+    roll += dt * wx;
+    wy += dt * (sp - (float)H6_KA * pitch - (float)H6_DA * wy);
+    pitch += dt * wy;
+    wz += dt * (sw - (float)H6_DRAG * wz);
+    s[36 * ss] = h; s[37 * ss] = vx; s[38 * ss] = vy; s[39 * ss] = vz;
+    s[40 * ss] = roll; s[41 * ss] = pitch; s[42 * ss] = wx; s[43 * ss] = wy; s[44 * ss] = wz;
+    r[0] = vx;
+    r[1] = -asq / 12.f;
+    r[2] = -(roll * roll + pitch * pitch);
+    r[3] = vy;
+    r[4] = -0.1f * qsq / 12.f;
+    r[5] = -(h * h + 0.1f * wz * wz);
+    return fabsf(roll) > (float)H6_FALL || fabsf(pitch) > (float)H6_FALL;
+}
+
 // do_step with a pre-clamped action; writes m rewards, returns terminated.
 __device__ __forceinline__ bool env_do_step(int kind, float* s, int ss, const float* a, float* r) {
     switch (kind) {
@@ -208,49 +266,10 @@ __device__ __forceinline__ bool env_do_step(int kind, float* s, int ss, const fl
             return false;
         }
         case ENV_HUMANOID6: {  // csrc/humanoid6_params.h
-            const float dt = (float)H6_DT;
-            float sx = 0, sy = 0, sz = 0, sr = 0, sp = 0, sw = 0, asq = 0, qsq = 0;
+            float sjv[12], ev[12], qdv[12];
 #pragma unroll
-            for (int j = 0; j < 12; ++j) {
-                float e = s[(24 + j) * ss], qd = s[(12 + j) * ss], q = s[j * ss];
-                e = __fadd_rn(e, __fmul_rn((float)H6_ALPHA, __fsub_rn(a[j], e)));
-                qd = __fadd_rn(qd, __fmul_rn(dt, __fsub_rn(__fsub_rn(__fmul_rn((float)H6_KT, e),
-                                                                      __fmul_rn((float)H6_KP, q)),
-                                                            __fmul_rn((float)H6_KD, qd))));
-                q = __fadd_rn(q, __fmul_rn(dt, qd));
-                s[(24 + j) * ss] = e;
-                s[(12 + j) * ss] = qd;
-                s[j * ss] = q;
-                const float sj = tanhf(qd);
-                sx += c_h6[0][j] * sj;
-                sy += c_h6[1][j] * sj;
-                sw += c_h6[5][j] * sj;
-                sz += c_h6[2][j] * e;
-                sr += c_h6[3][j] * e;
-                sp += c_h6[4][j] * e;
-                asq += a[j] * a[j];
-                qsq += qd * qd;
-            }
-            float h = s[36 * ss], vx = s[37 * ss], vy = s[38 * ss], vz = s[39 * ss];
-            float roll = s[40 * ss], pitch = s[41 * ss], wx = s[42 * ss], wy = s[43 * ss], wz = s[44 * ss];
-            vx += dt * (sx - (float)H6_DRAG * vx);
-            vy += dt * (sy - (float)H6_DRAG * vy);
-            vz += dt * (sz - (float)H6_KH * h - (float)H6_DZ * vz);
-            h += dt * vz;
-            wx += dt * (sr - (float)H6_KA * roll - (float)H6_DA * wx);
-            roll += dt * wx;
-            wy += dt * (sp - (float)H6_KA * pitch - (float)H6_DA * wy);
-            pitch += dt * wy;
-            wz += dt * (sw - (float)H6_DRAG * wz);
-            s[36 * ss] = h; s[37 * ss] = vx; s[38 * ss] = vy; s[39 * ss] = vz;
-            s[40 * ss] = roll; s[41 * ss] = pitch; s[42 * ss] = wx; s[43 * ss] = wy; s[44 * ss] = wz;
-            r[0] = vx;
-            r[1] = -asq / 12.f;
-            r[2] = -(roll * roll + pitch * pitch);
-            r[3] = vy;
-            r[4] = -0.1f * qsq / 12.f;
-            r[5] = -(h * h + 0.1f * wz * wz);
-            return fabsf(roll) > (float)H6_FALL || fabsf(pitch) > (float)H6_FALL;
+            for (int j = 0; j < 12; ++j) h6_joint(s, ss, j, a[j], &ev[j], &qdv[j], &sjv[j]);
+            return h6_body(s, ss, sjv, ev, a, qdv, 1, r);
         }
     }
     return false;

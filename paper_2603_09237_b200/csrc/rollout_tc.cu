@@ -52,6 +52,8 @@ constexpr int MAX_SLOTS = 4;     // weight-ring slots per net
 constexpr int SLOT_MAX = 16384;  // bytes per ring slot (largest chunk)
 constexpr uint32_t POL_COL = 0, CRI_COL = 256, OUT_OFF = 128;  // TMEM columns (512 allocated)
 constexpr int BAR_POL = 1, BAR_CRI = 2;                        // named barriers of the two groups
+// mo-humanoid6 joint scratch in the policy hidden buffer, after the sampling scratch (MU, ZS)
+constexpr int H6_SCRATCH_OFF = 2 * RE * 16 * 4, H6_SCRATCH_BYTES = 4 * RE * 12 * 4;
 
 #ifdef MB_ROLL_PROF  // phase timing in CTA 0 (debug builds only: NVCC="nvcc -DMB_ROLL_PROF")
 __shared__ unsigned long long g_rp[4][16], g_rp_last[4];  // (CTA 0 prints them)
@@ -532,28 +534,64 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             if (t > 0) wait_phase(&B->cdone[(t - 1) & 1], (t - 1) >> 1);
             RPROF(7);
             int any_reset = 0;
-            for (int r = gtid; r < nr; r += PGROUP) {
+            // mo-humanoid6 (when the scratch fits the policy hidden buffer): the twelve joints on
+            // the instance's 4 threads, the body update / bookkeeping on its first thread
+            const bool split = a.kind == ENV_HUMANOID6 && a.hb_bytes >= H6_SCRATCH_OFF + H6_SCRATCH_BYTES;
+            float* h6s = reinterpret_cast<float*>(hp + H6_SCRATCH_OFF);  // [4][RE][12]: s_j, e_j, a_j, qd_j
+            const int r_own = split ? gtid >> 2 : gtid;
+            const bool owner = split ? ((gtid & 3) == 0 && r_own < nr) : gtid < nr;
+            bool anyc = false;
+            if (split) {
+                if (r_own < nr) {
+#pragma unroll
+                    for (int jj = 0; jj < 3; ++jj) {
+                        const int j = (gtid & 3) + 4 * jj;
+                        const float xx = ZS[r_own * 16 + j];  // tanh(z), from the sampling pass
+                        if (!isfinite(xx)) atomicExch(a.err, 3);
+                        const float aj = fminf(fmaxf(xx, -1.f), 1.f);
+                        anyc |= aj != xx;
+                        float e, qd, sj;
+                        h6_joint(S + r_own, RE, j, aj, &e, &qd, &sj);
+                        h6s[(0 * RE + r_own) * 12 + j] = sj;
+                        h6s[(1 * RE + r_own) * 12 + j] = e;
+                        h6s[(2 * RE + r_own) * 12 + j] = aj;
+                        h6s[(3 * RE + r_own) * 12 + j] = qd;
+                    }
+                }
+                // the instance's 4 threads are adjacent lanes
+                anyc |= __shfl_xor_sync(0xffffffffu, anyc, 1);
+                anyc |= __shfl_xor_sync(0xffffffffu, anyc, 2);
+                umma::bar_sync(BAR_POL, PGROUP);
+            }
+            if (owner) {
+                const int r = r_own;
                 float lp = 0.f;  // action_logprob: the dims' terms in order
                 for (int d = 0; d < ad; ++d) lp += MU[r * 16 + d];
                 const long row = (long)(i0 + r) * T + t;
                 a.logprob[row] = lp;
                 // ---- env step (env.cpp:60-92), tracker (rollout.cpp:143-148)
-                float act[16], rw[8];  // compile-time indexed (predicated): registers, not local memory
-                bool anyc = false;
-#pragma unroll
-                for (int d = 0; d < 16; ++d) {
-                    act[d] = 0.f;
-                    if (d < ad) {
-                        const float xx = ZS[r * 16 + d];  // tanh(z), from the sampling pass
-                        if (!isfinite(xx)) atomicExch(a.err, 3);
-                        act[d] = fminf(fmaxf(xx, -1.f), 1.f);
-                        anyc |= act[d] != xx;
-                    }
-                }
+                float rw[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) rw[k] = 0.f;
+                bool tm;
+                if (split) {
+                    tm = h6_body(S + r, RE, h6s + (0 * RE + r) * 12, h6s + (1 * RE + r) * 12,
+                                 h6s + (2 * RE + r) * 12, h6s + (3 * RE + r) * 12, 1, rw);
+                } else {
+                    float act[16];  // compile-time indexed (predicated): registers, not local memory
+#pragma unroll
+                    for (int d = 0; d < 16; ++d) {
+                        act[d] = 0.f;
+                        if (d < ad) {
+                            const float xx = ZS[r * 16 + d];  // tanh(z), from the sampling pass
+                            if (!isfinite(xx)) atomicExch(a.err, 3);
+                            act[d] = fminf(fmaxf(xx, -1.f), 1.f);
+                            anyc |= act[d] != xx;
+                        }
+                    }
+                    tm = env_do_step(a.kind, S + r, RE, act, rw);
+                }
                 if (anyc) atomicAdd(a.clamp_count, 1ULL);
-                const bool tm = env_do_step(a.kind, S + r, RE, act, rw);
                 const int st = STP[r] + 1;
                 const bool tr = !tm && st >= a.max_steps;
                 a.term[row] = tm;
