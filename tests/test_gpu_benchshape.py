@@ -245,6 +245,42 @@ def test_rollout_teacher_forced_humanoid6_bench_widths(mb, o):
     print("humanoid6 teacher-forced max normwise errors:", errs, "term", n_term, "trunc", n_trunc)
 
 
+def _force_boundaries(c):
+    """Truncations and falls inside the window (mo-humanoid6)."""
+    def prepare(t):
+        N = c.N
+        steps = np.zeros(N, np.int32)
+        steps[::2] = 1000 - 1 - (np.arange(0, N, 2) * 7) % 90
+        t.set("env_steps", steps)
+        st = t.get("env_state")
+        fall = np.arange(N) % 16 == 3
+        st[40, fall] = 0.995
+        st[42, fall] = 0.8
+        t.set("env_state", st)
+    return prepare
+
+
+def test_rollout_teacher_forced_deep_ragged_nets(mb, o):
+    """Three hidden layers of unequal widths (the in-place hidden buffer
+    changes its padded K between layers: 200 -> 256 -> 100 features, one or
+    two 128-feature tiles, zeros in the padded features) and 40 instances
+    per cluster (nepad 48, a partial 8-env block)."""
+    c = bench_cfg(K=4, T=24, N=160, F=64, feat_hidden=[64], actor_hidden=[200, 256, 100],
+                  critic_hidden=[96, 256, 40], seed=5)
+    errs, n_term, n_trunc = _teacher_forced(mb, o, c, _force_boundaries(c))
+    assert n_term > 0 and n_trunc > 0, (n_term, n_trunc)
+    print("deep / ragged teacher-forced max normwise errors:", errs, "term", n_term, "trunc", n_trunc)
+
+
+def test_rollout_teacher_forced_two_ctas_per_cluster(mb, o):
+    """100 instances per cluster at bench widths: two rollout CTAs (64 + 36
+    instances) stream the same cluster's weights; boundaries forced in both."""
+    c = bench_cfg(K=2, T=32, N=200, seed=12)
+    errs, n_term, n_trunc = _teacher_forced(mb, o, c, _force_boundaries(c))
+    assert n_term > 0 and n_trunc > 0, (n_term, n_trunc)
+    print("two-CTA teacher-forced max normwise errors:", errs, "term", n_term, "trunc", n_trunc)
+
+
 def test_rollout_teacher_forced_pointmass_truncation(mb, o):
     """mo-pointmass past its 200-step horizon: every instance truncates and
     auto-resets inside the fused rollout (T = 210)."""
