@@ -671,6 +671,11 @@ Trainer::Trainer(const TrainConfig& cfg, int world, int rank, const void* nccl_i
     for (cudaEvent_t* e : {&ev_gather_, &ev_c_net_, &ev_chk_, &ev_cd_[0], &ev_cd_[1], &ev_ad_[0], &ev_ad_[1],
                            &ev_cfin_})
         MB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (int c = 0; c < 2; ++c) {
+        MB_CUDA(cudaStreamCreateWithFlags(&side_[c], cudaStreamNonBlocking));
+        MB_CUDA(cudaEventCreateWithFlags(&ev_fork_[c], cudaEventDisableTiming));
+        MB_CUDA(cudaEventCreateWithFlags(&ev_join_[c], cudaEventDisableTiming));
+    }
     for (cudaEvent_t e : {ev_cd_[0], ev_cd_[1], ev_cfin_}) MB_CUDA(cudaEventRecord(e, s2_));
     for (cudaEvent_t e : {ev_ad_[0], ev_ad_[1]}) MB_CUDA(cudaEventRecord(e, s_));
     // a communicator whenever an NCCL id or a loopback group is given (world
@@ -725,6 +730,11 @@ Trainer::~Trainer() {
         if (e) cudaEventDestroy(e);
     if (s2_) cudaStreamDestroy(s2_);
     if (s3_) cudaStreamDestroy(s3_);
+    for (int c = 0; c < 2; ++c) {
+        if (side_[c]) cudaStreamDestroy(side_[c]);
+        if (ev_fork_[c]) cudaEventDestroy(ev_fork_[c]);
+        if (ev_join_[c]) cudaEventDestroy(ev_join_[c]);
+    }
     for (auto& u : ub_) cudaFree(u.Zf);
     for (void* p : {(void*)d_term, (void*)d_trunc, (void*)d_ekey, (void*)d_ectr, (void*)d_steps, (void*)d_err,
                     (void*)d_clamps, (void*)d_rows, (void*)d_goff, (void*)d_lossrows,
@@ -1174,6 +1184,26 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
         }
         if (n) batch("mlp_dX", ds, n);
     }
+    // every bias gradient (per-tile column sums of G_l -> per cluster), the
+    // log-std gradients and the minibatch losses need only the epilogues'
+    // partials, all written by now: one launch on the side stream, beside
+    // the weight-gradient GEMMs (both feed the gtheta pass)
+    SegJobs jb;
+    for (int k = 0; k < nn; ++k) {
+        const Net& t = N[k];
+        const NetDims& nd = t.h->tgt;
+        const int L = nd.L;
+        for (int l = 0; l < L; ++l)  // output layer partials are written with a row stride of 16
+            jb.job[jb.n++] = SegJob{t.u->pbias[l], l == L - 1 ? 16 : nd.sz[l + 1], nd.sz[l + 1],
+                                    t.gth + nd.boff[l], t.h->ld};
+        if (t.actor) jb.job[jb.n++] = SegJob{t.u->psls, 16, es_.act_dim, t.gth + nd.mlp_n, t.h->ld};
+        jb.loss[jb.nloss++] = SegLoss{t.u->lossrows, Bp / 128, d_mbloss + slot * 2 + (t.actor ? 0 : 1)};
+    }
+    fork(s_);
+    {
+        ProfScope ps("segsum", 0, 4.0 * (Bp / 128) * 16 * 2 * 8 + 8.0 * Bp, side_of(s_));  // per-tile partials -> per cluster
+        segsum_multi(jb, goff, Kl_, side_of(s_));
+    }
     std::vector<IGemm> dws;
     for (int k = 0; k < nn; ++k) {
         const Net& t = N[k];
@@ -1190,24 +1220,7 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
         }
     }
     for (size_t k0 = 0; k0 < dws.size(); k0 += 3) batch("mlp_dW", &dws[k0], (int)std::min<size_t>(3, dws.size() - k0));
-    // every bias gradient (per-tile column sums of G_l -> per cluster), the
-    // log-std gradients and the minibatch losses: one launch
-    SegJobs jb;
-    for (int k = 0; k < nn; ++k) {
-        const Net& t = N[k];
-        const NetDims& nd = t.h->tgt;
-        const int L = nd.L;
-        for (int l = 0; l < L; ++l)  // output layer partials are written with a row stride of 16
-            jb.job[jb.n++] = SegJob{t.u->pbias[l], l == L - 1 ? 16 : nd.sz[l + 1], nd.sz[l + 1], t.gth + nd.boff[l],
-                                    t.h->ld};
-        if (t.actor) jb.job[jb.n++] = SegJob{t.u->psls, 16, es_.act_dim, t.gth + nd.mlp_n, t.h->ld};
-        jb.loss[k] = SegLoss{t.u->lossrows, Bp / 128, d_mbloss + slot * 2 + (t.actor ? 0 : 1)};
-    }
-    jb.nloss = nn;
-    {
-        ProfScope ps("segsum", 0, 4.0 * (Bp / 128) * 16 * 2 * 8 + 8.0 * Bp, s_);  // per-tile partials -> per cluster
-        segsum_multi(jb, goff, Kl_, s_);
-    }
+    join(s_);
 }
 
 // One PPO minibatch (train.cpp:163-180). The actor chain runs on s_, the
@@ -1221,6 +1234,17 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
 // MORLAX_FUSED_NETS=1: both nets in lockstep on one stream, every stage one
 // launch covering both (fewer, fuller launches but no overlap: 29.9 ms/iter).
 // Both losses are checked for finiteness before either Adam (train.cpp:174-178).
+void Trainer::fork(cudaStream_t s) {
+    const int c = s == s2_ ? 1 : 0;
+    MB_CUDA(cudaEventRecord(ev_fork_[c], s));
+    MB_CUDA(cudaStreamWaitEvent(side_[c], ev_fork_[c], 0));
+}
+void Trainer::join(cudaStream_t s) {
+    const int c = s == s2_ ? 1 : 0;
+    MB_CUDA(cudaEventRecord(ev_join_[c], side_[c]));
+    MB_CUDA(cudaStreamWaitEvent(s, ev_join_[c], 0));
+}
+
 void Trainer::use_mb_bufs(int p) {
     const MbBufs& b = mbb_[p];
     Xi_ = b.Xi; d_Z = b.Z; d_lpo = b.lpo; d_sa = b.sa; d_tg = b.tg; d_rowgroup = b.rg;
@@ -1295,11 +1319,18 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     check_finite_f64(d_mbloss + slot * 2, 2, d_err, 3, s_);  // train.cpp:174-178
     MB_CUDA(cudaEventRecord(ev_chk_, s_));
     MB_CUDA(cudaStreamWaitEvent(sc, ev_chk_, 0));
-    HyperNet::backward_multi(&both[1], 1, sc, 2);
-    critic_.adam_step(cfg_.critic_lr, d_err, sc);  // (+ the critic chain's all-gathers on comm2_)
-    MB_CUDA(cudaEventRecord(ev_cfin_, sc));
-    HyperNet::backward_multi(&both[0], 1, s_, 2);
-    actor_.adam_step(cfg_.actor_lr, d_err, s_);  // train.cpp:179-180
+    // single rank, fused dM + Adam: the feature / b Adam (adam_img) runs on
+    // the side stream beside it (disjoint parameter ranges, inputs complete;
+    // unfused, adam_img also updates M from the dM GEMM and must follow it)
+    const bool side = comm_ == nullptr && fuse;
+    for (int k = 1; k >= 0; --k) {  // critic chain, then actor chain
+        cudaStream_t st = k ? sc : s_;
+        if (side) fork(st);
+        HyperNet::backward_multi(&both[k], 1, st, 2);  // (+ the chain's all-gathers on its communicator)
+        both[k]->adam_step(k ? cfg_.critic_lr : cfg_.actor_lr, d_err, side ? side_of(st) : st);  // train.cpp:179-180
+        if (side) join(st);
+        if (k) MB_CUDA(cudaEventRecord(ev_cfin_, sc));
+    }
 }
 
 void Trainer::phase_update(int it, int max_minibatches) {

@@ -251,6 +251,15 @@ private:
     cudaEvent_t ev_cd_[2] = {nullptr, nullptr}, ev_ad_[2] = {nullptr, nullptr};  // critic / actor done with set p
     cudaEvent_t ev_cfin_ = nullptr;  // the critic chain's last Adam
     cudaStream_t s3_ = nullptr;      // the minibatch gathers
+    // per update chain (0: actor on s_, 1: critic on s2_) a side stream for
+    // the kernels that are independent of the chain's next one (the bias-
+    // gradient sums beside the weight-gradient GEMMs, the feature / b Adam
+    // beside the fused dM + Adam), forked and joined by events
+    cudaStream_t side_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork_[2] = {nullptr, nullptr}, ev_join_[2] = {nullptr, nullptr};
+    void fork(cudaStream_t s);            // side stream of s waits for s's work so far
+    void join(cudaStream_t s);            // s waits for its side stream's work so far
+    cudaStream_t side_of(cudaStream_t s) const { return s == s2_ ? side_[1] : side_[0]; }
     int mb_par_ = 0;
     struct MbBufs {
         Img Xi;
