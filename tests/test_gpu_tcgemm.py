@@ -42,7 +42,9 @@ def mb():
 
 @pytest.mark.parametrize("a_k,b_k", [(1, 1), (0, 1), (1, 0), (0, 0)])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (300, 256, 200), (77, 12, 45), (128, 48, 512),
-                                   (1000, 6, 256), (64, 200, 16)])
+                                   (1000, 6, 256), (64, 200, 16),
+                                   # 256-wide tiles over several row tiles, a partial N tile, a long K loop
+                                   (640, 256, 384), (384, 200, 128), (1024, 256, 1024)])
 def test_tc_gemm_matches_bf16_reference(mb, M, N, K, a_k, b_k):
     out, ref = run(mb, M, N, K, a_k, b_k, 1)
     err = np.abs(out - ref).max() / max(1.0, np.abs(ref).max())
