@@ -19,16 +19,23 @@ __device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, uint32_t lbo, uint32
 
 struct Cfg {
     int M, N, a_mn, b_mn, swz, background;  // background: 8 warps of epilogue-like work (tcgen05.ld, tanh, STS)
+    int chunk;  // > 0: the rollout's issue pattern, `chunk` MMAs then a commit (+ a ready-barrier wait and fence)
+    int parts = 7;  // chunk mode: 1 ready-barrier wait, 2 tcgen05.fence::after_thread_sync, 4 commit per chunk,
+                    // 8: the whole loop on lane 0 (no per-chunk warp reconvergence)
+                    // 16: the whole loop inside one elect.sync region
+                    // 32: per chunk elect, compile-time chunk of 4 MMAs (fully unrolled)
 };
 
 __global__ void k_bench(Cfg c, int NI, long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, ebar[4], rbar;
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x >> 5;
     if (warp == 0) umma::tmem_alloc(&tslot, 512);
     if (threadIdx.x == 32) {
         umma::mbar_init(&bar, 1);
+        for (int i = 0; i < 4; ++i) umma::mbar_init(&ebar[i], 1);
+        umma::mbar_init(&rbar, 1);
         umma::fence_barrier_init();
     }
     umma::fence_before_sync();
@@ -69,15 +76,77 @@ __global__ void k_bench(Cfg c, int NI, long long* out) {
         for (int rep = 0; rep < 2; ++rep) {
             __syncwarp();
             t0 = clock64();
-            if (umma::elect_one()) {
-                for (int i = 0; i < NI; ++i) {
-                    const int kk = i & 3;
-                    umma::mma_bf16(tb, ad + (uint64_t)((kk * kstep) >> 4), bd + (uint64_t)((kk * kstep) >> 4), idesc,
-                                   i ? 1u : 0u);
+            if (c.chunk == 0) {
+                if (umma::elect_one()) {
+                    for (int i = 0; i < NI; ++i) {
+                        const int kk = i & 3;
+                        umma::mma_bf16(tb, ad + (uint64_t)((kk * kstep) >> 4), bd + (uint64_t)((kk * kstep) >> 4),
+                                       idesc, i ? 1u : 0u);
+                    }
+                    umma::commit(&bar);
                 }
-                umma::commit(&bar);
+                __syncwarp();
+            } else {
+                if (rep == 0 && umma::elect_one()) umma::mbar_arrive(&rbar);  // a barrier that is already complete
+                __syncwarp();
+                if ((c.parts & 8) && (threadIdx.x & 31) == 0) {
+                    for (int i0 = 0; i0 < NI; i0 += c.chunk) {
+                        if (c.parts & 1) umma::mbar_wait(&rbar, 0u);
+                        if (c.parts & 2) umma::fence_after_sync();
+                        for (int i = i0; i < i0 + c.chunk; ++i) {
+                            const int kk = i & 3;
+                            umma::mma_bf16(tb, ad + (uint64_t)((kk * kstep) >> 4), bd + (uint64_t)((kk * kstep) >> 4),
+                                           idesc, i ? 1u : 0u);
+                        }
+                        if (c.parts & 4) umma::commit(&ebar[(i0 / c.chunk) & 3]);
+                    }
+                }
+                if (c.parts & 16) {
+                    if (umma::elect_one()) {
+                        for (int i0 = 0; i0 < NI; i0 += c.chunk) {
+                            if (c.parts & 1) umma::mbar_wait(&rbar, 0u);
+                            if (c.parts & 2) umma::fence_after_sync();
+                            for (int i = i0; i < i0 + c.chunk; ++i) {
+                                const int kk = i & 3;
+                                umma::mma_bf16(tb, ad + (uint64_t)((kk * kstep) >> 4),
+                                               bd + (uint64_t)((kk * kstep) >> 4), idesc, i ? 1u : 0u);
+                            }
+                            if (c.parts & 4) umma::commit(&ebar[(i0 / c.chunk) & 3]);
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (c.parts & 32) {
+                    for (int i0 = 0; i0 < NI; i0 += 4) {
+                        if (c.parts & 1) umma::mbar_wait(&rbar, 0u);
+                        if (c.parts & 2) umma::fence_after_sync();
+                        if (umma::elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma::mma_bf16(tb, ad + (uint64_t)((kk * kstep) >> 4), bd + (uint64_t)((kk * kstep) >> 4),
+                                               idesc, (i0 | kk) ? 1u : 0u);
+                            if (c.parts & 4) umma::commit(&ebar[(i0 >> 2) & 3]);
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (!(c.parts & 56))
+                for (int i0 = 0; i0 < NI; i0 += c.chunk) {
+                    if (c.parts & 1) umma::mbar_wait(&rbar, 0u);
+                    if (c.parts & 2) umma::fence_after_sync();
+                    if (umma::elect_one()) {
+                        for (int i = i0; i < i0 + c.chunk; ++i) {
+                            const int kk = i & 3;
+                            umma::mma_bf16(tb, ad + (uint64_t)((kk * kstep) >> 4), bd + (uint64_t)((kk * kstep) >> 4),
+                                           idesc, i ? 1u : 0u);
+                        }
+                        if (c.parts & 4) umma::commit(&ebar[(i0 / c.chunk) & 3]);
+                    }
+                    __syncwarp();
+                }
+                if (umma::elect_one()) umma::commit(&bar);
+                __syncwarp();
             }
-            __syncwarp();
             umma::mbar_wait(&bar, (uint32_t)rep);
             t1 = clock64();
         }
@@ -94,29 +163,23 @@ int main() {
     cudaMalloc(&d_out, 16);
     cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const Cfg cfgs[] = {
-        {128, 64, 0, 1, 0, 0},   // rollout hidden layer: A K-major, B MN-major, no swizzle
-        {128, 64, 0, 1, 0, 1},   // ... with 8 warps of epilogue-like work beside the MMA warp
-        {128, 64, 0, 0, 0, 0},   // both K-major, no swizzle
-        {128, 64, 0, 0, 1, 0},   // both K-major, 128B swizzle
-        {64, 16, 1, 0, 0, 0},    // rollout output layer
-        {64, 16, 1, 0, 0, 1},    // ... with background work
-        {128, 128, 0, 0, 0, 0},  // GEMM N = 128, no swizzle
-        {128, 128, 0, 0, 1, 0},  // GEMM N = 128, 128B swizzle
-        {128, 128, 1, 1, 0, 0},  // GEMM N = 128, both MN-major, no swizzle
-        {128, 256, 0, 0, 0, 0},  // N = 256, no swizzle
-        {128, 256, 0, 0, 1, 0},  // N = 256, 128B swizzle
-        {128, 256, 0, 0, 0, 1},  // N = 256 with background work
+        {128, 64, 0, 1, 0, 0, 0},       // rollout hidden layer: A K-major, B MN-major, no swizzle
+        {128, 64, 0, 1, 0, 0, 4, 7},    // the rollout's pattern: wait + fence + 4 MMAs + commit, per chunk elect
+        {128, 64, 0, 1, 0, 0, 4, 39},   // the same with a compile-time unrolled chunk
+        {128, 64, 0, 1, 0, 0, 4, 36},   // unrolled chunk + commit
+        {128, 64, 0, 1, 0, 0, 4, 32},   // unrolled chunk only
+        {128, 128, 0, 0, 0, 0, 4, 39},  // N = 128, unrolled 4 + wait + fence + commit
     };
     for (const Cfg& c : cfgs) {
-        for (int grid : {1, 148}) {
+        for (int grid : {1}) {
             const int NI = 512;
             k_bench<<<grid, 384, 200 * 1024>>>(c, NI, d_out);
             cudaError_t e = cudaDeviceSynchronize();
             long long cyc = 0;
             cudaMemcpy(&cyc, d_out, 8, cudaMemcpyDeviceToHost);
             const double flop_per = 2.0 * c.M * c.N * 16;
-            printf("M %3d N %3d a_mn %d b_mn %d swz %d bg %d grid %3d: %.1f cycles/MMA (floor %d) %s\n", c.M, c.N,
-                   c.a_mn, c.b_mn, c.swz, c.background, grid, (double)cyc / NI, (c.M < 128 ? 128 : c.M) * c.N / 256,
+            printf("M %3d N %3d a_mn %d b_mn %d swz %d bg %d chunk %2d parts %d grid %3d: %.1f cycles/MMA (floor %d) %s\n",
+                   c.M, c.N, c.a_mn, c.b_mn, c.swz, c.background, c.chunk, c.parts, grid, (double)cyc / NI, (c.M < 128 ? 128 : c.M) * c.N / 256,
                    e == cudaSuccess ? "" : cudaGetErrorString(e));
             (void)flop_per;
         }
