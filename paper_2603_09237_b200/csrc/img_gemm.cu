@@ -26,6 +26,19 @@
 namespace mb200 {
 
 namespace {
+#ifdef MB_GEMM_PROF  // role timing of CTA 0 (NVCC="nvcc -DMB_GEMM_PROF")
+#define GPROF_BEGIN const long long gp_start = clock64(); long long gp_wait = 0, gp_t0 = 0
+#define GPROF_T0 gp_t0 = clock64()
+#define GPROF_ADD(v) v += clock64() - gp_t0
+#define GPROF_END(role, what)                                                                                  \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                                                            \
+        printf("gemm CTA0 %s: total %lld cycles, %s %lld\n", role, clock64() - gp_start, what, gp_wait)
+#else
+#define GPROF_BEGIN
+#define GPROF_T0
+#define GPROF_ADD(v)
+#define GPROF_END(role, what)
+#endif
 constexpr int CHUNK = 32768;
 constexpr int EPI_WARP0 = 4;
 
@@ -130,6 +143,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
 
     if (warp == 0) {
         {  // ---------------- producer (converged warp; one elected lane issues)
+            GPROF_BEGIN;
             long g = 0;  // global chunk counter
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 MB_TILE(t);
@@ -143,7 +157,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 const int nbv = min(C::NB, (d.b_view ? CTb : img_rt(d.B.R)) - nt0);
                 for (int kc = 0; kc < ti.nk; ++kc, ++g) {
                     const int s = (int)(g % C::STAGES);
+                    GPROF_T0;
                     umma::mbar_wait(&empty[s], (uint32_t)(((g / C::STAGES) & 1) ^ 1));
+                    GPROF_ADD(gp_wait);
                     uint8_t* st = smem + s * C::STAGE;
                     if (umma::elect_one()) {
                         umma::mbar_arrive_expect_tx(&full[s], CHUNK + nbv * bbytes);
@@ -158,10 +174,15 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                     __syncwarp();
                 }
             }
+            GPROF_END("producer", "wait-stage");
         }
         __syncwarp();
     } else if (warp == 1) {
         {  // ---------------- MMA issuer (converged warp; one elected lane issues)
+            GPROF_BEGIN;
+#ifdef MB_GEMM_PROF
+            long long gp_wait2 = 0;
+#endif
             long g = 0;
             int it = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -174,7 +195,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 const uint32_t b_step = d.b_view ? 4096 : 256;
                 const int nbv = min(C::NB, (d.b_view ? img_ct(d.B.C) : img_rt(d.B.R)) - (ti.n0 >> 7));
                 const int acc = it & 1;
+                GPROF_T0;
                 umma::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
+                GPROF_ADD(gp_wait2);
                 umma::fence_after_sync();
                 const uint32_t dcol = tbase + (uint32_t)(acc * C::ACC);
                 // descriptors of stage 0's A and first B chunk; a stage / chunk / K step
@@ -183,7 +206,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 const uint64_t b_desc0 = umma::smem_desc(umma::smem_u32(smem) + CHUNK, b_lbo, b_sbo);
                 for (int kc = 0; kc < ti.nk; ++kc, ++g) {
                     const int s = (int)(g % C::STAGES);
+                    GPROF_T0;
                     umma::mbar_wait(&full[s], (uint32_t)((g / C::STAGES) & 1));
+                    GPROF_ADD(gp_wait);
                     umma::fence_after_sync();
                     if (umma::elect_one()) {
                         const uint64_t ad = a_desc0 + (uint64_t)((s * C::STAGE) >> 4);
@@ -204,10 +229,15 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 __syncwarp();
                 ++it;
             }
+#ifdef MB_GEMM_PROF
+            if (blockIdx.x == 0 && lane == 0) printf("gemm CTA0 mma: wait-accumulator %lld cycles\n", gp_wait2);
+#endif
+            GPROF_END("mma", "wait-data");
         }
         __syncwarp();
     } else if (warp >= EPI_WARP0) {  // ---------------- epilogue (NEPI warps)
         const int ew = warp - EPI_WARP0;           // 0..NEPI-1
+        GPROF_BEGIN;
         const int lg = ew & 3, half = ew >> 2;     // TMEM lane quadrant, column part
         const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..ET-1
         constexpr int NPART = NEPI / 4;
@@ -348,7 +378,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 uint4 cur[4], nxt[4];
                 aux(0, cur);
                 aux(1, cur + 2);
+                GPROF_T0;
                 umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+                GPROF_ADD(gp_wait);
                 umma::fence_after_sync();
 #pragma unroll 1
                 for (int ci = 0; ci < NCH; ci += 2) {
@@ -478,6 +510,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
             }
             ++it;
         }
+        if (ew == 0) GPROF_END("epilogue", "wait-accumulator");
     }
     __syncthreads();
     if (warp == 0) umma::tmem_free(tbase, C::TCOLS);
