@@ -375,21 +375,28 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                         dst[1] = *reinterpret_cast<const uint4*>(xb + coff(ci) + 128);
                     }
                 };
-                uint4 cur[4], nxt[4];
+                // the tanh' operands two chunk pairs ahead (their L2 latency is longer than
+                // one pair's math); the first two pairs are in flight under the accumulator wait
+                uint4 cur[4], nxt[4], nx2[4];
                 aux(0, cur);
                 aux(1, cur + 2);
+                aux(2, nxt);
+                aux(3, nxt + 2);
                 GPROF_T0;
                 umma::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
                 GPROF_ADD(gp_wait);
                 umma::fence_after_sync();
 #pragma unroll 1
                 for (int ci = 0; ci < NCH; ci += 2) {
-                    aux(ci + 2, nxt);
-                    aux(ci + 3, nxt + 2);
+                    aux(ci + 4, nx2);
+                    aux(ci + 5, nx2 + 2);
                     chunk(ci, cur);
                     if (ci + 1 < NCH) chunk(ci + 1, cur + 2);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+                    for (int q = 0; q < 4; ++q) {
+                        cur[q] = nxt[q];
+                        nxt[q] = nx2[q];
+                    }
                 }
             } else if (active) {
                 // partial tiles (edges of M or N): guarded, rolled
