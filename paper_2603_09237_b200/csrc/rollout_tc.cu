@@ -127,18 +127,40 @@ __device__ __forceinline__ void produce_pass(const NetPlan& pl, const uint8_t* b
     }
 }
 
+// the MMA warp's copy of a net's plan, one chunk per lane (chunks 32.. in
+// the second word): nk | k0 / 16 << 5 | tile << 10 | last-of-layer << 15;
+// per layer (lanes < 8) the input's padded K x 16 (its 8-env block stride).
+// Read with one shuffle per chunk instead of indexed constant loads.
+struct LanePlan {
+    uint32_t c0, c1, sbo;
+};
+__device__ __forceinline__ LanePlan lane_plan(const NetPlan& pl, int L, int lane) {
+    auto pack = [&](int c) -> uint32_t {
+        if (c >= pl.nchunks) return 0u;
+        const bool last = c + 1 == pl.nchunks || pl.chunk_layer[c + 1] != pl.chunk_layer[c];
+        return (uint32_t)(pl.chunk_kw[c] / 16) | (uint32_t)(pl.chunk_k0[c] / 16) << 5 |
+               (uint32_t)pl.chunk_tile[c] << 10 | (last ? 1u : 0u) << 15;
+    };
+    LanePlan lp;
+    lp.c0 = pack(lane);
+    lp.c1 = pack(lane + 32);
+    lp.sbo = lane < L ? (uint32_t)pl.kin_pad[lane] * 16 : 0u;
+    return lp;
+}
+
 // MMA warp (converged; one elected lane issues): one pass of a net on the
 // operand at smem address `in0`. Layer l > 0 waits for the group's epilogue
 // of layer l - 1 (`hready`); each layer ends with a commit to `acc`; the
 // layer-0 MMAs also release the input operand through `xfree` (when given).
 // Descriptors are built once per chunk and advanced by 256 B (+16 in the
 // address field) per K = 16 step.
-__device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint32_t tbase, uint32_t in0,
+__device__ __forceinline__ void mma_pass(const LanePlan& lp, int L, Ring& r, uint32_t tbase, uint32_t in0,
                                          uint32_t hb0, int nepad, uint64_t* acc, uint64_t* hready, int& hph,
                                          uint64_t* xfree) {
 #ifdef MB_ROLL_PROF
     long long cw_h = 0, cw_f = 0, c_all = clock64();
 #endif
+    const uint32_t ring0 = umma::smem_u32(r.base);
     int c = 0;
     for (int l = 0; l < L; ++l) {
         if (l > 0) {
@@ -153,10 +175,12 @@ __device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint
         }
         const bool last = l == L - 1;
         // input operand at K = 0; its 8-env block stride is this layer's padded K
-        const uint64_t in_desc = umma::smem_desc(l == 0 ? in0 : hb0, 128, (uint32_t)pl.kin_pad[l] * 16);
+        const uint64_t in_desc = umma::smem_desc(l == 0 ? in0 : hb0, 128, __shfl_sync(0xffffffffu, lp.sbo, l));
         const uint32_t idesc =
             last ? umma::idesc_bf16(64, 16, true, false) : umma::idesc_bf16(128, nepad, false, true);
-        for (; c < pl.nchunks && pl.chunk_layer[c] == l; ++c) {
+        for (;; ++c) {
+            const uint32_t info = __shfl_sync(0xffffffffu, c < 32 ? lp.c0 : lp.c1, c & 31);
+            const int nk = (int)(info & 31), k0s = (int)((info >> 5) & 31), tile = (int)((info >> 10) & 1);
 #ifdef MB_ROLL_PROF
             const long long q0 = clock64();
 #endif
@@ -165,14 +189,14 @@ __device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint
             cw_f += clock64() - q0;
 #endif
             umma::fence_after_sync();
-            const int kw = pl.chunk_kw[c], k0 = pl.chunk_k0[c];
-            const uint64_t w_desc =
-                umma::smem_desc(umma::smem_u32(r.base + r.slot * r.slot_bytes), 128, (uint32_t)kw * 16);
-            const uint64_t x_desc = in_desc + (uint64_t)k0;  // (k0 / 16) steps of 16
-            const int nk = kw / 16;
+            // SWIZZLE_NONE descriptor: address >> 4, LBO 128 B, SBO = the chunk's K x 16 B, version 1
+            const uint64_t w_desc = (uint64_t)(((ring0 + (uint32_t)(r.slot * r.slot_bytes)) >> 4) & 0x3FFF) |
+                                    ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(nk * 16) << 32) | ((uint64_t)1 << 46);
+            const uint64_t x_desc = in_desc + (uint64_t)(k0s * 16);  // k0 / 16 steps of 16
+            const int k0 = k0s;  // only its zero-ness matters for the accumulate flag
             if (umma::elect_one()) {
                 if (!last) {
-                    const uint32_t d = tbase + (uint32_t)(pl.chunk_tile[c] * nepad);
+                    const uint32_t d = tbase + (uint32_t)(tile * nepad);
 #pragma unroll 4
                     for (int kk = 0; kk < nk; ++kk)
                         umma::mma_bf16(d, w_desc + 16 * kk, x_desc + 16 * kk, idesc, (k0 | kk) ? 1u : 0u);
@@ -186,6 +210,10 @@ __device__ __forceinline__ void mma_pass(const NetPlan& pl, int L, Ring& r, uint
             }
             __syncwarp();
             r.advance();
+            if (info >> 15) {
+                ++c;
+                break;
+            }
         }
         if (umma::elect_one()) {
             if (l == 0 && xfree) umma::commit(xfree);
@@ -397,10 +425,11 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 for (int t = 0; t < T; ++t) produce_pass(PP, pblob, pr);
             } else if (warp == W_ISSUE + 1) {  // policy MMA
                 int hph = 0;
+                const LanePlan plp = lane_plan(PP, a.pol.L, lane);
                 for (int t = 0; t < T; ++t) {
                     wait_phase(&B->xp_ready[t & 1], t >> 1);
                     umma::fence_after_sync();
-                    mma_pass(PP, a.pol.L, pr, tbase + POL_COL, umma::smem_u32(xp + (t & 1) * a.xb_bytes),
+                    mma_pass(plp, a.pol.L, pr, tbase + POL_COL, umma::smem_u32(xp + (t & 1) * a.xb_bytes),
                              umma::smem_u32(hp), nepad, &B->pacc, &B->php, hph, nullptr);
                 }
             } else if (warp == W_ISSUE + 2) {  // critic producer: [C_final(s-1)], [C_cur(s) if VF(s)], ..., C_final(T-1)
@@ -412,11 +441,12 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 produce_pass(CP, cblob, cr);
             } else {  // critic MMA, same sequence
                 int hph = 0;
+                const LanePlan clp = lane_plan(CP, a.cri.L, lane);
                 for (int s = 0; s <= T; ++s) {
                     if (s > 0) {
                         wait_phase(&B->xc_ready, s - 1);
                         umma::fence_after_sync();
-                        mma_pass(CP, a.cri.L, cr, tbase + CRI_COL, umma::smem_u32(xc), umma::smem_u32(hc), nepad,
+                        mma_pass(clp, a.cri.L, cr, tbase + CRI_COL, umma::smem_u32(xc), umma::smem_u32(hc), nepad,
                                  &B->cacc, &B->chp, hph, &B->xc_free);
                     }
                     if (s == T) break;
@@ -424,7 +454,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                     if (VF[s & 1]) {
                         wait_phase(&B->xp_ready[s & 1], s >> 1);
                         umma::fence_after_sync();
-                        mma_pass(CP, a.cri.L, cr, tbase + CRI_COL, umma::smem_u32(xp + (s & 1) * a.xb_bytes),
+                        mma_pass(clp, a.cri.L, cr, tbase + CRI_COL, umma::smem_u32(xp + (s & 1) * a.xb_bytes),
                                  umma::smem_u32(hc), nepad, &B->cacc, &B->chp, hph, &B->xp_free[s & 1]);
                     } else {
                         if (umma::elect_one()) umma::mbar_arrive(&B->xp_free[s & 1]);
