@@ -195,13 +195,24 @@ __device__ __forceinline__ void mma_pass(const LanePlan& lp, int L, Ring& r, uin
             const uint64_t x_desc = in_desc + (uint64_t)(k0s * 16);  // k0 / 16 steps of 16
             const int k0 = k0s;  // only its zero-ness matters for the accumulate flag
             if (umma::elect_one()) {
+                // the common chunk widths as straight-line code: a runtime-trip MMA loop
+                // issues at about half the rate (tools/umma_bench.cu)
                 if (!last) {
                     const uint32_t d = tbase + (uint32_t)(tile * nepad);
-#pragma unroll 4
-                    for (int kk = 0; kk < nk; ++kk)
-                        umma::mma_bf16(d, w_desc + 16 * kk, x_desc + 16 * kk, idesc, (k0 | kk) ? 1u : 0u);
+                    if (nk == 4) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma::mma_bf16(d, w_desc + 16 * kk, x_desc + 16 * kk, idesc, (k0 | kk) ? 1u : 0u);
+                    } else {
+                        for (int kk = 0; kk < nk; ++kk)
+                            umma::mma_bf16(d, w_desc + 16 * kk, x_desc + 16 * kk, idesc, (k0 | kk) ? 1u : 0u);
+                    }
+                } else if (nk == 16) {
+#pragma unroll
+                    for (int kk = 0; kk < 16; ++kk)
+                        umma::mma_bf16(tbase + OUT_OFF, x_desc + 16 * kk, w_desc + 16 * kk, idesc,
+                                       (k0 | kk) ? 1u : 0u);
                 } else {
-#pragma unroll 4
                     for (int kk = 0; kk < nk; ++kk)
                         umma::mma_bf16(tbase + OUT_OFF, x_desc + 16 * kk, w_desc + 16 * kk, idesc,
                                        (k0 | kk) ? 1u : 0u);
