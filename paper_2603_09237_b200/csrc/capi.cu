@@ -882,6 +882,18 @@ int morlax_trainer_get_theta(morlax_trainer* t, int which, float* out) {
         const int g0 = (tr.local_groups() == tr.config().K) ? 0 : 0;
         MB_CUDA(cudaMemcpy2D(out, sizeof(float) * h.P, h.theta + (long)g0 * h.ld, sizeof(float) * h.ld,
                              sizeof(float) * h.P, tr.local_groups(), cudaMemcpyDeviceToHost));
+        if (h.theta16_last) {  // the update forward kept the hidden layers' weights in bf16 only
+            const int G = tr.local_groups();
+            std::vector<uint16_t> w((size_t)G * h.P);
+            MB_CUDA(cudaMemcpy2D(w.data(), sizeof(uint16_t) * h.P, h.theta16 + (long)g0 * h.ld,
+                                 sizeof(uint16_t) * h.ld, sizeof(uint16_t) * h.P, G, cudaMemcpyDeviceToHost));
+            for (int g = 0; g < G; ++g)
+                for (int l = 0; l + 1 < h.tgt.L; ++l)
+                    for (long p = h.tgt.woff[l]; p < h.tgt.woff[l] + (long)h.tgt.sz[l] * h.tgt.sz[l + 1]; ++p) {
+                        const uint32_t u = (uint32_t)w[(size_t)g * h.P + p] << 16;
+                        std::memcpy(&out[(size_t)g * h.P + p], &u, 4);
+                    }
+        }
     });
 }
 

@@ -295,6 +295,35 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                     }
                     __syncwarp();
                 };
+                // bf16 copy: the warp's 32 rows x 16 columns (32 B per row) through the
+                // same staging area, each store instruction writing 16 rows x 32 B
+                auto stage_store16 = [&](uint16_t* dst, const float* x) {
+                    uint32_t* st32 = reinterpret_cast<uint32_t*>(stg);
+                    uint4 q0, q1;
+                    q0.x = umma::pack_bf16(x[0], x[1]);
+                    q0.y = umma::pack_bf16(x[2], x[3]);
+                    q0.z = umma::pack_bf16(x[4], x[5]);
+                    q0.w = umma::pack_bf16(x[6], x[7]);
+                    q1.x = umma::pack_bf16(x[8], x[9]);
+                    q1.y = umma::pack_bf16(x[10], x[11]);
+                    q1.z = umma::pack_bf16(x[12], x[13]);
+                    q1.w = umma::pack_bf16(x[14], x[15]);
+                    *reinterpret_cast<uint4*>(st32 + lane * 8) = q0;
+                    *reinterpret_cast<uint4*>(st32 + lane * 8 + 4) = q1;
+                    __syncwarp();
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        const int piece = s2 * 32 + lane, r = piece >> 1, h = piece & 1;
+                        const uint4 y = *reinterpret_cast<const uint4*>(st32 + r * 8 + h * 4);
+                        *reinterpret_cast<uint4*>(dst + (long)r * d.c16m + h * 8) = y;
+                    }
+                    __syncwarp();
+                };
+                auto bf_only = [&](int n0c) {  // columns [n0c, n0c + 16) all inside one bf16-only range
+                    for (int k = 0; k < d.nbf; ++k)
+                        if (n0c >= d.bf_lo[k] && n0c + 16 <= d.bf_hi[k]) return true;
+                    return false;
+                };
                 // chunk ci = columns cb + 16 ci .. +15, inside one 128-column chunk
                 // for every BN ((cb & 127) + 16 ci <= 112): 2 core-matrix columns
                 auto coff = [](int ci) -> long { return (long)ci * 256; };
@@ -317,6 +346,10 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                         for (int i = 0; i < 16; ++i) v[i] += bm;
                     }
                     if (EPI == 0) {
+                        if (d.C16) {
+                            stage_store16(d.C16 + cz * d.c_gs + (long)(ti.m0 + lg * 32) * d.c16m + cb + ci * 16, v);
+                            if (bf_only(cb + ci * 16)) return;
+                        }
                         stage_store(d.C + wofs + ci * 16, v);
                         return;
                     }
@@ -435,6 +468,19 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                     }
                     if (EPI == 0) {
                         if (!any) continue;
+                        if (d.C16) {
+                            uint16_t* r16 = d.C16 + cz * d.c_gs + (long)m * d.c16m;
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (nb + i < d.N) {
+                                    const __nv_bfloat16 b = __float2bfloat16_rn(v[i]);
+                                    r16[nb + i] = *reinterpret_cast<const uint16_t*>(&b);
+                                }
+                            bool only = false;
+                            for (int k = 0; k < d.nbf; ++k)
+                                if (nb >= d.bf_lo[k] && nb + 16 <= d.bf_hi[k]) only = true;
+                            if (only) continue;
+                        }
                         if (d.accumulate)
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
@@ -711,6 +757,46 @@ void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& p
     if (n == 0) return;
     launch_pdl(k_pack_weights, dim3((unsigned)std::min<long>((n + 255) / 256, 148 * 16)), dim3(256), 0, s, theta, ld,
                g0, ng, pd, wimg, gs);
+    MB_LAUNCH();
+}
+
+// the same from the bf16 copy of theta: one 16-byte read and one 16-byte
+// image store per 8-column unit
+__global__ void k_pack_weights16(const uint16_t* __restrict__ theta16, long ld, int g0, int ng, PackDims pd,
+                                 uint8_t* wimg, long gs) {
+    pdl_enter();
+    const long per = pd.ustart[pd.L];
+    for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < per * ng; u += (long)gridDim.x * blockDim.x) {
+        const int z = (int)(u / per);
+        const long r = u - (long)z * per;
+        int l = 0;
+        while (r >= pd.ustart[l + 1]) ++l;
+        const int in = pd.in[l], cpr = (in + 7) >> 3;
+        const int e = (int)(r - pd.ustart[l]);
+        const int j = e / cpr, c = (e - j * cpr) * 8;
+        if (j >= pd.out[l]) continue;
+        const uint16_t* src = theta16 + (long)(g0 + z) * ld + pd.woff[l] + (long)j * in + c;
+        uint4 w;
+        if (c + 8 <= in && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            w = *reinterpret_cast<const uint4*>(src);
+        } else {
+            uint16_t v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = c + q < in ? src[q] : (uint16_t)0;
+            w.x = v[0] | (uint32_t)v[1] << 16;
+            w.y = v[2] | (uint32_t)v[3] << 16;
+            w.z = v[4] | (uint32_t)v[5] << 16;
+            w.w = v[6] | (uint32_t)v[7] << 16;
+        }
+        *reinterpret_cast<uint4*>(wimg + (long)z * gs + pd.ioff[l] + img_off(j, c, img_ct(in))) = w;
+    }
+}
+void pack_weights16(const uint16_t* theta16, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
+                    cudaStream_t s) {
+    const long n = pd.ustart[pd.L] * ng;
+    if (n == 0) return;
+    launch_pdl(k_pack_weights16, dim3((unsigned)std::min<long>((n + 255) / 256, 148 * 16)), dim3(256), 0, s,
+               theta16, ld, g0, ng, pd, wimg, gs);
     MB_LAUNCH();
 }
 

@@ -62,6 +62,13 @@ struct IGemm {
     int N_tile = 0;              // set by the launcher
     float* psum = nullptr;       // act 2: per-128-row-tile column sums [Bp/128][psum_ld]
     long psum_ld = 0;
+    // act 0: a bf16 copy of C (row stride c16m elements, cn == 1); 16-column
+    // chunks entirely inside one of the nbf column ranges [bf_lo, bf_hi) are
+    // written only there (their fp32 C is left as it was)
+    uint16_t* C16 = nullptr;
+    long c16m = 0;
+    int nbf = 0;
+    long bf_lo[7] = {}, bf_hi[7] = {};
 };
 // out[z*out_gs + j] = sum over row tiles t of group z (goff/128) of psum[t*ld + j]
 void img_gemm(const IGemm& d, cudaStream_t s);
@@ -91,6 +98,9 @@ void segsum_multi(const SegJobs& jb, const int* goff, int G, cudaStream_t s);
 void to_img(const float* src, long ld, long src_gs, int R, int C, const Img& dst, int G, cudaStream_t s);
 void pack_weights(const float* theta, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
                   cudaStream_t s);
+// the same from the bf16 copy of theta (a relayout, no rounding)
+void pack_weights16(const uint16_t* theta16, long ld, int g0, int ng, const PackDims& pd, uint8_t* wimg, long gs,
+                    cudaStream_t s);
 // gtheta [G][ld] -> bf16 image + column sums db[P] in one pass (db may be null)
 void gtheta_prep(const float* gt, long ld, int G, int P, const Img& gimg, float* db, cudaStream_t s);
 // sharded optimizer: the local clusters' gtheta rows [Kl][ld] split by

@@ -240,6 +240,7 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
         fd.boff[l] = fboff[l];
     }
     theta = dalloc<float>((size_t)G * ld);
+    theta16 = dalloc<uint16_t>((size_t)G * ld);
     gtheta = dalloc<float>((size_t)G * ld);
     gf = dalloc<float>((size_t)G * F);
     splits = (int)std::min<long>(64, std::max<long>(1, P / 1024));
@@ -298,7 +299,7 @@ void HyperNet::free_all() {
     dfree(p); dfree(g); dfree(m1); dfree(m2);
     for (auto& a : fact) dfree(a);
     for (auto& a : fgz) dfree(a);
-    dfree(theta); dfree(gtheta); dfree(gf); dfree(parts); dfree(d_split_bounds);
+    dfree(theta); dfree(theta16); dfree(gtheta); dfree(gf); dfree(parts); dfree(d_split_bounds);
     dfree(mimg.p); dfree(fimg.p); dfree(gimg.p); dfree(wimg.p);
 }
 
@@ -330,7 +331,11 @@ static double igemm_bytes(const IGemm& d) {
     if (d.act == 2) b += 2.0 * M * N;              // tanh' operand image
     const double outs = M * N * (d.gmode == 2 ? Z : (d.gmode == 0 ? Z : 1.0));
     if (d.o_mode) b += 2.0 * outs;
-    if (d.C) b += 4.0 * outs;
+    if (d.C) {
+        double bf = 0;  // columns written in bf16 only
+        for (int k = 0; d.C16 && k < d.nbf; ++k) bf += (double)(d.bf_hi[k] - d.bf_lo[k]);
+        b += (d.C16 ? 2.0 * outs : 0.0) + 4.0 * outs * (1.0 - bf / N);
+    }
     return b;
 }
 static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
@@ -342,14 +347,15 @@ static void igemm(const char* cls, const IGemm& d, cudaStream_t s) {
 // feature map f(w) for all G groups (SIMT: K = m is tiny), then on the tensor
 // cores theta[g][p] = b[p] + sum_k M[p][k] f[g][k] (hypernet.cpp:73-88) for
 // this rank's clusters [g0, g0+ng) only (theta rows keep global indices).
-void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s) {
+void HyperNet::forward(const float* w, int g0, int ng, cudaStream_t s, bool upd) {
     HyperNet* self = this;
-    forward_multi(&self, 1, w, g0, ng, s);
+    forward_multi(&self, 1, w, g0, ng, s, upd);
 }
 
 // the forward of one or two hypernetworks (actor and critic) in lockstep:
 // each stage is one launch covering both
-void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s) {
+void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s,
+                             bool upd) {
     {
         double fl = 0;
         FeatJob jobs[2];
@@ -375,6 +381,16 @@ void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0
             d.M = ng; d.N = (int)h.P; d.K = h.F;
             d.bias = h.p + h.nf + h.P * h.F; d.bias_mode = 1;
             d.C = h.theta + (long)g0 * h.ld; d.cm = h.ld; d.cn = 1;
+            h.theta16_last = upd;
+            if (upd) {  // the hidden layers' weights only feed the bf16 weight packing
+                d.C16 = h.theta16 + (long)g0 * h.ld;
+                d.c16m = h.ld;
+                for (int l = 0; l + 1 < h.tgt.L && d.nbf < 7; ++l) {
+                    d.bf_lo[d.nbf] = h.tgt.woff[l];
+                    d.bf_hi[d.nbf] = h.tgt.woff[l] + (long)h.tgt.sz[l] * h.tgt.sz[l + 1];
+                    ++d.nbf;
+                }
+            }
             fl += 2.0 * d.M * d.N * d.K;
             by += igemm_bytes(d);
         }
@@ -392,8 +408,9 @@ void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0
             pd.ioff[l] = h.wimg_off[l];
             pd.ustart[l + 1] = pd.ustart[l] + (long)((h.tgt.sz[l + 1] + 7) / 8 * 8) * ((h.tgt.sz[l] + 7) / 8);
         }
-        ProfScope ps("pack_weights", 0, 6.0 * ng * h.tgt.mlp_n, s);
-        pack_weights(h.theta, h.ld, g0, ng, pd, h.wimg.p, h.wimg.gs, s);
+        ProfScope ps("pack_weights", 0, (upd ? 4.0 : 6.0) * ng * h.tgt.mlp_n, s);
+        if (upd) pack_weights16(h.theta16, h.ld, g0, ng, pd, h.wimg.p, h.wimg.gs, s);
+        else pack_weights(h.theta, h.ld, g0, ng, pd, h.wimg.p, h.wimg.gs, s);
     }
 }
 
@@ -1286,7 +1303,7 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     HyperNet* both[2] = {&actor_, &critic_};
     const bool roles[2] = {true, false};
     if (!two) {
-        HyperNet::forward_multi(both, 2, d_cw, g_lo_, Kl_, s_);  // hypernet_forward per loss (losses.cpp:79,167)
+        HyperNet::forward_multi(both, 2, d_cw, g_lo_, Kl_, s_, true);  // hypernet_forward per loss (losses.cpp:79,167)
         MB_CUDA(cudaStreamWaitEvent(s_, ev_gather_, 0));
         net_step(both, roles, 2, Bp, inv_B, maxg, rows, goff, slot, s_);
         MB_CUDA(cudaEventRecord(ev_ad_[mb_par_], s_));
@@ -1300,7 +1317,7 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
         return;
     }
     // the forwards (feature map, theta, weight packing) need no minibatch rows
-    critic_.forward(d_cw, g_lo_, Kl_, sc);
+    critic_.forward(d_cw, g_lo_, Kl_, sc, true);
     MB_CUDA(cudaStreamWaitEvent(sc, ev_gather_, 0));
     net_step(&both[1], &roles[1], 1, Bp, inv_B, maxg, rows, goff, slot, sc);
     MB_CUDA(cudaEventRecord(ev_c_net_, sc));
@@ -1309,7 +1326,7 @@ void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, 
     // communicator they hold the chain's exchange collectives): each chain
     // runs them before the finiteness join
     HyperNet::backward_multi(&both[1], 1, sc, 1);
-    actor_.forward(d_cw, g_lo_, Kl_, s_);
+    actor_.forward(d_cw, g_lo_, Kl_, s_, true);
     MB_CUDA(cudaStreamWaitEvent(s_, ev_gather_, 0));
     net_step(&both[0], &roles[0], 1, Bp, inv_B, maxg, rows, goff, slot, s_);
     MB_CUDA(cudaEventRecord(ev_ad_[mb_par_], s_));

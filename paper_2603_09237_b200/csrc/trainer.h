@@ -72,6 +72,11 @@ struct HyperNet {
     long steps[3] = {0, 0, 0};
     std::vector<float*> fact;  // feature activations [G][fsz[l]], l = 0..Lf
     float *theta = nullptr, *gtheta = nullptr, *gf = nullptr, *parts = nullptr;
+    // the update forward's theta: bf16 for the hidden layers' weights (only the
+    // weight packing reads them), fp32 kept for biases, the output layer and
+    // the log-std (theta16_last: the last forward wrote the weights here only)
+    uint16_t* theta16 = nullptr;
+    bool theta16_last = false;
     std::vector<float*> fgz;   // feature pre-activation gradients [G][fsz[l+1]]
     FeatDims fd{};             // device view of the feature MLP (feature.cu)
     const float* w_last = nullptr;  // cluster weights of the last forward (feature-map input)
@@ -93,9 +98,11 @@ struct HyperNet {
     void free_all();
     void init_params(uint64_t key, cudaStream_t s);  // init_hypernet (hypernet.cpp:124-145)
     // f (all G clusters), theta for groups [g0, g0+ng) of the G cluster weights w[G][m]
-    void forward(const float* w, int g0, int ng, cudaStream_t s);
+    // upd: the update's forward (hidden-layer weights of theta in bf16 only)
+    void forward(const float* w, int g0, int ng, cudaStream_t s, bool upd = false);
     // the same for nh (1 or 2) hypernetworks in lockstep, one launch per stage
-    static void forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s);
+    static void forward_multi(HyperNet* const* hs, int nh, const float* w, int g0, int ng, cudaStream_t s,
+                              bool upd = false);
     // part 0: all; 1: the gradient passes (gtheta image, shard exchange, df,
     // feature map: no parameter is written); 2: dM (+ the fused M-block Adam)
     static void backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int part = 0);
