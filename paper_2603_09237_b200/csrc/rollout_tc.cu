@@ -540,6 +540,20 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             }
         };
         load_eps(0);
+        // this thread's sampling items (instance, dim) and their step-invariant terms
+        int s_row[EPT], s_dim[EPT];
+        float s_sig[EPT], s_ls[EPT];
+        bool s_ok[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int e = gtid + k * PGROUP;
+            s_ok[k] = e < nr * ad;
+            const int ee = s_ok[k] ? e : 0;
+            s_row[k] = ee / ad;
+            s_dim[k] = ee - s_row[k] * ad;
+            s_ls[k] = LS[s_dim[k]];
+            s_sig[k] = __expf(s_ls[k]);
+        }
         for (int t = 0; t < T; ++t) {
             // ---- policy(obs_t)
             group_pass(PP, a.pol, th, hp, tbase + POL_COL, nepad, &B->pacc, aph, &B->php, gw, lane, warp >> 2, 2,
@@ -552,23 +566,31 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             RPROF(1);
             // ---- Gaussian sample (nn.cpp:192-202): the precomputed draw of (t, instance, dim),
             // loaded into registers one step ahead
+            // all items' math first (independent chains the compiler can interleave),
+            // then the stores of the items that exist
+            float s_z[EPT], s_lp[EPT], s_tz[EPT];
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
-                const int e = gtid + k * PGROUP;
-                if (e < nr * ad) {
-                    const int r = e / ad, d = e - r * ad;
-                    const float sig = __expf(LS[d]);
-                    const float mu = MU[r * 16 + d];
-                    const float z = mu + sig * epsr[k];
-                    a.act_pre[((long)(i0 + r) * T + t) * ad + d] = z;
-                    // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
-                    // squashed action tanh(z) for the env step
-                    const float zn = (z - mu) / sig;
-                    MU[r * 16 + d] = (-0.5f * zn * zn - LS[d] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
-                    ZS[r * 16 + d] = tanhf(z);
-                }
+                const float mu = MU[s_row[k] * 16 + s_dim[k]];
+                const float z = mu + s_sig[k] * epsr[k];
+                // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
+                // squashed action tanh(z) for the env step
+                const float zn = (z - mu) / s_sig[k];
+                s_z[k] = z;
+                s_lp[k] = (-0.5f * zn * zn - s_ls[k] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
+                s_tz[k] = tanhf(z);
             }
+#pragma unroll
+            for (int k = 0; k < EPT; ++k)
+                if (s_ok[k]) {
+                    const int r = s_row[k], d = s_dim[k];
+                    a.act_pre[((long)(i0 + r) * T + t) * ad + d] = s_z[k];
+                    MU[r * 16 + d] = s_lp[k];
+                    ZS[r * 16 + d] = s_tz[k];
+                }
+            RPROF(9);
             if (t + 1 < T) load_eps(t + 1);
+            RPROF(10);
             umma::bar_sync(BAR_POL, PGROUP);
             RPROF(2);
             // NEED / VF of step t - 1 are reused for step t + 1: the critic group must be done with them
@@ -699,10 +721,10 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
 #ifdef MB_ROLL_PROF
         if (blockIdx.x == 0 && gtid == 0) {
             const unsigned long long* q = g_rp[0];
-            printf("rollout CTA0 policy group us: out+MU %.1f sample %.1f wait-cdone %.1f env %.1f "
-                   "wait-free %.1f operands+reset %.1f epilogues %.1f wait-acc %.1f\n",
-                   q[1] * 1e-3, q[2] * 1e-3, q[7] * 1e-3, q[3] * 1e-3, q[8] * 1e-3, q[4] * 1e-3, q[5] * 1e-3,
-                   q[6] * 1e-3);
+            printf("rollout CTA0 policy group us: out+MU %.1f sample %.1f (math %.1f eps-loads %.1f bar %.1f) "
+                   "wait-cdone %.1f env %.1f wait-free %.1f operands+reset %.1f epilogues %.1f wait-acc %.1f\n",
+                   q[1] * 1e-3, (q[9] + q[10] + q[2]) * 1e-3, q[9] * 1e-3, q[10] * 1e-3, q[2] * 1e-3, q[7] * 1e-3,
+                   q[3] * 1e-3, q[8] * 1e-3, q[4] * 1e-3, q[5] * 1e-3, q[6] * 1e-3);
         }
 #endif
         umma::bar_sync(BAR_POL, PGROUP);
