@@ -4,6 +4,6 @@ for v in "$@"; do
   for rep in 1 2; do
     env $vv timeout 300 python bench.py --no-legs --no-cpu-baseline --steps 10 > gpurun_out/ab.json 2>/dev/null
     python -c "
-import json; d=json.load(open('gpurun_out/ab.json')); print('== $v', 'iter_ms %.3f' % d['ms_per_step'])"
+import json; d=json.load(open('gpurun_out/ab.json')); print('== $v', 'iter_ms %.3f' % d['ms_per_step'], d.get('clocks'))"
   done
 done
