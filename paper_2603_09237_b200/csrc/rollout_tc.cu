@@ -104,10 +104,12 @@ struct Ring {
     }
 };
 
+// sech^2 z = 4 e / (1 + e)^2, e = exp(-2 |z|) (= 1 - tanh^2 z without its
+// cancellation at large |z|); the fast MUFU division: it only feeds a log
 __device__ __forceinline__ float sech2(float z) {
     const float e = __expf(-2.f * fabsf(z));
     const float d = 1.f + e;
-    return 4.f * e / (d * d);
+    return __fdividef(4.f * e, d * d);
 }
 
 __device__ __forceinline__ void wait_phase(uint64_t* b, int n) { umma::mbar_wait(b, (uint32_t)(n & 1)); }
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
         load_eps(0);
         // this thread's sampling items (instance, dim) and their step-invariant terms
         int s_row[EPT], s_dim[EPT];
-        float s_sig[EPT], s_ls[EPT];
+        float s_sig[EPT], s_isig[EPT], s_ls[EPT];
         bool s_ok[EPT];
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
             s_dim[k] = ee - s_row[k] * ad;
             s_ls[k] = LS[s_dim[k]];
             s_sig[k] = __expf(s_ls[k]);
+            s_isig[k] = 1.f / s_sig[k];
         }
         for (int t = 0; t < T; ++t) {
             // ---- policy(obs_t)
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 const float z = mu + s_sig[k] * epsr[k];
                 // action_logprob's per-dim term (nn.cpp:204-219), summed per row below; the
                 // squashed action tanh(z) for the env step
-                const float zn = (z - mu) / s_sig[k];
+                const float zn = (z - mu) * s_isig[k];
                 s_z[k] = z;
                 s_lp[k] = (-0.5f * zn * zn - s_ls[k] - 0.9189385332046727f) - __logf(sech2(z) + 1e-6f);
                 s_tz[k] = tanhf(z);
