@@ -627,7 +627,9 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 // the instance's 4 threads are adjacent lanes
                 anyc |= __shfl_xor_sync(0xffffffffu, anyc, 1);
                 anyc |= __shfl_xor_sync(0xffffffffu, anyc, 2);
+                RPROF(11);
                 umma::bar_sync(BAR_POL, PGROUP);
+                RPROF(12);
             }
             if (owner) {
                 const int r = r_own;
@@ -635,6 +637,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 for (int d = 0; d < ad; ++d) lp += MU[r * 16 + d];
                 const long row = (long)(i0 + r) * T + t;
                 a.logprob[row] = lp;
+                RPROF(14);
                 // ---- env step (env.cpp:60-92), tracker (rollout.cpp:143-148)
                 float rw[8];
 #pragma unroll
@@ -657,6 +660,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                     }
                     tm = env_do_step(a.kind, S + r, RE, act, rw);
                 }
+                RPROF(15);
                 if (anyc) atomicAdd(a.clamp_count, 1ULL);
                 const int st = STP[r] + 1;
                 const bool tr = !tm && st >= a.max_steps;
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                 NEED[((t + 1) & 1) * RE + r] = done;
                 any_reset |= done;
             }
+            RPROF(13);
             any_reset = umma::bar_sync_or(BAR_POL, PGROUP, any_reset);
             RPROF(3);
             // ---- pre-reset final obs -> critic operand (once C_final(t-1) has consumed the
@@ -728,6 +733,9 @@ __global__ void __launch_bounds__(RNT, 1) k_rollout_tc(const __grid_constant__ R
                    "wait-cdone %.1f env %.1f wait-free %.1f operands+reset %.1f epilogues %.1f wait-acc %.1f\n",
                    q[1] * 1e-3, (q[9] + q[10] + q[2]) * 1e-3, q[9] * 1e-3, q[10] * 1e-3, q[2] * 1e-3, q[7] * 1e-3,
                    q[3] * 1e-3, q[8] * 1e-3, q[4] * 1e-3, q[5] * 1e-3, q[6] * 1e-3);
+            printf("rollout CTA0 env: joints %.1f bar %.1f owner: logprob-sum %.1f body %.1f bookkeeping %.1f; "
+                   "bar-or %.1f\n", q[11] * 1e-3, q[12] * 1e-3, q[14] * 1e-3, q[15] * 1e-3, q[13] * 1e-3,
+                   q[3] * 1e-3);
         }
 #endif
         umma::bar_sync(BAR_POL, PGROUP);
