@@ -1240,17 +1240,8 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
     join(s_);
 }
 
-// One PPO minibatch (train.cpp:163-180). The actor chain runs on s_, the
-// critic chain on s2_: the two losses / backward passes / Adam steps are
-// independent, so their many small kernels overlap. Joins: both losses are
-// checked for finiteness before either Adam (train.cpp:174-178), and the
-// next minibatch's gather waits for the critic to release the shared inputs.
-// One PPO minibatch (train.cpp:163-180). Default: one stream per net (actor
-// on s_, critic on s2_) joined for the finiteness check, so one net's
-// HBM-bound Adam overlaps the other net's GEMMs (measured 26.5 ms/iter).
-// MORLAX_FUSED_NETS=1: both nets in lockstep on one stream, every stage one
-// launch covering both (fewer, fuller launches but no overlap: 29.9 ms/iter).
-// Both losses are checked for finiteness before either Adam (train.cpp:174-178).
+// a chain's side stream: fork = it waits for the chain's work so far; join =
+// the chain waits for the side stream's work so far
 void Trainer::fork(cudaStream_t s) {
     const int c = s == s2_ ? 1 : 0;
     MB_CUDA(cudaEventRecord(ev_fork_[c], s));
@@ -1267,6 +1258,15 @@ void Trainer::use_mb_bufs(int p) {
     Xi_ = b.Xi; d_Z = b.Z; d_lpo = b.lpo; d_sa = b.sa; d_tg = b.tg; d_rowgroup = b.rg;
 }
 
+// One PPO minibatch (train.cpp:163-180). Default: one stream per net (actor
+// on s_, critic on s2_): the two losses / backward passes / Adam steps are
+// independent, so one net's HBM-bound Adam overlaps the other net's GEMMs.
+// Joins: both losses are checked for finiteness before either Adam
+// (train.cpp:174-178), and the next minibatch's gather waits for the last
+// readers of its input buffer set. Single rank: each chain's bias-gradient
+// sums and feature / b Adam run on its side stream. MORLAX_FUSED_NETS=1: both
+// nets in lockstep on one stream, every stage one launch covering both
+// (fewer, fuller launches but no overlap; slower).
 void Trainer::minibatch(int slot, int Bp, int Bglob, int maxg, const int* rows, const int* goff) {
     const int od = es_.obs_dim, ad = es_.act_dim, m = es_.m;
     const float inv_B = (float)(1.0 / (double)Bglob);  // global 1/B (losses.cpp:66,155)
