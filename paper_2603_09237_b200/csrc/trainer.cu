@@ -191,6 +191,10 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     F = F_;
     G = G_;
     comm = comm_;
+    if (comm && !xs) {
+        MB_CUDA(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+        for (auto& e : xev) MB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     world = comm ? comm_world(comm) : 1;
     rank = comm ? comm_rank(comm) : 0;
     Kl = comm ? Kl_ : G_;
@@ -295,6 +299,11 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
 }
 
 void HyperNet::free_all() {
+    if (xs) cudaStreamDestroy(xs);
+    for (auto& e : xev)
+        if (e) cudaEventDestroy(e);
+    xs = nullptr;
+    xev[0] = xev[1] = nullptr;
     dfree(gshard.p); dfree(fall.p); dfree(gsend); dfree(grecv);
     dfree(p); dfree(g); dfree(m1); dfree(m2);
     for (auto& a : fact) dfree(a);
@@ -445,7 +454,18 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
             ProfScope ps("gtheta_prep", 0, 6.0 * h.fng * h.P + (h.comm ? 8.0 * h.world * h.Kl * h.S : 4.0 * h.P), s);
             gtheta_prep(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, (int)h.P, h.gimg,
                         h.comm ? nullptr : h.g + h.nf + h.P * h.F, s);
-            if (h.comm) pack_shards(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, h.S, h.world, h.gsend, s);
+            if (h.comm) {
+                pack_shards(h.gtheta + (long)h.fg0 * h.ld, h.ld, h.fng, h.S, h.world, h.gsend, s);
+                // the exchange starts now on xs, beside the df GEMM and the local feature backward
+                MB_CUDA(cudaEventRecord(h.xev[0], s));
+                MB_CUDA(cudaStreamWaitEvent(h.xs, h.xev[0], 0));
+                ProfScope ps2("exchange", 0, 4.0 * h.world * h.Kl * h.S, h.xs);
+                // every cluster's gtheta on this rank's shard, then its image and db (all clusters, in order)
+                comm_alltoall_bytes(h.comm, h.gsend, h.grecv, sizeof(float) * (size_t)h.Kl * h.S, h.xs);
+                if (h.row_hi > h.row_lo)
+                    gtheta_prep(h.grecv, h.S, h.G, (int)(h.row_hi - h.row_lo), h.gshard,
+                                h.g + h.nf + h.P * h.F + h.row_lo, h.xs);
+            }
         }
         {
             IGemm ds[2];
@@ -487,12 +507,16 @@ void HyperNet::backward_multi(HyperNet* const* hs, int nh, cudaStream_t s, int p
             feature_backward_multi(jl, nh, s, 1);
             for (int k = 0; k < nh; ++k) {
                 HyperNet& h = *hs[k];
-                ProfScope ps("exchange", 0, 4.0 * h.world * h.Kl * h.S + 4.0 * h.G * h.F, s);
-                // every cluster's gtheta on this rank's shard, then its image and db (all clusters, in order)
-                comm_alltoall_bytes(h.comm, h.gsend, h.grecv, sizeof(float) * (size_t)h.Kl * h.S, s);
-                if (h.row_hi > h.row_lo)
-                    gtheta_prep(h.grecv, h.S, h.G, (int)(h.row_hi - h.row_lo), h.gshard, h.g + h.nf + h.P * h.F + h.row_lo, s);
-                comm_allgather_bytes(h.comm, h.fd.gz[h.fd.L - 1], sizeof(float) * (size_t)h.Kl * h.F, s);
+                // the local gz rows are done: all-gather them behind the exchange on xs
+                // (one communicator, the same order on every rank), then rejoin
+                MB_CUDA(cudaEventRecord(h.xev[0], s));
+                MB_CUDA(cudaStreamWaitEvent(h.xs, h.xev[0], 0));
+                {
+                    ProfScope ps("exchange", 0, 4.0 * h.G * h.F, h.xs);
+                    comm_allgather_bytes(h.comm, h.fd.gz[h.fd.L - 1], sizeof(float) * (size_t)h.Kl * h.F, h.xs);
+                }
+                MB_CUDA(cudaEventRecord(h.xev[1], h.xs));
+                MB_CUDA(cudaStreamWaitEvent(s, h.xev[1], 0));
             }
             double fl = 0;
             for (int k = 0; k < nh; ++k)

@@ -126,6 +126,11 @@ struct HyperNet {
     // reduction keeps the single-rank order, so any rank count gives the
     // single-rank result bit for bit.
     Comm* comm = nullptr;
+    // the gtheta exchange (all-to-all + this shard's gtheta pass) and the gz
+    // all-gather run on xs, beside the df GEMM and the local feature-map
+    // backward (xev: fork / join)
+    cudaStream_t xs = nullptr;
+    cudaEvent_t xev[2] = {nullptr, nullptr};
     int world = 1, rank = 0, Kl = 0;
     long S = 0, row_lo = 0, row_hi = 0;  // shard width (multiple of 128) and this rank's rows
     float *gsend = nullptr, *grecv = nullptr;  // [W][Kl][S] fp32
