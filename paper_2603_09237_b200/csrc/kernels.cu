@@ -499,8 +499,12 @@ void critic_rows_img(int Bp, int m, const int* rows, const float* v, int ldv, co
 // plus per-tile column sums of g (output bias grads), of the log-std terms
 // and of g_prev (bias grads of the last hidden layer), and the tile's loss.
 // The output layer is only act_dim / m (<= 16) wide: both contractions run
-// on mma.sync m16n8k16 (bf16 operands, fp32 accumulation; a 16-column MMA
-// is below the tcgen05 minimum tile), each warp owning two 16-row m-tiles.
+// on mma.sync m16n8k16 (bf16 operands, fp32 accumulation), each warp owning
+// two 16-row m-tiles. tcgen05 would accept the shape (M = 128, N = 16), but
+// the kernel is bound by the activation-image read and the per-row loss
+// math: ~12 x 256 MACs per row fill the tensor pipe for a few % of the
+// kernel either way, and register fragments loaded straight from the image
+// need no shared-memory staging, TMEM allocation or commit round trips.
 // The accumulator fragment of the forward (rows x out) is exactly the A
 // fragment of the backward (rows x K = out), and the forward's A fragments
 // (the activations) are exactly the tanh' operands of the backward's
