@@ -301,11 +301,19 @@ def test_rollout_teacher_forced_dst_terminals(mb, o):
 
 
 # ------------------------------------------------------------------ losses / gradients at bench widths
-def test_losses_and_grads_bench_widths(mb, o):
+# ragged widths: partial 128-row / 256-column GEMM tiles everywhere, a
+# last hidden layer that is not a multiple of 16 (k_head's K loop), a
+# 3-hidden-layer actor, F = 192 (the fused dM + Adam's 64-wide tiles)
+RAGGED = dict(F=192, feat_hidden=[100], actor_hidden=[200, 136, 72], critic_hidden=[96, 40])
+
+
+@pytest.mark.parametrize("widths", ["bench", "ragged"])
+def test_losses_and_grads_bench_widths(mb, o, widths):
     """actor_loss / critic_loss + hypernet backward (losses.cpp:46-189) at
     config-3 widths on the device's own rollout batch (fed unchanged to the
-    oracle): the act_dim-12 head, 256-wide dX epilogues and grouped dW."""
-    c = bench_cfg(K=4, T=8)
+    oracle): the act_dim-12 head, 256-wide dX epilogues and grouped dW; and
+    at ragged widths."""
+    c = bench_cfg(K=4, T=8, **(RAGGED if widths == "ragged" else {}))
     t = mb.Trainer(_mbcfg(mb, c))
     t.phase(0, 1)
     t.phase(0, 2)
@@ -335,11 +343,12 @@ def test_losses_and_grads_bench_widths(mb, o):
 
 
 # ------------------------------------------------------------------ full iteration at bench widths
-def test_full_iteration_bench_widths(mb, o):
+@pytest.mark.parametrize("widths", ["bench", "ragged"])
+def test_full_iteration_bench_widths(mb, o, widths):
     """One whole training iteration (rollout -> GAE -> 2 x 2 minibatches of
-    both losses + Adam) at config-3 widths vs the fp64 oracle, compared in
-    update space per hypernet block."""
-    c = bench_cfg(K=4, T=8)
+    both losses + Adam) at config-3 widths (and at ragged widths) vs the fp64
+    oracle, compared in update space per hypernet block."""
+    c = bench_cfg(K=4, T=8, **(RAGGED if widths == "ragged" else {}))
     t = mb.Trainer(_mbcfg(mb, c))
     ot = OracleTrainer(o, c)
     a0, c0 = t.params("actor"), t.params("critic")
@@ -354,4 +363,4 @@ def test_full_iteration_bench_widths(mb, o):
                              rel_l2=0.1, sign_agree=0.999, what="actor")
     ec = assert_update_close(t.params("critic"), ot.critic_params(), c0, c.critic_lr, hyper_blocks(c_s),
                              rel_l2=0.1, sign_agree=0.999, what="critic")
-    print("bench-width iteration update errors: actor", ea, "critic", ec)
+    print(widths, "iteration update errors: actor", ea, "critic", ec)
