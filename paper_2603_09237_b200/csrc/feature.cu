@@ -1,16 +1,20 @@
 // Hypernetwork feature map f(w) (hypernet.cpp:10-17, 92-122): a tanh MLP
 // (tanh on the output too) over the K cluster weight vectors. The work is
 // tiny (K = 128 rows, widths of a few hundred) and sits on the critical path
-// of every minibatch, so the limit is L2 latency, not bandwidth or flops:
-// every contraction is one launch of k_dense16, a 16 x 16 output tile per
-// CTA (>= 128 CTAs per layer) that stages its whole K extent (in 256-wide
-// slices) of both operands in shared memory with one round of loads, then
-// one FMA chain per thread. fp32 throughout.
-//   forward : per layer Y = tanh(X W^T + b); the last layer also writes the
-//             bf16 image of f for the theta GEMM;
-//   backward: gz_L = (sum of the split-K partials of M^T gtheta) * tanh';
+// of every minibatch, so the limit is L2 latency, not bandwidth or flops.
+// fp32 throughout.
+//   forward : all layers in one launch (k_feat_fwd, a block per 4 clusters,
+//             activations in shared memory): per layer Y = tanh(X W^T + b);
+//             the last layer also writes the bf16 image of f for the theta GEMM;
+//   backward: every contraction is one launch of k_dense16, a 16 x 16 output
+//             tile per CTA (>= 128 CTAs per layer) that stages its whole K
+//             extent (in 256-wide slices) of both operands in shared memory
+//             with one round of loads, then one FMA chain per thread;
+//             gz_L = (sum of the split-K partials of M^T gtheta) * tanh';
 //             per layer gz_{l-1} = (gz_l W_l) * tanh'(a_l);
 //             dW_l = gz_l^T a_l with db_l as an extra all-ones column.
+#include <algorithm>
+
 #include "common.cuh"
 #include "img.cuh"
 #include "kernels.h"
@@ -168,34 +172,133 @@ __global__ void __launch_bounds__(256) k_split_dtanh(const float* __restrict__ p
         gz[i] = ((part[0][ol] + part[1][ol]) + (part[2][ol] + part[3][ol])) * (1.f - x * x);
     }
 }
+
+// The whole forward of the feature map in one launch (hypernet.cpp:10-17):
+// a block per kFfClusters clusters (both maps' blocks side by side in y)
+// keeps its rows' activations in shared memory, layer after layer. A warp
+// computes kFfRows output features of the block's clusters at a time: lanes
+// split K in float4 pieces (scalar when a row is not 16-byte aligned), the
+// 16 partial dot products per lane go through one reduce-scatter shuffle
+// tree (16 shuffles), and lane 2q ends with (feature q / kFfClusters,
+// cluster q % kFfClusters). Little shared memory (4 KB at width 256).
+constexpr int kFfClusters = 2, kFfWarps = 16, kFfRows = 16 / kFfClusters;
+struct FeatFwdJob {
+    FeatDims fd;
+    const float* p;
+    const float* w;
+    int G;
+    Img fimg;
+    int r0, rn;
+};
+struct FeatFwdArgs {
+    FeatFwdJob job[2];
+    int nj = 1, maxw = 0;
+};
+__global__ void __launch_bounds__(32 * kFfWarps) k_feat_fwd(const __grid_constant__ FeatFwdArgs a) {
+    extern __shared__ __align__(16) float fsm[];
+    const FeatFwdJob& J = a.job[blockIdx.y];
+    const FeatDims& fd = J.fd;
+    const int g0 = blockIdx.x * kFfClusters;
+    if (g0 >= J.G) return;
+    const int nc = min(kFfClusters, J.G - g0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* cur = fsm;                            // [kFfClusters][maxw]
+    float* nxt = fsm + kFfClusters * a.maxw;
+    pdl_enter();
+    for (int e = threadIdx.x; e < kFfClusters * a.maxw; e += blockDim.x) {
+        const int c = e / a.maxw, k = e - c * a.maxw;
+        cur[e] = (c < nc && k < fd.sz[0]) ? J.w[(long)(g0 + c) * fd.sz[0] + k] : 0.f;
+    }
+    __syncthreads();
+    for (int l = 0; l < fd.L; ++l) {
+        const int in = fd.sz[l], out = fd.sz[l + 1];
+        const float* W = J.p + fd.woff[l];
+        const float* bias = J.p + fd.boff[l];
+        const bool vec = (in & 3) == 0 && (fd.woff[l] & 3) == 0;
+        for (int j0 = warp * kFfRows; j0 < out; j0 += kFfWarps * kFfRows) {
+            float s[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) s[q] = 0.f;
+            if (vec) {
+                for (int k = lane * 4; k < in; k += 128) {
+                    float4 xv[kFfClusters];
+#pragma unroll
+                    for (int c = 0; c < kFfClusters; ++c) xv[c] = *reinterpret_cast<const float4*>(cur + c * a.maxw + k);
+#pragma unroll
+                    for (int r = 0; r < kFfRows; ++r) {
+                        const float4 wv = j0 + r < out ? __ldg(reinterpret_cast<const float4*>(W + (long)(j0 + r) * in + k))
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int c = 0; c < kFfClusters; ++c) {
+                            float t = s[r * kFfClusters + c];
+                            t = fmaf(wv.x, xv[c].x, t);
+                            t = fmaf(wv.y, xv[c].y, t);
+                            t = fmaf(wv.z, xv[c].z, t);
+                            t = fmaf(wv.w, xv[c].w, t);
+                            s[r * kFfClusters + c] = t;
+                        }
+                    }
+                }
+            } else {
+                for (int k = lane; k < in; k += 32) {
+#pragma unroll
+                    for (int r = 0; r < kFfRows; ++r) {
+                        const float wv = j0 + r < out ? __ldg(W + (long)(j0 + r) * in + k) : 0.f;
+#pragma unroll
+                        for (int c = 0; c < kFfClusters; ++c)
+                            s[r * kFfClusters + c] = fmaf(wv, cur[c * a.maxw + k], s[r * kFfClusters + c]);
+                    }
+                }
+            }
+            // reduce-scatter of the 16 sums over the warp (fixed order)
+#pragma unroll
+            for (int w = 8; w >= 1; w >>= 1) {
+                const bool up = (lane & (2 * w)) != 0;
+#pragma unroll
+                for (int i = 0; i < w; ++i) {
+                    const float mine = up ? s[w + i] : s[i];
+                    const float other = up ? s[i] : s[w + i];
+                    s[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * w);
+                }
+            }
+            s[0] += __shfl_xor_sync(0xffffffffu, s[0], 1);
+            const int q = (lane >> 1) & 15, r = q / kFfClusters, c = q % kFfClusters, j = j0 + r;
+            if ((lane & 1) == 0 && j < out && c < nc) {
+                const float v = tanhf(s[0] + bias[j]);
+                nxt[c * a.maxw + j] = v;
+                const int g = g0 + c;
+                fd.act[l + 1][(long)g * out + j] = v;
+                if (l == fd.L - 1 && J.fimg.p && g >= J.r0 && g < J.r0 + J.rn)
+                    *reinterpret_cast<__nv_bfloat16*>(J.fimg.p + img_off(g - J.r0, j, img_ct(J.fimg.C))) =
+                        __float2bfloat16_rn(v);
+            }
+        }
+        __syncthreads();
+        float* t = cur;  // (rows of clusters >= nc are never written: they only feed sums that are dropped)
+        cur = nxt;
+        nxt = t;
+    }
+}
 }  // namespace
 
 void feature_forward_multi(const FeatJob* jobs, int nj, cudaStream_t s) {
-    const int L = jobs[0].fd->L;
-    for (int k = 1; k < nj; ++k)
-        if (jobs[k].fd->L != L) throw ShapeError("feature_forward_multi: the feature maps must have equal depth");
-    for (int l = 0; l < L; ++l) {
-        Dense16 ds[4];
-        for (int k = 0; k < nj; ++k) {
-            const FeatJob& j = jobs[k];
-            const FeatDims& fd = *j.fd;
-            Dense16 d{};
-            d.A = l == 0 ? j.w : fd.act[l];  // act[0] is not materialised: w is the input
-            d.ar = fd.sz[l]; d.ak = 1;
-            d.B = j.p + fd.woff[l]; d.bc = fd.sz[l]; d.bk = 1;  // W [out][in]
-            d.R = j.G; d.N = fd.sz[l + 1]; d.K = fd.sz[l];
-            d.bias = j.p + fd.boff[l];
-            d.act = 1;
-            d.C = fd.act[l + 1]; d.cr = fd.sz[l + 1]; d.cc = 1;
-            if (l == L - 1) {
-                d.img = j.fimg;
-                d.img_r0 = j.r0;
-                d.img_rn = j.rn;
-            }
-            ds[k] = d;
-        }
-        dense16_multi(ds, nj, s);
+    if (nj < 1 || nj > 2) throw ShapeError("feature_forward_multi: one or two feature maps");
+    FeatFwdArgs a;
+    a.nj = nj;
+    int maxw = 0, nb = 0;
+    for (int k = 0; k < nj; ++k) {
+        const FeatJob& j = jobs[k];
+        if (j.fd->L != jobs[0].fd->L) throw ShapeError("feature_forward_multi: the feature maps must have equal depth");
+        a.job[k] = FeatFwdJob{*j.fd, j.p, j.w, j.G, j.fimg, j.r0, j.rn};
+        for (int l = 0; l <= j.fd->L; ++l) maxw = std::max(maxw, j.fd->sz[l]);
+        nb = std::max(nb, (j.G + kFfClusters - 1) / kFfClusters);
     }
+    a.maxw = (maxw + 3) & ~3;
+    if (nb == 0) return;
+    const size_t smem = sizeof(float) * 2 * kFfClusters * a.maxw;
+    if (smem > 48 * 1024) throw ShapeError("feature_forward_multi: feature width above 1536");
+    launch_pdl(k_feat_fwd, dim3((unsigned)nb, (unsigned)nj), dim3(32 * kFfWarps), smem, s, a);
+    MB_LAUNCH();
 }
 
 void feature_backward_multi(const FeatJob* jobs, int nj, cudaStream_t s, int stage) {
