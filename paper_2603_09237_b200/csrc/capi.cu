@@ -54,7 +54,10 @@ struct DBuf {  // scoped device buffer
     size_t n = 0;
     explicit DBuf(size_t n_) : n(n_) { MB_CUDA(cudaMalloc(&p, (n ? n : 1) * sizeof(T))); }
     DBuf(const T* host, size_t n_) : DBuf(n_) {
-        if (n) MB_CUDA(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+        if (n) {
+            MB_CUDA(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+            MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
+        }
     }
     ~DBuf() { cudaFree(p); }
     void get(T* host) const {
@@ -84,6 +87,7 @@ struct HyperHandle {
     void load(const double* flat) {
         std::vector<float> f(flat, flat + h.n);
         MB_CUDA(cudaMemcpy(h.p, f.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+        MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
         h.refresh_images(0);
     }
 };
@@ -255,6 +259,7 @@ int morlax_env_create(const char* name, int n, morlax_env** out) {
         MB_CUDA(cudaMemset(e->steps, 0, sizeof(int) * n));
         MB_CUDA(cudaMemset(e->err, 0, sizeof(int)));
         MB_CUDA(cudaMemset(e->clamps, 0, sizeof(unsigned long long)));
+        MB_CUDA(cudaStreamSynchronize(0));  // the legacy-stream fills, before e->s (non-blocking) uses them
         MB_CUDA(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
         *out = e;
     });
@@ -315,6 +320,7 @@ int morlax_env_current_obs(morlax_env* e, float* out) {
 }
 uint64_t morlax_env_clamp_count(morlax_env* e) {
     unsigned long long c = 0;
+    cudaStreamSynchronize(e->s);  // the env kernels run on e->s (non-blocking)
     cudaMemcpy(&c, e->clamps, sizeof(c), cudaMemcpyDeviceToHost);
     return c;
 }
@@ -389,6 +395,7 @@ int morlax_policy_set_params(morlax_policy* h, const double* flat) {
         HyperNet& hn = h->p->h;
         std::vector<float> f(flat, flat + hn.n);
         MB_CUDA(cudaMemcpy(hn.p, f.data(), sizeof(float) * hn.n, cudaMemcpyHostToDevice));
+        MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
         hn.refresh_images(0);
         MB_CUDA(cudaDeviceSynchronize());
     });
@@ -483,6 +490,7 @@ int morlax_hypernet_backward(const morlax_hypernet_spec* s, const double* flat, 
         std::vector<float> gt(gtheta, gtheta + (size_t)G * hh.h.P);
         MB_CUDA(cudaMemcpy2D(hh.h.gtheta, sizeof(float) * hh.h.ld, gt.data(), sizeof(float) * hh.h.P,
                              sizeof(float) * hh.h.P, G, cudaMemcpyHostToDevice));
+        MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
         hh.h.backward(0);
         std::vector<float> g(hh.h.n);
         MB_CUDA(cudaMemcpy(g.data(), hh.h.g, sizeof(float) * g.size(), cudaMemcpyDeviceToHost));
@@ -838,6 +846,7 @@ int morlax_trainer_load_checkpoint(morlax_trainer* t, const char* path, int64_t*
             const std::vector<double>& v = w ? c : a;
             std::vector<float> fl(v.begin(), v.end());
             MB_CUDA(cudaMemcpy(h.p, fl.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+            MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
             h.refresh_images(tr.stream());
         }
         MB_CUDA(cudaStreamSynchronize(tr.stream()));
@@ -860,6 +869,7 @@ int morlax_trainer_set_params(morlax_trainer* t, int which, const double* in) {
         std::vector<float> f(in, in + h.n);
         MB_CUDA(cudaStreamSynchronize(t->t->stream()));
         MB_CUDA(cudaMemcpy(h.p, f.data(), sizeof(float) * h.n, cudaMemcpyHostToDevice));
+        MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
         h.refresh_images(t->t->stream());
         MB_CUDA(cudaStreamSynchronize(t->t->stream()));
     });
@@ -958,6 +968,7 @@ int morlax_trainer_set(morlax_trainer* t, const char* field, const void* in) {
         if (!dev) throw ConfigError("field is read-only: " + f);
         MB_CUDA(cudaStreamSynchronize(tr.stream()));
         MB_CUDA(cudaMemcpy(dev, in, bytes, cudaMemcpyHostToDevice));
+        MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
     });
 }
 int morlax_trainer_losses(morlax_trainer* t, const int32_t* rows, int n, double* al, double* cl) {

@@ -43,6 +43,10 @@ extern std::atomic<long> g_kernel_launches;
 // of the >48 KB kernels are cached per CUDA device (keyed by cudaGetDevice, a
 // mutex around the cache): one process may drive several GPUs from several
 // host threads (kernels.cu).
+// Host-side ordering rule: every stream of ours is non-blocking, so work on
+// the legacy default stream (the synchronous-API cudaMemset, and cudaMemcpy
+// from pageable host memory, which may return before its DMA lands) is not
+// ordered before it. Such calls are followed by cudaStreamSynchronize(0).
 int device_sms();
 void ensure_smem(const void* func, size_t bytes);
 

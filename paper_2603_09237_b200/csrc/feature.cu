@@ -22,7 +22,7 @@
 namespace mb200 {
 
 namespace {
-constexpr int KC = 256;  // K slice staged per round
+constexpr int KC = 64;  // K slice staged per round (8.5 KB of shared memory: fits beside the optimizer)
 
 struct Dense16 {
     const float* A;  // A(r, k) = A[r * ar + k * ak]
@@ -42,17 +42,19 @@ struct Dense16 {
     int img_r0, img_rn; // rows [img_r0, img_r0 + img_rn) go to the image
 };
 
-// 16 rows x kn (<= KC) of one operand into smem, all 16 loads in flight
-// before the stores; k-fast thread mapping when k is the unit-stride index
-// (coalesced), row-fast when the row is (the transposed operands of dW)
+// 16 rows x kn (<= KC) of one operand into smem, all of a thread's loads in
+// flight before the stores; k-fast thread mapping when k is the unit-stride
+// index (coalesced), row-fast when the row is (the transposed operands of dW)
 __device__ __forceinline__ void stage16(const float* __restrict__ P, long pr, long pk, int r0, int rlim, int k0,
                                         int kn, int ones_row, float (*S)[KC + 4]) {
-    float v[16];
+    constexpr int PER = 16 * KC / 256;  // elements per thread
+    float v[PER];
     const bool kfast = pk == 1 || pr != 1;
     const int t = threadIdx.x;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int rr = kfast ? i : (t & 15), kk = kfast ? t : (t >> 4) + 16 * i;
+    for (int i = 0; i < PER; ++i) {
+        const int e = t + 256 * i;
+        const int rr = kfast ? e / KC : (e & 15), kk = kfast ? e % KC : (e >> 4);
         const int r = r0 + rr;
         float x = 0.f;
         if (kk < kn) {
@@ -62,8 +64,9 @@ __device__ __forceinline__ void stage16(const float* __restrict__ P, long pr, lo
         v[i] = x;
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int rr = kfast ? i : (t & 15), kk = kfast ? t : (t >> 4) + 16 * i;
+    for (int i = 0; i < PER; ++i) {
+        const int e = t + 256 * i;
+        const int rr = kfast ? e / KC : (e & 15), kk = kfast ? e % KC : (e >> 4);
         S[rr][kk] = v[i];
     }
 }

@@ -166,6 +166,7 @@ void linear_dominance(int nn, int m, const double* nd, uint8_t* keep, int* scrat
     if (!d_binom) {
         MB_CUDA(cudaMalloc(&d_binom, sizeof(unsigned long long) * b.size()));
         MB_CUDA(cudaMemcpy(d_binom, b.data(), sizeof(unsigned long long) * b.size(), cudaMemcpyHostToDevice));
+        MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
     }
     const unsigned long long nw = b[(kLdfRes + m - 1) * 9 + (m - 1)];  // C(60 + m - 1, m - 1)
     MB_CUDA(cudaMemsetAsync(keep, 0, nn, s));

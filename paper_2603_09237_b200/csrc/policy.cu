@@ -135,6 +135,7 @@ GroupPolicy::GroupPolicy(int m, int F, const std::vector<int>& fh, const std::ve
         im.C = C;
         MB_CUDA(cudaMalloc(&im.p, (size_t)img_bytes((int)rows, C)));
         MB_CUDA(cudaMemset(im.p, 0, (size_t)img_bytes((int)rows, C)));
+        MB_CUDA(cudaStreamSynchronize(0));  // legacy-stream fill, before the non-blocking streams use it
         return im;
     };
     X = img(h.tgt.sz[0]);
@@ -145,6 +146,7 @@ GroupPolicy::GroupPolicy(int m, int F, const std::vector<int>& fh, const std::ve
     for (int g = 0; g <= G; ++g) go[g] = g * Rp;
     MB_CUDA(cudaMalloc(&goff, sizeof(int) * (G + 1)));
     MB_CUDA(cudaMemcpy(goff, go.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice));
+    MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
     k_rowmap<<<(unsigned)((rows + 255) / 256), 256>>>(G, R, Rp, rowmap);
     MB_LAUNCH();
     MB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));

@@ -21,7 +21,11 @@ static T* dalloc(size_t n) {
     T* p = nullptr;
     if (n == 0) n = 1;
     MB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    // cudaMemset runs asynchronously on the legacy default stream, which does
+    // not order against our non-blocking streams: wait for it, or a kernel or
+    // copy on another stream can land before the zero fill
     MB_CUDA(cudaMemset(p, 0, n * sizeof(T)));
+    MB_CUDA(cudaStreamSynchronize(0));
     return p;
 }
 template <typename T>
@@ -253,6 +257,7 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     for (int z = 0; z <= splits; ++z) bounds[z] = (int)(P * z / splits);
     d_split_bounds = dalloc<int>(splits + 1);
     MB_CUDA(cudaMemcpy(d_split_bounds, bounds.data(), sizeof(int) * (splits + 1), cudaMemcpyHostToDevice));
+    MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
     // images (zero-filled: padding stays zero forever)
     auto mk = [](int R, int C, long gs, int groups) {
         Img im;
@@ -294,6 +299,7 @@ void HyperNet::init(int m_, int F_, const std::vector<int>& fh, const std::vecto
     cudaFree(d_split_bounds);
     d_split_bounds = dalloc<int>(splits + 1);
     MB_CUDA(cudaMemcpy(d_split_bounds, kb.data(), sizeof(int) * (splits + 1), cudaMemcpyHostToDevice));
+    MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
     cudaFree(parts);
     parts = dalloc<float>((size_t)splits * G * F);
 }
@@ -1438,6 +1444,7 @@ void Trainer::finish(IterStats* st) {
 void Trainer::set_clusters(const float* cw) {
     cw_h_.assign(cw, cw + (size_t)cfg_.K * es_.m);
     MB_CUDA(cudaMemcpy(d_cw, cw, sizeof(float) * cfg_.K * es_.m, cudaMemcpyHostToDevice));
+    MB_CUDA(cudaStreamSynchronize(0));  // a pageable H2D copy may return before its DMA lands
 }
 
 void Trainer::losses_only(const int* rows, int n, double* al, double* cl) {
