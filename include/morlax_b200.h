@@ -268,7 +268,7 @@ int morlax_shard_minibatch(const int32_t* perm, int lo, int hi, int T, int inst_
                            int* max_group_out);
 
 /* ---- test hook: C[M][N] = A(m,k) B(k,n) with strided fp32 operands, on the
- *      tcgen05 path (use_tc = 1) or the SIMT path (0) ---------------------- */
+ *      tcgen05 path (use_tc must be 1; the SIMT path was removed: ConfigError) */
 int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, const float* B, long bk, long bn,
                      float* C, int use_tc);
 

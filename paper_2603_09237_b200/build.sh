@@ -7,7 +7,7 @@ NVCC=${NVCC:-nvcc}
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="-O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr -Xptxas -v"
 mkdir -p build
-SRCS="csrc/kernels.cu csrc/gemm_simt.cu csrc/pareto.cu csrc/trainer.cu csrc/comm.cu csrc/capi.cu csrc/rollout_tc.cu csrc/img_gemm.cu csrc/feature.cu csrc/hv_exact.cu csrc/policy.cu csrc/evaluate.cu csrc/dm_adam.cu"
+SRCS="csrc/kernels.cu csrc/pareto.cu csrc/trainer.cu csrc/comm.cu csrc/capi.cu csrc/rollout_tc.cu csrc/img_gemm.cu csrc/feature.cu csrc/hv_exact.cu csrc/policy.cu csrc/evaluate.cu csrc/dm_adam.cu"
 pids=()
 objs=()
 for s in $SRCS; do

@@ -1072,12 +1072,7 @@ int morlax_gemm_test(int M, int N, int K, const float* A, long am, long ak, cons
             d.C = dc.p; d.cm = N; d.cn = 1;
             img_gemm(d, 0);
         } else {
-            GemmDesc d;
-            d.A = da.p; d.am = am; d.ak = ak;
-            d.B = db.p; d.bk = bk; d.bn = bn;
-            d.C = dc.p; d.cm = N; d.cn = 1;
-            d.M = M; d.N = N; d.K = K;
-            gemm_simt(d, 0);
+            throw ConfigError("gemm_test: the SIMT GEMM was removed; use_tc must be 1");
         }
         MB_CUDA(cudaDeviceSynchronize());
         dc.get(C);

@@ -10,30 +10,6 @@
 
 namespace mb200 {
 
-// ---------------------------------------------------------------- GEMM (SIMT)
-// C(m,n) [+]= sum_k A(m,k) B(k,n) with arbitrary strides, then epilogue.
-// gmode 0: batch over z (offsets a_bz/b_bz/c_bz/bias_bz per z)
-// gmode 1: M-grouped: for z, m in [goff[z], goff[z+1]) (absolute row index);
-//          B / bias offset z*b_bz / z*bias_bz
-// gmode 2: K-grouped: for z, k in [goff[z], goff[z+1]); C offset z*c_bz
-struct GemmDesc {
-    const float* A = nullptr; long am = 0, ak = 0, a_bz = 0;
-    const float* B = nullptr; long bk = 0, bn = 0, b_bz = 0;
-    float* C = nullptr; long cm = 0, cn = 0, c_bz = 0;
-    int M = 0, N = 0, K = 0, Z = 1;
-    const int* goff = nullptr;
-    int gmode = 0;
-    int max_group = 0;            // host-known max group extent (gmode 1)
-    const float* bias = nullptr;  // bias_mode 1: bias[n], 2: bias[m]
-    long bias_bz = 0;
-    int bias_mode = 0;
-    int act = 0;                  // 0 none, 1 tanh (C2 <- preact), 2 C *= (1 - aux^2)
-    const float* aux = nullptr; long xm = 0, xn = 0;
-    float* C2 = nullptr; long c2m = 0, c2n = 0;
-    int accumulate = 0;
-};
-void gemm_simt(const GemmDesc& d, cudaStream_t s);
-
 // all layers' generated weights of groups [g0, g0+ng) -> per-group layer images
 struct PackDims {
     int L = 0;

@@ -1,4 +1,4 @@
-"""tcgen05 GEMM (tc_gemm.cu) vs an fp64 numpy reference on bf16-rounded
+"""tcgen05 GEMM (img_gemm.cu) vs an fp64 numpy reference on bf16-rounded
 operands, for every operand major-ness the training step uses and ragged
 sizes (tile tails in M, N and K)."""
 import ctypes as C
