@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 MB_TILE(t);
                 if (!ti.valid) continue;
                 const int CTa = img_ct(d.A.C), CTb = img_ct(d.B.C);
-                const uint32_t bbytes = (d.b_view == 0 && BN < 128) ? (uint32_t)BN * 256 : (uint32_t)CHUNK;
+                const uint32_t bbytes =
+                    (d.b_view == 0 && BN < 128 && !d.b_tma) ? (uint32_t)BN * 256 : (uint32_t)CHUNK;
                 const uint8_t* Ab = d.A.p + (d.gmode == 0 ? ti.z * d.A.gs : 0);
                 const uint8_t* Bb = d.B.p + (d.gmode != 2 ? ti.z * d.B.gs : 0);
                 const int mt = ti.m0 >> 7, nt0 = ti.n0 >> 7, kc0 = ti.k_lo >> 7;
@@ -165,11 +166,20 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                         umma::mbar_arrive_expect_tx(&full[s], CHUNK + nbv * bbytes);
                         umma::bulk_g2s(st, Ab + chunk_index(d.a_view, mt, kc0 + kc, CTa) * CHUNK, CHUNK, &full[s]);
 #pragma unroll
-                        for (int j = 0; j < C::NB; ++j)
-                            if (j < nbv)
+                        for (int j = 0; j < C::NB; ++j) {
+                            if (j >= nbv) continue;
+                            if (d.b_tma) {  // (row chunk, column chunk) of B's [R][C] rows: two 64-column boxes
+                                const int rc = d.b_view ? kc0 + kc : nt0 + j, cc = d.b_view ? nt0 + j : kc0 + kc;
+                                const int z = d.gmode != 2 ? ti.z : 0;
+                                umma::tma_load_3d(st + CHUNK * (1 + j), &d.bmap, cc * 128, rc * 128, z, &full[s]);
+                                umma::tma_load_3d(st + CHUNK * (1 + j) + CHUNK / 2, &d.bmap, cc * 128 + 64, rc * 128, z,
+                                                  &full[s]);
+                            } else {
                                 umma::bulk_g2s(st + CHUNK * (1 + j),
                                                Bb + chunk_index(d.b_view, nt0 + j, kc0 + kc, CTb) * CHUNK, bbytes,
                                                &full[s]);
+                            }
+                        }
                     }
                     __syncwarp();
                 }
@@ -203,7 +213,17 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
                 // descriptors of stage 0's A and first B chunk; a stage / chunk / K step
                 // only moves the start address (+bytes >> 4 in the low field)
                 const uint64_t a_desc0 = umma::smem_desc(umma::smem_u32(smem), a_lbo, a_sbo);
-                const uint64_t b_desc0 = umma::smem_desc(umma::smem_u32(smem) + CHUNK, b_lbo, b_sbo);
+                // tensor-map B chunks: 128-byte swizzle, two 64-column halves 16 KB apart;
+                // K-major (view 0): SBO 1024 (8-row groups), K step +32 B inside a half;
+                // MN-major (view 1): LBO 16 KB (the halves), SBO 1024, K step +2 KB
+                const uint64_t b_desc0 =
+                    d.b_tma ? (umma::smem_desc(umma::smem_u32(smem) + CHUNK, d.b_view ? CHUNK / 2 : 16, 1024) |
+                               ((uint64_t)2 << 61))
+                            : umma::smem_desc(umma::smem_u32(smem) + CHUNK, b_lbo, b_sbo);
+                auto b_koff = [&](int kk) -> uint32_t {
+                    if (!d.b_tma) return (uint32_t)kk * b_step;
+                    return d.b_view ? (uint32_t)kk * 2048 : (uint32_t)((kk >> 2) * (CHUNK / 2) + (kk & 3) * 32);
+                };
                 for (int kc = 0; kc < ti.nk; ++kc, ++g) {
                     const int s = (int)(g % C::STAGES);
                     GPROF_T0;
@@ -219,7 +239,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI>::NT, 1) k_img_gemm(const __grid_c
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk)
                                 umma::mma_bf16(dcol + j * 128, ad + (uint64_t)(kk * (a_step >> 4)),
-                                               bd + (uint64_t)(kk * (b_step >> 4)), idesc, (kc | kk) ? 1u : 0u);
+                                               bd + (uint64_t)(b_koff(kk) >> 4), idesc, (kc | kk) ? 1u : 0u);
                         }
                         umma::commit(&empty[s]);
                     }
@@ -628,6 +648,27 @@ void img_gemm_batch(const IGemm* ds, int n, cudaStream_t s) {
 }
 
 void img_gemm(const IGemm& d, cudaStream_t s) { img_gemm_batch(&d, 1, s); }
+
+bool make_weight_map(CUtensorMap* map, const uint16_t* base, int R, int C, long gs, int Z) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode enc = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<Encode>(f);
+    }();
+    if (!enc || C % 8 || gs % 8 || (reinterpret_cast<uintptr_t>(base) & 15) || R < 1 || Z < 1) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)R, (cuuint64_t)Z};
+    const cuuint64_t strides[2] = {(cuuint64_t)C * 2, (cuuint64_t)gs * 2};
+    const cuuint32_t box[3] = {64, 128, 1}, es[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 // every per-cluster segment sum of one net's minibatch step in one launch:
 // block z < G sums job j's tiles of cluster z (fixed order), block G sums

@@ -2,6 +2,7 @@
 // All take an explicit stream; none synchronise.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -45,7 +46,18 @@ struct IGemm {
     long c16m = 0;
     int nbf = 0;
     long bf_lo[7] = {}, bf_hi[7] = {};
+    // b_tma: B chunks come straight from row-major bf16 rows through a tiled
+    // tensor map (make_weight_map) instead of the packed image B.p: per group
+    // z a [B.R][B.C] matrix; a 128 x 128 chunk lands as two 128-row x 64-column
+    // boxes in the 128-byte-swizzled layout (K-major for view 0, MN-major for
+    // view 1). B.R / B.C still give the extents.
+    int b_tma = 0;
+    alignas(64) CUtensorMap bmap;
 };
+// tensor map over rows [z][R][C] of bf16 (row stride C, group stride gs
+// elements; C % 8 == 0, base 16-byte aligned) for b_tma: 64 x 128 x 1 boxes,
+// SWIZZLE_128B, zero fill past R and C
+bool make_weight_map(CUtensorMap* map, const uint16_t* base, int R, int C, long gs, int Z);
 // out[z*out_gs + j] = sum over row tiles t of group z (goff/128) of psum[t*ld + j]
 void img_gemm(const IGemm& d, cudaStream_t s);
 // 1-3 independent GEMMs with the same epilogue kind in one persistent launch

@@ -414,16 +414,33 @@ void HyperNet::forward_multi(HyperNet* const* hs, int nh, const float* w, int g0
     }
     for (int k = 0; k < nh; ++k) {
         HyperNet& h = *hs[k];
-        PackDims pd;  // generated weights of this rank's clusters -> per-layer bf16 images
-        pd.L = h.tgt.L;
-        for (int l = 0; l < h.tgt.L; ++l) {
-            pd.in[l] = h.tgt.sz[l];
-            pd.out[l] = h.tgt.sz[l + 1];
-            pd.woff[l] = h.tgt.woff[l];
-            pd.ioff[l] = h.wimg_off[l];
-            pd.ustart[l + 1] = pd.ustart[l] + (long)((h.tgt.sz[l + 1] + 7) / 8 * 8) * ((h.tgt.sz[l] + 7) / 8);
+        if (upd && (h.wmap_g0 != g0 || h.wmap_ng != ng)) {  // tensor maps over theta16 (once per cluster range)
+            h.wmap.assign(h.tgt.L, CUtensorMap{});
+            h.wmap_ok.assign(h.tgt.L, 0);
+            static const bool tma = [] {
+                const char* e = std::getenv("MORLAX_WEIGHT_TMA");  // "0": pack every layer (A/B, tests)
+                return !(e && e[0] == '0');
+            }();
+            for (int l = 0; tma && l < h.tgt.L; ++l)
+                h.wmap_ok[l] = make_weight_map(&h.wmap[l], h.theta16 + (long)g0 * h.ld + h.tgt.woff[l],
+                                               h.tgt.sz[l + 1], h.tgt.sz[l], h.ld, ng);
+            h.wmap_g0 = g0;
+            h.wmap_ng = ng;
         }
-        ProfScope ps("pack_weights", 0, (upd ? 4.0 : 6.0) * ng * h.tgt.mlp_n, s);
+        PackDims pd;  // generated weights of this rank's clusters -> per-layer bf16 images
+        long units = 0;
+        for (int l = 0; l < h.tgt.L; ++l) {
+            if (upd && h.wmap_ok[l]) continue;  // read through its tensor map instead
+            const int q = pd.L++;
+            pd.in[q] = h.tgt.sz[l];
+            pd.out[q] = h.tgt.sz[l + 1];
+            pd.woff[q] = h.tgt.woff[l];
+            pd.ioff[q] = h.wimg_off[l];
+            pd.ustart[q + 1] = pd.ustart[q] + (long)((h.tgt.sz[l + 1] + 7) / 8 * 8) * ((h.tgt.sz[l] + 7) / 8);
+            units += (long)h.tgt.sz[l] * h.tgt.sz[l + 1];
+        }
+        if (pd.L == 0) continue;
+        ProfScope ps("pack_weights", 0, (upd ? 4.0 : 6.0) * ng * units, s);
         if (upd) pack_weights16(h.theta16, h.ld, g0, ng, pd, h.wimg.p, h.wimg.gs, s);
         else pack_weights(h.theta, h.ld, g0, ng, pd, h.wimg.p, h.wimg.gs, s);
     }
@@ -1143,6 +1160,13 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
         w.C = h.tgt.sz[l];
         return w;
     };
+    auto set_w = [&](IGemm& d, const HyperNet& h, int l) {  // layer l's weights as the B operand
+        d.B = wl(h, l);
+        if (h.weight_tma(l)) {
+            d.b_tma = 1;
+            d.bmap = h.wmap[l];
+        }
+    };
     auto batch = [&](const char* cls, const IGemm* ds, int n) {
         double fl = 0, by = 0;
         for (int k = 0; k < n; ++k) {
@@ -1163,7 +1187,7 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
             const bool last = (l == nd.L - 1);
             IGemm& d = ds[n++];
             d.A = l == 0 ? Xi_ : t.u->A[l - 1]; d.a_view = 0;  // (m = row, k = in)
-            d.B = wl(*t.h, l); d.b_view = 0;                   // (n = out, k = in)
+            set_w(d, *t.h, l); d.b_view = 0;                   // (n = out, k = in)
             d.M = Bp; d.N = nd.sz[l + 1]; d.K = nd.sz[l]; d.Z = Kl_;
             d.gmode = 1; d.goff = goff; d.max_group = maxg;
             d.bias = t.th + nd.boff[l]; d.bias_gs = t.h->ld; d.bias_mode = 1;
@@ -1222,7 +1246,7 @@ void Trainer::net_step(HyperNet* const* hs, const bool* actor, int nn, int Bp, f
             if (l >= nd.L || (t.fused_head && l == nd.L - 1)) continue;  // k_head produced G_{L-2}
             IGemm& e = ds[n++];  // G_{l-1}[q][i] = (sum_j G_l[q][j] W_l[z][j][i]) (1 - A_{l-1}[q][i]^2)
             e.A = t.u->G[l]; e.a_view = 0;  // (m = q, k = j)
-            e.B = wl(*t.h, l); e.b_view = 1;  // (n = i, k = j)
+            set_w(e, *t.h, l); e.b_view = 1;  // (n = i, k = j)
             e.M = Bp; e.N = nd.sz[l]; e.K = nd.sz[l + 1]; e.Z = Kl_;
             e.gmode = 1; e.goff = goff; e.max_group = maxg;
             e.act = 2; e.aux = t.u->A[l - 1];

@@ -77,6 +77,13 @@ struct HyperNet {
     // the log-std (theta16_last: the last forward wrote the weights here only)
     uint16_t* theta16 = nullptr;
     bool theta16_last = false;
+    // the update's weight GEMMs read the layers whose rows are 16-byte
+    // aligned in theta16 through tensor maps (no packing): wmap_ok[l]; built
+    // for the clusters [wmap_g0, wmap_g0 + wmap_ng)
+    std::vector<CUtensorMap> wmap;
+    std::vector<int> wmap_ok;
+    int wmap_g0 = -1, wmap_ng = -1;
+    bool weight_tma(int l) const { return theta16_last && l < (int)wmap_ok.size() && wmap_ok[l]; }
     std::vector<float*> fgz;   // feature pre-activation gradients [G][fsz[l+1]]
     FeatDims fd{};             // device view of the feature MLP (feature.cu)
     const float* w_last = nullptr;  // cluster weights of the last forward (feature-map input)

@@ -167,6 +167,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// 3-D tiled tensor-map load (TMA) into shared memory, completing on `mbar`
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(mbar))
+        : "memory");
+}
+
 __device__ __forceinline__ float tanh_approx(float x) {  // MUFU.TANH, |rel err| < 2^-10.99
     float y;
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
