@@ -1135,6 +1135,15 @@ int morlax_gemm_bench(int M, int N, int K, int a_view, int b_view, int act, int 
         d.M = M; d.N = N; d.K = K;
         if (act == 0) { d.C = c.p; d.cm = N; d.cn = 1; }
         else { d.act = act; d.O = Img{io.p, M, N, 0}; d.o_mode = 1; d.aux = Img{ix.p, M, N, 0}; }
+        // MORLAX_BENCH_TMA=1: B from row-major bf16 rows through a tensor map (the update's weight path)
+        const char* te = std::getenv("MORLAX_BENCH_TMA");
+        DBuf<uint16_t> brow((size_t)bR * bC);
+        if (te && te[0] == '1') {
+            MB_CUDA(cudaMemset(brow.p, 0x3c, sizeof(uint16_t) * (size_t)bR * bC));
+            MB_CUDA(cudaStreamSynchronize(0));
+            if (!make_weight_map(&d.bmap, brow.p, bR, bC, (long)bR * bC, 1)) throw ConfigError("gemm_bench: tensor map");
+            d.b_tma = 1;
+        }
         img_gemm(d, 0);
         cudaEvent_t e0, e1;
         MB_CUDA(cudaEventCreate(&e0));
